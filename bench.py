@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark: train examples/sec of the B200 hot path (+ embedding pull/push
+HBM GB/s against the measured peak), BASELINE.json configs[1] at N=1 and
+configs[2] (the same model, table hash-sharded over N GPUs) for N>1.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A step is one Trainer::train_batch over one synthetic batch (per rank:
+65536 instances x 100 slots, one Zipf(1.1) feature per slot over a 1e8-key
+space, AdaGrad sparse rows of dim 64, MLP [6400 -> 256 -> 128 -> 1], k=1).
+`value` times the device-resident path (inputs already in HBM); `e2e` times
+the same public call with pinned HOST buffers (H2D of the batch and D2H of the
+loss inside the timed region). Multi-GPU: one process per GPU (torchrun),
+weak scaling (65536 instances per rank), NCCL all-to-all of keys/rows/grads,
+device time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train examples/sec at 1/2/4/8 B200; embedding pull/push HBM GB/s vs peak"
+UNIT = "examples/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--batch", type=int, default=65536, help="instances per rank per step")
+    p.add_argument("--slots", type=int, default=100)
+    p.add_argument("--dim", type=int, default=64)
+    p.add_argument("--vocab", type=int, default=100_000_000)
+    p.add_argument("--zipf", type=float, default=1.1)
+    p.add_argument("--hidden", default="256,128")
+    p.add_argument("--pool", type=int, default=3, help="distinct pre-generated batches")
+    p.add_argument("--no-prefill", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=4096, help="instances for the CPU baseline")
+    return p.parse_args()
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def peaks():
+    m = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"))
+    if m:
+        return float(m["hbm_gbs"]), float(m["bf16_tflops"]), float(m.get("bf16_tflops_sustained", m["bf16_tflops"])), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (the profiling recipe's clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- reference arm --
+def run_reference(args, rank):
+    """The reference's own CPU implementation (oracle/_ref/libkpsim_ref.so, the
+    unmodified /root/reference/proj sources) on this host's cores: one
+    single-threaded reference Trainer per core, each training a bounded sample
+    of the same workload folded to the reference's S=1 model."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2201_05500_b200.data import make_batch
+    import tempfile
+    cores = len(os.sched_getaffinity(0))
+    per = 96  # instances per thread per step (~0.1 s of reference work each)
+    need = cores * per * (args.steps + args.warmup)
+    bt = make_batch(min(need, args.batch), V=args.vocab, zipf_s=args.zipf, n_slots=args.slots, seed=1000)
+    fb = bt.folded()
+    hidden = tuple(int(h) for h in args.hidden.split(",") if h)
+    cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=1 << 30, embedding_dim=args.dim,
+                       hidden=hidden, alpha=0.01, sparse_lr=0.05)
+    refs = [O.Ref(cfg, tempfile.mkdtemp(prefix="kpref_")) for _ in range(cores)]
+    cursor = [0]
+
+    def slice_for(i, step):
+        lo = ((step * cores + i) * per) % max(fb.n - per, 1)
+        return fb.slice(lo, lo + per)
+
+    def one_step(step):
+        ths = []
+        for i, r in enumerate(refs):
+            s = slice_for(i, step)
+            ths.append(threading.Thread(target=r.batch, args=(s.offs, s.keys, s.labels)))
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+
+    for w in range(args.warmup):
+        one_step(w)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        one_step(args.warmup + k)
+    dt = time.perf_counter() - t0
+    value = cores * per * args.steps / dt
+    sample = (f"{per} instances x {cores} threads per step, each thread an independent reference "
+              f"Trainer (N=1,k=1) on the configs[1] batch folded to S=1 (reference semantics: "
+              f"model [{args.dim}->{args.hidden.replace(',', '->')}->1])")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic Zipf(1.1) CTR", "config": workload_config(args, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world):
+    return {
+        "workload": f"configs[{1 if world == 1 else 2}]: {args.vocab // 1_000_000}M-key table, emb dim "
+                    f"{args.dim}, {args.slots} slots, batch {args.batch}/GPU, Zipf({args.zipf}) keys, "
+                    f"AdaGrad rows, k=1",
+        "global_batch": args.batch * world,
+        "slots": args.slots,
+        "embedding_dim": args.dim,
+        "table_keys": args.vocab,
+        "mlp": f"[{args.slots * args.dim}->{args.hidden.replace(',', '->')}->1]",
+        "parallelism": f"table sharded key%{world}, dp{world}" if world > 1 else "single GPU",
+        "l2": "per-step working set ~5 GB >> 126 MB L2 (no flush needed)",
+        "prefill": "table pre-populated with all keys (steady state)" if not args.no_prefill else "cold",
+    }
+
+
+# ---------------------------------------------------------------- B200 arm --
+def cpu_baseline(args, bt):
+    from oracle import oracle as O
+    import tempfile
+    n = min(args.cpu_sample, bt.n)
+    fb = bt.slice(0, n).folded()
+    hidden = tuple(int(h) for h in args.hidden.split(",") if h)
+    cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=1 << 30, embedding_dim=args.dim,
+                       hidden=hidden, alpha=0.01, sparse_lr=0.05)
+    kind = "reference" if O.ref_available() else "port"
+    r = O.Ref(cfg, tempfile.mkdtemp(prefix="kpref_")) if kind == "reference" else O.Orc(cfg, 64)
+    t0 = time.perf_counter()
+    r.batch(fb.offs, fb.keys, fb.labels)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{n} instances of the step-0 batch folded to S=1 (reference semantics, model "
+                      f"[{args.dim}->{args.hidden.replace(',', '->')}->1]), one Trainer::train_batch, "
+                      f"single-threaded like the reference"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_2201_05500_b200 as kp
+    from paper_2201_05500_b200.data import make_batch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")
+    comm = None
+    if world > 1:
+        obj = [kp.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = kp.Comm(obj[0], rank, world, local)
+
+    hidden = [int(h) for h in args.hidden.split(",") if h]
+    per_rank_keys = (args.vocab - rank + world - 1) // world
+    capacity = per_rank_keys + 1_000_000
+    tr = kp.Trainer(comm=comm, table_capacity=capacity, device=local, n_workers=world,
+                    minibatch_size=args.batch, embedding_dim=args.dim, n_slots=args.slots,
+                    hidden=hidden, k=1, alpha=0.01, sparse_lr=0.05, seed=42)
+    if not args.no_prefill:
+        tr.prefill(rank, world, per_rank_keys)
+
+    batches = [make_batch(args.batch, V=args.vocab, zipf_s=args.zipf, n_slots=args.slots,
+                          seed=1000 + 97 * rank + b) for b in range(args.pool)]
+    gfirst = rank * args.batch
+    gn = args.batch * world
+    # device-resident copies (value) and pinned host copies (e2e)
+    dev, pin = [], []
+    for bt in batches:
+        d = {"offs": torch.from_numpy(bt.offs.view(np.int32)).cuda(),
+             "keys": torch.from_numpy(bt.keys.view(np.int64)).cuda(),
+             "slots": torch.from_numpy(bt.slots.view(np.int16)).cuda(),
+             "labels": torch.from_numpy(bt.labels).cuda()}
+        dev.append(d)
+        p = {k: torch.from_numpy(v).pin_memory() for k, v in
+             (("offs", bt.offs.view(np.int32)), ("keys", bt.keys.view(np.int64)),
+              ("slots", bt.slots.view(np.int16)), ("labels", bt.labels))}
+        pin.append({"offs": p["offs"].numpy().view(np.uint32), "keys": p["keys"].numpy().view(np.uint64),
+                    "slots": p["slots"].numpy().view(np.uint16), "labels": p["labels"].numpy(),
+                    "_t": p})
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(tr.stream())
+
+    def step_dev(i):
+        bt, d = batches[i % len(batches)], dev[i % len(dev)]
+        return tr.train_batch_device(bt.offs, d["offs"].data_ptr(), d["keys"].data_ptr(),
+                                     d["slots"].data_ptr(), d["labels"].data_ptr(), bt.n,
+                                     global_n=gn, global_first=gfirst)
+
+    def step_host(i):
+        p = pin[i % len(pin)]
+        return tr.train_batch(p["offs"], p["keys"], p["labels"], slots=p["slots"], global_n=gn,
+                              global_first=gfirst)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident path -------------------------------------------
+    for i in range(args.warmup):
+        step_dev(i)
+    tr.profile(True)
+    l0 = kp.launch_count()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        w0 = time.perf_counter()
+        for i in range(args.steps):
+            r = step_dev(args.warmup + i)
+        ev1.record(stream)
+        barrier()
+        wall = time.perf_counter() - w0
+    launches = kp.launch_count() - l0
+    prof = tr.profile(False)
+    dev_ms = ev0.elapsed_time(ev1)
+    dev_ms = max_over_ranks(dev_ms)
+    value = args.batch * world * args.steps / (dev_ms / 1e3)
+    loss = r["loss"]
+
+    # ---- end-to-end through the public API with host buffers ------------
+    e2e = None
+    if not args.no_e2e:
+        step_host(0)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            step_host(i + 1)
+        e1.record(stream)
+        barrier()
+        e_ms = max_over_ranks(e0.elapsed_time(e1))
+        bt = batches[0]
+        h2d = bt.offs.nbytes + bt.keys.nbytes + bt.slots.nbytes + bt.labels.nbytes
+        e2e = {"value": args.batch * world * args.steps / (e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 + 8 + 16,
+               "ms_per_step": e_ms / args.steps}
+
+    # ---- roofline (per-stage CUDA events on the trainer's stream) --------
+    hbm, bf16, bf16s, pk = peaks()
+    K = max(prof["steps"], 1)
+    U = prof["unique"] / K
+    O_ = prof["occurrences"] / K
+    e, B, S = args.dim, args.batch, args.slots
+    R = 2  # AdaGrad {w, acc}
+    D_in = S * e
+    flops = 6.0 * B * (D_in * hidden[0] + sum(a * b for a, b in zip(hidden, hidden[1:] + [1])))
+    stage_bytes = {
+        "dedup": 8 * O_ + 8 * U + 4 * O_,                  # keys in, unique out, inverse out
+        "pull": 16 * U,                                     # one slot read per unique key
+        "pool": 4 * e * U + 4 * O_ + 4 * e * B * S,         # rows, inverse, pooled out
+        "push": 4 * e * B * S + 8 * O_ + 2 * R * 4 * e * U, # dpooled in, order, state r/w (fused)
+    }
+    stages = {}
+    for name, ms in ((k, prof[k]) for k in ("dedup", "pull", "pool", "mlp", "push", "dense", "exchange")):
+        per = ms / K
+        ent = {"ms_per_step": per}
+        if name in stage_bytes and per > 0:
+            gbs = stage_bytes[name] / (per / 1e3) / 1e9
+            ent.update({"bytes": stage_bytes[name], "achieved_gbs": gbs, "frac": gbs / hbm})
+        if name == "mlp" and per > 0:
+            tf = flops / (per / 1e3) / 1e12
+            ent.update({"flops": flops, "achieved_tflops": tf, "frac_bf16_sustained": tf / bf16s})
+        stages[name] = ent
+    dom = max(stages, key=lambda k: stages[k]["ms_per_step"])
+    if dom == "mlp":
+        roof = {"kernel": "mlp (fp32 SIMT fwd+bwd)", "bound": "tensor",
+                "achieved": stages["mlp"]["achieved_tflops"], "peak": bf16s, "unit": "TFLOP/s",
+                "frac": stages["mlp"]["achieved_tflops"] / bf16s, "traffic": None,
+                "peak_kind": f"{pk} bf16 sustained"}
+    else:
+        roof = {"kernel": dom, "bound": "hbm", "achieved": stages[dom].get("achieved_gbs"),
+                "peak": hbm, "unit": "GB/s", "frac": stages[dom].get("frac"), "traffic": None,
+                "peak_kind": f"{pk} copy"}
+    emb = {k: stages[k] for k in ("pool", "push") if "achieved_gbs" in stages[k]}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline(args, batches[0])
+            except Exception as ex:  # the baseline is reported, never required
+                cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                       "sample": f"unavailable: {ex}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic Zipf CTR batches (random-init dense weights)",
+            "config": workload_config(args, world),
+            "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "stages": stages,
+            "embedding_pull_push": emb, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "loss": loss, "unique_keys_per_step": U, "occurrences_per_step": O_,
+            "wall_ms_per_step": wall / args.steps * 1e3,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,1040 @@
+// The C ABI (include/kpsim_b200.h) and the per-batch trainer orchestration.
+//
+// Trainer::process_batch (proj/src/trainer.cpp:115-259) becomes, per
+// minibatch step on each rank:
+//   dedup(step keys) -> [G>1: owner bucket, key all-to-all, owner dedup]
+//   -> table pull (insert-if-absent) -> [G>1: row all-to-all] -> bag pooling
+//   -> per local worker MLP fwd/bwd -> segmented reduce by unique key
+//   -> [G>1: grad all-to-all, owner reduce in source order] -> x 1/N + rule
+//   -> dense k-step Adam (allgather + centered mean at merges).
+// NCCL runs on the trainer's stream; one process per GPU.
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kp_table.cuh"
+#include "../../include/kpsim_b200.h"
+
+using namespace kp;
+
+namespace {
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return KP_OK;
+  } catch (const KpError& e) {
+    return set_err(e.status, e.what());
+  } catch (const std::exception& e) {
+    return set_err(KP_ERR, e.what());
+  }
+}
+
+#define KP_NCCL(x)                                                                        \
+  do {                                                                                    \
+    ncclResult_t r_ = (x);                                                                \
+    if (r_ != ncclSuccess)                                                                \
+      throw KpError(kErrNccl, std::string("NCCL error ") + ncclGetErrorString(r_) + " at " + \
+                                  __FILE__ + ":" + std::to_string(__LINE__));             \
+  } while (0)
+
+cudaStream_t st(kp_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+__global__ void k_gather_u64(const uint64_t* __restrict__ src, const uint32_t* __restrict__ idx,
+                             uint32_t n, uint64_t* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = src[idx[i]];
+}
+__global__ void k_compose(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, uint32_t n,
+                          uint32_t* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = a[b[i]];
+}
+__global__ void k_key_range(uint64_t start, uint64_t step, uint32_t n, uint64_t* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = start + (uint64_t)i * step;
+}
+unsigned grid1(uint64_t n) {
+  uint64_t g = (n + 255) / 256;
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, 148 * 16));
+}
+}  // namespace
+
+std::atomic<uint64_t> g_launches{0};
+void kp::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+struct MergeWs {
+  DevBuf allg, cm, terms;
+};
+
+struct kp_table {
+  Table* t = nullptr;
+  cudaStream_t s = nullptr;
+  DevBuf keys, rows, w, s1, s2, grads, scratch;
+};
+
+struct kp_comm {
+  ncclComm_t nc = nullptr;
+  int rank = 0, world = 1, device = 0;
+};
+
+// ---------------------------------------------------------------------------
+struct kp_trainer {
+  kp_trainer_config cfg{};
+  int device = 0;
+  cudaStream_t s = nullptr;
+  kp_comm* comm = nullptr;
+  int rank = 0, world = 1;
+  uint32_t W = 1, N = 1, S = 1, e = 1;
+  MlpShape shape;
+  kp_table tab;
+  float *x = nullptr, *m = nullptr, *v = nullptr, *vbar = nullptr, *g = nullptr;
+  uint64_t D = 0;
+  uint64_t t_global = 0, merges = 0;
+  // inputs
+  DevBuf in_offs, in_keys, in_slots, in_labels;
+  std::vector<uint32_t> h_offs;
+  // step buffers
+  DevBuf st_offs, st_keys, st_slots, st_labels;
+  DedupWs dd, dd_owner;
+  ShardWs sh;
+  SegWs sg, sg_owner;
+  MlpWs mlp;
+  MergeWs mws;
+  DevBuf rows, bag_offs, bag_of_occ, pooled, inv_count, dpooled, preds, err, loss, check;
+  DevBuf xbar, pred_keep, lossg;
+  // exchange buffers (G > 1)
+  DevBuf perm, pos, send_keys, recv_keys, owner_rows, owner_idx, send_rows, recv_rows, send_grads,
+      recv_grads, counts_dev;
+  std::vector<uint64_t> cnt_send, cnt_recv, off_send, off_recv;
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  double stage_ms[7] = {0};
+  uint64_t prof_steps = 0, prof_unique = 0, prof_occ = 0, prof_owner_unique = 0, prof_recv = 0;
+  std::vector<std::pair<int, int>> marks;  // (stage, event index) pairs for this batch
+  int ev_used = 0;
+
+  cudaEvent_t next_event() {
+    if (ev_used >= (int)ev.size()) {
+      cudaEvent_t e;
+      KP_CUDA(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+    return ev[ev_used++];
+  }
+  // mark the END of `stage` (the previous mark is its start)
+  void mark(int stage) {
+    if (!prof) return;
+    cudaEvent_t e = next_event();
+    KP_CUDA(cudaEventRecord(e, s));
+    marks.push_back({stage, ev_used - 1});
+  }
+  void harvest() {
+    if (!prof) return;
+    KP_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 1; i < marks.size(); ++i) {
+      if (marks[i].first < 0) continue;
+      float ms = 0;
+      KP_CUDA(cudaEventElapsedTime(&ms, ev[marks[i - 1].second], ev[marks[i].second]));
+      stage_ms[marks[i].first] += ms;
+    }
+    marks.clear();
+    ev_used = 0;
+  }
+  ~kp_trainer() {
+    for (auto e : ev) cudaEventDestroy(e);
+    if (tab.t) table_destroy(tab.t);
+    if (tab.s) cudaStreamDestroy(tab.s);
+    cudaFree(x);
+    cudaFree(m);
+    cudaFree(v);
+    cudaFree(vbar);
+    cudaFree(g);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+namespace {
+
+void all_to_all(kp_trainer* tr, const void* send, const std::vector<uint64_t>& scnt,
+                const std::vector<uint64_t>& soff, void* recv, const std::vector<uint64_t>& rcnt,
+                const std::vector<uint64_t>& roff, size_t elem, ncclDataType_t dt) {
+  const int R = tr->world, me = tr->rank;
+  auto* sb = static_cast<const char*>(send);
+  auto* rb = static_cast<char*>(recv);
+  const size_t dts = (dt == ncclUint64 || dt == ncclFloat64) ? 8 : 4;
+  const size_t per = elem / dts;  // datatype elements per logical element
+  if (scnt[me])
+    KP_CUDA(cudaMemcpyAsync(rb + roff[me] * elem, sb + soff[me] * elem, scnt[me] * elem,
+                            cudaMemcpyDeviceToDevice, tr->s));
+  KP_NCCL(ncclGroupStart());
+  for (int p = 0; p < R; ++p) {
+    if (p == me) continue;
+    if (scnt[p]) KP_NCCL(ncclSend(sb + soff[p] * elem, scnt[p] * per, dt, p, tr->comm->nc, tr->s));
+    if (rcnt[p]) KP_NCCL(ncclRecv(rb + roff[p] * elem, rcnt[p] * per, dt, p, tr->comm->nc, tr->s));
+  }
+  KP_NCCL(ncclGroupEnd());
+}
+
+// gather [W][D] local blocks of every rank into out [N][D] (ascending global worker)
+void allgather_workers(kp_comm* comm, cudaStream_t s, const float* local, float* out, size_t n) {
+  if (!comm || comm->world == 1) {
+    if (out != local) KP_CUDA(cudaMemcpyAsync(out, local, n * 4, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  KP_NCCL(ncclAllGather(local, out, n, ncclFloat32, comm->nc, s));
+}
+
+// global_merge (optimizer.cpp:56-84) over W local workers x all ranks; moments
+// already accumulated. v_bar = cmean(v_i); x_i = cmean(x_j - a m_j/sqrt(v_bar)).
+void merge_states(kp_comm* comm, cudaStream_t s, uint32_t W, uint64_t D, float* x, float* m,
+                  float* v, float* vbar, float alpha, bool reset, MergeWs& ws) {
+  const uint32_t N = W * (comm ? comm->world : 1);
+  const bool local = !comm || comm->world == 1;
+  float* all = local ? nullptr : ws.allg.get<float>((size_t)N * D);
+  float* vb = ws.cm.get<float>(D);
+  float* terms = ws.terms.get<float>((size_t)W * D);
+  if (!local) allgather_workers(comm, s, v, all, (size_t)W * D);
+  centered_mean(local ? v : all, D, N, D, vb, s);
+  for (uint32_t l = 0; l < W; ++l) merge_terms(x + l * D, m + l * D, vb, D, alpha, terms + l * D, s);
+  if (!local) allgather_workers(comm, s, terms, all, (size_t)W * D);
+  centered_mean(local ? terms : all, D, N, D, x, s);  // merged x into worker 0
+  for (uint32_t l = 0; l < W; ++l) {
+    if (l) KP_CUDA(cudaMemcpyAsync(x + l * D, x, D * 4, cudaMemcpyDeviceToDevice, s));
+    KP_CUDA(cudaMemcpyAsync(vbar + l * D, vb, D * 4, cudaMemcpyDeviceToDevice, s));
+    if (reset) KP_CUDA(cudaMemcpyAsync(v + l * D, vb, D * 4, cudaMemcpyDeviceToDevice, s));
+  }
+}
+
+void compute_xbar(kp_trainer* tr, float* out) {
+  float* all = tr->x;
+  if (tr->world > 1) {
+    all = tr->mws.allg.get<float>((size_t)tr->N * tr->D);
+    allgather_workers(tr->comm, tr->s, tr->x, all, (size_t)tr->W * tr->D);
+  }
+  centered_mean(all, tr->D, tr->N, tr->D, out, tr->s);
+}
+
+struct StepView {
+  const uint32_t* offs;  // device, n_inst+1 entries, absolute values with occ_base
+  uint32_t occ_base;
+  const uint64_t* keys;  // device, starting at the step's first occurrence
+  const uint16_t* slots;
+  const int32_t* labels;
+  uint32_t n_inst, n_occ;
+  std::vector<uint32_t> wlo, whi;  // local worker instance ranges in step coords
+};
+
+// Embedding stage for a step: dedup, (exchange), pull, pool. Leaves the
+// segment structure in tr->dd and the per-unique source index for the push.
+struct PullResult {
+  const float* src;
+  const uint32_t* idx;
+  uint32_t U;
+};
+
+PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
+  cudaStream_t s = tr->s;
+  dedup(sv.keys, sv.n_occ, tr->dd, s);
+  tr->mark(0);
+  const uint32_t U = tr->dd.n_unique;
+  PullResult pr{};
+  pr.U = U;
+  if (tr->world == 1) {
+    uint32_t* rows = tr->rows.get<uint32_t>(std::max<uint32_t>(U, 1));
+    table_pull(tr->tab.t, tr->dd.d_unique, U, rows, stamp, s);
+    pr.src = tr->tab.t->d_w;
+    pr.idx = rows;
+    tr->mark(1);
+  } else {
+    const int R = tr->world;
+    uint32_t* perm = tr->perm.get<uint32_t>(std::max<uint32_t>(U, 1));
+    uint32_t* pos = tr->pos.get<uint32_t>(std::max<uint32_t>(U, 1));
+    tr->cnt_send.assign(R, 0);
+    shard(tr->dd.d_unique, U, R, perm, pos, tr->cnt_send.data(), tr->sh, s);
+    uint64_t* sk = tr->send_keys.get<uint64_t>(std::max<uint32_t>(U, 1));
+    if (U) k_gather_u64<<<grid1(U), 256, 0, s>>>(tr->dd.d_unique, perm, U, sk); ::kp::count_launch();
+    // counts matrix via allgather
+    uint64_t* cd = tr->counts_dev.get<uint64_t>((size_t)R * R + R);
+    KP_CUDA(cudaMemcpyAsync(cd, tr->cnt_send.data(), R * 8, cudaMemcpyHostToDevice, s));
+    KP_NCCL(ncclAllGather(cd, cd + R, R, ncclUint64, tr->comm->nc, s));
+    std::vector<uint64_t> mat((size_t)R * R);
+    KP_CUDA(cudaMemcpyAsync(mat.data(), cd + R, (size_t)R * R * 8, cudaMemcpyDeviceToHost, s));
+    KP_CUDA(cudaStreamSynchronize(s));
+    tr->cnt_recv.assign(R, 0);
+    tr->off_send.assign(R, 0);
+    tr->off_recv.assign(R, 0);
+    uint64_t tot = 0;
+    for (int p = 0; p < R; ++p) {
+      tr->cnt_recv[p] = mat[(size_t)p * R + tr->rank];
+      tr->off_recv[p] = tot;
+      tot += tr->cnt_recv[p];
+    }
+    for (int p = 1; p < R; ++p) tr->off_send[p] = tr->off_send[p - 1] + tr->cnt_send[p - 1];
+    const uint32_t Rn = (uint32_t)tot;
+    uint64_t* rk = tr->recv_keys.get<uint64_t>(std::max<uint32_t>(Rn, 1));
+    all_to_all(tr, sk, tr->cnt_send, tr->off_send, rk, tr->cnt_recv, tr->off_recv, 8, ncclUint64);
+    tr->mark(6);
+    // owner side: dedup received keys (stable: source order inside a key)
+    dedup(rk, Rn, tr->dd_owner, s);
+    tr->mark(0);
+    const uint32_t Uo = tr->dd_owner.n_unique;
+    uint32_t* orows = tr->owner_rows.get<uint32_t>(std::max<uint32_t>(Uo, 1));
+    table_pull(tr->tab.t, tr->dd_owner.d_unique, Uo, orows, stamp, s);
+    uint32_t* oidx = tr->owner_idx.get<uint32_t>(std::max<uint32_t>(Rn, 1));
+    if (Rn) k_compose<<<grid1(Rn), 256, 0, s>>>(orows, tr->dd_owner.d_inverse, Rn, oidx); ::kp::count_launch();
+    float* srows = tr->send_rows.get<float>((size_t)std::max<uint32_t>(Rn, 1) * tr->e);
+    gather_rows(tr->tab.t->d_w, oidx, Rn, tr->e, srows, s);
+    tr->mark(1);
+    float* rrows = tr->recv_rows.get<float>((size_t)std::max<uint32_t>(U, 1) * tr->e);
+    all_to_all(tr, srows, tr->cnt_recv, tr->off_recv, rrows, tr->cnt_send, tr->off_send,
+               4 * (size_t)tr->e, ncclFloat32);
+    // NB: all_to_all counts are in elements of `elem` bytes: rows of e floats
+    tr->mark(6);
+    pr.src = rrows;
+    pr.idx = pos;
+  }
+  // bags + pooling
+  const uint32_t nb = sv.n_inst * tr->S;
+  uint32_t* bag_offs = tr->bag_offs.get<uint32_t>(nb + 1);
+  uint32_t* bag_of_occ = tr->bag_of_occ.get<uint32_t>(std::max<uint32_t>(sv.n_occ, 1));
+  uint32_t* err = tr->err.get<uint32_t>(4);
+  prepare_bags(sv.offs, sv.occ_base, sv.slots, sv.n_inst, tr->S, bag_offs, bag_of_occ, err, s);
+  float* pooled = tr->pooled.get<float>((size_t)std::max<uint32_t>(nb, 1) * tr->e);
+  float* invc = tr->inv_count.get<float>(std::max<uint32_t>(nb, 1));
+  pool(bag_offs, nb, tr->dd.d_inverse, pr.idx, pr.src, tr->e, tr->cfg.pooling == 1, pooled, invc, s);
+  tr->mark(2);
+  return pr;
+}
+
+void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fused_preds) {
+  cudaStream_t s = tr->s;
+  const uint64_t D = tr->D;
+  const uint32_t in_w = tr->S * tr->e;
+  tr->mark(-1);
+  PullResult pr = pull_and_pool(tr, sv, false);
+  if (tr->prof) {
+    tr->prof_unique += pr.U;
+    tr->prof_occ += sv.n_occ;
+    if (tr->world > 1) {
+      tr->prof_owner_unique += tr->dd_owner.n_unique;
+      for (auto c : tr->cnt_recv) tr->prof_recv += c;
+    }
+  }
+  const float* pooled = static_cast<const float*>(tr->pooled.p);
+  const float* invc = static_cast<const float*>(tr->inv_count.p);
+  float* dpooled = tr->dpooled.get<float>((size_t)std::max<uint32_t>(sv.n_inst, 1) * in_w);
+  float* preds = tr->preds.get<float>(std::max<uint32_t>(sv.n_inst, 1));
+  for (uint32_t l = 0; l < tr->W; ++l) {
+    const uint32_t lo = sv.wlo[l], hi = sv.whi[l], Bw = hi - lo;
+    if (Bw == 0) {
+      KP_CUDA(cudaMemsetAsync(tr->g + l * D, 0, D * 4, s));
+      continue;
+    }
+    mlp_forward(tr->shape, tr->x + l * D, pooled + (size_t)lo * in_w, Bw, preds + lo, tr->mlp, s);
+    mlp_backward(tr->shape, tr->x + l * D, pooled + (size_t)lo * in_w, Bw, preds + lo,
+                 sv.labels + lo, tr->g + l * D, dpooled + (size_t)lo * in_w,
+                 tr->cfg.pooling == 1 ? invc + (size_t)lo * tr->S : nullptr, tr->S, tr->e,
+                 d_loss_slot, tr->mlp, s);
+  }
+  if (fused_preds)
+    KP_CUDA(cudaMemcpyAsync(fused_preds, preds, (size_t)sv.n_inst * 4, cudaMemcpyDeviceToDevice, s));
+  tr->mark(3);
+  // sparse push (x 1/N, trainer.cpp:202-207)
+  SparseRule rule{tr->cfg.sparse_rule, (float)tr->cfg.sparse_lr, (float)tr->cfg.sparse_beta1,
+                  (float)tr->cfg.sparse_beta2};
+  const float inv_n = (float)(1.0 / (double)tr->N);
+  if (tr->world == 1) {
+    seg_reduce_apply(tr->dd.d_seg, pr.U, tr->dd.sorted_vals, static_cast<const uint32_t*>(tr->bag_of_occ.p),
+                     sv.n_occ, dpooled, tr->e, inv_n, tr->tab.t, pr.idx, rule, nullptr, nullptr,
+                     tr->sg, s);
+    tr->mark(4);
+  } else {
+    float* sgr = tr->send_grads.get<float>((size_t)std::max<uint32_t>(pr.U, 1) * tr->e);
+    seg_reduce_apply(tr->dd.d_seg, pr.U, tr->dd.sorted_vals, static_cast<const uint32_t*>(tr->bag_of_occ.p),
+                     sv.n_occ, dpooled, tr->e, 1.0f, nullptr, nullptr, rule, sgr,
+                     static_cast<const uint32_t*>(tr->pos.p), tr->sg, s);
+    tr->mark(4);
+    uint64_t Rn = 0;
+    for (auto c : tr->cnt_recv) Rn += c;
+    float* rgr = tr->recv_grads.get<float>((size_t)std::max<uint64_t>(Rn, 1) * tr->e);
+    all_to_all(tr, sgr, tr->cnt_send, tr->off_send, rgr, tr->cnt_recv, tr->off_recv,
+               4 * (size_t)tr->e, ncclFloat32);
+    tr->mark(6);
+    seg_reduce_apply(tr->dd_owner.d_seg, tr->dd_owner.n_unique, tr->dd_owner.sorted_vals, nullptr,
+                     (uint32_t)Rn, rgr, tr->e, inv_n, tr->tab.t,
+                     static_cast<const uint32_t*>(tr->owner_rows.p), rule, nullptr, nullptr,
+                     tr->sg_owner, s);
+    tr->mark(4);
+  }
+  // dense k-step Adam (KStepEngine::step, optimizer.cpp:113-144)
+  const uint64_t t = tr->t_global + 1;
+  const bool merged = (t % tr->cfg.k) == 0;
+  AdamParams h{(float)tr->cfg.alpha, (float)tr->cfg.beta1, (float)tr->cfg.beta2};
+  if (!merged) {
+    for (uint32_t l = 0; l < tr->W; ++l)
+      dense_local_step(tr->x + l * D, tr->m + l * D, tr->v + l * D, tr->vbar + l * D, tr->g + l * D,
+                       D, h, s);
+  } else {
+    for (uint32_t l = 0; l < tr->W; ++l) dense_moments(tr->m + l * D, tr->v + l * D, tr->g + l * D, D, h, s);
+    merge_states(tr->comm, s, tr->W, D, tr->x, tr->m, tr->v, tr->vbar, h.alpha,
+                 tr->cfg.reset_local_v != 0, tr->mws);
+    tr->merges++;
+  }
+  tr->t_global = t;
+  uint32_t* chk = static_cast<uint32_t*>(tr->check.p);
+  for (uint32_t l = 0; l < tr->W; ++l)
+    dense_check(tr->v + l * D, tr->vbar + l * D, tr->x + l * D, D, chk, s);
+  tr->mark(5);
+}
+
+void predict_pass(kp_trainer* tr, const StepView& sv, float* d_preds_out) {
+  float* xb = tr->xbar.get<float>(tr->D);
+  compute_xbar(tr, xb);
+  pull_and_pool(tr, sv, false);
+  mlp_forward(tr->shape, xb, static_cast<const float*>(tr->pooled.p), sv.n_inst, d_preds_out,
+              tr->mlp, tr->s);
+  tr->mark(3);
+}
+
+void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_offs,
+                      const uint64_t* d_keys, const uint16_t* d_slots, const int32_t* d_labels,
+                      uint32_t n, uint64_t global_n, uint64_t global_first, bool predict_first,
+                      float* h_preds, kp_batch_result* out) {
+  KP_CHECK(n >= 1 || tr->world > 1, kErrGeneric, "train_batch: empty batch");
+  KP_CHECK(global_n >= 1, kErrGeneric, "train_batch: empty batch");
+  KP_CHECK(tr->S == 1 || d_slots != nullptr, kErrConfig, "slots must be given when n_slots > 1");
+  cudaStream_t s = tr->s;
+  const uint64_t N = tr->N, W = tr->W, r = tr->rank;
+  const uint64_t mb = tr->cfg.minibatch_size;
+  const uint64_t n_mb = std::max<uint64_t>(1, (global_n + N * mb - 1) / (N * mb));
+  const uint64_t cells = N * n_mb, base = global_n / cells, extra = global_n % cells;
+  auto cstart = [&](uint64_t c) { return c * base + std::min(c, extra); };
+  const uint64_t my_lo = cstart(r * W * n_mb), my_hi = cstart((r + 1) * W * n_mb);
+  KP_CHECK(global_first == my_lo && global_first + n == my_hi, kErrConfig,
+           "train_batch: slice [" + std::to_string(global_first) + ", " +
+               std::to_string(global_first + n) + ") is not this rank's shard_batch range [" +
+               std::to_string(my_lo) + ", " + std::to_string(my_hi) + ")");
+  KP_CHECK(h_offs[0] == 0, kErrGeneric, "offs[0] must be 0");
+  uint32_t* err = tr->err.get<uint32_t>(4);
+  KP_CUDA(cudaMemsetAsync(err, 0xFF, 4, s));
+  KP_CUDA(cudaMemsetAsync(tr->check.get<uint32_t>(1), 0, 4, s));
+  double* d_loss = tr->loss.get<double>(n_mb);
+  KP_CUDA(cudaMemsetAsync(d_loss, 0, n_mb * 8, s));
+
+  const bool fused = predict_first && n_mb == 1 && (tr->t_global % tr->cfg.k == 0);
+  float* d_pred_keep = nullptr;
+  if (predict_first) {
+    d_pred_keep = tr->pred_keep.get<float>(std::max<uint32_t>(n, 1));
+    if (!fused) {
+      StepView pv;
+      pv.offs = d_offs;
+      pv.occ_base = 0;
+      pv.keys = d_keys;
+      pv.slots = d_slots;
+      pv.labels = d_labels;
+      pv.n_inst = n;
+      pv.n_occ = h_offs[n];
+      tr->mark(-1);
+      predict_pass(tr, pv, d_pred_keep);
+    }
+  }
+  const uint64_t steps_before = tr->t_global, merges_before = tr->merges;
+  for (uint64_t j = 0; j < n_mb; ++j) {
+    StepView sv;
+    sv.wlo.resize(W);
+    sv.whi.resize(W);
+    std::vector<uint64_t> lo(W), hi(W);
+    for (uint64_t l = 0; l < W; ++l) {
+      const uint64_t c = (r * W + l) * n_mb + j;
+      lo[l] = cstart(c) - global_first;
+      hi[l] = cstart(c + 1) - global_first;
+    }
+    const bool contiguous = W == 1 || n_mb == 1;
+    if (contiguous) {
+      const uint64_t a = lo[0], b = hi[W - 1];
+      sv.offs = d_offs + a;
+      sv.occ_base = h_offs[a];
+      sv.keys = d_keys + h_offs[a];
+      sv.slots = d_slots ? d_slots + h_offs[a] : nullptr;
+      sv.labels = d_labels + a;
+      sv.n_inst = (uint32_t)(b - a);
+      sv.n_occ = h_offs[b] - h_offs[a];
+      for (uint64_t l = 0; l < W; ++l) {
+        sv.wlo[l] = (uint32_t)(lo[l] - a);
+        sv.whi[l] = (uint32_t)(hi[l] - a);
+      }
+    } else {
+      // gather the local workers' cells for minibatch j into step buffers
+      uint32_t ninst = 0, nocc = 0;
+      for (uint64_t l = 0; l < W; ++l) {
+        ninst += (uint32_t)(hi[l] - lo[l]);
+        nocc += h_offs[hi[l]] - h_offs[lo[l]];
+      }
+      std::vector<uint32_t> so(ninst + 1);
+      uint64_t* sk = tr->st_keys.get<uint64_t>(std::max<uint32_t>(nocc, 1));
+      uint16_t* ss = d_slots ? tr->st_slots.get<uint16_t>(std::max<uint32_t>(nocc, 1)) : nullptr;
+      int32_t* sl = tr->st_labels.get<int32_t>(std::max<uint32_t>(ninst, 1));
+      uint32_t* sof = tr->st_offs.get<uint32_t>(ninst + 1);
+      uint32_t ci = 0, co = 0;
+      so[0] = 0;
+      for (uint64_t l = 0; l < W; ++l) {
+        sv.wlo[l] = ci;
+        const uint32_t o0 = h_offs[lo[l]], o1 = h_offs[hi[l]];
+        for (uint64_t i = lo[l]; i < hi[l]; ++i) so[++ci] = co + (h_offs[i + 1] - o0);
+        if (o1 > o0) {
+          KP_CUDA(cudaMemcpyAsync(sk + co, d_keys + o0, (size_t)(o1 - o0) * 8, cudaMemcpyDeviceToDevice, s));
+          if (ss) KP_CUDA(cudaMemcpyAsync(ss + co, d_slots + o0, (size_t)(o1 - o0) * 2, cudaMemcpyDeviceToDevice, s));
+        }
+        if (hi[l] > lo[l])
+          KP_CUDA(cudaMemcpyAsync(sl + sv.wlo[l], d_labels + lo[l], (hi[l] - lo[l]) * 4, cudaMemcpyDeviceToDevice, s));
+        co += o1 - o0;
+        sv.whi[l] = ci;
+      }
+      KP_CUDA(cudaMemcpyAsync(sof, so.data(), (ninst + 1) * 4, cudaMemcpyHostToDevice, s));
+      KP_CUDA(cudaStreamSynchronize(s));  // `so` is a host temporary
+      sv.offs = sof;
+      sv.occ_base = 0;
+      sv.keys = sk;
+      sv.slots = ss;
+      sv.labels = sl;
+      sv.n_inst = ninst;
+      sv.n_occ = nocc;
+    }
+    run_step(tr, sv, d_loss + j, fused && j == 0 ? d_pred_keep : nullptr);
+  }
+  // error flags, loss, predictions
+  uint32_t h_err = 0, h_chk = 0;
+  KP_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, s));
+  KP_CUDA(cudaMemcpyAsync(&h_chk, tr->check.p, 4, cudaMemcpyDeviceToHost, s));
+  std::vector<double> lsum(n_mb);
+  KP_CUDA(cudaMemcpyAsync(lsum.data(), d_loss, n_mb * 8, cudaMemcpyDeviceToHost, s));
+  if (predict_first && h_preds)
+    KP_CUDA(cudaMemcpyAsync(h_preds, d_pred_keep, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+  KP_CUDA(cudaStreamSynchronize(s));
+  tr->harvest();
+  if (tr->prof) tr->prof_steps += n_mb;
+  KP_CHECK(h_err == 0xFFFFFFFFu, kErrConfig,
+           "slot ids must be < n_slots and non-decreasing within an instance (occurrence " +
+               std::to_string(h_err) + ")");
+  table_check_full(tr->tab.t, s);
+  KP_CHECK(!(h_chk & 1), kErrGeneric, "non-finite worker state after step " + std::to_string(tr->t_global));
+  KP_CHECK(!(h_chk & 2), kErrGeneric, "second moment lost positivity at step " + std::to_string(tr->t_global));
+  // per-step loss = sum_workers loss_i*|mb_i| / sum |mb_i|  (trainer.cpp:177-178,221-223)
+  if (tr->world > 1) {
+    double* dl = tr->lossg.get<double>((size_t)n_mb * tr->world);
+    KP_CUDA(cudaMemcpyAsync(d_loss, lsum.data(), n_mb * 8, cudaMemcpyHostToDevice, s));
+    KP_NCCL(ncclAllGather(d_loss, dl, n_mb, ncclFloat64, tr->comm->nc, s));
+    std::vector<double> all((size_t)n_mb * tr->world);
+    KP_CUDA(cudaMemcpyAsync(all.data(), dl, all.size() * 8, cudaMemcpyDeviceToHost, s));
+    KP_CUDA(cudaStreamSynchronize(s));
+    for (uint64_t j = 0; j < n_mb; ++j) {
+      double t = 0;
+      for (int p = 0; p < tr->world; ++p) t += all[(size_t)p * n_mb + j];
+      lsum[j] = t;
+    }
+  }
+  double total = 0;
+  uint64_t cnt = 0;
+  for (uint64_t j = 0; j < n_mb; ++j) {
+    uint64_t count = 0;
+    for (uint64_t w = 0; w < N; ++w) count += cstart(w * n_mb + j + 1) - cstart(w * n_mb + j);
+    if (count > 0) {
+      total += lsum[j] / (double)count;
+      ++cnt;
+    }
+  }
+  out->loss = cnt ? total / (double)cnt : std::nan("");
+  out->minibatch_steps = tr->t_global - steps_before;
+  out->merges = tr->merges - merges_before;
+  out->steps_total = tr->t_global;
+  out->merges_total = tr->merges;
+}
+
+}  // namespace
+
+// ============================================================== C ABI ====
+extern "C" {
+
+const char* kp_last_error(void) { return g_err.c_str(); }
+const char* kp_version(void) { return "kpsim_b200 0.1.0 (sm_100a)"; }
+uint64_t kp_launch_count(void) { return g_launches.load(); }
+
+int kp_device_count(int* n) {
+  return guard([&] { KP_CUDA(cudaGetDeviceCount(n)); });
+}
+int kp_host_alloc(size_t bytes, void** out) {
+  return guard([&] { KP_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocDefault)); });
+}
+int kp_host_free(void* p) {
+  return guard([&] { KP_CUDA(cudaFreeHost(p)); });
+}
+int kp_set_device(int device) {
+  return guard([&] { KP_CUDA(cudaSetDevice(device)); });
+}
+int kp_dev_alloc(size_t bytes, void** out) {
+  return guard([&] { KP_CUDA(cudaMalloc(out, bytes ? bytes : 1)); });
+}
+int kp_dev_free(void* p) {
+  return guard([&] { KP_CUDA(cudaFree(p)); });
+}
+int kp_memcpy_h2d(void* d_dst, const void* src, size_t bytes) {
+  return guard([&] { if (bytes) KP_CUDA(cudaMemcpy(d_dst, src, bytes, cudaMemcpyHostToDevice)); });
+}
+int kp_memcpy_d2h(void* dst, const void* d_src, size_t bytes) {
+  return guard([&] { if (bytes) KP_CUDA(cudaMemcpy(dst, d_src, bytes, cudaMemcpyDeviceToHost)); });
+}
+int kp_memset_d(void* d_dst, int value, size_t bytes) {
+  return guard([&] { if (bytes) KP_CUDA(cudaMemset(d_dst, value, bytes)); });
+}
+
+// ---- table ----
+int kp_table_create(int device, uint64_t capacity, uint32_t dim, int rule, float init_w,
+                    float init_s1, float init_s2, kp_table** out) {
+  return guard([&] {
+    auto h = std::make_unique<kp_table>();
+    h->t = table_create(device, capacity, dim, rule, init_w, init_s1, init_s2);
+    KP_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    *out = h.release();
+  });
+}
+int kp_table_destroy(kp_table* t) {
+  return guard([&] {
+    if (!t) return;
+    if (t->s) cudaStreamDestroy(t->s);
+    table_destroy(t->t);
+    delete t;
+  });
+}
+int kp_table_size(kp_table* t, uint64_t* n) {
+  return guard([&] { *n = table_size(t->t, t->s); });
+}
+int kp_table_pull(kp_table* t, const uint64_t* d_keys, uint32_t n, uint32_t* d_rows, kp_stream s) {
+  return guard([&] { table_pull(t->t, d_keys, n, d_rows, false, st(s)); });
+}
+int kp_table_insert_range(kp_table* t, uint64_t start, uint64_t step, uint64_t count, kp_stream s) {
+  return guard([&] {
+    KP_CUDA(cudaSetDevice(t->t->device));
+    const uint64_t chunk = 1ull << 24;
+    uint64_t* dk = t->keys.get<uint64_t>(std::min(count, chunk));
+    uint32_t* dr = t->rows.get<uint32_t>(std::min(count, chunk));
+    for (uint64_t i = 0; i < count; i += chunk) {
+      const uint32_t n = (uint32_t)std::min(chunk, count - i);
+      k_key_range<<<grid1(n), 256, 0, st(s)>>>(start + i * step, step, n, dk); ::kp::count_launch();
+      table_pull(t->t, dk, n, dr, false, st(s));
+    }
+    KP_CUDA(cudaStreamSynchronize(st(s)));
+    table_check_full(t->t, st(s));
+  });
+}
+int kp_table_lookup(kp_table* t, const uint64_t* d_keys, uint32_t n, uint32_t* d_rows, kp_stream s) {
+  return guard([&] { table_lookup(t->t, d_keys, n, d_rows, st(s)); });
+}
+int kp_table_gather(kp_table* t, const uint32_t* d_rows, uint32_t n, float* d_w, float* d_s1,
+                    float* d_s2, kp_stream s) {
+  return guard([&] { table_gather(t->t, d_rows, n, d_w, d_s1, d_s2, st(s)); });
+}
+int kp_table_set_rows(kp_table* t, const uint32_t* d_rows, uint32_t n, const float* d_w,
+                      const float* d_s1, const float* d_s2, kp_stream s) {
+  return guard([&] { table_set_rows(t->t, d_rows, n, d_w, d_s1, d_s2, st(s)); });
+}
+int kp_table_apply(kp_table* t, const uint32_t* d_rows, const float* d_grads, uint32_t n, float lr,
+                   float beta1, float beta2, kp_stream s) {
+  return guard([&] { table_apply(t->t, d_rows, d_grads, n, lr, beta1, beta2, st(s)); });
+}
+
+int kp_store_pull_batch(kp_table* t, const uint64_t* keys, uint32_t n, float* w, float* s1,
+                        float* s2) {
+  return guard([&] {
+    KP_CHECK(n >= 1, kErrStore, "pull_batch: empty key set");
+    Table* tb = t->t;
+    KP_CUDA(cudaSetDevice(tb->device));
+    uint64_t* dk = t->keys.get<uint64_t>(n);
+    uint32_t* dr = t->rows.get<uint32_t>(n);
+    KP_CUDA(cudaMemcpyAsync(dk, keys, (size_t)n * 8, cudaMemcpyHostToDevice, t->s));
+    tb->epoch++;  // new working set (store.cpp:187)
+    table_pull(tb, dk, n, dr, true, t->s);
+    const size_t rn = (size_t)n * tb->dim;
+    float* dw = t->w.get<float>(rn);
+    float* d1 = t->s1.get<float>(rn);
+    float* d2 = t->s2.get<float>(rn);
+    table_gather(tb, dr, n, dw, d1, tb->rule == 1 ? d2 : nullptr, t->s);
+    if (w) KP_CUDA(cudaMemcpyAsync(w, dw, rn * 4, cudaMemcpyDeviceToHost, t->s));
+    if (s1) KP_CUDA(cudaMemcpyAsync(s1, d1, rn * 4, cudaMemcpyDeviceToHost, t->s));
+    if (s2 && tb->rule == 1) KP_CUDA(cudaMemcpyAsync(s2, d2, rn * 4, cudaMemcpyDeviceToHost, t->s));
+    KP_CUDA(cudaStreamSynchronize(t->s));
+    table_check_full(tb, t->s);
+  });
+}
+
+int kp_store_push_updates(kp_table* t, const uint64_t* keys, const float* grads, uint32_t n,
+                          float lr, float beta1, float beta2, uint32_t* applied) {
+  if (applied) *applied = 0;
+  return guard([&] {
+    if (n == 0) return;
+    Table* tb = t->t;
+    KP_CUDA(cudaSetDevice(tb->device));
+    uint64_t* dk = t->keys.get<uint64_t>(n);
+    uint32_t* dr = t->rows.get<uint32_t>(n);
+    uint32_t* bad = t->scratch.get<uint32_t>(1);
+    float* dg = t->grads.get<float>((size_t)n * tb->dim);
+    KP_CUDA(cudaMemcpyAsync(dk, keys, (size_t)n * 8, cudaMemcpyHostToDevice, t->s));
+    KP_CUDA(cudaMemcpyAsync(dg, grads, (size_t)n * tb->dim * 4, cudaMemcpyHostToDevice, t->s));
+    table_lookup(tb, dk, n, dr, t->s);
+    table_ws_check(tb, dr, n, bad, t->s);
+    uint32_t h_bad = n;
+    KP_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, t->s));
+    KP_CUDA(cudaStreamSynchronize(t->s));
+    table_apply(tb, dr, dg, h_bad, lr, beta1, beta2, t->s);
+    KP_CUDA(cudaStreamSynchronize(t->s));
+    if (applied) *applied = h_bad;
+    KP_CHECK(h_bad == n, kErrStore,
+             "push_updates: key " + std::to_string(keys[h_bad]) + " not in the current working set");
+  });
+}
+
+int kp_store_lookup(kp_table* t, uint64_t key, float* w, float* s1, float* s2) {
+  return guard([&] {
+    Table* tb = t->t;
+    KP_CUDA(cudaSetDevice(tb->device));
+    uint64_t* dk = t->keys.get<uint64_t>(1);
+    uint32_t* dr = t->rows.get<uint32_t>(1);
+    uint32_t* bad = t->scratch.get<uint32_t>(1);
+    KP_CUDA(cudaMemcpyAsync(dk, &key, 8, cudaMemcpyHostToDevice, t->s));
+    table_lookup(tb, dk, 1, dr, t->s);
+    table_ws_check(tb, dr, 1, bad, t->s);
+    uint32_t h_bad = 1;
+    KP_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, t->s));
+    KP_CUDA(cudaStreamSynchronize(t->s));
+    KP_CHECK(h_bad == 1, kErrStore, "lookup: key " + std::to_string(key) + " not in the current working set");
+    float* dw = t->w.get<float>(tb->dim);
+    float* d1 = t->s1.get<float>(tb->dim);
+    float* d2 = t->s2.get<float>(tb->dim);
+    table_gather(tb, dr, 1, dw, d1, tb->rule == 1 ? d2 : nullptr, t->s);
+    if (w) KP_CUDA(cudaMemcpyAsync(w, dw, tb->dim * 4, cudaMemcpyDeviceToHost, t->s));
+    if (s1) KP_CUDA(cudaMemcpyAsync(s1, d1, tb->dim * 4, cudaMemcpyDeviceToHost, t->s));
+    if (s2 && tb->rule == 1) KP_CUDA(cudaMemcpyAsync(s2, d2, tb->dim * 4, cudaMemcpyDeviceToHost, t->s));
+    KP_CUDA(cudaStreamSynchronize(t->s));
+  });
+}
+
+int kp_table_export(kp_table* t, uint64_t* keys, float* w, float* s1, float* s2, uint64_t cap,
+                    uint64_t* n_out) {
+  return guard([&] {
+    Table* tb = t->t;
+    KP_CUDA(cudaSetDevice(tb->device));
+    const uint64_t n = table_size(tb, t->s);
+    *n_out = n;
+    if (!keys) return;
+    KP_CHECK(cap >= n, kErrGeneric, "table_export: output capacity too small");
+    if (n == 0) return;
+    uint64_t* dk = t->keys.get<uint64_t>(n);
+    uint32_t* dr = t->rows.get<uint32_t>(n);
+    auto* cnt = reinterpret_cast<unsigned long long*>(t->scratch.get<uint64_t>(1));
+    table_export(tb, dk, dr, cnt, t->s);
+    std::vector<uint64_t> hk(n);
+    std::vector<uint32_t> hr(n);
+    KP_CUDA(cudaMemcpyAsync(hk.data(), dk, n * 8, cudaMemcpyDeviceToHost, t->s));
+    KP_CUDA(cudaMemcpyAsync(hr.data(), dr, n * 4, cudaMemcpyDeviceToHost, t->s));
+    KP_CUDA(cudaStreamSynchronize(t->s));
+    std::vector<uint64_t> order(n);
+    for (uint64_t i = 0; i < n; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { return hk[a] < hk[b]; });
+    std::vector<uint32_t> sr(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      keys[i] = hk[order[i]];
+      sr[i] = hr[order[i]];
+    }
+    KP_CUDA(cudaMemcpyAsync(dr, sr.data(), n * 4, cudaMemcpyHostToDevice, t->s));
+    const size_t rn = (size_t)n * tb->dim;
+    float* dw = t->w.get<float>(rn);
+    float* d1 = t->s1.get<float>(rn);
+    float* d2 = t->s2.get<float>(rn);
+    table_gather(tb, dr, (uint32_t)n, dw, d1, tb->rule == 1 ? d2 : nullptr, t->s);
+    if (w) KP_CUDA(cudaMemcpyAsync(w, dw, rn * 4, cudaMemcpyDeviceToHost, t->s));
+    if (s1) KP_CUDA(cudaMemcpyAsync(s1, d1, rn * 4, cudaMemcpyDeviceToHost, t->s));
+    if (s2 && tb->rule == 1) KP_CUDA(cudaMemcpyAsync(s2, d2, rn * 4, cudaMemcpyDeviceToHost, t->s));
+    KP_CUDA(cudaStreamSynchronize(t->s));
+  });
+}
+
+// ---- dedup / shard ----
+int kp_dedup(const uint64_t* d_keys, uint32_t n, uint64_t* d_unique, uint32_t* d_inverse,
+             uint32_t* d_seg, uint32_t* n_unique, kp_stream s) {
+  return guard([&] {
+    static thread_local DedupWs ws;
+    dedup(d_keys, n, ws, st(s));
+    const uint32_t U = ws.n_unique;
+    *n_unique = U;
+    if (U) KP_CUDA(cudaMemcpyAsync(d_unique, ws.d_unique, (size_t)U * 8, cudaMemcpyDeviceToDevice, st(s)));
+    if (n && d_inverse)
+      KP_CUDA(cudaMemcpyAsync(d_inverse, ws.d_inverse, (size_t)n * 4, cudaMemcpyDeviceToDevice, st(s)));
+    if (d_seg) KP_CUDA(cudaMemcpyAsync(d_seg, ws.d_seg, (size_t)(U + 1) * 4, cudaMemcpyDeviceToDevice, st(s)));
+    KP_CUDA(cudaStreamSynchronize(st(s)));
+  });
+}
+int kp_shard(const uint64_t* d_unique, uint32_t n, uint32_t G, uint32_t* d_perm, uint32_t* d_pos,
+             uint64_t* counts, kp_stream s) {
+  return guard([&] {
+    static thread_local ShardWs ws;
+    shard(d_unique, n, G, d_perm, d_pos, counts, ws, st(s));
+  });
+}
+
+// ---- dense ----
+int kp_dense_local_step(float* d_x, float* d_m, float* d_v, const float* d_vbar, const float* d_g,
+                        uint64_t D, float alpha, float beta1, float beta2, kp_stream s) {
+  return guard([&] { dense_local_step(d_x, d_m, d_v, d_vbar, d_g, D, {alpha, beta1, beta2}, st(s)); });
+}
+int kp_dense_moments(float* d_m, float* d_v, const float* d_g, uint64_t D, float beta1, float beta2,
+                     kp_stream s) {
+  return guard([&] { dense_moments(d_m, d_v, d_g, D, {0.f, beta1, beta2}, st(s)); });
+}
+int kp_centered_mean(const float* d_vecs, uint64_t stride, uint32_t n, uint64_t D, float* d_out,
+                     kp_stream s) {
+  return guard([&] {
+    KP_CHECK(n >= 1, kErrGeneric, "global_merge: empty worker list");
+    centered_mean(d_vecs, stride, n, D, d_out, st(s));
+  });
+}
+int kp_kstep_merge(kp_comm* comm, float* d_x, float* d_m, float* d_v, float* d_vbar, uint32_t W,
+                   uint64_t D, float alpha, int reset_local_v, kp_stream s) {
+  return guard([&] {
+    KP_CHECK(W >= 1, kErrGeneric, "global_merge: empty worker list");
+    static thread_local MergeWs ws;
+    merge_states(comm, st(s), W, D, d_x, d_m, d_v, d_vbar, alpha, reset_local_v != 0, ws);
+    KP_CUDA(cudaStreamSynchronize(st(s)));
+  });
+}
+
+// ---- comm ----
+int kp_comm_unique_id(uint8_t id[128]) {
+  return guard([&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId u;
+    KP_NCCL(ncclGetUniqueId(&u));
+    std::memcpy(id, &u, 128);
+  });
+}
+int kp_comm_init(const uint8_t id[128], int rank, int world, int device, kp_comm** out) {
+  return guard([&] {
+    KP_CUDA(cudaSetDevice(device));
+    auto c = std::make_unique<kp_comm>();
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    KP_NCCL(ncclCommInitRank(&c->nc, world, u, rank));
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    *out = c.release();
+  });
+}
+int kp_comm_destroy(kp_comm* c) {
+  return guard([&] {
+    if (!c) return;
+    if (c->nc) ncclCommDestroy(c->nc);
+    delete c;
+  });
+}
+int kp_comm_rank(kp_comm* c, int* rank, int* world) {
+  return guard([&] {
+    *rank = c->rank;
+    *world = c->world;
+  });
+}
+
+// ---- trainer ----
+int kp_trainer_create(const kp_trainer_config* cfg, kp_comm* comm, int device, kp_trainer** out) {
+  return guard([&] {
+    const kp_trainer_config& c = *cfg;
+    KP_CHECK(c.n_workers >= 1 && c.local_workers >= 1, kErrConfig, "workers must be >= 1");
+    const int world = comm ? comm->world : 1;
+    KP_CHECK((uint64_t)c.local_workers * world == c.n_workers, kErrConfig,
+             "n_workers must equal world_size * local_workers");
+    KP_CHECK(c.minibatch_size >= 1, kErrConfig, "minibatch_size must be >= 1");
+    KP_CHECK(c.alpha > 0, kErrConfig, "adam: alpha must be > 0");
+    KP_CHECK(c.beta1 >= 0 && c.beta1 < 1, kErrConfig, "adam: beta1 must be in [0,1)");
+    KP_CHECK(c.beta2 >= 0 && c.beta2 < 1, kErrConfig, "adam: beta2 must be in [0,1)");
+    KP_CHECK(c.epsilon > 0, kErrConfig, "adam: epsilon must be > 0");
+    KP_CHECK(c.k >= 1, kErrConfig, "adam: k must be >= 1");
+    KP_CHECK(c.embedding_dim >= 1, kErrConfig, "model: embedding_dim must be >= 1");
+    KP_CHECK(c.n_slots >= 1 && c.n_slots <= 65535, kErrConfig, "n_slots must be in [1, 65535]");
+    KP_CHECK(c.n_hidden <= 8, kErrConfig, "at most 8 hidden layers");
+    for (uint32_t i = 0; i < c.n_hidden; ++i)
+      KP_CHECK(c.hidden[i] >= 1, kErrConfig, "model: hidden widths must be >= 1");
+    KP_CHECK(c.table_capacity >= 1, kErrConfig, "table_capacity must be >= 1");
+    KP_CUDA(cudaSetDevice(device));
+    auto tr = std::make_unique<kp_trainer>();
+    tr->cfg = c;
+    tr->device = device;
+    tr->comm = comm;
+    tr->world = world;
+    tr->rank = comm ? comm->rank : 0;
+    tr->W = c.local_workers;
+    tr->N = c.n_workers;
+    tr->S = c.n_slots;
+    tr->e = c.embedding_dim;
+    KP_CUDA(cudaStreamCreateWithFlags(&tr->s, cudaStreamNonBlocking));
+    // model shape, flat layout per layer W then bias (model.cpp:55-66)
+    MlpShape& m = tr->shape;
+    m.widths[0] = c.n_slots * c.embedding_dim;
+    for (uint32_t i = 0; i < c.n_hidden; ++i) m.widths[i + 1] = c.hidden[i];
+    m.widths[c.n_hidden + 1] = 1;
+    m.n_layers = c.n_hidden + 1;
+    m.activation = c.activation;
+    for (uint32_t l = 0; l < m.n_layers; ++l) {
+      m.w_off[l] = m.D;
+      m.D += (uint64_t)m.widths[l] * m.widths[l + 1];
+      m.b_off[l] = m.D;
+      m.D += m.widths[l + 1];
+    }
+    tr->D = m.D;
+    const uint64_t D = m.D, W = tr->W;
+    std::vector<double> x0(D);
+    init_dense_host(c.seed, D, x0.data());
+    std::vector<float> hx(D), hv(D, (float)c.epsilon);
+    for (uint64_t j = 0; j < D; ++j) hx[j] = (float)x0[j];
+    KP_CUDA(cudaMalloc(&tr->x, W * D * 4));
+    KP_CUDA(cudaMalloc(&tr->m, W * D * 4));
+    KP_CUDA(cudaMalloc(&tr->v, W * D * 4));
+    KP_CUDA(cudaMalloc(&tr->vbar, W * D * 4));
+    KP_CUDA(cudaMalloc(&tr->g, W * D * 4));
+    KP_CUDA(cudaMemset(tr->m, 0, W * D * 4));
+    for (uint64_t l = 0; l < W; ++l) {
+      KP_CUDA(cudaMemcpy(tr->x + l * D, hx.data(), D * 4, cudaMemcpyHostToDevice));
+      KP_CUDA(cudaMemcpy(tr->v + l * D, hv.data(), D * 4, cudaMemcpyHostToDevice));
+      KP_CUDA(cudaMemcpy(tr->vbar + l * D, hv.data(), D * 4, cudaMemcpyHostToDevice));
+    }
+    const int rule = c.sparse_rule;
+    tr->tab.t = table_create(device, c.table_capacity, c.embedding_dim, rule, 0.f,
+                             rule == 0 ? 1e-6f : 0.f, rule == 0 ? 0.f : (float)c.sparse_eps);
+    tr->tab.s = nullptr;
+    tr->check.get<uint32_t>(1);
+    *out = tr.release();
+  });
+}
+
+int kp_trainer_destroy(kp_trainer* tr) {
+  return guard([&] {
+    if (!tr) return;
+    cudaSetDevice(tr->device);
+    delete tr;
+  });
+}
+
+int kp_trainer_train_batch(kp_trainer* tr, const uint32_t* offs, const uint64_t* keys,
+                           const uint16_t* slots, const int32_t* labels, uint32_t n,
+                           uint64_t global_n, uint64_t global_first, int predict_first,
+                           float* preds, kp_batch_result* out) {
+  return guard([&] {
+    KP_CUDA(cudaSetDevice(tr->device));
+    const uint32_t O = offs[n];
+    uint32_t* d_offs = tr->in_offs.get<uint32_t>(n + 1);
+    uint64_t* d_keys = tr->in_keys.get<uint64_t>(std::max<uint32_t>(O, 1));
+    uint16_t* d_slots = slots ? tr->in_slots.get<uint16_t>(std::max<uint32_t>(O, 1)) : nullptr;
+    int32_t* d_labels = tr->in_labels.get<int32_t>(std::max<uint32_t>(n, 1));
+    KP_CUDA(cudaMemcpyAsync(d_offs, offs, (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, tr->s));
+    KP_CUDA(cudaMemcpyAsync(d_keys, keys, (size_t)O * 8, cudaMemcpyHostToDevice, tr->s));
+    if (slots) KP_CUDA(cudaMemcpyAsync(d_slots, slots, (size_t)O * 2, cudaMemcpyHostToDevice, tr->s));
+    KP_CUDA(cudaMemcpyAsync(d_labels, labels, (size_t)n * 4, cudaMemcpyHostToDevice, tr->s));
+    train_batch_impl(tr, offs, d_offs, d_keys, d_slots, d_labels, n, global_n, global_first,
+                     predict_first != 0, preds, out);
+  });
+}
+
+int kp_trainer_train_batch_device(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_offs,
+                                  const uint64_t* d_keys, const uint16_t* d_slots,
+                                  const int32_t* d_labels, uint32_t n, uint64_t global_n,
+                                  uint64_t global_first, int predict_first, float* preds,
+                                  kp_batch_result* out) {
+  return guard([&] {
+    KP_CUDA(cudaSetDevice(tr->device));
+    train_batch_impl(tr, h_offs, d_offs, d_keys, d_slots, d_labels, n, global_n, global_first,
+                     predict_first != 0, preds, out);
+  });
+}
+
+int kp_trainer_dense_dim(kp_trainer* tr, uint64_t* D) {
+  return guard([&] { *D = tr->D; });
+}
+
+int kp_trainer_worker_state(kp_trainer* tr, uint32_t l, float* x, float* m, float* v, float* vbar) {
+  return guard([&] {
+    KP_CHECK(l < tr->W, kErrGeneric, "worker index out of range");
+    KP_CUDA(cudaSetDevice(tr->device));
+    const uint64_t D = tr->D;
+    if (x) KP_CUDA(cudaMemcpyAsync(x, tr->x + l * D, D * 4, cudaMemcpyDeviceToHost, tr->s));
+    if (m) KP_CUDA(cudaMemcpyAsync(m, tr->m + l * D, D * 4, cudaMemcpyDeviceToHost, tr->s));
+    if (v) KP_CUDA(cudaMemcpyAsync(v, tr->v + l * D, D * 4, cudaMemcpyDeviceToHost, tr->s));
+    if (vbar) KP_CUDA(cudaMemcpyAsync(vbar, tr->vbar + l * D, D * 4, cudaMemcpyDeviceToHost, tr->s));
+    KP_CUDA(cudaStreamSynchronize(tr->s));
+  });
+}
+
+int kp_trainer_set_worker_state(kp_trainer* tr, uint32_t l, const float* x, const float* m,
+                                const float* v, const float* vbar) {
+  return guard([&] {
+    KP_CHECK(l < tr->W, kErrGeneric, "worker index out of range");
+    KP_CUDA(cudaSetDevice(tr->device));
+    const uint64_t D = tr->D;
+    if (x) KP_CUDA(cudaMemcpyAsync(tr->x + l * D, x, D * 4, cudaMemcpyHostToDevice, tr->s));
+    if (m) KP_CUDA(cudaMemcpyAsync(tr->m + l * D, m, D * 4, cudaMemcpyHostToDevice, tr->s));
+    if (v) KP_CUDA(cudaMemcpyAsync(tr->v + l * D, v, D * 4, cudaMemcpyHostToDevice, tr->s));
+    if (vbar) KP_CUDA(cudaMemcpyAsync(tr->vbar + l * D, vbar, D * 4, cudaMemcpyHostToDevice, tr->s));
+    KP_CUDA(cudaStreamSynchronize(tr->s));
+  });
+}
+
+int kp_trainer_xbar(kp_trainer* tr, float* out) {
+  return guard([&] {
+    KP_CUDA(cudaSetDevice(tr->device));
+    float* xb = tr->xbar.get<float>(tr->D);
+    compute_xbar(tr, xb);
+    KP_CUDA(cudaMemcpyAsync(out, xb, tr->D * 4, cudaMemcpyDeviceToHost, tr->s));
+    KP_CUDA(cudaStreamSynchronize(tr->s));
+  });
+}
+
+int kp_trainer_table(kp_trainer* tr, kp_table** out) {
+  return guard([&] {
+    if (!tr->tab.s) KP_CUDA(cudaStreamCreateWithFlags(&tr->tab.s, cudaStreamNonBlocking));
+    *out = &tr->tab;
+  });
+}
+
+int kp_trainer_profile(kp_trainer* tr, int enable, double* stage_ms, uint64_t* counters) {
+  return guard([&] {
+    if (stage_ms)
+      for (int i = 0; i < 7; ++i) stage_ms[i] = tr->stage_ms[i];
+    if (counters) {
+      counters[0] = tr->prof_steps;
+      counters[1] = tr->prof_unique;
+      counters[2] = tr->prof_occ;
+      counters[3] = tr->prof_owner_unique;
+      counters[4] = tr->prof_recv;
+    }
+    for (double& d : tr->stage_ms) d = 0;
+    tr->prof_steps = tr->prof_unique = tr->prof_occ = tr->prof_owner_unique = tr->prof_recv = 0;
+    tr->prof = enable != 0;
+  });
+}
+
+int kp_trainer_stream(kp_trainer* tr, kp_stream* s) {
+  return guard([&] { *s = tr->s; });
+}
+
+}  // extern "C"

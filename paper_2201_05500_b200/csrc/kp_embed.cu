@@ -1,0 +1,373 @@
+// Embedding pull + per-slot sum pooling, and the backward segmented reduce
+// fused with the in-place sparse update (the "push").
+//
+// Reference: pooling in CtrModel::forward (proj/src/model.cpp:88-99) via the
+// per-occurrence EmbeddingSource lookup (proj/src/trainer.cpp:137-139); sparse
+// grads scattered per key in backward (proj/src/model.cpp:180-188), summed over
+// workers in ascending order (proj/src/trainer.cpp:180-186), scaled by 1/N
+// (:202-207) and pushed through AdaGrad (proj/src/store.cpp:191-208).
+//
+// Layout: a "bag" is one (instance, slot) pair; bag b = instance*S + slot and
+// pooled rows are [bags][e] = [B][S*e] (S=1: the reference's one pooled vector
+// per instance). Rows move as float4 (16 B per lane, e/4 lanes per row).
+// Sums run in occurrence order inside a lane, so pooling is bit-identical to
+// the fp32 oracle; the backward reduce is a fixed-order two-level segmented
+// sum (chunk partials combined in chunk order) -- deterministic, no float
+// atomics.
+#include "kp_table.cuh"
+
+namespace kp {
+namespace {
+
+unsigned grid_cap(uint64_t blocks) {
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148ull * 32) blocks = 148ull * 32;
+  return (unsigned)blocks;
+}
+
+__global__ void k_prepare_bags(const uint32_t* __restrict__ offs, uint32_t occ_base,
+                               const uint16_t* __restrict__ slots, uint32_t n_inst, uint32_t S,
+                               uint32_t* __restrict__ bag_offs, uint32_t* __restrict__ bag_of_occ,
+                               uint32_t* __restrict__ err) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = w0; i < n_inst; i += nw) {
+    const uint32_t o0 = offs[i] - occ_base, o1 = offs[i + 1] - occ_base;
+    if (S == 1) {
+      if (lane == 0) bag_offs[i] = o0;
+      for (uint32_t o = o0 + lane; o < o1; o += 32) bag_of_occ[o] = i;
+    } else {
+      if (o0 == o1) {
+        for (uint32_t s = lane; s < S; s += 32) bag_offs[(uint64_t)i * S + s] = o0;
+        continue;
+      }
+      for (uint32_t o = o0 + lane; o < o1; o += 32) {
+        const uint32_t s = slots[o];
+        const int prev = o == o0 ? -1 : (int)slots[o - 1];
+        if (s >= S || (int)s < prev) {
+          atomicMin(err, o);
+          continue;
+        }
+        for (int t = prev + 1; t <= (int)s; ++t) bag_offs[(uint64_t)i * S + t] = o;
+        if (o == o1 - 1)
+          for (uint32_t t = s + 1; t < S; ++t) bag_offs[(uint64_t)i * S + t] = o1;
+        bag_of_occ[o] = i * S + s;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) bag_offs[(uint64_t)n_inst * S] = offs[n_inst] - occ_base;
+}
+
+// ---- row access policies -------------------------------------------------
+// V4: lane gl of an LPG-lane group owns dims [4*gl, 4*gl+4); e == 4*LPG.
+// Scalar: LPG = 32, lane owns dims gl + 32*q (q < NV), masked by j < e.
+template <int LPG, int NV, bool V4>
+struct Row {
+  float v[V4 ? 4 : NV];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int q = 0; q < (V4 ? 4 : NV); ++q) v[q] = 0.f;
+  }
+  __device__ __forceinline__ void load(const float* __restrict__ p, int gl, uint32_t e) {
+    if (V4) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(p) + gl);
+      v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const uint32_t j = gl + 32 * q;
+        v[q] = j < e ? __ldg(p + j) : 0.f;
+      }
+    }
+  }
+  __device__ __forceinline__ void store(float* __restrict__ p, int gl, uint32_t e) const {
+    if (V4) {
+      reinterpret_cast<float4*>(p)[gl] = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const uint32_t j = gl + 32 * q;
+        if (j < e) p[j] = v[q];
+      }
+    }
+  }
+  __device__ __forceinline__ void add(const Row& o) {
+#pragma unroll
+    for (int q = 0; q < (V4 ? 4 : NV); ++q) v[q] = __fadd_rn(v[q], o.v[q]);
+  }
+  __device__ __forceinline__ void scale(float s) {
+#pragma unroll
+    for (int q = 0; q < (V4 ? 4 : NV); ++q) v[q] = __fmul_rn(v[q], s);
+  }
+  __device__ __forceinline__ int dim(int gl, int q) const { return V4 ? 4 * gl + q : gl + 32 * q; }
+};
+
+template <int LPG, int NV, bool V4>
+__global__ void __launch_bounds__(256) k_pool(const uint32_t* __restrict__ bag_offs, uint32_t n_bags,
+                                              const uint32_t* __restrict__ inverse,
+                                              const uint32_t* __restrict__ idx,
+                                              const float* __restrict__ src, uint32_t e, int mean,
+                                              float* __restrict__ pooled,
+                                              float* __restrict__ inv_count) {
+  const int gl = threadIdx.x % LPG;
+  const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
+  const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
+  for (uint64_t b = g0; b < n_bags; b += ng) {
+    const uint32_t o0 = bag_offs[b], o1 = bag_offs[b + 1];
+    Row<LPG, NV, V4> acc, r[4];
+    acc.zero();
+    uint32_t o = o0;
+    for (; o + 4 <= o1; o += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u].load(src + (uint64_t)idx[inverse[o + u]] * e, gl, e);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc.add(r[u]);  // occurrence order (model.cpp:93)
+    }
+    for (; o < o1; ++o) {
+      r[0].load(src + (uint64_t)idx[inverse[o]] * e, gl, e);
+      acc.add(r[0]);
+    }
+    if (mean) {
+      const float inv = o1 > o0 ? __fdiv_rn(1.f, (float)(o1 - o0)) : 1.f;  // model.cpp:95-97
+      if (o1 > o0) acc.scale(inv);
+      if (gl == 0) inv_count[b] = inv;
+    }
+    acc.store(pooled + b * e, gl, e);
+  }
+}
+
+// ---- segmented reduce + sparse rule ---------------------------------------
+struct SegArgs {
+  const uint32_t* seg;
+  uint32_t U;
+  const uint32_t* sorted_vals;
+  const uint32_t* bag_of_occ;
+  uint32_t n_pos;
+  const float* rows_src;
+  uint32_t e;
+  float inv_n;
+  const uint32_t* table_rows;
+  float* grad_out;
+  const uint32_t* out_idx;
+  float* partials;
+  uint32_t CH;
+  int apply;
+  int rule;
+  float lr, b1, b2;
+};
+
+template <int LPG, int NV, bool V4>
+__device__ __forceinline__ void finalize(const SegArgs& a, const TView& t, uint32_t u,
+                                         Row<LPG, NV, V4>& g, int gl) {
+  g.scale(a.inv_n);  // trainer.cpp:204-206 (x 1/N)
+  if (!a.apply) {
+    g.store(a.grad_out + (uint64_t)(a.out_idx ? a.out_idx[u] : u) * a.e, gl, a.e);
+    return;
+  }
+  const uint64_t o = (uint64_t)a.table_rows[u] * a.e;
+#pragma unroll
+  for (int q = 0; q < (V4 ? 4 : NV); ++q) {
+    const int j = g.dim(gl, q);
+    if (j >= (int)a.e) continue;
+    if (a.rule == 0) {
+      float w = t.w[o + j], acc = t.s1[o + j];
+      adagrad1(w, acc, g.v[q], a.lr);
+      t.w[o + j] = w;
+      t.s1[o + j] = acc;
+    } else {
+      float w = t.w[o + j], m = t.s1[o + j], v = t.s2[o + j];
+      adam1(w, m, v, g.v[q], a.lr, a.b1, a.b2);
+      t.w[o + j] = w;
+      t.s1[o + j] = m;
+      t.s2[o + j] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t src_row(const SegArgs& a, uint32_t p) {
+  const uint32_t occ = a.sorted_vals[p];
+  return a.bag_of_occ ? a.bag_of_occ[occ] : occ;
+}
+
+template <int LPG, int NV, bool V4>
+__device__ __forceinline__ void sum_range(const SegArgs& a, uint32_t p, uint32_t q,
+                                          Row<LPG, NV, V4>& acc, int gl) {
+  Row<LPG, NV, V4> r[4];
+  for (; p + 4 <= q; p += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u].load(a.rows_src + (uint64_t)src_row(a, p + u) * a.e, gl, a.e);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc.add(r[u]);
+  }
+  for (; p < q; ++p) {
+    r[0].load(a.rows_src + (uint64_t)src_row(a, p) * a.e, gl, a.e);
+    acc.add(r[0]);
+  }
+}
+
+// Phase 1: one group per chunk of CH sorted positions.
+template <int LPG, int NV, bool V4>
+__global__ void __launch_bounds__(256) k_seg_chunks(SegArgs a, TView t) {
+  const int gl = threadIdx.x % LPG;
+  const uint32_t nchunks = (a.n_pos + a.CH - 1) / a.CH;
+  const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
+  const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
+  const uint32_t pw = (uint32_t)(a.e * (V4 ? 1 : 1));
+  (void)pw;
+  for (uint64_t c = g0; c < nchunks; c += ng) {
+    const uint32_t p0 = (uint32_t)c * a.CH, p1 = min(a.n_pos, p0 + a.CH);
+    // largest u with seg[u] <= p0
+    uint32_t lo = 0, hi = a.U;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (a.seg[mid] <= p0) lo = mid; else hi = mid;
+    }
+    uint32_t u = lo;
+    for (;;) {
+      const uint32_t s0 = a.seg[u], s1 = a.seg[u + 1];
+      Row<LPG, NV, V4> acc;
+      acc.zero();
+      sum_range(a, max(s0, p0), min(s1, p1), acc, gl);
+      const bool before = s0 < p0, after = s1 > p1;
+      if (!before && !after) {
+        finalize(a, t, u, acc, gl);
+      } else {
+        acc.store(a.partials + ((uint64_t)c * 2 + (before ? 0 : 1)) * a.e, gl, a.e);
+      }
+      if (s1 >= p1) break;
+      ++u;
+    }
+  }
+}
+
+// Phase 2: segments spanning chunks: first chunk's tail partial, then the
+// head partials of the following chunks, in chunk order.
+template <int LPG, int NV, bool V4>
+__global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t) {
+  const int gl = threadIdx.x % LPG;
+  const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
+  const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
+  for (uint64_t u = g0; u < a.U; u += ng) {
+    const uint32_t s0 = a.seg[u], s1 = a.seg[u + 1];
+    const uint32_t c0 = s0 / a.CH, c1 = (s1 - 1) / a.CH;
+    if (c0 == c1) continue;
+    Row<LPG, NV, V4> acc, r;
+    acc.load(a.partials + ((uint64_t)c0 * 2 + 1) * a.e, gl, a.e);
+    for (uint32_t c = c0 + 1; c <= c1; ++c) {
+      r.load(a.partials + (uint64_t)c * 2 * a.e, gl, a.e);
+      acc.add(r);
+    }
+    finalize(a, t, (uint32_t)u, acc, gl);
+  }
+}
+
+template <int LPG, int NV, bool V4>
+void launch_seg(const SegArgs& a, const TView& t, cudaStream_t s) {
+  const uint32_t nchunks = (a.n_pos + a.CH - 1) / a.CH;
+  k_seg_chunks<LPG, NV, V4><<<grid_cap(((uint64_t)nchunks * LPG + 255) / 256), 256, 0, s>>>(a, t); ::kp::count_launch();
+  k_seg_fix<LPG, NV, V4><<<grid_cap(((uint64_t)a.U * LPG + 255) / 256), 256, 0, s>>>(a, t); ::kp::count_launch();
+}
+
+template <int LPG, int NV, bool V4>
+void launch_pool(const uint32_t* bag_offs, uint32_t n_bags, const uint32_t* inverse,
+                 const uint32_t* idx, const float* src, uint32_t e, bool mean, float* pooled,
+                 float* inv_count, cudaStream_t s) {
+  k_pool<LPG, NV, V4><<<grid_cap(((uint64_t)n_bags * LPG + 255) / 256), 256, 0, s>>>(
+      bag_offs, n_bags, inverse, idx, src, e, mean ? 1 : 0, pooled, inv_count); ::kp::count_launch();
+}
+
+// Dispatch on the embedding width: float4 groups for e in {4,8,...,128},
+// 32-lane scalar groups otherwise (e <= 256).
+template <template <int, int, bool> class F, class... Args>
+void dispatch_e(uint32_t e, Args&&... args) {
+  switch (e) {
+    case 4: F<1, 4, true>::run(args...); return;
+    case 8: F<2, 4, true>::run(args...); return;
+    case 16: F<4, 4, true>::run(args...); return;
+    case 32: F<8, 4, true>::run(args...); return;
+    case 64: F<16, 4, true>::run(args...); return;
+    case 128: F<32, 4, true>::run(args...); return;
+    default: break;
+  }
+  KP_CHECK(e <= 256, kErrConfig, "embedding_dim > 256 not supported");
+  if (e <= 32) F<32, 1, false>::run(args...);
+  else if (e <= 64) F<32, 2, false>::run(args...);
+  else if (e <= 128) F<32, 4, false>::run(args...);
+  else F<32, 8, false>::run(args...);
+}
+
+template <int LPG, int NV, bool V4>
+struct PoolF {
+  template <class... A>
+  static void run(A... a) { launch_pool<LPG, NV, V4>(a...); }
+};
+template <int LPG, int NV, bool V4>
+struct SegF {
+  static void run(const SegArgs& a, const TView& t, cudaStream_t s) { launch_seg<LPG, NV, V4>(a, t, s); }
+};
+
+__global__ void k_gather_rows(const float* __restrict__ src, const uint32_t* __restrict__ idx,
+                              uint32_t n, uint32_t e, float* __restrict__ out) {
+  const uint64_t total = (uint64_t)n * e;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = q / e, j = q % e;
+    out[q] = src[(uint64_t)idx[i] * e + j];
+  }
+}
+
+}  // namespace
+
+void prepare_bags(const uint32_t* d_offs, uint32_t occ_base, const uint16_t* d_slots,
+                  uint32_t n_inst, uint32_t S, uint32_t* d_bag_offs, uint32_t* d_bag_of_occ,
+                  uint32_t* d_err, cudaStream_t s) {
+  k_prepare_bags<<<grid_cap(((uint64_t)n_inst * 32 + 255) / 256), 256, 0, s>>>(
+      d_offs, occ_base, d_slots, n_inst, S, d_bag_offs, d_bag_of_occ, d_err); ::kp::count_launch();
+}
+
+void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_inverse,
+          const uint32_t* d_idx, const float* d_src, uint32_t e, bool mean, float* d_pooled,
+          float* d_inv_count, cudaStream_t s) {
+  if (n_bags == 0) return;
+  dispatch_e<PoolF>(e, d_bag_offs, n_bags, d_inverse, d_idx, d_src, e, mean, d_pooled, d_inv_count, s);
+}
+
+void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* d_sorted_vals,
+                      const uint32_t* d_bag_of_occ, uint32_t n_pos, const float* d_rows_src,
+                      uint32_t e, float inv_n, Table* t, const uint32_t* d_table_rows,
+                      const SparseRule& r, float* d_grad_out, const uint32_t* d_out_idx,
+                      SegWs& ws, cudaStream_t s) {
+  if (n_unique == 0 || n_pos == 0) return;
+  SegArgs a;
+  a.seg = d_seg;
+  a.U = n_unique;
+  a.sorted_vals = d_sorted_vals;
+  a.bag_of_occ = d_bag_of_occ;
+  a.n_pos = n_pos;
+  a.rows_src = d_rows_src;
+  a.e = e;
+  a.inv_n = inv_n;
+  a.table_rows = d_table_rows;
+  a.grad_out = d_grad_out;
+  a.out_idx = d_out_idx;
+  a.CH = 128;
+  const uint32_t nchunks = (n_pos + a.CH - 1) / a.CH;
+  a.partials = ws.partials.get<float>((size_t)nchunks * 2 * e);
+  a.apply = t != nullptr;
+  a.rule = r.rule;
+  a.lr = r.lr;
+  a.b1 = r.beta1;
+  a.b2 = r.beta2;
+  TView tv{};
+  if (t) tv = view(t);
+  dispatch_e<SegF>(e, a, tv, s);
+}
+
+void gather_rows(const float* d_src, const uint32_t* d_idx, uint32_t n, uint32_t e, float* d_out,
+                 cudaStream_t s) {
+  if (n == 0) return;
+  k_gather_rows<<<grid_cap(((uint64_t)n * e + 255) / 256), 256, 0, s>>>(d_src, d_idx, n, e, d_out); ::kp::count_launch();
+}
+
+}  // namespace kp

@@ -1,0 +1,151 @@
+// Internal (C++) interfaces between the kernel files; the C ABI in
+// include/kpsim_b200.h is built on these.
+#pragma once
+#include "kp_common.cuh"
+
+namespace kp {
+
+// ------------------------------------------------------------- dedup ----
+// Workspace for one dedup: sorted (key, occurrence) pairs, unique keys,
+// inverse index and segment starts. All device memory, grown on demand.
+struct DedupWs {
+  DevBuf keys_a, keys_b, vals_a, vals_b;  // radix ping-pong
+  DevBuf counts, totals, minmax, bcount, scalars;
+  DevBuf unique, inverse, seg;
+  // results of the last run (device pointers into the buffers above)
+  const uint64_t* sorted_keys = nullptr;
+  const uint32_t* sorted_vals = nullptr;  // occurrence index per sorted position
+  uint64_t* d_unique = nullptr;           // [U] ascending
+  uint32_t* d_inverse = nullptr;          // [n] occurrence -> unique index
+  uint32_t* d_seg = nullptr;              // [U+1] segment starts in sorted order
+  uint32_t* d_nunique = nullptr;          // device scalar U
+  uint32_t n = 0, n_unique = 0;
+};
+
+// Radix sort (stable) of (key, occurrence index) + unique + inverse + segment
+// starts. Writes U to ws.n_unique (host; one sync) and ws.d_nunique.
+void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s);
+
+// Stable bucket of ascending unique keys by owner = key % G.
+// perm[i] = unique index placed at bucket slot i; pos[u] = slot of unique u;
+// counts[G] on host.
+struct ShardWs {
+  DevBuf bcount, scalars;
+};
+void shard(const uint64_t* d_unique, uint32_t n, uint32_t G, uint32_t* d_perm,
+           uint32_t* d_pos, uint64_t* h_counts, ShardWs& ws, cudaStream_t s);
+
+// ------------------------------------------------------------- table ----
+struct Table {
+  int device = 0;
+  uint64_t capacity = 0;  // max rows
+  uint64_t nslots = 0;    // power of two, 16 slots per 128 B bucket
+  uint32_t dim = 0;
+  int rule = 0;  // 0 adagrad {w, acc}; 1 adam {w, m, v}
+  float init_w = 0.f, init_s1 = 0.f, init_s2 = 0.f;
+  uint64_t* d_keys = nullptr;
+  uint32_t* d_rows = nullptr;
+  uint64_t* d_row_key = nullptr;
+  float* d_w = nullptr;
+  float* d_s1 = nullptr;
+  float* d_s2 = nullptr;
+  uint32_t* d_epoch = nullptr;    // working-set stamp per row (TieredStore API)
+  uint32_t* d_scalars = nullptr;  // [0]=rows used, [1]=row of key u64max, [2]=full flag, [3]=error idx
+  uint32_t epoch = 0;
+};
+Table* table_create(int device, uint64_t capacity, uint32_t dim, int rule, float init_w,
+                    float init_s1, float init_s2);
+void table_destroy(Table* t);
+// insert-if-absent; rows_out[i] = row of keys[i] (kNoRow if the table is full)
+void table_pull(Table* t, const uint64_t* d_keys, uint32_t n, uint32_t* d_rows_out,
+                bool stamp_epoch, cudaStream_t s);
+// lookup only; kNoRow when absent
+void table_lookup(const Table* t, const uint64_t* d_keys, uint32_t n, uint32_t* d_rows_out,
+                  cudaStream_t s);
+uint64_t table_size(const Table* t, cudaStream_t s);
+void table_check_full(const Table* t, cudaStream_t s);  // throws kErrTableFull
+void table_export(const Table* t, uint64_t* d_keys_out, uint32_t* d_rows_out,
+                  unsigned long long* d_cnt, cudaStream_t s);
+void table_ws_check(const Table* t, const uint32_t* d_rows, uint32_t n, uint32_t* d_first_bad,
+                    cudaStream_t s);
+void table_apply(Table* t, const uint32_t* d_rows, const float* d_grads, uint32_t n, float lr,
+                 float b1, float b2, cudaStream_t s);
+void table_set_rows(Table* t, const uint32_t* d_rows, uint32_t n, const float* d_w,
+                    const float* d_s1, const float* d_s2, cudaStream_t s);
+void table_gather(const Table* t, const uint32_t* d_rows, uint32_t n, float* d_w, float* d_s1,
+                  float* d_s2, cudaStream_t s);
+
+// ----------------------------------------------------------- embedding ---
+// bags: CSR over occurrences; bag b = instance*S + slot.
+void prepare_bags(const uint32_t* d_offs, uint32_t occ_base, const uint16_t* d_slots,
+                  uint32_t n_inst, uint32_t S, uint32_t* d_bag_offs, uint32_t* d_bag_of_occ,
+                  uint32_t* d_err, cudaStream_t s);
+// pooled[bag][e] = sum_{o in bag} src[idx[inverse[o]]][e]  (x 1/|bag| when mean)
+void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_inverse,
+          const uint32_t* d_idx, const float* d_src, uint32_t e, bool mean, float* d_pooled,
+          float* d_inv_count, cudaStream_t s);
+// Deterministic segmented reduce of coefficient-scaled upstream rows by
+// unique key, times inv_n, then the sparse rule applied in place to the row.
+struct SegWs {
+  DevBuf partials;
+};
+struct SparseRule {
+  int rule;  // 0 adagrad, 1 adam
+  float lr, beta1, beta2;
+};
+// Segments are [seg[u], seg[u+1]) of sorted positions p; the upstream row of
+// position p is rows_src[map(p)] with map(p) = bag_of_occ[sorted_vals[p]]
+// (bag_of_occ may be null: identity). Output: apply the rule to table row
+// table_rows[u] (fused push) when `t` is set, else store to grad_out[out_idx[u]].
+void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* d_sorted_vals,
+                      const uint32_t* d_bag_of_occ, uint32_t n_pos, const float* d_rows_src,
+                      uint32_t e, float inv_n, Table* t, const uint32_t* d_table_rows,
+                      const SparseRule& r, float* d_grad_out, const uint32_t* d_out_idx,
+                      SegWs& ws, cudaStream_t s);
+void gather_rows(const float* d_src, const uint32_t* d_idx, uint32_t n, uint32_t e, float* d_out,
+                 cudaStream_t s);
+
+// ---------------------------------------------------------------- MLP ----
+struct MlpShape {
+  uint32_t n_layers = 0;          // hidden + 1
+  uint32_t widths[10] = {0};      // in, hidden..., 1
+  uint64_t w_off[9] = {0}, b_off[9] = {0};
+  uint64_t D = 0;
+  int activation = 0;             // 0 relu, 1 tanh
+};
+struct MlpWs {
+  DevBuf act[9];    // per hidden layer activations [B][width]
+  DevBuf dz[2];     // ping-pong upstream grads
+  DevBuf logits, delta, partials, lossp;
+};
+// Forward over B instances (input [B][in]); writes preds (sigmoid) and
+// logits; keeps activations in ws for backward.
+void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_t B,
+                 float* d_preds, MlpWs& ws, cudaStream_t s);
+// Backward: d_grad[D] (overwritten), d_dinput[B][in] scaled by d_coeff
+// (per bag; null = 1), loss sum (f64, device) accumulated into d_loss.
+void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32_t B,
+                  const float* d_preds, const int32_t* d_labels, float* d_grad, float* d_dinput, const float* d_coeff,
+                  uint32_t S, uint32_t e, double* d_loss_sum, MlpWs& ws, cudaStream_t s);
+
+// -------------------------------------------------------------- dense ----
+struct AdamParams {
+  float alpha, beta1, beta2;
+};
+void dense_local_step(float* x, float* m, float* v, const float* vbar, const float* g, uint64_t D,
+                      const AdamParams& h, cudaStream_t s);
+void dense_moments(float* m, float* v, const float* g, uint64_t D, const AdamParams& h,
+                   cudaStream_t s);
+// out[j] = centered mean over n vectors at vecs + i*stride (ascending i)
+void centered_mean(const float* vecs, uint64_t stride, uint32_t n, uint64_t D, float* out,
+                   cudaStream_t s);
+void merge_terms(const float* x, const float* m, const float* vbar, uint64_t D, float alpha,
+                 float* out, cudaStream_t s);
+void dense_check(const float* v, const float* vbar, const float* x, uint64_t D, uint32_t* d_flag,
+                 cudaStream_t s);
+
+// init_dense (proj/src/model.cpp:68-74): mt19937_64 + libstdc++ uniform(-0.05,0.05)
+void init_dense_host(uint64_t seed, uint64_t dim, double* out);
+uint64_t splitmix64_host(uint64_t x);
+
+}  // namespace kp

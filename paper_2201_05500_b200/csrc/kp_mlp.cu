@@ -1,0 +1,422 @@
+// Dense MLP forward/backward over pooled embeddings (fp32).
+//
+// Reference: CtrModel::forward/backward (proj/src/model.cpp:76-191); flat dense
+// layout per layer W(out x in, row-major) then bias (:55-66); hidden
+// activation relu/tanh, linear logit head, sigmoid, mean BCE (:34-38,126-135);
+// upstream (p - y)/n with n the worker's minibatch size (:153-155).
+//
+// Round-1 implementation: a tiled fp32 SIMT GEMM (128x128x8 tiles, 8x8 per
+// thread, register double buffering) with fused epilogues (bias+activation,
+// activation derivative, mean-pooling coefficient) and deterministic split-K
+// for the weight gradients; the out=1 head is a warp-per-instance GEMV fused
+// with sigmoid, loss and the upstream gradient. fp32 keeps the stated
+// tolerance against the reference; the tcgen05 (3xTF32) replacement is the
+// next step.
+#include "kp_internal.cuh"
+
+namespace kp {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 8, GT = 256;
+
+enum Epi : int { kStore = 0, kBiasAct = 1, kDAct = 2, kCoeff = 3 };
+
+struct EpiArgs {
+  int mode;
+  int act;             // 0 relu, 1 tanh
+  const float* bias;   // [N]           (kBiasAct)
+  const float* aux;    // [M][ldc]      (kDAct: activations of that layer)
+  const float* coeff;  // [M*S + n/e]   (kCoeff)
+  uint32_t S, e;
+};
+
+__device__ __forceinline__ float act_fwd(int act, float z) {
+  return act == 0 ? (z > 0.f ? z : 0.f) : tanhf(z);
+}
+// derivative from the layer OUTPUT y (relu: y>0 <=> z>0; tanh: 1-y^2), model.cpp:45-51
+__device__ __forceinline__ float act_bwd(int act, float y) {
+  return act == 0 ? (y > 0.f ? 1.f : 0.f) : __fsub_rn(1.f, __fmul_rn(y, y));
+}
+
+// C[m][n] (+ split offset) = sum_k A(m,k) * B(n,k)
+//   A(m,k) = A_K ? A[m*lda+k] : A[k*lda+m];  B(n,k) = B_K ? B[n*ldb+k] : B[k*ldb+n]
+template <bool A_K, bool B_K, bool VEC>
+__global__ void __launch_bounds__(GT) k_gemm(int M, int N, int K, const float* __restrict__ A,
+                                             int lda, const float* __restrict__ B, int ldb,
+                                             float* __restrict__ C, int ldc, int kps, EpiArgs ep) {
+  __shared__ __align__(16) float As[2][BK][BM + 4];
+  __shared__ __align__(16) float Bs[2][BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int kb = blockIdx.z * kps, ke = min(K, kb + kps);
+  if (blockIdx.z > 0) C += (size_t)blockIdx.z * M * ldc;
+
+  // loader coordinates (4 elements per thread per operand)
+  float ra[4], rb[4];
+  auto load_a = [&](int k0) {
+    if (A_K) {
+      const int m = tid >> 1, k = (tid & 1) * 4;
+      const int gm = m0 + m, gk = k0 + k;
+      if (VEC && gm < M && gk + 3 < ke) {
+        const float4 v = *reinterpret_cast<const float4*>(A + (size_t)gm * lda + gk);
+        ra[0] = v.x, ra[1] = v.y, ra[2] = v.z, ra[3] = v.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          ra[q] = (gm < M && gk + q < ke) ? A[(size_t)gm * lda + gk + q] : 0.f;
+      }
+    } else {
+      const int k = tid >> 5, m = (tid & 31) * 4;
+      const int gm = m0 + m, gk = k0 + k;
+      if (VEC && gk < ke && gm + 3 < M) {
+        const float4 v = *reinterpret_cast<const float4*>(A + (size_t)gk * lda + gm);
+        ra[0] = v.x, ra[1] = v.y, ra[2] = v.z, ra[3] = v.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          ra[q] = (gk < ke && gm + q < M) ? A[(size_t)gk * lda + gm + q] : 0.f;
+      }
+    }
+  };
+  auto load_b = [&](int k0) {
+    if (B_K) {
+      const int n = tid >> 1, k = (tid & 1) * 4;
+      const int gn = n0 + n, gk = k0 + k;
+      if (VEC && gn < N && gk + 3 < ke) {
+        const float4 v = *reinterpret_cast<const float4*>(B + (size_t)gn * ldb + gk);
+        rb[0] = v.x, rb[1] = v.y, rb[2] = v.z, rb[3] = v.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          rb[q] = (gn < N && gk + q < ke) ? B[(size_t)gn * ldb + gk + q] : 0.f;
+      }
+    } else {
+      const int k = tid >> 5, n = (tid & 31) * 4;
+      const int gn = n0 + n, gk = k0 + k;
+      if (VEC && gk < ke && gn + 3 < N) {
+        const float4 v = *reinterpret_cast<const float4*>(B + (size_t)gk * ldb + gn);
+        rb[0] = v.x, rb[1] = v.y, rb[2] = v.z, rb[3] = v.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          rb[q] = (gk < ke && gn + q < N) ? B[(size_t)gk * ldb + gn + q] : 0.f;
+      }
+    }
+  };
+  auto store_ab = [&](int buf) {
+    if (A_K) {
+      const int m = tid >> 1, k = (tid & 1) * 4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) As[buf][k + q][m] = ra[q];
+    } else {
+      const int k = tid >> 5, m = (tid & 31) * 4;
+      *reinterpret_cast<float4*>(&As[buf][k][m]) = make_float4(ra[0], ra[1], ra[2], ra[3]);
+    }
+    if (B_K) {
+      const int n = tid >> 1, k = (tid & 1) * 4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Bs[buf][k + q][n] = rb[q];
+    } else {
+      const int k = tid >> 5, n = (tid & 31) * 4;
+      *reinterpret_cast<float4*>(&Bs[buf][k][n]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
+    }
+  };
+
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  const int tx = tid & 15, ty = tid >> 4;
+  int buf = 0;
+  if (kb < ke) {
+    load_a(kb);
+    load_b(kb);
+    store_ab(0);
+  }
+  __syncthreads();
+  for (int k0 = kb; k0 < ke; k0 += BK) {
+    const bool more = k0 + BK < ke;
+    if (more) {
+      load_a(k0 + BK);
+      load_b(k0 + BK);
+    }
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      float a[8], b[8];
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][64 + tx * 4]);
+      a[0] = a0.x, a[1] = a0.y, a[2] = a0.z, a[3] = a0.w;
+      a[4] = a1.x, a[5] = a1.y, a[6] = a1.z, a[7] = a1.w;
+      b[0] = b0.x, b[1] = b0.y, b[2] = b0.z, b[3] = b0.w;
+      b[4] = b1.x, b[5] = b1.y, b[6] = b1.z, b[7] = b1.w;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (more) {
+      store_ab(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (n >= N) continue;
+      float v = acc[i][j];
+      if (ep.mode == kBiasAct) {
+        v = act_fwd(ep.act, __fadd_rn(v, ep.bias[n]));
+      } else if (ep.mode == kDAct) {
+        v = __fmul_rn(v, act_bwd(ep.act, ep.aux[(size_t)m * ldc + n]));
+      } else if (ep.mode == kCoeff) {
+        v = __fmul_rn(v, ep.coeff[(size_t)m * ep.S + n / ep.e]);
+      }
+      C[(size_t)m * ldc + n] = v;
+    }
+  }
+}
+
+template <bool A_K, bool B_K>
+int gemm(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
+          int splits, const EpiArgs& ep, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return 0;
+  splits = splits < 1 ? 1 : splits;
+  int kps = (K + splits - 1) / splits;
+  kps = (kps + BK - 1) / BK * BK;
+  splits = K > 0 ? (K + kps - 1) / kps : 1;
+  if (kps == 0) kps = BK;
+  dim3 grid(ceil_div(N, BN), ceil_div(M, BM), splits);
+  const bool vec = (lda % 4 == 0) && (ldb % 4 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(B) % 16 == 0);
+  if (vec)
+    k_gemm<A_K, B_K, true><<<grid, GT, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, kps, ep);
+  else
+    k_gemm<A_K, B_K, false><<<grid, GT, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, kps, ep);
+  ::kp::count_launch();
+  return splits;
+}
+
+// out[i] = sum_z part[z][i], z ascending (deterministic split-K reduce)
+__global__ void k_reduce_splits(const float* __restrict__ part, int splits, size_t n,
+                                float* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float v = part[i];
+    for (int z = 1; z < splits; ++z) v = __fadd_rn(v, part[(size_t)z * n + i]);
+    out[i] = v;
+  }
+}
+
+// column sums (optionally weighted): partial[c][n] = sum_{b in chunk c} w[b]*X[b][n]
+__global__ void k_colsum_part(const float* __restrict__ X, const float* __restrict__ w, int B,
+                              int N, int rows_per_chunk, float* __restrict__ part) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (n >= N) return;
+  const int b0 = c * rows_per_chunk, b1 = min(B, b0 + rows_per_chunk);
+  float acc = 0.f;
+  for (int b = b0; b < b1; ++b) {
+    const float x = X[(size_t)b * N + n];
+    acc = w ? fmaf(w[b], x, acc) : __fadd_rn(acc, x);
+  }
+  part[(size_t)c * N + n] = acc;
+}
+
+// Head (out = 1): logit = b + w . a ; pred = sigmoid (model.cpp:34-38,118-123)
+__global__ void k_head_fwd(const float* __restrict__ in, int B, int W, const float* __restrict__ w,
+                           const float* __restrict__ bias, float* __restrict__ logits,
+                           float* __restrict__ preds) {
+  const int lane = threadIdx.x & 31;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int b = wid; b < B; b += nw) {
+    const float* a = in + (size_t)b * W;
+    float s = 0.f;
+    for (int i = lane; i < W; i += 32) s = fmaf(w[i], a[i], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const float z = __fadd_rn(s, bias[0]);
+      float p;
+      if (z >= 0.f) {
+        p = __fdiv_rn(1.f, __fadd_rn(1.f, expf(-z)));
+      } else {
+        const float e = expf(z);
+        p = __fdiv_rn(e, __fadd_rn(1.f, e));
+      }
+      logits[b] = z;
+      preds[b] = p;
+    }
+  }
+}
+
+// delta = (p - y)/n; loss term softplus(z) - y z (model.cpp:126-135,153-155);
+// dprev[b][i] = (delta * w[i]) * act'(a[b][i])  or  * coeff  (layer-0 input)
+__global__ void k_head_bwd(const float* __restrict__ in, int B, int W, const float* __restrict__ w,
+                           const float* __restrict__ logits, const float* __restrict__ preds,
+                           const int32_t* __restrict__ labels, float nb,
+                           float* __restrict__ delta, float* __restrict__ dprev, int mode, int act,
+                           const float* __restrict__ coeff, uint32_t S, uint32_t e,
+                           double* __restrict__ loss_part) {
+  __shared__ double s_loss[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  double lsum = 0.0;
+  for (int b = wid; b < B; b += nw) {
+    const float y = (float)labels[b];
+    const float d = __fdiv_rn(__fsub_rn(preds[b], y), nb);
+    if (lane == 0) {
+      delta[b] = d;
+      const float z = logits[b];
+      const float sp = __fadd_rn(fmaxf(z, 0.f), log1pf(expf(-fabsf(z))));
+      lsum += (double)__fsub_rn(sp, __fmul_rn(y, z));
+    }
+    if (dprev) {
+      for (int i = lane; i < W; i += 32) {
+        float g = __fmul_rn(d, w[i]);
+        if (mode == kDAct) g = __fmul_rn(g, act_bwd(act, in[(size_t)b * W + i]));
+        else if (mode == kCoeff) g = __fmul_rn(g, coeff[(size_t)b * S + i / e]);
+        dprev[(size_t)b * W + i] = g;
+      }
+    }
+  }
+  if (lane == 0) s_loss[warp] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += s_loss[q];
+    loss_part[blockIdx.x] = t;
+  }
+}
+
+// loss_sum += (sum / n) * n  -- the reference's loss_sum += bwd.loss * mb.size
+__global__ void k_loss_finalize(const double* __restrict__ part, int nparts, int n,
+                                double* __restrict__ loss_sum) {
+  double t = 0.0;
+  for (int i = 0; i < nparts; ++i) t += part[i];
+  *loss_sum += (t / (double)n) * (double)n;
+}
+
+unsigned grid_cap(uint64_t blocks) {
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  return (unsigned)blocks;
+}
+
+// split-K count: enough CTAs to cover ~2 waves of 148 SMs
+int pick_splits(int M, int N, int K) {
+  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, BN));
+  int sp = (2 * 148 + tiles - 1) / tiles;
+  const int max_sp = (K + 255) / 256;  // >= 256 rows per split
+  if (sp > max_sp) sp = max_sp;
+  return sp < 1 ? 1 : sp;
+}
+
+}  // namespace
+
+void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_t B,
+                 float* d_preds, MlpWs& ws, cudaStream_t s) {
+  if (B == 0) return;
+  const float* in = d_in;
+  const uint32_t L = m.n_layers;
+  for (uint32_t l = 0; l + 1 < L; ++l) {
+    const int K = m.widths[l], N = m.widths[l + 1];
+    float* out = ws.act[l].get<float>((size_t)B * N);
+    EpiArgs ep{kBiasAct, m.activation, d_x + m.b_off[l], nullptr, nullptr, 1, 1};
+    gemm<true, true>(B, N, K, in, K, d_x + m.w_off[l], K, out, N, 1, ep, s);
+    in = out;
+  }
+  const int W = m.widths[L - 1];
+  float* logits = ws.logits.get<float>(B);
+  k_head_fwd<<<grid_cap(((uint64_t)B * 32 + 255) / 256), 256, 0, s>>>(
+      in, B, W, d_x + m.w_off[L - 1], d_x + m.b_off[L - 1], logits, d_preds); ::kp::count_launch();
+}
+
+namespace {
+void colsum(const float* X, const float* w, int B, int N, float* out, MlpWs& ws, cudaStream_t s) {
+  int chunks = (B + 511) / 512;
+  if (chunks > 64) chunks = 64;
+  if (chunks < 1) chunks = 1;
+  const int rpc = (B + chunks - 1) / chunks;
+  float* part = ws.partials.get<float>((size_t)chunks * N);
+  dim3 g(ceil_div(N, 128), chunks);
+  k_colsum_part<<<g, 128, 0, s>>>(X, w, B, N, rpc, part); ::kp::count_launch();
+  k_reduce_splits<<<grid_cap(ceil_div(N, 256)), 256, 0, s>>>(part, chunks, (size_t)N, out); ::kp::count_launch();
+}
+}  // namespace
+
+void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32_t B,
+                  const float* d_preds, const int32_t* d_labels, float* d_grad, float* d_dinput,
+                  const float* d_coeff, uint32_t S, uint32_t e, double* d_loss_sum, MlpWs& ws,
+                  cudaStream_t s) {
+  const uint32_t L = m.n_layers;
+  if (B == 0) {
+    KP_CUDA(cudaMemsetAsync(d_grad, 0, m.D * 4, s));
+    return;
+  }
+  auto layer_in = [&](uint32_t l) -> const float* {
+    return l == 0 ? d_in : static_cast<const float*>(ws.act[l - 1].p);
+  };
+  // ---- head (out = 1) ----
+  const int W = m.widths[L - 1];
+  float* delta = ws.delta.get<float>(B);
+  float* dprev = nullptr;
+  int mode = kStore;
+  if (L >= 2) {
+    dprev = ws.dz[0].get<float>((size_t)B * W);
+    mode = kDAct;
+  } else if (d_dinput) {
+    dprev = d_dinput;
+    mode = d_coeff ? kCoeff : kStore;
+  }
+  const unsigned hb = grid_cap(((uint64_t)B * 32 + 255) / 256);
+  double* lossp = ws.lossp.get<double>(hb);
+  k_head_bwd<<<hb, 256, 0, s>>>(layer_in(L - 1), B, W, d_x + m.w_off[L - 1],
+                                 static_cast<const float*>(ws.logits.p), d_preds, d_labels,
+                                 (float)B, delta, dprev, mode, m.activation, d_coeff, S, e, lossp); ::kp::count_launch();
+  k_loss_finalize<<<1, 1, 0, s>>>(lossp, hb, B, d_loss_sum); ::kp::count_launch();
+  colsum(layer_in(L - 1), delta, B, W, d_grad + m.w_off[L - 1], ws, s);
+  colsum(delta, nullptr, B, 1, d_grad + m.b_off[L - 1], ws, s);
+  // ---- hidden layers, top down ----
+  int cur = 0;
+  for (int l = (int)L - 2; l >= 0; --l) {
+    const int N = m.widths[l + 1], K = m.widths[l];
+    float* dZ = static_cast<float*>(ws.dz[cur].p);
+    const float* in = layer_in(l);
+    // dW_l[o][i] = sum_b dZ[b][o] in[b][i]   (deterministic split-K)
+    const int sp = pick_splits(N, K, B);
+    EpiArgs plain{kStore, 0, nullptr, nullptr, nullptr, 1, 1};
+    if (sp == 1) {
+      gemm<false, false>(N, K, B, dZ, N, in, K, d_grad + m.w_off[l], K, 1, plain, s);
+    } else {
+      float* part = ws.partials.get<float>((size_t)sp * N * K);
+      const int got = gemm<false, false>(N, K, B, dZ, N, in, K, part, K, sp, plain, s);
+      k_reduce_splits<<<grid_cap(ceil_div((uint64_t)N * K, 256)), 256, 0, s>>>(
+          part, got, (size_t)N * K, d_grad + m.w_off[l]); ::kp::count_launch();
+    }
+    colsum(dZ, nullptr, B, N, d_grad + m.b_off[l], ws, s);
+    // upstream for the layer below: dX = dZ . W_l, then act' or pooling coeff
+    if (l > 0) {
+      float* next = ws.dz[cur ^ 1].get<float>((size_t)B * K);
+      EpiArgs ep{kDAct, m.activation, nullptr, static_cast<const float*>(ws.act[l - 1].p), nullptr, 1, 1};
+      gemm<true, false>(B, K, N, dZ, N, d_x + m.w_off[l], K, next, K, 1, ep, s);
+      cur ^= 1;
+    } else if (d_dinput) {
+      EpiArgs ep{d_coeff ? kCoeff : kStore, 0, nullptr, nullptr, d_coeff, S, e};
+      gemm<true, false>(B, K, N, dZ, N, d_x + m.w_off[l], K, d_dinput, K, 1, ep, s);
+    }
+  }
+}
+
+}  // namespace kp

@@ -1,0 +1,404 @@
+// Key dedup for the working set: LSD radix sort of (key, occurrence) pairs,
+// then unique + inverse index + segment starts; and the key % G owner bucket.
+//
+// Replaces the reference's std::set working-set build
+// (proj/src/trainer.cpp:121-124) and the per-key owner map
+// (proj/src/trainer.cpp:83). Output order is ascending key -- bit-identical to
+// std::set iteration order.
+//
+// Design (HBM-bound integer work, no tensor cores):
+//  * only the bits where keys differ are sorted: digits of (key - min), so a
+//    100M key space costs 4 passes of 8 bits, not 8;
+//  * per pass: upsweep histogram (warp-aggregated smem atomics), per-digit
+//    scan, downsweep with a stable block rank (__match_any_sync) and a
+//    shared-memory staged scatter so global writes are digit-run coalesced;
+//  * tiles of 2048 pairs (256 threads x 8), grids are multiples of the SM
+//    count for every config that matters.
+#include "kp_internal.cuh"
+
+namespace kp {
+namespace {
+
+constexpr int ST = 256;              // threads per sort block
+constexpr int IPT = 8;               // items per thread
+constexpr int TILE = ST * IPT;       // 2048
+constexpr int RADIX = 256;
+constexpr int NW = ST / 32;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Block-wide exclusive scan of one value per thread (256 threads).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  uint32_t wpre = 0;
+  total = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const uint32_t t = s_warp[w];
+    if (w < warp) wpre += t;
+    total += t;
+  }
+  __syncthreads();
+  return wpre + x - v;
+}
+
+__global__ void k_minmax_init(unsigned long long* mm) {
+  mm[0] = ~0ull;
+  mm[1] = 0ull;
+}
+
+__global__ void k_minmax(const uint64_t* __restrict__ keys, uint32_t n, unsigned long long* mm) {
+  uint64_t lo = ~0ull, hi = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t a = __shfl_xor_sync(0xffffffffu, lo, o);
+    const uint64_t b = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[0], (unsigned long long)lo);
+    atomicMax(&mm[1], (unsigned long long)hi);
+  }
+}
+
+__global__ void __launch_bounds__(ST) k_upsweep(const uint64_t* __restrict__ keys, uint32_t n,
+                                                const unsigned long long* __restrict__ mm,
+                                                int shift, uint32_t* __restrict__ counts,
+                                                uint32_t nb) {
+  __shared__ uint32_t hist[RADIX];
+  hist[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t kmin = mm[0];
+  const uint32_t base = blockIdx.x * TILE;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const uint32_t idx = base + r * ST + threadIdx.x;
+    const uint32_t d = idx < n ? (uint32_t)((keys[idx] - kmin) >> shift) & 255u : RADIX;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (d < RADIX && lane == __ffs(peers) - 1) atomicAdd(&hist[d], __popc(peers));
+  }
+  __syncthreads();
+  counts[threadIdx.x * nb + blockIdx.x] = hist[threadIdx.x];
+}
+
+// rows of `counts` ([rows][nb]) scanned exclusive in place; totals[row].
+__global__ void __launch_bounds__(ST) k_scan_rows(uint32_t* __restrict__ counts, uint32_t nb,
+                                                  uint32_t* __restrict__ totals) {
+  __shared__ uint32_t s_warp[NW];
+  uint32_t* row = counts + (size_t)blockIdx.x * nb;
+  uint32_t running = 0;
+  for (uint32_t base = 0; base < nb; base += ST * 4) {
+    uint32_t v[4], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t j = base + threadIdx.x * 4 + i;
+      v[i] = j < nb ? row[j] : 0;
+      sum += v[i];
+    }
+    uint32_t total;
+    uint32_t pre = block_excl_scan(sum, s_warp, total) + running;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t j = base + threadIdx.x * 4 + i;
+      if (j < nb) row[j] = pre;
+      pre += v[i];
+    }
+    running += total;
+  }
+  if (threadIdx.x == 0) totals[blockIdx.x] = running;
+}
+
+// Stable rank of the tile's items within their digit. Items are striped:
+// item r of thread t is tile element r*ST + t, so processing rounds r in
+// order, warps in order, lanes in order is element order. d == R: invalid.
+template <int R>
+__device__ __forceinline__ void stable_rank(const uint32_t (&d)[IPT], uint32_t (&rank)[IPT],
+                                            uint32_t* s_run, uint16_t (*s_wcnt)[NW][R]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const int buf = r & 1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d[r]);
+    const bool leader = lane == __ffs(peers) - 1;
+    const uint32_t cnt = __popc(peers);
+    const uint32_t rw = __popc(peers & lt);
+    if (leader && d[r] < R) s_wcnt[buf][warp][d[r]] = (uint16_t)cnt;
+    __syncthreads();
+    if (d[r] < R) {
+      uint32_t pre = s_run[d[r]];
+      for (int w = 0; w < warp; ++w) pre += s_wcnt[buf][w][d[r]];
+      rank[r] = pre + rw;
+    }
+    __syncthreads();
+    if (leader && d[r] < R) {
+      atomicAdd(&s_run[d[r]], cnt);
+      s_wcnt[buf][warp][d[r]] = 0;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(ST) k_downsweep(
+    const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
+    uint32_t* __restrict__ vout, uint32_t n, const unsigned long long* __restrict__ mm, int shift,
+    const uint32_t* __restrict__ counts, const uint32_t* __restrict__ totals, uint32_t nb) {
+  __shared__ uint64_t s_keys[TILE];
+  __shared__ uint32_t s_vals[TILE];
+  __shared__ uint32_t s_hist[RADIX], s_start[RADIX], s_off[RADIX], s_run[RADIX];
+  __shared__ uint16_t s_wcnt[2][NW][RADIX];
+  __shared__ uint32_t s_warp[NW];
+  const int tid = threadIdx.x, lane = tid & 31;
+  s_hist[tid] = 0;
+  s_run[tid] = 0;
+  for (int i = tid; i < 2 * NW * RADIX; i += ST) (&s_wcnt[0][0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t kmin = mm[0];
+  const uint32_t base = blockIdx.x * TILE;
+  const uint32_t tile_n = min((uint32_t)TILE, n - base);
+  uint64_t k[IPT];
+  uint32_t v[IPT], d[IPT], rank[IPT];
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const uint32_t i = r * ST + tid;
+    if (i < tile_n) {
+      k[r] = kin[base + i];
+      v[r] = vin ? vin[base + i] : base + i;
+      d[r] = (uint32_t)((k[r] - kmin) >> shift) & 255u;
+    } else {
+      d[r] = RADIX;
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, d[r]);
+    if (d[r] < RADIX && lane == __ffs(peers) - 1) atomicAdd(&s_hist[d[r]], __popc(peers));
+  }
+  __syncthreads();
+  // digit prefix over the whole array + this block's offset within the digit
+  uint32_t tot;
+  const uint32_t dpre = block_excl_scan(totals[tid], s_warp, tot);
+  const uint32_t tstart = block_excl_scan(s_hist[tid], s_warp, tot);
+  s_start[tid] = tstart;
+  s_off[tid] = dpre + counts[tid * nb + blockIdx.x] - tstart;
+  __syncthreads();
+  stable_rank<RADIX>(d, rank, s_run, s_wcnt);
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    if (d[r] < RADIX) {
+      const uint32_t p = s_start[d[r]] + rank[r];
+      s_keys[p] = k[r];
+      s_vals[p] = v[r];
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < tile_n; i += ST) {
+    const uint64_t key = s_keys[i];
+    const uint32_t dd = (uint32_t)((key - kmin) >> shift) & 255u;
+    const uint32_t g = s_off[dd] + i;
+    kout[g] = key;
+    vout[g] = s_vals[i];
+  }
+}
+
+// ---- unique / inverse / segments -----------------------------------------
+__global__ void __launch_bounds__(ST) k_head_count(const uint64_t* __restrict__ sk, uint32_t n,
+                                                   uint32_t* __restrict__ bcount) {
+  __shared__ uint32_t s_warp[NW];
+  const uint32_t base = blockIdx.x * TILE + threadIdx.x * IPT;
+  uint32_t c = 0;
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const uint32_t i = base + r;
+    if (i < n && (i == 0 || sk[i] != sk[i - 1])) ++c;
+  }
+  uint32_t tot;
+  block_excl_scan(c, s_warp, tot);
+  if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(ST) k_dedup_emit(const uint64_t* __restrict__ sk,
+                                                   const uint32_t* __restrict__ sv, uint32_t n,
+                                                   const uint32_t* __restrict__ bbase,
+                                                   uint64_t* __restrict__ uniq,
+                                                   uint32_t* __restrict__ inverse,
+                                                   uint32_t* __restrict__ seg,
+                                                   uint32_t* __restrict__ nuniq, uint32_t nb) {
+  __shared__ uint32_t s_warp[NW];
+  const uint32_t base = blockIdx.x * TILE + threadIdx.x * IPT;
+  bool f[IPT];
+  uint32_t c = 0;
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const uint32_t i = base + r;
+    f[r] = i < n && (i == 0 || sk[i] != sk[i - 1]);
+    c += f[r];
+  }
+  uint32_t tot;
+  uint32_t uid = bbase[blockIdx.x] + block_excl_scan(c, s_warp, tot);  // uniques before my items
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const uint32_t i = base + r;
+    if (i >= n) break;
+    if (f[r]) {
+      uniq[uid] = sk[i];
+      seg[uid] = i;
+      ++uid;
+    }
+    inverse[sv[i]] = uid - 1;
+  }
+  if (blockIdx.x == nb - 1 && threadIdx.x == 0) {
+    const uint32_t U = bbase[blockIdx.x] + tot;
+    seg[U] = n;
+    *nuniq = U;
+  }
+}
+
+// ---- owner bucket (key % G) ---------------------------------------------
+constexpr int MAXG = 64;
+
+__global__ void __launch_bounds__(ST) k_shard_count(const uint64_t* __restrict__ keys, uint32_t n,
+                                                    uint32_t G, uint32_t* __restrict__ counts,
+                                                    uint32_t nb) {
+  __shared__ uint32_t hist[MAXG];
+  if (threadIdx.x < MAXG) hist[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * TILE;
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const uint32_t i = base + r * ST + threadIdx.x;
+    if (i < n) atomicAdd(&hist[keys[i] % G], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < G) counts[threadIdx.x * nb + blockIdx.x] = hist[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(ST) k_shard_emit(const uint64_t* __restrict__ keys, uint32_t n,
+                                                   uint32_t G, const uint32_t* __restrict__ counts,
+                                                   const uint32_t* __restrict__ totals,
+                                                   uint32_t nb, uint32_t* __restrict__ perm,
+                                                   uint32_t* __restrict__ pos) {
+  __shared__ uint32_t s_off[MAXG], s_run[MAXG];
+  __shared__ uint16_t s_wcnt[2][NW][MAXG];
+  const int tid = threadIdx.x;
+  if (tid < MAXG) {
+    s_run[tid] = 0;
+    uint32_t pre = 0;
+    for (uint32_t g = 0; g < (uint32_t)tid && g < G; ++g) pre += totals[g];
+    s_off[tid] = tid < (int)G ? pre + counts[tid * nb + blockIdx.x] : 0;
+  }
+  for (int i = tid; i < 2 * NW * MAXG; i += ST) (&s_wcnt[0][0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * TILE;
+  uint32_t d[IPT], rank[IPT];
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const uint32_t i = base + r * ST + tid;
+    d[r] = i < n ? (uint32_t)(keys[i] % G) : MAXG;
+  }
+  stable_rank<MAXG>(d, rank, s_run, s_wcnt);
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const uint32_t i = base + r * ST + tid;
+    if (i < n) {
+      const uint32_t p = s_off[d[r]] + rank[r];
+      perm[p] = i;
+      pos[i] = p;
+    }
+  }
+}
+
+}  // namespace
+
+void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s) {
+  ws.n = n;
+  ws.d_nunique = ws.scalars.get<uint32_t>(4);
+  if (n == 0) {
+    ws.n_unique = 0;
+    ws.d_unique = ws.unique.get<uint64_t>(1);
+    ws.d_inverse = ws.inverse.get<uint32_t>(1);
+    ws.d_seg = ws.seg.get<uint32_t>(1);
+    KP_CUDA(cudaMemsetAsync(ws.d_seg, 0, 4, s));
+    KP_CUDA(cudaMemsetAsync(ws.d_nunique, 0, 4, s));
+    return;
+  }
+  const uint32_t nb = ceil_div(n, TILE);
+  auto* mm = ws.minmax.get<unsigned long long>(2);
+  k_minmax_init<<<1, 1, 0, s>>>(mm); ::kp::count_launch();
+  k_minmax<<<min(nb * 2, 1184u), 256, 0, s>>>(d_keys, n, mm); ::kp::count_launch();
+  unsigned long long h_mm[2];
+  KP_CUDA(cudaMemcpyAsync(h_mm, mm, 16, cudaMemcpyDeviceToHost, s));
+  KP_CUDA(cudaStreamSynchronize(s));
+  const uint64_t span = h_mm[1] - h_mm[0];
+  const int bits = span == 0 ? 0 : 64 - __builtin_clzll(span);
+  const int passes = bits == 0 ? 1 : (bits + 7) / 8;  // >=1: identity when all equal
+
+  uint64_t* ka = ws.keys_a.get<uint64_t>(n);
+  uint64_t* kb = ws.keys_b.get<uint64_t>(n);
+  uint32_t* va = ws.vals_a.get<uint32_t>(n);
+  uint32_t* vb = ws.vals_b.get<uint32_t>(n);
+  uint32_t* counts = ws.counts.get<uint32_t>((size_t)RADIX * nb);
+  uint32_t* totals = ws.totals.get<uint32_t>(RADIX);
+  const uint64_t* kin = d_keys;
+  const uint32_t* vin = nullptr;
+  uint64_t* kout = ka;
+  uint32_t* vout = va;
+  for (int p = 0; p < passes; ++p) {
+    const int shift = p * 8;
+    k_upsweep<<<nb, ST, 0, s>>>(kin, n, mm, shift, counts, nb); ::kp::count_launch();
+    k_scan_rows<<<RADIX, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
+    k_downsweep<<<nb, ST, 0, s>>>(kin, vin, kout, vout, n, mm, shift, counts, totals, nb); ::kp::count_launch();
+    kin = kout;
+    vin = vout;
+    kout = (kout == ka) ? kb : ka;
+    vout = (vout == va) ? vb : va;
+  }
+  ws.sorted_keys = kin;
+  ws.sorted_vals = vin;
+
+  uint32_t* bcount = ws.bcount.get<uint32_t>(nb);
+  k_head_count<<<nb, ST, 0, s>>>(kin, n, bcount); ::kp::count_launch();
+  k_scan_rows<<<1, ST, 0, s>>>(bcount, nb, ws.d_nunique + 1); ::kp::count_launch();
+  ws.d_unique = ws.unique.get<uint64_t>(n);
+  ws.d_inverse = ws.inverse.get<uint32_t>(n);
+  ws.d_seg = ws.seg.get<uint32_t>(n + 1);
+  k_dedup_emit<<<nb, ST, 0, s>>>(kin, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
+                                  ws.d_nunique, nb); ::kp::count_launch();
+  KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
+  KP_CUDA(cudaStreamSynchronize(s));
+}
+
+void shard(const uint64_t* d_unique, uint32_t n, uint32_t G, uint32_t* d_perm, uint32_t* d_pos,
+           uint64_t* h_counts, ShardWs& ws, cudaStream_t s) {
+  KP_CHECK(G >= 1 && G <= MAXG, kErrConfig, "shard: G must be in [1, 64]");
+  for (uint32_t g = 0; g < G; ++g) h_counts[g] = 0;
+  if (n == 0) return;
+  const uint32_t nb = ceil_div(n, TILE);
+  uint32_t* counts = ws.bcount.get<uint32_t>((size_t)G * nb);
+  uint32_t* totals = ws.scalars.get<uint32_t>(MAXG);
+  k_shard_count<<<nb, ST, 0, s>>>(d_unique, n, G, counts, nb); ::kp::count_launch();
+  k_scan_rows<<<G, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
+  k_shard_emit<<<nb, ST, 0, s>>>(d_unique, n, G, counts, totals, nb, d_perm, d_pos); ::kp::count_launch();
+  uint32_t h[MAXG];
+  KP_CUDA(cudaMemcpyAsync(h, totals, G * 4, cudaMemcpyDeviceToHost, s));
+  KP_CUDA(cudaStreamSynchronize(s));
+  for (uint32_t g = 0; g < G; ++g) h_counts[g] = h[g];
+}
+
+}  // namespace kp

@@ -1,0 +1,272 @@
+"""GPU parity: the sm_100a path (through the C ABI / C++ shim) against the oracle.
+
+Bars:
+  * integer/byte/index work -- dedup output + inverse, owner shard, table key
+    sets -- BIT-EXACT;
+  * elementwise rules (AdaGrad, dense Adam, merge) -- bit-exact against fp32
+    numpy/oracle arithmetic when the inputs are identical;
+  * training state after N steps (embeddings, optimizer state, dense x, loss,
+    AUC) -- within the stated fp32 tolerance of the f64 reference:
+        TOL_W    = 2e-4 abs + 1e-3 rel   (embeddings, dense x)
+        TOL_ACC  = 1e-3 rel             (AdaGrad accumulators, Adam v)
+        TOL_LOSS = 1e-4 abs             (batch loss)
+        TOL_AUC  = 5e-3 abs             (batch / cumulative AUC; rank-based,
+                                          near-ties may flip)
+    The f32 restatement's own drift from f64 on the same fixtures is
+    <=1e-5 (w, x), <=4.4e-4 (AUC), <=5e-7 (loss) -- tests/test_oracle.py.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from helpers import golden_batches, load_golden, rel_err, trainer_kwargs
+from oracle import oracle as O
+from paper_2201_05500_b200.data import make_batch
+
+pytestmark = pytest.mark.gpu
+
+TOL_W_ABS, TOL_W_REL = 2e-4, 1e-3
+TOL_ACC_REL = 1e-3
+TOL_LOSS = 1e-4
+TOL_AUC = 5e-3
+
+
+def close(a, b, atol=TOL_W_ABS, rtol=TOL_W_REL):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    err = np.abs(a - b) - (atol + rtol * np.abs(b))
+    return float(err.max()) <= 0 if a.size else True
+
+
+# ------------------------------------------------------------------ dedup ---
+@pytest.mark.parametrize("n,V,zipf", [(0, 10, None), (1, 10, None), (1000, 1, None),
+                                      (5000, 50, None), (300_000, 10**6, 1.1),
+                                      (2_000_000, 10**8, 1.1), (100_000, 2**64 - 1, None)])
+def test_dedup_bit_exact(kp, n, V, zipf):
+    rng = np.random.default_rng(n + 1)
+    if zipf:
+        from paper_2201_05500_b200.data import ZipfSampler, rank_to_key
+        keys = rank_to_key(ZipfSampler(V, zipf).sample(n, rng), V)
+    else:
+        keys = rng.integers(0, V, n, dtype=np.uint64) if V < 2**63 else \
+            rng.integers(0, 2**63, n, dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+    if n > 2:
+        keys[1] = np.uint64(2**64 - 1)
+    u, inv, seg = kp.dedup(keys)
+    want, winv = O.orc_dedup(keys)
+    assert np.array_equal(u, want)
+    assert np.array_equal(inv, winv)
+    if n:
+        assert seg[0] == 0 and seg[-1] == n and np.all(np.diff(seg.astype(np.int64)) > 0)
+        assert np.array_equal(np.diff(seg.astype(np.int64)), np.bincount(inv, minlength=len(u)))
+    if O.ref_available() and n <= 300_000:
+        assert np.array_equal(u, O.ref_dedup(keys))
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
+def test_shard_bit_exact(kp, G):
+    rng = np.random.default_rng(G)
+    u = np.unique(rng.integers(0, 10**9, 100_000).astype(np.uint64))
+    perm, pos, counts = kp.shard(u, G)
+    wperm, wcounts = O.orc_shard(u, G)
+    assert np.array_equal(perm, wperm) and np.array_equal(counts, wcounts)
+    assert np.array_equal(pos[perm], np.arange(len(u)))
+
+
+# ------------------------------------------------------------------ store ---
+def test_store_fresh_and_adagrad_goldens(kp, tmp_path):
+    # test_store.cpp:61-83, test_smoke.py:86-97 (values through fp32)
+    s = kp.TieredStore(cache_capacity=2, cold_dir=str(tmp_path / "cold"), embedding_dim=2)
+    got = s.pull([1, 2, 3])
+    assert got[3] == ([0.0, 0.0], [np.float32(1e-6)] * 2)
+    s.push({1: [1.0, -1.0]}, lr=0.1)
+    w, acc = s.pull([1])[1]
+    a32 = np.float32(1e-6) + np.float32(1.0)
+    assert acc == [float(a32)] * 2
+    assert w[0] == float(np.float32(0) - np.float32(0.1) * np.float32(1.0) / np.sqrt(a32))
+    assert abs(w[0] + 0.1 / np.sqrt(1 + 1e-6)) < 1e-7
+    assert s.cache_size == 3
+    with pytest.raises(kp.StoreError, match="not in the current working set"):
+        s.push({99: [1.0, 1.0]}, lr=0.1)
+    with pytest.raises(kp.StoreError, match="dimension mismatch"):
+        s.push({1: [1.0]}, lr=0.1)
+    with pytest.raises(kp.StoreError, match="empty key set"):
+        s.pull([])
+    w2, _ = kp.adagrad_sparse_update([1.0], [1.0], [3.0], 0.1)
+    assert abs(w2[0] - 0.9051316701949486) < 1e-6
+
+
+def test_store_u64max_key(kp, tmp_path):
+    s = kp.TieredStore(cache_capacity=8, cold_dir=str(tmp_path), embedding_dim=4)
+    big = 2**64 - 1
+    s.pull([0, big, 5])
+    s.push({big: [1.0, 2.0, 3.0, 4.0]}, lr=0.5)
+    w, acc = s.pull([big])[big]
+    assert acc[3] == float(np.float32(1e-6) + np.float32(16.0))
+    k, W, A = s.export()
+    assert list(k) == [0, 5, big]
+
+
+def test_store_flat_map_oracle(kp, tmp_path):
+    # acceptance.cpp:332-414 restated: 1000 keys, dim 4, lr 0.05, seed 41; the
+    # fp32 flat map uses the same expression tree -> bit-exact
+    s = kp.TieredStore(cache_capacity=64, cold_dir=str(tmp_path), embedding_dim=4)
+    rng = np.random.default_rng(41)
+    flat = {}
+    lr = np.float32(0.05)
+    for op in range(3000):
+        n = 1 + int(rng.integers(0, 8))
+        keys = sorted(set(int(k) for k in rng.integers(0, 1000, n)))
+        got = s.pull(keys)
+        for k in keys:
+            w, a = flat.setdefault(k, (np.zeros(4, np.float32), np.full(4, np.float32(1e-6))))
+            assert np.array_equal(np.float32(got[k][0]), w) and np.array_equal(np.float32(got[k][1]), a)
+        if rng.random() < 0.75:
+            upd = {k: rng.uniform(-1, 1, 4) for k in keys}
+            s.push(upd, lr=0.05)
+            for k, g in upd.items():
+                w, a = flat[k]
+                g = g.astype(np.float32)
+                a = a + g * g
+                w = w - (lr * g) / np.sqrt(a)
+                flat[k] = (w, a)
+    k, W, A = s.export()
+    assert list(k) == sorted(flat)
+    for i, key in enumerate(k):
+        assert np.array_equal(W[i], flat[int(key)][0]) and np.array_equal(A[i], flat[int(key)][1])
+
+
+# ------------------------------------------------------------------ dense ---
+def test_dense_kats(kp):
+    h = kp.AdamHyper()
+    h.alpha, h.beta1, h.beta2, h.epsilon, h.k = 0.1, 0.0, 0.999, 0.01, 4
+    s = kp.local_adam_step(kp.WorkerState.init([1.0], 0.01), [0.5], h)
+    assert abs(s.m[0] - 0.5) < 1e-7 and abs(s.v[0] - 0.01024) < 1e-7 and abs(s.x[0] - 0.5) < 1e-6
+    assert s.v_bar[0] == float(np.float32(0.01))
+    h.alpha = 0.1
+    a = kp.WorkerState.init([1.0], 0.01)
+    b = kp.WorkerState.init([0.0], 0.01)
+    a.m, a.v = [0.2], [0.04]
+    b.m, b.v = [-0.2], [0.16]
+    m = kp.global_merge([a, b], h)
+    assert abs(m[0].v_bar[0] - 0.1) < 1e-7 and abs(m[0].x[0] - 0.5) < 1e-6
+    assert m[0].x == m[1].x and m[0].v == m[0].v_bar and m[0].m == [0.2] and m[1].m == [-0.2]
+    one = kp.WorkerState.init([1.5, -0.5], 0.01)
+    one.m, one.v = [0.3, 0.1], [0.2, 0.4]
+    merged = kp.global_merge([one] * 5, h)
+    x32 = np.float32([1.5, -0.5]) - np.float32(0.1) * np.float32([0.3, 0.1]) / np.sqrt(np.float32([0.2, 0.4]))
+    assert merged[0].x == [float(v) for v in x32]  # identical workers: bit-identical to N=1
+
+
+@pytest.mark.parametrize("key", ["n1_k1", "n2_k2", "n3_k5", "n8_k4"])
+def test_kstep_engine_fixture(kp, key):
+    from helpers import GOLDEN
+    z = np.load(GOLDEN + "/kstep.npz")
+    N, k = (int(p[1:]) for p in key.split("_"))
+    h = kp.AdamHyper()
+    h.alpha, h.beta1, h.beta2, h.epsilon, h.k = 0.05, 0.9, 0.99, 0.01, k
+    e = kp.KStepEngine(h, N, list(z[key + "_x0"]))
+    o32 = O.orc_kstep(32, 0.05, 0.9, 0.99, 0.01, k, N, z[key + "_x0"], z[key + "_g"])
+    for t, g in enumerate(z[key + "_g"]):
+        merged, _ = e.step([list(r) for r in g])
+        assert merged == bool(z[key + "_merged"][t])
+        st = e.states()
+        for i in range(N):
+            # bit-exact vs the fp32 restatement, tolerance vs the f64 reference
+            assert np.array_equal(np.float32(st[i].x), np.float32(o32["x"][t, i])), (t, i)
+            assert close(st[i].x, z[key + "_x"][t, i], 1e-5, 1e-4)
+
+
+def test_replica_invariance_bitwise(kp):
+    h = kp.AdamHyper()
+    h.alpha, h.beta1, h.beta2, h.epsilon, h.k = 0.01, 0.9, 0.999, 0.01, 5
+    rng = np.random.default_rng(2)
+    x0 = list(rng.uniform(-1, 1, 10))
+    solo, octo = kp.KStepEngine(h, 1, x0), kp.KStepEngine(h, 8, x0)
+    for _ in range(60):
+        g = list(rng.normal(size=10))
+        solo.step([g])
+        octo.step([g] * 8)
+        assert octo.x_bar() == solo.x_bar()
+
+
+# ---------------------------------------------------------------- trainer ---
+@pytest.mark.parametrize("name", ["n1_k1", "n4_k4_mean", "desk"])
+def test_trainer_vs_reference_fixture(kp, name):
+    d, meta = load_golden("trainer_" + name)
+    cfg = meta["cfg"]
+    tr = kp.Trainer(table_capacity=1 << 16, **trainer_kwargs(cfg))
+    for b, (offs, keys, labels) in enumerate(golden_batches(d, meta["batches"])):
+        r = tr.train_batch(offs.astype(np.uint32), keys, labels, predict_first=True)
+        assert abs(r["loss"] - d[f"b{b}_loss"]) <= TOL_LOSS, (b, r["loss"], d[f"b{b}_loss"])
+        auc = O.orc_auc(r["preds"].astype(np.float64), labels)
+        assert abs(auc - d[f"b{b}_auc"]) <= TOL_AUC
+    keys, w, s1, _ = tr.table()
+    assert np.array_equal(keys, d["table_keys"])  # key set bit-exact
+    assert close(w, d["table_w"]), rel_err(w, d["table_w"])
+    assert close(s1, d["table_acc"], 0, TOL_ACC_REL)
+    n_workers = cfg.get("n_workers", 1)
+    for i in range(n_workers):
+        ws = tr.worker_state(i)
+        assert close(ws["x"], d[f"w{i}_x"]), i
+        assert close(ws["v"], d[f"w{i}_v"], 1e-9, TOL_ACC_REL)
+    assert tr.completed_steps == d["steps"]
+
+
+@pytest.mark.parametrize("S,pool,rule", [(4, "sum", "adagrad"), (6, "mean", "adagrad"),
+                                         (1, "sum", "adam"), (3, "mean", "adam")])
+def test_trainer_slots_and_sparse_adam_vs_oracle(kp, S, pool, rule):
+    cfg = O.TrainerCfg(n_workers=2, k=3, minibatch_size=64, embedding_dim=8, n_slots=S,
+                       hidden=(16,), pooling=pool, activation="relu", alpha=0.02, sparse_lr=0.1,
+                       sparse_rule=rule, sparse_beta1=0.9, sparse_beta2=0.99, sparse_eps=1e-6)
+    o64 = O.Orc(cfg, 64)
+    tr = kp.Trainer(table_capacity=1 << 16, **trainer_kwargs(vars(cfg)))
+    for b in range(3):
+        if S > 1:
+            bt = make_batch(256, V=3000, zipf_s=1.1, n_slots=S, seed=b)
+            # multi-hot slots: duplicate every other occurrence into the same slot
+            keys = np.repeat(bt.keys, 2)[: 2 * len(bt.keys)]
+            slots = np.repeat(bt.slots, 2)
+            offs = (bt.offs.astype(np.int64) * 2).astype(np.uint32)
+        else:
+            bt = make_batch(256, V=3000, zipf_s=1.1, nnz=9, poisson=True, seed=b)
+            keys, slots, offs = bt.keys, None, bt.offs
+        ro = o64.batch(offs, keys, bt.labels, slots=slots, predict_first=True)
+        rg = tr.train_batch(offs, keys, bt.labels, slots=slots, predict_first=True)
+        assert abs(ro["loss"] - rg["loss"]) <= TOL_LOSS
+    k64, w64, a64, v64 = o64.table()
+    kg, wg, s1, s2 = tr.table()
+    assert np.array_equal(k64, kg)
+    assert close(wg, w64)
+    assert close(s1, a64, 1e-9 if rule == "adagrad" else 1e-6, TOL_ACC_REL if rule == "adagrad" else 1e-2)
+    for i in range(2):
+        assert close(tr.worker_state(i)["x"], o64.worker_state(i)["x"])
+
+
+def test_trainer_deterministic(kp):
+    def run():
+        tr = kp.Trainer(table_capacity=1 << 18, n_workers=1, k=1, minibatch_size=4096,
+                        embedding_dim=16, n_slots=8, hidden=[32, 16])
+        for b in range(2):
+            bt = make_batch(4096, V=10**6, zipf_s=1.1, n_slots=8, seed=b)
+            tr.train_batch(bt.offs, bt.keys, bt.labels, slots=bt.slots)
+        return tr.table(), tr.worker_state(0)["x"]
+    (k1, w1, a1, _), x1 = run()
+    (k2, w2, a2, _), x2 = run()
+    assert np.array_equal(k1, k2) and np.array_equal(w1, w2) and np.array_equal(a1, a2)
+    assert np.array_equal(x1, x2)
+
+
+def test_trainer_errors(kp):
+    with pytest.raises(kp.ConfigError):
+        kp.Trainer(n_workers=1, k=0)
+    tr = kp.Trainer(table_capacity=8, n_workers=1, embedding_dim=4, hidden=[])
+    bt = make_batch(64, V=10**6, zipf_s=None, nnz=4, seed=0)
+    with pytest.raises(kp.StoreError, match="table full"):
+        tr.train_batch(bt.offs, bt.keys, bt.labels)
+    tr2 = kp.Trainer(n_workers=1, embedding_dim=4, n_slots=2, hidden=[])
+    bad = np.array([1, 0], np.uint16)
+    with pytest.raises(kp.ConfigError, match="slot"):
+        tr2.train_batch(np.array([0, 2], np.uint32), np.array([5, 6], np.uint64),
+                        np.array([1], np.int32), slots=bad)
