@@ -82,11 +82,15 @@ class Clocks:
         self.proc = None
 
     def __enter__(self):
+        import tempfile
+        self.path = tempfile.mktemp(prefix="kp_clocks_", suffix=".csv")
         try:
+            # -f: nvidia-smi writes (and flushes) each sample to the file itself
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
         except Exception:
             self.proc = None
         return self
@@ -94,11 +98,18 @@ class Clocks:
     def __exit__(self, *a):
         self.out = ""
         if self.proc:
+            time.sleep(0.2)
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            try:
+                with open(self.path) as f:
+                    self.out = f.read()
+                os.unlink(self.path)
+            except OSError:
+                pass
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()

@@ -139,6 +139,13 @@ int kp_centered_mean(const float* d_vecs, uint64_t stride, uint32_t n, uint64_t 
 int kp_kstep_merge(kp_comm* comm, float* d_x, float* d_m, float* d_v, float* d_vbar, uint32_t W,
                    uint64_t D, float alpha, int reset_local_v, kp_stream s);
 
+/* ------------------------------------------------------------- GEMM ---
+ * C[M][N] = A[M][K] . B[N][K]^T in fp32 (the MLP's contraction, model.cpp:107-109).
+ * engine 0 = auto (tcgen05 3xTF32 when the shapes allow TMA), 1 = SIMT fp32,
+ * 2 = tcgen05 only (KP_ERR_CONFIG if unsupported). */
+int kp_gemm_nt(const float* d_A, int lda, const float* d_B, int ldb, float* d_C, int ldc, int M,
+               int N, int K, int engine, kp_stream s);
+
 /* ------------------------------------------------------------- comm ---
  * One process per GPU; NCCL over NVLink/NVSwitch. The caller broadcasts the
  * 128-byte id from rank 0 (e.g. with torch.distributed) before kp_comm_init. */

@@ -25,6 +25,7 @@ try:
         comm_unique_id,
         compute_auc,
         dedup,
+        gemm_nt,
         device_count,
         global_merge,
         launch_count,
@@ -41,7 +42,7 @@ except ImportError as e:  # pragma: no cover - exercised only on broken installs
 __all__ = [
     "AdamHyper", "Comm", "ConfigError", "DeviceError", "KpsimError", "KStepEngine", "StoreError",
     "TieredStore", "Trainer", "WorkerState", "accumulate_moments", "adagrad_sparse_update",
-    "comm_unique_id", "compute_auc", "dedup", "device_count", "global_merge", "launch_count",
+    "comm_unique_id", "compute_auc", "dedup", "gemm_nt", "device_count", "global_merge", "launch_count",
     "local_adam_step", "shard", "version",
 ]
 

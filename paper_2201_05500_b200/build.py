@@ -28,7 +28,20 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE,
            "--expt-relaxed-constexpr", "-Xptxas", "-v"] + ARCH
-CUDA_SRCS = ["kp_sort", "kp_table", "kp_embed", "kp_mlp", "kp_dense", "kp_capi"]
+# NCCL: the copy torch ships (nvidia/nccl, 2.28), so the library and torch share
+# one libnccl.so.2 in a process (the system 2.27 lacks symbols torch needs).
+def _nccl_dir():
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (list(spec.submodule_search_locations) if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "lib", "libnccl.so.2")):
+            return d
+    return None
+
+
+NCCL_DIR = _nccl_dir()
+CUDA_SRCS = ["kp_sort", "kp_table", "kp_embed", "kp_mlp", "kp_gemm_tc", "kp_dense", "kp_capi"]
 HOST_SRCS = ["kpsim_b200", "module"]
 
 
@@ -61,14 +74,17 @@ def build(verbose: bool = False) -> str:
         src = os.path.join(CSRC, name + ".cu")
         out = os.path.join(OBJ, name + ".o")
         if not _newer(out, [src] + hdrs):
-            _run([NVCC] + NVFLAGS + ["-c", src, "-o", out], os.path.join(OBJ, name + ".ptxas.log"))
+            inc = ["-I" + os.path.join(NCCL_DIR, "include")] if NCCL_DIR else []
+            _run([NVCC] + NVFLAGS + inc + ["-c", src, "-o", out], os.path.join(OBJ, name + ".ptxas.log"))
         return out
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(cu, CUDA_SRCS))
     if not _newer(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs +
-             ["-L/usr/lib/x86_64-linux-gnu", "-lnccl", "-Xlinker", "-soname=libkpsim_b200.so"])
+        nccl = (["-L" + os.path.join(NCCL_DIR, "lib"), "-l:libnccl.so.2", "-Xlinker",
+                 "-rpath=" + os.path.join(NCCL_DIR, "lib")] if NCCL_DIR else ["-lnccl"])
+        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + nccl +
+             ["-Xlinker", "-soname=libkpsim_b200.so"])
 
     import pybind11
     py_inc = sysconfig.get_paths()["include"]

@@ -821,6 +821,27 @@ int kp_kstep_merge(kp_comm* comm, float* d_x, float* d_m, float* d_v, float* d_v
   });
 }
 
+// ---- GEMM ----
+int kp_gemm_nt(const float* d_A, int lda, const float* d_B, int ldb, float* d_C, int ldc, int M,
+               int N, int K, int engine, kp_stream s) {
+  return guard([&] {
+    const bool tc_ok = tc_gemm_supported(M, N, K, d_A, lda, d_B, ldb);
+    KP_CHECK(engine != 2 || tc_ok, kErrConfig, "gemm_nt: shape/alignment not supported by tcgen05 path");
+    if (engine == 1 || !tc_ok) {
+      simt_gemm_nt(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, st(s));
+    } else {
+      DevBuf hi, lo;
+      float* bhi = hi.get<float>((size_t)N * ldb);
+      float* blo = lo.get<float>((size_t)N * ldb);
+      split_hilo(d_B, bhi, blo, (size_t)N * ldb, st(s));
+      GemmEpi ep{0, 0, nullptr, nullptr, 0, nullptr, 1, 1};
+      tc_gemm_nt(M, N, K, d_A, lda, bhi, blo, ldb, d_C, ldc, ep, st(s));
+      KP_CUDA(cudaStreamSynchronize(st(s)));
+    }
+    KP_CUDA(cudaGetLastError());
+  });
+}
+
 // ---- comm ----
 int kp_comm_unique_id(uint8_t id[128]) {
   return guard([&] {

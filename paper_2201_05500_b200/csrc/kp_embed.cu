@@ -120,12 +120,18 @@ __global__ void __launch_bounds__(256) k_pool(const uint32_t* __restrict__ bag_o
     uint32_t o = o0;
     for (; o + 4 <= o1; o += 4) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) r[u].load(src + (uint64_t)idx[inverse[o + u]] * e, gl, e);
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t rr = idx[inverse[o + u]];
+        if (rr == kNoRow) r[u].zero();  // table full: error raised at the batch end
+        else r[u].load(src + (uint64_t)rr * e, gl, e);
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) acc.add(r[u]);  // occurrence order (model.cpp:93)
     }
     for (; o < o1; ++o) {
-      r[0].load(src + (uint64_t)idx[inverse[o]] * e, gl, e);
+      const uint32_t rr = idx[inverse[o]];
+      if (rr == kNoRow) r[0].zero();
+      else r[0].load(src + (uint64_t)rr * e, gl, e);
       acc.add(r[0]);
     }
     if (mean) {
@@ -165,6 +171,7 @@ __device__ __forceinline__ void finalize(const SegArgs& a, const TView& t, uint3
     g.store(a.grad_out + (uint64_t)(a.out_idx ? a.out_idx[u] : u) * a.e, gl, a.e);
     return;
   }
+  if (a.table_rows[u] == kNoRow) return;  // table full: error raised at the batch end
   const uint64_t o = (uint64_t)a.table_rows[u] * a.e;
 #pragma unroll
   for (int q = 0; q < (V4 ? 4 : NV); ++q) {
@@ -313,7 +320,7 @@ __global__ void k_gather_rows(const float* __restrict__ src, const uint32_t* __r
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total;
        q += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = q / e, j = q % e;
-    out[q] = src[(uint64_t)idx[i] * e + j];
+    out[q] = idx[i] == kNoRow ? 0.f : src[(uint64_t)idx[i] * e + j];
   }
 }
 

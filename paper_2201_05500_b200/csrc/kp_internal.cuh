@@ -105,6 +105,28 @@ void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* 
 void gather_rows(const float* d_src, const uint32_t* d_idx, uint32_t n, uint32_t e, float* d_out,
                  cudaStream_t s);
 
+// --------------------------------------------------------------- GEMM ----
+// epilogue: 0 store, 1 act(acc + bias[n]), 2 acc * act'(aux[m][n]),
+//           3 acc * coeff[m*S + n/e] (mean-pooling coefficient)
+struct GemmEpi {
+  int mode;
+  int act;
+  const float* bias;
+  const float* aux;
+  int ld_aux;
+  const float* coeff;
+  uint32_t S, e;
+};
+// tcgen05 3xTF32 GEMM: C = epi(A[M][K] . B[N][K]^T), (B, Blo) = split_hilo(B)
+bool tc_gemm_supported(int M, int N, int K, const float* A, int lda, const float* B, int ldb);
+void tc_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, const float* Blo,
+                int ldb, float* C, int ldc, const GemmEpi& ep, cudaStream_t s);
+void split_hilo(const float* x, float* hi, float* lo, size_t n, cudaStream_t s);
+bool tc_enabled();  // KP_GEMM=simt disables the tensor-core path
+// C = A . B^T on the SIMT fp32 path (reference engine for the tensor-core path)
+void simt_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+                  int ldc, cudaStream_t s);
+
 // ---------------------------------------------------------------- MLP ----
 struct MlpShape {
   uint32_t n_layers = 0;          // hidden + 1
@@ -116,7 +138,7 @@ struct MlpShape {
 struct MlpWs {
   DevBuf act[9];    // per hidden layer activations [B][width]
   DevBuf dz[2];     // ping-pong upstream grads
-  DevBuf logits, delta, partials, lossp;
+  DevBuf logits, delta, partials, lossp, whi, wlo, wt, wthi, wtlo;
 };
 // Forward over B instances (input [B][in]); writes preds (sigmoid) and
 // logits; keeps activations in ws for backward.

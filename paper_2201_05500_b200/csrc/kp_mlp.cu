@@ -21,14 +21,7 @@ constexpr int BM = 128, BN = 128, BK = 8, GT = 256;
 
 enum Epi : int { kStore = 0, kBiasAct = 1, kDAct = 2, kCoeff = 3 };
 
-struct EpiArgs {
-  int mode;
-  int act;             // 0 relu, 1 tanh
-  const float* bias;   // [N]           (kBiasAct)
-  const float* aux;    // [M][ldc]      (kDAct: activations of that layer)
-  const float* coeff;  // [M*S + n/e]   (kCoeff)
-  uint32_t S, e;
-};
+using EpiArgs = GemmEpi;
 
 __device__ __forceinline__ float act_fwd(int act, float z) {
   return act == 0 ? (z > 0.f ? z : 0.f) : tanhf(z);
@@ -177,7 +170,7 @@ __global__ void __launch_bounds__(GT) k_gemm(int M, int N, int K, const float* _
       if (ep.mode == kBiasAct) {
         v = act_fwd(ep.act, __fadd_rn(v, ep.bias[n]));
       } else if (ep.mode == kDAct) {
-        v = __fmul_rn(v, act_bwd(ep.act, ep.aux[(size_t)m * ldc + n]));
+        v = __fmul_rn(v, act_bwd(ep.act, ep.aux[(size_t)m * ep.ld_aux + n]));
       } else if (ep.mode == kCoeff) {
         v = __fmul_rn(v, ep.coeff[(size_t)m * ep.S + n / ep.e]);
       }
@@ -325,6 +318,12 @@ int pick_splits(int M, int N, int K) {
 
 }  // namespace
 
+void simt_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+                  int ldc, cudaStream_t s) {
+  EpiArgs plain{kStore, 0, nullptr, nullptr, 0, nullptr, 1, 1};
+  gemm<true, true>(M, N, K, A, lda, B, ldb, C, ldc, 1, plain, s);
+}
+
 void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_t B,
                  float* d_preds, MlpWs& ws, cudaStream_t s) {
   if (B == 0) return;
@@ -333,8 +332,16 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
   for (uint32_t l = 0; l + 1 < L; ++l) {
     const int K = m.widths[l], N = m.widths[l + 1];
     float* out = ws.act[l].get<float>((size_t)B * N);
-    EpiArgs ep{kBiasAct, m.activation, d_x + m.b_off[l], nullptr, nullptr, 1, 1};
-    gemm<true, true>(B, N, K, in, K, d_x + m.w_off[l], K, out, N, 1, ep, s);
+    EpiArgs ep{kBiasAct, m.activation, d_x + m.b_off[l], nullptr, 0, nullptr, 1, 1};
+    const float* W = d_x + m.w_off[l];
+    if (tc_enabled() && tc_gemm_supported(B, N, K, in, K, W, K)) {
+      float* whi = ws.whi.get<float>((size_t)N * K);
+      float* wlo = ws.wlo.get<float>((size_t)N * K);
+      split_hilo(W, whi, wlo, (size_t)N * K, s);
+      tc_gemm_nt(B, N, K, in, K, whi, wlo, K, out, N, ep, s);
+    } else {
+      gemm<true, true>(B, N, K, in, K, W, K, out, N, 1, ep, s);
+    }
     in = out;
   }
   const int W = m.widths[L - 1];
@@ -344,6 +351,33 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
 }
 
 namespace {
+__global__ void k_transpose(const float* __restrict__ in, int R, int Cc, float* __restrict__ out) {
+  __shared__ float t[32][33];
+  const int c = blockIdx.x * 32 + threadIdx.x, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8)
+    if (r0 + i < R && c < Cc) t[i][threadIdx.x] = in[(size_t)(r0 + i) * Cc + c];
+  __syncthreads();
+  const int r = r0 + threadIdx.x, c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += 8)
+    if (c0 + i < Cc && r < R) out[(size_t)(c0 + i) * R + r] = t[threadIdx.x][i];
+}
+
+// dX[B][K] = dZ[B][N] . W[N][K]  (W^T kept K-major for the tensor-core path)
+void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, const EpiArgs& ep,
+             MlpWs& ws, cudaStream_t s) {
+  if (tc_enabled() && tc_gemm_supported(B, K, N, dZ, N, W, N)) {
+    float* wt = ws.wt.get<float>((size_t)N * K);
+    float* wthi = ws.wthi.get<float>((size_t)N * K);
+    float* wtlo = ws.wtlo.get<float>((size_t)N * K);
+    dim3 g(ceil_div(K, 32), ceil_div(N, 32));
+    k_transpose<<<g, dim3(32, 8), 0, s>>>(W, N, K, wt); ::kp::count_launch();
+    split_hilo(wt, wthi, wtlo, (size_t)N * K, s);
+    tc_gemm_nt(B, K, N, dZ, N, wthi, wtlo, N, out, K, ep, s);
+  } else {
+    gemm<true, false>(B, K, N, dZ, N, W, K, out, K, 1, ep, s);
+  }
+}
+
 void colsum(const float* X, const float* w, int B, int N, float* out, MlpWs& ws, cudaStream_t s) {
   int chunks = (B + 511) / 512;
   if (chunks > 64) chunks = 64;
@@ -396,7 +430,7 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
     const float* in = layer_in(l);
     // dW_l[o][i] = sum_b dZ[b][o] in[b][i]   (deterministic split-K)
     const int sp = pick_splits(N, K, B);
-    EpiArgs plain{kStore, 0, nullptr, nullptr, nullptr, 1, 1};
+    EpiArgs plain{kStore, 0, nullptr, nullptr, 0, nullptr, 1, 1};
     if (sp == 1) {
       gemm<false, false>(N, K, B, dZ, N, in, K, d_grad + m.w_off[l], K, 1, plain, s);
     } else {
@@ -409,12 +443,12 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
     // upstream for the layer below: dX = dZ . W_l, then act' or pooling coeff
     if (l > 0) {
       float* next = ws.dz[cur ^ 1].get<float>((size_t)B * K);
-      EpiArgs ep{kDAct, m.activation, nullptr, static_cast<const float*>(ws.act[l - 1].p), nullptr, 1, 1};
-      gemm<true, false>(B, K, N, dZ, N, d_x + m.w_off[l], K, next, K, 1, ep, s);
+      EpiArgs ep{kDAct, m.activation, nullptr, static_cast<const float*>(ws.act[l - 1].p), K, nullptr, 1, 1};
+      dx_gemm(B, K, N, dZ, d_x + m.w_off[l], next, ep, ws, s);
       cur ^= 1;
     } else if (d_dinput) {
-      EpiArgs ep{d_coeff ? kCoeff : kStore, 0, nullptr, nullptr, d_coeff, S, e};
-      gemm<true, false>(B, K, N, dZ, N, d_x + m.w_off[l], K, d_dinput, K, 1, ep, s);
+      EpiArgs ep{d_coeff ? kCoeff : kStore, 0, nullptr, nullptr, 0, d_coeff, S, e};
+      dx_gemm(B, K, N, dZ, d_x + m.w_off[l], d_dinput, ep, ws, s);
     }
   }
 }

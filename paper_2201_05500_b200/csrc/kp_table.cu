@@ -12,6 +12,7 @@ namespace kp {
 namespace {
 
 constexpr uint32_t kPending = 0xFFFFFFFEu;
+constexpr uint32_t kFullRow = 0xFFFFFFFDu;  // slot claimed but the table had no free row
 constexpr int GS = 16;  // lanes per probing group = slots per bucket
 
 __device__ __forceinline__ void init_row(const TView& t, uint32_t row, int gl) {
@@ -57,6 +58,7 @@ __device__ uint32_t probe(const TView& t, uint64_t key, int gl, uint32_t gmask, 
     return r;
   }
   uint64_t b = mix64(key) & t.bmask;
+  uint64_t probes = 0;
   for (;;) {
     const uint64_t slot = b * GS + gl;
     const uint64_t k = *(volatile uint64_t*)(t.keys + slot);
@@ -66,7 +68,7 @@ __device__ uint32_t probe(const TView& t, uint64_t key, int gl, uint32_t gmask, 
       volatile uint32_t* rp = t.rows + s;
       uint32_t r = *rp;
       while (r == kNoRow && INSERT) r = *rp;  // inserter in flight (same key, same launch)
-      return r;
+      return r >= kFullRow ? kNoRow : r;
     }
     const uint32_t empty = __ballot_sync(gmask, k == kEmptyKey) >> gbase;
     if (empty) {
@@ -92,18 +94,22 @@ __device__ uint32_t probe(const TView& t, uint64_t key, int gl, uint32_t gmask, 
         row = __shfl_sync(gmask, row, gbase + el);
         if (row != kNoRow) init_row(t, row, gl);
         __threadfence();
-        if (gl == el) *(volatile uint32_t*)(t.rows + s) = row;
+        if (gl == el) *(volatile uint32_t*)(t.rows + s) = row == kNoRow ? kFullRow : row;
         return row;
       }
       if (old == key) {
         volatile uint32_t* rp = t.rows + s;
         uint32_t r = *rp;
         while (r == kNoRow) r = *rp;
-        return r;
+        return r >= kFullRow ? kNoRow : r;
       }
       continue;  // lost the slot to another key: re-read this bucket
     }
     b = (b + 1) & t.bmask;
+    if (++probes > t.bmask) {  // every bucket visited: no slot left
+      if (gl == 0) t.sc[2] = 1;
+      return kNoRow;
+    }
   }
 }
 
@@ -129,7 +135,7 @@ __global__ void k_export(TView t, uint64_t nslots, uint64_t* __restrict__ out_ke
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < nslots;
        s += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t r = t.rows[s];
-    if (r != kNoRow && r < t.capacity) {
+    if (r < t.capacity) {
       const unsigned long long p = atomicAdd(cnt, 1ull);
       out_keys[p] = t.keys[s];
       out_rows[p] = r;

@@ -248,6 +248,28 @@ PYBIND11_MODULE(_kpsim_b200, m) {
         },
         py::arg("unique"), py::arg("G"), py::arg("device") = 0);
 
+  m.def("gemm_nt",
+        [](Arr<float> A, Arr<float> B, int engine, int device) {
+          if (A.ndim() != 2 || B.ndim() != 2 || A.shape(1) != B.shape(1))
+            throw Error("gemm_nt: A[M][K], B[N][K] expected");
+          check(kp_set_device(device));
+          const int M = (int)A.shape(0), K = (int)A.shape(1), N = (int)B.shape(0);
+          void *da, *db, *dc;
+          check(kp_dev_alloc((size_t)M * K * 4, &da));
+          check(kp_dev_alloc((size_t)N * K * 4, &db));
+          check(kp_dev_alloc((size_t)M * N * 4, &dc));
+          int rc = kp_memcpy_h2d(da, A.data(), (size_t)M * K * 4);
+          if (rc == KP_OK) rc = kp_memcpy_h2d(db, B.data(), (size_t)N * K * 4);
+          if (rc == KP_OK)
+            rc = kp_gemm_nt((const float*)da, K, (const float*)db, K, (float*)dc, N, M, N, K, engine, nullptr);
+          Arr<float> C({(py::ssize_t)M, (py::ssize_t)N});
+          if (rc == KP_OK) rc = kp_memcpy_d2h(C.mutable_data(), dc, (size_t)M * N * 4);
+          for (void* p2 : {da, db, dc}) kp_dev_free(p2);
+          check(rc);
+          return C;
+        },
+        py::arg("A"), py::arg("B"), py::arg("engine") = 0, py::arg("device") = 0);
+
   // ---- comm ----
   m.def("comm_unique_id", [] {
     uint8_t id[128];

@@ -270,3 +270,23 @@ def test_trainer_errors(kp):
     with pytest.raises(kp.ConfigError, match="slot"):
         tr2.train_batch(np.array([0, 2], np.uint32), np.array([5, 6], np.uint64),
                         np.array([1], np.int32), slots=bad)
+
+
+# ------------------------------------------------------------------- GEMM ---
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (300, 256, 6400), (65, 40, 100), (1000, 8, 96),
+                                   (4096, 128, 256)])
+def test_tcgen05_gemm_fp32_accuracy(kp, M, N, K):
+    """3xTF32 tcgen05 GEMM vs an f64 numpy product: fp32-level error."""
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    want = A.astype(np.float64) @ B.astype(np.float64).T
+    scale = np.sqrt(K)
+    tc = kp.gemm_nt(A, B, engine=2)
+    simt = kp.gemm_nt(A, B, engine=1)
+    err_tc = np.max(np.abs(tc - want)) / scale
+    err_simt = np.max(np.abs(simt - want)) / scale
+    print(f"gemm M={M} N={N} K={K}: normalized max err tc={err_tc:.3e} simt={err_simt:.3e}")
+    assert err_simt < 5e-5
+    # 3xTF32 keeps fp32-level accuracy: within a small factor of the fp32 SIMT path
+    assert err_tc < 3 * err_simt + 2e-6, (err_tc, err_simt)
