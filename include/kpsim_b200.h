@@ -145,6 +145,10 @@ int kp_kstep_merge(kp_comm* comm, float* d_x, float* d_m, float* d_v, float* d_v
  * 2 = tcgen05 only (KP_ERR_CONFIG if unsupported). */
 int kp_gemm_nt(const float* d_A, int lda, const float* d_B, int ldb, float* d_C, int ldc, int M,
                int N, int K, int engine, kp_stream s);
+/* C[M][N] = A[K][M]^T . B[K][N] (the weight gradient dW = dZ^T X of
+ * model.cpp:184-186, contracted over the minibatch); deterministic split-K. */
+int kp_gemm_tn(const float* d_A, int lda, const float* d_B, int ldb, float* d_C, int ldc, int M,
+               int N, int K, int engine, kp_stream s);
 
 /* ------------------------------------------------------------- comm ---
  * One process per GPU; NCCL over NVLink/NVSwitch. The caller broadcasts the

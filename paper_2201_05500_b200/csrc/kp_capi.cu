@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -138,6 +139,12 @@ struct kp_trainer {
   }
   // mark the END of `stage` (the previous mark is its start)
   void mark(int stage) {
+    static const bool dbg = getenv("KP_SYNC_DEBUG") != nullptr;
+    if (dbg) {  // localise asynchronous faults to a stage
+      const cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess)
+        throw KpError(kErrCuda, std::string("stage ") + std::to_string(stage) + ": " + cudaGetErrorString(e));
+    }
     if (!prof) return;
     cudaEvent_t e = next_event();
     KP_CUDA(cudaEventRecord(e, s));
@@ -830,14 +837,34 @@ int kp_gemm_nt(const float* d_A, int lda, const float* d_B, int ldb, float* d_C,
     if (engine == 1 || !tc_ok) {
       simt_gemm_nt(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, st(s));
     } else {
-      DevBuf hi, lo;
-      float* bhi = hi.get<float>((size_t)N * ldb);
-      float* blo = lo.get<float>((size_t)N * ldb);
-      split_hilo(d_B, bhi, blo, (size_t)N * ldb, st(s));
       GemmEpi ep{0, 0, nullptr, nullptr, 0, nullptr, 1, 1};
-      tc_gemm_nt(M, N, K, d_A, lda, bhi, blo, ldb, d_C, ldc, ep, st(s));
+      tc_gemm_nt(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, ep, st(s));
       KP_CUDA(cudaStreamSynchronize(st(s)));
     }
+    KP_CUDA(cudaGetLastError());
+  });
+}
+
+int kp_gemm_tn(const float* d_A, int lda, const float* d_B, int ldb, float* d_C, int ldc, int M,
+               int N, int K, int engine, kp_stream s) {
+  return guard([&] {
+    const bool tc_ok = tc_gemm_supported(M, N, K, d_A, lda, d_B, ldb);
+    KP_CHECK(engine != 2 || tc_ok, kErrConfig, "gemm_tn: shape/alignment not supported by tcgen05 path");
+    if (engine == 1 || !tc_ok) {
+      simt_gemm_tn(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, st(s));
+    } else {
+      const int sp = tc_splits(M, N, K);
+      if (sp == 1) {
+        tc_gemm_tn(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, 1, st(s));
+      } else {
+        DevBuf part;
+        float* p = part.get<float>((size_t)sp * M * ldc);
+        const int got = tc_gemm_tn(M, N, K, d_A, lda, d_B, ldb, p, ldc, sp, st(s));
+        reduce_splits(p, got, (size_t)M * ldc, d_C, st(s));
+        KP_CUDA(cudaStreamSynchronize(st(s)));
+      }
+    }
+    KP_CUDA(cudaStreamSynchronize(st(s)));
     KP_CUDA(cudaGetLastError());
   });
 }

@@ -241,6 +241,10 @@ __global__ void __launch_bounds__(256) k_seg_chunks(SegArgs a, TView t) {
         finalize(a, t, u, acc, gl);
       } else {
         acc.store(a.partials + ((uint64_t)c * 2 + (before ? 0 : 1)) * a.e, gl, a.e);
+        if (before && after) {  // spans the chunk: its (unused) tail slot reads as 0
+          acc.zero();
+          acc.store(a.partials + ((uint64_t)c * 2 + 1) * a.e, gl, a.e);
+        }
       }
       if (s1 >= p1) break;
       ++u;
@@ -248,10 +252,48 @@ __global__ void __launch_bounds__(256) k_seg_chunks(SegArgs a, TView t) {
   }
 }
 
-// Phase 2: segments spanning chunks: first chunk's tail partial, then the
-// head partials of the following chunks, in chunk order.
+// Phase 2: a segment spanning chunks c0 < c1 owns the contiguous flattened
+// partial range P[2c0+1 .. 2c1] (tail of c0, then head of each later chunk;
+// the unused tail slots in between hold 0). Short ranges are summed in order;
+// long ones (Zipf-hot keys) as loose head + 64-entry block sums Q + loose tail.
+constexpr uint32_t QB = 64;
+
 template <int LPG, int NV, bool V4>
-__global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t) {
+__global__ void __launch_bounds__(256) k_seg_blocksum(SegArgs a, uint32_t nP, float* __restrict__ Q) {
+  const int gl = threadIdx.x % LPG;
+  const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
+  const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
+  for (uint64_t j = g0; j < nP / QB; j += ng) {
+    Row<LPG, NV, V4> acc, r[4];
+    acc.zero();
+    for (uint32_t i = 0; i < QB; i += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u].load(a.partials + (j * QB + i + u) * a.e, gl, a.e);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc.add(r[u]);
+    }
+    acc.store(Q + j * a.e, gl, a.e);
+  }
+}
+
+template <int LPG, int NV, bool V4>
+__device__ __forceinline__ void sum_p(const float* P, uint64_t lo, uint64_t hi, uint32_t e,
+                                      Row<LPG, NV, V4>& acc, int gl) {
+  Row<LPG, NV, V4> r[4];
+  for (; lo + 4 <= hi; lo += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u].load(P + (lo + u) * e, gl, e);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc.add(r[u]);
+  }
+  for (; lo < hi; ++lo) {
+    r[0].load(P + lo * e, gl, e);
+    acc.add(r[0]);
+  }
+}
+
+template <int LPG, int NV, bool V4>
+__global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t, const float* __restrict__ Q) {
   const int gl = threadIdx.x % LPG;
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
   const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
@@ -259,21 +301,30 @@ __global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t) {
     const uint32_t s0 = a.seg[u], s1 = a.seg[u + 1];
     const uint32_t c0 = s0 / a.CH, c1 = (s1 - 1) / a.CH;
     if (c0 == c1) continue;
-    Row<LPG, NV, V4> acc, r;
-    acc.load(a.partials + ((uint64_t)c0 * 2 + 1) * a.e, gl, a.e);
-    for (uint32_t c = c0 + 1; c <= c1; ++c) {
-      r.load(a.partials + (uint64_t)c * 2 * a.e, gl, a.e);
-      acc.add(r);
+    const uint64_t lo = 2ull * c0 + 1, hi = 2ull * c1 + 1;  // [lo, hi)
+    Row<LPG, NV, V4> acc;
+    acc.zero();
+    if (hi - lo <= 2 * QB) {
+      sum_p(a.partials, lo, hi, a.e, acc, gl);
+    } else {
+      const uint64_t qa = (lo + QB - 1) / QB, qb = hi / QB;
+      sum_p(a.partials, lo, qa * QB, a.e, acc, gl);
+      sum_p(Q, qa, qb, a.e, acc, gl);
+      sum_p(a.partials, qb * QB, hi, a.e, acc, gl);
     }
     finalize(a, t, (uint32_t)u, acc, gl);
   }
 }
 
 template <int LPG, int NV, bool V4>
-void launch_seg(const SegArgs& a, const TView& t, cudaStream_t s) {
+void launch_seg(const SegArgs& a, const TView& t, float* Q, cudaStream_t s) {
   const uint32_t nchunks = (a.n_pos + a.CH - 1) / a.CH;
+  const uint32_t nP = 2 * nchunks;
   k_seg_chunks<LPG, NV, V4><<<grid_cap(((uint64_t)nchunks * LPG + 255) / 256), 256, 0, s>>>(a, t); ::kp::count_launch();
-  k_seg_fix<LPG, NV, V4><<<grid_cap(((uint64_t)a.U * LPG + 255) / 256), 256, 0, s>>>(a, t); ::kp::count_launch();
+  if (nP >= QB) {
+    k_seg_blocksum<LPG, NV, V4><<<grid_cap(((uint64_t)(nP / QB) * LPG + 255) / 256), 256, 0, s>>>(a, nP, Q); ::kp::count_launch();
+  }
+  k_seg_fix<LPG, NV, V4><<<grid_cap(((uint64_t)a.U * LPG + 255) / 256), 256, 0, s>>>(a, t, Q); ::kp::count_launch();
 }
 
 template <int LPG, int NV, bool V4>
@@ -311,7 +362,9 @@ struct PoolF {
 };
 template <int LPG, int NV, bool V4>
 struct SegF {
-  static void run(const SegArgs& a, const TView& t, cudaStream_t s) { launch_seg<LPG, NV, V4>(a, t, s); }
+  static void run(const SegArgs& a, const TView& t, float* Q, cudaStream_t s) {
+    launch_seg<LPG, NV, V4>(a, t, Q, s);
+  }
 };
 
 __global__ void k_gather_rows(const float* __restrict__ src, const uint32_t* __restrict__ idx,
@@ -368,7 +421,8 @@ void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* 
   a.b2 = r.beta2;
   TView tv{};
   if (t) tv = view(t);
-  dispatch_e<SegF>(e, a, tv, s);
+  float* Q = ws.qsums.get<float>((size_t)(2 * nchunks / QB + 1) * e);
+  dispatch_e<SegF>(e, a, tv, Q, s);
 }
 
 void gather_rows(const float* d_src, const uint32_t* d_idx, uint32_t n, uint32_t e, float* d_out,

@@ -1,22 +1,28 @@
 // fp32-accurate GEMM on the 5th-generation tensor cores (tcgen05, 3xTF32).
 //
-//   C[m][n] = epi( sum_k A[m][k] * B[n][k] )      A, B K-major fp32
+//   C[z][m][n] = epi( sum_{k in split z} A(m,k) * B(n,k) )
 //
-// The MLP's forward (Z = X W^T) and input-gradient (dX = dZ W, with W^T kept
-// as a K-major copy) products. Inputs stay fp32 in HBM; each operand x is
-// split as hi = x with the low 13 mantissa bits ignored (what kind::tf32
-// reads) and lo = x - hi, and three tcgen05.mma per k-step accumulate
-// A*B + A*B_lo + A_lo*B in a TMEM fp32 accumulator (the dropped lo*lo term is
-// ~2^-21 relative): fp32-level accuracy at tensor-core rate.
+// Operands stay fp32 in HBM and are read by TMA in either major order:
+//   K-major  (X[row][k], k contiguous):   the forward Z = X W^T and the
+//            input gradient dX = dZ W (with W^T kept K-major);
+//   MN-major (X[k][row], row contiguous): the weight gradient dW = dZ^T X, whose
+//            contraction runs over the batch.
+// Each operand tile x is split in shared memory into hi = tf32_rn(x) and
+// lo = x - hi; three tcgen05.mma per k-step accumulate hi*hi + hi*lo + lo*hi
+// (the dropped lo*lo term is ~2^-21 relative). The tensor-core accumulator's
+// adds are not IEEE round-to-nearest (its error grows with K), so every
+// TC_CH k-blocks the MMA switches between two TMEM accumulators and the
+// epilogue warps fold the finished one into fp32 registers with RN adds:
+// fp32-level accuracy, independent of K, at tensor-core rate.
 //
-// CTA = one 128 x BN output tile, 192 threads, warp-specialised:
-//   warp 0    TMA producer: A tile (128x32) + B, B_lo tiles (BNx32) per stage,
-//             128B-swizzled (the canonical K-major SW128 UMMA layout)
+// CTA = one 128 x 128 output tile of one K split, 192 threads:
+//   warp 0    TMA producer (128B-swizzled tiles, canonical UMMA SW128 layouts)
 //   warp 1    TMEM allocator + single-thread MMA issuer (tcgen05.mma/commit)
-//   warps 2-5 A_lo converters (smem -> smem, fence.proxy.async), then the
-//             epilogue (tcgen05.ld 32x32b -> bias/activation/derivative -> HBM)
-// Pipelines: full[s] (TMA tx bytes) -> conv[s] (128 arrivals) -> MMA ->
-// empty[s] (tcgen05.commit) back to the producer; done -> epilogue.
+//   warps 2-5 hi/lo splitters (smem -> smem, fence.proxy.async), chunk
+//             drains (tcgen05.ld 32x32b) and the epilogue (bias/activation/
+//             derivative/pooling coefficient -> HBM)
+// Pipelines: full[s] (TMA tx) -> conv[s] (128 arrivals) -> MMA -> empty[s]
+// (tcgen05.commit); tfull[b] (commit) -> drain -> tempty[b] (128 arrivals).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -29,10 +35,10 @@
 namespace kp {
 namespace {
 
-constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32, TC_STAGES = 3;
+constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32, TC_STAGES = 3, TC_CH = 4;
 constexpr int TC_THREADS = 192;
-constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;   // 16 KB
-constexpr uint32_t B_BYTES = TC_BN * TC_BK * 4;   // 16 KB
+constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
+constexpr uint32_t B_BYTES = TC_BN * TC_BK * 4;  // 16 KB
 constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
 constexpr uint32_t SMEM_BYTES = TC_STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
@@ -77,31 +83,42 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// K-major, 128B-swizzled UMMA shared-memory descriptor (sm100 version bits)
-__device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
+// UMMA shared-memory descriptors (sm100 version bits).
+//  K-major : SWIZZLE_128B; 8-row groups of 128 B rows at SBO = 1024 B.
+//  MN-major: tf32 MN-major operands only come in SWIZZLE_128B_BASE32B (32 B
+//            swizzle atoms, TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 32-element
+//            (128 B) MN atoms at LBO = 4096 B (one 32x32 TMA box), 4-row K
+//            groups at SBO = 512 B.
+template <bool MN>
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);       // start address
-  d |= (uint64_t)1 << 16;                        // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;              // SBO: 8 rows x 128 B
-  d |= (uint64_t)1 << 46;                        // version = 1 (Blackwell)
-  d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(MN ? (4096 >> 4) : 1) << 16;
+  d |= (uint64_t)(MN ? (512 >> 4) : (1024 >> 4)) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(MN ? 1 : 2) << 61;
   return d;
 }
-
-// instruction descriptor: D f32, A/B tf32, K-major both, M=128, N=TC_BN
-constexpr uint32_t idesc_tf32() {
-  return (1u << 4)            // c_format F32
-         | (2u << 7)          // a_format TF32
-         | (2u << 10)         // b_format TF32
-         | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+// byte offset of UMMA k-step kk (8 tf32) inside a stage tile
+template <bool MN>
+__device__ __forceinline__ uint32_t kstep_off(int kk) {
+  return MN ? (uint32_t)kk * 1024u : (uint32_t)kk * 32u;
 }
 
+// instruction descriptor: D f32, A/B tf32, M=128, N=TC_BN, per-operand major
+template <bool AMN, bool BMN>
+__host__ __device__ constexpr uint32_t idesc_tf32() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((AMN ? 1u : 0u) << 15) | ((BMN ? 1u : 0u) << 16) |
+         ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+}
+
+template <bool AMN, bool BMN>
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc_tf32()), "r"(accum));
+      "l"(a), "l"(b), "r"(idesc_tf32<AMN, BMN>()), "r"(accum));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -109,8 +126,7 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// x -> (hi, lo): hi = tf32 round-to-nearest of x, lo = x - hi (exact in fp32);
-// the MMA reads lo as tf32 too, leaving ~2^-21 relative error per product.
+// x -> (hi, lo): hi = tf32 round-to-nearest of x, lo = x - hi (exact in fp32)
 __device__ __forceinline__ void split3(float& x, float& lo) {
   uint32_t h;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
@@ -137,30 +153,54 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 
-// Two-level accumulation: the tensor-core accumulator adds are not IEEE
-// round-to-nearest, so its error grows ~linearly with K. Every TC_CH k-blocks
-// (128 of K) the MMA switches to the other of two TMEM accumulators and the
-// epilogue warps fold the finished chunk into fp32 registers with RN adds.
-constexpr int TC_CH = 4;
+// TMA a 128-row x 32-k operand tile into smem (one K-major box, or four
+// 32x32 MN-major boxes at LBO spacing)
+template <bool MN>
+__device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int k0,
+                                          int r0) {
+  if (MN) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tma_load_2d(dst + i * 4096, map, bar, r0 + 32 * i, k0);
+  } else {
+    tma_load_2d(dst, map, bar, k0, r0);
+  }
+}
 
+__device__ __forceinline__ void split_tile(uint8_t* tile, uint8_t* lo_tile, int ct) {
+  float4* hi = reinterpret_cast<float4*>(tile);
+  float4* lo = reinterpret_cast<float4*>(lo_tile);
+#pragma unroll
+  for (int i = 0; i < (int)(A_BYTES / 16 / 128); ++i) {
+    float4 x = hi[ct + 128 * i], l;
+    split3(x.x, l.x);
+    split3(x.y, l.y);
+    split3(x.z, l.z);
+    split3(x.w, l.w);
+    hi[ct + 128 * i] = x;
+    lo[ct + 128 * i] = l;
+  }
+}
+
+template <bool AMN, bool BMN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmBlo, int M, int N, int K, float* __restrict__ C,
-              int ldc, GemmEpi ep) {
+    k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+              int N, int K, int kps, float* __restrict__ C, int ldc, GemmEpi ep) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES);
   uint64_t* full = bars;
   uint64_t* conv = bars + TC_STAGES;
   uint64_t* empty = bars + 2 * TC_STAGES;
-  uint64_t* tfull = bars + 3 * TC_STAGES;       // [2] chunk accumulated (MMA commit)
-  uint64_t* tempty = bars + 3 * TC_STAGES + 2;  // [2] chunk drained (128 arrivals)
+  uint64_t* tfull = bars + 3 * TC_STAGES;
+  uint64_t* tempty = bars + 3 * TC_STAGES + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * TC_STAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * TC_BN;
-  const int nk = (K + TC_BK - 1) / TC_BK;
+  const int kbeg = blockIdx.z * kps, kend = min(K, kbeg + kps);
+  const int nk = kend > kbeg ? (kend - kbeg + TC_BK - 1) / TC_BK : 0;
   const int nchunks = (nk + TC_CH - 1) / TC_CH;
+  C += (size_t)blockIdx.z * M * ldc;
   auto sA = [&](int s) { return smem + s * STAGE_BYTES; };
   auto sAlo = [&](int s) { return smem + s * STAGE_BYTES + A_BYTES; };
   auto sB = [&](int s) { return smem + s * STAGE_BYTES + 2 * A_BYTES; };
@@ -193,15 +233,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBlo)) : "memory");
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % TC_STAGES;
         const uint32_t ph = (kb / TC_STAGES) & 1;
         if (kb >= TC_STAGES) mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], A_BYTES + 2 * B_BYTES);
-        tma_load_2d(sA(s), &tmA, &full[s], kb * TC_BK, m0);
-        tma_load_2d(sB(s), &tmB, &full[s], kb * TC_BK, n0);
-        tma_load_2d(sBlo(s), &tmBlo, &full[s], kb * TC_BK, n0);
+        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+        load_tile<AMN>(sA(s), &tmA, &full[s], kbeg + kb * TC_BK, m0);
+        load_tile<BMN>(sB(s), &tmB, &full[s], kbeg + kb * TC_BK, n0);
       }
     }
   } else if (warp == 1) {
@@ -211,7 +249,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t ph = (kb / TC_STAGES) & 1;
         const int c = kb / TC_CH, buf = c & 1, kin = kb % TC_CH;
         if (kin == 0 && c >= 2) mbar_wait(&tempty[buf], ((c >> 1) - 1) & 1);
-        mbar_wait(&full[s], ph);
         mbar_wait(&conv[s], ph);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(buf * TC_BN);
@@ -219,10 +256,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t b = smem_u32(sB(s)), blo = smem_u32(sBlo(s));
 #pragma unroll
         for (int kk = 0; kk < TC_BK / 8; ++kk) {
-          const uint32_t off = kk * 32;  // 8 tf32 = 32 B along K inside the swizzle atom
-          mma_tf32(d, sdesc_k_sw128(a + off), sdesc_k_sw128(b + off), (kin | kk) != 0);
-          mma_tf32(d, sdesc_k_sw128(a + off), sdesc_k_sw128(blo + off), 1);
-          mma_tf32(d, sdesc_k_sw128(alo + off), sdesc_k_sw128(b + off), 1);
+          const uint32_t oa = kstep_off<AMN>(kk), ob = kstep_off<BMN>(kk);
+          mma_tf32<AMN, BMN>(d, sdesc<AMN>(a + oa), sdesc<BMN>(b + ob), (kin | kk) != 0);
+          mma_tf32<AMN, BMN>(d, sdesc<AMN>(a + oa), sdesc<BMN>(blo + ob), 1);
+          mma_tf32<AMN, BMN>(d, sdesc<AMN>(alo + oa), sdesc<BMN>(b + ob), 1);
         }
         mma_commit(&empty[s]);
         if (kin == TC_CH - 1 || kb == nk - 1) mma_commit(&tfull[buf]);
@@ -250,31 +287,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&tempty[buf]);
     };
-    // ---- A hi/lo converters, draining finished chunks as they go ----
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % TC_STAGES;
       const uint32_t ph = (kb / TC_STAGES) & 1;
       mbar_wait(&full[s], ph);
-      float4* hi = reinterpret_cast<float4*>(sA(s));
-      float4* lo = reinterpret_cast<float4*>(sAlo(s));
-#pragma unroll
-      for (int i = 0; i < (int)(A_BYTES / 16 / 128); ++i) {
-        float4 x = hi[ct + 128 * i], l;
-        split3(x.x, l.x);
-        split3(x.y, l.y);
-        split3(x.z, l.z);
-        split3(x.w, l.w);
-        hi[ct + 128 * i] = x;
-        lo[ct + 128 * i] = l;
-      }
+      split_tile(sA(s), sAlo(s), ct);
+      split_tile(sB(s), sBlo(s), ct);
       fence_proxy_async();
       mbar_arrive(&conv[s]);
       while (drained < kb / TC_CH) drain(drained++);
     }
     while (drained < nchunks) drain(drained++);
     // ---- epilogue: registers -> HBM ----
-    const int row = q * 32 + lane;
-    const int m = m0 + row;
+    const int m = m0 + q * 32 + lane;
     if (m < M) {
       float* crow = C + (size_t)m * ldc;
 #pragma unroll
@@ -319,17 +344,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// row-major [rows][cols] fp32 with leading dimension ld, box = box_rows x 32 cols
+// row-major [rows][cols] fp32 (leading dimension ld) with a box of
+// box_rows x 32 columns, 128B swizzle
 bool make_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t cols, uint64_t ld,
-              uint32_t box_rows) {
+              uint32_t box_rows, bool atom32 = false) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {ld * 4};
-  cuuint32_t box[2] = {(cuuint32_t)TC_BK, box_rows};
+  cuuint32_t box[2] = {32, box_rows};
   cuuint32_t es[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
+            atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -341,6 +368,28 @@ __global__ void k_split(const float* __restrict__ x, float* __restrict__ hi, flo
     hi[i] = v;
     lo[i] = l;
   }
+}
+
+template <bool AMN, bool BMN>
+int launch(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
+           int splits, const GemmEpi& ep, cudaStream_t s) {
+  CUtensorMap ta, tb;
+  // K-major: [rows][K] with 128-row boxes; MN-major: [K][rows] with 32x32 boxes
+  const bool ok = (AMN ? make_map(&ta, A, K, M, lda, 32, true) : make_map(&ta, A, M, K, lda, TC_BM)) &&
+                  (BMN ? make_map(&tb, B, K, N, ldb, 32, true) : make_map(&tb, B, N, K, ldb, TC_BN));
+  KP_CHECK(ok, kErrCuda, "cuTensorMapEncodeTiled failed");
+  static bool attr = false;
+  if (!attr) {
+    KP_CUDA(cudaFuncSetAttribute(k_tc_gemm<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM_BYTES));
+    attr = true;
+  }
+  int kps = (K + splits - 1) / splits;
+  kps = (kps + TC_BK - 1) / TC_BK * TC_BK;
+  const unsigned nz = ceil_div(K, kps);
+  dim3 grid(ceil_div(N, TC_BN), ceil_div(M, TC_BM), nz);
+  k_tc_gemm<AMN, BMN><<<grid, TC_THREADS, SMEM_BYTES, s>>>(ta, tb, M, N, K, kps, C, ldc, ep); ::kp::count_launch();
+  return (int)nz;
 }
 
 }  // namespace
@@ -365,20 +414,24 @@ void split_hilo(const float* x, float* hi, float* lo, size_t n, cudaStream_t s) 
   k_split<<<g ? g : 1, 256, 0, s>>>(x, hi, lo, n); ::kp::count_launch();
 }
 
-// C = epi(A[M][K] . B[N][K]^T); (B_hi, B_lo) = split_hilo(B) precomputed by the caller.
-void tc_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, const float* Blo,
-                int ldb, float* C, int ldc, const GemmEpi& ep, cudaStream_t s) {
-  CUtensorMap ta, tb, tbl;
-  KP_CHECK(make_map(&ta, A, M, K, lda, TC_BM) && make_map(&tb, B, N, K, ldb, TC_BN) &&
-               make_map(&tbl, Blo, N, K, ldb, TC_BN),
-           kErrCuda, "cuTensorMapEncodeTiled failed");
-  static bool attr = false;
-  if (!attr) {
-    KP_CUDA(cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr = true;
-  }
-  dim3 grid(ceil_div(N, TC_BN), ceil_div(M, TC_BM));
-  k_tc_gemm<<<grid, TC_THREADS, SMEM_BYTES, s>>>(ta, tb, tbl, M, N, K, C, ldc, ep); ::kp::count_launch();
+int tc_splits(int M, int N, int K) {
+  const int tiles = (int)(ceil_div(M, TC_BM) * ceil_div(N, TC_BN));
+  const int sp = (2 * 148 + tiles - 1) / tiles;
+  const int max_sp = std::max(1, K / 512);  // >= 16 k-blocks per split
+  return std::max(1, std::min(sp, max_sp));
+}
+
+// C[m][n] = epi(sum_k A[m][k] B[n][k])   (both K-major)
+void tc_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+                int ldc, const GemmEpi& ep, cudaStream_t s) {
+  launch<false, false>(M, N, K, A, lda, B, ldb, C, ldc, 1, ep, s);
+}
+
+// C[z][m][n] = sum_{k in split z} A[k][m] B[k][n]   (both MN-major); returns #splits
+int tc_gemm_tn(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+               int ldc, int splits, cudaStream_t s) {
+  GemmEpi ep{0, 0, nullptr, nullptr, 0, nullptr, 1, 1};
+  return launch<true, true>(M, N, K, A, lda, B, ldb, C, ldc, splits, ep, s);
 }
 
 }  // namespace kp

@@ -87,7 +87,7 @@ void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_inverse
 // Deterministic segmented reduce of coefficient-scaled upstream rows by
 // unique key, times inv_n, then the sparse rule applied in place to the row.
 struct SegWs {
-  DevBuf partials;
+  DevBuf partials, qsums;
 };
 struct SparseRule {
   int rule;  // 0 adagrad, 1 adam
@@ -117,15 +117,25 @@ struct GemmEpi {
   const float* coeff;
   uint32_t S, e;
 };
-// tcgen05 3xTF32 GEMM: C = epi(A[M][K] . B[N][K]^T), (B, Blo) = split_hilo(B)
+// tcgen05 3xTF32 GEMMs (operands split hi/lo on the fly in shared memory)
 bool tc_gemm_supported(int M, int N, int K, const float* A, int lda, const float* B, int ldb);
-void tc_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, const float* Blo,
-                int ldb, float* C, int ldc, const GemmEpi& ep, cudaStream_t s);
+// C = epi(A[M][K] . B[N][K]^T)
+void tc_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+                int ldc, const GemmEpi& ep, cudaStream_t s);
+// C[z] = A[K][M]^T . B[K][N] over K split z (deterministic split-K partials); returns #splits
+int tc_gemm_tn(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+               int ldc, int splits, cudaStream_t s);
+int tc_splits(int M, int N, int K);
 void split_hilo(const float* x, float* hi, float* lo, size_t n, cudaStream_t s);
 bool tc_enabled();  // KP_GEMM=simt disables the tensor-core path
 // C = A . B^T on the SIMT fp32 path (reference engine for the tensor-core path)
 void simt_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
                   int ldc, cudaStream_t s);
+// C = A[K][M]^T . B[K][N] on the SIMT fp32 path
+void simt_gemm_tn(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+                  int ldc, cudaStream_t s);
+// out[i] = sum_z part[z][i] in z order
+void reduce_splits(const float* part, int splits, size_t n, float* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- MLP ----
 struct MlpShape {

@@ -205,24 +205,51 @@ __global__ void k_reduce_splits(const float* __restrict__ part, int splits, size
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
     float v = part[i];
-    for (int z = 1; z < splits; ++z) v = __fadd_rn(v, part[(size_t)z * n + i]);
+    int z = 1;
+    for (; z + 4 <= splits; z += 4) {  // loads in flight, adds in z order
+      const float a = part[(size_t)z * n + i], b = part[(size_t)(z + 1) * n + i];
+      const float c = part[(size_t)(z + 2) * n + i], d = part[(size_t)(z + 3) * n + i];
+      v = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(v, a), b), c), d);
+    }
+    for (; z < splits; ++z) v = __fadd_rn(v, part[(size_t)z * n + i]);
     out[i] = v;
   }
 }
 
 // column sums (optionally weighted): partial[c][n] = sum_{b in chunk c} w[b]*X[b][n]
+// column sums (optionally weighted): part[c][n] = sum_{b in chunk c} w[b]*X[b][n];
+// block (32 columns x 8 row lanes), fixed-order combine of the 8 lanes.
+constexpr int COLSUM_ROWS = 512;
 __global__ void k_colsum_part(const float* __restrict__ X, const float* __restrict__ w, int B,
-                              int N, int rows_per_chunk, float* __restrict__ part) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+                              int N, float* __restrict__ part) {
+  __shared__ float red[8][33];
+  const int n = blockIdx.x * 32 + threadIdx.x;
   const int c = blockIdx.y;
-  if (n >= N) return;
-  const int b0 = c * rows_per_chunk, b1 = min(B, b0 + rows_per_chunk);
+  const int b0 = c * COLSUM_ROWS, b1 = min(B, b0 + COLSUM_ROWS);
   float acc = 0.f;
-  for (int b = b0; b < b1; ++b) {
-    const float x = X[(size_t)b * N + n];
-    acc = w ? fmaf(w[b], x, acc) : __fadd_rn(acc, x);
+  if (n < N) {
+    int b = b0 + threadIdx.y;
+    for (; b + 24 < b1; b += 32) {  // 4 independent loads in flight
+      float x0 = X[(size_t)b * N + n], x1 = X[(size_t)(b + 8) * N + n];
+      float x2 = X[(size_t)(b + 16) * N + n], x3 = X[(size_t)(b + 24) * N + n];
+      if (w) {
+        x0 = __fmul_rn(w[b], x0), x1 = __fmul_rn(w[b + 8], x1);
+        x2 = __fmul_rn(w[b + 16], x2), x3 = __fmul_rn(w[b + 24], x3);
+      }
+      acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, x0), x1), x2), x3);
+    }
+    for (; b < b1; b += 8) {
+      const float x = X[(size_t)b * N + n];
+      acc = __fadd_rn(acc, w ? __fmul_rn(w[b], x) : x);
+    }
   }
-  part[(size_t)c * N + n] = acc;
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && n < N) {
+    float t = red[0][threadIdx.x];
+    for (int i = 1; i < 8; ++i) t = __fadd_rn(t, red[i][threadIdx.x]);
+    part[(size_t)c * N + n] = t;
+  }
 }
 
 // Head (out = 1): logit = b + w . a ; pred = sigmoid (model.cpp:34-38,118-123)
@@ -296,9 +323,17 @@ __global__ void k_head_bwd(const float* __restrict__ in, int B, int W, const flo
 // loss_sum += (sum / n) * n  -- the reference's loss_sum += bwd.loss * mb.size
 __global__ void k_loss_finalize(const double* __restrict__ part, int nparts, int n,
                                 double* __restrict__ loss_sum) {
+  // 32 lanes sum strided partials, then lane 0 combines them in lane order
   double t = 0.0;
-  for (int i = 0; i < nparts; ++i) t += part[i];
-  *loss_sum += (t / (double)n) * (double)n;
+  for (int i = threadIdx.x; i < nparts; i += 32) t += part[i];
+  __shared__ double s[32];
+  s[threadIdx.x] = t;
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    double u = 0.0;
+    for (int i = 0; i < 32; ++i) u += s[i];
+    *loss_sum += (u / (double)n) * (double)n;
+  }
 }
 
 unsigned grid_cap(uint64_t blocks) {
@@ -324,6 +359,16 @@ void simt_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, 
   gemm<true, true>(M, N, K, A, lda, B, ldb, C, ldc, 1, plain, s);
 }
 
+void simt_gemm_tn(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+                  int ldc, cudaStream_t s) {
+  EpiArgs plain{kStore, 0, nullptr, nullptr, 0, nullptr, 1, 1};
+  gemm<false, false>(M, N, K, A, lda, B, ldb, C, ldc, 1, plain, s);
+}
+
+void reduce_splits(const float* part, int splits, size_t n, float* out, cudaStream_t s) {
+  k_reduce_splits<<<grid_cap(ceil_div(n, 256)), 256, 0, s>>>(part, splits, n, out); ::kp::count_launch();
+}
+
 void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_t B,
                  float* d_preds, MlpWs& ws, cudaStream_t s) {
   if (B == 0) return;
@@ -335,10 +380,7 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
     EpiArgs ep{kBiasAct, m.activation, d_x + m.b_off[l], nullptr, 0, nullptr, 1, 1};
     const float* W = d_x + m.w_off[l];
     if (tc_enabled() && tc_gemm_supported(B, N, K, in, K, W, K)) {
-      float* whi = ws.whi.get<float>((size_t)N * K);
-      float* wlo = ws.wlo.get<float>((size_t)N * K);
-      split_hilo(W, whi, wlo, (size_t)N * K, s);
-      tc_gemm_nt(B, N, K, in, K, whi, wlo, K, out, N, ep, s);
+      tc_gemm_nt(B, N, K, in, K, W, K, out, N, ep, s);
     } else {
       gemm<true, true>(B, N, K, in, K, W, K, out, N, 1, ep, s);
     }
@@ -367,25 +409,19 @@ void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, c
              MlpWs& ws, cudaStream_t s) {
   if (tc_enabled() && tc_gemm_supported(B, K, N, dZ, N, W, N)) {
     float* wt = ws.wt.get<float>((size_t)N * K);
-    float* wthi = ws.wthi.get<float>((size_t)N * K);
-    float* wtlo = ws.wtlo.get<float>((size_t)N * K);
     dim3 g(ceil_div(K, 32), ceil_div(N, 32));
     k_transpose<<<g, dim3(32, 8), 0, s>>>(W, N, K, wt); ::kp::count_launch();
-    split_hilo(wt, wthi, wtlo, (size_t)N * K, s);
-    tc_gemm_nt(B, K, N, dZ, N, wthi, wtlo, N, out, K, ep, s);
+    tc_gemm_nt(B, K, N, dZ, N, wt, N, out, K, ep, s);
   } else {
     gemm<true, false>(B, K, N, dZ, N, W, K, out, K, 1, ep, s);
   }
 }
 
 void colsum(const float* X, const float* w, int B, int N, float* out, MlpWs& ws, cudaStream_t s) {
-  int chunks = (B + 511) / 512;
-  if (chunks > 64) chunks = 64;
-  if (chunks < 1) chunks = 1;
-  const int rpc = (B + chunks - 1) / chunks;
+  const int chunks = std::max(1, (B + COLSUM_ROWS - 1) / COLSUM_ROWS);
   float* part = ws.partials.get<float>((size_t)chunks * N);
-  dim3 g(ceil_div(N, 128), chunks);
-  k_colsum_part<<<g, 128, 0, s>>>(X, w, B, N, rpc, part); ::kp::count_launch();
+  dim3 g(ceil_div(N, 32), chunks);
+  k_colsum_part<<<g, dim3(32, 8), 0, s>>>(X, w, B, N, part); ::kp::count_launch();
   k_reduce_splits<<<grid_cap(ceil_div(N, 256)), 256, 0, s>>>(part, chunks, (size_t)N, out); ::kp::count_launch();
 }
 }  // namespace
@@ -419,7 +455,7 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
   k_head_bwd<<<hb, 256, 0, s>>>(layer_in(L - 1), B, W, d_x + m.w_off[L - 1],
                                  static_cast<const float*>(ws.logits.p), d_preds, d_labels,
                                  (float)B, delta, dprev, mode, m.activation, d_coeff, S, e, lossp); ::kp::count_launch();
-  k_loss_finalize<<<1, 1, 0, s>>>(lossp, hb, B, d_loss_sum); ::kp::count_launch();
+  k_loss_finalize<<<1, 32, 0, s>>>(lossp, hb, B, d_loss_sum); ::kp::count_launch();
   colsum(layer_in(L - 1), delta, B, W, d_grad + m.w_off[L - 1], ws, s);
   colsum(delta, nullptr, B, 1, d_grad + m.b_off[L - 1], ws, s);
   // ---- hidden layers, top down ----
@@ -429,9 +465,18 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
     float* dZ = static_cast<float*>(ws.dz[cur].p);
     const float* in = layer_in(l);
     // dW_l[o][i] = sum_b dZ[b][o] in[b][i]   (deterministic split-K)
-    const int sp = pick_splits(N, K, B);
     EpiArgs plain{kStore, 0, nullptr, nullptr, 0, nullptr, 1, 1};
-    if (sp == 1) {
+    if (tc_enabled() && tc_gemm_supported(N, K, B, dZ, N, in, K)) {
+      const int tsp = tc_splits(N, K, B);
+      if (tsp == 1) {
+        tc_gemm_tn(N, K, B, dZ, N, in, K, d_grad + m.w_off[l], K, 1, s);
+      } else {
+        float* part = ws.partials.get<float>((size_t)tsp * N * K);
+        const int got = tc_gemm_tn(N, K, B, dZ, N, in, K, part, K, tsp, s);
+        k_reduce_splits<<<grid_cap(ceil_div((uint64_t)N * K, 256)), 256, 0, s>>>(
+            part, got, (size_t)N * K, d_grad + m.w_off[l]); ::kp::count_launch();
+      }
+    } else if (const int sp = pick_splits(N, K, B); sp == 1) {
       gemm<false, false>(N, K, B, dZ, N, in, K, d_grad + m.w_off[l], K, 1, plain, s);
     } else {
       float* part = ws.partials.get<float>((size_t)sp * N * K);

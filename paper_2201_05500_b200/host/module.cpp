@@ -270,6 +270,28 @@ PYBIND11_MODULE(_kpsim_b200, m) {
         },
         py::arg("A"), py::arg("B"), py::arg("engine") = 0, py::arg("device") = 0);
 
+  m.def("gemm_tn",
+        [](Arr<float> A, Arr<float> B, int engine, int device) {
+          if (A.ndim() != 2 || B.ndim() != 2 || A.shape(0) != B.shape(0))
+            throw Error("gemm_tn: A[K][M], B[K][N] expected");
+          check(kp_set_device(device));
+          const int K = (int)A.shape(0), M = (int)A.shape(1), N = (int)B.shape(1);
+          void *da, *db, *dc;
+          check(kp_dev_alloc((size_t)M * K * 4, &da));
+          check(kp_dev_alloc((size_t)N * K * 4, &db));
+          check(kp_dev_alloc((size_t)M * N * 4, &dc));
+          int rc = kp_memcpy_h2d(da, A.data(), (size_t)M * K * 4);
+          if (rc == KP_OK) rc = kp_memcpy_h2d(db, B.data(), (size_t)N * K * 4);
+          if (rc == KP_OK)
+            rc = kp_gemm_tn((const float*)da, M, (const float*)db, N, (float*)dc, N, M, N, K, engine, nullptr);
+          Arr<float> C({(py::ssize_t)M, (py::ssize_t)N});
+          if (rc == KP_OK) rc = kp_memcpy_d2h(C.mutable_data(), dc, (size_t)M * N * 4);
+          for (void* p2 : {da, db, dc}) kp_dev_free(p2);
+          check(rc);
+          return C;
+        },
+        py::arg("A"), py::arg("B"), py::arg("engine") = 0, py::arg("device") = 0);
+
   // ---- comm ----
   m.def("comm_unique_id", [] {
     uint8_t id[128];

@@ -290,3 +290,19 @@ def test_tcgen05_gemm_fp32_accuracy(kp, M, N, K):
     assert err_simt < 5e-5
     # 3xTF32 keeps fp32-level accuracy: within a small factor of the fp32 SIMT path
     assert err_tc < 3 * err_simt + 2e-6, (err_tc, err_simt)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 6400, 4096), (128, 256, 65536), (40, 100, 300)])
+def test_tcgen05_gemm_tn_fp32_accuracy(kp, M, N, K):
+    """MN-major operands (the weight gradient dZ^T X over the batch), split-K."""
+    rng = np.random.default_rng(M * N + K)
+    A = rng.standard_normal((K, M)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    want = A.astype(np.float64).T @ B.astype(np.float64)
+    scale = np.sqrt(K)
+    tc = kp.gemm_tn(A, B, engine=2)
+    simt = kp.gemm_tn(A, B, engine=1)
+    err_tc = np.max(np.abs(tc - want)) / scale
+    err_simt = np.max(np.abs(simt - want)) / scale
+    print(f"gemm_tn M={M} N={N} K={K}: normalized max err tc={err_tc:.3e} simt={err_simt:.3e}")
+    assert err_tc < 3 * err_simt + 2e-6, (err_tc, err_simt)
