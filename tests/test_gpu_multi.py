@@ -1,0 +1,47 @@
+"""GPU, G>=2 ranks (one process per GPU, NCCL all-to-all of keys/rows/grads and
+the k-step merge): the hash-sharded table must hold exactly the oracle's key
+set (owner = key % G, bit-exact) and training state must match the f64
+oracle's N=G workers within the stated tolerance. Skipped with < 2 GPUs."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpus():
+    try:
+        import paper_2201_05500_b200 as kp
+        return kp.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("k,S", [(1, 1), (3, 1), (2, 4)])
+def test_sharded_training_matches_oracle(tmp_path, k, S):
+    world = min(_gpus(), 4)
+    out = tmp_path / "res.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29577", os.path.join(ROOT, "tools", "mgpu_parity.py"),
+           str(out), str(k), str(S)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    assert res["owners_ok"]
+    assert res["keyset_equal"]
+    assert res["w_max_abs"] <= 2e-4
+    assert res["acc_max_rel"] <= 1e-3
+    assert res["x_max_abs"] <= 2e-4
+    for a, b in zip(res["loss"], res["oracle_loss"]):
+        assert abs(a - b) <= 1e-4
+    for a, b in zip(res["auc"], res["oracle_auc"]):
+        if a is not None and b == b:
+            assert abs(a - b) <= 5e-3
