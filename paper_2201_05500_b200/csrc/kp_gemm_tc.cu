@@ -181,10 +181,13 @@ __device__ __forceinline__ void split_tile(uint8_t* tile, uint8_t* lo_tile, int 
   }
 }
 
-template <bool AMN, bool BMN>
+// BPRE: B arrives pre-split (hi, lo) from HBM (weights, split once per step);
+// otherwise the splitter warps split B in shared memory like A.
+template <bool AMN, bool BMN, bool BPRE>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-              int N, int K, int kps, float* __restrict__ C, int ldc, GemmEpi ep) {
+    k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmBlo, int M, int N, int K, int kps,
+              float* __restrict__ C, int ldc, GemmEpi ep) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES);
@@ -233,13 +236,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      if (BPRE) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBlo)) : "memory");
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % TC_STAGES;
         const uint32_t ph = (kb / TC_STAGES) & 1;
         if (kb >= TC_STAGES) mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+        mbar_expect_tx(&full[s], A_BYTES + (BPRE ? 2 : 1) * B_BYTES);
         load_tile<AMN>(sA(s), &tmA, &full[s], kbeg + kb * TC_BK, m0);
         load_tile<BMN>(sB(s), &tmB, &full[s], kbeg + kb * TC_BK, n0);
+        if (BPRE) load_tile<BMN>(sBlo(s), &tmBlo, &full[s], kbeg + kb * TC_BK, n0);
       }
     }
   } else if (warp == 1) {
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t ph = (kb / TC_STAGES) & 1;
       mbar_wait(&full[s], ph);
       split_tile(sA(s), sAlo(s), ct);
-      split_tile(sB(s), sBlo(s), ct);
+      if (!BPRE) split_tile(sB(s), sBlo(s), ct);
       fence_proxy_async();
       mbar_arrive(&conv[s]);
       while (drained < kb / TC_CH) drain(drained++);
@@ -370,25 +375,29 @@ __global__ void k_split(const float* __restrict__ x, float* __restrict__ hi, flo
   }
 }
 
-template <bool AMN, bool BMN>
-int launch(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
-           int splits, const GemmEpi& ep, cudaStream_t s) {
-  CUtensorMap ta, tb;
+template <bool AMN, bool BMN, bool BPRE>
+int launch(int M, int N, int K, const float* A, int lda, const float* B, const float* Blo, int ldb,
+           float* C, int ldc, int splits, const GemmEpi& ep, cudaStream_t s) {
+  CUtensorMap ta, tb, tbl;
   // K-major: [rows][K] with 128-row boxes; MN-major: [K][rows] with 32x32 boxes
-  const bool ok = (AMN ? make_map(&ta, A, K, M, lda, 32, true) : make_map(&ta, A, M, K, lda, TC_BM)) &&
-                  (BMN ? make_map(&tb, B, K, N, ldb, 32, true) : make_map(&tb, B, N, K, ldb, TC_BN));
+  auto mk = [&](CUtensorMap* m, const float* p, bool mn, int rows, int ld) {
+    return mn ? make_map(m, p, K, rows, ld, 32, true) : make_map(m, p, rows, K, ld, TC_BM);
+  };
+  const bool ok = mk(&ta, A, AMN, M, lda) && mk(&tb, B, BMN, N, ldb) &&
+                  (!BPRE || mk(&tbl, Blo, BMN, N, ldb));
+  if (!BPRE) tbl = tb;
   KP_CHECK(ok, kErrCuda, "cuTensorMapEncodeTiled failed");
   static bool attr = false;
   if (!attr) {
-    KP_CUDA(cudaFuncSetAttribute(k_tc_gemm<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 SMEM_BYTES));
+    KP_CUDA(cudaFuncSetAttribute(k_tc_gemm<AMN, BMN, BPRE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     attr = true;
   }
   int kps = (K + splits - 1) / splits;
   kps = (kps + TC_BK - 1) / TC_BK * TC_BK;
   const unsigned nz = ceil_div(K, kps);
   dim3 grid(ceil_div(N, TC_BN), ceil_div(M, TC_BM), nz);
-  k_tc_gemm<AMN, BMN><<<grid, TC_THREADS, SMEM_BYTES, s>>>(ta, tb, M, N, K, kps, C, ldc, ep); ::kp::count_launch();
+  k_tc_gemm<AMN, BMN, BPRE><<<grid, TC_THREADS, SMEM_BYTES, s>>>(ta, tb, tbl, M, N, K, kps, C, ldc, ep); ::kp::count_launch();
   return (int)nz;
 }
 
@@ -414,24 +423,38 @@ void split_hilo(const float* x, float* hi, float* lo, size_t n, cudaStream_t s) 
   k_split<<<g ? g : 1, 256, 0, s>>>(x, hi, lo, n); ::kp::count_launch();
 }
 
+// split-K count: best wave efficiency (CTAs / (waves * 148)) with >= 16
+// k-blocks per split; ties go to fewer splits (less partial traffic)
 int tc_splits(int M, int N, int K) {
   const int tiles = (int)(ceil_div(M, TC_BM) * ceil_div(N, TC_BN));
-  const int sp = (2 * 148 + tiles - 1) / tiles;
-  const int max_sp = std::max(1, K / 512);  // >= 16 k-blocks per split
-  return std::max(1, std::min(sp, max_sp));
+  const int max_sp = std::max(1, std::min(16, K / 512));
+  int best = 1;
+  double best_eff = 0;
+  for (int sp = 1; sp <= max_sp; ++sp) {
+    const int ctas = tiles * sp;
+    const int waves = (ctas + 147) / 148;
+    const double eff = (double)ctas / (waves * 148.0) - 0.004 * sp;
+    if (eff > best_eff + 1e-9) best_eff = eff, best = sp;
+  }
+  return best;
 }
 
-// C[m][n] = epi(sum_k A[m][k] B[n][k])   (both K-major)
+// C[m][n] = epi(sum_k A[m][k] B[n][k])   (both K-major; B split in smem)
 void tc_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
                 int ldc, const GemmEpi& ep, cudaStream_t s) {
-  launch<false, false>(M, N, K, A, lda, B, ldb, C, ldc, 1, ep, s);
+  launch<false, false, false>(M, N, K, A, lda, B, nullptr, ldb, C, ldc, 1, ep, s);
+}
+// same with (B, B_lo) = split_hilo(B) precomputed (weights)
+void tc_gemm_nt_pre(int M, int N, int K, const float* A, int lda, const float* Bhi, const float* Blo,
+                    int ldb, float* C, int ldc, const GemmEpi& ep, cudaStream_t s) {
+  launch<false, false, true>(M, N, K, A, lda, Bhi, Blo, ldb, C, ldc, 1, ep, s);
 }
 
 // C[z][m][n] = sum_{k in split z} A[k][m] B[k][n]   (both MN-major); returns #splits
 int tc_gemm_tn(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
                int ldc, int splits, cudaStream_t s) {
   GemmEpi ep{0, 0, nullptr, nullptr, 0, nullptr, 1, 1};
-  return launch<true, true>(M, N, K, A, lda, B, ldb, C, ldc, splits, ep, s);
+  return launch<true, true, false>(M, N, K, A, lda, B, nullptr, ldb, C, ldc, splits, ep, s);
 }
 
 }  // namespace kp

@@ -122,6 +122,8 @@ bool tc_gemm_supported(int M, int N, int K, const float* A, int lda, const float
 // C = epi(A[M][K] . B[N][K]^T)
 void tc_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
                 int ldc, const GemmEpi& ep, cudaStream_t s);
+void tc_gemm_nt_pre(int M, int N, int K, const float* A, int lda, const float* Bhi, const float* Blo,
+                    int ldb, float* C, int ldc, const GemmEpi& ep, cudaStream_t s);
 // C[z] = A[K][M]^T . B[K][N] over K split z (deterministic split-K partials); returns #splits
 int tc_gemm_tn(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
                int ldc, int splits, cudaStream_t s);

@@ -380,7 +380,10 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
     EpiArgs ep{kBiasAct, m.activation, d_x + m.b_off[l], nullptr, 0, nullptr, 1, 1};
     const float* W = d_x + m.w_off[l];
     if (tc_enabled() && tc_gemm_supported(B, N, K, in, K, W, K)) {
-      tc_gemm_nt(B, N, K, in, K, W, K, out, N, ep, s);
+      float* whi = ws.whi.get<float>((size_t)N * K);
+      float* wlo = ws.wlo.get<float>((size_t)N * K);
+      split_hilo(W, whi, wlo, (size_t)N * K, s);
+      tc_gemm_nt_pre(B, N, K, in, K, whi, wlo, K, out, N, ep, s);
     } else {
       gemm<true, true>(B, N, K, in, K, W, K, out, N, 1, ep, s);
     }
@@ -411,7 +414,10 @@ void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, c
     float* wt = ws.wt.get<float>((size_t)N * K);
     dim3 g(ceil_div(K, 32), ceil_div(N, 32));
     k_transpose<<<g, dim3(32, 8), 0, s>>>(W, N, K, wt); ::kp::count_launch();
-    tc_gemm_nt(B, K, N, dZ, N, wt, N, out, K, ep, s);
+    float* wthi = ws.wthi.get<float>((size_t)N * K);
+    float* wtlo = ws.wtlo.get<float>((size_t)N * K);
+    split_hilo(wt, wthi, wtlo, (size_t)N * K, s);
+    tc_gemm_nt_pre(B, K, N, dZ, N, wthi, wtlo, N, out, K, ep, s);
   } else {
     gemm<true, false>(B, K, N, dZ, N, W, K, out, K, 1, ep, s);
   }

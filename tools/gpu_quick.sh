@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout=240 --timeout-method=thread > gpurun_out/pytest_gpu.log 2>&1; echo rc=$?; grep -E "FAIL|passed|failed" gpurun_out/pytest_gpu.log | tail -6
+timeout 800 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; echo bench rc=$?
+tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['e2e']['value']), {k:round(v['ms_per_step'],3) for k,v in d['stages'].items()}, d['loss'], d['clocks'])"
