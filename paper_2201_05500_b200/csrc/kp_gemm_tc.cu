@@ -36,11 +36,10 @@ namespace kp {
 namespace {
 
 constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32, TC_STAGES = 3, TC_CH = 4;
-constexpr int TC_THREADS = 192;
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
 constexpr uint32_t B_BYTES = TC_BN * TC_BK * 4;  // 16 KB
 constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-constexpr uint32_t SMEM_BYTES = TC_STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t SMEM_BYTES = TC_STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -181,10 +180,23 @@ __device__ __forceinline__ void split_tile(uint8_t* tile, uint8_t* lo_tile, int 
   }
 }
 
+// Persistent, warp-specialised kernel: one CTA per SM walks work items
+// (m-block, n-block, k-split) w = blockIdx.x, +gridDim.x, ...; the smem
+// pipeline, the TMEM chunk buffers and their barriers run continuously across
+// work items, so the epilogue of one tile overlaps the mainloop of the next.
+//   warp 0      TMA producer
+//   warp 1      TMEM allocator + MMA issuer
+//   warps 2-5   hi/lo splitters (128 threads)
+//   warps 6-13  drain + epilogue: warp w owns TMEM lane quarter w%4 and column
+//               half (w-6)/4 -> 64 fp32 register accumulators per thread
 // BPRE: B arrives pre-split (hi, lo) from HBM (weights, split once per step);
-// otherwise the splitter warps split B in shared memory like A.
+// otherwise the splitters split B in shared memory like A.
+constexpr int TC_NBUF = 4;  // TMEM chunk buffers (4 x 128 columns = all 512)
+constexpr int TC_WARPS = 14;
+constexpr int TC_EPI_T = 256;  // drain/epilogue threads
+
 template <bool AMN, bool BMN, bool BPRE>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TC_WARPS * 32, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmBlo, int M, int N, int K, int kps,
               float* __restrict__ C, int ldc, GemmEpi ep) {
@@ -195,15 +207,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* conv = bars + TC_STAGES;
   uint64_t* empty = bars + 2 * TC_STAGES;
   uint64_t* tfull = bars + 3 * TC_STAGES;
-  uint64_t* tempty = bars + 3 * TC_STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * TC_STAGES + 4);
+  uint64_t* tempty = bars + 3 * TC_STAGES + TC_NBUF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * TC_STAGES + 2 * TC_NBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * TC_BN;
-  const int kbeg = blockIdx.z * kps, kend = min(K, kbeg + kps);
-  const int nk = kend > kbeg ? (kend - kbeg + TC_BK - 1) / TC_BK : 0;
-  const int nchunks = (nk + TC_CH - 1) / TC_CH;
-  C += (size_t)blockIdx.z * M * ldc;
+  const int mblocks = (M + TC_BM - 1) / TC_BM, nblocks = (N + TC_BN - 1) / TC_BN;
+  const int splits = (K + kps - 1) / kps;
+  const int works = mblocks * nblocks * splits;
+  // work w -> (n-block fastest, then m-block, then split): CTAs in flight share A rows
+  auto decode = [&](int w, int& m0, int& n0, int& z, int& nk) {
+    const int nb = w % nblocks, r = w / nblocks, mb = r % mblocks;
+    z = r / mblocks;
+    m0 = mb * TC_BM;
+    n0 = nb * TC_BN;
+    const int kbeg = z * kps, kend = min(K, kbeg + kps);
+    nk = kend > kbeg ? (kend - kbeg + TC_BK - 1) / TC_BK : 0;
+  };
   auto sA = [&](int s) { return smem + s * STAGE_BYTES; };
   auto sAlo = [&](int s) { return smem + s * STAGE_BYTES + A_BYTES; };
   auto sB = [&](int s) { return smem + s * STAGE_BYTES + 2 * A_BYTES; };
@@ -215,16 +234,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&conv[s], 128);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < TC_NBUF; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], TC_EPI_T);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(2 * TC_BN));
+                 "r"(TC_NBUF * TC_BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -237,102 +256,128 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
       if (BPRE) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBlo)) : "memory");
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % TC_STAGES;
-        const uint32_t ph = (kb / TC_STAGES) & 1;
-        if (kb >= TC_STAGES) mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], A_BYTES + (BPRE ? 2 : 1) * B_BYTES);
-        load_tile<AMN>(sA(s), &tmA, &full[s], kbeg + kb * TC_BK, m0);
-        load_tile<BMN>(sB(s), &tmB, &full[s], kbeg + kb * TC_BK, n0);
-        if (BPRE) load_tile<BMN>(sBlo(s), &tmBlo, &full[s], kbeg + kb * TC_BK, n0);
+      int g = 0;  // global k-block counter (stage pipeline)
+      for (int w = blockIdx.x; w < works; w += gridDim.x) {
+        int m0, n0, z, nk;
+        decode(w, m0, n0, z, nk);
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % TC_STAGES;
+          const uint32_t ph = (g / TC_STAGES) & 1;
+          if (g >= TC_STAGES) mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], A_BYTES + (BPRE ? 2 : 1) * B_BYTES);
+          const int k0 = z * kps + kb * TC_BK;
+          load_tile<AMN>(sA(s), &tmA, &full[s], k0, m0);
+          load_tile<BMN>(sB(s), &tmB, &full[s], k0, n0);
+          if (BPRE) load_tile<BMN>(sBlo(s), &tmBlo, &full[s], k0, n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % TC_STAGES;
-        const uint32_t ph = (kb / TC_STAGES) & 1;
-        const int c = kb / TC_CH, buf = c & 1, kin = kb % TC_CH;
-        if (kin == 0 && c >= 2) mbar_wait(&tempty[buf], ((c >> 1) - 1) & 1);
-        mbar_wait(&conv[s], ph);
-        tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(buf * TC_BN);
-        const uint32_t a = smem_u32(sA(s)), alo = smem_u32(sAlo(s));
-        const uint32_t b = smem_u32(sB(s)), blo = smem_u32(sBlo(s));
+      int g = 0, c = 0;  // global k-block and chunk counters
+      for (int w = blockIdx.x; w < works; w += gridDim.x) {
+        int m0, n0, z, nk;
+        decode(w, m0, n0, z, nk);
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % TC_STAGES;
+          const uint32_t ph = (g / TC_STAGES) & 1;
+          const int kin = kb % TC_CH, buf = c % TC_NBUF;
+          if (kin == 0 && c >= TC_NBUF) mbar_wait(&tempty[buf], ((c / TC_NBUF) - 1) & 1);
+          mbar_wait(&conv[s], ph);
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(buf * TC_BN);
+          const uint32_t a = smem_u32(sA(s)), alo = smem_u32(sAlo(s));
+          const uint32_t b = smem_u32(sB(s)), blo = smem_u32(sBlo(s));
 #pragma unroll
-        for (int kk = 0; kk < TC_BK / 8; ++kk) {
-          const uint32_t oa = kstep_off<AMN>(kk), ob = kstep_off<BMN>(kk);
-          mma_tf32<AMN, BMN>(d, sdesc<AMN>(a + oa), sdesc<BMN>(b + ob), (kin | kk) != 0);
-          mma_tf32<AMN, BMN>(d, sdesc<AMN>(a + oa), sdesc<BMN>(blo + ob), 1);
-          mma_tf32<AMN, BMN>(d, sdesc<AMN>(alo + oa), sdesc<BMN>(b + ob), 1);
+          for (int kk = 0; kk < TC_BK / 8; ++kk) {
+            const uint32_t oa = kstep_off<AMN>(kk), ob = kstep_off<BMN>(kk);
+            mma_tf32<AMN, BMN>(d, sdesc<AMN>(a + oa), sdesc<BMN>(b + ob), (kin | kk) != 0);
+            mma_tf32<AMN, BMN>(d, sdesc<AMN>(a + oa), sdesc<BMN>(blo + ob), 1);
+            mma_tf32<AMN, BMN>(d, sdesc<AMN>(alo + oa), sdesc<BMN>(b + ob), 1);
+          }
+          mma_commit(&empty[s]);
+          if (kin == TC_CH - 1 || kb == nk - 1) {
+            mma_commit(&tfull[buf]);
+            ++c;
+          }
         }
-        mma_commit(&empty[s]);
-        if (kin == TC_CH - 1 || kb == nk - 1) mma_commit(&tfull[buf]);
+      }
+    }
+  } else if (warp < 6) {
+    // ---- hi/lo splitters ----
+    const int ct = threadIdx.x - 64;
+    int g = 0;
+    for (int w = blockIdx.x; w < works; w += gridDim.x) {
+      int m0, n0, z, nk;
+      decode(w, m0, n0, z, nk);
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = g % TC_STAGES;
+        const uint32_t ph = (g / TC_STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        split_tile(sA(s), sAlo(s), ct);
+        if (!BPRE) split_tile(sB(s), sBlo(s), ct);
+        fence_proxy_async();
+        mbar_arrive(&conv[s]);
       }
     }
   } else {
-    const int ct = threadIdx.x - 64;
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    float acc[TC_BN];
+    // ---- drain + epilogue (256 threads) ----
+    const int q = warp & 3;               // TMEM lane quarter
+    const int half = (warp - 6) >> 2;     // column half of the 128-wide tile
+    int c = 0;
+    for (int w = blockIdx.x; w < works; w += gridDim.x) {
+      int m0, n0, z, nk;
+      decode(w, m0, n0, z, nk);
+      float acc[64];
 #pragma unroll
-    for (int j = 0; j < TC_BN; ++j) acc[j] = 0.f;
-    int drained = 0;
-    auto drain = [&](int c) {
-      const int buf = c & 1;
-      mbar_wait(&tfull[buf], (c >> 1) & 1);
-      tc_fence_after();
+      for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+      const int nch = (nk + TC_CH - 1) / TC_CH;
+      for (int ci = 0; ci < nch; ++ci, ++c) {
+        const int buf = c % TC_NBUF;
+        mbar_wait(&tfull[buf], (c / TC_NBUF) & 1);
+        tc_fence_after();
 #pragma unroll
-      for (int c0 = 0; c0 < TC_BN; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * TC_BN + c0), r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * TC_BN + half * 64 + c0), r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[c0 + j] = __fadd_rn(acc[c0 + j], __uint_as_float(r[j]));
-      }
-      tc_fence_before();
-      mbar_arrive(&tempty[buf]);
-    };
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % TC_STAGES;
-      const uint32_t ph = (kb / TC_STAGES) & 1;
-      mbar_wait(&full[s], ph);
-      split_tile(sA(s), sAlo(s), ct);
-      if (!BPRE) split_tile(sB(s), sBlo(s), ct);
-      fence_proxy_async();
-      mbar_arrive(&conv[s]);
-      while (drained < kb / TC_CH) drain(drained++);
-    }
-    while (drained < nchunks) drain(drained++);
-    // ---- epilogue: registers -> HBM ----
-    const int m = m0 + q * 32 + lane;
-    if (m < M) {
-      float* crow = C + (size_t)m * ldc;
-#pragma unroll
-      for (int j = 0; j < TC_BN; ++j) {
-        const int n = n0 + j;
-        if (n < N) {
-          float v = acc[j];
-          if (ep.mode == 1) v = act_fwd(ep.act, __fadd_rn(v, ep.bias[n]));
-          else if (ep.mode == 2) v = __fmul_rn(v, act_bwd(ep.act, ep.aux[(size_t)m * ep.ld_aux + n]));
-          else if (ep.mode == 3) v = __fmul_rn(v, ep.coeff[(size_t)m * ep.S + n / ep.e]);
-          acc[j] = v;
+          for (int j = 0; j < 32; ++j) acc[c0 + j] = __fadd_rn(acc[c0 + j], __uint_as_float(r[j]));
         }
+        tc_fence_before();
+        mbar_arrive(&tempty[buf]);
       }
-      if (n0 + TC_BN <= N && (ldc & 3) == 0) {
+      const int m = m0 + q * 32 + lane;
+      const int nb0 = n0 + half * 64;
+      if (m < M) {
+        float* crow = C + (size_t)z * M * ldc + (size_t)m * ldc;
 #pragma unroll
-        for (int j = 0; j < TC_BN; j += 4)
-          *reinterpret_cast<float4*>(crow + n0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-      } else {
+        for (int j = 0; j < 64; ++j) {
+          const int n = nb0 + j;
+          if (n < N) {
+            float v = acc[j];
+            if (ep.mode == 1) v = act_fwd(ep.act, __fadd_rn(v, ep.bias[n]));
+            else if (ep.mode == 2) v = __fmul_rn(v, act_bwd(ep.act, ep.aux[(size_t)m * ep.ld_aux + n]));
+            else if (ep.mode == 3) v = __fmul_rn(v, ep.coeff[(size_t)m * ep.S + n / ep.e]);
+            acc[j] = v;
+          }
+        }
+        if (nb0 + 64 <= N && (ldc & 3) == 0) {
 #pragma unroll
-        for (int j = 0; j < TC_BN; ++j)
-          if (n0 + j < N) crow[n0 + j] = acc[j];
+          for (int j = 0; j < 64; j += 4)
+            *reinterpret_cast<float4*>(crow + nb0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (nb0 + j < N) crow[nb0 + j] = acc[j];
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * TC_BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_NBUF * TC_BN));
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -396,8 +441,11 @@ int launch(int M, int N, int K, const float* A, int lda, const float* B, const f
   int kps = (K + splits - 1) / splits;
   kps = (kps + TC_BK - 1) / TC_BK * TC_BK;
   const unsigned nz = ceil_div(K, kps);
-  dim3 grid(ceil_div(N, TC_BN), ceil_div(M, TC_BM), nz);
-  k_tc_gemm<AMN, BMN, BPRE><<<grid, TC_THREADS, SMEM_BYTES, s>>>(ta, tb, tbl, M, N, K, kps, C, ldc, ep); ::kp::count_launch();
+  const uint64_t works = (uint64_t)ceil_div(N, TC_BN) * ceil_div(M, TC_BM) * nz;
+  static int sms = 0;
+  if (!sms) KP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const unsigned grid = (unsigned)std::min<uint64_t>(works, (uint64_t)sms);
+  k_tc_gemm<AMN, BMN, BPRE><<<grid, TC_WARPS * 32, SMEM_BYTES, s>>>(ta, tb, tbl, M, N, K, kps, C, ldc, ep); ::kp::count_launch();
   return (int)nz;
 }
 
