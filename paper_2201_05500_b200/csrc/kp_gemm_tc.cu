@@ -152,6 +152,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
 // TMA a 128-row x 32-k operand tile into smem (one K-major box, or four
 // 32x32 MN-major boxes at LBO spacing)
 template <bool MN>
@@ -165,18 +174,23 @@ __device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* map, 
   }
 }
 
+// 256 splitter threads: 4 float4 each per 16 KB tile (loads first for ILP)
 __device__ __forceinline__ void split_tile(uint8_t* tile, uint8_t* lo_tile, int ct) {
   float4* hi = reinterpret_cast<float4*>(tile);
   float4* lo = reinterpret_cast<float4*>(lo_tile);
+  constexpr int PER = (int)(A_BYTES / 16 / 256);
+  float4 x[PER];
 #pragma unroll
-  for (int i = 0; i < (int)(A_BYTES / 16 / 128); ++i) {
-    float4 x = hi[ct + 128 * i], l;
-    split3(x.x, l.x);
-    split3(x.y, l.y);
-    split3(x.z, l.z);
-    split3(x.w, l.w);
-    hi[ct + 128 * i] = x;
-    lo[ct + 128 * i] = l;
+  for (int i = 0; i < PER; ++i) x[i] = hi[ct + 256 * i];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    float4 l;
+    split3(x[i].x, l.x);
+    split3(x[i].y, l.y);
+    split3(x[i].z, l.z);
+    split3(x[i].w, l.w);
+    hi[ct + 256 * i] = x[i];
+    lo[ct + 256 * i] = l;
   }
 }
 
@@ -186,13 +200,14 @@ __device__ __forceinline__ void split_tile(uint8_t* tile, uint8_t* lo_tile, int 
 // work items, so the epilogue of one tile overlaps the mainloop of the next.
 //   warp 0      TMA producer
 //   warp 1      TMEM allocator + MMA issuer
-//   warps 2-5   hi/lo splitters (128 threads)
-//   warps 6-13  drain + epilogue: warp w owns TMEM lane quarter w%4 and column
-//               half (w-6)/4 -> 64 fp32 register accumulators per thread
+//   warps 2-9   hi/lo splitters (256 threads)
+//   warps 10-17 drain + epilogue: warp w owns TMEM lane quarter w%4 and column
+//               half (w-10)/4 -> 64 fp32 register accumulators per thread
 // BPRE: B arrives pre-split (hi, lo) from HBM (weights, split once per step);
 // otherwise the splitters split B in shared memory like A.
 constexpr int TC_NBUF = 4;  // TMEM chunk buffers (4 x 128 columns = all 512)
-constexpr int TC_WARPS = 14;
+constexpr int TC_WARPS = 18;
+constexpr int TC_SPLIT_T = 256;  // splitter threads
 constexpr int TC_EPI_T = 256;  // drain/epilogue threads
 
 template <bool AMN, bool BMN, bool BPRE>
@@ -231,7 +246,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 128);
+      mbar_init(&conv[s], TC_SPLIT_T);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < TC_NBUF; ++b) {
@@ -303,7 +318,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
         }
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < 10) {
     // ---- hi/lo splitters ----
     const int ct = threadIdx.x - 64;
     int g = 0;
@@ -323,7 +338,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   } else {
     // ---- drain + epilogue (256 threads) ----
     const int q = warp & 3;               // TMEM lane quarter
-    const int half = (warp - 6) >> 2;     // column half of the 128-wide tile
+    const int half = (warp - 10) >> 2;    // column half of the 128-wide tile
     int c = 0;
     for (int w = blockIdx.x; w < works; w += gridDim.x) {
       int m0, n0, z, nk;
@@ -337,12 +352,12 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
         mbar_wait(&tfull[buf], (c / TC_NBUF) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * TC_BN + half * 64 + c0), r);
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * TC_BN + half * 64 + c0), r);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int j = 0; j < 32; ++j) acc[c0 + j] = __fadd_rn(acc[c0 + j], __uint_as_float(r[j]));
+          for (int j = 0; j < 16; ++j) acc[c0 + j] = __fadd_rn(acc[c0 + j], __uint_as_float(r[j]));
         }
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
