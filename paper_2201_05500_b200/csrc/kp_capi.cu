@@ -115,7 +115,7 @@ struct kp_trainer {
   SegWs sg, sg_owner;
   MlpWs mlp;
   MergeWs mws;
-  DevBuf rows, bag_offs, bag_of_occ, pooled, inv_count, dpooled, preds, err, loss, check;
+  DevBuf rows, rowocc, bag_offs, bag_of_occ, pooled, inv_count, dpooled, preds, err, loss, check;
   DevBuf xbar, pred_keep, lossg;
   // exchange buffers (G > 1)
   DevBuf perm, pos, send_keys, recv_keys, owner_rows, owner_idx, send_rows, recv_rows, send_grads,
@@ -256,7 +256,13 @@ struct PullResult {
 
 PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   cudaStream_t s = tr->s;
-  dedup(sv.keys, sv.n_occ, tr->dd, s);
+  // bags first, so dedup can emit the bag of every sorted position
+  const uint32_t nb = sv.n_inst * tr->S;
+  uint32_t* bag_offs = tr->bag_offs.get<uint32_t>(nb + 1);
+  uint32_t* bag_of_occ = tr->bag_of_occ.get<uint32_t>(std::max<uint32_t>(sv.n_occ, 1));
+  uint32_t* err = tr->err.get<uint32_t>(4);
+  prepare_bags(sv.offs, sv.occ_base, sv.slots, sv.n_inst, tr->S, bag_offs, bag_of_occ, err, s);
+  dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ);
   tr->mark(0);
   const uint32_t U = tr->dd.n_unique;
   PullResult pr{};
@@ -315,15 +321,12 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
     pr.src = rrows;
     pr.idx = pos;
   }
-  // bags + pooling
-  const uint32_t nb = sv.n_inst * tr->S;
-  uint32_t* bag_offs = tr->bag_offs.get<uint32_t>(nb + 1);
-  uint32_t* bag_of_occ = tr->bag_of_occ.get<uint32_t>(std::max<uint32_t>(sv.n_occ, 1));
-  uint32_t* err = tr->err.get<uint32_t>(4);
-  prepare_bags(sv.offs, sv.occ_base, sv.slots, sv.n_inst, tr->S, bag_offs, bag_of_occ, err, s);
+  // pooling over the composed per-occurrence source rows
+  uint32_t* rowocc = tr->rowocc.get<uint32_t>(std::max<uint32_t>(sv.n_occ, 1));
+  compose(pr.idx, tr->dd.d_inverse, sv.n_occ, rowocc, s);
   float* pooled = tr->pooled.get<float>((size_t)std::max<uint32_t>(nb, 1) * tr->e);
   float* invc = tr->inv_count.get<float>(std::max<uint32_t>(nb, 1));
-  pool(bag_offs, nb, tr->dd.d_inverse, pr.idx, pr.src, tr->e, tr->cfg.pooling == 1, pooled, invc, s);
+  pool(bag_offs, nb, rowocc, pr.src, tr->e, tr->cfg.pooling == 1, pooled, invc, s);
   tr->mark(2);
   return pr;
 }
@@ -366,15 +369,14 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
                   (float)tr->cfg.sparse_beta2};
   const float inv_n = (float)(1.0 / (double)tr->N);
   if (tr->world == 1) {
-    seg_reduce_apply(tr->dd.d_seg, pr.U, tr->dd.sorted_vals, static_cast<const uint32_t*>(tr->bag_of_occ.p),
-                     sv.n_occ, dpooled, tr->e, inv_n, tr->tab.t, pr.idx, rule, nullptr, nullptr,
-                     tr->sg, s);
+    seg_reduce_apply(tr->dd.d_seg, pr.U, tr->dd.d_sorted_mapped, nullptr, sv.n_occ, dpooled, tr->e,
+                     inv_n, tr->tab.t, pr.idx, rule, nullptr, nullptr, tr->sg, s);
     tr->mark(4);
   } else {
     float* sgr = tr->send_grads.get<float>((size_t)std::max<uint32_t>(pr.U, 1) * tr->e);
-    seg_reduce_apply(tr->dd.d_seg, pr.U, tr->dd.sorted_vals, static_cast<const uint32_t*>(tr->bag_of_occ.p),
-                     sv.n_occ, dpooled, tr->e, 1.0f, nullptr, nullptr, rule, sgr,
-                     static_cast<const uint32_t*>(tr->pos.p), tr->sg, s);
+    seg_reduce_apply(tr->dd.d_seg, pr.U, tr->dd.d_sorted_mapped, nullptr, sv.n_occ, dpooled, tr->e,
+                     1.0f, nullptr, nullptr, rule, sgr, static_cast<const uint32_t*>(tr->pos.p),
+                     tr->sg, s);
     tr->mark(4);
     uint64_t Rn = 0;
     for (auto c : tr->cnt_recv) Rn += c;

@@ -103,44 +103,63 @@ struct Row {
   __device__ __forceinline__ int dim(int gl, int q) const { return V4 ? 4 * gl + q : gl + 32 * q; }
 };
 
+// Each group pools PB consecutive bags per iteration: their row loads are
+// independent, so PB rows are in flight even for one-feature bags (S slots of
+// one feature each); inside a bag rows are still summed in occurrence order.
+constexpr int PB = 4;
+
 template <int LPG, int NV, bool V4>
 __global__ void __launch_bounds__(256) k_pool(const uint32_t* __restrict__ bag_offs, uint32_t n_bags,
-                                              const uint32_t* __restrict__ inverse,
-                                              const uint32_t* __restrict__ idx,
+                                              const uint32_t* __restrict__ rowocc,
                                               const float* __restrict__ src, uint32_t e, int mean,
                                               float* __restrict__ pooled,
                                               float* __restrict__ inv_count) {
   const int gl = threadIdx.x % LPG;
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
   const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
-  for (uint64_t b = g0; b < n_bags; b += ng) {
-    const uint32_t o0 = bag_offs[b], o1 = bag_offs[b + 1];
-    Row<LPG, NV, V4> acc, r[4];
-    acc.zero();
-    uint32_t o = o0;
-    for (; o + 4 <= o1; o += 4) {
+  for (uint64_t b0 = g0 * PB; b0 < n_bags; b0 += ng * PB) {
+    uint32_t o[PB + 1];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t rr = idx[inverse[o + u]];
-        if (rr == kNoRow) r[u].zero();  // table full: error raised at the batch end
-        else r[u].load(src + (uint64_t)rr * e, gl, e);
+    for (int i = 0; i <= PB; ++i) o[i] = bag_offs[b0 + i < n_bags ? b0 + i : n_bags];
+    Row<LPG, NV, V4> acc[PB], r[PB];
+    uint32_t maxlen = 0;
+#pragma unroll
+    for (int i = 0; i < PB; ++i) {
+      acc[i].zero();
+      maxlen = max(maxlen, o[i + 1] - o[i]);
+    }
+    for (uint32_t j = 0; j < maxlen; ++j) {
+#pragma unroll
+      for (int i = 0; i < PB; ++i) {
+        if (o[i] + j < o[i + 1]) {
+          const uint32_t rr = rowocc[o[i] + j];
+          if (rr == kNoRow) r[i].zero();  // table full: error raised at the batch end
+          else r[i].load(src + (uint64_t)rr * e, gl, e);
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc.add(r[u]);  // occurrence order (model.cpp:93)
+      for (int i = 0; i < PB; ++i)
+        if (o[i] + j < o[i + 1]) acc[i].add(r[i]);  // occurrence order (model.cpp:93)
     }
-    for (; o < o1; ++o) {
-      const uint32_t rr = idx[inverse[o]];
-      if (rr == kNoRow) r[0].zero();
-      else r[0].load(src + (uint64_t)rr * e, gl, e);
-      acc.add(r[0]);
+#pragma unroll
+    for (int i = 0; i < PB; ++i) {
+      const uint64_t b = b0 + i;
+      if (b >= n_bags) break;
+      const uint32_t len = o[i + 1] - o[i];
+      if (mean) {
+        const float inv = len ? __fdiv_rn(1.f, (float)len) : 1.f;  // model.cpp:95-97
+        if (len) acc[i].scale(inv);
+        if (gl == 0) inv_count[b] = inv;
+      }
+      acc[i].store(pooled + b * e, gl, e);
     }
-    if (mean) {
-      const float inv = o1 > o0 ? __fdiv_rn(1.f, (float)(o1 - o0)) : 1.f;  // model.cpp:95-97
-      if (o1 > o0) acc.scale(inv);
-      if (gl == 0) inv_count[b] = inv;
-    }
-    acc.store(pooled + b * e, gl, e);
   }
+}
+
+__global__ void k_compose(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ inverse,
+                          uint32_t n, uint32_t* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = idx[inverse[i]];
 }
 
 // ---- segmented reduce + sparse rule ---------------------------------------
@@ -200,12 +219,16 @@ __device__ __forceinline__ uint32_t src_row(const SegArgs& a, uint32_t p) {
 template <int LPG, int NV, bool V4>
 __device__ __forceinline__ void sum_range(const SegArgs& a, uint32_t p, uint32_t q,
                                           Row<LPG, NV, V4>& acc, int gl) {
-  Row<LPG, NV, V4> r[4];
-  for (; p + 4 <= q; p += 4) {
+  constexpr int UR = V4 ? 8 : 4;  // rows in flight per group
+  Row<LPG, NV, V4> r[UR];
+  for (; p + UR <= q; p += UR) {
+    uint32_t sr[UR];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) r[u].load(a.rows_src + (uint64_t)src_row(a, p + u) * a.e, gl, a.e);
+    for (int u = 0; u < UR; ++u) sr[u] = src_row(a, p + u);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc.add(r[u]);
+    for (int u = 0; u < UR; ++u) r[u].load(a.rows_src + (uint64_t)sr[u] * a.e, gl, a.e);
+#pragma unroll
+    for (int u = 0; u < UR; ++u) acc.add(r[u]);
   }
   for (; p < q; ++p) {
     r[0].load(a.rows_src + (uint64_t)src_row(a, p) * a.e, gl, a.e);
@@ -328,11 +351,11 @@ void launch_seg(const SegArgs& a, const TView& t, float* Q, cudaStream_t s) {
 }
 
 template <int LPG, int NV, bool V4>
-void launch_pool(const uint32_t* bag_offs, uint32_t n_bags, const uint32_t* inverse,
-                 const uint32_t* idx, const float* src, uint32_t e, bool mean, float* pooled,
-                 float* inv_count, cudaStream_t s) {
-  k_pool<LPG, NV, V4><<<grid_cap(((uint64_t)n_bags * LPG + 255) / 256), 256, 0, s>>>(
-      bag_offs, n_bags, inverse, idx, src, e, mean ? 1 : 0, pooled, inv_count); ::kp::count_launch();
+void launch_pool(const uint32_t* bag_offs, uint32_t n_bags, const uint32_t* rowocc,
+                 const float* src, uint32_t e, bool mean, float* pooled, float* inv_count,
+                 cudaStream_t s) {
+  k_pool<LPG, NV, V4><<<grid_cap(((uint64_t)(n_bags + PB - 1) / PB * LPG + 255) / 256), 256, 0, s>>>(
+      bag_offs, n_bags, rowocc, src, e, mean ? 1 : 0, pooled, inv_count); ::kp::count_launch();
 }
 
 // Dispatch on the embedding width: float4 groups for e in {4,8,...,128},
@@ -386,11 +409,17 @@ void prepare_bags(const uint32_t* d_offs, uint32_t occ_base, const uint16_t* d_s
       d_offs, occ_base, d_slots, n_inst, S, d_bag_offs, d_bag_of_occ, d_err); ::kp::count_launch();
 }
 
-void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_inverse,
-          const uint32_t* d_idx, const float* d_src, uint32_t e, bool mean, float* d_pooled,
-          float* d_inv_count, cudaStream_t s) {
+void compose(const uint32_t* d_idx, const uint32_t* d_inverse, uint32_t n, uint32_t* d_out,
+             cudaStream_t s) {
+  if (n == 0) return;
+  k_compose<<<grid_cap(((uint64_t)n + 255) / 256), 256, 0, s>>>(d_idx, d_inverse, n, d_out); ::kp::count_launch();
+}
+
+void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_row_of_occ,
+          const float* d_src, uint32_t e, bool mean, float* d_pooled, float* d_inv_count,
+          cudaStream_t s) {
   if (n_bags == 0) return;
-  dispatch_e<PoolF>(e, d_bag_offs, n_bags, d_inverse, d_idx, d_src, e, mean, d_pooled, d_inv_count, s);
+  dispatch_e<PoolF>(e, d_bag_offs, n_bags, d_row_of_occ, d_src, e, mean, d_pooled, d_inv_count, s);
 }
 
 void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* d_sorted_vals,

@@ -11,7 +11,7 @@ namespace kp {
 struct DedupWs {
   DevBuf keys_a, keys_b, vals_a, vals_b;  // radix ping-pong
   DevBuf counts, totals, minmax, bcount, scalars;
-  DevBuf unique, inverse, seg;
+  DevBuf unique, inverse, seg, mapped;
   // results of the last run (device pointers into the buffers above)
   const uint64_t* sorted_keys = nullptr;
   const uint32_t* sorted_vals = nullptr;  // occurrence index per sorted position
@@ -19,12 +19,16 @@ struct DedupWs {
   uint32_t* d_inverse = nullptr;          // [n] occurrence -> unique index
   uint32_t* d_seg = nullptr;              // [U+1] segment starts in sorted order
   uint32_t* d_nunique = nullptr;          // device scalar U
+  uint32_t* d_sorted_mapped = nullptr;    // occ_map[sorted_vals[p]] (when requested)
   uint32_t n = 0, n_unique = 0;
 };
 
 // Radix sort (stable) of (key, occurrence index) + unique + inverse + segment
 // starts. Writes U to ws.n_unique (host; one sync) and ws.d_nunique.
-void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s);
+// d_occ_map (optional): per-occurrence map materialised in sorted order
+// (ws.d_sorted_mapped[p] = occ_map[sorted_vals[p]]), e.g. the bag of each occurrence.
+void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
+           const uint32_t* d_occ_map = nullptr);
 
 // Stable bucket of ascending unique keys by owner = key % G.
 // perm[i] = unique index placed at bucket slot i; pos[u] = slot of unique u;
@@ -80,10 +84,13 @@ void table_gather(const Table* t, const uint32_t* d_rows, uint32_t n, float* d_w
 void prepare_bags(const uint32_t* d_offs, uint32_t occ_base, const uint16_t* d_slots,
                   uint32_t n_inst, uint32_t S, uint32_t* d_bag_offs, uint32_t* d_bag_of_occ,
                   uint32_t* d_err, cudaStream_t s);
-// pooled[bag][e] = sum_{o in bag} src[idx[inverse[o]]][e]  (x 1/|bag| when mean)
-void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_inverse,
-          const uint32_t* d_idx, const float* d_src, uint32_t e, bool mean, float* d_pooled,
-          float* d_inv_count, cudaStream_t s);
+// row_of_occ[o] = idx[inverse[o]]  (source row of every occurrence)
+void compose(const uint32_t* d_idx, const uint32_t* d_inverse, uint32_t n, uint32_t* d_out,
+             cudaStream_t s);
+// pooled[bag][e] = sum_{o in bag} src[row_of_occ[o]][e]  (x 1/|bag| when mean)
+void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_row_of_occ,
+          const float* d_src, uint32_t e, bool mean, float* d_pooled, float* d_inv_count,
+          cudaStream_t s);
 // Deterministic segmented reduce of coefficient-scaled upstream rows by
 // unique key, times inv_n, then the sparse rule applied in place to the row.
 struct SegWs {

@@ -239,7 +239,9 @@ __global__ void __launch_bounds__(ST) k_dedup_emit(const uint64_t* __restrict__ 
                                                    uint64_t* __restrict__ uniq,
                                                    uint32_t* __restrict__ inverse,
                                                    uint32_t* __restrict__ seg,
-                                                   uint32_t* __restrict__ nuniq, uint32_t nb) {
+                                                   uint32_t* __restrict__ nuniq, uint32_t nb,
+                                                   const uint32_t* __restrict__ occ_map,
+                                                   uint32_t* __restrict__ sorted_mapped) {
   __shared__ uint32_t s_warp[NW];
   const uint32_t base = blockIdx.x * TILE + threadIdx.x * IPT;
   bool f[IPT];
@@ -261,7 +263,9 @@ __global__ void __launch_bounds__(ST) k_dedup_emit(const uint64_t* __restrict__ 
       seg[uid] = i;
       ++uid;
     }
-    inverse[sv[i]] = uid - 1;
+    const uint32_t occ = sv[i];
+    inverse[occ] = uid - 1;
+    if (occ_map) sorted_mapped[i] = occ_map[occ];  // e.g. bag of each sorted position
   }
   if (blockIdx.x == nb - 1 && threadIdx.x == 0) {
     const uint32_t U = bbase[blockIdx.x] + tot;
@@ -326,7 +330,8 @@ __global__ void __launch_bounds__(ST) k_shard_emit(const uint64_t* __restrict__ 
 
 }  // namespace
 
-void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s) {
+void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
+           const uint32_t* d_occ_map) {
   ws.n = n;
   ws.d_nunique = ws.scalars.get<uint32_t>(4);
   if (n == 0) {
@@ -378,8 +383,9 @@ void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s) {
   ws.d_unique = ws.unique.get<uint64_t>(n);
   ws.d_inverse = ws.inverse.get<uint32_t>(n);
   ws.d_seg = ws.seg.get<uint32_t>(n + 1);
+  ws.d_sorted_mapped = d_occ_map ? ws.mapped.get<uint32_t>(n) : nullptr;
   k_dedup_emit<<<nb, ST, 0, s>>>(kin, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
-                                  ws.d_nunique, nb); ::kp::count_launch();
+                                  ws.d_nunique, nb, d_occ_map, ws.d_sorted_mapped); ::kp::count_launch();
   KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaStreamSynchronize(s));
 }
