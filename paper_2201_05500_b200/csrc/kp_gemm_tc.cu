@@ -35,10 +35,10 @@
 namespace kp {
 namespace {
 
-constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32, TC_STAGES = 3, TC_CH = 4;
+constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32, TC_STAGES = 4, TC_CH = 4;
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
 constexpr uint32_t B_BYTES = TC_BN * TC_BK * 4;  // 16 KB
-constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+constexpr uint32_t STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // A fp32 (split into TMEM), B, B_lo
 constexpr uint32_t SMEM_BYTES = TC_STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -119,6 +119,25 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc_tf32<AMN, BMN>()), "r"(accum));
 }
+// A (hi or lo) from TMEM (lane = row, 32-bit column = k), B from smem
+template <bool BMN>
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc_tf32<false, BMN>()), "r"(accum));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+        "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15])
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -174,11 +193,31 @@ __device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* map, 
   }
 }
 
-// 256 splitter threads: 4 float4 each per 16 KB tile (loads first for ILP)
+
+// Persistent, warp-specialised kernel: one CTA per SM walks work items
+// (m-block, n-block, k-split) w = blockIdx.x, +gridDim.x, ...; the smem
+// pipeline, the TMEM chunk buffers and their barriers run continuously across
+// work items, so the epilogue of one tile overlaps the mainloop of the next.
+//   warp 0      TMA producer
+//   warp 1      TMEM allocator + MMA issuer
+//   warps 2-9   splitters: A (fp32 in smem) -> hi/lo in TMEM (the MMA's A
+//               operand comes from TMEM, so shared memory only feeds B); B is
+//               split in smem too unless it arrives pre-split (BPRE)
+//   warps 10-17 drain + epilogue: warp w owns TMEM lane quarter w%4 and column
+//               half (w-10)/4 -> 64 fp32 register accumulators per thread
+// TMEM: [0,256) two 128-column accumulator chunks; [256,512) per stage A hi
+// (32 columns) + A lo (32 columns).
+constexpr int TC_NBUF = 2;
+constexpr int TC_WARPS = 18;
+constexpr int TC_SPLIT_T = 256;  // splitter threads
+constexpr int TC_EPI_T = 256;    // drain/epilogue threads
+constexpr uint32_t TC_ACOL = TC_NBUF * TC_BN;  // first A-operand column
+
+// 256 splitter threads split a 16 KB B tile in place (hi) + into lo
 __device__ __forceinline__ void split_tile(uint8_t* tile, uint8_t* lo_tile, int ct) {
   float4* hi = reinterpret_cast<float4*>(tile);
   float4* lo = reinterpret_cast<float4*>(lo_tile);
-  constexpr int PER = (int)(A_BYTES / 16 / 256);
+  constexpr int PER = (int)(B_BYTES / 16 / 256);
   float4 x[PER];
 #pragma unroll
   for (int i = 0; i < PER; ++i) x[i] = hi[ct + 256 * i];
@@ -194,21 +233,30 @@ __device__ __forceinline__ void split_tile(uint8_t* tile, uint8_t* lo_tile, int 
   }
 }
 
-// Persistent, warp-specialised kernel: one CTA per SM walks work items
-// (m-block, n-block, k-split) w = blockIdx.x, +gridDim.x, ...; the smem
-// pipeline, the TMEM chunk buffers and their barriers run continuously across
-// work items, so the epilogue of one tile overlaps the mainloop of the next.
-//   warp 0      TMA producer
-//   warp 1      TMEM allocator + MMA issuer
-//   warps 2-9   hi/lo splitters (256 threads)
-//   warps 10-17 drain + epilogue: warp w owns TMEM lane quarter w%4 and column
-//               half (w-10)/4 -> 64 fp32 register accumulators per thread
-// BPRE: B arrives pre-split (hi, lo) from HBM (weights, split once per step);
-// otherwise the splitters split B in shared memory like A.
-constexpr int TC_NBUF = 4;  // TMEM chunk buffers (4 x 128 columns = all 512)
-constexpr int TC_WARPS = 18;
-constexpr int TC_SPLIT_T = 256;  // splitter threads
-constexpr int TC_EPI_T = 256;  // drain/epilogue threads
+// row r, k columns [k0, k0+16) of the stage's A tile -> 16 floats
+template <bool MN>
+__device__ __forceinline__ void load_a_row16(const uint8_t* tile, int r, int k0, float (&v)[16]) {
+  if (!MN) {
+    // K-major SW128: row r is 128 B; 16-byte chunk c sits at chunk c ^ (r & 7)
+    const uint8_t* row = tile + r * 128;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = (k0 >> 2) + i;
+      const float4 x = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 4));
+      v[4 * i] = x.x, v[4 * i + 1] = x.y, v[4 * i + 2] = x.z, v[4 * i + 3] = x.w;
+    }
+  } else {
+    // MN-major SWIZZLE_128B_ATOM_32B: 32x32 boxes (4 KB) along m; in a box,
+    // element (m, k) at k*128 + ((m%32)*4 ^ ((k & 3) << 5))
+    const uint8_t* box = tile + (r >> 5) * 4096;
+    const int mm = (r & 31) * 4;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int k = k0 + j;
+      v[j] = *reinterpret_cast<const float*>(box + k * 128 + (mm ^ ((k & 3) << 5)));
+    }
+  }
+}
 
 template <bool AMN, bool BMN, bool BPRE>
 __global__ void __launch_bounds__(TC_WARPS * 32, 1)
@@ -239,9 +287,8 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     nk = kend > kbeg ? (kend - kbeg + TC_BK - 1) / TC_BK : 0;
   };
   auto sA = [&](int s) { return smem + s * STAGE_BYTES; };
-  auto sAlo = [&](int s) { return smem + s * STAGE_BYTES + A_BYTES; };
-  auto sB = [&](int s) { return smem + s * STAGE_BYTES + 2 * A_BYTES; };
-  auto sBlo = [&](int s) { return smem + s * STAGE_BYTES + 2 * A_BYTES + B_BYTES; };
+  auto sB = [&](int s) { return smem + s * STAGE_BYTES + A_BYTES; };
+  auto sBlo = [&](int s) { return smem + s * STAGE_BYTES + A_BYTES + B_BYTES; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
@@ -258,7 +305,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(TC_NBUF * TC_BN));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -301,14 +348,14 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           mbar_wait(&conv[s], ph);
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(buf * TC_BN);
-          const uint32_t a = smem_u32(sA(s)), alo = smem_u32(sAlo(s));
+          const uint32_t ahi = tmem + TC_ACOL + 64u * s, alo = ahi + 32u;
           const uint32_t b = smem_u32(sB(s)), blo = smem_u32(sBlo(s));
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 8; ++kk) {
-            const uint32_t oa = kstep_off<AMN>(kk), ob = kstep_off<BMN>(kk);
-            mma_tf32<AMN, BMN>(d, sdesc<AMN>(a + oa), sdesc<BMN>(b + ob), (kin | kk) != 0);
-            mma_tf32<AMN, BMN>(d, sdesc<AMN>(a + oa), sdesc<BMN>(blo + ob), 1);
-            mma_tf32<AMN, BMN>(d, sdesc<AMN>(alo + oa), sdesc<BMN>(b + ob), 1);
+            const uint32_t ob = kstep_off<BMN>(kk);
+            mma_tf32_ts<BMN>(d, ahi + 8u * kk, sdesc<BMN>(b + ob), (kin | kk) != 0);
+            mma_tf32_ts<BMN>(d, ahi + 8u * kk, sdesc<BMN>(blo + ob), 1);
+            mma_tf32_ts<BMN>(d, alo + 8u * kk, sdesc<BMN>(b + ob), 1);
           }
           mma_commit(&empty[s]);
           if (kin == TC_CH - 1 || kb == nk - 1) {
@@ -319,8 +366,10 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
       }
     }
   } else if (warp < 10) {
-    // ---- hi/lo splitters ----
+    // ---- splitters: A -> TMEM hi/lo (+ B in smem unless pre-split) ----
     const int ct = threadIdx.x - 64;
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    const int r = q * 32 + lane;  // tile row == TMEM lane
     int g = 0;
     for (int w = blockIdx.x; w < works; w += gridDim.x) {
       int m0, n0, z, nk;
@@ -329,9 +378,26 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
         const int s = g % TC_STAGES;
         const uint32_t ph = (g / TC_STAGES) & 1;
         mbar_wait(&full[s], ph);
-        split_tile(sA(s), sAlo(s), ct);
+        float v[16];
+        load_a_row16<AMN>(sA(s), r, h * 16, v);
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float x = v[j], l;
+          split3(x, l);
+          hi[j] = __float_as_uint(x);
+          lo[j] = __float_as_uint(l);
+        }
+        // MMA of this stage's previous round has finished (empty[s] -> TMA ->
+        // full[s]), so its TMEM A columns are free to overwrite
+        tc_fence_after();
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + 64u * s + 16u * h;
+        tmem_st16(ta, hi);
+        tmem_st16(ta + 32u, lo);
         if (!BPRE) split_tile(sB(s), sBlo(s), ct);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         fence_proxy_async();
+        tc_fence_before();
         mbar_arrive(&conv[s]);
       }
     }
@@ -391,8 +457,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_NBUF * TC_BN));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
 // ---- host side ---------------------------------------------------------------
