@@ -210,6 +210,13 @@ int kp_trainer_train_batch_device(kp_trainer* tr, const uint32_t* h_offs, const 
                                   const int32_t* d_labels, uint32_t n, uint64_t global_n,
                                   uint64_t global_first, int predict_first, float* preds,
                                   kp_batch_result* out);
+/* Pipelined ingestion: stage a HOST batch (pinned memory for true overlap)
+ * into one of two device buffer slots with an async H2D on a copy stream, then
+ * train on it. Staging batch i+1 while batch i trains hides the H2D. */
+int kp_trainer_stage_batch(kp_trainer* tr, int slot, const uint32_t* offs, const uint64_t* keys,
+                           const uint16_t* slots, const int32_t* labels, uint32_t n);
+int kp_trainer_train_staged(kp_trainer* tr, int slot, uint64_t global_n, uint64_t global_first,
+                            int predict_first, float* preds, kp_batch_result* out);
 int kp_trainer_dense_dim(kp_trainer* tr, uint64_t* D);
 /* KStepEngine::states()[w] (optimizer.hpp:118), host copies [D] */
 int kp_trainer_worker_state(kp_trainer* tr, uint32_t local_worker, float* x, float* m, float* v,

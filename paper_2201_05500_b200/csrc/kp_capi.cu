@@ -108,6 +108,15 @@ struct kp_trainer {
   // inputs
   DevBuf in_offs, in_keys, in_slots, in_labels;
   std::vector<uint32_t> h_offs;
+  // double-buffered staged batches (H2D on a copy stream overlapping compute)
+  struct Staged {
+    DevBuf offs, keys, slots, labels;
+    std::vector<uint32_t> h_offs;
+    uint32_t n = 0;
+    bool has_slots = false, ready = false;
+    cudaEvent_t ev = nullptr;
+  } stage[2];
+  cudaStream_t copy_s = nullptr;
   // step buffers
   DevBuf st_offs, st_keys, st_slots, st_labels;
   DedupWs dd, dd_owner;
@@ -164,6 +173,9 @@ struct kp_trainer {
   }
   ~kp_trainer() {
     for (auto e : ev) cudaEventDestroy(e);
+    for (auto& st : stage)
+      if (st.ev) cudaEventDestroy(st.ev);
+    if (copy_s) cudaStreamDestroy(copy_s);
     if (tab.t) table_destroy(tab.t);
     if (tab.s) cudaStreamDestroy(tab.s);
     cudaFree(x);
@@ -1002,6 +1014,48 @@ int kp_trainer_train_batch(kp_trainer* tr, const uint32_t* offs, const uint64_t*
     if (slots) KP_CUDA(cudaMemcpyAsync(d_slots, slots, (size_t)O * 2, cudaMemcpyHostToDevice, tr->s));
     KP_CUDA(cudaMemcpyAsync(d_labels, labels, (size_t)n * 4, cudaMemcpyHostToDevice, tr->s));
     train_batch_impl(tr, offs, d_offs, d_keys, d_slots, d_labels, n, global_n, global_first,
+                     predict_first != 0, preds, out);
+  });
+}
+
+int kp_trainer_stage_batch(kp_trainer* tr, int slot, const uint32_t* offs, const uint64_t* keys,
+                           const uint16_t* slots, const int32_t* labels, uint32_t n) {
+  return guard([&] {
+    KP_CHECK(slot == 0 || slot == 1, kErrGeneric, "stage slot must be 0 or 1");
+    KP_CUDA(cudaSetDevice(tr->device));
+    if (!tr->copy_s) KP_CUDA(cudaStreamCreateWithFlags(&tr->copy_s, cudaStreamNonBlocking));
+    auto& st = tr->stage[slot];
+    if (!st.ev) KP_CUDA(cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming));
+    const uint32_t O = offs[n];
+    uint32_t* d_offs = st.offs.get<uint32_t>(n + 1);
+    uint64_t* d_keys = st.keys.get<uint64_t>(std::max<uint32_t>(O, 1));
+    uint16_t* d_slots = slots ? st.slots.get<uint16_t>(std::max<uint32_t>(O, 1)) : nullptr;
+    int32_t* d_labels = st.labels.get<int32_t>(std::max<uint32_t>(n, 1));
+    KP_CUDA(cudaMemcpyAsync(d_offs, offs, (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, tr->copy_s));
+    KP_CUDA(cudaMemcpyAsync(d_keys, keys, (size_t)O * 8, cudaMemcpyHostToDevice, tr->copy_s));
+    if (slots) KP_CUDA(cudaMemcpyAsync(d_slots, slots, (size_t)O * 2, cudaMemcpyHostToDevice, tr->copy_s));
+    KP_CUDA(cudaMemcpyAsync(d_labels, labels, (size_t)n * 4, cudaMemcpyHostToDevice, tr->copy_s));
+    KP_CUDA(cudaEventRecord(st.ev, tr->copy_s));
+    st.h_offs.assign(offs, offs + n + 1);
+    st.n = n;
+    st.has_slots = slots != nullptr;
+    st.ready = true;
+  });
+}
+
+int kp_trainer_train_staged(kp_trainer* tr, int slot, uint64_t global_n, uint64_t global_first,
+                            int predict_first, float* preds, kp_batch_result* out) {
+  return guard([&] {
+    KP_CHECK(slot == 0 || slot == 1, kErrGeneric, "stage slot must be 0 or 1");
+    auto& st = tr->stage[slot];
+    KP_CHECK(st.ready, kErrGeneric, "train_staged: nothing staged in this slot");
+    KP_CUDA(cudaSetDevice(tr->device));
+    KP_CUDA(cudaStreamWaitEvent(tr->s, st.ev, 0));
+    st.ready = false;
+    train_batch_impl(tr, st.h_offs.data(), static_cast<const uint32_t*>(st.offs.p),
+                     static_cast<const uint64_t*>(st.keys.p),
+                     st.has_slots ? static_cast<const uint16_t*>(st.slots.p) : nullptr,
+                     static_cast<const int32_t*>(st.labels.p), st.n, global_n, global_first,
                      predict_first != 0, preds, out);
   });
 }

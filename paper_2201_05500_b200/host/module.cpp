@@ -381,6 +381,48 @@ PYBIND11_MODULE(_kpsim_b200, m) {
            py::arg("h_offs"), py::arg("d_offs"), py::arg("d_keys"), py::arg("d_slots"),
            py::arg("d_labels"), py::arg("n"), py::arg("global_n") = py::none(),
            py::arg("global_first") = 0, py::arg("predict_first") = false)
+      .def("stage_batch",
+           [](PyTrainer& p, int slot, Arr<uint32_t> offs, Arr<uint64_t> keys, Arr<int32_t> labels,
+              py::object slots) {
+             const uint32_t n = (uint32_t)labels.size();
+             if ((uint32_t)offs.size() != n + 1) throw Error("offs must have n+1 entries");
+             if ((uint64_t)keys.size() != offs.data()[n]) throw Error("keys size != offs[n]");
+             Arr<uint16_t> sl;
+             const uint16_t* sp = nullptr;
+             if (!slots.is_none()) {
+               sl = slots.cast<Arr<uint16_t>>();
+               sp = sl.data();
+             }
+             check(kp_trainer_stage_batch(p.tr->handle(), slot, offs.data(), keys.data(), sp,
+                                          labels.data(), n));
+           },
+           py::arg("slot"), py::arg("offs"), py::arg("keys"), py::arg("labels"),
+           py::arg("slots") = py::none())
+      .def("train_staged",
+           [](PyTrainer& p, int slot, py::object global_n, uint64_t global_first, bool predict_first,
+              uint32_t n_local) {
+             kp_batch_result br{};
+             std::vector<float> preds(predict_first ? n_local : 0);
+             const uint64_t gn = global_n.is_none() ? n_local : global_n.cast<uint64_t>();
+             {
+               py::gil_scoped_release rel;
+               check(kp_trainer_train_staged(p.tr->handle(), slot, gn, global_first,
+                                             predict_first ? 1 : 0,
+                                             predict_first ? preds.data() : nullptr, &br));
+             }
+             py::dict d;
+             d["loss"] = br.loss;
+             d["minibatch_steps"] = br.minibatch_steps;
+             d["merges"] = br.merges;
+             if (predict_first) {
+               Arr<float> pr((py::ssize_t)preds.size());
+               std::copy(preds.begin(), preds.end(), pr.mutable_data());
+               d["preds"] = pr;
+             }
+             return d;
+           },
+           py::arg("slot"), py::arg("global_n") = py::none(), py::arg("global_first") = 0,
+           py::arg("predict_first") = false, py::arg("n_local") = 0)
       .def("worker_state",
            [](PyTrainer& p, std::size_t l) {
              const auto st = p.tr->worker_states().at(l);

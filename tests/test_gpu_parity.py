@@ -306,3 +306,27 @@ def test_tcgen05_gemm_tn_fp32_accuracy(kp, M, N, K):
     err_simt = np.max(np.abs(simt - want)) / scale
     print(f"gemm_tn M={M} N={N} K={K}: normalized max err tc={err_tc:.3e} simt={err_simt:.3e}")
     assert err_tc < 3 * err_simt + 2e-6, (err_tc, err_simt)
+
+
+def test_staged_ingestion_matches_direct(kp):
+    """Double-buffered H2D staging (kp_trainer_stage_batch/train_staged) trains
+    bit-identically to the synchronous host path."""
+    def run(staged):
+        tr = kp.Trainer(table_capacity=1 << 18, n_workers=1, k=1, minibatch_size=2048,
+                        embedding_dim=16, n_slots=8, hidden=[32])
+        bts = [make_batch(2048, V=10**6, zipf_s=1.1, n_slots=8, seed=b) for b in range(3)]
+        if staged:
+            tr.stage_batch(0, bts[0].offs, bts[0].keys, bts[0].labels, slots=bts[0].slots)
+            for b in range(3):
+                if b + 1 < 3:
+                    nb = bts[b + 1]
+                    tr.stage_batch((b + 1) % 2, nb.offs, nb.keys, nb.labels, slots=nb.slots)
+                tr.train_staged(b % 2, n_local=2048)
+        else:
+            for bt in bts:
+                tr.train_batch(bt.offs, bt.keys, bt.labels, slots=bt.slots)
+        return tr.table(), tr.worker_state(0)["x"]
+    (k1, w1, a1, _), x1 = run(False)
+    (k2, w2, a2, _), x2 = run(True)
+    assert np.array_equal(k1, k2) and np.array_equal(w1, w2) and np.array_equal(a1, a2)
+    assert np.array_equal(x1, x2)
