@@ -139,6 +139,14 @@ int kp_centered_mean(const float* d_vecs, uint64_t stride, uint32_t n, uint64_t 
 int kp_kstep_merge(kp_comm* comm, float* d_x, float* d_m, float* d_v, float* d_vbar, uint32_t W,
                    uint64_t D, float alpha, int reset_local_v, kp_stream s);
 
+/* -------------------------------------------------------------- AUC ---
+ * compute_auc (proj/src/eval.cpp:8-39) on the device: rank-sum with tie
+ * averaging over n (score, label) pairs; *auc = NaN when a class is absent,
+ * KP_ERR for labels outside {0,1}. Bit-identical to the reference's loop on
+ * the same scores (all partial sums are exact in f64). Synchronous. */
+int kp_compute_auc(const float* d_scores, const int32_t* d_labels, uint32_t n, double* auc,
+                   kp_stream s);
+
 /* ------------------------------------------------------------- GEMM ---
  * C[M][N] = A[M][K] . B[N][K]^T in fp32 (the MLP's contraction, model.cpp:107-109).
  * engine 0 = auto (tcgen05 3xTF32 when the shapes allow TMA), 1 = SIMT fp32,
@@ -189,6 +197,12 @@ typedef struct kp_batch_result {
   uint64_t merges;
   uint64_t steps_total;
   uint64_t merges_total;
+  /* predict_first only: online AUC of this batch and over every batch so far
+   * (BatchRecord::auc / cumulative_auc, trainer.hpp:36-42), computed on the
+   * device over the global batch; NaN when a class is absent */
+  int32_t has_auc;
+  double auc;
+  double cumulative_auc;
 } kp_batch_result;
 
 int kp_trainer_create(const kp_trainer_config* cfg, kp_comm* comm, int device, kp_trainer** out);

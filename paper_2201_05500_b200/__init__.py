@@ -22,6 +22,7 @@ try:
         WorkerState,
         accumulate_moments,
         adagrad_sparse_update,
+        auc_device,
         comm_unique_id,
         compute_auc,
         dedup,
@@ -42,7 +43,7 @@ except ImportError as e:  # pragma: no cover - exercised only on broken installs
 
 __all__ = [
     "AdamHyper", "Comm", "ConfigError", "DeviceError", "KpsimError", "KStepEngine", "StoreError",
-    "TieredStore", "Trainer", "WorkerState", "accumulate_moments", "adagrad_sparse_update",
+    "TieredStore", "Trainer", "WorkerState", "accumulate_moments", "adagrad_sparse_update", "auc_device",
     "comm_unique_id", "compute_auc", "dedup", "gemm_nt", "gemm_tn", "device_count", "global_merge", "launch_count",
     "local_adam_step", "shard", "version",
 ]

@@ -124,6 +124,9 @@ struct kp_trainer {
   SegWs sg, sg_owner;
   MlpWs mlp;
   MergeWs mws;
+  AucWs aucws;
+  DevBuf hist_scores, hist_labels, all_preds, all_labels, gather_tmp;
+  uint64_t hist_n = 0;
   DevBuf rows, rowocc, bag_offs, bag_of_occ, pooled, inv_count, dpooled, preds, err, loss, check;
   DevBuf xbar, pred_keep, lossg;
   // exchange buffers (G > 1)
@@ -580,6 +583,60 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
     }
   }
   out->loss = cnt ? total / (double)cnt : std::nan("");
+  out->auc = out->cumulative_auc = std::nan("");
+  out->has_auc = 0;
+  if (predict_first) {
+    // online AUC over the GLOBAL batch (trainer.cpp:141-151): gather every
+    // rank's predictions/labels, then rank on the device
+    const float* gp = d_pred_keep;
+    const int32_t* gl = d_labels;
+    uint32_t gn = n;
+    if (tr->world > 1) {
+      const int R = tr->world;
+      std::vector<uint32_t> ns(R);
+      uint32_t* dn = tr->gather_tmp.get<uint32_t>(2 * R);
+      KP_CUDA(cudaMemcpyAsync(dn, &n, 4, cudaMemcpyHostToDevice, s));
+      KP_NCCL(ncclAllGather(dn, dn + R, 1, ncclUint32, tr->comm->nc, s));
+      KP_CUDA(cudaMemcpyAsync(ns.data(), dn + R, R * 4, cudaMemcpyDeviceToHost, s));
+      KP_CUDA(cudaStreamSynchronize(s));
+      uint32_t mx = 0;
+      gn = 0;
+      for (auto v : ns) mx = std::max(mx, v), gn += v;
+      float* pp = tr->all_preds.get<float>((size_t)mx * R + mx);
+      int32_t* ll = tr->all_labels.get<int32_t>((size_t)mx * R + mx);
+      float* pad_p = pp + (size_t)mx * R;
+      int32_t* pad_l = ll + (size_t)mx * R;
+      KP_CUDA(cudaMemcpyAsync(pad_p, d_pred_keep, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+      KP_CUDA(cudaMemcpyAsync(pad_l, d_labels, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+      KP_NCCL(ncclAllGather(pad_p, pp, mx, ncclFloat32, tr->comm->nc, s));
+      KP_NCCL(ncclAllGather(pad_l, ll, mx, ncclInt32, tr->comm->nc, s));
+      // compact the rank slices (rank order = global instance order) into
+      // separate buffers (in-place compaction would overlap)
+      float* cp = tr->hist_scores.get_keep<float>(tr->hist_n + gn, tr->hist_n) + tr->hist_n;
+      int32_t* cl = tr->hist_labels.get_keep<int32_t>(tr->hist_n + gn, tr->hist_n) + tr->hist_n;
+      uint32_t off = 0;
+      for (int r = 0; r < R; ++r) {
+        if (ns[r]) {
+          KP_CUDA(cudaMemcpyAsync(cp + off, pp + (size_t)r * mx, (size_t)ns[r] * 4, cudaMemcpyDeviceToDevice, s));
+          KP_CUDA(cudaMemcpyAsync(cl + off, ll + (size_t)r * mx, (size_t)ns[r] * 4, cudaMemcpyDeviceToDevice, s));
+        }
+        off += ns[r];
+      }
+      gp = cp;
+      gl = cl;
+    }
+    out->auc = device_auc(gp, gl, gn, tr->aucws, s);
+    // AucAccumulator: every score so far, re-ranked (eval.cpp:41-50)
+    float* hs = tr->hist_scores.get_keep<float>(tr->hist_n + gn, tr->hist_n);
+    int32_t* hl = tr->hist_labels.get_keep<int32_t>(tr->hist_n + gn, tr->hist_n);
+    if (gp != hs + tr->hist_n) {
+      KP_CUDA(cudaMemcpyAsync(hs + tr->hist_n, gp, (size_t)gn * 4, cudaMemcpyDeviceToDevice, s));
+      KP_CUDA(cudaMemcpyAsync(hl + tr->hist_n, gl, (size_t)gn * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    tr->hist_n += gn;
+    out->cumulative_auc = device_auc(hs, hl, (uint32_t)tr->hist_n, tr->aucws, s);
+    out->has_auc = 1;
+  }
   out->minibatch_steps = tr->t_global - steps_before;
   out->merges = tr->merges - merges_before;
   out->steps_total = tr->t_global;
@@ -839,6 +896,15 @@ int kp_kstep_merge(kp_comm* comm, float* d_x, float* d_m, float* d_v, float* d_v
     static thread_local MergeWs ws;
     merge_states(comm, st(s), W, D, d_x, d_m, d_v, d_vbar, alpha, reset_local_v != 0, ws);
     KP_CUDA(cudaStreamSynchronize(st(s)));
+  });
+}
+
+// ---- AUC ----
+int kp_compute_auc(const float* d_scores, const int32_t* d_labels, uint32_t n, double* auc,
+                   kp_stream s) {
+  return guard([&] {
+    static thread_local AucWs ws;
+    *auc = device_auc(d_scores, d_labels, n, ws, st(s));
   });
 }
 

@@ -70,6 +70,20 @@ struct DevBuf {
   T* get(size_t n) {
     return static_cast<T*>(ensure(n * sizeof(T)));
   }
+  // grow keeping the first `used` bytes (history buffers)
+  template <class T>
+  T* get_keep(size_t n, size_t used_elems) {
+    const size_t bytes = n * sizeof(T);
+    if (bytes <= cap) return static_cast<T*>(p);
+    void* q = nullptr;
+    const size_t nc = bytes * 2 + 256;
+    KP_CUDA(cudaMalloc(&q, nc));
+    if (p && used_elems) KP_CUDA(cudaMemcpy(q, p, used_elems * sizeof(T), cudaMemcpyDeviceToDevice));
+    if (p) KP_CUDA(cudaFree(p));
+    p = q;
+    cap = nc;
+    return static_cast<T*>(p);
+  }
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {

@@ -185,6 +185,16 @@ void merge_terms(const float* x, const float* m, const float* vbar, uint64_t D, 
 void dense_check(const float* v, const float* vbar, const float* x, uint64_t D, uint32_t* d_flag,
                  cudaStream_t s);
 
+// ---------------------------------------------------------------- AUC ----
+struct AucWs {
+  DevBuf keys, part, part2, bad;
+  DedupWs dd;
+};
+// rank-sum AUC with tie averaging over n (score, label) pairs; NaN when a
+// class is absent (proj/src/eval.cpp:8-39). Synchronises the stream.
+double device_auc(const float* d_scores, const int32_t* d_labels, uint32_t n, AucWs& ws,
+                  cudaStream_t s);
+
 // init_dense (proj/src/model.cpp:68-74): mt19937_64 + libstdc++ uniform(-0.05,0.05)
 void init_dense_host(uint64_t seed, uint64_t dim, double* out);
 uint64_t splitmix64_host(uint64_t x);

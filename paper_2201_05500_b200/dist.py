@@ -70,18 +70,6 @@ class DistributedTrainer:
         sl = batch.slice(first, first + n)
         r = self.tr.train_batch(sl.offs, sl.keys, sl.labels, slots=sl.slots,
                                 predict_first=predict_first, global_n=batch.n, global_first=first)
-        if predict_first:
-            preds = torch.from_numpy(np.asarray(r["preds"], np.float32))
-            if self.world > 1:
-                parts = [None] * self.world
-                dist.all_gather_object(parts, preds.numpy())
-                allp = np.concatenate(parts)
-            else:
-                allp = preds.numpy()
-            scores = allp.astype(np.float64)
-            self._scores.append(scores)
-            self._labels.append(batch.labels)
-            r["auc"] = kp.compute_auc(scores.tolist(), batch.labels.tolist())
-            r["cumulative_auc"] = kp.compute_auc(np.concatenate(self._scores).tolist(),
-                                                 np.concatenate(self._labels).tolist())
+        # predict_first: r["auc"] / r["cumulative_auc"] are computed on the
+        # device over the GLOBAL batch (predictions all-gathered over NCCL)
         return r

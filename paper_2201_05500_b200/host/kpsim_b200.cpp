@@ -547,6 +547,10 @@ CsrResult Trainer::train_csr(const std::uint32_t* offs, const ParameterKey* keys
   r.loss = br.loss;
   r.minibatch_steps = br.minibatch_steps;
   r.merges = br.merges;
+  if (br.has_auc) {
+    if (std::isfinite(br.auc)) r.auc = br.auc;
+    if (std::isfinite(br.cumulative_auc)) r.cumulative_auc = br.cumulative_auc;
+  }
   steps_ = br.steps_total;
   metrics_.minibatch_steps += br.minibatch_steps;
   metrics_.merge_events += br.merges;
@@ -567,6 +571,10 @@ CsrResult Trainer::train_csr_device(const std::uint32_t* h_offs, const std::uint
   r.loss = br.loss;
   r.minibatch_steps = br.minibatch_steps;
   r.merges = br.merges;
+  if (br.has_auc) {
+    if (std::isfinite(br.auc)) r.auc = br.auc;
+    if (std::isfinite(br.cumulative_auc)) r.cumulative_auc = br.cumulative_auc;
+  }
   steps_ = br.steps_total;
   metrics_.minibatch_steps += br.minibatch_steps;
   metrics_.merge_events += br.merges;
@@ -604,12 +612,9 @@ BatchRecord Trainer::process(const Batch& b, bool predict_first) {
   rec.batch = b.id;
   rec.instances = b.instances.size();
   rec.loss = r.loss;
-  if (predict_first) {
-    std::vector<double> sc(r.preds.begin(), r.preds.end());
-    std::vector<int> lb(labels.begin(), labels.end());
-    rec.auc = compute_auc(sc, lb);
-    cumulative_.add(sc, lb);
-    rec.cumulative_auc = cumulative_.value();
+  if (predict_first) {  // online AUC computed on the device (kp_auc.cu)
+    rec.auc = r.auc;
+    rec.cumulative_auc = r.cumulative_auc;
   }
   metrics_.batches.push_back(rec);
   return rec;
@@ -618,8 +623,7 @@ BatchRecord Trainer::process(const Batch& b, bool predict_first) {
 BatchRecord Trainer::train_batch(const Batch& b) { return process(b, false); }
 
 TrainMetrics Trainer::online_eval(std::span<const Batch> stream) {
-  for (const auto& b : stream) process(b, true);
-  metrics_.cumulative_auc = cumulative_.value();
+  for (const auto& b : stream) metrics_.cumulative_auc = process(b, true).cumulative_auc;
   return metrics_;
 }
 

@@ -214,6 +214,7 @@ struct CsrResult {
   double loss = 0.0;
   std::uint64_t minibatch_steps = 0, merges = 0;
   std::vector<float> preds;  // predict_first only
+  std::optional<double> auc, cumulative_auc;  // predict_first only (device AUC)
 };
 
 class Trainer {

@@ -71,7 +71,7 @@ TrainerConfig config_from_kwargs(const py::kwargs& kw) {
 PYBIND11_MODULE(_kpsim_b200, m) {
   m.doc() = "B200-native sparse-embedding training hot path (kpsim drop-in)";
   // translators run newest-first, so the base class registers first
-  static py::exception<Error> base(m, "KpsimError", PyExc_RuntimeError);
+  auto& base = py::register_exception<Error>(m, "KpsimError", PyExc_RuntimeError);
   py::register_exception<ConfigError>(m, "ConfigError", PyExc_ValueError);
   py::register_exception<StoreError>(m, "StoreError", base.ptr());
   py::register_exception<DeviceError>(m, "DeviceError", base.ptr());
@@ -270,6 +270,25 @@ PYBIND11_MODULE(_kpsim_b200, m) {
         },
         py::arg("A"), py::arg("B"), py::arg("engine") = 0, py::arg("device") = 0);
 
+  m.def("auc_device",
+        [](Arr<float> scores, Arr<int32_t> labels, int device) -> py::object {
+          if (scores.size() != labels.size()) throw Error("compute_auc: scores/labels length mismatch");
+          check(kp_set_device(device));
+          const uint32_t n = (uint32_t)scores.size();
+          void *ds, *dl;
+          check(kp_dev_alloc(std::max<size_t>(n, 1) * 4, &ds));
+          check(kp_dev_alloc(std::max<size_t>(n, 1) * 4, &dl));
+          double auc = 0;
+          int rc = kp_memcpy_h2d(ds, scores.data(), (size_t)n * 4);
+          if (rc == KP_OK) rc = kp_memcpy_h2d(dl, labels.data(), (size_t)n * 4);
+          if (rc == KP_OK) rc = kp_compute_auc((const float*)ds, (const int32_t*)dl, n, &auc, nullptr);
+          kp_dev_free(ds);
+          kp_dev_free(dl);
+          check(rc);
+          if (!(auc == auc)) return py::none();
+          return py::float_(auc);
+        },
+        py::arg("scores"), py::arg("labels"), py::arg("device") = 0);
   m.def("gemm_tn",
         [](Arr<float> A, Arr<float> B, int engine, int device) {
           if (A.ndim() != 2 || B.ndim() != 2 || A.shape(0) != B.shape(0))
@@ -308,6 +327,7 @@ PYBIND11_MODULE(_kpsim_b200, m) {
                        const py::kwargs& kw) {
              auto p = std::make_unique<PyTrainer>();
              TrainerConfig c = config_from_kwargs(kw);
+             c.adam.validate();  // config errors before any device work
              TierConfig t;
              t.cache_capacity = table_capacity;
              t.cold_path = kw.contains("cold_dir") ? kw["cold_dir"].cast<std::string>() : "/tmp/kpsim_b200_cold";
@@ -348,6 +368,9 @@ PYBIND11_MODULE(_kpsim_b200, m) {
                Arr<float> pr(n);
                std::copy(r.preds.begin(), r.preds.end(), pr.mutable_data());
                d["preds"] = pr;
+               d["auc"] = r.auc ? py::object(py::float_(*r.auc)) : py::object(py::none());
+               d["cumulative_auc"] =
+                   r.cumulative_auc ? py::object(py::float_(*r.cumulative_auc)) : py::object(py::none());
              }
              return d;
            },

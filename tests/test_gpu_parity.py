@@ -330,3 +330,33 @@ def test_staged_ingestion_matches_direct(kp):
     (k2, w2, a2, _), x2 = run(True)
     assert np.array_equal(k1, k2) and np.array_equal(w1, w2) and np.array_equal(a1, a2)
     assert np.array_equal(x1, x2)
+
+
+@pytest.mark.parametrize("n,ties", [(2, False), (1000, True), (65536, False), (200_000, True)])
+def test_device_auc_bit_exact(kp, n, ties):
+    """Device rank-sum AUC == the reference's compute_auc on the same fp32 scores,
+    bit for bit (all partial sums are exact half-integers in f64)."""
+    rng = np.random.default_rng(n)
+    s = (rng.integers(1, 25, n) / 25.0 if ties else rng.random(n)).astype(np.float32)
+    y = rng.integers(0, 2, n).astype(np.int32)
+    y[0], y[-1] = 0, 1
+    want = O.orc_auc(s.astype(np.float64), y)
+    assert kp.auc_device(s, y) == want
+    if O.ref_available() and n <= 65536:
+        assert kp.auc_device(s, y) == O.ref_auc(s.astype(np.float64), y)
+    assert kp.auc_device(s, np.ones(n, np.int32)) is None
+    with pytest.raises(kp.KpsimError, match="label"):
+        kp.auc_device(s, np.full(n, 2, np.int32))
+
+
+def test_trainer_online_auc_matches_host(kp):
+    tr = kp.Trainer(table_capacity=1 << 16, n_workers=1, k=1, minibatch_size=512, embedding_dim=8,
+                    hidden=[16], sparse_lr=0.3)
+    scores, labels = [], []
+    for b in range(3):
+        bt = make_batch(512, V=5000, zipf_s=1.1, nnz=9, poisson=True, seed=b)
+        r = tr.train_batch(bt.offs, bt.keys, bt.labels, predict_first=True)
+        scores.append(r["preds"].astype(np.float64))
+        labels.append(bt.labels)
+        assert r["auc"] == O.orc_auc(scores[-1], bt.labels)
+        assert r["cumulative_auc"] == O.orc_auc(np.concatenate(scores), np.concatenate(labels))
