@@ -440,7 +440,7 @@ void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* 
   a.table_rows = d_table_rows;
   a.grad_out = d_grad_out;
   a.out_idx = d_out_idx;
-  a.CH = 128;
+  a.CH = 64;
   const uint32_t nchunks = (n_pos + a.CH - 1) / a.CH;
   a.partials = ws.partials.get<float>((size_t)nchunks * 2 * e);
   a.apply = t != nullptr;
