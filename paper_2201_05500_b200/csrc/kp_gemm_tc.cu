@@ -39,7 +39,10 @@ constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32, TC_STAGES = 4, TC_CH = 4;
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
 constexpr uint32_t B_BYTES = TC_BN * TC_BK * 4;  // 16 KB
 constexpr uint32_t STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // A fp32 (split into TMEM), B, B_lo
-constexpr uint32_t SMEM_BYTES = TC_STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+constexpr int EPI_LD = 20;  // epilogue transpose row stride (floats): conflict-free float4 rows
+constexpr uint32_t EPI_BYTES = 8 * 32 * EPI_LD * 4;  // 8 epilogue warps x 32 rows x 16 columns
+constexpr uint32_t SMEM_BYTES =
+    TC_STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -272,6 +275,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   uint64_t* tfull = bars + 3 * TC_STAGES;
   uint64_t* tempty = bars + 3 * TC_STAGES + TC_NBUF;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * TC_STAGES + 2 * TC_NBUF);
+  float* epi_smem = reinterpret_cast<float*>(smem + TC_STAGES * STAGE_BYTES + 512);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mblocks = (M + TC_BM - 1) / TC_BM, nblocks = (N + TC_BN - 1) / TC_BN;
@@ -428,29 +432,63 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
       }
-      const int m = m0 + q * 32 + lane;
-      const int nb0 = n0 + half * 64;
-      if (m < M) {
-        float* crow = C + (size_t)z * M * ldc + (size_t)m * ldc;
+      // Epilogue through a per-warp smem transpose: the drain holds one ROW
+      // per lane (tcgen05.ld 32x32b); stores want consecutive COLUMNS per
+      // lane. Per 16-column group: lane -> smem row, then 4 lanes per row
+      // (float4 each, 64 B contiguous) x 8 rows per instruction -> HBM, with
+      // the epilogue's bias / activation-derivative / coefficient loads
+      // coalesced the same way.
+      float* st = epi_smem + (warp - 10) * (32 * EPI_LD);
+      const int rsub = lane >> 2, c4 = (lane & 3) * 4;
+      const bool cvec = (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          const int n = nb0 + j;
-          if (n < N) {
-            float v = acc[j];
-            if (ep.mode == 1) v = act_fwd(ep.act, __fadd_rn(v, ep.bias[n]));
-            else if (ep.mode == 2) v = __fmul_rn(v, act_bwd(ep.act, ep.aux[(size_t)m * ep.ld_aux + n]));
-            else if (ep.mode == 3) v = __fmul_rn(v, ep.coeff[(size_t)m * ep.S + n / ep.e]);
-            acc[j] = v;
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(st + lane * EPI_LD + j) =
+              make_float4(acc[c0 + j], acc[c0 + j + 1], acc[c0 + j + 2], acc[c0 + j + 3]);
+        __syncwarp();
+        const int n = n0 + half * 64 + c0 + c4;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int rr = it * 8 + rsub;
+          const int m = m0 + q * 32 + rr;
+          if (m >= M || n >= N) continue;
+          float4 v = *reinterpret_cast<const float4*>(st + rr * EPI_LD + c4);
+          float* vv = reinterpret_cast<float*>(&v);
+          const bool full4 = n + 4 <= N;
+          if (ep.mode == 1) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (n + t < N) vv[t] = act_fwd(ep.act, __fadd_rn(vv[t], ep.bias[n + t]));
+          } else if (ep.mode == 2) {
+            const float* ap = ep.aux + (size_t)m * ep.ld_aux + n;
+            if (full4 && ((ep.ld_aux & 3) == 0) && ((reinterpret_cast<uintptr_t>(ep.aux) & 15) == 0)) {
+              const float4 a = __ldg(reinterpret_cast<const float4*>(ap));
+              vv[0] = __fmul_rn(vv[0], act_bwd(ep.act, a.x));
+              vv[1] = __fmul_rn(vv[1], act_bwd(ep.act, a.y));
+              vv[2] = __fmul_rn(vv[2], act_bwd(ep.act, a.z));
+              vv[3] = __fmul_rn(vv[3], act_bwd(ep.act, a.w));
+            } else {
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                if (n + t < N) vv[t] = __fmul_rn(vv[t], act_bwd(ep.act, ap[t]));
+            }
+          } else if (ep.mode == 3) {
+            const float* cp = ep.coeff + (size_t)m * ep.S;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (n + t < N) vv[t] = __fmul_rn(vv[t], cp[(n + t) / ep.e]);
           }
-        }
-        if (nb0 + 64 <= N && (ldc & 3) == 0) {
+          float* crow = C + (size_t)z * M * ldc + (size_t)m * ldc + n;
+          if (full4 && cvec) {
+            *reinterpret_cast<float4*>(crow) = v;
+          } else {
 #pragma unroll
-          for (int j = 0; j < 64; j += 4)
-            *reinterpret_cast<float4*>(crow + nb0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 64; ++j)
-            if (nb0 + j < N) crow[nb0 + j] = acc[j];
+            for (int t = 0; t < 4; ++t)
+              if (n + t < N) crow[t] = vv[t];
+          }
         }
       }
     }
