@@ -937,7 +937,7 @@ int kp_gemm_tn(const float* d_A, int lda, const float* d_B, int ldb, float* d_C,
       if (sp == 1) {
         tc_gemm_tn(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, 1, st(s));
       } else {
-        DevBuf part;
+        static thread_local DevBuf part;
         float* p = part.get<float>((size_t)sp * M * ldc);
         const int got = tc_gemm_tn(M, N, K, d_A, lda, d_B, ldb, p, ldc, sp, st(s));
         reduce_splits(p, got, (size_t)M * ldc, d_C, st(s));

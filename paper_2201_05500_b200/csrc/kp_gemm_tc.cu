@@ -35,14 +35,10 @@
 namespace kp {
 namespace {
 
-constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32, TC_STAGES = 4, TC_CH = 4;
+constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 32, TC_CH = 4;
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 4;  // 16 KB
-constexpr uint32_t B_BYTES = TC_BN * TC_BK * 4;  // 16 KB
-constexpr uint32_t STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // A fp32 (split into TMEM), B, B_lo
 constexpr int EPI_LD = 20;  // epilogue transpose row stride (floats): conflict-free float4 rows
 constexpr uint32_t EPI_BYTES = 8 * 32 * EPI_LD * 4;  // 8 epilogue warps x 32 rows x 16 columns
-constexpr uint32_t SMEM_BYTES =
-    TC_STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -107,31 +103,6 @@ __device__ __forceinline__ uint32_t kstep_off(int kk) {
   return MN ? (uint32_t)kk * 1024u : (uint32_t)kk * 32u;
 }
 
-// instruction descriptor: D f32, A/B tf32, M=128, N=TC_BN, per-operand major
-template <bool AMN, bool BMN>
-__host__ __device__ constexpr uint32_t idesc_tf32() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((AMN ? 1u : 0u) << 15) | ((BMN ? 1u : 0u) << 16) |
-         ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
-}
-
-template <bool AMN, bool BMN>
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc_tf32<AMN, BMN>()), "r"(accum));
-}
-// A (hi or lo) from TMEM (lane = row, 32-bit column = k), B from smem
-template <bool BMN>
-__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
-                                            uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(b), "r"(idesc_tf32<false, BMN>()), "r"(accum));
-}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
@@ -183,44 +154,127 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 
-// TMA a 128-row x 32-k operand tile into smem (one K-major box, or four
+// Persistent, warp-specialised kernel. A work unit is one CTA (CG = 1) or one
+// CTA pair (CG = 2, a 2-CTA cluster on one TPC issuing tcgen05.mma.cta_group::2
+// with M = 256: each CTA holds 128 rows of A and HALF of the B tile, so every
+// SM streams half the B bytes per MMA cycle -- the L2->SM operand stream is
+// what bounds 3xTF32). Units walk work items (m-block, n-block, k-split)
+// w = unit, +units, ...; the smem pipeline, the TMEM chunk buffers and their
+// barriers run continuously across work items, so the epilogue of one tile
+// overlaps the mainloop of the next.
+//   warp 0      TMA producer (this CTA's A rows and B half -> local full[s])
+//   warp 1      TMEM allocator; lane 0 of the leader CTA issues the MMAs
+//   warps 2-9   splitters: A (fp32 in smem) -> hi/lo in TMEM (the MMA's A
+//               operand comes from TMEM, so shared memory only feeds B); B is
+//               split in smem too unless it arrives pre-split (BPRE); then one
+//               arrival per CTA on the leader's conv[s]
+//   warps 10-17 drain + epilogue: warp w owns TMEM lane quarter w%4 and column
+//               half (w-10)/4 -> 64 fp32 register accumulators per thread;
+//               one arrival per CTA on the leader's tempty[b]
+// TMEM (per CTA): [0,256) two 128-column accumulator chunks; [256,512) per
+// stage A hi (32 columns) + A lo (32 columns).
+constexpr int TC_NBUF = 2;
+constexpr int TC_ASLOTS = 4;  // TMEM A (hi+lo) k-block slots: 4 x 64 columns
+constexpr int TC_WARPS = 18;
+constexpr int TC_EPI_T = 256;  // drain/epilogue threads
+constexpr uint32_t TC_ACOL = TC_NBUF * TC_BN;  // first A-operand column
+
+template <int CG>
+struct TcCfg {
+  static constexpr int BROWS = TC_BN / CG;  // B rows held by one CTA
+  static constexpr uint32_t B_BYTES = BROWS * TC_BK * 4;
+  static constexpr uint32_t STAGE = A_BYTES + 2 * B_BYTES;  // A fp32, B (hi), B lo
+  // smem ring depth (a deeper ring, 6 stages at CG = 2 with separate TMEM A
+  // slot barriers, measured no faster)
+  static constexpr int STAGES = 4;
+  static constexpr uint32_t SMEM = STAGES * STAGE + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// one arrival on barrier `b` of the leader CTA (rank 0) of the pair
+template <int CG>
+__device__ __forceinline__ void arrive_leader(uint64_t* b) {
+  if (CG == 1) {
+    mbar_arrive(b);
+  } else {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(b)));
+    // default (.release.cta) semantics: a .cluster-scoped release costs a
+    // MEMBAR.ALL.GPU per arrival; the TMEM/smem operands are ordered by the
+    // tcgen05 / proxy fences before the named barrier
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* b, uint32_t parity) {
+  mbar_wait(b, parity);
+}
+// instruction descriptor: D f32, A/B tf32, M = 128*CG, N = TC_BN, per-operand major
+template <bool AMN, bool BMN, int CG>
+__host__ __device__ constexpr uint32_t idesc_tf32_cg() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((AMN ? 1u : 0u) << 15) | ((BMN ? 1u : 0u) << 16) |
+         ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((TC_BM * CG) >> 4) << 24);
+}
+// A (hi or lo) from TMEM (lane = row, 32-bit column = k), B from smem
+template <bool BMN, int CG>
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t accum) {
+  if (CG == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc_tf32_cg<false, BMN, 1>()), "r"(accum));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc_tf32_cg<false, BMN, 2>()), "r"(accum));
+  }
+}
+// MMA completion -> barrier b in this CTA (CG = 1) or in both CTAs of the pair
+template <int CG>
+__device__ __forceinline__ void commit_cg(uint64_t* b) {
+  if (CG == 1) {
+    mma_commit(b);
+  } else {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(b)),
+        "h"((uint16_t)3)
+        : "memory");
+  }
+}
+
+// TMA `rows` x 32-k operand rows into smem (one K-major box, or rows/32
 // 32x32 MN-major boxes at LBO spacing)
-template <bool MN>
-__device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int k0,
+template <bool MN, int ROWS>
+__device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int k0,
                                           int r0) {
   if (MN) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) tma_load_2d(dst + i * 4096, map, bar, r0 + 32 * i, k0);
+    for (int i = 0; i < ROWS / 32; ++i) tma_load_2d(dst + i * 4096, map, bar, r0 + 32 * i, k0);
   } else {
     tma_load_2d(dst, map, bar, k0, r0);
   }
 }
 
-
-// Persistent, warp-specialised kernel: one CTA per SM walks work items
-// (m-block, n-block, k-split) w = blockIdx.x, +gridDim.x, ...; the smem
-// pipeline, the TMEM chunk buffers and their barriers run continuously across
-// work items, so the epilogue of one tile overlaps the mainloop of the next.
-//   warp 0      TMA producer
-//   warp 1      TMEM allocator + MMA issuer
-//   warps 2-9   splitters: A (fp32 in smem) -> hi/lo in TMEM (the MMA's A
-//               operand comes from TMEM, so shared memory only feeds B); B is
-//               split in smem too unless it arrives pre-split (BPRE)
-//   warps 10-17 drain + epilogue: warp w owns TMEM lane quarter w%4 and column
-//               half (w-10)/4 -> 64 fp32 register accumulators per thread
-// TMEM: [0,256) two 128-column accumulator chunks; [256,512) per stage A hi
-// (32 columns) + A lo (32 columns).
-constexpr int TC_NBUF = 2;
-constexpr int TC_WARPS = 18;
-constexpr int TC_SPLIT_T = 256;  // splitter threads
-constexpr int TC_EPI_T = 256;    // drain/epilogue threads
-constexpr uint32_t TC_ACOL = TC_NBUF * TC_BN;  // first A-operand column
-
-// 256 splitter threads split a 16 KB B tile in place (hi) + into lo
+// 256 splitter threads split this CTA's B tile in place (hi) + into lo
+template <int CG>
 __device__ __forceinline__ void split_tile(uint8_t* tile, uint8_t* lo_tile, int ct) {
   float4* hi = reinterpret_cast<float4*>(tile);
   float4* lo = reinterpret_cast<float4*>(lo_tile);
-  constexpr int PER = (int)(B_BYTES / 16 / 256);
+  constexpr int PER = (int)(TcCfg<CG>::B_BYTES / 16 / 256);
   float4 x[PER];
 #pragma unroll
   for (int i = 0; i < PER; ++i) x[i] = hi[ct + 256 * i];
@@ -261,59 +315,72 @@ __device__ __forceinline__ void load_a_row16(const uint8_t* tile, int r, int k0,
   }
 }
 
-template <bool AMN, bool BMN, bool BPRE>
+template <bool AMN, bool BMN, bool BPRE, int CG>
 __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmBlo, int M, int N, int K, int kps,
               float* __restrict__ C, int ldc, GemmEpi ep) {
+  using Cfg = TcCfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES);
-  uint64_t* full = bars;
-  uint64_t* conv = bars + TC_STAGES;
-  uint64_t* empty = bars + 2 * TC_STAGES;
-  uint64_t* tfull = bars + 3 * TC_STAGES;
-  uint64_t* tempty = bars + 3 * TC_STAGES + TC_NBUF;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * TC_STAGES + 2 * TC_NBUF);
-  float* epi_smem = reinterpret_cast<float*>(smem + TC_STAGES * STAGE_BYTES + 512);
+  constexpr int NS = Cfg::STAGES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * Cfg::STAGE);
+  uint64_t* full = bars;                     // TMA -> splitters (local)
+  uint64_t* conv = bars + NS;                // splitters -> MMA (leader; CG arrivals)
+  uint64_t* empty = bars + 2 * NS;           // MMA -> producer (both CTAs)
+  uint64_t* afree = bars + 3 * NS;           // MMA -> splitters: TMEM A slot free (both CTAs)
+  uint64_t* tfull = afree + TC_ASLOTS;       // MMA -> drain (both CTAs)
+  uint64_t* tempty = tfull + TC_NBUF;        // drain -> MMA (leader; CG arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + TC_NBUF);
+  float* epi_smem = reinterpret_cast<float*>(smem + NS * Cfg::STAGE + 512);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mblocks = (M + TC_BM - 1) / TC_BM, nblocks = (N + TC_BN - 1) / TC_BN;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const int unit = blockIdx.x / CG, units = gridDim.x / CG;
+  const int TM = TC_BM * CG;
+  const int mblocks = (M + TM - 1) / TM, nblocks = (N + TC_BN - 1) / TC_BN;
   const int splits = (K + kps - 1) / kps;
   const int works = mblocks * nblocks * splits;
-  // work w -> (n-block fastest, then m-block, then split): CTAs in flight share A rows
+  // work w -> (n-block fastest, then m-block, then split): units in flight share A rows
   auto decode = [&](int w, int& m0, int& n0, int& z, int& nk) {
     const int nb = w % nblocks, r = w / nblocks, mb = r % mblocks;
     z = r / mblocks;
-    m0 = mb * TC_BM;
+    m0 = mb * TM + (int)rank * TC_BM;  // this CTA's rows
     n0 = nb * TC_BN;
     const int kbeg = z * kps, kend = min(K, kbeg + kps);
     nk = kend > kbeg ? (kend - kbeg + TC_BK - 1) / TC_BK : 0;
   };
-  auto sA = [&](int s) { return smem + s * STAGE_BYTES; };
-  auto sB = [&](int s) { return smem + s * STAGE_BYTES + A_BYTES; };
-  auto sBlo = [&](int s) { return smem + s * STAGE_BYTES + A_BYTES + B_BYTES; };
+  auto sA = [&](int s) { return smem + s * Cfg::STAGE; };
+  auto sB = [&](int s) { return smem + s * Cfg::STAGE + A_BYTES; };
+  auto sBlo = [&](int s) { return smem + s * Cfg::STAGE + A_BYTES + Cfg::B_BYTES; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], TC_SPLIT_T);
+      mbar_init(&conv[s], CG);
       mbar_init(&empty[s], 1);
     }
+    for (int a = 0; a < TC_ASLOTS; ++a) mbar_init(&afree[a], 1);
     for (int b = 0; b < TC_NBUF; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], TC_EPI_T);
+      mbar_init(&tempty[b], CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)), "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)), "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote arrival
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -323,47 +390,49 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
       if (BPRE) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBlo)) : "memory");
       int g = 0;  // global k-block counter (stage pipeline)
-      for (int w = blockIdx.x; w < works; w += gridDim.x) {
+      for (int w = unit; w < works; w += units) {
         int m0, n0, z, nk;
         decode(w, m0, n0, z, nk);
+        const int nb0 = n0 + (int)rank * Cfg::BROWS;  // this CTA's half of the B tile
         for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int s = g % TC_STAGES;
-          const uint32_t ph = (g / TC_STAGES) & 1;
-          if (g >= TC_STAGES) mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], A_BYTES + (BPRE ? 2 : 1) * B_BYTES);
+          const int s = g % NS;
+          const uint32_t ph = (g / NS) & 1;
+          if (g >= NS) mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], A_BYTES + (BPRE ? 2 : 1) * Cfg::B_BYTES);
           const int k0 = z * kps + kb * TC_BK;
-          load_tile<AMN>(sA(s), &tmA, &full[s], k0, m0);
-          load_tile<BMN>(sB(s), &tmB, &full[s], k0, n0);
-          if (BPRE) load_tile<BMN>(sBlo(s), &tmBlo, &full[s], k0, n0);
+          load_rows<AMN, TC_BM>(sA(s), &tmA, &full[s], k0, m0);
+          load_rows<BMN, Cfg::BROWS>(sB(s), &tmB, &full[s], k0, nb0);
+          if (BPRE) load_rows<BMN, Cfg::BROWS>(sBlo(s), &tmBlo, &full[s], k0, nb0);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       int g = 0, c = 0;  // global k-block and chunk counters
-      for (int w = blockIdx.x; w < works; w += gridDim.x) {
+      for (int w = unit; w < works; w += units) {
         int m0, n0, z, nk;
         decode(w, m0, n0, z, nk);
         for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int s = g % TC_STAGES;
-          const uint32_t ph = (g / TC_STAGES) & 1;
+          const int s = g % NS;
+          const uint32_t ph = (g / NS) & 1;
           const int kin = kb % TC_CH, buf = c % TC_NBUF;
-          if (kin == 0 && c >= TC_NBUF) mbar_wait(&tempty[buf], ((c / TC_NBUF) - 1) & 1);
-          mbar_wait(&conv[s], ph);
+          if (kin == 0 && c >= TC_NBUF) mbar_wait_cl<CG>(&tempty[buf], ((c / TC_NBUF) - 1) & 1);
+          mbar_wait_cl<CG>(&conv[s], ph);
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(buf * TC_BN);
-          const uint32_t ahi = tmem + TC_ACOL + 64u * s, alo = ahi + 32u;
+          const uint32_t ahi = tmem + TC_ACOL + 64u * (uint32_t)(g % TC_ASLOTS), alo = ahi + 32u;
           const uint32_t b = smem_u32(sB(s)), blo = smem_u32(sBlo(s));
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 8; ++kk) {
             const uint32_t ob = kstep_off<BMN>(kk);
-            mma_tf32_ts<BMN>(d, ahi + 8u * kk, sdesc<BMN>(b + ob), (kin | kk) != 0);
-            mma_tf32_ts<BMN>(d, ahi + 8u * kk, sdesc<BMN>(blo + ob), 1);
-            mma_tf32_ts<BMN>(d, alo + 8u * kk, sdesc<BMN>(b + ob), 1);
+            mma_ts<BMN, CG>(d, ahi + 8u * kk, sdesc<BMN>(b + ob), (kin | kk) != 0);
+            mma_ts<BMN, CG>(d, ahi + 8u * kk, sdesc<BMN>(blo + ob), 1);
+            mma_ts<BMN, CG>(d, alo + 8u * kk, sdesc<BMN>(b + ob), 1);
           }
-          mma_commit(&empty[s]);
+          commit_cg<CG>(&empty[s]);
+          if (NS > TC_ASLOTS) commit_cg<CG>(&afree[g % TC_ASLOTS]);
           if (kin == TC_CH - 1 || kb == nk - 1) {
-            mma_commit(&tfull[buf]);
+            commit_cg<CG>(&tfull[buf]);
             ++c;
           }
         }
@@ -375,12 +444,12 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     const int q = warp & 3, h = (warp - 2) >> 2;
     const int r = q * 32 + lane;  // tile row == TMEM lane
     int g = 0;
-    for (int w = blockIdx.x; w < works; w += gridDim.x) {
+    for (int w = unit; w < works; w += units) {
       int m0, n0, z, nk;
       decode(w, m0, n0, z, nk);
       for (int kb = 0; kb < nk; ++kb, ++g) {
-        const int s = g % TC_STAGES;
-        const uint32_t ph = (g / TC_STAGES) & 1;
+        const int s = g % NS;
+        const uint32_t ph = (g / NS) & 1;
         mbar_wait(&full[s], ph);
         float v[16];
         load_a_row16<AMN>(sA(s), r, h * 16, v);
@@ -392,25 +461,29 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           hi[j] = __float_as_uint(x);
           lo[j] = __float_as_uint(l);
         }
-        // MMA of this stage's previous round has finished (empty[s] -> TMA ->
-        // full[s]), so its TMEM A columns are free to overwrite
+        // the MMAs of k-block g - TC_ASLOTS have finished reading this TMEM A slot
+        const int as = g % TC_ASLOTS;
+        // (NS == TC_ASLOTS: implied by empty[s] -> TMA -> full[s])
+        if (NS > TC_ASLOTS && g >= TC_ASLOTS) mbar_wait(&afree[as], ((g / TC_ASLOTS) - 1) & 1);
         tc_fence_after();
-        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + 64u * s + 16u * h;
+        const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + 64u * (uint32_t)as + 16u * h;
         tmem_st16(ta, hi);
         tmem_st16(ta + 32u, lo);
-        if (!BPRE) split_tile(sB(s), sBlo(s), ct);
+        if (!BPRE) split_tile<CG>(sB(s), sBlo(s), ct);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         fence_proxy_async();
         tc_fence_before();
-        mbar_arrive(&conv[s]);
+        named_sync(1, 256);
+        if (ct == 0) arrive_leader<CG>(&conv[s]);
       }
     }
   } else {
     // ---- drain + epilogue (256 threads) ----
     const int q = warp & 3;               // TMEM lane quarter
     const int half = (warp - 10) >> 2;    // column half of the 128-wide tile
+    const int et = threadIdx.x - 320;
     int c = 0;
-    for (int w = blockIdx.x; w < works; w += gridDim.x) {
+    for (int w = unit; w < works; w += units) {
       int m0, n0, z, nk;
       decode(w, m0, n0, z, nk);
       float acc[64];
@@ -430,7 +503,8 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           for (int j = 0; j < 16; ++j) acc[c0 + j] = __fadd_rn(acc[c0 + j], __uint_as_float(r[j]));
         }
         tc_fence_before();
-        mbar_arrive(&tempty[buf]);
+        named_sync(2, TC_EPI_T);
+        if (et == 0) arrive_leader<CG>(&tempty[buf]);
       }
       // Epilogue through a per-warp smem transpose: the drain holds one ROW
       // per lane (tcgen05.ld 32x32b); stores want consecutive COLUMNS per
@@ -495,7 +569,13 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  if (CG == 2) cluster_sync_all();  // no CTA leaves while its peer may still signal it
+  if (warp == 1) {
+    if (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
 }
 
 // ---- host side ---------------------------------------------------------------
@@ -538,33 +618,93 @@ __global__ void k_split(const float* __restrict__ x, float* __restrict__ hi, flo
   }
 }
 
-template <bool AMN, bool BMN, bool BPRE>
-int launch(int M, int N, int K, const float* A, int lda, const float* B, const float* Blo, int ldb,
-           float* C, int ldc, int splits, const GemmEpi& ep, cudaStream_t s) {
+// CTA-pair (cta_group::2) mode for M > 128; KP_GEMM_CG=1 forces single-CTA tiles
+int choose_cg(int M) {
+  static const int force = [] {
+    const char* e = getenv("KP_GEMM_CG");
+    return e ? atoi(e) : 0;
+  }();
+  if (force == 1 || force == 2) return force;
+  return M > TC_BM ? 2 : 1;
+}
+
+// concurrently resident work units (CTAs or CTA pairs)
+template <bool AMN, bool BMN, bool BPRE, int CG>
+int resident_units() {
+  static int units = 0;
+  if (units) return units;
+  int sms = 0;
+  KP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  units = sms / CG;
+  if (CG > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * CG, 1, 1);
+    cfg.blockDim = dim3(TC_WARPS * 32, 1, 1);
+    cfg.dynamicSmemBytes = TcCfg<CG>::SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CG;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_tc_gemm<AMN, BMN, BPRE, CG>, &cfg) == cudaSuccess && n > 0)
+      units = std::min(units, n);
+    cudaGetLastError();
+  }
+  return units;
+}
+
+template <bool AMN, bool BMN, bool BPRE, int CG>
+int launch_cg(int M, int N, int K, const float* A, int lda, const float* B, const float* Blo, int ldb,
+              float* C, int ldc, int splits, const GemmEpi& ep, cudaStream_t s) {
+  using Cfg = TcCfg<CG>;
   CUtensorMap ta, tb, tbl;
-  // K-major: [rows][K] with 128-row boxes; MN-major: [K][rows] with 32x32 boxes
-  auto mk = [&](CUtensorMap* m, const float* p, bool mn, int rows, int ld) {
-    return mn ? make_map(m, p, K, rows, ld, 32, true) : make_map(m, p, rows, K, ld, TC_BM);
+  // K-major: [rows][K] with box_rows-row boxes; MN-major: [K][rows] with 32x32 boxes
+  auto mk = [&](CUtensorMap* m, const float* p, bool mn, int rows, int ld, int box_rows) {
+    return mn ? make_map(m, p, K, rows, ld, 32, true) : make_map(m, p, rows, K, ld, box_rows);
   };
-  const bool ok = mk(&ta, A, AMN, M, lda) && mk(&tb, B, BMN, N, ldb) &&
-                  (!BPRE || mk(&tbl, Blo, BMN, N, ldb));
+  const bool ok = mk(&ta, A, AMN, M, lda, TC_BM) && mk(&tb, B, BMN, N, ldb, Cfg::BROWS) &&
+                  (!BPRE || mk(&tbl, Blo, BMN, N, ldb, Cfg::BROWS));
   if (!BPRE) tbl = tb;
   KP_CHECK(ok, kErrCuda, "cuTensorMapEncodeTiled failed");
   static bool attr = false;
   if (!attr) {
-    KP_CUDA(cudaFuncSetAttribute(k_tc_gemm<AMN, BMN, BPRE>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    KP_CUDA(cudaFuncSetAttribute(k_tc_gemm<AMN, BMN, BPRE, CG>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     attr = true;
   }
   int kps = (K + splits - 1) / splits;
   kps = (kps + TC_BK - 1) / TC_BK * TC_BK;
   const unsigned nz = ceil_div(K, kps);
-  const uint64_t works = (uint64_t)ceil_div(N, TC_BN) * ceil_div(M, TC_BM) * nz;
-  static int sms = 0;
-  if (!sms) KP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  const unsigned grid = (unsigned)std::min<uint64_t>(works, (uint64_t)sms);
-  k_tc_gemm<AMN, BMN, BPRE><<<grid, TC_WARPS * 32, SMEM_BYTES, s>>>(ta, tb, tbl, M, N, K, kps, C, ldc, ep); ::kp::count_launch();
+  const uint64_t works = (uint64_t)ceil_div(N, TC_BN) * ceil_div(M, TC_BM * CG) * nz;
+  const int units = resident_units<AMN, BMN, BPRE, CG>();
+  const unsigned grid = (unsigned)std::min<uint64_t>(works, (uint64_t)units) * CG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(TC_WARPS * 32, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  KP_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<AMN, BMN, BPRE, CG>, ta, tb, tbl, M, N, K, kps, C, ldc,
+                             ep));
+  ::kp::count_launch();
   return (int)nz;
+}
+
+template <bool AMN, bool BMN, bool BPRE>
+int launch(int M, int N, int K, const float* A, int lda, const float* B, const float* Blo, int ldb,
+           float* C, int ldc, int splits, const GemmEpi& ep, cudaStream_t s) {
+  if (choose_cg(M) == 2)
+    return launch_cg<AMN, BMN, BPRE, 2>(M, N, K, A, lda, B, Blo, ldb, C, ldc, splits, ep, s);
+  return launch_cg<AMN, BMN, BPRE, 1>(M, N, K, A, lda, B, Blo, ldb, C, ldc, splits, ep, s);
 }
 
 }  // namespace
@@ -589,17 +729,19 @@ void split_hilo(const float* x, float* hi, float* lo, size_t n, cudaStream_t s) 
   k_split<<<g ? g : 1, 256, 0, s>>>(x, hi, lo, n); ::kp::count_launch();
 }
 
-// split-K count: best wave efficiency (CTAs / (waves * 148)) with >= 16
-// k-blocks per split; ties go to fewer splits (less partial traffic)
+// split-K count: best wave efficiency (units / (waves * resident units)) with
+// >= 16 k-blocks per split; ties go to fewer splits (less partial traffic)
 int tc_splits(int M, int N, int K) {
-  const int tiles = (int)(ceil_div(M, TC_BM) * ceil_div(N, TC_BN));
+  const int cg = choose_cg(M);
+  const int tiles = (int)(ceil_div(M, TC_BM * cg) * ceil_div(N, TC_BN));
+  const int slots = cg == 2 ? resident_units<true, true, false, 2>() : resident_units<true, true, false, 1>();
   const int max_sp = std::max(1, std::min(16, K / 512));
   int best = 1;
   double best_eff = 0;
   for (int sp = 1; sp <= max_sp; ++sp) {
-    const int ctas = tiles * sp;
-    const int waves = (ctas + 147) / 148;
-    const double eff = (double)ctas / (waves * 148.0) - 0.004 * sp;
+    const int u = tiles * sp;
+    const int waves = (u + slots - 1) / slots;
+    const double eff = (double)u / ((double)waves * slots) - 0.004 * sp;
     if (eff > best_eff + 1e-9) best_eff = eff, best = sp;
   }
   return best;

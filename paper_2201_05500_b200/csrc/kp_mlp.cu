@@ -12,6 +12,8 @@
 // with sigmoid, loss and the upstream gradient. fp32 keeps the stated
 // tolerance against the reference; the tcgen05 (3xTF32) replacement is the
 // next step.
+#include <cstdlib>
+
 #include "kp_internal.cuh"
 
 namespace kp {
@@ -369,6 +371,14 @@ void reduce_splits(const float* part, int splits, size_t n, float* out, cudaStre
   k_reduce_splits<<<grid_cap(ceil_div(n, 256)), 256, 0, s>>>(part, splits, n, out); ::kp::count_launch();
 }
 
+static bool gemm_pre() {
+  static const bool on = [] {
+    const char* e = getenv("KP_GEMM_PRE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_t B,
                  float* d_preds, MlpWs& ws, cudaStream_t s) {
   if (B == 0) return;
@@ -382,8 +392,12 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
     if (tc_enabled() && tc_gemm_supported(B, N, K, in, K, W, K)) {
       float* whi = ws.whi.get<float>((size_t)N * K);
       float* wlo = ws.wlo.get<float>((size_t)N * K);
-      split_hilo(W, whi, wlo, (size_t)N * K, s);
-      tc_gemm_nt_pre(B, N, K, in, K, whi, wlo, K, out, N, ep, s);
+      if (gemm_pre()) {
+        split_hilo(W, whi, wlo, (size_t)N * K, s);
+        tc_gemm_nt_pre(B, N, K, in, K, whi, wlo, K, out, N, ep, s);
+      } else {
+        tc_gemm_nt(B, N, K, in, K, W, K, out, N, ep, s);
+      }
     } else {
       gemm<true, true>(B, N, K, in, K, W, K, out, N, 1, ep, s);
     }
@@ -416,8 +430,12 @@ void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, c
     k_transpose<<<g, dim3(32, 8), 0, s>>>(W, N, K, wt); ::kp::count_launch();
     float* wthi = ws.wthi.get<float>((size_t)N * K);
     float* wtlo = ws.wtlo.get<float>((size_t)N * K);
-    split_hilo(wt, wthi, wtlo, (size_t)N * K, s);
-    tc_gemm_nt_pre(B, K, N, dZ, N, wthi, wtlo, N, out, K, ep, s);
+    if (gemm_pre()) {
+      split_hilo(wt, wthi, wtlo, (size_t)N * K, s);
+      tc_gemm_nt_pre(B, K, N, dZ, N, wthi, wtlo, N, out, K, ep, s);
+    } else {
+      tc_gemm_nt(B, K, N, dZ, N, wt, N, out, K, ep, s);
+    }
   } else {
     gemm<true, false>(B, K, N, dZ, N, W, K, out, K, 1, ep, s);
   }
