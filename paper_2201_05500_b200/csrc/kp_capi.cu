@@ -78,7 +78,7 @@ std::atomic<uint64_t> g_launches{0};
 void kp::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 struct MergeWs {
-  DevBuf allg, cm, terms;
+  DevBuf allg, cm, terms, chunk, full;
 };
 
 struct kp_table {
@@ -89,6 +89,7 @@ struct kp_table {
 
 struct kp_comm {
   ncclComm_t nc = nullptr;
+  ncclComm_t nc2 = nullptr;  // second channel: gradient exchange overlapping the GEMM
   int rank = 0, world = 1, device = 0;
 };
 
@@ -105,6 +106,10 @@ struct kp_trainer {
   float *x = nullptr, *m = nullptr, *v = nullptr, *vbar = nullptr, *g = nullptr;
   uint64_t D = 0;
   uint64_t t_global = 0, merges = 0;
+  // all replicas (every worker on every rank) hold the same x: initial state
+  // and right after a merge. Cleared by local steps and set_worker_state
+  // (which, with several ranks, must be called symmetrically on all of them).
+  bool x_uniform = true;
   // inputs
   DevBuf in_offs, in_keys, in_slots, in_labels;
   std::vector<uint32_t> h_offs;
@@ -117,6 +122,9 @@ struct kp_trainer {
     cudaEvent_t ev = nullptr;
   } stage[2];
   cudaStream_t copy_s = nullptr;
+  // gradient exchange stream (G > 1): the all-to-all overlaps the last GEMM
+  cudaStream_t xs = nullptr;
+  cudaEvent_t ev_dinput = nullptr, ev_xdone = nullptr;
   // step buffers
   DevBuf st_offs, st_keys, st_slots, st_labels;
   DedupWs dd, dd_owner;
@@ -179,6 +187,9 @@ struct kp_trainer {
     for (auto& st : stage)
       if (st.ev) cudaEventDestroy(st.ev);
     if (copy_s) cudaStreamDestroy(copy_s);
+    if (xs) cudaStreamDestroy(xs);
+    if (ev_dinput) cudaEventDestroy(ev_dinput);
+    if (ev_xdone) cudaEventDestroy(ev_xdone);
     if (tab.t) table_destroy(tab.t);
     if (tab.s) cudaStreamDestroy(tab.s);
     cudaFree(x);
@@ -194,7 +205,10 @@ namespace {
 
 void all_to_all(kp_trainer* tr, const void* send, const std::vector<uint64_t>& scnt,
                 const std::vector<uint64_t>& soff, void* recv, const std::vector<uint64_t>& rcnt,
-                const std::vector<uint64_t>& roff, size_t elem, ncclDataType_t dt) {
+                const std::vector<uint64_t>& roff, size_t elem, ncclDataType_t dt,
+                cudaStream_t st = nullptr, ncclComm_t nc = nullptr) {
+  if (!st) st = tr->s;
+  if (!nc) nc = tr->comm->nc;
   const int R = tr->world, me = tr->rank;
   auto* sb = static_cast<const char*>(send);
   auto* rb = static_cast<char*>(recv);
@@ -202,39 +216,87 @@ void all_to_all(kp_trainer* tr, const void* send, const std::vector<uint64_t>& s
   const size_t per = elem / dts;  // datatype elements per logical element
   if (scnt[me])
     KP_CUDA(cudaMemcpyAsync(rb + roff[me] * elem, sb + soff[me] * elem, scnt[me] * elem,
-                            cudaMemcpyDeviceToDevice, tr->s));
+                            cudaMemcpyDeviceToDevice, st));
   KP_NCCL(ncclGroupStart());
   for (int p = 0; p < R; ++p) {
     if (p == me) continue;
-    if (scnt[p]) KP_NCCL(ncclSend(sb + soff[p] * elem, scnt[p] * per, dt, p, tr->comm->nc, tr->s));
-    if (rcnt[p]) KP_NCCL(ncclRecv(rb + roff[p] * elem, rcnt[p] * per, dt, p, tr->comm->nc, tr->s));
+    if (scnt[p]) KP_NCCL(ncclSend(sb + soff[p] * elem, scnt[p] * per, dt, p, nc, st));
+    if (rcnt[p]) KP_NCCL(ncclRecv(rb + roff[p] * elem, rcnt[p] * per, dt, p, nc, st));
   }
   KP_NCCL(ncclGroupEnd());
 }
 
-// gather [W][D] local blocks of every rank into out [N][D] (ascending global worker)
-void allgather_workers(kp_comm* comm, cudaStream_t s, const float* local, float* out, size_t n) {
-  if (!comm || comm->world == 1) {
-    if (out != local) KP_CUDA(cudaMemcpyAsync(out, local, n * 4, cudaMemcpyDeviceToDevice, s));
-    return;
+
+// Chunked exchange for the merge (SURVEY.md 8e "recommended merge for large
+// D"): rank c owns chunk c = [c*C, c*C + len_c) of the D parameters and
+// receives every global worker's slice of it, [N][C] in ascending global
+// worker order (rank-major, then local worker).
+void exchange_chunks(kp_comm* comm, cudaStream_t s, uint32_t W, uint64_t D, uint64_t C,
+                     const float* src, float* dst) {
+  const int R = comm->world, me = comm->rank;
+  const uint64_t my_len = std::min<uint64_t>(C, D > me * C ? D - me * C : 0);
+  KP_NCCL(ncclGroupStart());
+  for (int p = 0; p < R; ++p) {
+    const uint64_t len_p = std::min<uint64_t>(C, D > p * C ? D - p * C : 0);
+    for (uint32_t l = 0; l < W; ++l) {
+      const float* sp = src + (size_t)l * D + (size_t)p * C;
+      float* rp = dst + ((size_t)p * W + l) * C;
+      if (p == me) {
+        if (my_len) KP_CUDA(cudaMemcpyAsync(dst + ((size_t)me * W + l) * C, sp, my_len * 4,
+                                            cudaMemcpyDeviceToDevice, s));
+        continue;
+      }
+      if (len_p) KP_NCCL(ncclSend(sp, len_p, ncclFloat32, p, comm->nc, s));
+      if (my_len) KP_NCCL(ncclRecv(rp, my_len, ncclFloat32, p, comm->nc, s));
+    }
   }
-  KP_NCCL(ncclAllGather(local, out, n, ncclFloat32, comm->nc, s));
+  KP_NCCL(ncclGroupEnd());
 }
 
 // global_merge (optimizer.cpp:56-84) over W local workers x all ranks; moments
 // already accumulated. v_bar = cmean(v_i); x_i = cmean(x_j - a m_j/sqrt(v_bar)).
+// Multi-rank: two rounds (v, then the term) of chunk exchange -> owner
+// centered mean over its chunk -> allgather, ~2*2*(R-1)/R*4D bytes per rank.
+// The centered mean is elementwise in a fixed worker order, so the result is
+// bitwise the one a single process computes over all N workers.
 void merge_states(kp_comm* comm, cudaStream_t s, uint32_t W, uint64_t D, float* x, float* m,
                   float* v, float* vbar, float alpha, bool reset, MergeWs& ws) {
-  const uint32_t N = W * (comm ? comm->world : 1);
   const bool local = !comm || comm->world == 1;
-  float* all = local ? nullptr : ws.allg.get<float>((size_t)N * D);
   float* vb = ws.cm.get<float>(D);
   float* terms = ws.terms.get<float>((size_t)W * D);
-  if (!local) allgather_workers(comm, s, v, all, (size_t)W * D);
-  centered_mean(local ? v : all, D, N, D, vb, s);
-  for (uint32_t l = 0; l < W; ++l) merge_terms(x + l * D, m + l * D, vb, D, alpha, terms + l * D, s);
-  if (!local) allgather_workers(comm, s, terms, all, (size_t)W * D);
-  centered_mean(local ? terms : all, D, N, D, x, s);  // merged x into worker 0
+  // small models / few ranks: one allgather per round beats the three-step
+  // chunked exchange on latency; same fixed-order arithmetic either way
+  const bool gather_all = !local && (uint64_t)(comm->world - 1) * W * D * 4 <= (24ull << 20);
+  if (local || gather_all) {
+    const uint32_t N = W * (local ? 1 : comm->world);
+    float* all = local ? nullptr : ws.allg.get<float>((size_t)N * D);
+    if (!local) KP_NCCL(ncclAllGather(v, all, (size_t)W * D, ncclFloat32, comm->nc, s));
+    centered_mean(local ? v : all, D, N, D, vb, s);
+    for (uint32_t l = 0; l < W; ++l) merge_terms(x + l * D, m + l * D, vb, D, alpha, terms + l * D, s);
+    if (!local) KP_NCCL(ncclAllGather(terms, all, (size_t)W * D, ncclFloat32, comm->nc, s));
+    centered_mean(local ? terms : all, D, N, D, x, s);  // merged x into worker 0
+  } else {
+    const int R = comm->world, me = comm->rank;
+    const uint32_t N = W * R;
+    const uint64_t C = (D + R - 1) / R;
+    const uint64_t my_len = std::min<uint64_t>(C, D > me * C ? D - me * C : 0);
+    float* recv = ws.allg.get<float>((size_t)N * C);
+    float* mine = ws.chunk.get<float>(C);
+    float* full = ws.full.get<float>((size_t)R * C);
+    // round 1: v_bar
+    exchange_chunks(comm, s, W, D, C, v, recv);
+    KP_CUDA(cudaMemsetAsync(mine, 0, C * 4, s));
+    if (my_len) centered_mean(recv, C, N, my_len, mine, s);
+    KP_NCCL(ncclAllGather(mine, full, C, ncclFloat32, comm->nc, s));
+    KP_CUDA(cudaMemcpyAsync(vb, full, D * 4, cudaMemcpyDeviceToDevice, s));
+    // round 2: x = cmean(x_j - a m_j / sqrt(v_bar))
+    for (uint32_t l = 0; l < W; ++l) merge_terms(x + l * D, m + l * D, vb, D, alpha, terms + l * D, s);
+    exchange_chunks(comm, s, W, D, C, terms, recv);
+    KP_CUDA(cudaMemsetAsync(mine, 0, C * 4, s));
+    if (my_len) centered_mean(recv, C, N, my_len, mine, s);
+    KP_NCCL(ncclAllGather(mine, full, C, ncclFloat32, comm->nc, s));
+    KP_CUDA(cudaMemcpyAsync(x, full, D * 4, cudaMemcpyDeviceToDevice, s));
+  }
   for (uint32_t l = 0; l < W; ++l) {
     if (l) KP_CUDA(cudaMemcpyAsync(x + l * D, x, D * 4, cudaMemcpyDeviceToDevice, s));
     KP_CUDA(cudaMemcpyAsync(vbar + l * D, vb, D * 4, cudaMemcpyDeviceToDevice, s));
@@ -243,12 +305,28 @@ void merge_states(kp_comm* comm, cudaStream_t s, uint32_t W, uint64_t D, float* 
 }
 
 void compute_xbar(kp_trainer* tr, float* out) {
-  float* all = tr->x;
-  if (tr->world > 1) {
-    all = tr->mws.allg.get<float>((size_t)tr->N * tr->D);
-    allgather_workers(tr->comm, tr->s, tr->x, all, (size_t)tr->W * tr->D);
+  const uint64_t D = tr->D;
+  if (tr->x_uniform) {
+    // every replica holds the same x (initial state, or just merged): the
+    // centered mean of identical vectors is that vector, bit for bit
+    KP_CUDA(cudaMemcpyAsync(out, tr->x, D * 4, cudaMemcpyDeviceToDevice, tr->s));
+    return;
   }
-  centered_mean(all, tr->D, tr->N, tr->D, out, tr->s);
+  if (tr->world == 1) {
+    centered_mean(tr->x, D, tr->N, D, out, tr->s);
+    return;
+  }
+  const int R = tr->world, me = tr->rank;
+  const uint64_t C = (D + R - 1) / R;
+  const uint64_t my_len = std::min<uint64_t>(C, D > me * C ? D - me * C : 0);
+  float* recv = tr->mws.allg.get<float>((size_t)tr->N * C);
+  float* mine = tr->mws.chunk.get<float>(C);
+  float* full = tr->mws.full.get<float>((size_t)R * C);
+  exchange_chunks(tr->comm, tr->s, tr->W, D, C, tr->x, recv);
+  KP_CUDA(cudaMemsetAsync(mine, 0, C * 4, tr->s));
+  if (my_len) centered_mean(recv, C, tr->N, my_len, mine, tr->s);
+  KP_NCCL(ncclAllGather(mine, full, C, ncclFloat32, tr->comm->nc, tr->s));
+  KP_CUDA(cudaMemcpyAsync(out, full, D * 4, cudaMemcpyDeviceToDevice, tr->s));
 }
 
 struct StepView {
@@ -364,6 +442,48 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
   const float* invc = static_cast<const float*>(tr->inv_count.p);
   float* dpooled = tr->dpooled.get<float>((size_t)std::max<uint32_t>(sv.n_inst, 1) * in_w);
   float* preds = tr->preds.get<float>(std::max<uint32_t>(sv.n_inst, 1));
+  SparseRule rule{tr->cfg.sparse_rule, (float)tr->cfg.sparse_lr, (float)tr->cfg.sparse_beta1,
+                  (float)tr->cfg.sparse_beta2};
+  const float inv_n = (float)(1.0 / (double)tr->N);
+  // G > 1: per-unique gradients for the owners, then the all-to-all. With
+  // overlap (default), both are issued right after the first layer's input
+  // gradient: the reduction on the compute stream, the all-to-all on the
+  // exchange stream (own NCCL channel) while the weight-gradient GEMM runs on
+  // all but kXReserve SMs.
+  float* sgr = nullptr;
+  float* rgr = nullptr;
+  uint64_t Rn = 0;
+  if (tr->world > 1) {
+    sgr = tr->send_grads.get<float>((size_t)std::max<uint32_t>(pr.U, 1) * tr->e);
+    for (auto c : tr->cnt_recv) Rn += c;
+    rgr = tr->recv_grads.get<float>((size_t)std::max<uint64_t>(Rn, 1) * tr->e);
+  }
+  auto send_grads = [&] {
+    seg_reduce_apply(tr->dd.d_seg, pr.U, tr->dd.d_sorted_mapped, nullptr, sv.n_occ, dpooled, tr->e,
+                     1.0f, nullptr, nullptr, rule, sgr, static_cast<const uint32_t*>(tr->pos.p),
+                     tr->sg, s);
+  };
+  static const int reserve = [] {
+    const char* e = getenv("KP_XRESERVE");
+    return e ? atoi(e) : 16;
+  }();
+  const bool overlap = tr->world > 1 && reserve > 0;
+  bool exchanged = false;
+  std::function<void()> hook = [&] {
+    send_grads();
+    if (!tr->xs) {
+      KP_CUDA(cudaStreamCreateWithFlags(&tr->xs, cudaStreamNonBlocking));
+      KP_CUDA(cudaEventCreateWithFlags(&tr->ev_dinput, cudaEventDisableTiming));
+      KP_CUDA(cudaEventCreateWithFlags(&tr->ev_xdone, cudaEventDisableTiming));
+    }
+    KP_CUDA(cudaEventRecord(tr->ev_dinput, s));
+    KP_CUDA(cudaStreamWaitEvent(tr->xs, tr->ev_dinput, 0));
+    all_to_all(tr, sgr, tr->cnt_send, tr->off_send, rgr, tr->cnt_recv, tr->off_recv,
+               4 * (size_t)tr->e, ncclFloat32, tr->xs, tr->comm->nc2);
+    KP_CUDA(cudaEventRecord(tr->ev_xdone, tr->xs));
+    tc_reserve_sms(reserve);
+    exchanged = true;
+  };
   for (uint32_t l = 0; l < tr->W; ++l) {
     const uint32_t lo = sv.wlo[l], hi = sv.whi[l], Bw = hi - lo;
     if (Bw == 0) {
@@ -374,30 +494,26 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
     mlp_backward(tr->shape, tr->x + l * D, pooled + (size_t)lo * in_w, Bw, preds + lo,
                  sv.labels + lo, tr->g + l * D, dpooled + (size_t)lo * in_w,
                  tr->cfg.pooling == 1 ? invc + (size_t)lo * tr->S : nullptr, tr->S, tr->e,
-                 d_loss_slot, tr->mlp, s);
+                 d_loss_slot, tr->mlp, s, (overlap && l + 1 == tr->W) ? &hook : nullptr);
   }
+  tc_reserve_sms(0);
   if (fused_preds)
     KP_CUDA(cudaMemcpyAsync(fused_preds, preds, (size_t)sv.n_inst * 4, cudaMemcpyDeviceToDevice, s));
   tr->mark(3);
   // sparse push (x 1/N, trainer.cpp:202-207)
-  SparseRule rule{tr->cfg.sparse_rule, (float)tr->cfg.sparse_lr, (float)tr->cfg.sparse_beta1,
-                  (float)tr->cfg.sparse_beta2};
-  const float inv_n = (float)(1.0 / (double)tr->N);
   if (tr->world == 1) {
     seg_reduce_apply(tr->dd.d_seg, pr.U, tr->dd.d_sorted_mapped, nullptr, sv.n_occ, dpooled, tr->e,
                      inv_n, tr->tab.t, pr.idx, rule, nullptr, nullptr, tr->sg, s);
     tr->mark(4);
   } else {
-    float* sgr = tr->send_grads.get<float>((size_t)std::max<uint32_t>(pr.U, 1) * tr->e);
-    seg_reduce_apply(tr->dd.d_seg, pr.U, tr->dd.d_sorted_mapped, nullptr, sv.n_occ, dpooled, tr->e,
-                     1.0f, nullptr, nullptr, rule, sgr, static_cast<const uint32_t*>(tr->pos.p),
-                     tr->sg, s);
-    tr->mark(4);
-    uint64_t Rn = 0;
-    for (auto c : tr->cnt_recv) Rn += c;
-    float* rgr = tr->recv_grads.get<float>((size_t)std::max<uint64_t>(Rn, 1) * tr->e);
-    all_to_all(tr, sgr, tr->cnt_send, tr->off_send, rgr, tr->cnt_recv, tr->off_recv,
-               4 * (size_t)tr->e, ncclFloat32);
+    if (exchanged) {
+      KP_CUDA(cudaStreamWaitEvent(s, tr->ev_xdone, 0));
+    } else {
+      send_grads();
+      tr->mark(4);
+      all_to_all(tr, sgr, tr->cnt_send, tr->off_send, rgr, tr->cnt_recv, tr->off_recv,
+                 4 * (size_t)tr->e, ncclFloat32);
+    }
     tr->mark(6);
     seg_reduce_apply(tr->dd_owner.d_seg, tr->dd_owner.n_unique, tr->dd_owner.sorted_vals, nullptr,
                      (uint32_t)Rn, rgr, tr->e, inv_n, tr->tab.t,
@@ -413,11 +529,13 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
     for (uint32_t l = 0; l < tr->W; ++l)
       dense_local_step(tr->x + l * D, tr->m + l * D, tr->v + l * D, tr->vbar + l * D, tr->g + l * D,
                        D, h, s);
+    tr->x_uniform = false;
   } else {
     for (uint32_t l = 0; l < tr->W; ++l) dense_moments(tr->m + l * D, tr->v + l * D, tr->g + l * D, D, h, s);
     merge_states(tr->comm, s, tr->W, D, tr->x, tr->m, tr->v, tr->vbar, h.alpha,
                  tr->cfg.reset_local_v != 0, tr->mws);
     tr->merges++;
+    tr->x_uniform = true;
   }
   tr->t_global = t;
   uint32_t* chk = static_cast<uint32_t*>(tr->check.p);
@@ -965,6 +1083,7 @@ int kp_comm_init(const uint8_t id[128], int rank, int world, int device, kp_comm
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
     KP_NCCL(ncclCommInitRank(&c->nc, world, u, rank));
+    KP_NCCL(ncclCommSplit(c->nc, 0, rank, &c->nc2, nullptr));
     c->rank = rank;
     c->world = world;
     c->device = device;
@@ -974,6 +1093,7 @@ int kp_comm_init(const uint8_t id[128], int rank, int world, int device, kp_comm
 int kp_comm_destroy(kp_comm* c) {
   return guard([&] {
     if (!c) return;
+    if (c->nc2) ncclCommDestroy(c->nc2);
     if (c->nc) ncclCommDestroy(c->nc);
     delete c;
   });
@@ -1147,6 +1267,7 @@ int kp_trainer_worker_state(kp_trainer* tr, uint32_t l, float* x, float* m, floa
     KP_CHECK(l < tr->W, kErrGeneric, "worker index out of range");
     KP_CUDA(cudaSetDevice(tr->device));
     const uint64_t D = tr->D;
+    if (x) tr->x_uniform = false;
     if (x) KP_CUDA(cudaMemcpyAsync(x, tr->x + l * D, D * 4, cudaMemcpyDeviceToHost, tr->s));
     if (m) KP_CUDA(cudaMemcpyAsync(m, tr->m + l * D, D * 4, cudaMemcpyDeviceToHost, tr->s));
     if (v) KP_CUDA(cudaMemcpyAsync(v, tr->v + l * D, D * 4, cudaMemcpyDeviceToHost, tr->s));
@@ -1161,6 +1282,7 @@ int kp_trainer_set_worker_state(kp_trainer* tr, uint32_t l, const float* x, cons
     KP_CHECK(l < tr->W, kErrGeneric, "worker index out of range");
     KP_CUDA(cudaSetDevice(tr->device));
     const uint64_t D = tr->D;
+    if (x) tr->x_uniform = false;
     if (x) KP_CUDA(cudaMemcpyAsync(tr->x + l * D, x, D * 4, cudaMemcpyHostToDevice, tr->s));
     if (m) KP_CUDA(cudaMemcpyAsync(tr->m + l * D, m, D * 4, cudaMemcpyHostToDevice, tr->s));
     if (v) KP_CUDA(cudaMemcpyAsync(tr->v + l * D, v, D * 4, cudaMemcpyHostToDevice, tr->s));

@@ -618,6 +618,8 @@ __global__ void k_split(const float* __restrict__ x, float* __restrict__ hi, flo
   }
 }
 
+thread_local int g_reserve_sms = 0;
+
 // CTA-pair (cta_group::2) mode for M > 128; KP_GEMM_CG=1 forces single-CTA tiles
 int choose_cg(int M) {
   static const int force = [] {
@@ -679,7 +681,7 @@ int launch_cg(int M, int N, int K, const float* A, int lda, const float* B, cons
   kps = (kps + TC_BK - 1) / TC_BK * TC_BK;
   const unsigned nz = ceil_div(K, kps);
   const uint64_t works = (uint64_t)ceil_div(N, TC_BN) * ceil_div(M, TC_BM * CG) * nz;
-  const int units = resident_units<AMN, BMN, BPRE, CG>();
+  const int units = std::max(1, resident_units<AMN, BMN, BPRE, CG>() - (g_reserve_sms + CG - 1) / CG);
   const unsigned grid = (unsigned)std::min<uint64_t>(works, (uint64_t)units) * CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
@@ -709,6 +711,8 @@ int launch(int M, int N, int K, const float* A, int lda, const float* B, const f
 
 }  // namespace
 
+void tc_reserve_sms(int n) { g_reserve_sms = n < 0 ? 0 : n; }
+
 bool tc_enabled() {
   static const bool on = [] {
     const char* e = getenv("KP_GEMM");
@@ -734,7 +738,9 @@ void split_hilo(const float* x, float* hi, float* lo, size_t n, cudaStream_t s) 
 int tc_splits(int M, int N, int K) {
   const int cg = choose_cg(M);
   const int tiles = (int)(ceil_div(M, TC_BM * cg) * ceil_div(N, TC_BN));
-  const int slots = cg == 2 ? resident_units<true, true, false, 2>() : resident_units<true, true, false, 1>();
+  const int slots = std::max(1, (cg == 2 ? resident_units<true, true, false, 2>()
+                                         : resident_units<true, true, false, 1>()) -
+                                     (g_reserve_sms + cg - 1) / cg);
   const int max_sp = std::max(1, std::min(16, K / 512));
   int best = 1;
   double best_eff = 0;

@@ -1,6 +1,8 @@
 // Internal (C++) interfaces between the kernel files; the C ABI in
 // include/kpsim_b200.h is built on these.
 #pragma once
+
+#include <functional>
 #include "kp_common.cuh"
 
 namespace kp {
@@ -137,6 +139,9 @@ int tc_gemm_tn(int M, int N, int K, const float* A, int lda, const float* B, int
 int tc_splits(int M, int N, int K);
 void split_hilo(const float* x, float* hi, float* lo, size_t n, cudaStream_t s);
 bool tc_enabled();  // KP_GEMM=simt disables the tensor-core path
+// leave `n` SMs free of persistent GEMM CTAs (for kernels overlapping the GEMM
+// on another stream, e.g. NCCL); 0 = use every SM
+void tc_reserve_sms(int n);
 // C = A . B^T on the SIMT fp32 path (reference engine for the tensor-core path)
 void simt_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
                   int ldc, cudaStream_t s);
@@ -165,9 +170,13 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
                  float* d_preds, MlpWs& ws, cudaStream_t s);
 // Backward: d_grad[D] (overwritten), d_dinput[B][in] scaled by d_coeff
 // (per bag; null = 1), loss sum (f64, device) accumulated into d_loss.
+// `after_dinput` (optional) runs right after d_dinput is enqueued and before
+// the first layer's weight gradient, so a caller can start consuming it
+// (e.g. the gradient exchange) while the last GEMM runs.
 void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32_t B,
                   const float* d_preds, const int32_t* d_labels, float* d_grad, float* d_dinput, const float* d_coeff,
-                  uint32_t S, uint32_t e, double* d_loss_sum, MlpWs& ws, cudaStream_t s);
+                  uint32_t S, uint32_t e, double* d_loss_sum, MlpWs& ws, cudaStream_t s,
+                  const std::function<void()>* after_dinput = nullptr);
 
 // -------------------------------------------------------------- dense ----
 struct AdamParams {

@@ -453,7 +453,7 @@ void colsum(const float* X, const float* w, int B, int N, float* out, MlpWs& ws,
 void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32_t B,
                   const float* d_preds, const int32_t* d_labels, float* d_grad, float* d_dinput,
                   const float* d_coeff, uint32_t S, uint32_t e, double* d_loss_sum, MlpWs& ws,
-                  cudaStream_t s) {
+                  cudaStream_t s, const std::function<void()>* after_dinput) {
   const uint32_t L = m.n_layers;
   if (B == 0) {
     KP_CUDA(cudaMemsetAsync(d_grad, 0, m.D * 4, s));
@@ -488,6 +488,13 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
     const int N = m.widths[l + 1], K = m.widths[l];
     float* dZ = static_cast<float*>(ws.dz[cur].p);
     const float* in = layer_in(l);
+    // first layer: the input gradient goes first so its consumer can overlap
+    // the weight-gradient GEMM
+    if (l == 0 && d_dinput) {
+      EpiArgs ep{d_coeff ? kCoeff : kStore, 0, nullptr, nullptr, 0, d_coeff, S, e};
+      dx_gemm(B, K, N, dZ, d_x + m.w_off[l], d_dinput, ep, ws, s);
+      if (after_dinput) (*after_dinput)();
+    }
     // dW_l[o][i] = sum_b dZ[b][o] in[b][i]   (deterministic split-K)
     EpiArgs plain{kStore, 0, nullptr, nullptr, 0, nullptr, 1, 1};
     if (tc_enabled() && tc_gemm_supported(N, K, B, dZ, N, in, K)) {
@@ -515,9 +522,6 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
       EpiArgs ep{kDAct, m.activation, nullptr, static_cast<const float*>(ws.act[l - 1].p), K, nullptr, 1, 1};
       dx_gemm(B, K, N, dZ, d_x + m.w_off[l], next, ep, ws, s);
       cur ^= 1;
-    } else if (d_dinput) {
-      EpiArgs ep{d_coeff ? kCoeff : kStore, 0, nullptr, nullptr, 0, d_coeff, S, e};
-      dx_gemm(B, K, N, dZ, d_x + m.w_off[l], d_dinput, ep, ws, s);
     }
   }
 }
