@@ -141,6 +141,19 @@ struct kp_trainer {
   DevBuf perm, pos, send_keys, recv_keys, owner_rows, owner_idx, send_rows, recv_rows, send_grads,
       recv_grads, counts_dev;
   std::vector<uint64_t> cnt_send, cnt_recv, off_send, off_recv;
+  std::vector<uint64_t> mat;  // [R][R] unique keys rank p sends to owner q (mat[p*R+q])
+  // NVLink peer windows (kp_peer.cu); mode -1 undecided, 0 NCCL, 1 peer
+  struct PeerWin {
+    void* local = nullptr;
+    size_t bytes = 0;
+    std::vector<void*> remote;
+  };
+  struct {
+    int mode = -1;
+    PeerWin keys, rows, grads, flags;
+    uint64_t seq[3] = {0, 0, 0};
+    DevBuf scratch;
+  } peer;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev;
@@ -188,6 +201,11 @@ struct kp_trainer {
       if (st.ev) cudaEventDestroy(st.ev);
     if (copy_s) cudaStreamDestroy(copy_s);
     if (xs) cudaStreamDestroy(xs);
+    for (PeerWin* w : {&peer.keys, &peer.rows, &peer.grads, &peer.flags}) {
+      for (size_t p = 0; p < w->remote.size(); ++p)
+        if (w->remote[p] && w->remote[p] != w->local) cudaIpcCloseMemHandle(w->remote[p]);
+      if (w->local) cudaFree(w->local);
+    }
     if (ev_dinput) cudaEventDestroy(ev_dinput);
     if (ev_xdone) cudaEventDestroy(ev_xdone);
     if (tab.t) table_destroy(tab.t);
@@ -347,6 +365,138 @@ struct PullResult {
   uint32_t U;
 };
 
+// ---- NVLink peer windows ------------------------------------------------
+// all ranks: min over ranks of `ok` (also a barrier)
+bool all_ok(kp_trainer* tr, bool ok) {
+  int* d = tr->peer.scratch.get<int>(2);
+  const int h = ok ? 1 : 0;
+  KP_CUDA(cudaMemcpyAsync(d, &h, 4, cudaMemcpyHostToDevice, tr->s));
+  KP_NCCL(ncclAllReduce(d, d + 1, 1, ncclInt32, ncclMin, tr->comm->nc, tr->s));
+  int r = 0;
+  KP_CUDA(cudaMemcpyAsync(&r, d + 1, 4, cudaMemcpyDeviceToHost, tr->s));
+  KP_CUDA(cudaStreamSynchronize(tr->s));
+  return r == 1;
+}
+
+void win_release(kp_trainer* tr, kp_trainer::PeerWin& w) {
+  if (!w.local) return;
+  KP_CUDA(cudaStreamSynchronize(tr->s));
+  all_ok(tr, true);  // every rank is past its last use of the window
+  for (size_t p = 0; p < w.remote.size(); ++p)
+    if (w.remote[p] && w.remote[p] != w.local) cudaIpcCloseMemHandle(w.remote[p]);
+  all_ok(tr, true);  // every mapping of ours is closed
+  KP_CUDA(cudaFree(w.local));
+  w.local = nullptr;
+  w.remote.clear();
+  w.bytes = 0;
+}
+
+// collective: (re)allocate a window of `bytes` on every rank and map the peers'
+bool win_alloc(kp_trainer* tr, kp_trainer::PeerWin& w, size_t bytes) {
+  const int R = tr->world, me = tr->rank;
+  win_release(tr, w);
+  KP_CUDA(cudaMalloc(&w.local, bytes));
+  KP_CUDA(cudaMemset(w.local, 0, bytes));
+  w.bytes = bytes;
+  cudaIpcMemHandle_t h;
+  bool ok = cudaIpcGetMemHandle(&h, w.local) == cudaSuccess;
+  cudaGetLastError();
+  char* d = tr->peer.scratch.get<char>((size_t)R * 64 + 64);
+  KP_CUDA(cudaMemcpyAsync(d + (size_t)me * 64, &h, 64, cudaMemcpyHostToDevice, tr->s));
+  KP_NCCL(ncclAllGather(d + (size_t)me * 64, d, 64, ncclChar, tr->comm->nc, tr->s));
+  std::vector<cudaIpcMemHandle_t> hs(R);
+  KP_CUDA(cudaMemcpyAsync(hs.data(), d, (size_t)R * 64, cudaMemcpyDeviceToHost, tr->s));
+  KP_CUDA(cudaStreamSynchronize(tr->s));
+  w.remote.assign(R, nullptr);
+  for (int p = 0; p < R; ++p) {
+    if (p == me) {
+      w.remote[p] = w.local;
+      continue;
+    }
+    if (ok && cudaIpcOpenMemHandle(&w.remote[p], hs[p], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      w.remote[p] = nullptr;
+      ok = false;
+    }
+  }
+  return ok;
+}
+
+// Decide (collectively) whether this step's exchange runs over peer windows,
+// growing them when the global counts matrix needs more room. Every rank holds
+// the same matrix, so every rank takes the same decisions.
+bool peer_ready(kp_trainer* tr) {
+  auto& P = tr->peer;
+  if (P.mode == 0) return false;
+  const int R = tr->world;
+  if (P.mode == -1) {
+    const char* e = getenv("KP_PEER");
+    if (R > kMaxPeers || (e && e[0] == '0')) {
+      P.mode = 0;
+      return false;
+    }
+  }
+  uint64_t maxcol = 1, maxrow = 1;
+  for (int r = 0; r < R; ++r) {
+    uint64_t c = 0, w = 0;
+    for (int p = 0; p < R; ++p) {
+      c += tr->mat[(size_t)p * R + r];
+      w += tr->mat[(size_t)r * R + p];
+    }
+    maxcol = std::max(maxcol, c);
+    maxrow = std::max(maxrow, w);
+  }
+  const size_t row = (size_t)tr->e * 4;
+  auto room = [](uint64_t n, size_t b) { return (size_t)((n + n / 4 + 1024) * b); };
+  bool ok = true;
+  if (P.mode == -1) ok = win_alloc(tr, P.flags, 3 * kMaxPeers * 8);
+  if (P.keys.bytes < maxcol * 8) ok = win_alloc(tr, P.keys, room(maxcol, 8)) && ok;
+  if (P.grads.bytes < maxcol * row) ok = win_alloc(tr, P.grads, room(maxcol, row)) && ok;
+  if (P.rows.bytes < maxrow * row) ok = win_alloc(tr, P.rows, room(maxrow, row)) && ok;
+  if (P.mode == -1 || !ok) {
+    P.mode = all_ok(tr, ok) ? 1 : 0;
+    if (P.mode == 0)
+      for (auto* w : {&P.keys, &P.rows, &P.grads, &P.flags}) win_release(tr, *w);
+  }
+  return P.mode == 1;
+}
+
+// phase 0 keys (requester -> owner), 2 grads (requester -> owner): element i of
+// the local send order goes to owner p's window after the segments of the
+// lower ranks; phase 1 rows (owner -> requester): received element i goes
+// back to requester p's window at p's own send position.
+PeerMap peer_map(kp_trainer* tr, int phase, uint32_t n_local) {
+  const int R = tr->world, me = tr->rank;
+  const auto& P = tr->peer;
+  PeerMap pm{};
+  pm.R = R;
+  const size_t row = (size_t)tr->e * 4;
+  pm.stride = phase == 0 ? 8 : (uint32_t)row;
+  const kp_trainer::PeerWin& w = phase == 0 ? P.keys : phase == 1 ? P.rows : P.grads;
+  for (int p = 0; p < R; ++p) {
+    uint64_t before = 0;  // my segment's offset inside p's window
+    for (int q = 0; q < me; ++q) before += phase == 1 ? tr->mat[(size_t)p * R + q] : tr->mat[(size_t)q * R + p];
+    pm.start[p] = (uint32_t)(phase == 1 ? tr->off_recv[p] : tr->off_send[p]);
+    pm.base[p] = reinterpret_cast<uintptr_t>(w.remote[p]) + before * pm.stride;
+  }
+  pm.start[R] = n_local;
+  return pm;
+}
+
+void peer_exchange_sync(kp_trainer* tr, int phase, bool signal, bool wait) {
+  const int R = tr->world, me = tr->rank;
+  auto& P = tr->peer;
+  if (signal) {
+    PeerFlags f{};
+    for (int p = 0; p < R; ++p)
+      f.flag[p] = reinterpret_cast<uintptr_t>(P.flags.remote[p]) + ((size_t)phase * kMaxPeers + me) * 8;
+    peer_signal(f, R, ++P.seq[phase], tr->s);
+  }
+  if (wait)
+    peer_wait(static_cast<const uint64_t*>(P.flags.local) + (size_t)phase * kMaxPeers, R, P.seq[phase],
+              static_cast<uint32_t*>(tr->check.p), tr->s);
+}
+
 PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   cudaStream_t s = tr->s;
   // bags first, so dedup can emit the bag of every sorted position
@@ -372,15 +522,14 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
     uint32_t* pos = tr->pos.get<uint32_t>(std::max<uint32_t>(U, 1));
     tr->cnt_send.assign(R, 0);
     shard(tr->dd.d_unique, U, R, perm, pos, tr->cnt_send.data(), tr->sh, s);
-    uint64_t* sk = tr->send_keys.get<uint64_t>(std::max<uint32_t>(U, 1));
-    if (U) k_gather_u64<<<grid1(U), 256, 0, s>>>(tr->dd.d_unique, perm, U, sk); ::kp::count_launch();
     // counts matrix via allgather
     uint64_t* cd = tr->counts_dev.get<uint64_t>((size_t)R * R + R);
     KP_CUDA(cudaMemcpyAsync(cd, tr->cnt_send.data(), R * 8, cudaMemcpyHostToDevice, s));
     KP_NCCL(ncclAllGather(cd, cd + R, R, ncclUint64, tr->comm->nc, s));
-    std::vector<uint64_t> mat((size_t)R * R);
-    KP_CUDA(cudaMemcpyAsync(mat.data(), cd + R, (size_t)R * R * 8, cudaMemcpyDeviceToHost, s));
+    tr->mat.assign((size_t)R * R, 0);
+    KP_CUDA(cudaMemcpyAsync(tr->mat.data(), cd + R, (size_t)R * R * 8, cudaMemcpyDeviceToHost, s));
     KP_CUDA(cudaStreamSynchronize(s));
+    const std::vector<uint64_t>& mat = tr->mat;
     tr->cnt_recv.assign(R, 0);
     tr->off_send.assign(R, 0);
     tr->off_recv.assign(R, 0);
@@ -392,8 +541,19 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
     }
     for (int p = 1; p < R; ++p) tr->off_send[p] = tr->off_send[p - 1] + tr->cnt_send[p - 1];
     const uint32_t Rn = (uint32_t)tot;
-    uint64_t* rk = tr->recv_keys.get<uint64_t>(std::max<uint32_t>(Rn, 1));
-    all_to_all(tr, sk, tr->cnt_send, tr->off_send, rk, tr->cnt_recv, tr->off_recv, 8, ncclUint64);
+    const bool peer = peer_ready(tr);
+    uint64_t* rk;
+    if (peer) {
+      // keys straight into the owners' windows over NVLink
+      peer_send_keys(tr->dd.d_unique, perm, U, peer_map(tr, 0, U), s);
+      peer_exchange_sync(tr, 0, true, true);
+      rk = static_cast<uint64_t*>(tr->peer.keys.local);
+    } else {
+      uint64_t* sk = tr->send_keys.get<uint64_t>(std::max<uint32_t>(U, 1));
+      if (U) k_gather_u64<<<grid1(U), 256, 0, s>>>(tr->dd.d_unique, perm, U, sk); ::kp::count_launch();
+      rk = tr->recv_keys.get<uint64_t>(std::max<uint32_t>(Rn, 1));
+      all_to_all(tr, sk, tr->cnt_send, tr->off_send, rk, tr->cnt_recv, tr->off_recv, 8, ncclUint64);
+    }
     tr->mark(6);
     // owner side: dedup received keys (stable: source order inside a key)
     dedup(rk, Rn, tr->dd_owner, s);
@@ -403,13 +563,21 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
     table_pull(tr->tab.t, tr->dd_owner.d_unique, Uo, orows, stamp, s);
     uint32_t* oidx = tr->owner_idx.get<uint32_t>(std::max<uint32_t>(Rn, 1));
     if (Rn) k_compose<<<grid1(Rn), 256, 0, s>>>(orows, tr->dd_owner.d_inverse, Rn, oidx); ::kp::count_launch();
-    float* srows = tr->send_rows.get<float>((size_t)std::max<uint32_t>(Rn, 1) * tr->e);
-    gather_rows(tr->tab.t->d_w, oidx, Rn, tr->e, srows, s);
-    tr->mark(1);
-    float* rrows = tr->recv_rows.get<float>((size_t)std::max<uint32_t>(U, 1) * tr->e);
-    all_to_all(tr, srows, tr->cnt_recv, tr->off_recv, rrows, tr->cnt_send, tr->off_send,
-               4 * (size_t)tr->e, ncclFloat32);
-    // NB: all_to_all counts are in elements of `elem` bytes: rows of e floats
+    float* rrows;
+    if (peer) {
+      // rows straight back into the requesters' windows
+      peer_send_rows(tr->tab.t->d_w, oidx, Rn, tr->e, peer_map(tr, 1, Rn), s);
+      tr->mark(1);
+      peer_exchange_sync(tr, 1, true, true);
+      rrows = static_cast<float*>(tr->peer.rows.local);
+    } else {
+      float* srows = tr->send_rows.get<float>((size_t)std::max<uint32_t>(Rn, 1) * tr->e);
+      gather_rows(tr->tab.t->d_w, oidx, Rn, tr->e, srows, s);
+      tr->mark(1);
+      rrows = tr->recv_rows.get<float>((size_t)std::max<uint32_t>(U, 1) * tr->e);
+      all_to_all(tr, srows, tr->cnt_recv, tr->off_recv, rrows, tr->cnt_send, tr->off_send,
+                 4 * (size_t)tr->e, ncclFloat32);
+    }
     tr->mark(6);
     pr.src = rrows;
     pr.idx = pos;
@@ -453,24 +621,35 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
   float* sgr = nullptr;
   float* rgr = nullptr;
   uint64_t Rn = 0;
+  const bool peer = tr->world > 1 && tr->peer.mode == 1;
+  PeerMap pmg{};
   if (tr->world > 1) {
-    sgr = tr->send_grads.get<float>((size_t)std::max<uint32_t>(pr.U, 1) * tr->e);
     for (auto c : tr->cnt_recv) Rn += c;
-    rgr = tr->recv_grads.get<float>((size_t)std::max<uint64_t>(Rn, 1) * tr->e);
+    if (peer) {
+      // reduced gradients go straight into the owners' windows (NVLink)
+      pmg = peer_map(tr, 2, pr.U);
+      rgr = static_cast<float*>(tr->peer.grads.local);
+    } else {
+      sgr = tr->send_grads.get<float>((size_t)std::max<uint32_t>(pr.U, 1) * tr->e);
+      rgr = tr->recv_grads.get<float>((size_t)std::max<uint64_t>(Rn, 1) * tr->e);
+    }
   }
   auto send_grads = [&] {
     seg_reduce_apply(tr->dd.d_seg, pr.U, tr->dd.d_sorted_mapped, nullptr, sv.n_occ, dpooled, tr->e,
                      1.0f, nullptr, nullptr, rule, sgr, static_cast<const uint32_t*>(tr->pos.p),
-                     tr->sg, s);
+                     tr->sg, s, peer ? &pmg : nullptr);
+    if (peer) peer_exchange_sync(tr, 2, true, false);
   };
   static const int reserve = [] {
     const char* e = getenv("KP_XRESERVE");
     return e ? atoi(e) : 16;
   }();
-  const bool overlap = tr->world > 1 && reserve > 0;
+  const bool overlap = tr->world > 1 && (reserve > 0 || peer);
   bool exchanged = false;
   std::function<void()> hook = [&] {
     send_grads();
+    exchanged = true;
+    if (peer) return;  // the reduction itself moved the data; no SMs to reserve
     if (!tr->xs) {
       KP_CUDA(cudaStreamCreateWithFlags(&tr->xs, cudaStreamNonBlocking));
       KP_CUDA(cudaEventCreateWithFlags(&tr->ev_dinput, cudaEventDisableTiming));
@@ -506,14 +685,16 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
                      inv_n, tr->tab.t, pr.idx, rule, nullptr, nullptr, tr->sg, s);
     tr->mark(4);
   } else {
-    if (exchanged) {
-      KP_CUDA(cudaStreamWaitEvent(s, tr->ev_xdone, 0));
-    } else {
+    if (!exchanged) {
       send_grads();
       tr->mark(4);
-      all_to_all(tr, sgr, tr->cnt_send, tr->off_send, rgr, tr->cnt_recv, tr->off_recv,
-                 4 * (size_t)tr->e, ncclFloat32);
+      if (!peer)
+        all_to_all(tr, sgr, tr->cnt_send, tr->off_send, rgr, tr->cnt_recv, tr->off_recv,
+                   4 * (size_t)tr->e, ncclFloat32);
+    } else if (!peer) {
+      KP_CUDA(cudaStreamWaitEvent(s, tr->ev_xdone, 0));
     }
+    if (peer) peer_exchange_sync(tr, 2, false, true);
     tr->mark(6);
     seg_reduce_apply(tr->dd_owner.d_seg, tr->dd_owner.n_unique, tr->dd_owner.sorted_vals, nullptr,
                      (uint32_t)Rn, rgr, tr->e, inv_n, tr->tab.t,
@@ -676,6 +857,7 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
   table_check_full(tr->tab.t, s);
   KP_CHECK(!(h_chk & 1), kErrGeneric, "non-finite worker state after step " + std::to_string(tr->t_global));
   KP_CHECK(!(h_chk & 2), kErrGeneric, "second moment lost positivity at step " + std::to_string(tr->t_global));
+  KP_CHECK(!(h_chk & 16), kErrCuda, "peer exchange timed out waiting for another rank (NVLink window flags)");
   // per-step loss = sum_workers loss_i*|mb_i| / sum |mb_i|  (trainer.cpp:177-178,221-223)
   if (tr->world > 1) {
     double* dl = tr->lossg.get<double>((size_t)n_mb * tr->world);

@@ -178,6 +178,8 @@ struct SegArgs {
   float* partials;
   uint32_t CH;
   int apply;
+  int peer;     // store through pm (remote windows) instead of grad_out
+  PeerMap pm;
   int rule;
   float lr, b1, b2;
 };
@@ -187,7 +189,9 @@ __device__ __forceinline__ void finalize(const SegArgs& a, const TView& t, uint3
                                          Row<LPG, NV, V4>& g, int gl) {
   g.scale(a.inv_n);  // trainer.cpp:204-206 (x 1/N)
   if (!a.apply) {
-    g.store(a.grad_out + (uint64_t)(a.out_idx ? a.out_idx[u] : u) * a.e, gl, a.e);
+    const uint32_t o = a.out_idx ? a.out_idx[u] : u;
+    float* dst = a.peer ? reinterpret_cast<float*>(peer_dst(a.pm, o)) : a.grad_out + (uint64_t)o * a.e;
+    g.store(dst, gl, a.e);
     return;
   }
   if (a.table_rows[u] == kNoRow) return;  // table full: error raised at the batch end
@@ -273,6 +277,7 @@ __global__ void __launch_bounds__(256) k_seg_chunks(SegArgs a, TView t) {
       ++u;
     }
   }
+  if (a.peer) __threadfence_system();  // remote stores complete before the signal
 }
 
 // Phase 2: a segment spanning chunks c0 < c1 owns the contiguous flattened
@@ -337,6 +342,7 @@ __global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t, const float
     }
     finalize(a, t, (uint32_t)u, acc, gl);
   }
+  if (a.peer) __threadfence_system();
 }
 
 template <int LPG, int NV, bool V4>
@@ -426,7 +432,7 @@ void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* 
                       const uint32_t* d_bag_of_occ, uint32_t n_pos, const float* d_rows_src,
                       uint32_t e, float inv_n, Table* t, const uint32_t* d_table_rows,
                       const SparseRule& r, float* d_grad_out, const uint32_t* d_out_idx,
-                      SegWs& ws, cudaStream_t s) {
+                      SegWs& ws, cudaStream_t s, const PeerMap* pm) {
   if (n_unique == 0 || n_pos == 0) return;
   SegArgs a;
   a.seg = d_seg;
@@ -444,6 +450,8 @@ void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* 
   const uint32_t nchunks = (n_pos + a.CH - 1) / a.CH;
   a.partials = ws.partials.get<float>((size_t)nchunks * 2 * e);
   a.apply = t != nullptr;
+  a.peer = pm != nullptr;
+  if (pm) a.pm = *pm;
   a.rule = r.rule;
   a.lr = r.lr;
   a.b1 = r.beta1;

@@ -98,6 +98,40 @@ void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_row_of_
 struct SegWs {
   DevBuf partials, qsums;
 };
+// ---------------------------------------------------------- peer memory ----
+// Destination map for kernels that write their output straight into the
+// peers' exchange windows over NVLink (CUDA IPC mappings): local element i
+// belongs to peer p with start[p] <= i < start[p+1] and lands at
+// base[p] + (i - start[p]) * stride bytes (base already holds the offset of
+// this rank's segment inside peer p's window).
+constexpr int kMaxPeers = 16;
+struct PeerMap {
+  int R;
+  uint32_t stride;
+  uint32_t start[kMaxPeers + 1];
+  uintptr_t base[kMaxPeers];
+};
+__device__ __forceinline__ char* peer_dst(const PeerMap& pm, uint32_t i) {
+  int p = 0;
+#pragma unroll 1
+  while (p + 1 < pm.R && i >= pm.start[p + 1]) ++p;
+  return reinterpret_cast<char*>(pm.base[p]) + (uint64_t)(i - pm.start[p]) * pm.stride;
+}
+struct PeerFlags {
+  uintptr_t flag[kMaxPeers];  // &flags_p[phase][me] in every peer p's window
+};
+// keys[t] = unique[perm[t]] -> peer windows (the owner's received keys)
+void peer_send_keys(const uint64_t* d_unique, const uint32_t* d_perm, uint32_t n, const PeerMap& pm,
+                    cudaStream_t s);
+// rows src[idx[i]] (e floats; kNoRow -> zeros) -> peer windows
+void peer_send_rows(const float* d_src, const uint32_t* d_idx, uint32_t n, uint32_t e,
+                    const PeerMap& pm, cudaStream_t s);
+// after this stream's writes: flag_p = seq in every peer (system-scope release)
+void peer_signal(const PeerFlags& f, int R, uint64_t seq, cudaStream_t s);
+// wait until every peer's flag in this rank's window reached seq (bit 4 of
+// *d_err on timeout instead of hanging)
+void peer_wait(const uint64_t* d_my_flags, int R, uint64_t seq, uint32_t* d_err, cudaStream_t s);
+
 struct SparseRule {
   int rule;  // 0 adagrad, 1 adam
   float lr, beta1, beta2;
@@ -105,12 +139,13 @@ struct SparseRule {
 // Segments are [seg[u], seg[u+1]) of sorted positions p; the upstream row of
 // position p is rows_src[map(p)] with map(p) = bag_of_occ[sorted_vals[p]]
 // (bag_of_occ may be null: identity). Output: apply the rule to table row
-// table_rows[u] (fused push) when `t` is set, else store to grad_out[out_idx[u]].
+// table_rows[u] (fused push) when `t` is set, else store to grad_out[out_idx[u]]
+// -- or, with `pm`, to peer_dst(pm, out_idx[u]) in the owners' windows.
 void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* d_sorted_vals,
                       const uint32_t* d_bag_of_occ, uint32_t n_pos, const float* d_rows_src,
                       uint32_t e, float inv_n, Table* t, const uint32_t* d_table_rows,
                       const SparseRule& r, float* d_grad_out, const uint32_t* d_out_idx,
-                      SegWs& ws, cudaStream_t s);
+                      SegWs& ws, cudaStream_t s, const PeerMap* pm = nullptr);
 void gather_rows(const float* d_src, const uint32_t* d_idx, uint32_t n, uint32_t e, float* d_out,
                  cudaStream_t s);
 

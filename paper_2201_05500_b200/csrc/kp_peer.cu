@@ -1,0 +1,100 @@
+// NVLink peer-memory exchange (G > 1, one process per GPU).
+//
+// The reference exchanges nothing (one process, trainer.cpp:163,180-186 sums
+// worker gradients in a std::map); the B200 design shards the table by
+// key % G and moves keys, rows and gradients between GPUs.
+// Instead of staging into send buffers for an NCCL all-to-all, the producing
+// kernels store their output directly into the destination rank's exchange
+// window (CUDA IPC mapping, NVSwitch P2P), so the transfer overlaps the
+// kernel's own HBM-bound work:
+//   keys   unique keys in owner order      -> owner's key window
+//   rows   owner's table rows               -> requester's row window
+//   grads  per-unique reduced gradients     -> owner's gradient window
+//          (stored by the segmented reduction's finalize, kp_embed.cu)
+// Completion is a per-(phase, source) sequence flag written with a
+// system-scope release after the data; the consumer spins on its own flags
+// (bounded, error bit instead of a hang) before reading the window.
+#include "kp_internal.cuh"
+
+namespace kp {
+namespace {
+
+__global__ void k_send_keys(const uint64_t* __restrict__ unique, const uint32_t* __restrict__ perm,
+                            uint32_t n, PeerMap pm) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+    *reinterpret_cast<uint64_t*>(peer_dst(pm, t)) = unique[perm[t]];
+  __threadfence_system();
+}
+
+// one 16-lane group per row, float4 lanes (e % 4 == 0) or scalar fallback
+__global__ void k_send_rows(const float* __restrict__ src, const uint32_t* __restrict__ idx,
+                            uint32_t n, uint32_t e, PeerMap pm) {
+  const uint32_t gl = threadIdx.x & 15;
+  const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 4;
+  const uint64_t ng = ((uint64_t)gridDim.x * blockDim.x) >> 4;
+  const bool v4 = (e & 3) == 0;
+  for (uint64_t i = g0; i < n; i += ng) {
+    float* dst = reinterpret_cast<float*>(peer_dst(pm, (uint32_t)i));
+    const uint32_t r = idx[i];
+    if (v4) {
+      const float4* sp = reinterpret_cast<const float4*>(src + (uint64_t)r * e);
+      for (uint32_t j = gl; j < e / 4; j += 16)
+        reinterpret_cast<float4*>(dst)[j] = r == kNoRow ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(sp + j);
+    } else {
+      for (uint32_t j = gl; j < e; j += 16) dst[j] = r == kNoRow ? 0.f : __ldg(src + (uint64_t)r * e + j);
+    }
+  }
+  __threadfence_system();
+}
+
+__global__ void k_signal(PeerFlags f, int R, uint64_t seq) {
+  const int p = threadIdx.x;
+  __threadfence_system();
+  if (p < R) {
+    volatile unsigned long long* q = reinterpret_cast<volatile unsigned long long*>(f.flag[p]);
+    *q = seq;
+  }
+  __threadfence_system();
+}
+
+__global__ void k_wait(const uint64_t* flags, int R, uint64_t seq, uint32_t* err) {
+  const int p = threadIdx.x;
+  if (p < R) {
+    const volatile unsigned long long* q = reinterpret_cast<const volatile unsigned long long*>(flags + p);
+    const long long t0 = clock64();
+    while (*q < seq) {
+      if (clock64() - t0 > 8000000000ll) {  // ~4 s at 2 GHz: a peer is gone
+        atomicOr(err, 16u);
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+  __threadfence_system();
+}
+
+}  // namespace
+
+void peer_send_keys(const uint64_t* d_unique, const uint32_t* d_perm, uint32_t n, const PeerMap& pm,
+                    cudaStream_t s) {
+  if (n == 0) return;
+  k_send_keys<<<std::min<uint32_t>(ceil_div(n, 256), 148 * 8), 256, 0, s>>>(d_unique, d_perm, n, pm); ::kp::count_launch();
+}
+
+void peer_send_rows(const float* d_src, const uint32_t* d_idx, uint32_t n, uint32_t e,
+                    const PeerMap& pm, cudaStream_t s) {
+  if (n == 0) return;
+  const uint64_t groups = n;
+  k_send_rows<<<(unsigned)std::min<uint64_t>((groups * 16 + 255) / 256, 148 * 16), 256, 0, s>>>(
+      d_src, d_idx, n, e, pm); ::kp::count_launch();
+}
+
+void peer_signal(const PeerFlags& f, int R, uint64_t seq, cudaStream_t s) {
+  k_signal<<<1, 32, 0, s>>>(f, R, seq); ::kp::count_launch();
+}
+
+void peer_wait(const uint64_t* d_my_flags, int R, uint64_t seq, uint32_t* d_err, cudaStream_t s) {
+  k_wait<<<1, 32, 0, s>>>(d_my_flags, R, seq, d_err); ::kp::count_launch();
+}
+
+}  // namespace kp
