@@ -505,7 +505,14 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   uint32_t* bag_of_occ = tr->bag_of_occ.get<uint32_t>(std::max<uint32_t>(sv.n_occ, 1));
   uint32_t* err = tr->err.get<uint32_t>(4);
   prepare_bags(sv.offs, sv.occ_base, sv.slots, sv.n_inst, tr->S, bag_offs, bag_of_occ, err, s);
-  dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ);
+  uint32_t h_err = 0xFFFFFFFFu;
+  KP_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, s));
+  dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ);  // synchronises the stream
+  if (sv.n_occ == 0) KP_CUDA(cudaStreamSynchronize(s));
+  // reject bad slot ids before any state (table, weights) changes
+  KP_CHECK(h_err == 0xFFFFFFFFu, kErrConfig,
+           "slot ids must be < n_slots and non-decreasing within an instance (occurrence " +
+               std::to_string(h_err) + ")");
   tr->mark(0);
   const uint32_t U = tr->dd.n_unique;
   PullResult pr{};

@@ -47,6 +47,7 @@ __global__ void k_prepare_bags(const uint32_t* __restrict__ offs, uint32_t occ_b
         const int prev = o == o0 ? -1 : (int)slots[o - 1];
         if (s >= S || (int)s < prev) {
           atomicMin(err, o);
+          bag_of_occ[o] = i * S;  // keep downstream indexing in bounds; the batch is rejected
           continue;
         }
         for (int t = prev + 1; t <= (int)s; ++t) bag_offs[(uint64_t)i * S + t] = o;

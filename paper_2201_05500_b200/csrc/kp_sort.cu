@@ -79,12 +79,21 @@ __global__ void k_minmax(const uint64_t* __restrict__ keys, uint32_t n, unsigned
   }
 }
 
-__global__ void __launch_bounds__(ST) k_upsweep(const uint64_t* __restrict__ keys, uint32_t n,
+// digit of an input key: (key - kmin) >> shift for raw u64 keys, key >> shift
+// for u32 keys that already are (key - kmin)
+template <typename KIN>
+__device__ __forceinline__ uint32_t digit_of(KIN k, uint64_t kmin, int shift, uint32_t mask) {
+  if constexpr (sizeof(KIN) == 4) return (uint32_t)(k >> shift) & mask;
+  else return (uint32_t)((k - kmin) >> shift) & mask;
+}
+
+template <typename KIN, int R>
+__global__ void __launch_bounds__(ST) k_upsweep(const KIN* __restrict__ keys, uint32_t n,
                                                 const unsigned long long* __restrict__ mm,
                                                 int shift, uint32_t* __restrict__ counts,
                                                 uint32_t nb) {
-  __shared__ uint32_t hist[RADIX];
-  hist[threadIdx.x] = 0;
+  __shared__ uint32_t hist[R];
+  for (int i = threadIdx.x; i < R; i += ST) hist[i] = 0;
   __syncthreads();
   const uint64_t kmin = mm[0];
   const uint32_t base = blockIdx.x * TILE;
@@ -92,12 +101,12 @@ __global__ void __launch_bounds__(ST) k_upsweep(const uint64_t* __restrict__ key
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     const uint32_t idx = base + r * ST + threadIdx.x;
-    const uint32_t d = idx < n ? (uint32_t)((keys[idx] - kmin) >> shift) & 255u : RADIX;
+    const uint32_t d = idx < n ? digit_of<KIN>(keys[idx], kmin, shift, R - 1) : R;
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    if (d < RADIX && lane == __ffs(peers) - 1) atomicAdd(&hist[d], __popc(peers));
+    if (d < R && lane == __ffs(peers) - 1) atomicAdd(&hist[d], __popc(peers));
   }
   __syncthreads();
-  counts[threadIdx.x * nb + blockIdx.x] = hist[threadIdx.x];
+  for (int i = threadIdx.x; i < R; i += ST) counts[i * nb + blockIdx.x] = hist[i];
 }
 
 // rows of `counts` ([rows][nb]) scanned exclusive in place; totals[row].
@@ -158,50 +167,78 @@ __device__ __forceinline__ void stable_rank(const uint32_t (&d)[IPT], uint32_t (
   __syncthreads();
 }
 
+// exclusive scan of R (256 or 512) values held as RPT consecutive values per thread
+template <int R>
+__device__ __forceinline__ void scan_digits(const uint32_t* in, uint32_t* out, uint32_t* s_warp) {
+  constexpr int RPT = R / ST;
+  uint32_t v[RPT], sum = 0;
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    v[i] = in[threadIdx.x * RPT + i];
+    sum += v[i];
+  }
+  uint32_t tot;
+  uint32_t pre = block_excl_scan(sum, s_warp, tot);
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    out[threadIdx.x * RPT + i] = pre;
+    pre += v[i];
+  }
+}
+
+// One LSD pass. KIN -> KOUT: u64 -> u64 (raw keys), u64 -> u32 (first pass of
+// the narrow mode: keys become key - kmin), u32 -> u32.
+template <typename KIN, typename KOUT, int R>
 __global__ void __launch_bounds__(ST) k_downsweep(
-    const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
+    const KIN* __restrict__ kin, const uint32_t* __restrict__ vin, KOUT* __restrict__ kout,
     uint32_t* __restrict__ vout, uint32_t n, const unsigned long long* __restrict__ mm, int shift,
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ totals, uint32_t nb) {
-  __shared__ uint64_t s_keys[TILE];
+  __shared__ KOUT s_keys[TILE];
   __shared__ uint32_t s_vals[TILE];
-  __shared__ uint32_t s_hist[RADIX], s_start[RADIX], s_off[RADIX], s_run[RADIX];
-  __shared__ uint16_t s_wcnt[2][NW][RADIX];
+  __shared__ uint32_t s_tmp[R], s_start[R], s_off[R], s_run[R];
+  __shared__ uint16_t s_wcnt[2][NW][R];
   __shared__ uint32_t s_warp[NW];
   const int tid = threadIdx.x, lane = tid & 31;
-  s_hist[tid] = 0;
-  s_run[tid] = 0;
-  for (int i = tid; i < 2 * NW * RADIX; i += ST) (&s_wcnt[0][0][0])[i] = 0;
+  for (int i = tid; i < R; i += ST) {
+    s_tmp[i] = 0;
+    s_run[i] = 0;
+  }
+  for (int i = tid; i < 2 * NW * R; i += ST) (&s_wcnt[0][0][0])[i] = 0;
   __syncthreads();
   const uint64_t kmin = mm[0];
   const uint32_t base = blockIdx.x * TILE;
   const uint32_t tile_n = min((uint32_t)TILE, n - base);
-  uint64_t k[IPT];
+  KOUT k[IPT];
   uint32_t v[IPT], d[IPT], rank[IPT];
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     const uint32_t i = r * ST + tid;
     if (i < tile_n) {
-      k[r] = kin[base + i];
+      const KIN x = kin[base + i];
+      d[r] = digit_of<KIN>(x, kmin, shift, R - 1);
+      if constexpr (sizeof(KOUT) == 4 && sizeof(KIN) == 8) k[r] = (KOUT)(x - kmin);
+      else k[r] = (KOUT)x;
       v[r] = vin ? vin[base + i] : base + i;
-      d[r] = (uint32_t)((k[r] - kmin) >> shift) & 255u;
     } else {
-      d[r] = RADIX;
+      d[r] = R;
     }
     const uint32_t peers = __match_any_sync(0xffffffffu, d[r]);
-    if (d[r] < RADIX && lane == __ffs(peers) - 1) atomicAdd(&s_hist[d[r]], __popc(peers));
+    if (d[r] < R && lane == __ffs(peers) - 1) atomicAdd(&s_tmp[d[r]], __popc(peers));
   }
   __syncthreads();
   // digit prefix over the whole array + this block's offset within the digit
-  uint32_t tot;
-  const uint32_t dpre = block_excl_scan(totals[tid], s_warp, tot);
-  const uint32_t tstart = block_excl_scan(s_hist[tid], s_warp, tot);
-  s_start[tid] = tstart;
-  s_off[tid] = dpre + counts[tid * nb + blockIdx.x] - tstart;
+  scan_digits<R>(s_tmp, s_start, s_warp);   // block-local digit starts
   __syncthreads();
-  stable_rank<RADIX>(d, rank, s_run, s_wcnt);
+  for (int i = tid; i < R; i += ST) s_off[i] = totals[i];
+  __syncthreads();
+  scan_digits<R>(s_off, s_off, s_warp);     // global digit starts (in place: values read first)
+  __syncthreads();
+  for (int i = tid; i < R; i += ST) s_off[i] += counts[i * nb + blockIdx.x] - s_start[i];
+  __syncthreads();
+  stable_rank<R>(d, rank, s_run, s_wcnt);
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
-    if (d[r] < RADIX) {
+    if (d[r] < R) {
       const uint32_t p = s_start[d[r]] + rank[r];
       s_keys[p] = k[r];
       s_vals[p] = v[r];
@@ -209,8 +246,8 @@ __global__ void __launch_bounds__(ST) k_downsweep(
   }
   __syncthreads();
   for (uint32_t i = tid; i < tile_n; i += ST) {
-    const uint64_t key = s_keys[i];
-    const uint32_t dd = (uint32_t)((key - kmin) >> shift) & 255u;
+    const KOUT key = s_keys[i];
+    const uint32_t dd = digit_of<KOUT>(key, kmin, shift, R - 1);
     const uint32_t g = s_off[dd] + i;
     kout[g] = key;
     vout[g] = s_vals[i];
@@ -218,7 +255,8 @@ __global__ void __launch_bounds__(ST) k_downsweep(
 }
 
 // ---- unique / inverse / segments -----------------------------------------
-__global__ void __launch_bounds__(ST) k_head_count(const uint64_t* __restrict__ sk, uint32_t n,
+template <typename KT>
+__global__ void __launch_bounds__(ST) k_head_count(const KT* __restrict__ sk, uint32_t n,
                                                    uint32_t* __restrict__ bcount) {
   __shared__ uint32_t s_warp[NW];
   const uint32_t base = blockIdx.x * TILE + threadIdx.x * IPT;
@@ -233,7 +271,9 @@ __global__ void __launch_bounds__(ST) k_head_count(const uint64_t* __restrict__ 
   if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(ST) k_dedup_emit(const uint64_t* __restrict__ sk,
+template <typename KT>
+__global__ void __launch_bounds__(ST) k_dedup_emit(const KT* __restrict__ sk,
+                                                   const unsigned long long* __restrict__ mm,
                                                    const uint32_t* __restrict__ sv, uint32_t n,
                                                    const uint32_t* __restrict__ bbase,
                                                    uint64_t* __restrict__ uniq,
@@ -259,7 +299,7 @@ __global__ void __launch_bounds__(ST) k_dedup_emit(const uint64_t* __restrict__ 
     const uint32_t i = base + r;
     if (i >= n) break;
     if (f[r]) {
-      uniq[uid] = sk[i];
+      uniq[uid] = sizeof(KT) == 4 ? (uint64_t)mm[0] + sk[i] : (uint64_t)sk[i];
       seg[uid] = i;
       ++uid;
     }
@@ -352,40 +392,88 @@ void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
   KP_CUDA(cudaStreamSynchronize(s));
   const uint64_t span = h_mm[1] - h_mm[0];
   const int bits = span == 0 ? 0 : 64 - __builtin_clzll(span);
-  const int passes = bits == 0 ? 1 : (bits + 7) / 8;  // >=1: identity when all equal
 
-  uint64_t* ka = ws.keys_a.get<uint64_t>(n);
-  uint64_t* kb = ws.keys_b.get<uint64_t>(n);
   uint32_t* va = ws.vals_a.get<uint32_t>(n);
   uint32_t* vb = ws.vals_b.get<uint32_t>(n);
-  uint32_t* counts = ws.counts.get<uint32_t>((size_t)RADIX * nb);
-  uint32_t* totals = ws.totals.get<uint32_t>(RADIX);
-  const uint64_t* kin = d_keys;
-  const uint32_t* vin = nullptr;
-  uint64_t* kout = ka;
-  uint32_t* vout = va;
-  for (int p = 0; p < passes; ++p) {
-    const int shift = p * 8;
-    k_upsweep<<<nb, ST, 0, s>>>(kin, n, mm, shift, counts, nb); ::kp::count_launch();
-    k_scan_rows<<<RADIX, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
-    k_downsweep<<<nb, ST, 0, s>>>(kin, vin, kout, vout, n, mm, shift, counts, totals, nb); ::kp::count_launch();
-    kin = kout;
-    vin = vout;
-    kout = (kout == ka) ? kb : ka;
-    vout = (vout == va) ? vb : va;
-  }
-  ws.sorted_keys = kin;
-  ws.sorted_vals = vin;
-
   uint32_t* bcount = ws.bcount.get<uint32_t>(nb);
-  k_head_count<<<nb, ST, 0, s>>>(kin, n, bcount); ::kp::count_launch();
-  k_scan_rows<<<1, ST, 0, s>>>(bcount, nb, ws.d_nunique + 1); ::kp::count_launch();
   ws.d_unique = ws.unique.get<uint64_t>(n);
   ws.d_inverse = ws.inverse.get<uint32_t>(n);
   ws.d_seg = ws.seg.get<uint32_t>(n + 1);
   ws.d_sorted_mapped = d_occ_map ? ws.mapped.get<uint32_t>(n) : nullptr;
-  k_dedup_emit<<<nb, ST, 0, s>>>(kin, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
-                                  ws.d_nunique, nb, d_occ_map, ws.d_sorted_mapped); ::kp::count_launch();
+  if (bits <= 32) {
+    // narrow mode: the first pass turns keys into u32 (key - kmin); 9-bit
+    // digits, so a 27-bit span (1e8 keys) takes 3 passes of 8 B per pair
+    const int np = bits == 0 ? 1 : (bits + 8) / 9;
+    const int db = bits == 0 ? 1 : (bits + np - 1) / np;  // digit bits per pass (<= 9)
+    uint32_t* ka = reinterpret_cast<uint32_t*>(ws.keys_a.get<uint64_t>((n + 1) / 2));
+    uint32_t* kb = reinterpret_cast<uint32_t*>(ws.keys_b.get<uint64_t>((n + 1) / 2));
+    uint32_t* counts = ws.counts.get<uint32_t>((size_t)512 * nb);
+    uint32_t* totals = ws.totals.get<uint32_t>(512);
+    const uint32_t* kin32 = nullptr;
+    const uint32_t* vin = nullptr;
+    uint32_t* kout = ka;
+    uint32_t* vout = va;
+    for (int p = 0; p < np; ++p) {
+      const int shift = p * db;
+      // digits of db bits, masked with R-1: use R = 2^db rounded to 256/512
+      const bool wide = db > 8;
+      if (p == 0) {
+        if (wide) {
+          k_upsweep<uint64_t, 512><<<nb, ST, 0, s>>>(d_keys, n, mm, shift, counts, nb); ::kp::count_launch();
+          k_scan_rows<<<512, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
+          k_downsweep<uint64_t, uint32_t, 512><<<nb, ST, 0, s>>>(d_keys, nullptr, kout, vout, n, mm, shift, counts, totals, nb); ::kp::count_launch();
+        } else {
+          k_upsweep<uint64_t, 256><<<nb, ST, 0, s>>>(d_keys, n, mm, shift, counts, nb); ::kp::count_launch();
+          k_scan_rows<<<256, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
+          k_downsweep<uint64_t, uint32_t, 256><<<nb, ST, 0, s>>>(d_keys, nullptr, kout, vout, n, mm, shift, counts, totals, nb); ::kp::count_launch();
+        }
+      } else if (wide) {
+        k_upsweep<uint32_t, 512><<<nb, ST, 0, s>>>(kin32, n, mm, shift, counts, nb); ::kp::count_launch();
+        k_scan_rows<<<512, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
+        k_downsweep<uint32_t, uint32_t, 512><<<nb, ST, 0, s>>>(kin32, vin, kout, vout, n, mm, shift, counts, totals, nb); ::kp::count_launch();
+      } else {
+        k_upsweep<uint32_t, 256><<<nb, ST, 0, s>>>(kin32, n, mm, shift, counts, nb); ::kp::count_launch();
+        k_scan_rows<<<256, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
+        k_downsweep<uint32_t, uint32_t, 256><<<nb, ST, 0, s>>>(kin32, vin, kout, vout, n, mm, shift, counts, totals, nb); ::kp::count_launch();
+      }
+      kin32 = kout;
+      vin = vout;
+      kout = (kout == ka) ? kb : ka;
+      vout = (vout == va) ? vb : va;
+    }
+    ws.sorted_keys = nullptr;
+    ws.sorted_vals = vin;
+    k_head_count<uint32_t><<<nb, ST, 0, s>>>(kin32, n, bcount); ::kp::count_launch();
+    k_scan_rows<<<1, ST, 0, s>>>(bcount, nb, ws.d_nunique + 1); ::kp::count_launch();
+    k_dedup_emit<uint32_t><<<nb, ST, 0, s>>>(kin32, mm, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
+                                             ws.d_nunique, nb, d_occ_map, ws.d_sorted_mapped); ::kp::count_launch();
+  } else {
+    const int passes = (bits + 7) / 8;
+    uint64_t* ka = ws.keys_a.get<uint64_t>(n);
+    uint64_t* kb = ws.keys_b.get<uint64_t>(n);
+    uint32_t* counts = ws.counts.get<uint32_t>((size_t)RADIX * nb);
+    uint32_t* totals = ws.totals.get<uint32_t>(RADIX);
+    const uint64_t* kin = d_keys;
+    const uint32_t* vin = nullptr;
+    uint64_t* kout = ka;
+    uint32_t* vout = va;
+    for (int p = 0; p < passes; ++p) {
+      const int shift = p * 8;
+      k_upsweep<uint64_t, RADIX><<<nb, ST, 0, s>>>(kin, n, mm, shift, counts, nb); ::kp::count_launch();
+      k_scan_rows<<<RADIX, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
+      k_downsweep<uint64_t, uint64_t, RADIX><<<nb, ST, 0, s>>>(kin, vin, kout, vout, n, mm, shift, counts, totals, nb); ::kp::count_launch();
+      kin = kout;
+      vin = vout;
+      kout = (kout == ka) ? kb : ka;
+      vout = (vout == va) ? vb : va;
+    }
+    ws.sorted_keys = kin;
+    ws.sorted_vals = vin;
+    k_head_count<uint64_t><<<nb, ST, 0, s>>>(kin, n, bcount); ::kp::count_launch();
+    k_scan_rows<<<1, ST, 0, s>>>(bcount, nb, ws.d_nunique + 1); ::kp::count_launch();
+    k_dedup_emit<uint64_t><<<nb, ST, 0, s>>>(kin, mm, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
+                                             ws.d_nunique, nb, d_occ_map, ws.d_sorted_mapped); ::kp::count_launch();
+  }
   KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaStreamSynchronize(s));
 }
