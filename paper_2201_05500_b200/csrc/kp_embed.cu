@@ -110,7 +110,7 @@ struct Row {
 constexpr int PB = 4;
 
 template <int LPG, int NV, bool V4>
-__global__ void __launch_bounds__(256) k_pool(const uint32_t* __restrict__ bag_offs, uint32_t n_bags,
+__global__ void __launch_bounds__(256, 5) k_pool(const uint32_t* __restrict__ bag_offs, uint32_t n_bags,
                                               const uint32_t* __restrict__ rowocc,
                                               const float* __restrict__ src, uint32_t e, int mean,
                                               float* __restrict__ pooled,
@@ -243,7 +243,7 @@ __device__ __forceinline__ void sum_range(const SegArgs& a, uint32_t p, uint32_t
 
 // Phase 1: one group per chunk of CH sorted positions.
 template <int LPG, int NV, bool V4>
-__global__ void __launch_bounds__(256) k_seg_chunks(SegArgs a, TView t) {
+__global__ void __launch_bounds__(256, 6) k_seg_chunks(SegArgs a, TView t) {
   const int gl = threadIdx.x % LPG;
   const uint32_t nchunks = (a.n_pos + a.CH - 1) / a.CH;
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;

@@ -67,6 +67,8 @@ def main(src, out_md, out_json=None):
     seq = load(src)
     starts = [i for i, s in enumerate(seq) if s["name"].startswith("k_prepare_bags")]
     step = seq[starts[-1]:] if starts else seq
+    # only this library's kernels (bench.py's cuBLAS calibration runs after the step)
+    step = [x for x in step if x["name"].startswith("k_")]
     tot = sum(s.get("us", 0.0) for s in step)
     L = [f"# ncu launch list: last training step of `{src.split('/')[-1]}`", "",
          f"{len(step)} launches, {tot:.1f} us serialised. ncu replays each kernel alone with a",
