@@ -146,12 +146,14 @@ struct kp_trainer {
   struct PeerWin {
     void* local = nullptr;
     size_t bytes = 0;
+    bool owned = true;  // false: an exported trainer buffer (x, v)
     std::vector<void*> remote;
   };
   struct {
     int mode = -1;
     PeerWin keys, rows, grads, flags;
-    uint64_t seq[3] = {0, 0, 0};
+    PeerWin dv, dx, terms, vb;  // k-step merge over NVLink
+    uint64_t seq[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     DevBuf scratch;
   } peer;
   // profiling
@@ -201,10 +203,11 @@ struct kp_trainer {
       if (st.ev) cudaEventDestroy(st.ev);
     if (copy_s) cudaStreamDestroy(copy_s);
     if (xs) cudaStreamDestroy(xs);
-    for (PeerWin* w : {&peer.keys, &peer.rows, &peer.grads, &peer.flags}) {
+    for (PeerWin* w : {&peer.keys, &peer.rows, &peer.grads, &peer.flags, &peer.dv, &peer.dx,
+                       &peer.terms, &peer.vb}) {
       for (size_t p = 0; p < w->remote.size(); ++p)
         if (w->remote[p] && w->remote[p] != w->local) cudaIpcCloseMemHandle(w->remote[p]);
-      if (w->local) cudaFree(w->local);
+      if (w->local && w->owned) cudaFree(w->local);
     }
     if (ev_dinput) cudaEventDestroy(ev_dinput);
     if (ev_xdone) cudaEventDestroy(ev_xdone);
@@ -385,18 +388,25 @@ void win_release(kp_trainer* tr, kp_trainer::PeerWin& w) {
   for (size_t p = 0; p < w.remote.size(); ++p)
     if (w.remote[p] && w.remote[p] != w.local) cudaIpcCloseMemHandle(w.remote[p]);
   all_ok(tr, true);  // every mapping of ours is closed
-  KP_CUDA(cudaFree(w.local));
+  if (w.owned) KP_CUDA(cudaFree(w.local));
   w.local = nullptr;
   w.remote.clear();
   w.bytes = 0;
 }
 
-// collective: (re)allocate a window of `bytes` on every rank and map the peers'
-bool win_alloc(kp_trainer* tr, kp_trainer::PeerWin& w, size_t bytes) {
+// collective: (re)allocate a window of `bytes` on every rank (or export the
+// existing allocation `existing`) and map the peers'
+bool win_alloc(kp_trainer* tr, kp_trainer::PeerWin& w, size_t bytes, void* existing = nullptr) {
   const int R = tr->world, me = tr->rank;
   win_release(tr, w);
-  KP_CUDA(cudaMalloc(&w.local, bytes));
-  KP_CUDA(cudaMemset(w.local, 0, bytes));
+  if (existing) {
+    w.local = existing;
+    w.owned = false;
+  } else {
+    KP_CUDA(cudaMalloc(&w.local, bytes));
+    KP_CUDA(cudaMemset(w.local, 0, bytes));
+    w.owned = true;
+  }
   w.bytes = bytes;
   cudaIpcMemHandle_t h;
   bool ok = cudaIpcGetMemHandle(&h, w.local) == cudaSuccess;
@@ -449,7 +459,7 @@ bool peer_ready(kp_trainer* tr) {
   const size_t row = (size_t)tr->e * 4;
   auto room = [](uint64_t n, size_t b) { return (size_t)((n + n / 4 + 1024) * b); };
   bool ok = true;
-  if (P.mode == -1) ok = win_alloc(tr, P.flags, 3 * kMaxPeers * 8);
+  if (P.mode == -1) ok = win_alloc(tr, P.flags, 8 * kMaxPeers * 8);
   if (P.keys.bytes < maxcol * 8) ok = win_alloc(tr, P.keys, room(maxcol, 8)) && ok;
   if (P.grads.bytes < maxcol * row) ok = win_alloc(tr, P.grads, room(maxcol, row)) && ok;
   if (P.rows.bytes < maxrow * row) ok = win_alloc(tr, P.rows, room(maxrow, row)) && ok;
@@ -495,6 +505,55 @@ void peer_exchange_sync(kp_trainer* tr, int phase, bool signal, bool wait) {
   if (wait)
     peer_wait(static_cast<const uint64_t*>(P.flags.local) + (size_t)phase * kMaxPeers, R, P.seq[phase],
               static_cast<uint32_t*>(tr->check.p), tr->s);
+}
+
+// k-step merge over NVLink (peer mode): the owner of chunk c reads every
+// rank's workers' v (then x - a m / sqrt(v_bar)) for its chunk straight from
+// their HBM, computes the fixed-order centered mean and stores the result into
+// every rank; four flag phases order the rounds. Same arithmetic and worker
+// order as merge_states, so the result is bitwise the same.
+void merge_states_peer(kp_trainer* tr, float alpha, bool reset) {
+  auto& P = tr->peer;
+  const int R = tr->world, me = tr->rank;
+  const uint32_t W = tr->W;
+  const uint64_t D = tr->D;
+  cudaStream_t s = tr->s;
+  if (!P.dv.local) {
+    bool ok = win_alloc(tr, P.dv, (size_t)W * D * 4, tr->v);
+    ok = win_alloc(tr, P.dx, (size_t)W * D * 4, tr->x) && ok;
+    ok = win_alloc(tr, P.terms, (size_t)W * D * 4) && ok;
+    ok = win_alloc(tr, P.vb, (size_t)D * 4) && ok;
+    KP_CHECK(all_ok(tr, ok), kErrCuda, "peer merge: IPC mapping of the dense state failed");
+  }
+  const uint64_t C = (D + R - 1) / R;
+  const uint64_t c0 = std::min<uint64_t>(D, (uint64_t)me * C), c1 = std::min<uint64_t>(D, c0 + C);
+  PeerVecs pv{};
+  // round 1: v_bar
+  peer_exchange_sync(tr, 3, true, true);  // every rank's v is final
+  for (int p = 0; p < R; ++p) {
+    pv.src[p] = reinterpret_cast<uintptr_t>(P.dv.remote[p]);
+    pv.dst[p] = reinterpret_cast<uintptr_t>(P.vb.remote[p]);
+  }
+  peer_cmean(pv, R, W, D, c0, c1, s);
+  peer_exchange_sync(tr, 4, true, true);  // v_bar complete everywhere
+  const float* vb = static_cast<const float*>(P.vb.local);
+  float* terms = static_cast<float*>(P.terms.local);
+  for (uint32_t l = 0; l < W; ++l)
+    merge_terms(tr->x + l * D, tr->m + l * D, vb, D, alpha, terms + l * D, s);
+  // round 2: x = cmean(terms), into worker 0 of every rank
+  peer_exchange_sync(tr, 5, true, true);
+  for (int p = 0; p < R; ++p) {
+    pv.src[p] = reinterpret_cast<uintptr_t>(P.terms.remote[p]);
+    pv.dst[p] = reinterpret_cast<uintptr_t>(P.dx.remote[p]);
+  }
+  peer_cmean(pv, R, W, D, c0, c1, s);
+  peer_exchange_sync(tr, 6, true, true);
+  float* x = tr->x;
+  for (uint32_t l = 0; l < W; ++l) {
+    if (l) KP_CUDA(cudaMemcpyAsync(x + l * D, x, D * 4, cudaMemcpyDeviceToDevice, s));
+    KP_CUDA(cudaMemcpyAsync(tr->vbar + l * D, vb, D * 4, cudaMemcpyDeviceToDevice, s));
+    if (reset) KP_CUDA(cudaMemcpyAsync(tr->v + l * D, vb, D * 4, cudaMemcpyDeviceToDevice, s));
+  }
 }
 
 PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
@@ -720,8 +779,11 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
     tr->x_uniform = false;
   } else {
     for (uint32_t l = 0; l < tr->W; ++l) dense_moments(tr->m + l * D, tr->v + l * D, tr->g + l * D, D, h, s);
-    merge_states(tr->comm, s, tr->W, D, tr->x, tr->m, tr->v, tr->vbar, h.alpha,
-                 tr->cfg.reset_local_v != 0, tr->mws);
+    if (tr->world > 1 && tr->peer.mode == 1)
+      merge_states_peer(tr, h.alpha, tr->cfg.reset_local_v != 0);
+    else
+      merge_states(tr->comm, s, tr->W, D, tr->x, tr->m, tr->v, tr->vbar, h.alpha,
+                   tr->cfg.reset_local_v != 0, tr->mws);
     tr->merges++;
     tr->x_uniform = true;
   }

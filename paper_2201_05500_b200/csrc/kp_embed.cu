@@ -177,6 +177,7 @@ struct SegArgs {
   float* grad_out;
   const uint32_t* out_idx;
   float* partials;
+  const uint32_t* first;  // [nchunks] segment holding the chunk's first position
   uint32_t CH;
   int apply;
   int peer;     // store through pm (remote windows) instead of grad_out
@@ -252,13 +253,7 @@ __global__ void __launch_bounds__(256, 6) k_seg_chunks(SegArgs a, TView t) {
   (void)pw;
   for (uint64_t c = g0; c < nchunks; c += ng) {
     const uint32_t p0 = (uint32_t)c * a.CH, p1 = min(a.n_pos, p0 + a.CH);
-    // largest u with seg[u] <= p0
-    uint32_t lo = 0, hi = a.U;
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (a.seg[mid] <= p0) lo = mid; else hi = mid;
-    }
-    uint32_t u = lo;
+    uint32_t u = a.first[c];  // largest u with seg[u] <= p0
     for (;;) {
       const uint32_t s0 = a.seg[u], s1 = a.seg[u + 1];
       Row<LPG, NV, V4> acc;
@@ -321,15 +316,29 @@ __device__ __forceinline__ void sum_p(const float* P, uint64_t lo, uint64_t hi, 
   }
 }
 
+// chunk c's first position c*CH lies in segment first[c]: for every u, the
+// chunks whose start falls in [seg[u], seg[u+1])
+__global__ void k_chunk_first(const uint32_t* __restrict__ seg, uint32_t U, uint32_t CH,
+                              uint32_t nchunks, uint32_t* __restrict__ first) {
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
+    const uint32_t c0 = (seg[u] + CH - 1) / CH, c1 = min(nchunks, (seg[u + 1] + CH - 1) / CH);
+    for (uint32_t c = c0; c < c1; ++c) first[c] = u;
+  }
+}
+
+// Segments crossing a chunk boundary: each is handled once, at the first
+// boundary it crosses (c = its start chunk + 1), found through first[c].
 template <int LPG, int NV, bool V4>
 __global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t, const float* __restrict__ Q) {
   const int gl = threadIdx.x % LPG;
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
   const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
-  for (uint64_t u = g0; u < a.U; u += ng) {
+  const uint32_t nchunks = (a.n_pos + a.CH - 1) / a.CH;
+  for (uint64_t c = 1 + g0; c < nchunks; c += ng) {
+    const uint32_t u = a.first[c];
     const uint32_t s0 = a.seg[u], s1 = a.seg[u + 1];
     const uint32_t c0 = s0 / a.CH, c1 = (s1 - 1) / a.CH;
-    if (c0 == c1) continue;
+    if (c0 + 1 != c || c1 == c0) continue;
     const uint64_t lo = 2ull * c0 + 1, hi = 2ull * c1 + 1;  // [lo, hi)
     Row<LPG, NV, V4> acc;
     acc.zero();
@@ -341,7 +350,7 @@ __global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t, const float
       sum_p(Q, qa, qb, a.e, acc, gl);
       sum_p(a.partials, qb * QB, hi, a.e, acc, gl);
     }
-    finalize(a, t, (uint32_t)u, acc, gl);
+    finalize(a, t, u, acc, gl);
   }
   if (a.peer) __threadfence_system();
 }
@@ -354,7 +363,9 @@ void launch_seg(const SegArgs& a, const TView& t, float* Q, cudaStream_t s) {
   if (nP >= QB) {
     k_seg_blocksum<LPG, NV, V4><<<grid_cap(((uint64_t)(nP / QB) * LPG + 255) / 256), 256, 0, s>>>(a, nP, Q); ::kp::count_launch();
   }
-  k_seg_fix<LPG, NV, V4><<<grid_cap(((uint64_t)a.U * LPG + 255) / 256), 256, 0, s>>>(a, t, Q); ::kp::count_launch();
+  if (nchunks > 1) {
+    k_seg_fix<LPG, NV, V4><<<grid_cap(((uint64_t)nchunks * LPG + 255) / 256), 256, 0, s>>>(a, t, Q); ::kp::count_launch();
+  }
 }
 
 template <int LPG, int NV, bool V4>
@@ -450,6 +461,9 @@ void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* 
   a.CH = 64;
   const uint32_t nchunks = (n_pos + a.CH - 1) / a.CH;
   a.partials = ws.partials.get<float>((size_t)nchunks * 2 * e);
+  uint32_t* first = ws.first.get<uint32_t>(nchunks);
+  k_chunk_first<<<grid_cap(((uint64_t)n_unique + 255) / 256), 256, 0, s>>>(d_seg, n_unique, a.CH, nchunks, first); ::kp::count_launch();
+  a.first = first;
   a.apply = t != nullptr;
   a.peer = pm != nullptr;
   if (pm) a.pm = *pm;

@@ -96,7 +96,7 @@ void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_row_of_
 // Deterministic segmented reduce of coefficient-scaled upstream rows by
 // unique key, times inv_n, then the sparse rule applied in place to the row.
 struct SegWs {
-  DevBuf partials, qsums;
+  DevBuf partials, qsums, first;
 };
 // ---------------------------------------------------------- peer memory ----
 // Destination map for kernels that write their output straight into the
@@ -120,6 +120,13 @@ __device__ __forceinline__ char* peer_dst(const PeerMap& pm, uint32_t i) {
 struct PeerFlags {
   uintptr_t flag[kMaxPeers];  // &flags_p[phase][me] in every peer p's window
 };
+struct PeerVecs {
+  uintptr_t src[kMaxPeers];  // rank p's [W][D] worker vectors
+  uintptr_t dst[kMaxPeers];  // rank p's [D] result
+};
+// centered mean of elements [c0, c1) over all ranks' workers, into every rank
+void peer_cmean(const PeerVecs& pv, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1,
+                cudaStream_t s);
 // keys[t] = unique[perm[t]] -> peer windows (the owner's received keys)
 void peer_send_keys(const uint64_t* d_unique, const uint32_t* d_perm, uint32_t n, const PeerMap& pm,
                     cudaStream_t s);

@@ -73,7 +73,33 @@ __global__ void k_wait(const uint64_t* flags, int R, uint64_t seq, uint32_t* err
   __threadfence_system();
 }
 
+// centered mean over all N = R*W global workers of elements [c0, c1):
+// worker i = (rank p, local l) at src[p] + l*D (remote loads over NVLink),
+// result stored into dst[p] of every rank (remote stores). Same expression
+// tree and worker order as k_cmean (common.hpp:27-45).
+__global__ void k_cmean_peer(PeerVecs pv, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1) {
+  const float n = (float)(R * W);
+  for (uint64_t j = c0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < c1;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const float base = reinterpret_cast<const float*>(pv.src[0])[j];
+    float acc = 0.f;
+    for (int p = 0; p < R; ++p) {
+      const float* sp = reinterpret_cast<const float*>(pv.src[p]);
+      for (uint32_t l = 0; l < W; ++l) acc = __fadd_rn(acc, __fsub_rn(sp[(uint64_t)l * D + j], base));
+    }
+    const float r = __fadd_rn(base, __fdiv_rn(acc, n));
+    for (int p = 0; p < R; ++p) reinterpret_cast<float*>(pv.dst[p])[j] = r;
+  }
+  __threadfence_system();
+}
+
 }  // namespace
+
+void peer_cmean(const PeerVecs& pv, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1,
+                cudaStream_t s) {
+  if (c1 <= c0) return;
+  k_cmean_peer<<<(unsigned)std::min<uint64_t>((c1 - c0 + 255) / 256, 148 * 8), 256, 0, s>>>(pv, R, W, D, c0, c1); ::kp::count_launch();
+}
 
 void peer_send_keys(const uint64_t* d_unique, const uint32_t* d_perm, uint32_t n, const PeerMap& pm,
                     cudaStream_t s) {
