@@ -118,6 +118,20 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Split mode. Truncating (default): the tensor core reads a raw fp32 operand
+// as tf32 by dropping the 13 low mantissa bits, so hi needs no conversion and
+// no copy -- the TMA-loaded fp32 tile IS the hi operand -- and only
+// lo = x - trunc(x) (exact) is produced: half the TMEM/smem split traffic.
+// KP_TC_RN selects the round-to-nearest split (hi = tf32_rn(x)).
+#ifdef KP_TC_RN
+constexpr bool kTrunc = false;
+#else
+constexpr bool kTrunc = true;
+#endif
+__device__ __forceinline__ float lo_trunc(float x) {
+  return __fsub_rn(x, __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
+}
+
 // x -> (hi, lo): hi = tf32 round-to-nearest of x, lo = x - hi (exact in fp32)
 __device__ __forceinline__ void split3(float& x, float& lo) {
   uint32_t h;
@@ -242,6 +256,23 @@ __device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_
         "r"(tmem_a), "l"(b), "r"(idesc_tf32_cg<false, BMN, 2>()), "r"(accum));
   }
 }
+// A and B from shared memory
+template <bool AMN, bool BMN, int CG>
+__device__ __forceinline__ void mma_ss(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
+  if (CG == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc_tf32_cg<AMN, BMN, 1>()), "r"(accum));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc_tf32_cg<AMN, BMN, 2>()), "r"(accum));
+  }
+}
 // MMA completion -> barrier b in this CTA (CG = 1) or in both CTAs of the pair
 template <int CG>
 __device__ __forceinline__ void commit_cg(uint64_t* b) {
@@ -281,11 +312,15 @@ __device__ __forceinline__ void split_tile(uint8_t* tile, uint8_t* lo_tile, int 
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     float4 l;
-    split3(x[i].x, l.x);
-    split3(x[i].y, l.y);
-    split3(x[i].z, l.z);
-    split3(x[i].w, l.w);
-    hi[ct + 256 * i] = x[i];
+    if (kTrunc) {  // hi stays the raw tile
+      l = make_float4(lo_trunc(x[i].x), lo_trunc(x[i].y), lo_trunc(x[i].z), lo_trunc(x[i].w));
+    } else {
+      split3(x[i].x, l.x);
+      split3(x[i].y, l.y);
+      split3(x[i].z, l.z);
+      split3(x[i].w, l.w);
+      hi[ct + 256 * i] = x[i];
+    }
     lo[ct + 256 * i] = l;
   }
 }
@@ -422,11 +457,18 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           const uint32_t d = tmem + (uint32_t)(buf * TC_BN);
           const uint32_t ahi = tmem + TC_ACOL + 64u * (uint32_t)(g % TC_ASLOTS), alo = ahi + 32u;
           const uint32_t b = smem_u32(sB(s)), blo = smem_u32(sBlo(s));
+          const uint32_t asm_ = smem_u32(sA(s));
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 8; ++kk) {
             const uint32_t ob = kstep_off<BMN>(kk);
-            mma_ts<BMN, CG>(d, ahi + 8u * kk, sdesc<BMN>(b + ob), (kin | kk) != 0);
-            mma_ts<BMN, CG>(d, ahi + 8u * kk, sdesc<BMN>(blo + ob), 1);
+            if (kTrunc) {
+              const uint64_t ad = sdesc<AMN>(asm_ + kstep_off<AMN>(kk));
+              mma_ss<AMN, BMN, CG>(d, ad, sdesc<BMN>(b + ob), (kin | kk) != 0);
+              mma_ss<AMN, BMN, CG>(d, ad, sdesc<BMN>(blo + ob), 1);
+            } else {
+              mma_ts<BMN, CG>(d, ahi + 8u * kk, sdesc<BMN>(b + ob), (kin | kk) != 0);
+              mma_ts<BMN, CG>(d, ahi + 8u * kk, sdesc<BMN>(blo + ob), 1);
+            }
             mma_ts<BMN, CG>(d, alo + 8u * kk, sdesc<BMN>(b + ob), 1);
           }
           commit_cg<CG>(&empty[s]);
@@ -457,7 +499,11 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           float x = v[j], l;
-          split3(x, l);
+          if (kTrunc) {
+            l = lo_trunc(x);
+          } else {
+            split3(x, l);
+          }
           hi[j] = __float_as_uint(x);
           lo[j] = __float_as_uint(l);
         }
@@ -467,7 +513,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
         if (NS > TC_ASLOTS && g >= TC_ASLOTS) mbar_wait(&afree[as], ((g / TC_ASLOTS) - 1) & 1);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + 64u * (uint32_t)as + 16u * h;
-        tmem_st16(ta, hi);
+        if (!kTrunc) tmem_st16(ta, hi);  // truncating: the MMA reads hi from the smem tile
         tmem_st16(ta + 32u, lo);
         if (!BPRE) split_tile<CG>(sB(s), sBlo(s), ct);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -612,7 +658,8 @@ __global__ void k_split(const float* __restrict__ x, float* __restrict__ hi, flo
                         size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     float v = x[i], l;
-    split3(v, l);
+    if (kTrunc) l = lo_trunc(v);
+    else split3(v, l);
     hi[i] = v;
     lo[i] = l;
   }
