@@ -116,6 +116,14 @@ int kp_table_export(kp_table* t, uint64_t* keys, float* w, float* s1, float* s2,
  * d_seg[U+1] (nullable) segment starts in sorted order. */
 int kp_dedup(const uint64_t* d_keys, uint32_t n, uint64_t* d_unique, uint32_t* d_inverse,
              uint32_t* d_seg, uint32_t* n_unique, kp_stream s);
+/* Owner-side dedup of the G > 1 exchange: the keys are R runs (one per source
+ * rank, run r = [run_off[r], run_off[r+1]), host array), each strictly
+ * ascending. Same outputs as kp_dedup (the cross-worker sparse_sum key union of
+ * proj/src/trainer.cpp:163,180-186, ties in source order), plus d_sorted_pos[p]
+ * = input position of sorted position p (may be NULL). */
+int kp_dedup_runs(const uint64_t* d_keys, uint32_t n, const uint64_t* run_off, uint32_t n_runs,
+                  uint64_t* d_unique, uint32_t* d_inverse, uint32_t* d_seg, uint32_t* d_sorted_pos,
+                  uint32_t* n_unique, kp_stream s);
 /* Owner shard = key % G (proj/src/trainer.cpp:83): stable bucket of ascending
  * unique keys; d_perm[slot] = unique index, d_pos[unique] = slot, counts[G] host. */
 int kp_shard(const uint64_t* d_unique, uint32_t n, uint32_t G, uint32_t* d_perm, uint32_t* d_pos,

@@ -26,6 +26,7 @@ try:
         comm_unique_id,
         compute_auc,
         dedup,
+        dedup_runs,
         gemm_nt,
         gemm_tn,
         device_count,
@@ -44,7 +45,7 @@ except ImportError as e:  # pragma: no cover - exercised only on broken installs
 __all__ = [
     "AdamHyper", "Comm", "ConfigError", "DeviceError", "KpsimError", "KStepEngine", "StoreError",
     "TieredStore", "Trainer", "WorkerState", "accumulate_moments", "adagrad_sparse_update", "auc_device",
-    "comm_unique_id", "compute_auc", "dedup", "gemm_nt", "gemm_tn", "device_count", "global_merge", "launch_count",
+    "comm_unique_id", "compute_auc", "dedup", "dedup_runs", "gemm_nt", "gemm_tn", "device_count", "global_merge", "launch_count",
     "local_adam_step", "shard", "version",
 ]
 

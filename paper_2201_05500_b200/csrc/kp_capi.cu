@@ -622,7 +622,12 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
     }
     tr->mark(6);
     // owner side: dedup received keys (stable: source order inside a key)
-    dedup(rk, Rn, tr->dd_owner, s);
+    {
+      // each source's keys arrive ascending: merge the R runs
+      std::vector<uint64_t> run_off(R + 1, 0);
+      for (int p = 0; p < R; ++p) run_off[p + 1] = run_off[p] + tr->cnt_recv[p];
+      dedup_runs(rk, Rn, run_off, tr->dd_owner, s);
+    }
     tr->mark(0);
     const uint32_t Uo = tr->dd_owner.n_unique;
     uint32_t* orows = tr->owner_rows.get<uint32_t>(std::max<uint32_t>(Uo, 1));
@@ -1231,6 +1236,26 @@ int kp_dedup(const uint64_t* d_keys, uint32_t n, uint64_t* d_unique, uint32_t* d
     if (n && d_inverse)
       KP_CUDA(cudaMemcpyAsync(d_inverse, ws.d_inverse, (size_t)n * 4, cudaMemcpyDeviceToDevice, st(s)));
     if (d_seg) KP_CUDA(cudaMemcpyAsync(d_seg, ws.d_seg, (size_t)(U + 1) * 4, cudaMemcpyDeviceToDevice, st(s)));
+    KP_CUDA(cudaStreamSynchronize(st(s)));
+  });
+}
+int kp_dedup_runs(const uint64_t* d_keys, uint32_t n, const uint64_t* run_off, uint32_t n_runs,
+                  uint64_t* d_unique, uint32_t* d_inverse, uint32_t* d_seg, uint32_t* d_sorted_pos,
+                  uint32_t* n_unique, kp_stream s) {
+  return guard([&] {
+    KP_CHECK(n_runs >= 1 && run_off && run_off[0] == 0 && run_off[n_runs] == n, kErrConfig,
+             "dedup_runs: run offsets must start at 0 and end at n");
+    static thread_local DedupWs ws;
+    std::vector<uint64_t> ro(run_off, run_off + n_runs + 1);
+    dedup_runs(d_keys, n, ro, ws, st(s));
+    const uint32_t U = ws.n_unique;
+    *n_unique = U;
+    if (U) KP_CUDA(cudaMemcpyAsync(d_unique, ws.d_unique, (size_t)U * 8, cudaMemcpyDeviceToDevice, st(s)));
+    if (n && d_inverse)
+      KP_CUDA(cudaMemcpyAsync(d_inverse, ws.d_inverse, (size_t)n * 4, cudaMemcpyDeviceToDevice, st(s)));
+    if (d_seg) KP_CUDA(cudaMemcpyAsync(d_seg, ws.d_seg, (size_t)(U + 1) * 4, cudaMemcpyDeviceToDevice, st(s)));
+    if (n && d_sorted_pos)
+      KP_CUDA(cudaMemcpyAsync(d_sorted_pos, ws.sorted_vals, (size_t)n * 4, cudaMemcpyDeviceToDevice, st(s)));
     KP_CUDA(cudaStreamSynchronize(st(s)));
   });
 }

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <functional>
+#include <vector>
 #include "kp_common.cuh"
 
 namespace kp {
@@ -31,6 +32,10 @@ struct DedupWs {
 // (ws.d_sorted_mapped[p] = occ_map[sorted_vals[p]]), e.g. the bag of each occurrence.
 void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
            const uint32_t* d_occ_map = nullptr);
+// dedup() of keys made of runs [run_off[i], run_off[i+1]), each strictly
+// ascending: merge tree instead of the radix sort, identical outputs
+void dedup_runs(const uint64_t* d_keys, uint32_t n, const std::vector<uint64_t>& run_off,
+                DedupWs& ws, cudaStream_t s);
 
 // Stable bucket of ascending unique keys by owner = key % G.
 // perm[i] = unique index placed at bucket slot i; pos[u] = slot of unique u;

@@ -14,6 +14,8 @@
 //    shared-memory staged scatter so global writes are digit-run coalesced;
 //  * tiles of 2048 pairs (256 threads x 8), grids are multiples of the SM
 //    count for every config that matters.
+#include <vector>
+
 #include "kp_internal.cuh"
 
 namespace kp {
@@ -368,6 +370,88 @@ __global__ void __launch_bounds__(ST) k_shard_emit(const uint64_t* __restrict__ 
   }
 }
 
+__global__ void k_key_iota(uint32_t* __restrict__ v, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
+}
+
+// ---- merge of sorted runs (owner side of the exchange) --------------------
+// Up to kMaxRuns pairs per level; block b -> (pair, output tile) through the
+// per-pair tile prefix. A wins ties (stable: lower source first).
+constexpr int kMaxRuns = 64;
+struct MergeLevel {
+  int pairs;
+  uint32_t a0[kMaxRuns / 2], na[kMaxRuns / 2], nb[kMaxRuns / 2];  // A = [a0, a0+na), B follows
+  uint32_t tile0[kMaxRuns / 2 + 1];                               // first block of each pair
+};
+
+__device__ __forceinline__ uint32_t merge_path(const uint64_t* A, uint32_t na, const uint64_t* B,
+                                               uint32_t nb, uint32_t d) {
+  uint32_t lo = d > nb ? d - nb : 0, hi = min(d, na);
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (A[mid] <= B[d - 1 - mid]) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(ST) k_merge_level(const uint64_t* __restrict__ kin,
+                                                    const uint32_t* __restrict__ vin,
+                                                    uint64_t* __restrict__ kout,
+                                                    uint32_t* __restrict__ vout, MergeLevel L) {
+  __shared__ uint64_t sk[TILE];
+  __shared__ uint32_t sv[TILE];
+  __shared__ uint32_t s_split[2];
+  int pr = 0;
+  while (pr + 1 < L.pairs && blockIdx.x >= L.tile0[pr + 1]) ++pr;
+  const uint32_t a0 = L.a0[pr], na = L.na[pr], nb = L.nb[pr];
+  const uint64_t* A = kin + a0;
+  const uint64_t* B = A + na;
+  const uint32_t d0 = (blockIdx.x - L.tile0[pr]) * TILE, d1 = min(na + nb, d0 + TILE);
+  if (threadIdx.x < 2) s_split[threadIdx.x] = merge_path(A, na, B, nb, threadIdx.x ? d1 : d0);
+  __syncthreads();
+  const uint32_t ia0 = s_split[0], ia1 = s_split[1];
+  const uint32_t ib0 = d0 - ia0, ib1 = d1 - ia1;
+  const uint32_t la = ia1 - ia0, lb = ib1 - ib0;
+  for (uint32_t i = threadIdx.x; i < la + lb; i += ST) {
+    if (i < la) {
+      sk[i] = A[ia0 + i];
+      sv[i] = vin ? vin[a0 + ia0 + i] : a0 + ia0 + i;
+    } else {
+      sk[i] = B[ib0 + i - la];
+      sv[i] = vin ? vin[a0 + na + ib0 + i - la] : a0 + na + ib0 + i - la;
+    }
+  }
+  __syncthreads();
+  // this thread's IPT outputs: diagonal t*IPT inside the tile
+  const uint32_t dt = min(threadIdx.x * IPT, la + lb);
+  uint32_t ia = merge_path(sk, la, sk + la, lb, dt), ib = dt - ia;
+  uint64_t ok[IPT];
+  uint32_t ov[IPT];
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const bool takeA = ib >= lb || (ia < la && sk[ia] <= sk[la + ib]);
+    const uint32_t src = takeA ? ia : la + ib;
+    ok[r] = sk[src < la + lb ? src : 0];
+    ov[r] = sv[src < la + lb ? src : 0];
+    if (takeA) ++ia; else ++ib;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
+    const uint32_t o = threadIdx.x * IPT + r;
+    if (o < la + lb) {
+      sk[o] = ok[r];
+      sv[o] = ov[r];
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < la + lb; i += ST) {
+    kout[a0 + d0 + i] = sk[i];
+    vout[a0 + d0 + i] = sv[i];
+  }
+}
+
 }  // namespace
 
 void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
@@ -474,6 +558,76 @@ void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
     k_dedup_emit<uint64_t><<<nb, ST, 0, s>>>(kin, mm, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
                                              ws.d_nunique, nb, d_occ_map, ws.d_sorted_mapped); ::kp::count_launch();
   }
+  KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
+  KP_CUDA(cudaStreamSynchronize(s));
+}
+
+// Same outputs as dedup() when the keys are R runs that are each strictly
+// ascending (the owner's received keys: each source sends its unique keys in
+// order): a pairwise merge tree (log2 R levels of merge path) replaces the
+// radix passes.
+void dedup_runs(const uint64_t* d_keys, uint32_t n, const std::vector<uint64_t>& run_off,
+                DedupWs& ws, cudaStream_t s) {
+  const int R = (int)run_off.size() - 1;
+  if (n == 0 || R < 1 || R > kMaxRuns) {
+    dedup(d_keys, n, ws, s);
+    return;
+  }
+  ws.n = n;
+  ws.d_nunique = ws.scalars.get<uint32_t>(4);
+  const uint32_t nb = ceil_div(n, TILE);
+  uint64_t* ka = ws.keys_a.get<uint64_t>(n);
+  uint64_t* kb = ws.keys_b.get<uint64_t>(n);
+  uint32_t* va = ws.vals_a.get<uint32_t>(n);
+  uint32_t* vb = ws.vals_b.get<uint32_t>(n);
+  std::vector<uint64_t> runs(run_off);
+  const uint64_t* kin = d_keys;
+  const uint32_t* vin = nullptr;
+  uint64_t* kout = ka;
+  uint32_t* vout = va;
+  if (R == 1) {  // already sorted
+    KP_CUDA(cudaMemcpyAsync(ka, d_keys, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
+    k_key_iota<<<std::min<uint32_t>(nb * 8, 148 * 16), 256, 0, s>>>(va, n); ::kp::count_launch();
+    kin = ka;
+    vin = va;
+  }
+  while (runs.size() > 2) {
+    MergeLevel L{};
+    std::vector<uint64_t> next{runs[0]};
+    uint32_t tiles = 0;
+    for (size_t i = 0; i + 1 < runs.size(); i += 2) {
+      const uint64_t a0 = runs[i], am = runs[i + 1];
+      const uint64_t b1 = i + 2 < runs.size() ? runs[i + 2] : am;  // odd run: merged with nothing
+      L.a0[L.pairs] = (uint32_t)a0;
+      L.na[L.pairs] = (uint32_t)(am - a0);
+      L.nb[L.pairs] = (uint32_t)(b1 - am);
+      L.tile0[L.pairs] = tiles;
+      tiles += ceil_div((uint32_t)(b1 - a0), TILE);
+      ++L.pairs;
+      next.push_back(b1);
+    }
+    L.tile0[L.pairs] = tiles;
+    if (tiles) {
+      k_merge_level<<<tiles, ST, 0, s>>>(kin, vin, kout, vout, L); ::kp::count_launch();
+    }
+    runs.swap(next);
+    kin = kout;
+    vin = vout;
+    kout = (kout == ka) ? kb : ka;
+    vout = (vout == va) ? vb : va;
+  }
+  ws.sorted_keys = kin;
+  ws.sorted_vals = vin;
+  uint32_t* bcount = ws.bcount.get<uint32_t>(nb);
+  ws.d_unique = ws.unique.get<uint64_t>(n);
+  ws.d_inverse = ws.inverse.get<uint32_t>(n);
+  ws.d_seg = ws.seg.get<uint32_t>(n + 1);
+  ws.d_sorted_mapped = nullptr;
+  auto* mm = ws.minmax.get<unsigned long long>(2);
+  k_head_count<uint64_t><<<nb, ST, 0, s>>>(kin, n, bcount); ::kp::count_launch();
+  k_scan_rows<<<1, ST, 0, s>>>(bcount, nb, ws.d_nunique + 1); ::kp::count_launch();
+  k_dedup_emit<uint64_t><<<nb, ST, 0, s>>>(kin, mm, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
+                                           ws.d_nunique, nb, nullptr, nullptr); ::kp::count_launch();
   KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaStreamSynchronize(s));
 }

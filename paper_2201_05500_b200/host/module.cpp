@@ -225,6 +225,35 @@ PYBIND11_MODULE(_kpsim_b200, m) {
           return py::make_tuple(uq, inv, seg);
         },
         py::arg("keys"), py::arg("device") = 0);
+  m.def("dedup_runs",
+        [](Arr<uint64_t> keys, Arr<uint64_t> run_lengths, int device) {
+          check(kp_set_device(device));
+          const uint32_t n = (uint32_t)keys.size();
+          const uint32_t R = (uint32_t)run_lengths.size();
+          std::vector<uint64_t> off(R + 1, 0);
+          for (uint32_t r = 0; r < R; ++r) off[r + 1] = off[r] + run_lengths.data()[r];
+          void *dk, *du, *di, *ds, *dp;
+          check(kp_dev_alloc(std::max<size_t>(n, 1) * 8, &dk));
+          check(kp_dev_alloc(std::max<size_t>(n, 1) * 8, &du));
+          check(kp_dev_alloc(std::max<size_t>(n, 1) * 4, &di));
+          check(kp_dev_alloc((std::max<size_t>(n, 1) + 1) * 4, &ds));
+          check(kp_dev_alloc(std::max<size_t>(n, 1) * 4, &dp));
+          uint32_t U = 0;
+          int rc = kp_memcpy_h2d(dk, keys.data(), (size_t)n * 8);
+          if (rc == KP_OK)
+            rc = kp_dedup_runs((const uint64_t*)dk, n, off.data(), R, (uint64_t*)du, (uint32_t*)di,
+                               (uint32_t*)ds, (uint32_t*)dp, &U, nullptr);
+          Arr<uint64_t> uq(U);
+          Arr<uint32_t> inv(n), seg(U + 1), pos(n);
+          if (rc == KP_OK) rc = kp_memcpy_d2h(uq.mutable_data(), du, (size_t)U * 8);
+          if (rc == KP_OK) rc = kp_memcpy_d2h(inv.mutable_data(), di, (size_t)n * 4);
+          if (rc == KP_OK) rc = kp_memcpy_d2h(seg.mutable_data(), ds, (size_t)(U + 1) * 4);
+          if (rc == KP_OK) rc = kp_memcpy_d2h(pos.mutable_data(), dp, (size_t)n * 4);
+          for (void* p : {dk, du, di, ds, dp}) kp_dev_free(p);
+          check(rc);
+          return py::make_tuple(uq, inv, seg, pos);
+        },
+        py::arg("keys"), py::arg("run_lengths"), py::arg("device") = 0);
   m.def("shard",
         [](Arr<uint64_t> uniq, uint32_t G, int device) {
           check(kp_set_device(device));

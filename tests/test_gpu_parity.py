@@ -64,6 +64,27 @@ def test_dedup_bit_exact(kp, n, V, zipf):
         assert np.array_equal(u, O.ref_dedup(keys))
 
 
+@pytest.mark.parametrize("R,n_per,V", [(1, 1000, 10**4), (2, 50_000, 10**5), (3, 7, 20),
+                                       (4, 300_000, 10**6), (8, 120_000, 10**6), (5, 0, 10)])
+def test_dedup_runs_matches_dedup(kp, R, n_per, V):
+    """Owner-side dedup of the exchange (merge of per-source ascending runs):
+    identical unique/inverse/segments to the radix dedup, and sorted positions
+    equal to a stable sort (ties in source order)."""
+    rng = np.random.default_rng(R * 1000 + n_per)
+    runs = []
+    for r in range(R):
+        k = np.unique(rng.integers(0, V, max(n_per - 3 * r, 0), dtype=np.uint64))
+        runs.append(k)
+    if R >= 2 and len(runs[0]):
+        runs[1] = np.unique(np.concatenate([runs[1], runs[0][:5], [np.uint64(2**64 - 1)]]))
+    keys = np.concatenate(runs).astype(np.uint64) if runs else np.zeros(0, np.uint64)
+    lens = np.array([len(r) for r in runs], np.uint64)
+    u, inv, seg, pos = kp.dedup_runs(keys, lens)
+    u2, inv2, seg2 = kp.dedup(keys)
+    assert np.array_equal(u, u2) and np.array_equal(inv, inv2) and np.array_equal(seg, seg2)
+    assert np.array_equal(pos, np.argsort(keys, kind="stable").astype(np.uint32))
+
+
 @pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
 def test_shard_bit_exact(kp, G):
     rng = np.random.default_rng(G)
