@@ -128,6 +128,14 @@ constexpr bool kTrunc = false;
 #else
 constexpr bool kTrunc = true;
 #endif
+// KP_ALO_SMEM: A lo operand in shared memory (all three MMAs SS, TMEM holds
+// only the accumulators). Measured slower (shared memory bandwidth is the
+// scarcer resource: +7% GEMM time); the default keeps A lo in TMEM.
+#ifdef KP_ALO_SMEM
+constexpr bool kAloSmem = kTrunc;
+#else
+constexpr bool kAloSmem = false;
+#endif
 __device__ __forceinline__ float lo_trunc(float x) {
   return __fsub_rn(x, __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
 }
@@ -197,10 +205,11 @@ template <int CG>
 struct TcCfg {
   static constexpr int BROWS = TC_BN / CG;  // B rows held by one CTA
   static constexpr uint32_t B_BYTES = BROWS * TC_BK * 4;
-  static constexpr uint32_t STAGE = A_BYTES + 2 * B_BYTES;  // A fp32, B (hi), B lo
+  // A fp32, B (hi), B lo, and (kAloSmem) the A lo tile
+  static constexpr uint32_t STAGE = A_BYTES + 2 * B_BYTES + (kAloSmem ? A_BYTES : 0);
   // smem ring depth (a deeper ring, 6 stages at CG = 2 with separate TMEM A
   // slot barriers, measured no faster)
-  static constexpr int STAGES = 4;
+  static constexpr int STAGES = (kAloSmem && CG == 1) ? 3 : 4;
   static constexpr uint32_t SMEM = STAGES * STAGE + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
 
@@ -350,6 +359,28 @@ __device__ __forceinline__ void load_a_row16(const uint8_t* tile, int r, int k0,
   }
 }
 
+// inverse of load_a_row16: 16 values (bit patterns) -> row r, k [k0, k0+16)
+template <bool MN>
+__device__ __forceinline__ void store_a_row16(uint8_t* tile, int r, int k0, const uint32_t (&v)[16]) {
+  if (!MN) {
+    uint8_t* row = tile + r * 128;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = (k0 >> 2) + i;
+      *reinterpret_cast<uint4*>(row + ((c ^ (r & 7)) << 4)) =
+          make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+  } else {
+    uint8_t* box = tile + (r >> 5) * 4096;
+    const int mm = (r & 31) * 4;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int k = k0 + j;
+      *reinterpret_cast<uint32_t*>(box + k * 128 + (mm ^ ((k & 3) << 5))) = v[j];
+    }
+  }
+}
+
 template <bool AMN, bool BMN, bool BPRE, int CG>
 __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -388,6 +419,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   auto sA = [&](int s) { return smem + s * Cfg::STAGE; };
   auto sB = [&](int s) { return smem + s * Cfg::STAGE + A_BYTES; };
   auto sBlo = [&](int s) { return smem + s * Cfg::STAGE + A_BYTES + Cfg::B_BYTES; };
+  auto sAlo = [&](int s) { return smem + s * Cfg::STAGE + A_BYTES + 2 * Cfg::B_BYTES; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -469,7 +501,10 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
               mma_ts<BMN, CG>(d, ahi + 8u * kk, sdesc<BMN>(b + ob), (kin | kk) != 0);
               mma_ts<BMN, CG>(d, ahi + 8u * kk, sdesc<BMN>(blo + ob), 1);
             }
-            mma_ts<BMN, CG>(d, alo + 8u * kk, sdesc<BMN>(b + ob), 1);
+            if (kAloSmem)
+              mma_ss<AMN, BMN, CG>(d, sdesc<AMN>(smem_u32(sAlo(s)) + kstep_off<AMN>(kk)), sdesc<BMN>(b + ob), 1);
+            else
+              mma_ts<BMN, CG>(d, alo + 8u * kk, sdesc<BMN>(b + ob), 1);
           }
           commit_cg<CG>(&empty[s]);
           if (NS > TC_ASLOTS) commit_cg<CG>(&afree[g % TC_ASLOTS]);
@@ -513,8 +548,12 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
         if (NS > TC_ASLOTS && g >= TC_ASLOTS) mbar_wait(&afree[as], ((g / TC_ASLOTS) - 1) & 1);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + 64u * (uint32_t)as + 16u * h;
-        if (!kTrunc) tmem_st16(ta, hi);  // truncating: the MMA reads hi from the smem tile
-        tmem_st16(ta + 32u, lo);
+        if (kAloSmem) {
+          store_a_row16<AMN>(sAlo(s), r, h * 16, lo);
+        } else {
+          if (!kTrunc) tmem_st16(ta, hi);  // truncating: the MMA reads hi from the smem tile
+          tmem_st16(ta + 32u, lo);
+        }
         if (!BPRE) split_tile<CG>(sB(s), sBlo(s), ct);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         fence_proxy_async();
