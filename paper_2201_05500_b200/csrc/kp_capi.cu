@@ -136,6 +136,7 @@ struct kp_trainer {
   DevBuf hist_scores, hist_labels, all_preds, all_labels, gather_tmp;
   uint64_t hist_n = 0;
   DevBuf rows, rowocc, bag_offs, bag_of_occ, pooled, inv_count, dpooled, preds, err, loss, check;
+  DevBuf inst_max;  // max |pooled row| per instance, from the pool kernel
   DevBuf xbar, pred_keep, lossg;
   // exchange buffers (G > 1)
   DevBuf perm, pos, send_keys, recv_keys, owner_rows, owner_idx, send_rows, recv_rows, send_grads,
@@ -658,7 +659,9 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   compose(pr.idx, tr->dd.d_inverse, sv.n_occ, rowocc, s);
   float* pooled = tr->pooled.get<float>((size_t)std::max<uint32_t>(nb, 1) * tr->e);
   float* invc = tr->inv_count.get<float>(std::max<uint32_t>(nb, 1));
-  pool(bag_offs, nb, rowocc, pr.src, tr->e, tr->cfg.pooling == 1, pooled, invc, s);
+  // max |row| of the MLP input per instance (fp16-operand first layer)
+  float* imax = tr->inst_max.get<float>(std::max<uint32_t>(sv.n_inst, 1));
+  pool(bag_offs, nb, rowocc, pr.src, tr->e, tr->cfg.pooling == 1, pooled, invc, s, imax, tr->S);
   tr->mark(2);
   return pr;
 }
@@ -740,7 +743,9 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
       KP_CUDA(cudaMemsetAsync(tr->g + l * D, 0, D * 4, s));
       continue;
     }
+    tr->mlp.in_rowmax = static_cast<const float*>(tr->inst_max.p) + lo;
     mlp_forward(tr->shape, tr->x + l * D, pooled + (size_t)lo * in_w, Bw, preds + lo, tr->mlp, s);
+    tr->mlp.in_rowmax = nullptr;
     mlp_backward(tr->shape, tr->x + l * D, pooled + (size_t)lo * in_w, Bw, preds + lo,
                  sv.labels + lo, tr->g + l * D, dpooled + (size_t)lo * in_w,
                  tr->cfg.pooling == 1 ? invc + (size_t)lo * tr->S : nullptr, tr->S, tr->e,
@@ -803,8 +808,10 @@ void predict_pass(kp_trainer* tr, const StepView& sv, float* d_preds_out) {
   float* xb = tr->xbar.get<float>(tr->D);
   compute_xbar(tr, xb);
   pull_and_pool(tr, sv, false);
+  tr->mlp.in_rowmax = static_cast<const float*>(tr->inst_max.p);
   mlp_forward(tr->shape, xb, static_cast<const float*>(tr->pooled.p), sv.n_inst, d_preds_out,
               tr->mlp, tr->s);
+  tr->mlp.in_rowmax = nullptr;
   tr->mark(3);
 }
 
@@ -1307,9 +1314,23 @@ int kp_gemm_nt(const float* d_A, int lda, const float* d_B, int ldb, float* d_C,
                int N, int K, int engine, kp_stream s) {
   return guard([&] {
     const bool tc_ok = tc_gemm_supported(M, N, K, d_A, lda, d_B, ldb);
-    KP_CHECK(engine != 2 || tc_ok, kErrConfig, "gemm_nt: shape/alignment not supported by tcgen05 path");
+    KP_CHECK(engine < 2 || tc_ok, kErrConfig, "gemm_nt: shape/alignment not supported by tcgen05 path");
+    KP_CHECK(engine != 3 || (ldb % 8 == 0 && K % 8 == 0), kErrConfig,
+             "gemm_nt: fp16 path needs K and ldb multiples of 8");
     if (engine == 1 || !tc_ok) {
       simt_gemm_nt(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, st(s));
+    } else if (engine == 3) {
+      // fp16-operand path (per-row scaled 3xFP16), as used for the first MLP layer
+      static thread_local DevBuf amax, bhi, blo, bexp;
+      float* am = amax.get<float>(M);
+      rowmax(d_A, M, K, lda, am, st(s));
+      __half* h = reinterpret_cast<__half*>(bhi.get<uint16_t>((size_t)N * ldb));
+      __half* l = reinterpret_cast<__half*>(blo.get<uint16_t>((size_t)N * ldb));
+      int* ex = bexp.get<int>(N);
+      split_h(d_B, N, K, ldb, h, l, ex, st(s));
+      GemmEpi ep{0, 0, nullptr, nullptr, 0, nullptr, 1, 1};
+      tc_gemm_nt_h(M, N, K, d_A, lda, am, h, l, ex, ldb, d_C, ldc, ep, st(s));
+      KP_CUDA(cudaStreamSynchronize(st(s)));
     } else {
       GemmEpi ep{0, 0, nullptr, nullptr, 0, nullptr, 1, 1};
       tc_gemm_nt(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, ep, st(s));

@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(256, 5) k_pool(const uint32_t* __restrict__ ba
                                               const uint32_t* __restrict__ rowocc,
                                               const float* __restrict__ src, uint32_t e, int mean,
                                               float* __restrict__ pooled,
-                                              float* __restrict__ inv_count) {
+                                              float* __restrict__ inv_count,
+                                              unsigned* __restrict__ inst_max, uint32_t S) {
   const int gl = threadIdx.x % LPG;
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
   const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
@@ -154,6 +155,110 @@ __global__ void __launch_bounds__(256, 5) k_pool(const uint32_t* __restrict__ ba
       }
       acc[i].store(pooled + b * e, gl, e);
     }
+    if (inst_max) {
+      // max |pooled| per instance (= per row of the [B][S*e] MLP input), the
+      // row scale of the fp16-operand first layer. S >= PB: the group's PB
+      // consecutive bags touch at most two instances -> two lane reductions
+      // and at most two atomics per group; else one per bag.
+      if (S >= PB) {
+        const uint64_t i0 = b0 / S;
+        float m0 = 0.f, m1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < PB; ++i) {
+          if (b0 + i >= n_bags) break;
+          float mx = 0.f;
+#pragma unroll
+          for (int q = 0; q < (V4 ? 4 : NV); ++q) mx = fmaxf(mx, fabsf(acc[i].v[q]));
+          if ((b0 + i) / S == i0) m0 = fmaxf(m0, mx);
+          else m1 = fmaxf(m1, mx);
+        }
+#pragma unroll
+        for (int o = LPG / 2; o; o >>= 1) {
+          m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o, LPG));
+          m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o, LPG));
+        }
+        if (gl == 0) {
+          if (m0 > 0.f) atomicMax(inst_max + i0, __float_as_uint(m0));
+          if (m1 > 0.f) atomicMax(inst_max + i0 + 1, __float_as_uint(m1));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < PB; ++i) {
+          float mx = 0.f;
+#pragma unroll
+          for (int q = 0; q < (V4 ? 4 : NV); ++q) mx = fmaxf(mx, fabsf(acc[i].v[q]));
+#pragma unroll
+          for (int o = LPG / 2; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o, LPG));
+          const uint64_t b = b0 + i;
+          if (gl == 0 && b < n_bags && mx > 0.f) atomicMax(inst_max + b / S, __float_as_uint(mx));
+        }
+      }
+    }
+  }
+}
+
+// Instance-major pooling (S >= 2*PB, row maxima requested): one warp owns an
+// instance's S bags -- its two 16-lane groups take PB bags each per
+// iteration -- so the max |pooled| of the instance (the fp16 first layer's row
+// scale) is a warp reduction and one store, no atomics. Same per-bag
+// arithmetic as k_pool.
+template <int LPG, int NV, bool V4>
+__global__ void __launch_bounds__(256, 5) k_pool_inst(const uint32_t* __restrict__ bag_offs,
+                                                      uint32_t n_inst, uint32_t S,
+                                                      const uint32_t* __restrict__ rowocc,
+                                                      const float* __restrict__ src, uint32_t e, int mean,
+                                                      float* __restrict__ pooled,
+                                                      float* __restrict__ inv_count,
+                                                      float* __restrict__ inst_max) {
+  constexpr int GPW = 32 / LPG;  // groups per warp
+  const int lane = threadIdx.x & 31, gl = lane % LPG, gw = lane / LPG;
+  const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t inst = w0; inst < n_inst; inst += nw) {
+    const uint64_t bend = (inst + 1) * S;
+    float wmax = 0.f;
+    for (uint64_t b0 = inst * S + (uint64_t)gw * PB; b0 < bend; b0 += (uint64_t)GPW * PB) {
+      uint32_t o[PB + 1];
+#pragma unroll
+      for (int i = 0; i <= PB; ++i) o[i] = bag_offs[b0 + i < bend ? b0 + i : bend];
+      Row<LPG, NV, V4> acc[PB], r[PB];
+      uint32_t maxlen = 0;
+#pragma unroll
+      for (int i = 0; i < PB; ++i) {
+        acc[i].zero();
+        maxlen = max(maxlen, o[i + 1] - o[i]);
+      }
+      for (uint32_t j = 0; j < maxlen; ++j) {
+#pragma unroll
+        for (int i = 0; i < PB; ++i) {
+          if (o[i] + j < o[i + 1]) {
+            const uint32_t rr = rowocc[o[i] + j];
+            if (rr == kNoRow) r[i].zero();
+            else r[i].load(src + (uint64_t)rr * e, gl, e);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < PB; ++i)
+          if (o[i] + j < o[i + 1]) acc[i].add(r[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < PB; ++i) {
+        const uint64_t b = b0 + i;
+        if (b >= bend) break;
+        const uint32_t len = o[i + 1] - o[i];
+        if (mean) {
+          const float inv = len ? __fdiv_rn(1.f, (float)len) : 1.f;
+          if (len) acc[i].scale(inv);
+          if (gl == 0) inv_count[b] = inv;
+        }
+        acc[i].store(pooled + b * e, gl, e);
+#pragma unroll
+        for (int q = 0; q < (V4 ? 4 : NV); ++q) wmax = fmaxf(wmax, fabsf(acc[i].v[q]));
+      }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, off));
+    if (lane == 0) inst_max[inst] = wmax;
   }
 }
 
@@ -371,9 +476,17 @@ void launch_seg(const SegArgs& a, const TView& t, float* Q, cudaStream_t s) {
 template <int LPG, int NV, bool V4>
 void launch_pool(const uint32_t* bag_offs, uint32_t n_bags, const uint32_t* rowocc,
                  const float* src, uint32_t e, bool mean, float* pooled, float* inv_count,
-                 cudaStream_t s) {
+                 float* inst_max, uint32_t S, cudaStream_t s) {
+  if (inst_max && S >= 2 * PB && LPG <= 16) {
+    const uint32_t n_inst = n_bags / S;
+    k_pool_inst<LPG, NV, V4><<<grid_cap(((uint64_t)n_inst * 32 + 255) / 256), 256, 0, s>>>(
+        bag_offs, n_inst, S, rowocc, src, e, mean ? 1 : 0, pooled, inv_count, inst_max); ::kp::count_launch();
+    return;
+  }
+  if (inst_max) KP_CUDA(cudaMemsetAsync(inst_max, 0, (size_t)(n_bags / S) * 4, s));
   k_pool<LPG, NV, V4><<<grid_cap(((uint64_t)(n_bags + PB - 1) / PB * LPG + 255) / 256), 256, 0, s>>>(
-      bag_offs, n_bags, rowocc, src, e, mean ? 1 : 0, pooled, inv_count); ::kp::count_launch();
+      bag_offs, n_bags, rowocc, src, e, mean ? 1 : 0, pooled, inv_count,
+      reinterpret_cast<unsigned*>(inst_max), S); ::kp::count_launch();
 }
 
 // Dispatch on the embedding width: float4 groups for e in {4,8,...,128},
@@ -435,9 +548,10 @@ void compose(const uint32_t* d_idx, const uint32_t* d_inverse, uint32_t n, uint3
 
 void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_row_of_occ,
           const float* d_src, uint32_t e, bool mean, float* d_pooled, float* d_inv_count,
-          cudaStream_t s) {
+          cudaStream_t s, float* d_inst_max, uint32_t S) {
   if (n_bags == 0) return;
-  dispatch_e<PoolF>(e, d_bag_offs, n_bags, d_row_of_occ, d_src, e, mean, d_pooled, d_inv_count, s);
+  dispatch_e<PoolF>(e, d_bag_offs, n_bags, d_row_of_occ, d_src, e, mean, d_pooled, d_inv_count,
+                    d_inst_max, S, s);
 }
 
 void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* d_sorted_vals,

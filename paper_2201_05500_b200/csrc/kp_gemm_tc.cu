@@ -25,6 +25,7 @@
 // (tcgen05.commit); tfull[b] (commit) -> drain -> tempty[b] (128 arrivals).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 
 #include <cstdlib>
 #include <mutex>
@@ -201,10 +202,13 @@ constexpr int TC_WARPS = 18;
 constexpr int TC_EPI_T = 256;  // drain/epilogue threads
 constexpr uint32_t TC_ACOL = TC_NBUF * TC_BN;  // first A-operand column
 
-template <int CG>
+// H: fp16 operands (kind::f16, 2x the tf32 rate) -- A split on chip into
+// fp16 hi/lo with a per-row power-of-two scale, B pre-split fp16 hi/lo (64-byte
+// K-major rows, SWIZZLE_64B) with per-row scales; see k_tc_gemm.
+template <int CG, bool H = false>
 struct TcCfg {
   static constexpr int BROWS = TC_BN / CG;  // B rows held by one CTA
-  static constexpr uint32_t B_BYTES = BROWS * TC_BK * 4;
+  static constexpr uint32_t B_BYTES = BROWS * TC_BK * (H ? 2 : 4);
   // A fp32, B (hi), B lo, and (kAloSmem) the A lo tile
   static constexpr uint32_t STAGE = A_BYTES + 2 * B_BYTES + (kAloSmem ? A_BYTES : 0);
   // smem ring depth (a deeper ring, 6 stages at CG = 2 with separate TMEM A
@@ -282,6 +286,54 @@ __device__ __forceinline__ void mma_ss(uint32_t tmem_d, uint64_t a, uint64_t b, 
         "l"(a), "l"(b), "r"(idesc_tf32_cg<AMN, BMN, 2>()), "r"(accum));
   }
 }
+// fp16 K-major operand with 64-byte rows (32 halves), SWIZZLE_64B: 8-row
+// groups at SBO = 512 B
+__device__ __forceinline__ uint64_t sdesc_h64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+template <int CG>
+__host__ __device__ constexpr uint32_t idesc_f16_cg() {
+  // D f32, A/B f16 (format 0), both K-major
+  return (1u << 4) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((TC_BM * CG) >> 4) << 24);
+}
+template <int CG>
+__device__ __forceinline__ void mma_h_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t accum) {
+  if (CG == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc_f16_cg<1>()), "r"(accum));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc_f16_cg<2>()), "r"(accum));
+  }
+}
+// power-of-two scale e of a row with max |x| = mx: mx * 2^e in [2^14, 2^15)
+__host__ __device__ __forceinline__ int row_exp(float mx) {
+  if (!(mx > 0.f) || !(mx < 3.0e38f)) return 0;
+  int ex;
+  frexpf(mx, &ex);
+  const int e = 15 - ex;
+  return e > 126 ? 126 : (e < -126 ? -126 : e);
+}
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((e + 127) << 23); }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+      "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+}
+
 // MMA completion -> barrier b in this CTA (CG = 1) or in both CTAs of the pair
 template <int CG>
 __device__ __forceinline__ void commit_cg(uint64_t* b) {
@@ -381,12 +433,13 @@ __device__ __forceinline__ void store_a_row16(uint8_t* tile, int r, int k0, cons
   }
 }
 
-template <bool AMN, bool BMN, bool BPRE, int CG>
+template <bool AMN, bool BMN, bool BPRE, int CG, bool H = false>
 __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmBlo, int M, int N, int K, int kps,
               float* __restrict__ C, int ldc, GemmEpi ep) {
-  using Cfg = TcCfg<CG>;
+  static_assert(!H || (!AMN && !BMN && BPRE), "fp16 mode: K-major A, pre-split K-major B");
+  using Cfg = TcCfg<CG, H>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int NS = Cfg::STAGES;
@@ -468,7 +521,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           mbar_expect_tx(&full[s], A_BYTES + (BPRE ? 2 : 1) * Cfg::B_BYTES);
           const int k0 = z * kps + kb * TC_BK;
           load_rows<AMN, TC_BM>(sA(s), &tmA, &full[s], k0, m0);
-          load_rows<BMN, Cfg::BROWS>(sB(s), &tmB, &full[s], k0, nb0);
+          load_rows<BMN, Cfg::BROWS>(sB(s), &tmB, &full[s], k0, nb0);  // (H: one 64 B-row box)
           if (BPRE) load_rows<BMN, Cfg::BROWS>(sBlo(s), &tmBlo, &full[s], k0, nb0);
         }
       }
@@ -490,6 +543,16 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           const uint32_t ahi = tmem + TC_ACOL + 64u * (uint32_t)(g % TC_ASLOTS), alo = ahi + 32u;
           const uint32_t b = smem_u32(sB(s)), blo = smem_u32(sBlo(s));
           const uint32_t asm_ = smem_u32(sA(s));
+          if constexpr (H) {
+            // A hi at slot columns [0,16), A lo at [16,32): 2 halves per column
+#pragma unroll
+            for (int kk = 0; kk < TC_BK / 16; ++kk) {
+              const uint64_t bh = sdesc_h64(b + 32u * kk), bl = sdesc_h64(blo + 32u * kk);
+              mma_h_ts<CG>(d, ahi + 8u * kk, bh, (kin | kk) != 0);
+              mma_h_ts<CG>(d, ahi + 8u * kk, bl, 1);
+              mma_h_ts<CG>(d, ahi + 16u + 8u * kk, bh, 1);
+            }
+          } else {
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 8; ++kk) {
             const uint32_t ob = kstep_off<BMN>(kk);
@@ -506,6 +569,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
             else
               mma_ts<BMN, CG>(d, alo + 8u * kk, sdesc<BMN>(b + ob), 1);
           }
+          }
           commit_cg<CG>(&empty[s]);
           if (NS > TC_ASLOTS) commit_cg<CG>(&afree[g % TC_ASLOTS]);
           if (kin == TC_CH - 1 || kb == nk - 1) {
@@ -520,6 +584,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     const int ct = threadIdx.x - 64;
     const int q = warp & 3, h = (warp - 2) >> 2;
     const int r = q * 32 + lane;  // tile row == TMEM lane
+    float h_scale = 1.f;          // (H) this row's 2^e
     int g = 0;
     for (int w = unit; w < works; w += units) {
       int m0, n0, z, nk;
@@ -530,6 +595,33 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
         mbar_wait(&full[s], ph);
         float v[16];
         load_a_row16<AMN>(sA(s), r, h * 16, v);
+        if constexpr (H) {
+          // row scale: the row's max |x| (a_rowmax) -> 2^e
+          if (kb == 0) {
+            const int m = m0 + r;
+            h_scale = pow2f(m < M ? row_exp(ep.a_rowmax[m]) : 0);
+          }
+          uint32_t hp[8], lp[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float x0 = __fmul_rn(v[2 * j], h_scale), x1 = __fmul_rn(v[2 * j + 1], h_scale);
+            const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+            const __half l0 = __float2half_rn(__fsub_rn(x0, __half2float(h0)));
+            const __half l1 = __float2half_rn(__fsub_rn(x1, __half2float(h1)));
+            hp[j] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+            lp[j] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+          }
+          const int as = g % TC_ASLOTS;
+          tc_fence_after();
+          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + 64u * (uint32_t)as + 8u * h;
+          tmem_st8(ta, hp);
+          tmem_st8(ta + 16u, lp);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          named_sync(1, 256);
+          if (ct == 0) arrive_leader<CG>(&conv[s]);
+          continue;
+        }
         uint32_t hi[16], lo[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -600,6 +692,14 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
       float* st = epi_smem + (warp - 10) * (32 * EPI_LD);
       const int rsub = lane >> 2, c4 = (lane & 3) * 4;
       const bool cvec = (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+      float rs[4] = {1.f, 1.f, 1.f, 1.f};  // (H) 2^-ea of this thread's 4 output rows
+      if constexpr (H) {
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int m = m0 + q * 32 + it * 8 + rsub;
+          rs[it] = m < M ? pow2f(-row_exp(__ldg(ep.a_rowmax + m))) : 1.f;
+        }
+      }
 #pragma unroll
       for (int c0 = 0; c0 < 64; c0 += 16) {
         __syncwarp();
@@ -609,6 +709,11 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
               make_float4(acc[c0 + j], acc[c0 + j + 1], acc[c0 + j + 2], acc[c0 + j + 3]);
         __syncwarp();
         const int n = n0 + half * 64 + c0 + c4;
+        float cs[4] = {1.f, 1.f, 1.f, 1.f};  // (H) 2^-eb of the 4 columns
+        if constexpr (H) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) cs[t] = n + t < N ? pow2f(-__ldg(ep.b_exp + n + t)) : 1.f;
+        }
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
           const int rr = it * 8 + rsub;
@@ -617,6 +722,10 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           float4 v = *reinterpret_cast<const float4*>(st + rr * EPI_LD + c4);
           float* vv = reinterpret_cast<float*>(&v);
           const bool full4 = n + 4 <= N;
+          if constexpr (H) {  // undo the operand scales: x 2^-(ea + eb[n]), exact
+#pragma unroll
+            for (int t = 0; t < 4; ++t) vv[t] = __fmul_rn(__fmul_rn(vv[t], rs[it]), cs[t]);
+          }
           if (ep.mode == 1) {
 #pragma unroll
             for (int t = 0; t < 4; ++t)
@@ -693,6 +802,64 @@ bool make_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t cols, u
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp16 [rows][cols] (leading dimension ld halves), boxes of box_rows x 32
+// halves (64-byte rows), 64B swizzle
+bool make_map_h(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// one block per row of W [N][K]: row max -> exponent e (row_exp), then the
+// fp16 split of W * 2^e: hi = rn(x), lo = rn(x - hi)
+__global__ void k_split_h(const float* __restrict__ w, int K, int ld, __half* __restrict__ hi,
+                          __half* __restrict__ lo, int* __restrict__ exps) {
+  __shared__ float red[32];
+  const float* row = w + (size_t)blockIdx.x * ld;
+  float mx = 0.f;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, fabsf(row[k]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (threadIdx.x == 0) red[0] = mx;
+  }
+  __syncthreads();
+  const int e = row_exp(red[0]);
+  if (threadIdx.x == 0) exps[blockIdx.x] = e;
+  const float sc = pow2f(e);
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const float x = __fmul_rn(row[k], sc);
+    const __half h = __float2half_rn(x);
+    hi[(size_t)blockIdx.x * ld + k] = h;
+    lo[(size_t)blockIdx.x * ld + k] = __float2half_rn(__fsub_rn(x, __half2float(h)));
+  }
+}
+
+// one warp per row: max |A[m][k]| (the per-row scale of the fp16 A operand)
+__global__ void k_rowmax(const float* __restrict__ a, int M, int K, int lda, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int m = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; m < M; m += (gridDim.x * blockDim.x) >> 5) {
+    const float* row = a + (size_t)m * lda;
+    float mx = 0.f;
+    for (int k = lane; k < K; k += 32) mx = fmaxf(mx, fabsf(row[k]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) out[m] = mx;
+  }
+}
+
 __global__ void k_split(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo,
                         size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -717,7 +884,7 @@ int choose_cg(int M) {
 }
 
 // concurrently resident work units (CTAs or CTA pairs)
-template <bool AMN, bool BMN, bool BPRE, int CG>
+template <bool AMN, bool BMN, bool BPRE, int CG, bool H = false>
 int resident_units() {
   static int units = 0;
   if (units) return units;
@@ -728,7 +895,7 @@ int resident_units() {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * CG, 1, 1);
     cfg.blockDim = dim3(TC_WARPS * 32, 1, 1);
-    cfg.dynamicSmemBytes = TcCfg<CG>::SMEM;
+    cfg.dynamicSmemBytes = TcCfg<CG, H>::SMEM;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CG;
@@ -737,21 +904,23 @@ int resident_units() {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k_tc_gemm<AMN, BMN, BPRE, CG>, &cfg) == cudaSuccess && n > 0)
+    if (cudaOccupancyMaxActiveClusters(&n, k_tc_gemm<AMN, BMN, BPRE, CG, H>, &cfg) == cudaSuccess && n > 0)
       units = std::min(units, n);
     cudaGetLastError();
   }
   return units;
 }
 
-template <bool AMN, bool BMN, bool BPRE, int CG>
-int launch_cg(int M, int N, int K, const float* A, int lda, const float* B, const float* Blo, int ldb,
+template <bool AMN, bool BMN, bool BPRE, int CG, bool H = false>
+int launch_cg(int M, int N, int K, const float* A, int lda, const void* B, const void* Blo, int ldb,
               float* C, int ldc, int splits, const GemmEpi& ep, cudaStream_t s) {
-  using Cfg = TcCfg<CG>;
+  using Cfg = TcCfg<CG, H>;
   CUtensorMap ta, tb, tbl;
   // K-major: [rows][K] with box_rows-row boxes; MN-major: [K][rows] with 32x32 boxes
-  auto mk = [&](CUtensorMap* m, const float* p, bool mn, int rows, int ld, int box_rows) {
-    return mn ? make_map(m, p, K, rows, ld, 32, true) : make_map(m, p, rows, K, ld, box_rows);
+  auto mk = [&](CUtensorMap* m, const void* p, bool mn, int rows, int ld, int box_rows) {
+    if (H && p != A) return make_map_h(m, p, rows, K, ld, box_rows);
+    const float* f = static_cast<const float*>(p);
+    return mn ? make_map(m, f, K, rows, ld, 32, true) : make_map(m, f, rows, K, ld, box_rows);
   };
   const bool ok = mk(&ta, A, AMN, M, lda, TC_BM) && mk(&tb, B, BMN, N, ldb, Cfg::BROWS) &&
                   (!BPRE || mk(&tbl, Blo, BMN, N, ldb, Cfg::BROWS));
@@ -759,7 +928,7 @@ int launch_cg(int M, int N, int K, const float* A, int lda, const float* B, cons
   KP_CHECK(ok, kErrCuda, "cuTensorMapEncodeTiled failed");
   static bool attr = false;
   if (!attr) {
-    KP_CUDA(cudaFuncSetAttribute(k_tc_gemm<AMN, BMN, BPRE, CG>,
+    KP_CUDA(cudaFuncSetAttribute(k_tc_gemm<AMN, BMN, BPRE, CG, H>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     attr = true;
   }
@@ -767,7 +936,7 @@ int launch_cg(int M, int N, int K, const float* A, int lda, const float* B, cons
   kps = (kps + TC_BK - 1) / TC_BK * TC_BK;
   const unsigned nz = ceil_div(K, kps);
   const uint64_t works = (uint64_t)ceil_div(N, TC_BN) * ceil_div(M, TC_BM * CG) * nz;
-  const int units = std::max(1, resident_units<AMN, BMN, BPRE, CG>() - (g_reserve_sms + CG - 1) / CG);
+  const int units = std::max(1, resident_units<AMN, BMN, BPRE, CG, H>() - (g_reserve_sms + CG - 1) / CG);
   const unsigned grid = (unsigned)std::min<uint64_t>(works, (uint64_t)units) * CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
@@ -781,7 +950,7 @@ int launch_cg(int M, int N, int K, const float* A, int lda, const float* B, cons
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  KP_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<AMN, BMN, BPRE, CG>, ta, tb, tbl, M, N, K, kps, C, ldc,
+  KP_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<AMN, BMN, BPRE, CG, H>, ta, tb, tbl, M, N, K, kps, C, ldc,
                              ep));
   ::kp::count_launch();
   return (int)nz;
@@ -848,6 +1017,32 @@ void tc_gemm_nt(int M, int N, int K, const float* A, int lda, const float* B, in
 void tc_gemm_nt_pre(int M, int N, int K, const float* A, int lda, const float* Bhi, const float* Blo,
                     int ldb, float* C, int ldc, const GemmEpi& ep, cudaStream_t s) {
   launch<false, false, true>(M, N, K, A, lda, Bhi, Blo, ldb, C, ldc, 1, ep, s);
+}
+
+// fp16 operands (see TcCfg): C = epi(2^-(ea[m]+eb[n]) * (A*2^ea)(B*2^eb)^T)
+void tc_gemm_nt_h(int M, int N, int K, const float* A, int lda, const float* a_rowmax,
+                  const __half* Bhi, const __half* Blo, const int* b_exp, int ldb, float* C, int ldc,
+                  const GemmEpi& ep, cudaStream_t s) {
+  GemmEpi e2 = ep;
+  e2.a_rowmax = a_rowmax;
+  e2.b_exp = b_exp;
+  if (choose_cg(M) == 2)
+    launch_cg<false, false, true, 2, true>(M, N, K, A, lda, Bhi, Blo, ldb, C, ldc, 1, e2, s);
+  else
+    launch_cg<false, false, true, 1, true>(M, N, K, A, lda, Bhi, Blo, ldb, C, ldc, 1, e2, s);
+}
+void split_h(const float* W, int N, int K, int ld, __half* hi, __half* lo, int* exps, cudaStream_t s) {
+  k_split_h<<<N, 256, 0, s>>>(W, K, ld, hi, lo, exps); ::kp::count_launch();
+}
+void rowmax(const float* A, int M, int K, int lda, float* out, cudaStream_t s) {
+  k_rowmax<<<std::min<unsigned>(ceil_div((uint64_t)M * 32, 256), 148 * 16), 256, 0, s>>>(A, M, K, lda, out); ::kp::count_launch();
+}
+bool tc_h_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("KP_GEMM_F16");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // C[z][m][n] = sum_{k in split z} A[k][m] B[k][n]   (both MN-major); returns #splits

@@ -2,6 +2,8 @@
 // include/kpsim_b200.h is built on these.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include <functional>
 #include <vector>
 #include "kp_common.cuh"
@@ -94,10 +96,11 @@ void prepare_bags(const uint32_t* d_offs, uint32_t occ_base, const uint16_t* d_s
 // row_of_occ[o] = idx[inverse[o]]  (source row of every occurrence)
 void compose(const uint32_t* d_idx, const uint32_t* d_inverse, uint32_t n, uint32_t* d_out,
              cudaStream_t s);
-// pooled[bag][e] = sum_{o in bag} src[row_of_occ[o]][e]  (x 1/|bag| when mean)
+// pooled[bag][e] = sum_{o in bag} src[row_of_occ[o]][e]  (x 1/|bag| when mean);
+// d_inst_max (optional): max |pooled| over each instance's S bags
 void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_row_of_occ,
           const float* d_src, uint32_t e, bool mean, float* d_pooled, float* d_inv_count,
-          cudaStream_t s);
+          cudaStream_t s, float* d_inst_max = nullptr, uint32_t S = 1);
 // Deterministic segmented reduce of coefficient-scaled upstream rows by
 // unique key, times inv_n, then the sparse rule applied in place to the row.
 struct SegWs {
@@ -172,6 +175,9 @@ struct GemmEpi {
   int ld_aux;
   const float* coeff;
   uint32_t S, e;
+  // fp16-operand GEMM (tc_gemm_nt_h): per-row max |A| and per-row exponent of B
+  const float* a_rowmax = nullptr;
+  const int* b_exp = nullptr;
 };
 // tcgen05 3xTF32 GEMMs (operands split hi/lo on the fly in shared memory)
 bool tc_gemm_supported(int M, int N, int K, const float* A, int lda, const float* B, int ldb);
@@ -184,6 +190,15 @@ void tc_gemm_nt_pre(int M, int N, int K, const float* A, int lda, const float* B
 int tc_gemm_tn(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
                int ldc, int splits, cudaStream_t s);
 int tc_splits(int M, int N, int K);
+// fp16-operand GEMM ("3xFP16": A, B split into fp16 hi + lo after a per-row
+// power-of-two scale; hi*hi + hi*lo + lo*hi at the f16 tensor rate). A is fp32
+// K-major with a_rowmax[m] = max_k |A[m][k]|; B is pre-split by split_h.
+void tc_gemm_nt_h(int M, int N, int K, const float* A, int lda, const float* a_rowmax,
+                  const __half* Bhi, const __half* Blo, const int* b_exp, int ldb, float* C, int ldc,
+                  const GemmEpi& ep, cudaStream_t s);
+void split_h(const float* W, int N, int K, int ld, __half* hi, __half* lo, int* exps, cudaStream_t s);
+void rowmax(const float* A, int M, int K, int lda, float* out, cudaStream_t s);
+bool tc_h_enabled();  // KP_GEMM_F16=0 keeps every GEMM on 3xTF32
 void split_hilo(const float* x, float* hi, float* lo, size_t n, cudaStream_t s);
 bool tc_enabled();  // KP_GEMM=simt disables the tensor-core path
 // leave `n` SMs free of persistent GEMM CTAs (for kernels overlapping the GEMM
@@ -210,6 +225,9 @@ struct MlpWs {
   DevBuf act[9];    // per hidden layer activations [B][width]
   DevBuf dz[2];     // ping-pong upstream grads
   DevBuf logits, delta, partials, lossp, whi, wlo, wt, wthi, wtlo;
+  // fp16-operand first layer: split weights (+ exponents) and row maxima
+  DevBuf hhi, hlo, hexp, thi, tlo, texp, amax;
+  const float* in_rowmax = nullptr;  // max |input row| from the producer (pool), else computed
 };
 // Forward over B instances (input [B][in]); writes preds (sigmoid) and
 // logits; keeps activations in ws for backward.

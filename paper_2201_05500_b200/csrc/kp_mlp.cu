@@ -14,6 +14,8 @@
 // next step.
 #include <cstdlib>
 
+#include <cuda_fp16.h>
+
 #include "kp_internal.cuh"
 
 namespace kp {
@@ -379,6 +381,11 @@ static bool gemm_pre() {
   return on;
 }
 
+// fp16-operand GEMM for the first layer: K-major, 16-byte aligned, K % 8 == 0
+static bool use_h(int M, int N, int K, const float* A, const float* W) {
+  return tc_enabled() && tc_h_enabled() && K % 8 == 0 && tc_gemm_supported(M, N, K, A, K, W, K);
+}
+
 void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_t B,
                  float* d_preds, MlpWs& ws, cudaStream_t s) {
   if (B == 0) return;
@@ -389,7 +396,20 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
     float* out = ws.act[l].get<float>((size_t)B * N);
     EpiArgs ep{kBiasAct, m.activation, d_x + m.b_off[l], nullptr, 0, nullptr, 1, 1};
     const float* W = d_x + m.w_off[l];
-    if (tc_enabled() && tc_gemm_supported(B, N, K, in, K, W, K)) {
+    if (l == 0 && use_h(B, N, K, in, W)) {
+      // first layer (the wide S*e contraction): fp16 operands, per-row scales
+      const float* am = ws.in_rowmax;
+      if (!am) {
+        float* t = ws.amax.get<float>(B);
+        rowmax(in, B, K, K, t, s);
+        am = t;
+      }
+      __half* hh = reinterpret_cast<__half*>(ws.hhi.get<uint16_t>((size_t)N * K));
+      __half* hl = reinterpret_cast<__half*>(ws.hlo.get<uint16_t>((size_t)N * K));
+      int* he = ws.hexp.get<int>(N);
+      split_h(W, N, K, K, hh, hl, he, s);
+      tc_gemm_nt_h(B, N, K, in, K, am, hh, hl, he, K, out, N, ep, s);
+    } else if (tc_enabled() && tc_gemm_supported(B, N, K, in, K, W, K)) {
       float* whi = ws.whi.get<float>((size_t)N * K);
       float* wlo = ws.wlo.get<float>((size_t)N * K);
       if (gemm_pre()) {
@@ -423,7 +443,21 @@ __global__ void k_transpose(const float* __restrict__ in, int R, int Cc, float* 
 
 // dX[B][K] = dZ[B][N] . W[N][K]  (W^T kept K-major for the tensor-core path)
 void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, const EpiArgs& ep,
-             MlpWs& ws, cudaStream_t s) {
+             MlpWs& ws, cudaStream_t s, bool first = false) {
+  if (first && N % 8 == 0 && use_h(B, K, N, dZ, W)) {
+    // first layer's input gradient (the wide output): fp16 operands
+    float* wt = ws.wt.get<float>((size_t)N * K);
+    dim3 g(ceil_div(K, 32), ceil_div(N, 32));
+    k_transpose<<<g, dim3(32, 8), 0, s>>>(W, N, K, wt); ::kp::count_launch();
+    __half* th = reinterpret_cast<__half*>(ws.thi.get<uint16_t>((size_t)N * K));
+    __half* tl = reinterpret_cast<__half*>(ws.tlo.get<uint16_t>((size_t)N * K));
+    int* te = ws.texp.get<int>(K);
+    split_h(wt, K, N, N, th, tl, te, s);
+    float* am = ws.amax.get<float>(B);
+    rowmax(dZ, B, N, N, am, s);
+    tc_gemm_nt_h(B, K, N, dZ, N, am, th, tl, te, N, out, K, ep, s);
+    return;
+  }
   if (tc_enabled() && tc_gemm_supported(B, K, N, dZ, N, W, N)) {
     float* wt = ws.wt.get<float>((size_t)N * K);
     dim3 g(ceil_div(K, 32), ceil_div(N, 32));
@@ -492,7 +526,7 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
     // the weight-gradient GEMM
     if (l == 0 && d_dinput) {
       EpiArgs ep{d_coeff ? kCoeff : kStore, 0, nullptr, nullptr, 0, d_coeff, S, e};
-      dx_gemm(B, K, N, dZ, d_x + m.w_off[l], d_dinput, ep, ws, s);
+      dx_gemm(B, K, N, dZ, d_x + m.w_off[l], d_dinput, ep, ws, s, true);
       if (after_dinput) (*after_dinput)();
     }
     // dW_l[o][i] = sum_b dZ[b][o] in[b][i]   (deterministic split-K)

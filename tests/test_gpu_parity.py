@@ -313,6 +313,30 @@ def test_tcgen05_gemm_fp32_accuracy(kp, M, N, K):
     assert err_tc < 3 * err_simt + 2e-6, (err_tc, err_simt)
 
 
+@pytest.mark.parametrize("M,N,K,spread", [(128, 128, 32, 0), (300, 256, 6400, 0), (65, 40, 96, 0),
+                                          (4096, 128, 256, 0), (1000, 256, 6400, 8), (512, 6400, 256, 4)])
+def test_tcgen05_gemm_f16_scaled_accuracy(kp, M, N, K, spread):
+    """fp16-operand GEMM (per-row power-of-two scales, hi*hi + hi*lo + lo*hi):
+    fp32-level error like the 3xTF32 path, also with rows spanning 2^+-spread
+    magnitudes, all-zero rows and tiny elements inside a row."""
+    rng = np.random.default_rng(M * 7 + N + K + spread)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    if spread:
+        A *= (2.0 ** rng.integers(-spread, spread + 1, (M, 1))).astype(np.float32)
+        B *= (2.0 ** rng.integers(-spread, spread + 1, (N, 1))).astype(np.float32)
+        A[0] = 0.0
+        A[1, :K // 2] *= np.float32(1e-6)
+    want = A.astype(np.float64) @ B.astype(np.float64).T
+    scale = np.sqrt(K) * np.maximum(np.abs(A).max(1, keepdims=True), 1e-30) * np.abs(B).max(1)
+    h = kp.gemm_nt(A, B, engine=3)
+    simt = kp.gemm_nt(A, B, engine=1)
+    err_h = np.max(np.abs(h - want) / scale)
+    err_simt = np.max(np.abs(simt - want) / scale)
+    print(f"gemm f16 M={M} N={N} K={K} spread={spread}: normalized err f16x3={err_h:.3e} simt={err_simt:.3e}")
+    assert err_h < 3 * err_simt + 2e-6, (err_h, err_simt)
+
+
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 6400, 4096), (128, 256, 65536), (40, 100, 300)])
 def test_tcgen05_gemm_tn_fp32_accuracy(kp, M, N, K):
     """MN-major operands (the weight gradient dZ^T X over the batch), split-K."""
