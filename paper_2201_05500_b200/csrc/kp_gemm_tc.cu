@@ -604,12 +604,13 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           uint32_t hp[8], lp[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
+            // packed conversions: cvt.rn.f16x2.f32 (low half = even k)
             const float x0 = __fmul_rn(v[2 * j], h_scale), x1 = __fmul_rn(v[2 * j + 1], h_scale);
-            const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
-            const __half l0 = __float2half_rn(__fsub_rn(x0, __half2float(h0)));
-            const __half l1 = __float2half_rn(__fsub_rn(x1, __half2float(h1)));
-            hp[j] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-            lp[j] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+            const __half2 hh = __floats2half2_rn(x0, x1);
+            const float2 hf = __half22float2(hh);
+            const __half2 ll = __floats2half2_rn(__fsub_rn(x0, hf.x), __fsub_rn(x1, hf.y));
+            hp[j] = *reinterpret_cast<const uint32_t*>(&hh);
+            lp[j] = *reinterpret_cast<const uint32_t*>(&ll);
           }
           const int as = g % TC_ASLOTS;
           tc_fence_after();
