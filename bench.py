@@ -410,18 +410,26 @@ def main():
     dom = max(stages, key=lambda k: stages[k]["ms_per_step"])
     traffic = ncu_traffic()
     if dom == "mlp":
-        # 3xTF32: every fp32 multiply-add is three tf32 MMAs (hi*hi + hi*lo +
-        # lo*hi), so the tensor pipe executes 3x the model flops. Peak: the
-        # tf32 dense rate, half the bf16 rate on Blackwell (measured bf16
-        # sustained / 2); the in-run cuBLAS tf32 GEMM is reported beside it.
-        tc = 3.0 * stages["mlp"]["achieved_tflops"]
-        peak_tf32 = bf16s / 2.0
-        roof = {"kernel": "mlp stage: tcgen05 3xTF32 GEMMs (fwd, dX, dW) + head/bias kernels",
-                "bound": "tensor", "achieved": tc, "peak": peak_tf32, "unit": "TFLOP/s",
-                "frac": tc / peak_tf32, "traffic": traffic.get("mlp"),
-                "peak_kind": f"{pk} bf16 sustained / 2 (tf32 tensor rate)",
-                "achieved_kind": "tf32 MMA work = 3 x fp32 model flops / stage time",
+        # Tensor work per step, in bf16-rate units. Every fp32 multiply-add is
+        # three MMAs: the first layer's forward and input-gradient GEMMs run
+        # them on fp16 operands (per-row scaled hi/lo, f16 = bf16 rate), the
+        # rest on tf32 (half the bf16 rate, so each tf32 MMA counts twice).
+        h_on = os.environ.get("KP_GEMM_F16", "1") != "0" and D_in % 8 == 0
+        f_l1 = 2.0 * B * D_in * hidden[0]                       # one first-layer GEMM
+        f16_flops = 2 * f_l1 if h_on else 0.0                   # fwd + dX of layer 1
+        tf32_flops = flops - f16_flops
+        work = 3.0 * f16_flops + 2 * 3.0 * tf32_flops            # bf16-equivalent MMA flops
+        sec = stages["mlp"]["ms_per_step"] / 1e3
+        tc = work / sec / 1e12
+        roof = {"kernel": "mlp stage: tcgen05 GEMMs (layer-1 fwd/dX 3xFP16 scaled, others 3xTF32) "
+                          "+ head/bias kernels",
+                "bound": "tensor", "achieved": tc, "peak": bf16s, "unit": "TFLOP/s",
+                "frac": tc / bf16s, "traffic": traffic.get("mlp"),
+                "peak_kind": f"{pk} bf16 sustained",
+                "achieved_kind": "bf16-rate-equivalent MMA work / stage time: 3 f16 MMAs per fp32 FMA "
+                                 "(layer-1 fwd, dX), 3 tf32 MMAs = 6 bf16-equivalent otherwise",
                 "fp32_model_tflops": stages["mlp"]["achieved_tflops"],
+                "mma_work_tflop_per_step": work / 1e12,
                 "cublas_tf32_tflops_8192": cublas_tf32()}
     else:
         roof = {"kernel": dom, "bound": "hbm", "achieved": stages[dom].get("achieved_gbs"),
