@@ -439,6 +439,9 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
               const __grid_constant__ CUtensorMap tmBlo, int M, int N, int K, int kps,
               float* __restrict__ C, int ldc, GemmEpi ep) {
   static_assert(!H || (!AMN && !BMN && BPRE), "fp16 mode: K-major A, pre-split K-major B");
+  // k-blocks per accumulator chunk: fp16 products are exact in fp32 and the
+  // chunk error stays below the fp32 SIMT GEMM's at 8 (256 k); tf32 keeps 4
+  constexpr int CH = H ? 2 * TC_CH : TC_CH;
   using Cfg = TcCfg<CG, H>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -535,7 +538,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = g % NS;
           const uint32_t ph = (g / NS) & 1;
-          const int kin = kb % TC_CH, buf = c % TC_NBUF;
+          const int kin = kb % CH, buf = c % TC_NBUF;
           if (kin == 0 && c >= TC_NBUF) mbar_wait_cl<CG>(&tempty[buf], ((c / TC_NBUF) - 1) & 1);
           mbar_wait_cl<CG>(&conv[s], ph);
           tc_fence_after();
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           }
           commit_cg<CG>(&empty[s]);
           if (NS > TC_ASLOTS) commit_cg<CG>(&afree[g % TC_ASLOTS]);
-          if (kin == TC_CH - 1 || kb == nk - 1) {
+          if (kin == CH - 1 || kb == nk - 1) {
             commit_cg<CG>(&tfull[buf]);
             ++c;
           }
@@ -667,7 +670,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
       float acc[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) acc[j] = 0.f;
-      const int nch = (nk + TC_CH - 1) / TC_CH;
+      const int nch = (nk + CH - 1) / CH;
       for (int ci = 0; ci < nch; ++ci, ++c) {
         const int buf = c % TC_NBUF;
         mbar_wait(&tfull[buf], (c / TC_NBUF) & 1);
