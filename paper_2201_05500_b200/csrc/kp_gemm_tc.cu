@@ -214,7 +214,10 @@ struct TcCfg {
   // smem ring depth (a deeper ring, 6 stages at CG = 2 with separate TMEM A
   // slot barriers, measured no faster)
   static constexpr int STAGES = (kAloSmem && CG == 1) ? 3 : 4;
-  static constexpr uint32_t SMEM = STAGES * STAGE + EPI_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  // CG == 2: per epilogue warp two dense 32x16 fp32 tiles (TMA-store sources)
+  static constexpr uint32_t EPI_DENSE = CG == 2 ? 8 * 2 * 32 * 16 * 4 : 0;
+  static constexpr uint32_t SMEM =
+      STAGES * STAGE + EPI_BYTES + EPI_DENSE + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -436,8 +439,8 @@ __device__ __forceinline__ void store_a_row16(uint8_t* tile, int r, int k0, cons
 template <bool AMN, bool BMN, bool BPRE, int CG, bool H = false>
 __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmBlo, int M, int N, int K, int kps,
-              float* __restrict__ C, int ldc, GemmEpi ep) {
+              const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmC,
+              int c_tma, int M, int N, int K, int kps, float* __restrict__ C, int ldc, GemmEpi ep) {
   static_assert(!H || (!AMN && !BMN && BPRE), "fp16 mode: K-major A, pre-split K-major B");
   // k-blocks per accumulator chunk: fp16 products are exact in fp32 and the
   // chunk error stays below the fp32 SIMT GEMM's at 8 (256 k); tf32 keeps 4
@@ -455,6 +458,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   uint64_t* tempty = tfull + TC_NBUF;        // drain -> MMA (leader; CG arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + TC_NBUF);
   float* epi_smem = reinterpret_cast<float*>(smem + NS * Cfg::STAGE + 512);
+  float* epi_dense = reinterpret_cast<float*>(smem + NS * Cfg::STAGE + 512 + EPI_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
@@ -663,6 +667,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     const int q = warp & 3;               // TMEM lane quarter
     const int half = (warp - 10) >> 2;    // column half of the 128-wide tile
     const int et = threadIdx.x - 320;
+    uint32_t tma_seq = 0;  // TMA stores issued by this warp (dense buffer parity)
     int c = 0;
     for (int w = unit; w < works; w += units) {
       int m0, n0, z, nk;
@@ -713,6 +718,12 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
               make_float4(acc[c0 + j], acc[c0 + j + 1], acc[c0 + j + 2], acc[c0 + j + 3]);
         __syncwarp();
         const int n = n0 + half * 64 + c0 + c4;
+        // dense 32x16 tile for the TMA store (double-buffered per warp)
+        float* dense = epi_dense + ((warp - 10) * 2 + (tma_seq & 1)) * (32 * 16);
+        if (Cfg::EPI_DENSE && c_tma) {
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+        }
         float cs[4] = {1.f, 1.f, 1.f, 1.f};  // (H) 2^-eb of the 4 columns
         if constexpr (H) {
 #pragma unroll
@@ -753,6 +764,10 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
             for (int t = 0; t < 4; ++t)
               if (n + t < N) vv[t] = __fmul_rn(vv[t], cp[(n + t) / ep.e]);
           }
+          if (Cfg::EPI_DENSE && c_tma) {
+            *reinterpret_cast<float4*>(dense + rr * 16 + c4) = v;
+            continue;
+          }
           float* crow = C + (size_t)z * M * ldc + (size_t)m * ldc + n;
           if (full4 && cvec) {
             *reinterpret_cast<float4*>(crow) = v;
@@ -762,8 +777,25 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
               if (n + t < N) crow[t] = vv[t];
           }
         }
+        if (Cfg::EPI_DENSE && c_tma) {
+          // generic-proxy smem writes -> visible to the TMA engine, then one
+          // bulk tensor store of the 32x16 tile (out-of-bounds rows/cols clipped)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            const int cx = n0 + half * 64 + c0, cy = z * M + m0 + q * 32;
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmC)),
+                "r"(smem_u32(dense)), "r"(cx), "r"(cy)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          ++tma_seq;
+        }
       }
     }
+    if (Cfg::EPI_DENSE && c_tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -877,6 +909,14 @@ __global__ void k_split(const float* __restrict__ x, float* __restrict__ hi, flo
 
 thread_local int g_reserve_sms = 0;
 
+bool tma_store_enabled() {  // KP_GEMM_TMA_STORE=0: per-thread global stores
+  static const bool on = [] {
+    const char* e = getenv("KP_GEMM_TMA_STORE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // CTA-pair (cta_group::2) mode for M > 128; KP_GEMM_CG=1 forces single-CTA tiles
 int choose_cg(int M) {
   static const int force = [] {
@@ -930,6 +970,26 @@ int launch_cg(int M, int N, int K, const float* A, int lda, const void* B, const
                   (!BPRE || mk(&tbl, Blo, BMN, N, ldb, Cfg::BROWS));
   if (!BPRE) tbl = tb;
   KP_CHECK(ok, kErrCuda, "cuTensorMapEncodeTiled failed");
+  // TMA-store epilogue (CTA pairs): C as a [nz*M][N] fp32 tensor, 32x16 boxes;
+  // split-K partials are stacked along rows, so it needs M % 128 == 0 there
+  int c_tma = 0;
+  CUtensorMap tc = ta;
+  {
+    int kps0 = (K + splits - 1) / splits;
+    kps0 = (kps0 + TC_BK - 1) / TC_BK * TC_BK;
+    const unsigned nz0 = ceil_div(K, kps0);
+    if (Cfg::EPI_DENSE && (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
+        (nz0 == 1 || M % TC_BM == 0) && tma_store_enabled()) {
+      auto fn = encode_fn();
+      cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M * nz0};
+      cuuint64_t strides[1] = {(cuuint64_t)ldc * 4};
+      cuuint32_t box[2] = {16, 32};
+      cuuint32_t es[2] = {1, 1};
+      c_tma = fn && fn(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+  }
   static bool attr = false;
   if (!attr) {
     KP_CUDA(cudaFuncSetAttribute(k_tc_gemm<AMN, BMN, BPRE, CG, H>,
@@ -954,8 +1014,8 @@ int launch_cg(int M, int N, int K, const float* A, int lda, const void* B, const
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  KP_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<AMN, BMN, BPRE, CG, H>, ta, tb, tbl, M, N, K, kps, C, ldc,
-                             ep));
+  KP_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<AMN, BMN, BPRE, CG, H>, ta, tb, tbl, tc, c_tma, M, N, K,
+                             kps, C, ldc, ep));
   ::kp::count_launch();
   return (int)nz;
 }
