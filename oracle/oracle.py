@@ -50,7 +50,7 @@ class TrainerCfg:
     def __init__(self, *, seed=42, n_workers=1, minibatch_size=128, sparse_lr=0.05,
                  alpha=0.01, beta1=0.0, beta2=0.999, epsilon=0.01, k=1, reset_local_v=True,
                  embedding_dim=8, n_slots=1, hidden=(16,), activation="relu", pooling="sum",
-                 sparse_rule="adagrad", sparse_beta1=0.9, sparse_beta2=0.999, sparse_eps=1e-6,
+                 sparse_rule="adagrad", sparse_beta1=0.9, sparse_beta2=0.999, sparse_eps=1e-8,
                  vocab=1 << 40):
         self.seed, self.n_workers, self.minibatch_size = seed, n_workers, minibatch_size
         self.sparse_lr, self.alpha, self.beta1, self.beta2 = sparse_lr, alpha, beta1, beta2

@@ -25,20 +25,23 @@ def _gpus():
 
 
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("k,S", [(1, 1), (3, 1), (2, 4)])
-def test_sharded_training_matches_oracle(tmp_path, k, S):
+@pytest.mark.parametrize("k,S,variant", [(1, 1, "base"), (3, 1, "base"), (2, 4, "base"),
+                                         (2, 4, "mean_adam")])
+def test_sharded_training_matches_oracle(tmp_path, k, S, variant):
+    """variant mean_adam: mean pooling, tanh, sparse Adam rows (acc_max_rel then
+    holds the max abs error of the first moment m)."""
     world = min(_gpus(), 4)
     out = tmp_path / "res.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29577", os.path.join(ROOT, "tools", "mgpu_parity.py"),
-           str(out), str(k), str(S)]
+           str(out), str(k), str(S), variant]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(out.read_text())
     assert res["owners_ok"]
     assert res["keyset_equal"]
     assert res["w_max_abs"] <= 2e-4
-    assert res["acc_max_rel"] <= 1e-3
+    assert res["acc_max_rel"] <= (1e-3 if variant == "base" else 2e-4)
     assert res["x_max_abs"] <= 2e-4
     for a, b in zip(res["loss"], res["oracle_loss"]):
         assert abs(a - b) <= 1e-4

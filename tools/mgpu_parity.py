@@ -27,12 +27,17 @@ def main():
     out_path = sys.argv[1]
     k = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     S = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+    variant = sys.argv[4] if len(sys.argv) > 4 else "base"
+    extra = (dict(pooling="mean", sparse_rule="adam", activation="tanh", sparse_eps=1e-6)
+             if variant == "mean_adam" else {})
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     cfg = dict(n_workers=world, k=k, minibatch_size=96, embedding_dim=8, n_slots=S, hidden=[16, 8],
-               alpha=0.05, beta1=0.9, beta2=0.99, sparse_lr=0.5, seed=5)
+               alpha=0.05, beta1=0.9, beta2=0.99, sparse_lr=0.5, seed=5, **extra)
+    if variant == "mean_adam":
+        cfg["sparse_lr"] = 0.05
     tr = DistributedTrainer(device=local, table_capacity=1 << 16, **cfg)
     res = {"loss": [], "auc": []}
     batches = []
@@ -51,7 +56,8 @@ def main():
     dist.all_gather_object(parts, (keys.tolist(), w.tolist(), s1.tolist(), x.tolist()))
     if rank == 0:
         ocfg = O.TrainerCfg(n_workers=world, k=k, minibatch_size=96, embedding_dim=8, n_slots=S,
-                            hidden=(16, 8), alpha=0.05, beta1=0.9, beta2=0.99, sparse_lr=0.5, seed=5)
+                            hidden=(16, 8), alpha=0.05, beta1=0.9, beta2=0.99,
+                            sparse_lr=cfg["sparse_lr"], seed=5, **extra)
         orc = O.Orc(ocfg, 64)
         oloss, oauc = [], []
         for bt in batches:
@@ -72,7 +78,9 @@ def main():
             "keyset_equal": bool(np.array_equal(allk, ok)),
             "owners_ok": bool(owners_ok),
             "w_max_abs": float(np.max(np.abs(allw - ow))) if np.array_equal(allk, ok) else None,
-            "acc_max_rel": float(np.max(np.abs(alla - oa) / oa)) if np.array_equal(allk, ok) else None,
+            "acc_max_rel": (float(np.max(np.abs(alla - oa) / oa)) if variant == "base" else
+                            float(np.max(np.abs(alla - oa)))) if np.array_equal(allk, ok) else None,
+            "variant": variant,
             "x_max_abs": float(max(np.max(np.abs(a - b)) for a, b in zip(xs, ox))),
             "loss": res["loss"], "oracle_loss": oloss,
             "auc": res["auc"], "oracle_auc": oauc,
