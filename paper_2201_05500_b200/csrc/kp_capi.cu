@@ -721,7 +721,9 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
   const bool overlap = tr->world > 1 && (reserve > 0 || peer);
   bool exchanged = false;
   std::function<void()> hook = [&] {
+    tr->mark(3);  // the backward so far is MLP time; the reduction is push time
     send_grads();
+    tr->mark(4);
     exchanged = true;
     if (peer) return;  // the reduction itself moved the data; no SMs to reserve
     if (!tr->xs) {
