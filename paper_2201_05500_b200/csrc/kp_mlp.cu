@@ -475,12 +475,30 @@ void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, c
   }
 }
 
+// column sums of the chunk partials [chunks][N]: one warp per column, lane j
+// adds chunks j, j+32, ... in order, then a fixed xor tree (deterministic)
+__global__ void k_reduce_chunks(const float* __restrict__ part, int chunks, int N,
+                                float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < N; n += (gridDim.x * blockDim.x) >> 5) {
+    float v = 0.f;
+    for (int c = lane; c < chunks; c += 32) v = __fadd_rn(v, part[(size_t)c * N + n]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) out[n] = v;
+  }
+}
+
 void colsum(const float* X, const float* w, int B, int N, float* out, MlpWs& ws, cudaStream_t s) {
   const int chunks = std::max(1, (B + COLSUM_ROWS - 1) / COLSUM_ROWS);
   float* part = ws.partials.get<float>((size_t)chunks * N);
   dim3 g(ceil_div(N, 32), chunks);
   k_colsum_part<<<g, dim3(32, 8), 0, s>>>(X, w, B, N, part); ::kp::count_launch();
-  k_reduce_splits<<<grid_cap(ceil_div(N, 256)), 256, 0, s>>>(part, chunks, (size_t)N, out); ::kp::count_launch();
+  if (chunks >= 32 && N <= 4096) {
+    k_reduce_chunks<<<grid_cap(ceil_div((uint64_t)N * 32, 256)), 256, 0, s>>>(part, chunks, N, out); ::kp::count_launch();
+  } else {
+    k_reduce_splits<<<grid_cap(ceil_div(N, 256)), 256, 0, s>>>(part, chunks, (size_t)N, out); ::kp::count_launch();
+  }
 }
 }  // namespace
 
