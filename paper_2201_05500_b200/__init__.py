@@ -4,7 +4,7 @@ Re-exports the reference module's names for the hot path
 (proj/python/kpsim/__init__.py:8-62) from the in-tree extension
 ``_kpsim_b200`` (C++ shim over the C ABI of include/kpsim_b200.h, which runs
 sm_100a kernels). There is no CPU fallback: importing fails loudly when the
-extension has not been built (``python -m paper_2201_05500_b200.build``).
+extension has not been built (``python paper_2201_05500_b200/build.py``).
 """
 from __future__ import annotations
 
@@ -39,7 +39,7 @@ try:
 except ImportError as e:  # pragma: no cover - exercised only on broken installs
     raise ImportError(
         "paper_2201_05500_b200: the CUDA extension is not built "
-        "(run `python -m paper_2201_05500_b200.build`); there is no CPU fallback"
+        "(run `python paper_2201_05500_b200/build.py`); there is no CPU fallback"
     ) from e
 
 __all__ = [
