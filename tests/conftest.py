@@ -8,6 +8,23 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def pytest_sessionstart(session):
+    """Build the in-tree extension (and the oracle checkers) when a fresh
+    checkout runs the tests before __graft_entry__.build(): the package refuses
+    to import without it. No-op when everything is up to date."""
+    import glob
+    import importlib.util
+    import subprocess
+    pkg = os.path.join(ROOT, "paper_2201_05500_b200")
+    if not (os.path.exists(os.path.join(pkg, "libkpsim_b200.so")) and glob.glob(os.path.join(pkg, "_kpsim_b200*.so"))):
+        spec = importlib.util.spec_from_file_location("_kp_build", os.path.join(pkg, "build.py"))
+        b = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(b)
+        b.build()
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "liborc64.so")):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-j8"], capture_output=True)
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the sm_100a kernels)")
     config.addinivalue_line("markers", "slow: long-running")
