@@ -436,12 +436,18 @@ __device__ __forceinline__ void store_a_row16(uint8_t* tile, int r, int k0, cons
   }
 }
 
-template <bool AMN, bool BMN, bool BPRE, int CG, bool H = false>
+// AR (A resident, fp16 only, K <= 256): a work unit is (m-block, run of
+// n-blocks); A is split into TMEM once per unit (hi at columns [256,384), lo at
+// [384,512)) and only B streams per n-block -- for dX = dZ.W1 (K = 256,
+// N = 6400) this removes re-reading the A tile 50 times through TMA/smem.
+template <bool AMN, bool BMN, bool BPRE, int CG, bool H = false, bool AR = false>
 __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmC,
               int c_tma, int M, int N, int K, int kps, float* __restrict__ C, int ldc, GemmEpi ep) {
   static_assert(!H || (!AMN && !BMN && BPRE), "fp16 mode: K-major A, pre-split K-major B");
+  static_assert(!AR || H, "A-resident mode is fp16 only");
+  constexpr uint32_t AR_COL = TC_NBUF * TC_BN;  // resident A hi; lo at +128
   // k-blocks per accumulator chunk: fp16 products are exact in fp32 and the
   // chunk error stays below the fp32 SIMT GEMM's at 8 (256 k); tf32 keeps 4
   constexpr int CH = H ? 2 * TC_CH : TC_CH;
@@ -466,7 +472,17 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   const int TM = TC_BM * CG;
   const int mblocks = (M + TM - 1) / TM, nblocks = (N + TC_BN - 1) / TC_BN;
   const int splits = (K + kps - 1) / kps;
-  const int works = mblocks * nblocks * splits;
+  // AR: n-blocks of an m-block split into nparts runs (kps carries nparts)
+  const int nparts = AR ? kps : 1;
+  const int nper = (nblocks + nparts - 1) / nparts;
+  const int works = AR ? mblocks * nparts : mblocks * nblocks * splits;
+  const int nkA = (K + TC_BK - 1) / TC_BK;  // AR: k-blocks of the resident A
+  auto ar_work = [&](int w, int& m0, int& nb_lo, int& nb_hi) {
+    const int mb = w / nparts, pt = w % nparts;
+    m0 = mb * TM + (int)rank * TC_BM;
+    nb_lo = pt * nper;
+    nb_hi = min(nblocks, nb_lo + nper);
+  };
   // work w -> (n-block fastest, then m-block, then split): units in flight share A rows
   auto decode = [&](int w, int& m0, int& n0, int& z, int& nk) {
     const int nb = w % nblocks, r = w / nblocks, mb = r % mblocks;
@@ -517,6 +533,28 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
       if (BPRE) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBlo)) : "memory");
       int g = 0;  // global k-block counter (stage pipeline)
+      if constexpr (AR) {
+        for (int w = unit; w < works; w += units) {
+          int m0, nlo, nhi;
+          ar_work(w, m0, nlo, nhi);
+          for (int kb = 0; kb < nkA; ++kb, ++g) {  // the unit's A, once
+            const int s = g % NS;
+            if (g >= NS) mbar_wait(&empty[s], ((g / NS) & 1) ^ 1);
+            mbar_expect_tx(&full[s], A_BYTES);
+            load_rows<false, TC_BM>(sA(s), &tmA, &full[s], kb * TC_BK, m0);
+          }
+          for (int nb = nlo; nb < nhi; ++nb) {  // then only B per n-block
+            const int nb0 = nb * TC_BN + (int)rank * Cfg::BROWS;
+            for (int kb = 0; kb < nkA; ++kb, ++g) {
+              const int s = g % NS;
+              if (g >= NS) mbar_wait(&empty[s], ((g / NS) & 1) ^ 1);
+              mbar_expect_tx(&full[s], 2 * Cfg::B_BYTES);
+              load_rows<false, Cfg::BROWS>(sB(s), &tmB, &full[s], kb * TC_BK, nb0);
+              load_rows<false, Cfg::BROWS>(sBlo(s), &tmBlo, &full[s], kb * TC_BK, nb0);
+            }
+          }
+        }
+      } else
       for (int w = unit; w < works; w += units) {
         int m0, n0, z, nk;
         decode(w, m0, n0, z, nk);
@@ -536,6 +574,40 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       int g = 0, c = 0;  // global k-block and chunk counters
+      if constexpr (AR) {
+        for (int w = unit; w < works; w += units) {
+          int m0, nlo, nhi;
+          ar_work(w, m0, nlo, nhi);
+          for (int kb = 0; kb < nkA; ++kb, ++g) {  // A split into TMEM: free the smem stage
+            const int s = g % NS;
+            mbar_wait_cl<CG>(&conv[s], (g / NS) & 1);
+            tc_fence_after();
+            commit_cg<CG>(&empty[s]);
+          }
+          for (int nb = nlo; nb < nhi; ++nb, ++c) {
+            const int buf = c % TC_NBUF;
+            if (c >= TC_NBUF) mbar_wait_cl<CG>(&tempty[buf], ((c / TC_NBUF) - 1) & 1);
+            const uint32_t d = tmem + (uint32_t)(buf * TC_BN);
+            for (int kb = 0; kb < nkA; ++kb, ++g) {
+              const int s = g % NS;
+              mbar_wait_cl<CG>(&conv[s], (g / NS) & 1);
+              tc_fence_after();
+              const uint32_t b = smem_u32(sB(s)), blo = smem_u32(sBlo(s));
+#pragma unroll
+              for (int kk = 0; kk < TC_BK / 16; ++kk) {
+                const uint64_t bh = sdesc_h64(b + 32u * kk), bl = sdesc_h64(blo + 32u * kk);
+                const uint32_t ah = tmem + AR_COL + 16u * kb + 8u * kk;
+                mma_h_ts<CG>(d, ah, bh, (kb | kk) != 0);
+                mma_h_ts<CG>(d, ah, bl, 1);
+                mma_h_ts<CG>(d, ah + 128u, bh, 1);
+              }
+              commit_cg<CG>(&empty[s]);
+            }
+            commit_cg<CG>(&tfull[buf]);
+          }
+          commit_cg<CG>(&afree[0]);  // the resident A may be overwritten
+        }
+      } else
       for (int w = unit; w < works; w += units) {
         int m0, n0, z, nk;
         decode(w, m0, n0, z, nk);
@@ -593,6 +665,52 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     const int r = q * 32 + lane;  // tile row == TMEM lane
     float h_scale = 1.f;          // (H) this row's 2^e
     int g = 0;
+    if constexpr (AR) {
+      int wi = 0;
+      for (int w = unit; w < works; w += units, ++wi) {
+        int m0, nlo, nhi;
+        ar_work(w, m0, nlo, nhi);
+        // the previous unit's MMAs have finished reading the resident A
+        if (wi > 0) mbar_wait(&afree[0], (wi - 1) & 1);
+        {
+          const int m = m0 + r;
+          h_scale = pow2f(m < M ? row_exp(ep.a_rowmax[m]) : 0);
+        }
+        for (int kb = 0; kb < nkA; ++kb, ++g) {
+          const int s = g % NS;
+          mbar_wait(&full[s], (g / NS) & 1);
+          float v[16];
+          load_a_row16<false>(sA(s), r, h * 16, v);
+          uint32_t hp[8], lp[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float x0 = __fmul_rn(v[2 * j], h_scale), x1 = __fmul_rn(v[2 * j + 1], h_scale);
+            const __half2 hh = __floats2half2_rn(x0, x1);
+            const float2 hf = __half22float2(hh);
+            const __half2 ll = __floats2half2_rn(__fsub_rn(x0, hf.x), __fsub_rn(x1, hf.y));
+            hp[j] = *reinterpret_cast<const uint32_t*>(&hh);
+            lp[j] = *reinterpret_cast<const uint32_t*>(&ll);
+          }
+          tc_fence_after();
+          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + AR_COL + 16u * kb + 8u * h;
+          tmem_st8(ta, hp);
+          tmem_st8(ta + 128u, lp);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          named_sync(1, 256);
+          if (ct == 0) arrive_leader<CG>(&conv[s]);
+        }
+        // B stages: forward TMA completion to the (leader's) MMA issuer
+        for (int nb = nlo; nb < nhi; ++nb)
+          for (int kb = 0; kb < nkA; ++kb, ++g) {
+            if (ct == 0) {
+              const int s = g % NS;
+              mbar_wait(&full[s], (g / NS) & 1);
+              arrive_leader<CG>(&conv[s]);
+            }
+          }
+      }
+    } else
     for (int w = unit; w < works; w += units) {
       int m0, n0, z, nk;
       decode(w, m0, n0, z, nk);
@@ -670,8 +788,15 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     uint32_t tma_seq = 0;  // TMA stores issued by this warp (dense buffer parity)
     int c = 0;
     for (int w = unit; w < works; w += units) {
-      int m0, n0, z, nk;
-      decode(w, m0, n0, z, nk);
+      int m0, n0 = 0, z = 0, nk, nlo = 0, nhi = 1;
+      if constexpr (AR) {
+        ar_work(w, m0, nlo, nhi);
+        nk = nkA;
+      } else {
+        decode(w, m0, n0, z, nk);
+      }
+      for (int nbi = nlo; nbi < nhi; ++nbi) {  // AR: the unit's n-blocks; else one tile
+      if constexpr (AR) n0 = nbi * TC_BN;
       float acc[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) acc[j] = 0.f;
@@ -793,6 +918,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           }
           ++tma_seq;
         }
+      }
       }
     }
     if (Cfg::EPI_DENSE && c_tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -928,7 +1054,7 @@ int choose_cg(int M) {
 }
 
 // concurrently resident work units (CTAs or CTA pairs)
-template <bool AMN, bool BMN, bool BPRE, int CG, bool H = false>
+template <bool AMN, bool BMN, bool BPRE, int CG, bool H = false, bool AR = false>
 int resident_units() {
   static int units = 0;
   if (units) return units;
@@ -948,14 +1074,14 @@ int resident_units() {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k_tc_gemm<AMN, BMN, BPRE, CG, H>, &cfg) == cudaSuccess && n > 0)
+    if (cudaOccupancyMaxActiveClusters(&n, k_tc_gemm<AMN, BMN, BPRE, CG, H, AR>, &cfg) == cudaSuccess && n > 0)
       units = std::min(units, n);
     cudaGetLastError();
   }
   return units;
 }
 
-template <bool AMN, bool BMN, bool BPRE, int CG, bool H = false>
+template <bool AMN, bool BMN, bool BPRE, int CG, bool H = false, bool AR = false>
 int launch_cg(int M, int N, int K, const float* A, int lda, const void* B, const void* Blo, int ldb,
               float* C, int ldc, int splits, const GemmEpi& ep, cudaStream_t s) {
   using Cfg = TcCfg<CG, H>;
@@ -992,7 +1118,7 @@ int launch_cg(int M, int N, int K, const float* A, int lda, const void* B, const
   }
   static bool attr = false;
   if (!attr) {
-    KP_CUDA(cudaFuncSetAttribute(k_tc_gemm<AMN, BMN, BPRE, CG, H>,
+    KP_CUDA(cudaFuncSetAttribute(k_tc_gemm<AMN, BMN, BPRE, CG, H, AR>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     attr = true;
   }
@@ -1000,7 +1126,7 @@ int launch_cg(int M, int N, int K, const float* A, int lda, const void* B, const
   kps = (kps + TC_BK - 1) / TC_BK * TC_BK;
   const unsigned nz = ceil_div(K, kps);
   const uint64_t works = (uint64_t)ceil_div(N, TC_BN) * ceil_div(M, TC_BM * CG) * nz;
-  const int units = std::max(1, resident_units<AMN, BMN, BPRE, CG, H>() - (g_reserve_sms + CG - 1) / CG);
+  const int units = std::max(1, resident_units<AMN, BMN, BPRE, CG, H, AR>() - (g_reserve_sms + CG - 1) / CG);
   const unsigned grid = (unsigned)std::min<uint64_t>(works, (uint64_t)units) * CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
@@ -1014,8 +1140,17 @@ int launch_cg(int M, int N, int K, const float* A, int lda, const void* B, const
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  KP_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<AMN, BMN, BPRE, CG, H>, ta, tb, tbl, tc, c_tma, M, N, K,
-                             kps, C, ldc, ep));
+  int kparam = kps;
+  uint64_t works_l = works;
+  if constexpr (AR) {
+    // runs of n-blocks per m-block: enough units for balance, A loaded per run
+    const int mb = (int)ceil_div(M, TC_BM * CG), nbl = (int)ceil_div(N, TC_BN);
+    kparam = std::max(1, std::min(nbl, (int)ceil_div((uint64_t)4 * units, (uint64_t)mb)));
+    works_l = (uint64_t)mb * kparam;
+    cfg.gridDim = dim3((unsigned)std::min<uint64_t>(works_l, (uint64_t)units) * CG, 1, 1);
+  }
+  KP_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<AMN, BMN, BPRE, CG, H, AR>, ta, tb, tbl, tc, c_tma, M, N, K,
+                             kparam, C, ldc, ep));
   ::kp::count_launch();
   return (int)nz;
 }
@@ -1090,10 +1225,18 @@ void tc_gemm_nt_h(int M, int N, int K, const float* A, int lda, const float* a_r
   GemmEpi e2 = ep;
   e2.a_rowmax = a_rowmax;
   e2.b_exp = b_exp;
-  if (choose_cg(M) == 2)
-    launch_cg<false, false, true, 2, true>(M, N, K, A, lda, Bhi, Blo, ldb, C, ldc, 1, e2, s);
-  else
-    launch_cg<false, false, true, 1, true>(M, N, K, A, lda, Bhi, Blo, ldb, C, ldc, 1, e2, s);
+  static const bool ar_on = [] {
+    const char* e = getenv("KP_GEMM_AR");
+    return !(e && e[0] == '0');
+  }();
+  const bool ar = ar_on && K <= 2 * TC_BN;  // the whole K of A fits the 256 free TMEM columns
+  if (choose_cg(M) == 2) {
+    if (ar) launch_cg<false, false, true, 2, true, true>(M, N, K, A, lda, Bhi, Blo, ldb, C, ldc, 1, e2, s);
+    else launch_cg<false, false, true, 2, true>(M, N, K, A, lda, Bhi, Blo, ldb, C, ldc, 1, e2, s);
+  } else {
+    if (ar) launch_cg<false, false, true, 1, true, true>(M, N, K, A, lda, Bhi, Blo, ldb, C, ldc, 1, e2, s);
+    else launch_cg<false, false, true, 1, true>(M, N, K, A, lda, Bhi, Blo, ldb, C, ldc, 1, e2, s);
+  }
 }
 void split_h(const float* W, int N, int K, int ld, __half* hi, __half* lo, int* exps, cudaStream_t s) {
   k_split_h<<<N, 256, 0, s>>>(W, K, ld, hi, lo, exps); ::kp::count_launch();
