@@ -216,8 +216,9 @@ struct TcCfg {
   static constexpr int STAGES = (kAloSmem && CG == 1) ? 3 : 4;
   // CG == 2: per epilogue warp two dense 32x16 fp32 tiles (TMA-store sources)
   static constexpr uint32_t EPI_DENSE = CG == 2 ? 8 * 2 * 32 * 16 * 4 : 0;
+  static constexpr uint32_t EPI_CS = H ? 8 * 64 * 4 : 0;  // (H) per-warp column scales
   static constexpr uint32_t SMEM =
-      STAGES * STAGE + EPI_BYTES + EPI_DENSE + 1024 /*align*/ + 512 /*barriers*/;
+      STAGES * STAGE + EPI_BYTES + EPI_DENSE + EPI_CS + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -465,6 +466,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + TC_NBUF);
   float* epi_smem = reinterpret_cast<float*>(smem + NS * Cfg::STAGE + 512);
   float* epi_dense = reinterpret_cast<float*>(smem + NS * Cfg::STAGE + 512 + EPI_BYTES);
+  float* epi_cs = reinterpret_cast<float*>(smem + NS * Cfg::STAGE + 512 + EPI_BYTES + Cfg::EPI_DENSE);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
@@ -827,12 +829,19 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
       const int rsub = lane >> 2, c4 = (lane & 3) * 4;
       const bool cvec = (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
       float rs[4] = {1.f, 1.f, 1.f, 1.f};  // (H) 2^-ea of this thread's 4 output rows
+      float* csw = epi_cs + (warp - 10) * 64;  // (H) 2^-eb of this warp's 64 columns
       if constexpr (H) {
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
           const int m = m0 + q * 32 + it * 8 + rsub;
           rs[it] = m < M ? pow2f(-row_exp(__ldg(ep.a_rowmax + m))) : 1.f;
         }
+        __syncwarp();
+        for (int j = lane; j < 64; j += 32) {
+          const int nn = n0 + half * 64 + j;
+          csw[j] = nn < N ? pow2f(-__ldg(ep.b_exp + nn)) : 1.f;
+        }
+        __syncwarp();
       }
 #pragma unroll
       for (int c0 = 0; c0 < 64; c0 += 16) {
@@ -851,8 +860,8 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
         }
         float cs[4] = {1.f, 1.f, 1.f, 1.f};  // (H) 2^-eb of the 4 columns
         if constexpr (H) {
-#pragma unroll
-          for (int t = 0; t < 4; ++t) cs[t] = n + t < N ? pow2f(-__ldg(ep.b_exp + n + t)) : 1.f;
+          const float4 c4v = *reinterpret_cast<const float4*>(csw + c0 + c4);
+          cs[0] = c4v.x, cs[1] = c4v.y, cs[2] = c4v.z, cs[3] = c4v.w;
         }
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
