@@ -863,6 +863,39 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           const float4 c4v = *reinterpret_cast<const float4*>(csw + c0 + c4);
           cs[0] = c4v.x, cs[1] = c4v.y, cs[2] = c4v.z, cs[3] = c4v.w;
         }
+        if (Cfg::EPI_DENSE && c_tma) {
+          // TMA-store fast path, branch-free: rows/columns outside C are
+          // clipped by the bulk store, so every lane processes its 4 rows;
+          // all shared-memory loads first, then the math, then the stores
+          float4 v4[4];
+#pragma unroll
+          for (int it = 0; it < 4; ++it) v4[it] = *reinterpret_cast<const float4*>(st + (it * 8 + rsub) * EPI_LD + c4);
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            float* vv = reinterpret_cast<float*>(&v4[it]);
+            const int m = min(m0 + q * 32 + it * 8 + rsub, M - 1);
+            const int nc = min(n, N - 4 >= 0 ? N - 4 : 0);
+            if constexpr (H) {
+#pragma unroll
+              for (int t = 0; t < 4; ++t) vv[t] = __fmul_rn(__fmul_rn(vv[t], rs[it]), cs[t]);
+            }
+            if (ep.mode == 1) {
+#pragma unroll
+              for (int t = 0; t < 4; ++t) vv[t] = act_fwd(ep.act, __fadd_rn(vv[t], ep.bias[min(n + t, N - 1)]));
+            } else if (ep.mode == 2) {
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                vv[t] = __fmul_rn(vv[t], act_bwd(ep.act, ep.aux[(size_t)m * ep.ld_aux + min(n + t, N - 1)]));
+            } else if (ep.mode == 3) {
+              const float* cp = ep.coeff + (size_t)m * ep.S;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) vv[t] = __fmul_rn(vv[t], cp[min(n + t, N - 1) / ep.e]);
+            }
+            (void)nc;
+          }
+#pragma unroll
+          for (int it = 0; it < 4; ++it) *reinterpret_cast<float4*>(dense + (it * 8 + rsub) * 16 + c4) = v4[it];
+        } else
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
           const int rr = it * 8 + rsub;
