@@ -843,6 +843,59 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
         }
         __syncwarp();
       }
+      if (Cfg::EPI_DENSE && c_tma) {
+        // TMA-store epilogue, row per lane: each lane writes its row's 16
+        // columns into a SWIZZLE_64B 32x16 smem tile (conflict-free float4
+        // stores) and one bulk tensor store moves it; no transpose. Rows and
+        // columns outside C are clipped by the store.
+        const int m = m0 + q * 32 + lane;
+        const int mc = min(m, M - 1);
+        float ra = 1.f;
+        if constexpr (H) ra = m < M ? pow2f(-row_exp(__ldg(ep.a_rowmax + m))) : 1.f;
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          uint8_t* dense = reinterpret_cast<uint8_t*>(epi_dense + ((warp - 10) * 2 + (tma_seq & 1)) * 512);
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          const int nb = n0 + half * 64 + c0;
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = acc[c0 + j];
+          if constexpr (H) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(__fmul_rn(v[j], ra), csw[c0 + j]);
+          }
+          if (ep.mode == 1) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = act_fwd(ep.act, __fadd_rn(v[j], __ldg(ep.bias + min(nb + j, N - 1))));
+          } else if (ep.mode == 2) {
+            const float* ap = ep.aux + (size_t)mc * ep.ld_aux;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], act_bwd(ep.act, __ldg(ap + min(nb + j, N - 1))));
+          } else if (ep.mode == 3) {
+            const float* cp = ep.coeff + (size_t)mc * ep.S;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], __ldg(cp + min(nb + j, N - 1) / ep.e));
+          }
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+            *reinterpret_cast<float4*>(dense + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4)) =
+                make_float4(v[4 * cc], v[4 * cc + 1], v[4 * cc + 2], v[4 * cc + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            const int cy = z * M + m0 + q * 32;
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmC)),
+                "r"(smem_u32(dense)), "r"(nb), "r"(cy)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          ++tma_seq;
+        }
+        continue;
+      }
 #pragma unroll
       for (int c0 = 0; c0 < 64; c0 += 16) {
         __syncwarp();
@@ -1154,7 +1207,7 @@ int launch_cg(int M, int N, int K, const float* A, int lda, const void* B, const
       cuuint32_t box[2] = {16, 32};
       cuuint32_t es[2] = {1, 1};
       c_tma = fn && fn(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
   }
