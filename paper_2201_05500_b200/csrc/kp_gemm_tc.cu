@@ -1290,7 +1290,7 @@ int tc_splits(int M, int N, int K) {
   const int slots = std::max(1, (cg == 2 ? resident_units<true, true, false, 2>()
                                          : resident_units<true, true, false, 1>()) -
                                      (g_reserve_sms + cg - 1) / cg);
-  const int max_sp = std::max(1, std::min(16, K / 512));
+  const int max_sp = std::max(1, std::min(64, K / 512));
   int best = 1;
   double best_eff = 0;
   for (int sp = 1; sp <= max_sp; ++sp) {

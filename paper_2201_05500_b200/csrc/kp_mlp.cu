@@ -572,7 +572,7 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
     if (l > 0) {
       float* next = ws.dz[cur ^ 1].get<float>((size_t)B * K);
       EpiArgs ep{kDAct, m.activation, nullptr, static_cast<const float*>(ws.act[l - 1].p), K, nullptr, 1, 1};
-      dx_gemm(B, K, N, dZ, d_x + m.w_off[l], next, ep, ws, s);
+      dx_gemm(B, K, N, dZ, d_x + m.w_off[l], next, ep, ws, s, true);
       cur ^= 1;
     }
   }
