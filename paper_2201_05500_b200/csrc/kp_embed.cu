@@ -421,13 +421,20 @@ __device__ __forceinline__ void sum_p(const float* P, uint64_t lo, uint64_t hi, 
   }
 }
 
-// chunk c's first position c*CH lies in segment first[c]: for every u, the
-// chunks whose start falls in [seg[u], seg[u+1])
+// chunk c's first position c*CH lies in segment first[c]: one thread per
+// chunk, binary search over the segment starts (a per-segment fill would put
+// a Zipf-hot key's thousands of chunks on one thread)
 __global__ void k_chunk_first(const uint32_t* __restrict__ seg, uint32_t U, uint32_t CH,
                               uint32_t nchunks, uint32_t* __restrict__ first) {
-  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
-    const uint32_t c0 = (seg[u] + CH - 1) / CH, c1 = min(nchunks, (seg[u + 1] + CH - 1) / CH);
-    for (uint32_t c = c0; c < c1; ++c) first[c] = u;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += gridDim.x * blockDim.x) {
+    const uint32_t p0 = c * CH;
+    uint32_t lo = 0, hi = U;  // largest u with seg[u] <= p0
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (seg[mid] <= p0) lo = mid;
+      else hi = mid;
+    }
+    first[c] = lo;
   }
 }
 
@@ -576,7 +583,7 @@ void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* 
   const uint32_t nchunks = (n_pos + a.CH - 1) / a.CH;
   a.partials = ws.partials.get<float>((size_t)nchunks * 2 * e);
   uint32_t* first = ws.first.get<uint32_t>(nchunks);
-  k_chunk_first<<<grid_cap(((uint64_t)n_unique + 255) / 256), 256, 0, s>>>(d_seg, n_unique, a.CH, nchunks, first); ::kp::count_launch();
+  k_chunk_first<<<grid_cap(((uint64_t)nchunks + 255) / 256), 256, 0, s>>>(d_seg, n_unique, a.CH, nchunks, first); ::kp::count_launch();
   a.first = first;
   a.apply = t != nullptr;
   a.peer = pm != nullptr;
