@@ -294,20 +294,28 @@ __global__ void __launch_bounds__(ST) k_dedup_emit(const KT* __restrict__ sk,
     f[r] = i < n && (i == 0 || sk[i] != sk[i - 1]);
     c += f[r];
   }
+  // the random accesses (occ_map gathers) all in flight before any store
+  uint32_t occ[IPT], mp[IPT];
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) occ[r] = base + r < n ? sv[base + r] : 0;
+  if (occ_map) {
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) mp[r] = base + r < n ? occ_map[occ[r]] : 0;
+  }
   uint32_t tot;
   uint32_t uid = bbase[blockIdx.x] + block_excl_scan(c, s_warp, tot);  // uniques before my items
+  const uint64_t kmin = sizeof(KT) == 4 ? (uint64_t)mm[0] : 0;
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     const uint32_t i = base + r;
     if (i >= n) break;
     if (f[r]) {
-      uniq[uid] = sizeof(KT) == 4 ? (uint64_t)mm[0] + sk[i] : (uint64_t)sk[i];
+      uniq[uid] = kmin + (uint64_t)sk[i];
       seg[uid] = i;
       ++uid;
     }
-    const uint32_t occ = sv[i];
-    inverse[occ] = uid - 1;
-    if (occ_map) sorted_mapped[i] = occ_map[occ];  // e.g. bag of each sorted position
+    inverse[occ[r]] = uid - 1;
+    if (occ_map) sorted_mapped[i] = mp[r];  // e.g. bag of each sorted position
   }
   if (blockIdx.x == nb - 1 && threadIdx.x == 0) {
     const uint32_t U = bbase[blockIdx.x] + tot;
