@@ -195,26 +195,28 @@ __global__ void __launch_bounds__(ST) k_downsweep(
     const KIN* __restrict__ kin, const uint32_t* __restrict__ vin, KOUT* __restrict__ kout,
     uint32_t* __restrict__ vout, uint32_t n, const unsigned long long* __restrict__ mm, int shift,
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ totals, uint32_t nb) {
+  // Warp-striped items (warp w owns tile elements [w*IPT*32, (w+1)*IPT*32),
+  // round r lane l -> w*IPT*32 + r*32 + l): element order = (warp, round,
+  // lane), so a warp-local running count per digit gives a stable rank with
+  // no block barrier per round; one scan over [digit][warp] counts (digit
+  // major) then turns (digit, warp, rank-in-warp) into the tile position.
   __shared__ KOUT s_keys[TILE];
   __shared__ uint32_t s_vals[TILE];
-  __shared__ uint32_t s_tmp[R], s_start[R], s_off[R], s_run[R];
-  __shared__ uint16_t s_wcnt[2][NW][R];
+  __shared__ uint32_t s_wh[R * NW];  // [digit][warp] counts -> exclusive tile positions
+  __shared__ uint32_t s_start[R], s_off[R];
   __shared__ uint32_t s_warp[NW];
-  const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < R; i += ST) {
-    s_tmp[i] = 0;
-    s_run[i] = 0;
-  }
-  for (int i = tid; i < 2 * NW * R; i += ST) (&s_wcnt[0][0][0])[i] = 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < R * NW; i += ST) s_wh[i] = 0;
   __syncthreads();
   const uint64_t kmin = mm[0];
   const uint32_t base = blockIdx.x * TILE;
   const uint32_t tile_n = min((uint32_t)TILE, n - base);
+  const uint32_t lt = lanemask_lt();
   KOUT k[IPT];
-  uint32_t v[IPT], d[IPT], rank[IPT];
+  uint32_t v[IPT], d[IPT], rw[IPT];
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
-    const uint32_t i = r * ST + tid;
+    const uint32_t i = (uint32_t)warp * (IPT * 32) + r * 32 + lane;
     if (i < tile_n) {
       const KIN x = kin[base + i];
       d[r] = digit_of<KIN>(x, kmin, shift, R - 1);
@@ -224,24 +226,51 @@ __global__ void __launch_bounds__(ST) k_downsweep(
     } else {
       d[r] = R;
     }
+  }
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) {
     const uint32_t peers = __match_any_sync(0xffffffffu, d[r]);
-    if (d[r] < R && lane == __ffs(peers) - 1) atomicAdd(&s_tmp[d[r]], __popc(peers));
+    const bool leader = lane == __ffs(peers) - 1;
+    uint32_t before = 0;
+    if (d[r] < R) before = s_wh[d[r] * NW + warp];
+    __syncwarp();
+    if (d[r] < R) {
+      rw[r] = before + __popc(peers & lt);
+      if (leader) s_wh[d[r] * NW + warp] = before + __popc(peers);
+    }
+    __syncwarp();
   }
   __syncthreads();
-  // digit prefix over the whole array + this block's offset within the digit
-  scan_digits<R>(s_tmp, s_start, s_warp);   // block-local digit starts
+  // exclusive scan of s_wh in (digit, warp) order: thread t owns R*NW/ST entries
+  {
+    constexpr int PER = R * NW / ST;
+    uint32_t loc[PER], sum = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      loc[j] = s_wh[tid * PER + j];
+      sum += loc[j];
+    }
+    uint32_t tot;
+    uint32_t pre = block_excl_scan(sum, s_warp, tot);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      s_wh[tid * PER + j] = pre;
+      pre += loc[j];
+    }
+  }
   __syncthreads();
-  for (int i = tid; i < R; i += ST) s_off[i] = totals[i];
+  for (int i = tid; i < R; i += ST) {
+    s_start[i] = s_wh[i * NW];  // first tile position of digit i
+    s_off[i] = totals[i];
+  }
   __syncthreads();
-  scan_digits<R>(s_off, s_off, s_warp);     // global digit starts (in place: values read first)
+  scan_digits<R>(s_off, s_off, s_warp);  // global digit starts (in place: values read first)
   __syncthreads();
   for (int i = tid; i < R; i += ST) s_off[i] += counts[i * nb + blockIdx.x] - s_start[i];
-  __syncthreads();
-  stable_rank<R>(d, rank, s_run, s_wcnt);
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     if (d[r] < R) {
-      const uint32_t p = s_start[d[r]] + rank[r];
+      const uint32_t p = s_wh[d[r] * NW + warp] + rw[r];
       s_keys[p] = k[r];
       s_vals[p] = v[r];
     }
