@@ -416,20 +416,19 @@ def main():
         # rest on tf32 (half the bf16 rate, so each tf32 MMA counts twice).
         h_on = os.environ.get("KP_GEMM_F16", "1") != "0" and D_in % 8 == 0
         f_l1 = 2.0 * B * D_in * hidden[0]                       # one first-layer GEMM
-        # fp16 path: layer-1 forward and every input-gradient GEMM (dX)
-        f_dx = sum(2.0 * B * a * b for a, b in zip(hidden, hidden[1:]))
-        f16_flops = (2 * f_l1 + f_dx) if h_on else 0.0
+        # fp16 path: layer-1 forward and layer-1 input gradient (dX)
+        f16_flops = 2 * f_l1 if h_on else 0.0
         tf32_flops = flops - f16_flops
         work = 3.0 * f16_flops + 2 * 3.0 * tf32_flops            # bf16-equivalent MMA flops
         sec = stages["mlp"]["ms_per_step"] / 1e3
         tc = work / sec / 1e12
-        roof = {"kernel": "mlp stage: tcgen05 GEMMs (layer-1 fwd + all dX: 3xFP16 scaled; dW, layer-2 "
-                          "fwd: 3xTF32) + head/bias kernels",
+        roof = {"kernel": "mlp stage: tcgen05 GEMMs (layer-1 fwd + dX: 3xFP16 scaled; dW and layer 2: "
+                          "3xTF32) + head/bias kernels",
                 "bound": "tensor", "achieved": tc, "peak": bf16s, "unit": "TFLOP/s",
                 "frac": tc / bf16s, "traffic": traffic.get("mlp"),
                 "peak_kind": f"{pk} bf16 sustained",
                 "achieved_kind": "bf16-rate-equivalent MMA work / stage time: 3 f16 MMAs per fp32 FMA "
-                                 "(layer-1 fwd, every dX), 3 tf32 MMAs = 6 bf16-equivalent otherwise",
+                                 "(layer-1 fwd, dX), 3 tf32 MMAs = 6 bf16-equivalent otherwise",
                 "fp32_model_tflops": stages["mlp"]["achieved_tflops"],
                 "mma_work_tflop_per_step": work / 1e12,
                 "cublas_tf32_tflops_8192": cublas_tf32()}

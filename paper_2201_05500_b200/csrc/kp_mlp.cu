@@ -572,7 +572,9 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
     if (l > 0) {
       float* next = ws.dz[cur ^ 1].get<float>((size_t)B * K);
       EpiArgs ep{kDAct, m.activation, nullptr, static_cast<const float*>(ws.act[l - 1].p), K, nullptr, 1, 1};
-      dx_gemm(B, K, N, dZ, d_x + m.w_off[l], next, ep, ws, s, true);
+      // hidden layers: the 3xTF32 path (measured faster than fp16 at K = 128,
+      // where the row-max/split passes and the A split per unit dominate)
+      dx_gemm(B, K, N, dZ, d_x + m.w_off[l], next, ep, ws, s, false);
       cur ^= 1;
     }
   }
