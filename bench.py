@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--vocab", type=int, default=100_000_000)
     p.add_argument("--zipf", type=float, default=1.1)
     p.add_argument("--hidden", default="256,128")
+    p.add_argument("--k", type=int, default=1, help="k-step merge period (configs C4 sweep)")
+    p.add_argument("--sparse-rule", default="adagrad", choices=["adagrad", "adam"])
     p.add_argument("--pool", type=int, default=3, help="distinct pre-generated batches")
     p.add_argument("--no-prefill", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -228,7 +230,7 @@ def workload_config(args, world):
     return {
         "workload": f"configs[{1 if world == 1 else 2}]: {args.vocab // 1_000_000}M-key table, emb dim "
                     f"{args.dim}, {args.slots} slots, batch {args.batch}/GPU, Zipf({args.zipf}) keys, "
-                    f"AdaGrad rows, k=1",
+                    f"{'AdaGrad' if args.sparse_rule == 'adagrad' else 'sparse Adam'} rows, k={args.k}",
         "global_batch": args.batch * world,
         "slots": args.slots,
         "embedding_dim": args.dim,
@@ -287,7 +289,8 @@ def main():
     capacity = per_rank_keys + 1_000_000
     tr = kp.Trainer(comm=comm, table_capacity=capacity, device=local, n_workers=world,
                     minibatch_size=args.batch, embedding_dim=args.dim, n_slots=args.slots,
-                    hidden=hidden, k=1, alpha=0.01, sparse_lr=0.05, seed=42)
+                    hidden=hidden, k=args.k, alpha=0.01, sparse_lr=0.05, seed=42,
+                    sparse_rule=args.sparse_rule)
     if not args.no_prefill:
         tr.prefill(rank, world, per_rank_keys)
 
@@ -387,7 +390,7 @@ def main():
     U = prof["unique"] / K
     O_ = prof["occurrences"] / K
     e, B, S = args.dim, args.batch, args.slots
-    R = 2  # AdaGrad {w, acc}
+    R = 2 if args.sparse_rule == "adagrad" else 3  # AdaGrad {w, acc} | Adam {w, m, v}
     D_in = S * e
     flops = 6.0 * B * (D_in * hidden[0] + sum(a * b for a, b in zip(hidden, hidden[1:] + [1])))
     stage_bytes = {

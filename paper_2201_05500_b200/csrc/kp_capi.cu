@@ -464,10 +464,22 @@ bool peer_ready(kp_trainer* tr) {
   if (P.keys.bytes < maxcol * 8) ok = win_alloc(tr, P.keys, room(maxcol, 8)) && ok;
   if (P.grads.bytes < maxcol * row) ok = win_alloc(tr, P.grads, room(maxcol, row)) && ok;
   if (P.rows.bytes < maxrow * row) ok = win_alloc(tr, P.rows, room(maxrow, row)) && ok;
-  if (P.mode == -1 || !ok) {
+  const bool first = P.mode == -1;
+  if (first) {
+    // the k-step merge's windows too, now: a one-time collective setup must
+    // not land in the middle of a run (the first merge may be k steps away)
+    const uint64_t D = tr->D;
+    const uint32_t W = tr->W;
+    ok = win_alloc(tr, P.dv, (size_t)W * D * 4, tr->v) && ok;
+    ok = win_alloc(tr, P.dx, (size_t)W * D * 4, tr->x) && ok;
+    ok = win_alloc(tr, P.terms, (size_t)W * D * 4) && ok;
+    ok = win_alloc(tr, P.vb, (size_t)D * 4) && ok;
+  }
+  if (first || !ok) {
     P.mode = all_ok(tr, ok) ? 1 : 0;
     if (P.mode == 0)
-      for (auto* w : {&P.keys, &P.rows, &P.grads, &P.flags}) win_release(tr, *w);
+      for (auto* w : {&P.keys, &P.rows, &P.grads, &P.flags, &P.dv, &P.dx, &P.terms, &P.vb})
+        win_release(tr, *w);
   }
   return P.mode == 1;
 }
@@ -520,13 +532,7 @@ void merge_states_peer(kp_trainer* tr, float alpha, bool reset) {
   const uint32_t W = tr->W;
   const uint64_t D = tr->D;
   cudaStream_t s = tr->s;
-  if (!P.dv.local) {
-    bool ok = win_alloc(tr, P.dv, (size_t)W * D * 4, tr->v);
-    ok = win_alloc(tr, P.dx, (size_t)W * D * 4, tr->x) && ok;
-    ok = win_alloc(tr, P.terms, (size_t)W * D * 4) && ok;
-    ok = win_alloc(tr, P.vb, (size_t)D * 4) && ok;
-    KP_CHECK(all_ok(tr, ok), kErrCuda, "peer merge: IPC mapping of the dense state failed");
-  }
+  KP_CHECK(P.dv.local != nullptr, kErrCuda, "peer merge: dense-state windows not mapped");
   const uint64_t C = (D + R - 1) / R;
   const uint64_t c0 = std::min<uint64_t>(D, (uint64_t)me * C), c1 = std::min<uint64_t>(D, c0 + C);
   PeerVecs pv{};
