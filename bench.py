@@ -443,6 +443,20 @@ def main():
         if k in traffic:
             stages[k]["ncu_dram_bytes"] = traffic[k]
     emb = {k: stages[k] for k in ("pool", "push") if "achieved_gbs" in stages[k]}
+    for v in emb.values():  # fraction of the nominal ~8 TB/s too
+        v["frac_nominal_8tbs"] = v["achieved_gbs"] / 8000.0
+    nvlink = None
+    if world > 1:
+        # per GPU per step: keys to owners, rows back, gradients to owners, for
+        # the (G-1)/G of the exchanged entries that cross NVLink (counts from
+        # the run); floor = those bytes at 900 GB/s per direction
+        recv = prof.get("received", 0) / K
+        remote = recv * (world - 1) / world
+        b = remote * (8 + 4 * e + 4 * e)
+        nvlink = {"bytes_per_gpu_per_step": b, "floor_ms_at_900_GBs": b / 900e9 * 1e3,
+                  "exchange_stage_ms": stages["exchange"]["ms_per_step"],
+                  "note": "rows and gradients move inside the pull/push kernels and the "
+                          "copy engines, overlapped; the stages above include them"}
 
     if rank == 0:
         cpu = None
@@ -459,7 +473,7 @@ def main():
             "data": "synthetic Zipf CTR batches (random-init dense weights)",
             "config": workload_config(args, world),
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "stages": stages,
-            "embedding_pull_push": emb, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "embedding_pull_push": emb, "nvlink": nvlink, "cpu_baseline": cpu, "clocks": clk.summary(),
             "loss": loss, "unique_keys_per_step": U, "occurrences_per_step": O_,
             "wall_ms_per_step": wall / args.steps * 1e3,
         }
