@@ -905,50 +905,11 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
               make_float4(acc[c0 + j], acc[c0 + j + 1], acc[c0 + j + 2], acc[c0 + j + 3]);
         __syncwarp();
         const int n = n0 + half * 64 + c0 + c4;
-        // dense 32x16 tile for the TMA store (double-buffered per warp)
-        float* dense = epi_dense + ((warp - 10) * 2 + (tma_seq & 1)) * (32 * 16);
-        if (Cfg::EPI_DENSE && c_tma) {
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          __syncwarp();
-        }
         float cs[4] = {1.f, 1.f, 1.f, 1.f};  // (H) 2^-eb of the 4 columns
         if constexpr (H) {
           const float4 c4v = *reinterpret_cast<const float4*>(csw + c0 + c4);
           cs[0] = c4v.x, cs[1] = c4v.y, cs[2] = c4v.z, cs[3] = c4v.w;
         }
-        if (Cfg::EPI_DENSE && c_tma) {
-          // TMA-store fast path, branch-free: rows/columns outside C are
-          // clipped by the bulk store, so every lane processes its 4 rows;
-          // all shared-memory loads first, then the math, then the stores
-          float4 v4[4];
-#pragma unroll
-          for (int it = 0; it < 4; ++it) v4[it] = *reinterpret_cast<const float4*>(st + (it * 8 + rsub) * EPI_LD + c4);
-#pragma unroll
-          for (int it = 0; it < 4; ++it) {
-            float* vv = reinterpret_cast<float*>(&v4[it]);
-            const int m = min(m0 + q * 32 + it * 8 + rsub, M - 1);
-            const int nc = min(n, N - 4 >= 0 ? N - 4 : 0);
-            if constexpr (H) {
-#pragma unroll
-              for (int t = 0; t < 4; ++t) vv[t] = __fmul_rn(__fmul_rn(vv[t], rs[it]), cs[t]);
-            }
-            if (ep.mode == 1) {
-#pragma unroll
-              for (int t = 0; t < 4; ++t) vv[t] = act_fwd(ep.act, __fadd_rn(vv[t], ep.bias[min(n + t, N - 1)]));
-            } else if (ep.mode == 2) {
-#pragma unroll
-              for (int t = 0; t < 4; ++t)
-                vv[t] = __fmul_rn(vv[t], act_bwd(ep.act, ep.aux[(size_t)m * ep.ld_aux + min(n + t, N - 1)]));
-            } else if (ep.mode == 3) {
-              const float* cp = ep.coeff + (size_t)m * ep.S;
-#pragma unroll
-              for (int t = 0; t < 4; ++t) vv[t] = __fmul_rn(vv[t], cp[min(n + t, N - 1) / ep.e]);
-            }
-            (void)nc;
-          }
-#pragma unroll
-          for (int it = 0; it < 4; ++it) *reinterpret_cast<float4*>(dense + (it * 8 + rsub) * 16 + c4) = v4[it];
-        } else
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
           const int rr = it * 8 + rsub;
@@ -984,10 +945,6 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
             for (int t = 0; t < 4; ++t)
               if (n + t < N) vv[t] = __fmul_rn(vv[t], cp[(n + t) / ep.e]);
           }
-          if (Cfg::EPI_DENSE && c_tma) {
-            *reinterpret_cast<float4*>(dense + rr * 16 + c4) = v;
-            continue;
-          }
           float* crow = C + (size_t)z * M * ldc + (size_t)m * ldc + n;
           if (full4 && cvec) {
             *reinterpret_cast<float4*>(crow) = v;
@@ -996,22 +953,6 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
             for (int t = 0; t < 4; ++t)
               if (n + t < N) crow[t] = vv[t];
           }
-        }
-        if (Cfg::EPI_DENSE && c_tma) {
-          // generic-proxy smem writes -> visible to the TMA engine, then one
-          // bulk tensor store of the 32x16 tile (out-of-bounds rows/cols clipped)
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) {
-            const int cx = n0 + half * 64 + c0, cy = z * M + m0 + q * 32;
-            asm volatile(
-                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                    reinterpret_cast<uint64_t>(&tmC)),
-                "r"(smem_u32(dense)), "r"(cx), "r"(cy)
-                : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          }
-          ++tma_seq;
         }
       }
       }
