@@ -25,17 +25,20 @@ def _gpus():
 
 
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("k,S,variant", [(1, 1, "base"), (3, 1, "base"), (2, 4, "base"),
-                                         (2, 4, "mean_adam")])
-def test_sharded_training_matches_oracle(tmp_path, k, S, variant):
+@pytest.mark.parametrize("k,S,variant,peer", [(1, 1, "base", "1"), (3, 1, "base", "1"),
+                                              (2, 4, "base", "1"), (2, 4, "mean_adam", "1"),
+                                              (3, 4, "base", "0")])
+def test_sharded_training_matches_oracle(tmp_path, k, S, variant, peer):
     """variant mean_adam: mean pooling, tanh, sparse Adam rows (acc_max_rel then
-    holds the max abs error of the first moment m)."""
+    holds the max abs error of the first moment m). peer "0": the exchange and
+    merge run over NCCL instead of the NVLink peer windows."""
     world = min(_gpus(), 4)
     out = tmp_path / "res.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29577", os.path.join(ROOT, "tools", "mgpu_parity.py"),
            str(out), str(k), str(S), variant]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = dict(os.environ, KP_PEER=peer)  # "0": the NCCL all-to-all / allgather path
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(out.read_text())
     assert res["owners_ok"]
