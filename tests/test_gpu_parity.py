@@ -265,6 +265,36 @@ def test_trainer_slots_and_sparse_adam_vs_oracle(kp, S, pool, rule):
         assert close(tr.worker_state(i)["x"], o64.worker_state(i)["x"])
 
 
+@pytest.mark.parametrize("S,e,pool,rule,multi", [(12, 16, "sum", "adagrad", False),
+                                                 (10, 128, "mean", "adam", True),
+                                                 (16, 64, "sum", "adagrad", False),
+                                                 (9, 4, "mean", "adagrad", True)])
+def test_trainer_pooling_paths_vs_oracle(kp, S, e, pool, rule, multi):
+    """Instance-major pooling (S >= 8, e <= 64: one warp per instance, row
+    maxima without atomics) and the atomic row-max path (e = 128 / multi-hot),
+    feeding the fp16 first layer: state vs the f64 oracle."""
+    cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=256, embedding_dim=e, n_slots=S,
+                       hidden=(32, 16), pooling=pool, activation="relu", alpha=0.02, sparse_lr=0.1,
+                       sparse_rule=rule, sparse_beta1=0.9, sparse_beta2=0.99, sparse_eps=1e-6)
+    o64 = O.Orc(cfg, 64)
+    tr = kp.Trainer(table_capacity=1 << 16, **trainer_kwargs(vars(cfg)))
+    for b in range(3):
+        bt = make_batch(256, V=5000, zipf_s=1.1, n_slots=S, seed=10 + b)
+        keys, slots, offs = bt.keys, bt.slots, bt.offs
+        if multi:
+            keys = np.repeat(bt.keys, 2)
+            slots = np.repeat(bt.slots, 2)
+            offs = (bt.offs.astype(np.int64) * 2).astype(np.uint32)
+        ro = o64.batch(offs, keys, bt.labels, slots=slots, predict_first=True)
+        rg = tr.train_batch(offs, keys, bt.labels, slots=slots, predict_first=True)
+        assert abs(ro["loss"] - rg["loss"]) <= TOL_LOSS
+    k64, w64, a64, _ = o64.table()
+    kg, wg, s1, _ = tr.table()
+    assert np.array_equal(k64, kg)
+    assert close(wg, w64)
+    assert close(tr.worker_state(0)["x"], o64.worker_state(0)["x"])
+
+
 def test_trainer_deterministic(kp):
     def run():
         tr = kp.Trainer(table_capacity=1 << 18, n_workers=1, k=1, minibatch_size=4096,
