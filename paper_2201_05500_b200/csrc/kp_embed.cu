@@ -408,12 +408,13 @@ __global__ void __launch_bounds__(256) k_seg_blocksum(SegArgs a, uint32_t nP, fl
 template <int LPG, int NV, bool V4>
 __device__ __forceinline__ void sum_p(const float* P, uint64_t lo, uint64_t hi, uint32_t e,
                                       Row<LPG, NV, V4>& acc, int gl) {
-  Row<LPG, NV, V4> r[4];
-  for (; lo + 4 <= hi; lo += 4) {
+  constexpr int UR = V4 ? 8 : 4;  // partial rows in flight (latency-bound tail of hot keys)
+  Row<LPG, NV, V4> r[UR];
+  for (; lo + UR <= hi; lo += UR) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) r[u].load(P + (lo + u) * e, gl, e);
+    for (int u = 0; u < UR; ++u) r[u].load(P + (lo + u) * e, gl, e);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc.add(r[u]);
+    for (int u = 0; u < UR; ++u) acc.add(r[u]);
   }
   for (; lo < hi; ++lo) {
     r[0].load(P + lo * e, gl, e);
