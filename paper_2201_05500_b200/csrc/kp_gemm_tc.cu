@@ -205,15 +205,19 @@ constexpr uint32_t TC_ACOL = TC_NBUF * TC_BN;  // first A-operand column
 // H: fp16 operands (kind::f16, 2x the tf32 rate) -- A split on chip into
 // fp16 hi/lo with a per-row power-of-two scale, B pre-split fp16 hi/lo (64-byte
 // K-major rows, SWIZZLE_64B) with per-row scales; see k_tc_gemm.
-template <int CG, bool H = false>
+template <int CG, bool H = false, bool AR = false>
 struct TcCfg {
   static constexpr int BROWS = TC_BN / CG;  // B rows held by one CTA
   static constexpr uint32_t B_BYTES = BROWS * TC_BK * (H ? 2 : 4);
-  // A fp32, B (hi), B lo, and (kAloSmem) the A lo tile
-  static constexpr uint32_t STAGE = A_BYTES + 2 * B_BYTES + (kAloSmem ? A_BYTES : 0);
+  // A fp32, B (hi), B lo, and (kAloSmem) the A lo tile. AR: a stage holds
+  // EITHER an A tile (unit start) or a B hi/lo pair, so stages are small and
+  // the ring deep -- B streams from L2 with nothing else to hide its latency
+  static constexpr uint32_t STAGE =
+      AR ? (A_BYTES > 2 * B_BYTES ? A_BYTES : 2 * B_BYTES)
+         : A_BYTES + 2 * B_BYTES + (kAloSmem ? A_BYTES : 0);
   // smem ring depth (a deeper ring, 6 stages at CG = 2 with separate TMEM A
-  // slot barriers, measured no faster)
-  static constexpr int STAGES = (kAloSmem && CG == 1) ? 3 : 4;
+  // slot barriers, measured no faster in the streaming-A modes)
+  static constexpr int STAGES = AR ? 8 : (kAloSmem && CG == 1) ? 3 : 4;
   // CG == 2: per epilogue warp two dense 32x16 fp32 tiles (TMA-store sources)
   static constexpr uint32_t EPI_DENSE = CG == 2 ? 8 * 2 * 32 * 16 * 4 : 0;
   static constexpr uint32_t EPI_CS = H ? 8 * 64 * 4 : 0;  // (H) per-warp column scales
@@ -452,7 +456,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
   // k-blocks per accumulator chunk: fp16 products are exact in fp32 and the
   // chunk error stays below the fp32 SIMT GEMM's at 8 (256 k); tf32 keeps 4
   constexpr int CH = H ? 2 * TC_CH : TC_CH;
-  using Cfg = TcCfg<CG, H>;
+  using Cfg = TcCfg<CG, H, AR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int NS = Cfg::STAGES;
@@ -495,8 +499,8 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
     nk = kend > kbeg ? (kend - kbeg + TC_BK - 1) / TC_BK : 0;
   };
   auto sA = [&](int s) { return smem + s * Cfg::STAGE; };
-  auto sB = [&](int s) { return smem + s * Cfg::STAGE + A_BYTES; };
-  auto sBlo = [&](int s) { return smem + s * Cfg::STAGE + A_BYTES + Cfg::B_BYTES; };
+  auto sB = [&](int s) { return smem + s * Cfg::STAGE + (AR ? 0 : A_BYTES); };
+  auto sBlo = [&](int s) { return smem + s * Cfg::STAGE + (AR ? 0 : A_BYTES) + Cfg::B_BYTES; };
   auto sAlo = [&](int s) { return smem + s * Cfg::STAGE + A_BYTES + 2 * Cfg::B_BYTES; };
 
   if (threadIdx.x == 0) {
@@ -1101,7 +1105,7 @@ int resident_units() {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * CG, 1, 1);
     cfg.blockDim = dim3(TC_WARPS * 32, 1, 1);
-    cfg.dynamicSmemBytes = TcCfg<CG, H>::SMEM;
+    cfg.dynamicSmemBytes = TcCfg<CG, H, AR>::SMEM;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CG;
@@ -1120,7 +1124,7 @@ int resident_units() {
 template <bool AMN, bool BMN, bool BPRE, int CG, bool H = false, bool AR = false>
 int launch_cg(int M, int N, int K, const float* A, int lda, const void* B, const void* Blo, int ldb,
               float* C, int ldc, int splits, const GemmEpi& ep, cudaStream_t s) {
-  using Cfg = TcCfg<CG, H>;
+  using Cfg = TcCfg<CG, H, AR>;
   CUtensorMap ta, tb, tbl;
   // K-major: [rows][K] with box_rows-row boxes; MN-major: [K][rows] with 32x32 boxes
   auto mk = [&](CUtensorMap* m, const void* p, bool mn, int rows, int ld, int box_rows) {
