@@ -217,7 +217,10 @@ struct TcCfg {
          : A_BYTES + 2 * B_BYTES + (kAloSmem ? A_BYTES : 0);
   // smem ring depth (a deeper ring, 6 stages at CG = 2 with separate TMEM A
   // slot barriers, measured no faster in the streaming-A modes)
-  static constexpr int STAGES = AR ? 8 : (kAloSmem && CG == 1) ? 3 : 4;
+  static constexpr int STAGES = AR ? 8 : H ? 6 : (kAloSmem && CG == 1) ? 3 : 4;
+  // fp16 A slot in TMEM = 32 columns (hi 16 + lo 16): the 256 free columns hold
+  // 8 slots, >= STAGES, so a slot is free whenever its smem stage is refilled
+  static constexpr uint32_t ASLOT_COLS = H ? 32 : 64;
   // CG == 2: per epilogue warp two dense 32x16 fp32 tiles (TMA-store sources)
   static constexpr uint32_t EPI_DENSE = CG == 2 ? 8 * 2 * 32 * 16 * 4 : 0;
   static constexpr uint32_t EPI_CS = H ? 8 * 64 * 4 : 0;  // (H) per-warp column scales
@@ -625,7 +628,9 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           mbar_wait_cl<CG>(&conv[s], ph);
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(buf * TC_BN);
-          const uint32_t ahi = tmem + TC_ACOL + 64u * (uint32_t)(g % TC_ASLOTS), alo = ahi + 32u;
+          const uint32_t ahi = tmem + TC_ACOL +
+                               Cfg::ASLOT_COLS * (uint32_t)(H ? g % NS : g % TC_ASLOTS),
+                         alo = ahi + 32u;
           const uint32_t b = smem_u32(sB(s)), blo = smem_u32(sBlo(s));
           const uint32_t asm_ = smem_u32(sA(s));
           if constexpr (H) {
@@ -656,7 +661,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
           }
           }
           commit_cg<CG>(&empty[s]);
-          if (NS > TC_ASLOTS) commit_cg<CG>(&afree[g % TC_ASLOTS]);
+          if (!H && NS > TC_ASLOTS) commit_cg<CG>(&afree[g % TC_ASLOTS]);
           if (kin == CH - 1 || kb == nk - 1) {
             commit_cg<CG>(&tfull[buf]);
             ++c;
@@ -743,9 +748,9 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
             hp[j] = *reinterpret_cast<const uint32_t*>(&hh);
             lp[j] = *reinterpret_cast<const uint32_t*>(&ll);
           }
-          const int as = g % TC_ASLOTS;
+          const int as = g % NS;  // (fp16: 8 slots >= NS, see TcCfg)
           tc_fence_after();
-          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + 64u * (uint32_t)as + 8u * h;
+          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + Cfg::ASLOT_COLS * (uint32_t)as + 8u * h;
           tmem_st8(ta, hp);
           tmem_st8(ta + 16u, lp);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
