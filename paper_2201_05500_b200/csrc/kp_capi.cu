@@ -1273,10 +1273,22 @@ int kp_table_export(kp_table* t, uint64_t* keys, float* w, float* s1, float* s2,
 }
 
 // ---- dedup / shard ----
+// Workspaces of the stand-alone entry points live on the device they were
+// first used on, so keep one per (thread, device).
+extern "C++" {
+template <class W>
+W& dev_ws() {
+  static thread_local W ws[16];
+  int dev = 0;
+  KP_CUDA(cudaGetDevice(&dev));
+  KP_CHECK(dev >= 0 && dev < 16, kErrConfig, "device ordinal out of range");
+  return ws[dev];
+}
+}
 int kp_dedup(const uint64_t* d_keys, uint32_t n, uint64_t* d_unique, uint32_t* d_inverse,
              uint32_t* d_seg, uint32_t* n_unique, kp_stream s) {
   return guard([&] {
-    static thread_local DedupWs ws;
+    DedupWs& ws = dev_ws<DedupWs>();
     dedup(d_keys, n, ws, st(s));
     const uint32_t U = ws.n_unique;
     *n_unique = U;
@@ -1293,7 +1305,7 @@ int kp_dedup_runs(const uint64_t* d_keys, uint32_t n, const uint64_t* run_off, u
   return guard([&] {
     KP_CHECK(n_runs >= 1 && run_off && run_off[0] == 0 && run_off[n_runs] == n, kErrConfig,
              "dedup_runs: run offsets must start at 0 and end at n");
-    static thread_local DedupWs ws;
+    DedupWs& ws = dev_ws<DedupWs>();
     std::vector<uint64_t> ro(run_off, run_off + n_runs + 1);
     dedup_runs(d_keys, n, ro, ws, st(s));
     const uint32_t U = ws.n_unique;
@@ -1310,7 +1322,7 @@ int kp_dedup_runs(const uint64_t* d_keys, uint32_t n, const uint64_t* run_off, u
 int kp_shard(const uint64_t* d_unique, uint32_t n, uint32_t G, uint32_t* d_perm, uint32_t* d_pos,
              uint64_t* counts, kp_stream s) {
   return guard([&] {
-    static thread_local ShardWs ws;
+    ShardWs& ws = dev_ws<ShardWs>();
     shard(d_unique, n, G, d_perm, d_pos, counts, ws, st(s));
   });
 }
@@ -1335,7 +1347,7 @@ int kp_kstep_merge(kp_comm* comm, float* d_x, float* d_m, float* d_v, float* d_v
                    uint64_t D, float alpha, int reset_local_v, kp_stream s) {
   return guard([&] {
     KP_CHECK(W >= 1, kErrGeneric, "global_merge: empty worker list");
-    static thread_local MergeWs ws;
+    MergeWs& ws = dev_ws<MergeWs>();
     merge_states(comm, st(s), W, D, d_x, d_m, d_v, d_vbar, alpha, reset_local_v != 0, ws);
     KP_CUDA(cudaStreamSynchronize(st(s)));
   });
@@ -1345,7 +1357,7 @@ int kp_kstep_merge(kp_comm* comm, float* d_x, float* d_m, float* d_v, float* d_v
 int kp_compute_auc(const float* d_scores, const int32_t* d_labels, uint32_t n, double* auc,
                    kp_stream s) {
   return guard([&] {
-    static thread_local AucWs ws;
+    AucWs& ws = dev_ws<AucWs>();
     *auc = device_auc(d_scores, d_labels, n, ws, st(s));
   });
 }
@@ -1362,7 +1374,11 @@ int kp_gemm_nt(const float* d_A, int lda, const float* d_B, int ldb, float* d_C,
       simt_gemm_nt(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, st(s));
     } else if (engine == 3) {
       // fp16-operand path (per-row scaled 3xFP16), as used for the first MLP layer
-      static thread_local DevBuf amax, bhi, blo, bexp;
+      struct HWs {
+        DevBuf amax, bhi, blo, bexp;
+      };
+      HWs& hw = dev_ws<HWs>();
+      DevBuf &amax = hw.amax, &bhi = hw.bhi, &blo = hw.blo, &bexp = hw.bexp;
       float* am = amax.get<float>(M);
       rowmax(d_A, M, K, lda, am, st(s));
       __half* h = reinterpret_cast<__half*>(bhi.get<uint16_t>((size_t)N * ldb));
@@ -1393,7 +1409,7 @@ int kp_gemm_tn(const float* d_A, int lda, const float* d_B, int ldb, float* d_C,
       if (sp == 1) {
         tc_gemm_tn(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, 1, st(s));
       } else {
-        static thread_local DevBuf part;
+        DevBuf& part = dev_ws<DevBuf>();
         float* p = part.get<float>((size_t)sp * M * ldc);
         const int got = tc_gemm_tn(M, N, K, d_A, lda, d_B, ldb, p, ldc, sp, st(s));
         reduce_splits(p, got, (size_t)M * ldc, d_C, st(s));

@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -808,6 +809,17 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
       }
       for (int nbi = nlo; nbi < nhi; ++nbi) {  // AR: the unit's n-blocks; else one tile
       if constexpr (AR) n0 = nbi * TC_BN;
+      if (ep.mode == 2) {
+        // activation-derivative operand: pull this lane's 64-column row
+        // segment into L2 while the tile's MMAs run, so the epilogue's
+        // loads do not pay an HBM round trip per 16-column group
+        const int m = min(m0 + q * 32 + lane, M - 1);
+        const int nb = min(n0 + half * 64, N - 1);
+        const char* a0 = reinterpret_cast<const char*>(ep.aux + (size_t)m * ep.ld_aux + nb);
+        const char* a1 = reinterpret_cast<const char*>(ep.aux + (size_t)m * ep.ld_aux + min(nb + 63, N - 1));
+        for (const char* pp = a0; pp <= a1; pp += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(pp));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a1));
+      }
       float acc[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) acc[j] = 0.f;
@@ -879,8 +891,16 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1)
             for (int j = 0; j < 16; ++j) v[j] = act_fwd(ep.act, __fadd_rn(v[j], __ldg(ep.bias + min(nb + j, N - 1))));
           } else if (ep.mode == 2) {
             const float* ap = ep.aux + (size_t)mc * ep.ld_aux;
+            if (nb + 16 <= N && ((reinterpret_cast<uintptr_t>(ap + nb) & 15) == 0)) {
+              float a[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], act_bwd(ep.act, __ldg(ap + min(nb + j, N - 1))));
+              for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(a + j) = __ldg(reinterpret_cast<const float4*>(ap + nb + j));
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], act_bwd(ep.act, a[j]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], act_bwd(ep.act, __ldg(ap + min(nb + j, N - 1))));
+            }
           } else if (ep.mode == 3) {
             const float* cp = ep.coeff + (size_t)mc * ep.S;
 #pragma unroll
@@ -1104,7 +1124,9 @@ int resident_units() {
   static int units = 0;
   if (units) return units;
   int sms = 0;
-  KP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  int dev = 0;
+  KP_CUDA(cudaGetDevice(&dev));
+  KP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   units = sms / CG;
   if (CG > 1) {
     cudaLaunchConfig_t cfg = {};
@@ -1161,11 +1183,15 @@ int launch_cg(int M, int N, int K, const float* A, int lda, const void* B, const
                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
   }
-  static bool attr = false;
-  if (!attr) {
+  // the smem opt-in is per device: one bit per device this instantiation ran on
+  static std::atomic<uint64_t> attr{0};
+  int dev = 0;
+  KP_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr.load(std::memory_order_acquire) & bit)) {
     KP_CUDA(cudaFuncSetAttribute(k_tc_gemm<AMN, BMN, BPRE, CG, H, AR>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    attr = true;
+    attr.fetch_or(bit, std::memory_order_release);
   }
   int kps = (K + splits - 1) / splits;
   kps = (kps + TC_BK - 1) / TC_BK * TC_BK;
