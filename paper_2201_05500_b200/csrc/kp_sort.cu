@@ -10,7 +10,7 @@
 //  * only the bits where keys differ are sorted: digits of (key - min), so a
 //    100M key space costs 4 passes of 8 bits, not 8;
 //  * per pass: upsweep histogram (warp-aggregated smem atomics), per-digit
-//    scan, downsweep with a stable block rank (__match_any_sync) and a
+//    scan, downsweep with a stable block rank (ballot digit match) and a
 //    shared-memory staged scatter so global writes are digit-run coalesced;
 //  * tiles of 2048 pairs (256 threads x 8), grids are multiples of the SM
 //    count for every config that matters.
@@ -89,6 +89,22 @@ __device__ __forceinline__ uint32_t digit_of(KIN k, uint64_t kmin, int shift, ui
   else return (uint32_t)((k - kmin) >> shift) & mask;
 }
 
+// lanes holding the same digit d in [0, R] (R = invalid): one ballot per
+// digit bit instead of MATCH.ANY (which issues through the MIO queue and
+// dominated the rank loop's stalls)
+template <int R>
+__device__ __forceinline__ uint32_t match_digit(uint32_t d) {
+  constexpr int BITS = (R == 256 ? 8 : R == 512 ? 9 : 16) + 1;
+  uint32_t peers = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const bool on = (d >> b) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, on);
+    peers &= on ? bal : ~bal;
+  }
+  return peers;
+}
+
 template <typename KIN, int R>
 __global__ void __launch_bounds__(ST) k_upsweep(const KIN* __restrict__ keys, uint32_t n,
                                                 const unsigned long long* __restrict__ mm,
@@ -104,7 +120,7 @@ __global__ void __launch_bounds__(ST) k_upsweep(const KIN* __restrict__ keys, ui
   for (int r = 0; r < IPT; ++r) {
     const uint32_t idx = base + r * ST + threadIdx.x;
     const uint32_t d = idx < n ? digit_of<KIN>(keys[idx], kmin, shift, R - 1) : R;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t peers = match_digit<R>(d);
     if (d < R && lane == __ffs(peers) - 1) atomicAdd(&hist[d], __popc(peers));
   }
   __syncthreads();
@@ -229,7 +245,7 @@ __global__ void __launch_bounds__(ST) k_downsweep(
   }
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
-    const uint32_t peers = __match_any_sync(0xffffffffu, d[r]);
+    const uint32_t peers = match_digit<R>(d[r]);
     const bool leader = lane == __ffs(peers) - 1;
     uint32_t before = 0;
     if (d[r] < R) before = s_wh[d[r] * NW + warp];
