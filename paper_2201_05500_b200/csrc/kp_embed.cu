@@ -384,11 +384,13 @@ __global__ void __launch_bounds__(256, 6) k_seg_chunks(SegArgs a, TView t) {
 // Phase 2: a segment spanning chunks c0 < c1 owns the contiguous flattened
 // partial range P[2c0+1 .. 2c1] (tail of c0, then head of each later chunk;
 // the unused tail slots in between hold 0). Short ranges are summed in order;
-// long ones (Zipf-hot keys) as loose head + 64-entry block sums Q + loose tail.
+// long ones (Zipf-hot keys) as loose head + 64-entry block sums Q + loose tail,
+// the hottest (more than 128 Q blocks) with a second level Q2 of 64-Q sums.
 constexpr uint32_t QB = 64;
 
 template <int LPG, int NV, bool V4>
-__global__ void __launch_bounds__(256) k_seg_blocksum(SegArgs a, uint32_t nP, float* __restrict__ Q) {
+__global__ void __launch_bounds__(256) k_seg_blocksum(const float* __restrict__ src, uint32_t nP, uint32_t e,
+                                                      float* __restrict__ Q) {
   const int gl = threadIdx.x % LPG;
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
   const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
@@ -397,18 +399,18 @@ __global__ void __launch_bounds__(256) k_seg_blocksum(SegArgs a, uint32_t nP, fl
     acc.zero();
     for (uint32_t i = 0; i < QB; i += 4) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) r[u].load(a.partials + (j * QB + i + u) * a.e, gl, a.e);
+      for (int u = 0; u < 4; ++u) r[u].load(src + (j * QB + i + u) * e, gl, e);
 #pragma unroll
       for (int u = 0; u < 4; ++u) acc.add(r[u]);
     }
-    acc.store(Q + j * a.e, gl, a.e);
+    acc.store(Q + j * e, gl, e);
   }
 }
 
 template <int LPG, int NV, bool V4>
 __device__ __forceinline__ void sum_p(const float* P, uint64_t lo, uint64_t hi, uint32_t e,
                                       Row<LPG, NV, V4>& acc, int gl) {
-  constexpr int UR = V4 ? 8 : 4;  // partial rows in flight (latency-bound tail of hot keys)
+  constexpr int UR = V4 ? 16 : 4;  // partial rows in flight (latency-bound tail of hot keys)
   Row<LPG, NV, V4> r[UR];
   for (; lo + UR <= hi; lo += UR) {
 #pragma unroll
@@ -442,7 +444,8 @@ __global__ void k_chunk_first(const uint32_t* __restrict__ seg, uint32_t U, uint
 // Segments crossing a chunk boundary: each is handled once, at the first
 // boundary it crosses (c = its start chunk + 1), found through first[c].
 template <int LPG, int NV, bool V4>
-__global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t, const float* __restrict__ Q) {
+__global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t, const float* __restrict__ Q,
+                                                 const float* __restrict__ Q2) {
   const int gl = threadIdx.x % LPG;
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
   const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
@@ -460,7 +463,14 @@ __global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t, const float
     } else {
       const uint64_t qa = (lo + QB - 1) / QB, qb = hi / QB;
       sum_p(a.partials, lo, qa * QB, a.e, acc, gl);
-      sum_p(Q, qa, qb, a.e, acc, gl);
+      if (qb - qa <= 2 * QB) {
+        sum_p(Q, qa, qb, a.e, acc, gl);
+      } else {  // the hottest keys: a second level of 64-block sums
+        const uint64_t q2a = (qa + QB - 1) / QB, q2b = qb / QB;
+        sum_p(Q, qa, q2a * QB, a.e, acc, gl);
+        sum_p(Q2, q2a, q2b, a.e, acc, gl);
+        sum_p(Q, q2b * QB, qb, a.e, acc, gl);
+      }
       sum_p(a.partials, qb * QB, hi, a.e, acc, gl);
     }
     finalize(a, t, u, acc, gl);
@@ -473,11 +483,16 @@ void launch_seg(const SegArgs& a, const TView& t, float* Q, cudaStream_t s) {
   const uint32_t nchunks = (a.n_pos + a.CH - 1) / a.CH;
   const uint32_t nP = 2 * nchunks;
   k_seg_chunks<LPG, NV, V4><<<grid_cap(((uint64_t)nchunks * LPG + 255) / 256), 256, 0, s>>>(a, t); ::kp::count_launch();
-  if (nP >= QB) {
-    k_seg_blocksum<LPG, NV, V4><<<grid_cap(((uint64_t)(nP / QB) * LPG + 255) / 256), 256, 0, s>>>(a, nP, Q); ::kp::count_launch();
+  const uint32_t nQ = nP / QB;
+  float* Q2 = Q + (uint64_t)(nQ + 1) * a.e;
+  if (nQ) {
+    k_seg_blocksum<LPG, NV, V4><<<grid_cap(((uint64_t)nQ * LPG + 255) / 256), 256, 0, s>>>(a.partials, nP, a.e, Q); ::kp::count_launch();
+  }
+  if (nQ >= QB) {
+    k_seg_blocksum<LPG, NV, V4><<<grid_cap(((uint64_t)(nQ / QB) * LPG + 255) / 256), 256, 0, s>>>(Q, nQ, a.e, Q2); ::kp::count_launch();
   }
   if (nchunks > 1) {
-    k_seg_fix<LPG, NV, V4><<<grid_cap(((uint64_t)nchunks * LPG + 255) / 256), 256, 0, s>>>(a, t, Q); ::kp::count_launch();
+    k_seg_fix<LPG, NV, V4><<<grid_cap(((uint64_t)nchunks * LPG + 255) / 256), 256, 0, s>>>(a, t, Q, Q2); ::kp::count_launch();
   }
 }
 
@@ -595,7 +610,7 @@ void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* 
   a.b2 = r.beta2;
   TView tv{};
   if (t) tv = view(t);
-  float* Q = ws.qsums.get<float>((size_t)(2 * nchunks / QB + 1) * e);
+  float* Q = ws.qsums.get<float>((size_t)(2 * nchunks / QB + 1 + 2 * nchunks / QB / QB + 1) * e);
   dispatch_e<SegF>(e, a, tv, Q, s);
 }
 

@@ -295,6 +295,29 @@ def test_trainer_pooling_paths_vs_oracle(kp, S, e, pool, rule, multi):
     assert close(tr.worker_state(0)["x"], o64.worker_state(0)["x"])
 
 
+def test_trainer_hot_key_block_sums_vs_oracle(kp):
+    """One key holding ~80% of a 512K-occurrence batch: its gradient spans
+    thousands of 64-position chunks, so the segmented reduction takes the
+    two-level block-sum path (kp_embed.cu k_seg_fix, Q2). State vs the f64
+    oracle."""
+    cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=65536, embedding_dim=4, n_slots=8,
+                       hidden=(16,), pooling="sum", activation="relu", alpha=0.02, sparse_lr=0.1)
+    o64 = O.Orc(cfg, 64)
+    tr = kp.Trainer(table_capacity=1 << 16, **trainer_kwargs(vars(cfg)))
+    for b in range(2):
+        bt = make_batch(65536, V=1000, zipf_s=3.0, n_slots=8, seed=40 + b)
+        assert np.bincount(bt.keys.astype(np.int64)).max() > 300_000
+        ro = o64.batch(bt.offs, bt.keys, bt.labels, slots=bt.slots, predict_first=True)
+        rg = tr.train_batch(bt.offs, bt.keys, bt.labels, slots=bt.slots, predict_first=True)
+        assert abs(ro["loss"] - rg["loss"]) <= TOL_LOSS
+    k64, w64, a64, _ = o64.table()
+    kg, wg, s1, _ = tr.table()
+    assert np.array_equal(k64, kg)
+    assert close(wg, w64)
+    assert close(s1, a64, 1e-9, TOL_ACC_REL)
+    assert close(tr.worker_state(0)["x"], o64.worker_state(0)["x"])
+
+
 def test_trainer_deterministic(kp):
     def run():
         tr = kp.Trainer(table_capacity=1 << 18, n_workers=1, k=1, minibatch_size=4096,
