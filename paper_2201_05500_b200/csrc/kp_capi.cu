@@ -118,8 +118,9 @@ struct kp_trainer {
     DevBuf offs, keys, slots, labels;
     std::vector<uint32_t> h_offs;
     uint32_t n = 0;
-    bool has_slots = false, ready = false;
-    cudaEvent_t ev = nullptr;
+    bool has_slots = false, ready = false, used_set = false;
+    cudaEvent_t ev = nullptr;    // H2D of this slot done (copy stream)
+    cudaEvent_t used = nullptr;  // last step reading this slot done (compute stream)
   } stage[2];
   cudaStream_t copy_s = nullptr;
   // gradient exchange stream (G > 1): the all-to-all overlaps the last GEMM
@@ -200,8 +201,10 @@ struct kp_trainer {
   }
   ~kp_trainer() {
     for (auto e : ev) cudaEventDestroy(e);
-    for (auto& st : stage)
+    for (auto& st : stage) {
       if (st.ev) cudaEventDestroy(st.ev);
+      if (st.used) cudaEventDestroy(st.used);
+    }
     if (copy_s) cudaStreamDestroy(copy_s);
     if (xs) cudaStreamDestroy(xs);
     for (PeerWin* w : {&peer.keys, &peer.rows, &peer.grads, &peer.flags, &peer.dv, &peer.dx,
@@ -1566,6 +1569,9 @@ int kp_trainer_stage_batch(kp_trainer* tr, int slot, const uint32_t* offs, const
     if (!tr->copy_s) KP_CUDA(cudaStreamCreateWithFlags(&tr->copy_s, cudaStreamNonBlocking));
     auto& st = tr->stage[slot];
     if (!st.ev) KP_CUDA(cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming));
+    // the step that consumed this slot last may still be reading it (labels
+    // are read by the loss head late in the step): order the overwrite after it
+    if (st.used_set) KP_CUDA(cudaStreamWaitEvent(tr->copy_s, st.used, 0));
     const uint32_t O = offs[n];
     uint32_t* d_offs = st.offs.get<uint32_t>(n + 1);
     uint64_t* d_keys = st.keys.get<uint64_t>(std::max<uint32_t>(O, 1));
@@ -1597,6 +1603,9 @@ int kp_trainer_train_staged(kp_trainer* tr, int slot, uint64_t global_n, uint64_
                      st.has_slots ? static_cast<const uint16_t*>(st.slots.p) : nullptr,
                      static_cast<const int32_t*>(st.labels.p), st.n, global_n, global_first,
                      predict_first != 0, preds, out);
+    if (!st.used) KP_CUDA(cudaEventCreateWithFlags(&st.used, cudaEventDisableTiming));
+    KP_CUDA(cudaEventRecord(st.used, tr->s));
+    st.used_set = true;
   });
 }
 
