@@ -307,11 +307,15 @@ __global__ void __launch_bounds__(ST) k_head_count(const KT* __restrict__ sk, ui
                                                    uint32_t* __restrict__ bcount) {
   __shared__ uint32_t s_warp[NW];
   const uint32_t base = blockIdx.x * TILE + threadIdx.x * IPT;
+  KT kv[IPT];
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) kv[r] = base + r < n ? sk[base + r] : KT(0);
+  const KT prev = base > 0 && base - 1 < n ? sk[base - 1] : KT(0);
   uint32_t c = 0;
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     const uint32_t i = base + r;
-    if (i < n && (i == 0 || sk[i] != sk[i - 1])) ++c;
+    if (i < n && (i == 0 || kv[r] != (r ? kv[r - 1] : prev))) ++c;
   }
   uint32_t tot;
   block_excl_scan(c, s_warp, tot);
@@ -331,18 +335,23 @@ __global__ void __launch_bounds__(ST) k_dedup_emit(const KT* __restrict__ sk,
                                                    uint32_t* __restrict__ sorted_mapped) {
   __shared__ uint32_t s_warp[NW];
   const uint32_t base = blockIdx.x * TILE + threadIdx.x * IPT;
+  // every load first (keys, the predecessor key, occurrences, then the
+  // occ_map gathers), so one latency covers the thread's IPT positions
+  KT kv[IPT];
+  uint32_t occ[IPT], mp[IPT];
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) kv[r] = base + r < n ? sk[base + r] : KT(0);
+  const KT prev = base > 0 && base - 1 < n ? sk[base - 1] : KT(0);
+#pragma unroll
+  for (int r = 0; r < IPT; ++r) occ[r] = base + r < n ? sv[base + r] : 0;
   bool f[IPT];
   uint32_t c = 0;
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     const uint32_t i = base + r;
-    f[r] = i < n && (i == 0 || sk[i] != sk[i - 1]);
+    f[r] = i < n && (i == 0 || kv[r] != (r ? kv[r - 1] : prev));
     c += f[r];
   }
-  // the random accesses (occ_map gathers) all in flight before any store
-  uint32_t occ[IPT], mp[IPT];
-#pragma unroll
-  for (int r = 0; r < IPT; ++r) occ[r] = base + r < n ? sv[base + r] : 0;
   if (occ_map) {
 #pragma unroll
     for (int r = 0; r < IPT; ++r) mp[r] = base + r < n ? occ_map[occ[r]] : 0;
@@ -355,7 +364,7 @@ __global__ void __launch_bounds__(ST) k_dedup_emit(const KT* __restrict__ sk,
     const uint32_t i = base + r;
     if (i >= n) break;
     if (f[r]) {
-      uniq[uid] = kmin + (uint64_t)sk[i];
+      uniq[uid] = kmin + (uint64_t)kv[r];
       seg[uid] = i;
       ++uid;
     }
