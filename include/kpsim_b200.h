@@ -234,8 +234,11 @@ int kp_trainer_train_batch_device(kp_trainer* tr, const uint32_t* h_offs, const 
                                   uint64_t global_first, int predict_first, float* preds,
                                   kp_batch_result* out);
 /* Pipelined ingestion: stage a HOST batch (pinned memory for true overlap)
- * into one of two device buffer slots with an async H2D on a copy stream, then
- * train on it. Staging batch i+1 while batch i trains hides the H2D. */
+ * into one of two device buffer slots, then train on it. The async H2D (copy
+ * stream) is issued once the running step has passed its last host readback
+ * (or at train_staged of that slot), so staging batch i+1 right before
+ * training batch i hides the copy behind batch i's compute. The host arrays
+ * must stay valid and unmodified until train_staged(slot) returns. */
 int kp_trainer_stage_batch(kp_trainer* tr, int slot, const uint32_t* offs, const uint64_t* keys,
                            const uint16_t* slots, const int32_t* labels, uint32_t n);
 int kp_trainer_train_staged(kp_trainer* tr, int slot, uint64_t global_n, uint64_t global_first,

@@ -121,6 +121,12 @@ struct kp_trainer {
     bool has_slots = false, ready = false, used_set = false;
     cudaEvent_t ev = nullptr;    // H2D of this slot done (copy stream)
     cudaEvent_t used = nullptr;  // last step reading this slot done (compute stream)
+    // H2D not issued yet (host sources, caller-owned until train_staged)
+    bool pending = false;
+    const uint32_t* h_src_offs = nullptr;
+    const uint64_t* h_src_keys = nullptr;
+    const uint16_t* h_src_slots = nullptr;
+    const int32_t* h_src_labels = nullptr;
   } stage[2];
   cudaStream_t copy_s = nullptr;
   // gradient exchange stream (G > 1): the all-to-all overlaps the last GEMM
@@ -567,6 +573,25 @@ void merge_states_peer(kp_trainer* tr, float alpha, bool reset) {
   }
 }
 
+// Issue the H2D of staged batches waiting for it (one slot, or all with
+// slot < 0). The copy is ordered after the last step that read the slot.
+void issue_staged(kp_trainer* tr, int slot) {
+  for (int i = 0; i < 2; ++i) {
+    if (slot >= 0 && i != slot) continue;
+    auto& st = tr->stage[i];
+    if (!st.pending) continue;
+    if (st.used_set) KP_CUDA(cudaStreamWaitEvent(tr->copy_s, st.used, 0));
+    const uint32_t n = st.n, O = st.h_offs[n];
+    KP_CUDA(cudaMemcpyAsync(st.offs.p, st.h_src_offs, (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, tr->copy_s));
+    KP_CUDA(cudaMemcpyAsync(st.keys.p, st.h_src_keys, (size_t)O * 8, cudaMemcpyHostToDevice, tr->copy_s));
+    if (st.has_slots)
+      KP_CUDA(cudaMemcpyAsync(st.slots.p, st.h_src_slots, (size_t)O * 2, cudaMemcpyHostToDevice, tr->copy_s));
+    KP_CUDA(cudaMemcpyAsync(st.labels.p, st.h_src_labels, (size_t)n * 4, cudaMemcpyHostToDevice, tr->copy_s));
+    KP_CUDA(cudaEventRecord(st.ev, tr->copy_s));
+    st.pending = false;
+  }
+}
+
 PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   cudaStream_t s = tr->s;
   // bags first, so dedup can emit the bag of every sorted position
@@ -673,6 +698,7 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   float* imax = tr->inst_max.get<float>(std::max<uint32_t>(sv.n_inst, 1));
   pool(bag_offs, nb, rowocc, pr.src, tr->e, tr->cfg.pooling == 1, pooled, invc, s, imax, tr->S);
   tr->mark(2);
+  issue_staged(tr, -1);  // this step's host readbacks are done
   return pr;
 }
 
@@ -1569,19 +1595,19 @@ int kp_trainer_stage_batch(kp_trainer* tr, int slot, const uint32_t* offs, const
     if (!tr->copy_s) KP_CUDA(cudaStreamCreateWithFlags(&tr->copy_s, cudaStreamNonBlocking));
     auto& st = tr->stage[slot];
     if (!st.ev) KP_CUDA(cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming));
-    // the step that consumed this slot last may still be reading it (labels
-    // are read by the loss head late in the step): order the overwrite after it
-    if (st.used_set) KP_CUDA(cudaStreamWaitEvent(tr->copy_s, st.used, 0));
     const uint32_t O = offs[n];
-    uint32_t* d_offs = st.offs.get<uint32_t>(n + 1);
-    uint64_t* d_keys = st.keys.get<uint64_t>(std::max<uint32_t>(O, 1));
-    uint16_t* d_slots = slots ? st.slots.get<uint16_t>(std::max<uint32_t>(O, 1)) : nullptr;
-    int32_t* d_labels = st.labels.get<int32_t>(std::max<uint32_t>(n, 1));
-    KP_CUDA(cudaMemcpyAsync(d_offs, offs, (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, tr->copy_s));
-    KP_CUDA(cudaMemcpyAsync(d_keys, keys, (size_t)O * 8, cudaMemcpyHostToDevice, tr->copy_s));
-    if (slots) KP_CUDA(cudaMemcpyAsync(d_slots, slots, (size_t)O * 2, cudaMemcpyHostToDevice, tr->copy_s));
-    KP_CUDA(cudaMemcpyAsync(d_labels, labels, (size_t)n * 4, cudaMemcpyHostToDevice, tr->copy_s));
-    KP_CUDA(cudaEventRecord(st.ev, tr->copy_s));
+    st.offs.get<uint32_t>(n + 1);
+    st.keys.get<uint64_t>(std::max<uint32_t>(O, 1));
+    if (slots) st.slots.get<uint16_t>(std::max<uint32_t>(O, 1));
+    st.labels.get<int32_t>(std::max<uint32_t>(n, 1));
+    // The H2D itself is issued at the next point where the trainer has no
+    // host readback left in its current step (issue_staged), so the step's
+    // small D2H readbacks never queue behind a 66 MB copy.
+    st.h_src_offs = offs;
+    st.h_src_keys = keys;
+    st.h_src_slots = slots;
+    st.h_src_labels = labels;
+    st.pending = true;
     st.h_offs.assign(offs, offs + n + 1);
     st.n = n;
     st.has_slots = slots != nullptr;
@@ -1596,6 +1622,7 @@ int kp_trainer_train_staged(kp_trainer* tr, int slot, uint64_t global_n, uint64_
     auto& st = tr->stage[slot];
     KP_CHECK(st.ready, kErrGeneric, "train_staged: nothing staged in this slot");
     KP_CUDA(cudaSetDevice(tr->device));
+    if (st.pending) issue_staged(tr, slot);
     KP_CUDA(cudaStreamWaitEvent(tr->s, st.ev, 0));
     st.ready = false;
     train_batch_impl(tr, st.h_offs.data(), static_cast<const uint32_t*>(st.offs.p),

@@ -36,6 +36,8 @@ struct PyTrainer {
   std::unique_ptr<TieredStore> store;
   std::unique_ptr<Trainer> tr;
   std::shared_ptr<Comm> comm;
+  // host arrays of the staged batches: the H2D reads them until train_staged
+  py::object staged[2];
 };
 
 TrainerConfig config_from_kwargs(const py::kwargs& kw) {
@@ -447,6 +449,7 @@ PYBIND11_MODULE(_kpsim_b200, m) {
              }
              check(kp_trainer_stage_batch(p.tr->handle(), slot, offs.data(), keys.data(), sp,
                                           labels.data(), n));
+             p.staged[slot] = py::make_tuple(offs, keys, labels, sl);
            },
            py::arg("slot"), py::arg("offs"), py::arg("keys"), py::arg("labels"),
            py::arg("slots") = py::none())
@@ -462,6 +465,7 @@ PYBIND11_MODULE(_kpsim_b200, m) {
                                              predict_first ? 1 : 0,
                                              predict_first ? preds.data() : nullptr, &br));
              }
+             p.staged[slot] = py::none();  // its H2D has completed
              py::dict d;
              d["loss"] = br.loss;
              d["minibatch_steps"] = br.minibatch_steps;
