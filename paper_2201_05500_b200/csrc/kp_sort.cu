@@ -63,10 +63,34 @@ __global__ void k_minmax_init(unsigned long long* mm) {
 
 __global__ void k_minmax(const uint64_t* __restrict__ keys, uint32_t n, unsigned long long* mm) {
   uint64_t lo = ~0ull, hi = 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
-    lo = k < lo ? k : lo;
-    hi = k > hi ? k : hi;
+  // 4 x 16-byte loads in flight per thread; an 8-byte-aligned start peels
+  // its first key
+  const uint32_t peel = (reinterpret_cast<uintptr_t>(keys) & 15) ? 1u : 0u;
+  if (peel && n && blockIdx.x == 0 && threadIdx.x == 0) lo = hi = keys[0];
+  keys += peel;
+  n = n > peel ? n - peel : 0;
+  const uint32_t n2 = n / 2;
+  const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n2; i += 4 * stride) {
+    ulonglong2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(k2 + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      lo = min(lo, (uint64_t)min(v[u].x, v[u].y));
+      hi = max(hi, (uint64_t)max(v[u].x, v[u].y));
+    }
+  }
+  for (; i < n2; i += stride) {
+    const ulonglong2 v = __ldg(k2 + i);
+    lo = min(lo, (uint64_t)min(v.x, v.y));
+    hi = max(hi, (uint64_t)max(v.x, v.y));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    lo = min(lo, keys[n - 1]);
+    hi = max(hi, keys[n - 1]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -75,7 +99,14 @@ __global__ void k_minmax(const uint64_t* __restrict__ keys, uint32_t n, unsigned
     lo = a < lo ? a : lo;
     hi = b > hi ? b : hi;
   }
-  if ((threadIdx.x & 31) == 0) {
+  // block reduce, then one atomic pair per block (per-warp atomics on the
+  // same two words serialised at L2)
+  __shared__ uint64_t s_lo[32], s_hi[32];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) s_lo[w] = lo, s_hi[w] = hi;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < nw; ++j) lo = min(lo, s_lo[j]), hi = max(hi, s_hi[j]);
     atomicMin(&mm[0], (unsigned long long)lo);
     atomicMax(&mm[1], (unsigned long long)hi);
   }

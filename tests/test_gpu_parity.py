@@ -42,7 +42,8 @@ def close(a, b, atol=TOL_W_ABS, rtol=TOL_W_REL):
 # ------------------------------------------------------------------ dedup ---
 @pytest.mark.parametrize("n,V,zipf", [(0, 10, None), (1, 10, None), (1000, 1, None),
                                       (5000, 50, None), (300_000, 10**6, 1.1),
-                                      (2_000_000, 10**8, 1.1), (100_000, 2**64 - 1, None)])
+                                      (2_000_000, 10**8, 1.1), (100_000, 2**64 - 1, None),
+                                      (7, 1000, None), (99_999, 10**6, 1.1)])
 def test_dedup_bit_exact(kp, n, V, zipf):
     rng = np.random.default_rng(n + 1)
     if zipf:
