@@ -42,18 +42,32 @@ __global__ void k_prepare_bags(const uint32_t* __restrict__ offs, uint32_t occ_b
         for (uint32_t s = lane; s < S; s += 32) bag_offs[(uint64_t)i * S + s] = o0;
         continue;
       }
-      for (uint32_t o = o0 + lane; o < o1; o += 32) {
-        const uint32_t s = slots[o];
-        const int prev = o == o0 ? -1 : (int)slots[o - 1];
-        if (s >= S || (int)s < prev) {
-          atomicMin(err, o);
-          bag_of_occ[o] = i * S;  // keep downstream indexing in bounds; the batch is rejected
-          continue;
+      for (uint32_t ob = o0; ob < o1; ob += 128) {
+        // the instance's slot ids (and predecessors) for 4 rounds in flight at once
+        uint32_t sv[4];
+        int pv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t o = ob + lane + 32 * k;
+          sv[k] = o < o1 ? slots[o] : 0;
+          pv[k] = o < o1 && o > o0 ? (int)slots[o - 1] : -1;
         }
-        for (int t = prev + 1; t <= (int)s; ++t) bag_offs[(uint64_t)i * S + t] = o;
-        if (o == o1 - 1)
-          for (uint32_t t = s + 1; t < S; ++t) bag_offs[(uint64_t)i * S + t] = o1;
-        bag_of_occ[o] = i * S + s;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t o = ob + lane + 32 * k;
+          if (o >= o1) break;
+          const uint32_t s = sv[k];
+          const int prev = pv[k];
+          if (s >= S || (int)s < prev) {
+            atomicMin(err, o);
+            bag_of_occ[o] = i * S;  // keep downstream indexing in bounds; the batch is rejected
+            continue;
+          }
+          for (int t = prev + 1; t <= (int)s; ++t) bag_offs[(uint64_t)i * S + t] = o;
+          if (o == o1 - 1)
+            for (uint32_t t = s + 1; t < S; ++t) bag_offs[(uint64_t)i * S + t] = o1;
+          bag_of_occ[o] = i * S + s;
+        }
       }
     }
   }
@@ -395,13 +409,14 @@ __global__ void __launch_bounds__(256) k_seg_blocksum(const float* __restrict__ 
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
   const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
   for (uint64_t j = g0; j < nP / QB; j += ng) {
-    Row<LPG, NV, V4> acc, r[4];
+    constexpr int UB = V4 ? 16 : 4;  // rows in flight (the Q2 level is latency-bound)
+    Row<LPG, NV, V4> acc, r[UB];
     acc.zero();
-    for (uint32_t i = 0; i < QB; i += 4) {
+    for (uint32_t i = 0; i < QB; i += UB) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) r[u].load(src + (j * QB + i + u) * e, gl, e);
+      for (int u = 0; u < UB; ++u) r[u].load(src + (j * QB + i + u) * e, gl, e);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc.add(r[u]);
+      for (int u = 0; u < UB; ++u) acc.add(r[u]);
     }
     acc.store(Q + j * e, gl, e);
   }
