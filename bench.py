@@ -212,7 +212,8 @@ def run_reference(args, rank):
     dt = time.perf_counter() - t0
     value = cores * per * args.steps / dt
     sample = (f"{per} instances x {cores} threads per step, each thread an independent reference "
-              f"Trainer (N=1,k=1) on the configs[1] batch folded to S=1 (reference semantics: "
+              f"Trainer (N=1,k=1) on the {workload_config(args, 1)['workload'].split(':')[0]} batch "
+              f"folded to S=1 (reference semantics: "
               f"model [{args.dim}->{args.hidden.replace(',', '->')}->1])")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -226,9 +227,22 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def config_index(args, world):
+    """Which BASELINE.json configs[i] these arguments reproduce (None: custom)."""
+    if (args.vocab, args.dim, args.slots, args.batch) == (1_000_000, 8, 26, 4096):
+        return 0
+    if args.vocab >= 500_000_000:
+        return 4
+    if (args.vocab, args.dim, args.slots, args.batch) == (100_000_000, 64, 100, 65536):
+        return 3 if args.k > 1 else (1 if world == 1 else 2)
+    return None
+
+
 def workload_config(args, world):
+    ci = config_index(args, world)
+    small = args.vocab * args.dim * 8 < 126e6
     return {
-        "workload": f"configs[{1 if world == 1 else 2}]: {args.vocab // 1_000_000}M-key table, emb dim "
+        "workload": f"{f'configs[{ci}]' if ci is not None else 'custom'}: {args.vocab // 1_000_000}M-key table, emb dim "
                     f"{args.dim}, {args.slots} slots, batch {args.batch}/GPU, Zipf({args.zipf}) keys, "
                     f"{'AdaGrad' if args.sparse_rule == 'adagrad' else 'sparse Adam'} rows, k={args.k}",
         "global_batch": args.batch * world,
@@ -237,7 +251,8 @@ def workload_config(args, world):
         "table_keys": args.vocab,
         "mlp": f"[{args.slots * args.dim}->{args.hidden.replace(',', '->')}->1]",
         "parallelism": f"table sharded key%{world}, dp{world}" if world > 1 else "single GPU",
-        "l2": "per-step working set ~5 GB >> 126 MB L2 (no flush needed)",
+        "l2": ("table fits the 126 MB L2 (small config, no flush; not the headline)" if small else
+               "per-step working set ~5 GB >> 126 MB L2 (no flush needed)"),
         "prefill": "table pre-populated with all keys (steady state)" if not args.no_prefill else "cold",
     }
 
