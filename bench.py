@@ -212,7 +212,7 @@ def run_reference(args, rank):
     dt = time.perf_counter() - t0
     value = cores * per * args.steps / dt
     sample = (f"{per} instances x {cores} threads per step, each thread an independent reference "
-              f"Trainer (N=1,k=1) on the {workload_config(args, 1)['workload'].split(':')[0]} batch "
+              f"Trainer (N=1,k=1) on the {workload_config(args, max(1, args.gpus))['workload'].split(':')[0]} batch "
               f"folded to S=1 (reference semantics: "
               f"model [{args.dim}->{args.hidden.replace(',', '->')}->1])")
     line = {
