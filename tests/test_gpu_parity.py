@@ -431,6 +431,42 @@ def test_staged_ingestion_matches_direct(kp):
     assert np.array_equal(x1, x2)
 
 
+def test_staged_restage_and_lifetime(kp):
+    """The staged H2D is issued lazily (after the running step's last host
+    readback): re-staging a slot before training it replaces the batch, and
+    the binding keeps the host arrays alive until train_staged returns even
+    when the caller drops them."""
+    import gc
+
+    def mk(b):
+        return make_batch(2048, V=10**6, zipf_s=1.1, n_slots=8, seed=100 + b)
+
+    def direct(order):
+        tr = kp.Trainer(table_capacity=1 << 18, n_workers=1, k=1, minibatch_size=2048,
+                        embedding_dim=16, n_slots=8, hidden=[32])
+        for b in order:
+            bt = mk(b)
+            tr.train_batch(bt.offs, bt.keys, bt.labels, slots=bt.slots)
+        return tr.table(), tr.worker_state(0)["x"]
+
+    tr = kp.Trainer(table_capacity=1 << 18, n_workers=1, k=1, minibatch_size=2048,
+                    embedding_dim=16, n_slots=8, hidden=[32])
+    b0, b1, b2 = mk(0), mk(1), mk(2)
+    tr.stage_batch(0, b0.offs, b0.keys, b0.labels, slots=b0.slots)
+    tr.stage_batch(1, b1.offs, b1.keys, b1.labels, slots=b1.slots)
+    # replace slot 1 with fresh copies the test then drops
+    tr.stage_batch(1, b2.offs.copy(), b2.keys.copy(), b2.labels.copy(), slots=b2.slots.copy())
+    gc.collect()
+    tr.train_staged(0, n_local=2048)
+    tr.train_staged(1, n_local=2048)
+    (k1, w1, a1, _), x1 = (tr.table(), tr.worker_state(0)["x"])
+    (k2, w2, a2, _), x2 = direct([0, 2])
+    assert np.array_equal(k1, k2) and np.array_equal(w1, w2) and np.array_equal(a1, a2)
+    assert np.array_equal(x1, x2)
+    with pytest.raises(Exception):
+        tr.train_staged(1, n_local=2048)  # consumed
+
+
 @pytest.mark.parametrize("n,ties", [(2, False), (1000, True), (65536, False), (200_000, True)])
 def test_device_auc_bit_exact(kp, n, ties):
     """Device rank-sum AUC == the reference's compute_auc on the same fp32 scores,
