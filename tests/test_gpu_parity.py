@@ -296,17 +296,19 @@ def test_trainer_pooling_paths_vs_oracle(kp, S, e, pool, rule, multi):
     assert close(tr.worker_state(0)["x"], o64.worker_state(0)["x"])
 
 
-def test_trainer_hot_key_block_sums_vs_oracle(kp):
-    """One key holding ~80% of a 512K-occurrence batch: its gradient spans
-    thousands of 64-position chunks, so the segmented reduction takes the
-    two-level block-sum path (kp_embed.cu k_seg_fix, Q2). State vs the f64
+@pytest.mark.parametrize("B,S", [(65536, 8), (16384, 80)])
+def test_trainer_hot_key_block_sums_vs_oracle(kp, B, S):
+    """One key holding ~80% of a 0.5M / 1.3M-occurrence batch: its gradient
+    spans thousands of chunks, so the segmented reduction takes the two-level
+    block-sum path (kp_embed.cu k_seg_fix, Q2); the 1.3M case runs the full
+    64-position chunks (shorter ones below 1.2M positions). State vs the f64
     oracle."""
-    cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=65536, embedding_dim=4, n_slots=8,
+    cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=B, embedding_dim=4, n_slots=S,
                        hidden=(16,), pooling="sum", activation="relu", alpha=0.02, sparse_lr=0.1)
     o64 = O.Orc(cfg, 64)
     tr = kp.Trainer(table_capacity=1 << 16, **trainer_kwargs(vars(cfg)))
     for b in range(2):
-        bt = make_batch(65536, V=1000, zipf_s=3.0, n_slots=8, seed=40 + b)
+        bt = make_batch(B, V=1000, zipf_s=3.0, n_slots=S, seed=40 + b)
         assert np.bincount(bt.keys.astype(np.int64)).max() > 300_000
         ro = o64.batch(bt.offs, bt.keys, bt.labels, slots=bt.slots, predict_first=True)
         rg = tr.train_batch(bt.offs, bt.keys, bt.labels, slots=bt.slots, predict_first=True)
