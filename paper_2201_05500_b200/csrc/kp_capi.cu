@@ -999,13 +999,16 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
   KP_CUDA(cudaMemcpyAsync(lsum.data(), d_loss, n_mb * 8, cudaMemcpyDeviceToHost, s));
   if (predict_first && h_preds)
     KP_CUDA(cudaMemcpyAsync(h_preds, d_pred_keep, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+  uint32_t h_sc[4] = {0, 0, 0, 0};  // table scalars ([2] = full flag), same readback
+  KP_CUDA(cudaMemcpyAsync(h_sc, tr->tab.t->d_scalars, 16, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaStreamSynchronize(s));
   tr->harvest();
   if (tr->prof) tr->prof_steps += n_mb;
   KP_CHECK(h_err == 0xFFFFFFFFu, kErrConfig,
            "slot ids must be < n_slots and non-decreasing within an instance (occurrence " +
                std::to_string(h_err) + ")");
-  table_check_full(tr->tab.t, s);
+  KP_CHECK(h_sc[2] == 0, kErrTableFull,
+           "embedding table full: capacity " + std::to_string(tr->tab.t->capacity) + " rows");
   KP_CHECK(!(h_chk & 1), kErrGeneric, "non-finite worker state after step " + std::to_string(tr->t_global));
   KP_CHECK(!(h_chk & 2), kErrGeneric, "second moment lost positivity at step " + std::to_string(tr->t_global));
   KP_CHECK(!(h_chk & 16), kErrCuda, "peer exchange timed out waiting for another rank (NVLink window flags)");
