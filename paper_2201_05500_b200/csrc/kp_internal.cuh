@@ -26,6 +26,7 @@ struct DedupWs {
   uint32_t* d_nunique = nullptr;          // device scalar U
   uint32_t* d_sorted_mapped = nullptr;    // occ_map[sorted_vals[p]] (when requested)
   uint32_t n = 0, n_unique = 0;
+  int spec_bits = -1;  // key-span bits of the last call (planned passes of the next)
 };
 
 // Radix sort (stable) of (key, occurrence index) + unique + inverse + segment

@@ -14,6 +14,7 @@
 //    shared-memory staged scatter so global writes are digit-run coalesced;
 //  * tiles of 2048 pairs (256 threads x 8), grids are multiples of the SM
 //    count for every config that matters.
+#include <cstdlib>
 #include <vector>
 
 #include "kp_internal.cuh"
@@ -547,29 +548,10 @@ __global__ void __launch_bounds__(ST) k_merge_level(const uint64_t* __restrict__
 
 }  // namespace
 
-void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
-           const uint32_t* d_occ_map) {
-  ws.n = n;
-  ws.d_nunique = ws.scalars.get<uint32_t>(4);
-  if (n == 0) {
-    ws.n_unique = 0;
-    ws.d_unique = ws.unique.get<uint64_t>(1);
-    ws.d_inverse = ws.inverse.get<uint32_t>(1);
-    ws.d_seg = ws.seg.get<uint32_t>(1);
-    KP_CUDA(cudaMemsetAsync(ws.d_seg, 0, 4, s));
-    KP_CUDA(cudaMemsetAsync(ws.d_nunique, 0, 4, s));
-    return;
-  }
-  const uint32_t nb = ceil_div(n, TILE);
-  auto* mm = ws.minmax.get<unsigned long long>(2);
-  k_minmax_init<<<1, 1, 0, s>>>(mm); ::kp::count_launch();
-  k_minmax<<<min(nb * 2, 1184u), 256, 0, s>>>(d_keys, n, mm); ::kp::count_launch();
-  unsigned long long h_mm[2];
-  KP_CUDA(cudaMemcpyAsync(h_mm, mm, 16, cudaMemcpyDeviceToHost, s));
-  KP_CUDA(cudaStreamSynchronize(s));
-  const uint64_t span = h_mm[1] - h_mm[0];
-  const int bits = span == 0 ? 0 : 64 - __builtin_clzll(span);
-
+// The radix passes + unique/inverse/segments for a key span of `bits` bits
+// (any plan whose passes cover the actual span sorts correctly).
+static void dedup_sort(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
+                       const uint32_t* d_occ_map, int bits, const unsigned long long* mm, uint32_t nb) {
   uint32_t* va = ws.vals_a.get<uint32_t>(n);
   uint32_t* vb = ws.vals_b.get<uint32_t>(n);
   uint32_t* bcount = ws.bcount.get<uint32_t>(nb);
@@ -651,6 +633,71 @@ void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
     k_dedup_emit<uint64_t><<<nb, ST, 0, s>>>(kin, mm, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
                                              ws.d_nunique, nb, d_occ_map, ws.d_sorted_mapped); ::kp::count_launch();
   }
+}
+
+static int span_bits(const unsigned long long* h_mm) {
+  const uint64_t span = h_mm[1] - h_mm[0];
+  return span == 0 ? 0 : 64 - __builtin_clzll(span);
+}
+
+// does a sort planned for `planned` span bits cover an actual span of `bits`?
+static bool plan_covers(int planned, int bits) {
+  if (planned > 32) return ((planned + 7) / 8) * 8 >= bits;  // wide: 8-bit digit passes
+  if (bits > 32) return false;                               // narrow keys are u32 (key - kmin)
+  const int np = planned == 0 ? 1 : (planned + 8) / 9;
+  const int db = planned == 0 ? 1 : (planned + np - 1) / np;
+  return np * db >= bits;
+}
+
+static bool spec_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("KP_DEDUP_SPEC");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
+           const uint32_t* d_occ_map) {
+  ws.n = n;
+  ws.d_nunique = ws.scalars.get<uint32_t>(4);
+  if (n == 0) {
+    ws.n_unique = 0;
+    ws.d_unique = ws.unique.get<uint64_t>(1);
+    ws.d_inverse = ws.inverse.get<uint32_t>(1);
+    ws.d_seg = ws.seg.get<uint32_t>(1);
+    KP_CUDA(cudaMemsetAsync(ws.d_seg, 0, 4, s));
+    KP_CUDA(cudaMemsetAsync(ws.d_nunique, 0, 4, s));
+    return;
+  }
+  const uint32_t nb = ceil_div(n, TILE);
+  auto* mm = ws.minmax.get<unsigned long long>(2);
+  k_minmax_init<<<1, 1, 0, s>>>(mm); ::kp::count_launch();
+  k_minmax<<<min(nb * 2, 1184u), 256, 0, s>>>(d_keys, n, mm); ::kp::count_launch();
+  if (spec_enabled() && ws.spec_bits >= 0) {
+    // Plan the passes from the previous call's key span and check it with
+    // the final readback (one host sync per dedup instead of two); a batch
+    // whose span outgrows the plan is sorted again with the exact plan.
+    const int planned = ws.spec_bits;
+    dedup_sort(d_keys, n, ws, s, d_occ_map, planned, mm, nb);
+    unsigned long long h_mm[2];
+    KP_CUDA(cudaMemcpyAsync(h_mm, mm, 16, cudaMemcpyDeviceToHost, s));
+    KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
+    KP_CUDA(cudaStreamSynchronize(s));
+    const int bits = span_bits(h_mm);
+    ws.spec_bits = bits;
+    if (plan_covers(planned, bits)) return;
+    dedup_sort(d_keys, n, ws, s, d_occ_map, bits, mm, nb);
+    KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
+    KP_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  unsigned long long h_mm[2];
+  KP_CUDA(cudaMemcpyAsync(h_mm, mm, 16, cudaMemcpyDeviceToHost, s));
+  KP_CUDA(cudaStreamSynchronize(s));
+  const int bits = span_bits(h_mm);
+  ws.spec_bits = bits;
+  dedup_sort(d_keys, n, ws, s, d_occ_map, bits, mm, nb);
   KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaStreamSynchronize(s));
 }

@@ -65,6 +65,23 @@ def test_dedup_bit_exact(kp, n, V, zipf):
         assert np.array_equal(u, O.ref_dedup(keys))
 
 
+def test_dedup_span_changes_between_calls(kp):
+    """dedup plans its radix passes from the previous call's key span and
+    re-sorts when a batch outgrows the plan: spans that grow (narrow ->
+    wider narrow -> full u64) and shrink must all stay bit-exact."""
+    rng = np.random.default_rng(7)
+    for V in (1000, 10**6, 10**8, 2**40, None, 50, 10**9, 1):
+        n = 200_000
+        if V is None:
+            keys = rng.integers(0, 2**63, n, dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+        else:
+            keys = rng.integers(0, V, n, dtype=np.uint64) + np.uint64(12345)
+        u, inv, _ = kp.dedup(keys)
+        want, winv = O.orc_dedup(keys)
+        assert np.array_equal(u, want), V
+        assert np.array_equal(inv, winv), V
+
+
 @pytest.mark.parametrize("R,n_per,V", [(1, 1000, 10**4), (2, 50_000, 10**5), (3, 7, 20),
                                        (4, 300_000, 10**6), (8, 120_000, 10**6), (5, 0, 10)])
 def test_dedup_runs_matches_dedup(kp, R, n_per, V):
