@@ -43,7 +43,8 @@ def close(a, b, atol=TOL_W_ABS, rtol=TOL_W_REL):
 @pytest.mark.parametrize("n,V,zipf", [(0, 10, None), (1, 10, None), (1000, 1, None),
                                       (5000, 50, None), (300_000, 10**6, 1.1),
                                       (2_000_000, 10**8, 1.1), (100_000, 2**64 - 1, None),
-                                      (7, 1000, None), (99_999, 10**6, 1.1)])
+                                      (7, 1000, None), (99_999, 10**6, 1.1),
+                                      (6_553_600, 10**8, 1.1), (3_276_800, 5 * 10**8, 1.3)])
 def test_dedup_bit_exact(kp, n, V, zipf):
     rng = np.random.default_rng(n + 1)
     if zipf:
@@ -350,6 +351,47 @@ def test_trainer_deterministic(kp):
     (k2, w2, a2, _), x2 = run()
     assert np.array_equal(k1, k2) and np.array_equal(w1, w2) and np.array_equal(a1, a2)
     assert np.array_equal(x1, x2)
+
+
+def test_trainer_full_size_properties(kp):
+    """configs[1] at full size (B=65536, 100 slots, e=64, Zipf(1.1) over 1e8
+    keys: 6.55M occurrences, ~1.09M unique per step), too big for the f64
+    oracle, checked through size-independent properties:
+      * the table key set after each step is the union of the steps' unique
+        keys (bit-exact, np.unique as the checker);
+      * first touch from the fresh entry {w=0, acc=1e-6} (store.hpp:49) with
+        AdaGrad (optimizer.cpp:86-95) gives acc = 1e-6 + g^2 and
+        w = -lr g / sqrt(acc), so |w| = lr sqrt(acc - 1e-6) / sqrt(acc) for
+        every row (fp32 tolerance 1e-4 rel, rows with acc >= 1e-5);
+      * the second push touches only its own working set: rows of keys absent
+        from batch 2 are bitwise unchanged."""
+    lr = 0.05
+    tr = kp.Trainer(table_capacity=1 << 22, n_workers=1, k=1, minibatch_size=65536,
+                    embedding_dim=64, n_slots=100, hidden=[256, 128], sparse_lr=lr)
+    b1 = make_batch(65536, V=10**8, zipf_s=1.1, n_slots=100, seed=20261018)
+    r1 = tr.train_batch(b1.offs, b1.keys, b1.labels, slots=b1.slots)
+    assert np.isfinite(r1["loss"]) and 0 < r1["loss"] < 2
+    u1 = np.unique(b1.keys)
+    assert len(u1) > 1_000_000
+    k1, w1, a1, _ = tr.table()
+    assert np.array_equal(k1, u1)
+    w1 = np.asarray(w1, np.float64).reshape(len(k1), 64)
+    a1 = np.asarray(a1, np.float64).reshape(len(k1), 64)
+    m = a1 >= 1e-5
+    assert m.mean() > 0.5
+    want = lr * np.sqrt(a1[m] - 1e-6) / np.sqrt(a1[m])
+    assert np.all(np.abs(np.abs(w1[m]) - want) <= 1e-4 * want)
+    assert np.all(a1 >= np.float32(1e-6))
+    b2 = make_batch(65536, V=10**8, zipf_s=1.1, n_slots=100, seed=20261019)
+    r2 = tr.train_batch(b2.offs, b2.keys, b2.labels, slots=b2.slots)
+    assert np.isfinite(r2["loss"])
+    k2, w2, _, _ = tr.table()
+    assert np.array_equal(k2, np.union1d(u1, np.unique(b2.keys)))
+    w2 = np.asarray(w2, np.float32).reshape(len(k2), 64)
+    keep = ~np.isin(k1, b2.keys)
+    assert keep.sum() > 100_000
+    pos = np.searchsorted(k2, k1[keep])
+    assert np.array_equal(w2[pos], w1[keep].astype(np.float32))
 
 
 def test_trainer_errors(kp):
