@@ -602,7 +602,7 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   prepare_bags(sv.offs, sv.occ_base, sv.slots, sv.n_inst, tr->S, bag_offs, bag_of_occ, err, s);
   uint32_t h_err = 0xFFFFFFFFu;
   KP_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, s));
-  dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ);  // synchronises the stream
+  dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ, err + 1);  // synchronises the stream
   if (sv.n_occ == 0) KP_CUDA(cudaStreamSynchronize(s));
   // reject bad slot ids before any state (table, weights) changes
   KP_CHECK(h_err == 0xFFFFFFFFu, kErrConfig,

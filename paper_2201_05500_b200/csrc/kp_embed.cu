@@ -32,11 +32,15 @@ __global__ void k_prepare_bags(const uint32_t* __restrict__ offs, uint32_t occ_b
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  bool nonid = false;  // some bag_of_occ[o] != o
   for (uint32_t i = w0; i < n_inst; i += nw) {
     const uint32_t o0 = offs[i] - occ_base, o1 = offs[i + 1] - occ_base;
     if (S == 1) {
       if (lane == 0) bag_offs[i] = o0;
-      for (uint32_t o = o0 + lane; o < o1; o += 32) bag_of_occ[o] = i;
+      for (uint32_t o = o0 + lane; o < o1; o += 32) {
+        bag_of_occ[o] = i;
+        nonid |= o != i;
+      }
     } else {
       if (o0 == o1) {
         for (uint32_t s = lane; s < S; s += 32) bag_offs[(uint64_t)i * S + s] = o0;
@@ -60,6 +64,7 @@ __global__ void k_prepare_bags(const uint32_t* __restrict__ offs, uint32_t occ_b
           const int prev = pv[k];
           if (s >= S || (int)s < prev) {
             atomicMin(err, o);
+            nonid = true;
             bag_of_occ[o] = i * S;  // keep downstream indexing in bounds; the batch is rejected
             continue;
           }
@@ -67,11 +72,14 @@ __global__ void k_prepare_bags(const uint32_t* __restrict__ offs, uint32_t occ_b
           if (o == o1 - 1)
             for (uint32_t t = s + 1; t < S; ++t) bag_offs[(uint64_t)i * S + t] = o1;
           bag_of_occ[o] = i * S + s;
+          nonid |= o != i * S + s;
         }
       }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) bag_offs[(uint64_t)n_inst * S] = offs[n_inst] - occ_base;
+  // one store per warp that saw a mismatch, skipped once another landed
+  if (__any_sync(0xffffffffu, nonid) && lane == 0 && *(volatile uint32_t*)(err + 1) != 0u) err[1] = 0u;
 }
 
 // ---- row access policies -------------------------------------------------
@@ -574,6 +582,7 @@ __global__ void k_gather_rows(const float* __restrict__ src, const uint32_t* __r
 void prepare_bags(const uint32_t* d_offs, uint32_t occ_base, const uint16_t* d_slots,
                   uint32_t n_inst, uint32_t S, uint32_t* d_bag_offs, uint32_t* d_bag_of_occ,
                   uint32_t* d_err, cudaStream_t s) {
+  KP_CUDA(cudaMemsetAsync(d_err + 1, 0xFF, 4, s));
   k_prepare_bags<<<grid_cap(((uint64_t)n_inst * 32 + 255) / 256), 256, 0, s>>>(
       d_offs, occ_base, d_slots, n_inst, S, d_bag_offs, d_bag_of_occ, d_err); ::kp::count_launch();
 }

@@ -33,8 +33,10 @@ struct DedupWs {
 // starts. Writes U to ws.n_unique (host; one sync) and ws.d_nunique.
 // d_occ_map (optional): per-occurrence map materialised in sorted order
 // (ws.d_sorted_mapped[p] = occ_map[sorted_vals[p]]), e.g. the bag of each occurrence.
+// d_occ_ident (optional, device word): 0xFFFFFFFF when occ_map is the identity
+// (one feature in every slot), which skips its random gather.
 void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
-           const uint32_t* d_occ_map = nullptr);
+           const uint32_t* d_occ_map = nullptr, const uint32_t* d_occ_ident = nullptr);
 // dedup() of keys made of runs [run_off[i], run_off[i+1]), each strictly
 // ascending: merge tree instead of the radix sort, identical outputs
 void dedup_runs(const uint64_t* d_keys, uint32_t n, const std::vector<uint64_t>& run_off,
@@ -90,7 +92,9 @@ void table_gather(const Table* t, const uint32_t* d_rows, uint32_t n, float* d_w
                   float* d_s2, cudaStream_t s);
 
 // ----------------------------------------------------------- embedding ---
-// bags: CSR over occurrences; bag b = instance*S + slot.
+// bags: CSR over occurrences; bag b = instance*S + slot. d_err[0]: first bad
+// occurrence (caller presets 0xFFFFFFFF); d_err[1]: 0xFFFFFFFF iff
+// bag_of_occ[o] == o for every occurrence (set here).
 void prepare_bags(const uint32_t* d_offs, uint32_t occ_base, const uint16_t* d_slots,
                   uint32_t n_inst, uint32_t S, uint32_t* d_bag_offs, uint32_t* d_bag_of_occ,
                   uint32_t* d_err, cudaStream_t s);

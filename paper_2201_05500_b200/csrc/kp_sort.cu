@@ -364,7 +364,8 @@ __global__ void __launch_bounds__(ST) k_dedup_emit(const KT* __restrict__ sk,
                                                    uint32_t* __restrict__ seg,
                                                    uint32_t* __restrict__ nuniq, uint32_t nb,
                                                    const uint32_t* __restrict__ occ_map,
-                                                   uint32_t* __restrict__ sorted_mapped) {
+                                                   uint32_t* __restrict__ sorted_mapped,
+                                                   const uint32_t* __restrict__ occ_ident) {
   __shared__ uint32_t s_warp[NW];
   const uint32_t base = blockIdx.x * TILE + threadIdx.x * IPT;
   // every load first (keys, the predecessor key, occurrences, then the
@@ -384,9 +385,11 @@ __global__ void __launch_bounds__(ST) k_dedup_emit(const KT* __restrict__ sk,
     f[r] = i < n && (i == 0 || kv[r] != (r ? kv[r - 1] : prev));
     c += f[r];
   }
+  // identity map (one feature per slot): the bag IS the occurrence, no gather
+  const bool ident = occ_ident && *occ_ident == 0xFFFFFFFFu;
   if (occ_map) {
 #pragma unroll
-    for (int r = 0; r < IPT; ++r) mp[r] = base + r < n ? occ_map[occ[r]] : 0;
+    for (int r = 0; r < IPT; ++r) mp[r] = base + r < n ? (ident ? occ[r] : occ_map[occ[r]]) : 0;
   }
   uint32_t tot;
   uint32_t uid = bbase[blockIdx.x] + block_excl_scan(c, s_warp, tot);  // uniques before my items
@@ -551,7 +554,8 @@ __global__ void __launch_bounds__(ST) k_merge_level(const uint64_t* __restrict__
 // The radix passes + unique/inverse/segments for a key span of `bits` bits
 // (any plan whose passes cover the actual span sorts correctly).
 static void dedup_sort(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
-                       const uint32_t* d_occ_map, int bits, const unsigned long long* mm, uint32_t nb) {
+                       const uint32_t* d_occ_map, const uint32_t* d_occ_ident, int bits,
+                       const unsigned long long* mm, uint32_t nb) {
   uint32_t* va = ws.vals_a.get<uint32_t>(n);
   uint32_t* vb = ws.vals_b.get<uint32_t>(n);
   uint32_t* bcount = ws.bcount.get<uint32_t>(nb);
@@ -605,7 +609,7 @@ static void dedup_sort(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStre
     k_head_count<uint32_t><<<nb, ST, 0, s>>>(kin32, n, bcount); ::kp::count_launch();
     k_scan_rows<<<1, ST, 0, s>>>(bcount, nb, ws.d_nunique + 1); ::kp::count_launch();
     k_dedup_emit<uint32_t><<<nb, ST, 0, s>>>(kin32, mm, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
-                                             ws.d_nunique, nb, d_occ_map, ws.d_sorted_mapped); ::kp::count_launch();
+                                             ws.d_nunique, nb, d_occ_map, ws.d_sorted_mapped, d_occ_ident); ::kp::count_launch();
   } else {
     const int passes = (bits + 7) / 8;
     uint64_t* ka = ws.keys_a.get<uint64_t>(n);
@@ -631,7 +635,7 @@ static void dedup_sort(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStre
     k_head_count<uint64_t><<<nb, ST, 0, s>>>(kin, n, bcount); ::kp::count_launch();
     k_scan_rows<<<1, ST, 0, s>>>(bcount, nb, ws.d_nunique + 1); ::kp::count_launch();
     k_dedup_emit<uint64_t><<<nb, ST, 0, s>>>(kin, mm, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
-                                             ws.d_nunique, nb, d_occ_map, ws.d_sorted_mapped); ::kp::count_launch();
+                                             ws.d_nunique, nb, d_occ_map, ws.d_sorted_mapped, d_occ_ident); ::kp::count_launch();
   }
 }
 
@@ -658,7 +662,7 @@ static bool spec_enabled() {
 }
 
 void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
-           const uint32_t* d_occ_map) {
+           const uint32_t* d_occ_map, const uint32_t* d_occ_ident) {
   ws.n = n;
   ws.d_nunique = ws.scalars.get<uint32_t>(4);
   if (n == 0) {
@@ -679,7 +683,7 @@ void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
     // the final readback (one host sync per dedup instead of two); a batch
     // whose span outgrows the plan is sorted again with the exact plan.
     const int planned = ws.spec_bits;
-    dedup_sort(d_keys, n, ws, s, d_occ_map, planned, mm, nb);
+    dedup_sort(d_keys, n, ws, s, d_occ_map, d_occ_ident, planned, mm, nb);
     unsigned long long h_mm[2];
     KP_CUDA(cudaMemcpyAsync(h_mm, mm, 16, cudaMemcpyDeviceToHost, s));
     KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
@@ -687,7 +691,7 @@ void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
     const int bits = span_bits(h_mm);
     ws.spec_bits = bits;
     if (plan_covers(planned, bits)) return;
-    dedup_sort(d_keys, n, ws, s, d_occ_map, bits, mm, nb);
+    dedup_sort(d_keys, n, ws, s, d_occ_map, d_occ_ident, bits, mm, nb);
     KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
     KP_CUDA(cudaStreamSynchronize(s));
     return;
@@ -697,7 +701,7 @@ void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
   KP_CUDA(cudaStreamSynchronize(s));
   const int bits = span_bits(h_mm);
   ws.spec_bits = bits;
-  dedup_sort(d_keys, n, ws, s, d_occ_map, bits, mm, nb);
+  dedup_sort(d_keys, n, ws, s, d_occ_map, d_occ_ident, bits, mm, nb);
   KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaStreamSynchronize(s));
 }
@@ -767,7 +771,7 @@ void dedup_runs(const uint64_t* d_keys, uint32_t n, const std::vector<uint64_t>&
   k_head_count<uint64_t><<<nb, ST, 0, s>>>(kin, n, bcount); ::kp::count_launch();
   k_scan_rows<<<1, ST, 0, s>>>(bcount, nb, ws.d_nunique + 1); ::kp::count_launch();
   k_dedup_emit<uint64_t><<<nb, ST, 0, s>>>(kin, mm, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
-                                           ws.d_nunique, nb, nullptr, nullptr); ::kp::count_launch();
+                                           ws.d_nunique, nb, nullptr, nullptr, nullptr); ::kp::count_launch();
   KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaStreamSynchronize(s));
 }
