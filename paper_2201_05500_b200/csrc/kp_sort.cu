@@ -147,14 +147,17 @@ __global__ void __launch_bounds__(ST) k_upsweep(const KIN* __restrict__ keys, ui
   __syncthreads();
   const uint64_t kmin = mm[0];
   const uint32_t base = blockIdx.x * TILE;
-  const int lane = threadIdx.x & 31;
+  // counts only (no ranks): one shared-memory atomic per item; integer adds,
+  // so the histogram is exact whatever order they land in
+  uint32_t d[IPT];
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     const uint32_t idx = base + r * ST + threadIdx.x;
-    const uint32_t d = idx < n ? digit_of<KIN>(keys[idx], kmin, shift, R - 1) : R;
-    const uint32_t peers = match_digit<R>(d);
-    if (d < R && lane == __ffs(peers) - 1) atomicAdd(&hist[d], __popc(peers));
+    d[r] = idx < n ? digit_of<KIN>(keys[idx], kmin, shift, R - 1) : R;
   }
+#pragma unroll
+  for (int r = 0; r < IPT; ++r)
+    if (d[r] < R) atomicAdd(&hist[d[r]], 1u);
   __syncthreads();
   for (int i = threadIdx.x; i < R; i += ST) counts[i * nb + blockIdx.x] = hist[i];
 }
