@@ -242,7 +242,7 @@ __device__ __forceinline__ void scan_digits(const uint32_t* in, uint32_t* out, u
 // One LSD pass. KIN -> KOUT: u64 -> u64 (raw keys), u64 -> u32 (first pass of
 // the narrow mode: keys become key - kmin), u32 -> u32.
 template <typename KIN, typename KOUT, int R>
-__global__ void __launch_bounds__(ST) k_downsweep(
+__global__ void __launch_bounds__(ST, 4) k_downsweep(
     const KIN* __restrict__ kin, const uint32_t* __restrict__ vin, KOUT* __restrict__ kout,
     uint32_t* __restrict__ vout, uint32_t n, const unsigned long long* __restrict__ mm, int shift,
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ totals, uint32_t nb) {
