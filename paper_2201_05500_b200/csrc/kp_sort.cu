@@ -124,13 +124,19 @@ __device__ __forceinline__ uint32_t digit_of(KIN k, uint64_t kmin, int shift, ui
 // lanes holding the same digit d in [0, R] (R = invalid): one ballot per
 // digit bit instead of MATCH.ANY (which issues through the MIO queue and
 // dominated the rank loop's stalls)
+// (full: no lane holds R -- a full tile -- so the validity bit is skipped)
 template <int R>
-__device__ __forceinline__ uint32_t match_digit(uint32_t d) {
-  constexpr int BITS = (R == 256 ? 8 : R == 512 ? 9 : 16) + 1;
+__device__ __forceinline__ uint32_t match_digit(uint32_t d, bool full = false) {
+  constexpr int BITS = R == 256 ? 8 : R == 512 ? 9 : 16;
   uint32_t peers = 0xffffffffu;
 #pragma unroll
   for (int b = 0; b < BITS; ++b) {
     const bool on = (d >> b) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, on);
+    peers &= on ? bal : ~bal;
+  }
+  if (!full) {
+    const bool on = (d >> BITS) & 1u;
     const uint32_t bal = __ballot_sync(0xffffffffu, on);
     peers &= on ? bal : ~bal;
   }
@@ -262,6 +268,7 @@ __global__ void __launch_bounds__(ST, 4) k_downsweep(
   const uint64_t kmin = mm[0];
   const uint32_t base = blockIdx.x * TILE;
   const uint32_t tile_n = min((uint32_t)TILE, n - base);
+  const bool full = tile_n == (uint32_t)TILE;
   const uint32_t lt = lanemask_lt();
   KOUT k[IPT];
   uint32_t v[IPT], d[IPT], rw[IPT];
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__(ST, 4) k_downsweep(
   }
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
-    const uint32_t peers = match_digit<R>(d[r]);
+    const uint32_t peers = match_digit<R>(d[r], full);
     const bool leader = lane == __ffs(peers) - 1;
     uint32_t before = 0;
     if (d[r] < R) before = s_wh[d[r] * NW + warp];
