@@ -1051,6 +1051,7 @@ __global__ void k_split_h(const float* __restrict__ w, int K, int ld, __half* __
   __shared__ float red[32];
   const float* row = w + (size_t)blockIdx.x * ld;
   float mx = 0.f;
+#pragma unroll 4
   for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, fabsf(row[k]));
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -1066,6 +1067,7 @@ __global__ void k_split_h(const float* __restrict__ w, int K, int ld, __half* __
   const int e = row_exp(red[0]);
   if (threadIdx.x == 0) exps[blockIdx.x] = e;
   const float sc = pow2f(e);
+#pragma unroll 4
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     const float x = __fmul_rn(row[k], sc);
     const __half h = __float2half_rn(x);
@@ -1310,7 +1312,9 @@ void tc_gemm_nt_h(int M, int N, int K, const float* A, int lda, const float* a_r
   }
 }
 void split_h(const float* W, int N, int K, int ld, __half* hi, __half* lo, int* exps, cudaStream_t s) {
-  k_split_h<<<N, 256, 0, s>>>(W, K, ld, hi, lo, exps); ::kp::count_launch();
+  // one block per row; long rows (the 6400-wide W1) get 1024 threads so the
+  // 256-row grid keeps enough loads in flight
+  k_split_h<<<N, K >= 4096 ? 1024 : 256, 0, s>>>(W, K, ld, hi, lo, exps); ::kp::count_launch();
 }
 void rowmax(const float* A, int M, int K, int lda, float* out, cudaStream_t s) {
   k_rowmax<<<std::min<unsigned>(ceil_div((uint64_t)M * 32, 256), 148 * 16), 256, 0, s>>>(A, M, K, lda, out); ::kp::count_launch();
