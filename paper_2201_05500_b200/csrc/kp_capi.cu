@@ -293,6 +293,10 @@ void exchange_chunks(kp_comm* comm, cudaStream_t s, uint32_t W, uint64_t D, uint
 void merge_states(kp_comm* comm, cudaStream_t s, uint32_t W, uint64_t D, float* x, float* m,
                   float* v, float* vbar, float alpha, bool reset, MergeWs& ws) {
   const bool local = !comm || comm->world == 1;
+  if (local && W == 1) {
+    merge_single(x, m, v, vbar, D, alpha, reset, s);
+    return;
+  }
   float* vb = ws.cm.get<float>(D);
   float* terms = ws.terms.get<float>((size_t)W * D);
   // small models / few ranks: one allgather per round beats the three-step

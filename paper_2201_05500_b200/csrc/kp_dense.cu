@@ -72,6 +72,23 @@ __global__ void k_terms(const float* __restrict__ x, const float* __restrict__ m
     out[j] = __fsub_rn(x[j], __fdiv_rn(__fmul_rn(alpha, m[j]), __fsqrt_rn(vbar[j])));
 }
 
+// One worker on one rank: the whole merge in one pass, the same expression
+// tree as k_cmean (n = 1) -> k_terms -> k_cmean (n = 1) -> copies, so the
+// result is bitwise the general path's (including x = -0 -> +0).
+__global__ void k_merge_single(float* __restrict__ x, const float* __restrict__ m,
+                               float* __restrict__ v, float* __restrict__ vbar, uint64_t D,
+                               float alpha, int reset) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < D;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const float vj = v[j];
+    const float vb = __fadd_rn(vj, __fdiv_rn(__fadd_rn(0.f, __fsub_rn(vj, vj)), 1.f));
+    const float t = __fsub_rn(x[j], __fdiv_rn(__fmul_rn(alpha, m[j]), __fsqrt_rn(vb)));
+    x[j] = __fadd_rn(t, __fdiv_rn(__fadd_rn(0.f, __fsub_rn(t, t)), 1.f));
+    vbar[j] = vb;
+    if (reset) v[j] = vb;
+  }
+}
+
 // bit 0: non-finite x or v; bit 1: v or v_bar lost positivity (optimizer.cpp:135-142)
 __global__ void k_check(const float* __restrict__ v, const float* __restrict__ vbar,
                         const float* __restrict__ x, uint64_t D, uint32_t* flag) {
@@ -97,6 +114,10 @@ void dense_moments(float* m, float* v, const float* g, uint64_t D, const AdamPar
 void centered_mean(const float* vecs, uint64_t stride, uint32_t n, uint64_t D, float* out,
                    cudaStream_t s) {
   k_cmean<<<grid_for(D), 256, 0, s>>>(vecs, stride, n, D, out); ::kp::count_launch();
+}
+void merge_single(float* x, const float* m, float* v, float* vbar, uint64_t D, float alpha,
+                  bool reset, cudaStream_t s) {
+  k_merge_single<<<grid_for(D), 256, 0, s>>>(x, m, v, vbar, D, alpha, reset ? 1 : 0); ::kp::count_launch();
 }
 void merge_terms(const float* x, const float* m, const float* vbar, uint64_t D, float alpha,
                  float* out, cudaStream_t s) {

@@ -259,6 +259,9 @@ void dense_moments(float* m, float* v, const float* g, uint64_t D, const AdamPar
 // out[j] = centered mean over n vectors at vecs + i*stride (ascending i)
 void centered_mean(const float* vecs, uint64_t stride, uint32_t n, uint64_t D, float* out,
                    cudaStream_t s);
+// local merge of a single worker (W = 1, one rank), fused; bitwise the general path
+void merge_single(float* x, const float* m, float* v, float* vbar, uint64_t D, float alpha,
+                  bool reset, cudaStream_t s);
 void merge_terms(const float* x, const float* m, const float* vbar, uint64_t D, float alpha,
                  float* out, cudaStream_t s);
 void dense_check(const float* v, const float* vbar, const float* x, uint64_t D, uint32_t* d_flag,
