@@ -54,7 +54,39 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=4096, help="instances for the CPU baseline")
+    p.add_argument("--ref-slice", type=int, default=1024,
+                   help="reference arm: instances per host thread per step")
+    p.add_argument("--ref-full-batch", type=int, default=1,
+                   help="reference arm: also time one whole folded batch on one core")
     return p.parse_args()
+
+
+def load_data_module():
+    """paper_2201_05500_b200/data.py (numpy only) loaded by path, so the
+    reference arm never runs the package __init__ (which maps this repo's
+    CUDA libraries into the process)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_kp_data", os.path.join(ROOT, "paper_2201_05500_b200", "data.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def repo_so_loaded():
+    """Shared objects under this repo mapped into the process (the reference
+    arm must show only oracle/_ref/*)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                path = line.split()[-1] if line.strip() else ""
+                if path.endswith(".so") or ".so." in path:
+                    if os.path.realpath(path).startswith(os.path.realpath(ROOT)):
+                        out.add(os.path.relpath(os.path.realpath(path), os.path.realpath(ROOT)))
+    except OSError:
+        pass
+    return sorted(out)
 
 
 def load_json(path):
@@ -177,21 +209,21 @@ def run_reference(args, rank):
     if rank != 0:
         return
     from oracle import oracle as O
-    from paper_2201_05500_b200.data import make_batch
     import tempfile
+    make_batch = load_data_module().make_batch
     cores = len(os.sched_getaffinity(0))
-    per = 96  # instances per thread per step (~0.1 s of reference work each)
-    need = cores * per * (args.steps + args.warmup)
+    need = cores * args.ref_slice * (args.steps + args.warmup)
     bt = make_batch(min(need, args.batch), V=args.vocab, zipf_s=args.zipf, n_slots=args.slots, seed=1000)
     fb = bt.folded()
+    per = min(args.ref_slice, fb.n)  # instances per thread per step
     hidden = tuple(int(h) for h in args.hidden.split(",") if h)
-    cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=1 << 30, embedding_dim=args.dim,
-                       hidden=hidden, alpha=0.01, sparse_lr=0.05)
-    refs = [O.Ref(cfg, tempfile.mkdtemp(prefix="kpref_")) for _ in range(cores)]
+    rcfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=1 << 30, embedding_dim=args.dim,
+                        hidden=hidden, alpha=0.01, sparse_lr=0.05)
+    refs = [O.Ref(rcfg, tempfile.mkdtemp(prefix="kpref_")) for _ in range(cores)]
     cursor = [0]
 
     def slice_for(i, step):
-        lo = ((step * cores + i) * per) % max(fb.n - per, 1)
+        lo = ((step * cores + i) * per) % max(fb.n - per + 1, 1)
         return fb.slice(lo, lo + per)
 
     def one_step(step):
@@ -211,17 +243,38 @@ def run_reference(args, rank):
         one_step(args.warmup + k)
     dt = time.perf_counter() - t0
     value = cores * per * args.steps / dt
+    ref_model = f"[{args.dim}->{args.hidden.replace(',', '->')}->1]"
     sample = (f"{per} instances x {cores} threads per step, each thread an independent reference "
-              f"Trainer (N=1,k=1) on the {workload_config(args, max(1, args.gpus))['workload'].split(':')[0]} batch "
-              f"folded to S=1 (reference semantics: "
-              f"model [{args.dim}->{args.hidden.replace(',', '->')}->1])")
+              f"Trainer (N=1,k=1) on its own slice of the "
+              f"{workload_config(args, max(1, args.gpus))['workload'].split(':')[0]} batch "
+              f"folded to S=1 (the reference model: one pooled vector per instance, {ref_model})")
+    # what this arm ran: the reference cannot express S slots (model.cpp:88-99),
+    # so the same batches are folded to its S=1 model
+    cfg = workload_config(args, max(1, args.gpus))
+    cfg.update({"slots": f"1 (the batch's {args.slots} slot features folded into one deduped feature set "
+                         "per instance, the reference's Instance semantics)",
+                "mlp": ref_model, "parallelism": f"{cores} host threads, one reference Trainer each"})
+    full = None
+    if args.ref_full_batch:
+        # one core, one whole folded batch (the reference is single-threaded):
+        # the stated baseline beside the many-thread sample figure
+        n_full = min(args.batch, fb.n)
+        rf = O.Ref(rcfg, tempfile.mkdtemp(prefix="kpref_full_"))
+        t1 = time.perf_counter()
+        rf.batch(fb.offs[:n_full + 1], fb.keys[:fb.offs[n_full]], fb.labels[:n_full])
+        d1 = time.perf_counter() - t1
+        full = {"value": n_full / d1, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"one Trainer::train_batch over {n_full} instances (the folded batch), "
+                          f"single-threaded"}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic Zipf(1.1) CTR", "config": workload_config(args, max(1, args.gpus)),
+        "data": "synthetic Zipf(1.1) CTR", "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
+        "cpu_baseline_1core_full_batch": full,
+        "repo_so_loaded": repo_so_loaded(),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -428,26 +481,28 @@ def main():
     dom = max(stages, key=lambda k: stages[k]["ms_per_step"])
     traffic = ncu_traffic()
     if dom == "mlp":
-        # Tensor work per step, in bf16-rate units. Every fp32 multiply-add is
-        # three MMAs: the first layer's forward and input-gradient GEMMs run
-        # them on fp16 operands (per-row scaled hi/lo, f16 = bf16 rate), the
-        # rest on tf32 (half the bf16 rate, so each tf32 MMA counts twice).
+        # achieved = the model's ALGORITHMIC fp32 flops (6 B sum in*out) over
+        # the stage time, against the bf16 tensor peak. The fp32-accurate
+        # emulation issues 3 MMAs per fp32 multiply-add (3xFP16 on the first
+        # layer's forward and input-gradient GEMMs, 3xTF32 elsewhere, a tf32
+        # MMA at half the bf16 rate); that pipe work is reported beside it.
         h_on = os.environ.get("KP_GEMM_F16", "1") != "0" and D_in % 8 == 0
         f_l1 = 2.0 * B * D_in * hidden[0]                       # one first-layer GEMM
-        # fp16 path: layer-1 forward and layer-1 input gradient (dX)
-        f16_flops = 2 * f_l1 if h_on else 0.0
+        f16_flops = 2 * f_l1 if h_on else 0.0  # layer-1 forward + input gradient
         tf32_flops = flops - f16_flops
         work = 3.0 * f16_flops + 2 * 3.0 * tf32_flops            # bf16-equivalent MMA flops
         sec = stages["mlp"]["ms_per_step"] / 1e3
-        tc = work / sec / 1e12
-        roof = {"kernel": "mlp stage: tcgen05 GEMMs (layer-1 fwd + dX: 3xFP16 scaled; dW and layer 2: "
-                          "3xTF32) + head/bias kernels",
-                "bound": "tensor", "achieved": tc, "peak": bf16s, "unit": "TFLOP/s",
-                "frac": tc / bf16s, "traffic": traffic.get("mlp"),
-                "peak_kind": f"{pk} bf16 sustained",
-                "achieved_kind": "bf16-rate-equivalent MMA work / stage time: 3 f16 MMAs per fp32 FMA "
-                                 "(layer-1 fwd, dX), 3 tf32 MMAs = 6 bf16-equivalent otherwise",
-                "fp32_model_tflops": stages["mlp"]["achieved_tflops"],
+        alg = flops / sec / 1e12
+        roof = {"kernel": "mlp stage: tcgen05 GEMMs (3xFP16 per-row scaled on the 6400-wide first "
+                          "layer, 3xTF32 on the rest) + head/bias kernels",
+                "bound": "tensor", "achieved": alg, "peak": bf16s, "unit": "TFLOP/s",
+                "frac": alg / bf16s, "traffic": traffic.get("mlp"),
+                "peak_kind": f"{pk} bf16 dense sustained",
+                "achieved_kind": "algorithmic fp32 model flops (6 B sum in*out) / stage time",
+                "mma_work_tflops": work / sec / 1e12,
+                "mma_work_frac": work / sec / 1e12 / bf16s,
+                "mma_work_kind": "bf16-rate-equivalent MMA work / stage time: 3 f16 MMAs per fp32 "
+                                 "FMA on the fp16 GEMMs, 3 tf32 MMAs = 6 bf16-equivalent otherwise",
                 "mma_work_tflop_per_step": work / 1e12,
                 "cublas_tf32_tflops_8192": cublas_tf32()}
     else:

@@ -368,3 +368,39 @@ def ref_auc(scores, labels):
     f.restype = C.c_double
     f.argtypes = [_f64p, _i32p, C.c_uint64]
     return f(np.ascontiguousarray(scores, np.float64), np.ascontiguousarray(labels, np.int32), len(scores))
+
+
+def _ref_csr(fn, *args):
+    """Two-call CSR export from the compiled reference (sizes, then data)."""
+    n, nnz = C.c_uint64(), C.c_uint64()
+    if fn(*args, None, None, None, C.byref(n), C.byref(nnz)):
+        raise RuntimeError(ref_fn("ref_last_error")().decode())
+    offs = np.zeros(n.value + 1, np.uint64)
+    keys = np.zeros(max(nnz.value, 1), np.uint64)
+    labels = np.zeros(max(n.value, 1), np.int32)
+    if fn(*args, offs.ctypes.data_as(C.c_void_p), keys.ctypes.data_as(C.c_void_p),
+          labels.ctypes.data_as(C.c_void_p), C.byref(n), C.byref(nnz)):
+        raise RuntimeError(ref_fn("ref_last_error")().decode())
+    return offs, keys[:nnz.value], labels[:n.value]
+
+
+def ref_synthetic(seed=42, n_instances=100000, vocab=10000, nnz_mean=10.0, signal_scale=4.0):
+    """The reference's SyntheticCtr stream (proj/src/data.cpp:11-57) as CSR
+    (offs u64[n+1], keys u64[nnz], labels i32[n]) -- the desk benchmark's
+    data when called with ExperimentConfig::defaults() (config.hpp:18-30)."""
+    f = ref_fn("ref_synthetic")
+    f.restype = C.c_int
+    f.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_double] + [C.c_void_p] * 3 + \
+        [C.POINTER(C.c_uint64)] * 2
+    ref_fn("ref_last_error").restype = C.c_char_p
+    return _ref_csr(f, seed, n_instances, vocab, nnz_mean, signal_scale)
+
+
+def ref_read_instances(path):
+    """read_instances (proj/src/data.cpp:72-110) through the compiled reference;
+    raises RuntimeError with the reference's message on a malformed file."""
+    f = ref_fn("ref_read_instances")
+    f.restype = C.c_int
+    f.argtypes = [C.c_char_p] + [C.c_void_p] * 3 + [C.POINTER(C.c_uint64)] * 2
+    ref_fn("ref_last_error").restype = C.c_char_p
+    return _ref_csr(f, str(path).encode())

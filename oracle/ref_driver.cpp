@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "kpsim/data.hpp"
 #include "kpsim/eval.hpp"
 #include "kpsim/model.hpp"
 #include "kpsim/optimizer.hpp"
@@ -266,6 +267,58 @@ double ref_auc(const double* scores, const int32_t* labels, uint64_t n) {
   std::vector<int> l(labels, labels + n);
   const auto a = compute_auc(std::span<const double>(scores, n), l);
   return a ? *a : std::nan("");
+}
+
+// The reference's own synthetic CTR stream (SyntheticCtr, proj/src/data.cpp:11-57,
+// resolved from ExperimentConfig as in proj/src/experiment.cpp:35-44), flattened
+// to CSR in stream order. Call with offs == NULL to size: *n_out instances,
+// *nnz_out feature ids.
+int ref_synthetic(uint64_t seed, uint64_t n_instances, uint64_t vocab, double nnz_mean,
+                  double signal_scale, uint64_t* offs, uint64_t* keys, int32_t* labels,
+                  uint64_t* n_out, uint64_t* nnz_out) {
+  return guard([&] {
+    SyntheticSpec spec;
+    spec.seed = seed;
+    spec.n_instances = n_instances;
+    spec.vocab = vocab;
+    spec.nnz_mean = nnz_mean;
+    spec.signal_scale = signal_scale;
+    SyntheticCtr gen(spec);
+    uint64_t o = 0;
+    for (uint64_t i = 0; i < n_instances; ++i) {
+      const Instance inst = gen.next();
+      if (offs) {
+        offs[i] = o;
+        std::memcpy(keys + o, inst.feature_ids.data(), inst.feature_ids.size() * 8);
+        labels[i] = inst.label;
+      }
+      o += inst.feature_ids.size();
+    }
+    if (offs) offs[n_instances] = o;
+    *n_out = n_instances;
+    *nnz_out = o;
+  });
+}
+
+// read_instances (proj/src/data.cpp:72-110) on a TSV file, flattened to CSR.
+// Same two-call sizing protocol as ref_synthetic.
+int ref_read_instances(const char* path, uint64_t* offs, uint64_t* keys, int32_t* labels,
+                       uint64_t* n_out, uint64_t* nnz_out) {
+  return guard([&] {
+    const auto insts = read_instances(path);
+    uint64_t o = 0;
+    for (uint64_t i = 0; i < insts.size(); ++i) {
+      if (offs) {
+        offs[i] = o;
+        std::memcpy(keys + o, insts[i].feature_ids.data(), insts[i].feature_ids.size() * 8);
+        labels[i] = insts[i].label;
+      }
+      o += insts[i].feature_ids.size();
+    }
+    if (offs) offs[insts.size()] = o;
+    *n_out = insts.size();
+    *nnz_out = o;
+  });
 }
 
 }  // extern "C"

@@ -74,6 +74,7 @@ unsigned grid1(uint64_t n) {
 }
 }  // namespace
 
+thread_local const uint32_t* kp::g_abort = nullptr;
 std::atomic<uint64_t> g_launches{0};
 void kp::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
@@ -472,11 +473,14 @@ bool peer_ready(kp_trainer* tr) {
   }
   const size_t row = (size_t)tr->e * 4;
   auto room = [](uint64_t n, size_t b) { return (size_t)((n + n / 4 + 1024) * b); };
-  bool ok = true;
+  // every grow decision below depends only on the shared counts matrix, so
+  // all ranks (re)allocate the same windows; `grew` makes the agreement
+  // collective whenever any window changed, on every rank alike
+  bool ok = true, grew = false;
   if (P.mode == -1) ok = win_alloc(tr, P.flags, 8 * kMaxPeers * 8);
-  if (P.keys.bytes < maxcol * 8) ok = win_alloc(tr, P.keys, room(maxcol, 8)) && ok;
-  if (P.grads.bytes < maxcol * row) ok = win_alloc(tr, P.grads, room(maxcol, row)) && ok;
-  if (P.rows.bytes < maxrow * row) ok = win_alloc(tr, P.rows, room(maxrow, row)) && ok;
+  if (P.keys.bytes < maxcol * 8) ok = win_alloc(tr, P.keys, room(maxcol, 8)) && ok, grew = true;
+  if (P.grads.bytes < maxcol * row) ok = win_alloc(tr, P.grads, room(maxcol, row)) && ok, grew = true;
+  if (P.rows.bytes < maxrow * row) ok = win_alloc(tr, P.rows, room(maxrow, row)) && ok, grew = true;
   const bool first = P.mode == -1;
   if (first) {
     // the k-step merge's windows too, now: a one-time collective setup must
@@ -488,7 +492,7 @@ bool peer_ready(kp_trainer* tr) {
     ok = win_alloc(tr, P.terms, (size_t)W * D * 4) && ok;
     ok = win_alloc(tr, P.vb, (size_t)D * 4) && ok;
   }
-  if (first || !ok) {
+  if (first || grew) {
     P.mode = all_ok(tr, ok) ? 1 : 0;
     if (P.mode == 0)
       for (auto* w : {&P.keys, &P.rows, &P.grads, &P.flags, &P.dv, &P.dx, &P.terms, &P.vb})
@@ -570,10 +574,11 @@ void merge_states_peer(kp_trainer* tr, float alpha, bool reset) {
   peer_cmean(pv, R, W, D, c0, c1, s);
   peer_exchange_sync(tr, 6, true, true);
   float* x = tr->x;
+  // guarded copies (not cudaMemcpy): a timed-out merge must not publish v_bar
   for (uint32_t l = 0; l < W; ++l) {
-    if (l) KP_CUDA(cudaMemcpyAsync(x + l * D, x, D * 4, cudaMemcpyDeviceToDevice, s));
-    KP_CUDA(cudaMemcpyAsync(tr->vbar + l * D, vb, D * 4, cudaMemcpyDeviceToDevice, s));
-    if (reset) KP_CUDA(cudaMemcpyAsync(tr->v + l * D, vb, D * 4, cudaMemcpyDeviceToDevice, s));
+    if (l) dense_copy(x + l * D, x, D, s);
+    dense_copy(tr->vbar + l * D, vb, D, s);
+    if (reset) dense_copy(tr->v + l * D, vb, D, s);
   }
 }
 
@@ -874,7 +879,7 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
   tr->t_global = t;
   uint32_t* chk = static_cast<uint32_t*>(tr->check.p);
   for (uint32_t l = 0; l < tr->W; ++l)
-    dense_check(tr->v + l * D, tr->vbar + l * D, tr->x + l * D, D, chk, s);
+    dense_check(tr->v + l * D, tr->vbar + l * D, tr->x + l * D, D, chk, s, l == 0 ? chk + 1 : nullptr);
   tr->mark(5);
 }
 
@@ -910,11 +915,18 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
   KP_CHECK(h_offs[0] == 0, kErrGeneric, "offs[0] must be 0");
   uint32_t* err = tr->err.get<uint32_t>(4);
   KP_CUDA(cudaMemsetAsync(err, 0xFF, 4, s));
-  KP_CUDA(cudaMemsetAsync(tr->check.get<uint32_t>(1), 0, 4, s));
+  KP_CUDA(cudaMemsetAsync(tr->check.get<uint32_t>(2), 0, 8, s));  // [0] flags [1] steps applied
+  // G > 1: every state-writing kernel of this batch (predict pass included)
+  // checks the peer-timeout bit (kAbortTimeout) of the check word first
+  AbortScope abort_guard(tr->world > 1 ? static_cast<const uint32_t*>(tr->check.p) : nullptr);
   double* d_loss = tr->loss.get<double>(n_mb);
   KP_CUDA(cudaMemsetAsync(d_loss, 0, n_mb * 8, s));
 
-  const bool fused = predict_first && n_mb == 1 && (tr->t_global % tr->cfg.k == 0);
+  // predictions use x_bar (trainer.cpp:141-151); when every replica holds
+  // the same x (initial state, right after a merge, no set_worker_state
+  // since) x_bar IS each worker's x, and the training forward doubles as the
+  // prediction
+  const bool fused = predict_first && n_mb == 1 && tr->x_uniform;
   float* d_pred_keep = nullptr;
   if (predict_first) {
     d_pred_keep = tr->pred_keep.get<float>(std::max<uint32_t>(n, 1));
@@ -932,6 +944,7 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
     }
   }
   const uint64_t steps_before = tr->t_global, merges_before = tr->merges;
+  const bool uniform_before = tr->x_uniform;
   for (uint64_t j = 0; j < n_mb; ++j) {
     StepView sv;
     sv.wlo.resize(W);
@@ -996,9 +1009,10 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
     run_step(tr, sv, d_loss + j, fused && j == 0 ? d_pred_keep : nullptr);
   }
   // error flags, loss, predictions
-  uint32_t h_err = 0, h_chk = 0;
+  uint32_t h_err = 0, h_chkw[2] = {0, 0};
   KP_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, s));
-  KP_CUDA(cudaMemcpyAsync(&h_chk, tr->check.p, 4, cudaMemcpyDeviceToHost, s));
+  KP_CUDA(cudaMemcpyAsync(h_chkw, tr->check.p, 8, cudaMemcpyDeviceToHost, s));
+  const uint32_t h_chk = h_chkw[0];
   std::vector<double> lsum(n_mb);
   KP_CUDA(cudaMemcpyAsync(lsum.data(), d_loss, n_mb * 8, cudaMemcpyDeviceToHost, s));
   if (predict_first && h_preds)
@@ -1013,9 +1027,25 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
                std::to_string(h_err) + ")");
   KP_CHECK(h_sc[2] == 0, kErrTableFull,
            "embedding table full: capacity " + std::to_string(tr->tab.t->capacity) + " rows");
+  if (h_chk & kAbortTimeout) {
+    // the steps before the timed-out one applied their updates, the rest
+    // wrote nothing: roll the host counters back to the applied count
+    const uint64_t applied = h_chkw[1];
+    if (applied < tr->t_global - steps_before) {
+      uint64_t merges = merges_before;
+      for (uint64_t t = steps_before + 1; t <= steps_before + applied; ++t)
+        if (t % tr->cfg.k == 0) ++merges;
+      tr->t_global = steps_before + applied;
+      tr->merges = merges;
+      tr->x_uniform = applied ? (tr->t_global % tr->cfg.k == 0) : uniform_before;
+    }
+  }
+  KP_CHECK(!(h_chk & kAbortTimeout), kErrCuda,
+           "peer exchange timed out waiting for another rank (NVLink window flags, "
+           "KP_PEER_TIMEOUT_S): the timed-out minibatch step and the rest of the batch "
+           "wrote no table or dense state");
   KP_CHECK(!(h_chk & 1), kErrGeneric, "non-finite worker state after step " + std::to_string(tr->t_global));
   KP_CHECK(!(h_chk & 2), kErrGeneric, "second moment lost positivity at step " + std::to_string(tr->t_global));
-  KP_CHECK(!(h_chk & 16), kErrCuda, "peer exchange timed out waiting for another rank (NVLink window flags)");
   // per-step loss = sum_workers loss_i*|mb_i| / sum |mb_i|  (trainer.cpp:177-178,221-223)
   if (tr->world > 1) {
     double* dl = tr->lossg.get<double>((size_t)n_mb * tr->world);
@@ -1561,7 +1591,7 @@ int kp_trainer_create(const kp_trainer_config* cfg, kp_comm* comm, int device, k
     tr->tab.t = table_create(device, c.table_capacity, c.embedding_dim, rule, 0.f,
                              rule == 0 ? 1e-6f : 0.f, rule == 0 ? 0.f : (float)c.sparse_eps);
     tr->tab.s = nullptr;
-    tr->check.get<uint32_t>(1);
+    tr->check.get<uint32_t>(2);
     *out = tr.release();
   });
 }
@@ -1664,7 +1694,8 @@ int kp_trainer_worker_state(kp_trainer* tr, uint32_t l, float* x, float* m, floa
     KP_CHECK(l < tr->W, kErrGeneric, "worker index out of range");
     KP_CUDA(cudaSetDevice(tr->device));
     const uint64_t D = tr->D;
-    if (x) tr->x_uniform = false;
+    // a read-only getter: x_uniform must stay rank-symmetric (it selects a
+    // collective path in compute_xbar), so reading a state never clears it
     if (x) KP_CUDA(cudaMemcpyAsync(x, tr->x + l * D, D * 4, cudaMemcpyDeviceToHost, tr->s));
     if (m) KP_CUDA(cudaMemcpyAsync(m, tr->m + l * D, D * 4, cudaMemcpyDeviceToHost, tr->s));
     if (v) KP_CUDA(cudaMemcpyAsync(v, tr->v + l * D, D * 4, cudaMemcpyDeviceToHost, tr->s));

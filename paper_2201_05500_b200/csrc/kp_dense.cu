@@ -30,7 +30,8 @@ __device__ __forceinline__ void moments(float& m, float& v, float g, float b1, f
 
 __global__ void k_local_step(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
                              const float* __restrict__ vbar, const float* __restrict__ g,
-                             uint64_t D, float alpha, float b1, float b2) {
+                             uint64_t D, float alpha, float b1, float b2, const uint32_t* abort) {
+  if (aborted(abort)) return;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < D;
        j += (uint64_t)gridDim.x * blockDim.x) {
     float mj = m[j], vj = v[j];
@@ -42,7 +43,8 @@ __global__ void k_local_step(float* __restrict__ x, float* __restrict__ m, float
 }
 
 __global__ void k_moments(float* __restrict__ m, float* __restrict__ v, const float* __restrict__ g,
-                          uint64_t D, float b1, float b2) {
+                          uint64_t D, float b1, float b2, const uint32_t* abort) {
+  if (aborted(abort)) return;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < D;
        j += (uint64_t)gridDim.x * blockDim.x) {
     float mj = m[j], vj = v[j];
@@ -54,7 +56,8 @@ __global__ void k_moments(float* __restrict__ m, float* __restrict__ v, const fl
 
 // base + sum_i (v_i - base) / n, ascending i (common.hpp:27-45)
 __global__ void k_cmean(const float* __restrict__ vecs, uint64_t stride, uint32_t n, uint64_t D,
-                        float* __restrict__ out) {
+                        float* __restrict__ out, const uint32_t* abort) {
+  if (aborted(abort)) return;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < D;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const float base = vecs[j];
@@ -66,7 +69,8 @@ __global__ void k_cmean(const float* __restrict__ vecs, uint64_t stride, uint32_
 
 __global__ void k_terms(const float* __restrict__ x, const float* __restrict__ m,
                         const float* __restrict__ vbar, uint64_t D, float alpha,
-                        float* __restrict__ out) {
+                        float* __restrict__ out, const uint32_t* abort) {
+  if (aborted(abort)) return;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < D;
        j += (uint64_t)gridDim.x * blockDim.x)
     out[j] = __fsub_rn(x[j], __fdiv_rn(__fmul_rn(alpha, m[j]), __fsqrt_rn(vbar[j])));
@@ -77,7 +81,8 @@ __global__ void k_terms(const float* __restrict__ x, const float* __restrict__ m
 // result is bitwise the general path's (including x = -0 -> +0).
 __global__ void k_merge_single(float* __restrict__ x, const float* __restrict__ m,
                                float* __restrict__ v, float* __restrict__ vbar, uint64_t D,
-                               float alpha, int reset) {
+                               float alpha, int reset, const uint32_t* abort) {
+  if (aborted(abort)) return;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < D;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const float vj = v[j];
@@ -89,9 +94,21 @@ __global__ void k_merge_single(float* __restrict__ x, const float* __restrict__ 
   }
 }
 
+__global__ void k_copy(float* __restrict__ dst, const float* __restrict__ src, uint64_t D,
+                       const uint32_t* abort) {
+  if (aborted(abort)) return;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < D;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    dst[j] = src[j];
+}
+
 // bit 0: non-finite x or v; bit 1: v or v_bar lost positivity (optimizer.cpp:135-142)
+// done (nullable): +1 once per call unless the step was aborted -- the count
+// of steps that applied their updates (the host rolls its counters back to it)
 __global__ void k_check(const float* __restrict__ v, const float* __restrict__ vbar,
-                        const float* __restrict__ x, uint64_t D, uint32_t* flag) {
+                        const float* __restrict__ x, uint64_t D, uint32_t* flag, uint32_t* done,
+                        const uint32_t* abort) {
+  if (done && blockIdx.x == 0 && threadIdx.x == 0 && !aborted(abort)) atomicAdd(done, 1u);
   uint32_t f = 0;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < D;
        j += (uint64_t)gridDim.x * blockDim.x) {
@@ -105,27 +122,30 @@ __global__ void k_check(const float* __restrict__ v, const float* __restrict__ v
 
 void dense_local_step(float* x, float* m, float* v, const float* vbar, const float* g, uint64_t D,
                       const AdamParams& h, cudaStream_t s) {
-  k_local_step<<<grid_for(D), 256, 0, s>>>(x, m, v, vbar, g, D, h.alpha, h.beta1, h.beta2); ::kp::count_launch();
+  k_local_step<<<grid_for(D), 256, 0, s>>>(x, m, v, vbar, g, D, h.alpha, h.beta1, h.beta2, g_abort); ::kp::count_launch();
 }
 void dense_moments(float* m, float* v, const float* g, uint64_t D, const AdamParams& h,
                    cudaStream_t s) {
-  k_moments<<<grid_for(D), 256, 0, s>>>(m, v, g, D, h.beta1, h.beta2); ::kp::count_launch();
+  k_moments<<<grid_for(D), 256, 0, s>>>(m, v, g, D, h.beta1, h.beta2, g_abort); ::kp::count_launch();
 }
 void centered_mean(const float* vecs, uint64_t stride, uint32_t n, uint64_t D, float* out,
                    cudaStream_t s) {
-  k_cmean<<<grid_for(D), 256, 0, s>>>(vecs, stride, n, D, out); ::kp::count_launch();
+  k_cmean<<<grid_for(D), 256, 0, s>>>(vecs, stride, n, D, out, g_abort); ::kp::count_launch();
 }
 void merge_single(float* x, const float* m, float* v, float* vbar, uint64_t D, float alpha,
                   bool reset, cudaStream_t s) {
-  k_merge_single<<<grid_for(D), 256, 0, s>>>(x, m, v, vbar, D, alpha, reset ? 1 : 0); ::kp::count_launch();
+  k_merge_single<<<grid_for(D), 256, 0, s>>>(x, m, v, vbar, D, alpha, reset ? 1 : 0, g_abort); ::kp::count_launch();
 }
 void merge_terms(const float* x, const float* m, const float* vbar, uint64_t D, float alpha,
                  float* out, cudaStream_t s) {
-  k_terms<<<grid_for(D), 256, 0, s>>>(x, m, vbar, D, alpha, out); ::kp::count_launch();
+  k_terms<<<grid_for(D), 256, 0, s>>>(x, m, vbar, D, alpha, out, g_abort); ::kp::count_launch();
+}
+void dense_copy(float* dst, const float* src, uint64_t D, cudaStream_t s) {
+  k_copy<<<grid_for(D), 256, 0, s>>>(dst, src, D, g_abort); ::kp::count_launch();
 }
 void dense_check(const float* v, const float* vbar, const float* x, uint64_t D, uint32_t* d_flag,
-                 cudaStream_t s) {
-  k_check<<<grid_for(D), 256, 0, s>>>(v, vbar, x, D, d_flag); ::kp::count_launch();
+                 cudaStream_t s, uint32_t* d_done) {
+  k_check<<<grid_for(D), 256, 0, s>>>(v, vbar, x, D, d_flag, d_done, g_abort); ::kp::count_launch();
 }
 
 uint64_t splitmix64_host(uint64_t x) {

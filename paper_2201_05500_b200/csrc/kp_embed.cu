@@ -372,6 +372,7 @@ __device__ __forceinline__ void sum_range(const SegArgs& a, uint32_t p, uint32_t
 // Phase 1: one group per chunk of CH sorted positions.
 template <int LPG, int NV, bool V4>
 __global__ void __launch_bounds__(256, 6) k_seg_chunks(SegArgs a, TView t) {
+  if (aborted(t.abort)) return;  // no row updates after a peer timeout
   const int gl = threadIdx.x % LPG;
   const uint32_t nchunks = (a.n_pos + a.CH - 1) / a.CH;
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
@@ -469,6 +470,7 @@ __global__ void k_chunk_first(const uint32_t* __restrict__ seg, uint32_t U, uint
 template <int LPG, int NV, bool V4>
 __global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t, const float* __restrict__ Q,
                                                  const float* __restrict__ Q2) {
+  if (aborted(t.abort)) return;
   const int gl = threadIdx.x % LPG;
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
   const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;

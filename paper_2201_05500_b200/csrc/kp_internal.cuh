@@ -10,6 +10,25 @@
 
 namespace kp {
 
+// ------------------------------------------------------------- abort -----
+// Peer-exchange timeout guard (G > 1). k_wait sets kAbortTimeout in the
+// trainer's device check word when a peer's flag never arrives; every kernel
+// that writes PERSISTENT state (table inserts and row updates, dense x/m/v/
+// v_bar, the merge) reads the word at entry and returns without writing, so
+// a timed-out step leaves the table and the dense state exactly as they were
+// before the wait (stream order makes k_wait's store visible to every later
+// kernel). g_abort is the word for the kernels launched on this host thread
+// (nullptr: no guard, single GPU); set it with AbortScope.
+constexpr uint32_t kAbortTimeout = 16u;
+extern thread_local const uint32_t* g_abort;
+struct AbortScope {
+  explicit AbortScope(const uint32_t* p) { g_abort = p; }
+  ~AbortScope() { g_abort = nullptr; }
+};
+__device__ __forceinline__ bool aborted(const uint32_t* a) {
+  return a != nullptr && (*reinterpret_cast<const volatile uint32_t*>(a) & kAbortTimeout);
+}
+
 // ------------------------------------------------------------- dedup ----
 // Workspace for one dedup: sorted (key, occurrence) pairs, unique keys,
 // inverse index and segment starts. All device memory, grown on demand.
@@ -265,7 +284,9 @@ void merge_single(float* x, const float* m, float* v, float* vbar, uint64_t D, f
 void merge_terms(const float* x, const float* m, const float* vbar, uint64_t D, float alpha,
                  float* out, cudaStream_t s);
 void dense_check(const float* v, const float* vbar, const float* x, uint64_t D, uint32_t* d_flag,
-                 cudaStream_t s);
+                 cudaStream_t s, uint32_t* d_done = nullptr);
+// dst = src (D floats), skipped when the step was aborted (g_abort)
+void dense_copy(float* dst, const float* src, uint64_t D, cudaStream_t s);
 
 // ---------------------------------------------------------------- AUC ----
 struct AucWs {

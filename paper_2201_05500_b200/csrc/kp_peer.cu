@@ -14,6 +14,8 @@
 // Completion is a per-(phase, source) sequence flag written with a
 // system-scope release after the data; the consumer spins on its own flags
 // (bounded, error bit instead of a hang) before reading the window.
+#include <cstdlib>
+
 #include "kp_internal.cuh"
 
 namespace kp {
@@ -57,14 +59,25 @@ __global__ void k_signal(PeerFlags f, int R, uint64_t seq) {
   __threadfence_system();
 }
 
-__global__ void k_wait(const uint64_t* flags, int R, uint64_t seq, uint32_t* err) {
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until every peer's flag reached seq. A peer that never signals (gone,
+// or slower than timeout_ns of wall time -- KP_PEER_TIMEOUT_S, default 120 s)
+// sets kAbortTimeout in *err instead of hanging the stream: every later
+// state-writing kernel of the step then returns without writing (aborted()),
+// and the host raises at the batch-end readback.
+__global__ void k_wait(const uint64_t* flags, int R, uint64_t seq, uint32_t* err, uint64_t timeout_ns) {
   const int p = threadIdx.x;
   if (p < R) {
     const volatile unsigned long long* q = reinterpret_cast<const volatile unsigned long long*>(flags + p);
-    const long long t0 = clock64();
+    const uint64_t t0 = globaltimer_ns();
     while (*q < seq) {
-      if (clock64() - t0 > 8000000000ll) {  // ~4 s at 2 GHz: a peer is gone
-        atomicOr(err, 16u);
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        atomicOr(err, kAbortTimeout);
         break;
       }
       __nanosleep(256);
@@ -77,7 +90,9 @@ __global__ void k_wait(const uint64_t* flags, int R, uint64_t seq, uint32_t* err
 // worker i = (rank p, local l) at src[p] + l*D (remote loads over NVLink),
 // result stored into dst[p] of every rank (remote stores). Same expression
 // tree and worker order as k_cmean (common.hpp:27-45).
-__global__ void k_cmean_peer(PeerVecs pv, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1) {
+__global__ void k_cmean_peer(PeerVecs pv, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1,
+                             const uint32_t* abort) {
+  if (aborted(abort)) return;
   const float n = (float)(R * W);
   for (uint64_t j = c0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < c1;
        j += (uint64_t)gridDim.x * blockDim.x) {
@@ -98,7 +113,7 @@ __global__ void k_cmean_peer(PeerVecs pv, int R, uint32_t W, uint64_t D, uint64_
 void peer_cmean(const PeerVecs& pv, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1,
                 cudaStream_t s) {
   if (c1 <= c0) return;
-  k_cmean_peer<<<(unsigned)std::min<uint64_t>((c1 - c0 + 255) / 256, 148 * 8), 256, 0, s>>>(pv, R, W, D, c0, c1); ::kp::count_launch();
+  k_cmean_peer<<<(unsigned)std::min<uint64_t>((c1 - c0 + 255) / 256, 148 * 8), 256, 0, s>>>(pv, R, W, D, c0, c1, g_abort); ::kp::count_launch();
 }
 
 void peer_send_keys(const uint64_t* d_unique, const uint32_t* d_perm, uint32_t n, const PeerMap& pm,
@@ -120,7 +135,12 @@ void peer_signal(const PeerFlags& f, int R, uint64_t seq, cudaStream_t s) {
 }
 
 void peer_wait(const uint64_t* d_my_flags, int R, uint64_t seq, uint32_t* d_err, cudaStream_t s) {
-  k_wait<<<1, 32, 0, s>>>(d_my_flags, R, seq, d_err); ::kp::count_launch();
+  static const uint64_t timeout_ns = [] {
+    const char* e = getenv("KP_PEER_TIMEOUT_S");
+    const double sec = e ? atof(e) : 120.0;
+    return (uint64_t)((sec > 0 ? sec : 120.0) * 1e9);
+  }();
+  k_wait<<<1, 32, 0, s>>>(d_my_flags, R, seq, d_err, timeout_ns); ::kp::count_launch();
 }
 
 }  // namespace kp

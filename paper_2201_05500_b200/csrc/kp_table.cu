@@ -116,6 +116,7 @@ __device__ uint32_t probe(const TView& t, uint64_t key, int gl, uint32_t gmask, 
 template <bool INSERT>
 __global__ void k_probe(TView t, const uint64_t* __restrict__ keys, uint32_t n,
                         uint32_t* __restrict__ rows_out, uint32_t epoch) {
+  if (INSERT && aborted(t.abort)) return;  // no inserts after a peer timeout
   const int lane = threadIdx.x & 31;
   const int gl = lane & (GS - 1), gbase = lane & GS;
   const uint32_t gmask = 0xFFFFu << gbase;
@@ -163,6 +164,7 @@ __global__ void k_ws_check(const uint32_t* __restrict__ rows, uint32_t n, const 
 __global__ void k_apply_grads(TView t, const uint32_t* __restrict__ rows,
                               const float* __restrict__ grads, uint32_t n, float lr, float b1,
                               float b2) {
+  if (aborted(t.abort)) return;
   const uint64_t total = (uint64_t)n * t.dim;
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total;
        q += (uint64_t)gridDim.x * blockDim.x) {

@@ -22,6 +22,7 @@ struct TView {
   uint32_t dim;
   int rule;
   float iw, is1, is2;
+  const uint32_t* abort;  // g_abort at view time (null: unguarded)
 };
 
 inline TView view(const Table* t) {
@@ -41,6 +42,7 @@ inline TView view(const Table* t) {
   v.iw = t->init_w;
   v.is1 = t->init_s1;
   v.is2 = t->init_s2;
+  v.abort = g_abort;
   return v;
 }
 

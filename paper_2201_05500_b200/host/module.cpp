@@ -445,6 +445,7 @@ PYBIND11_MODULE(_kpsim_b200, m) {
              const uint16_t* sp = nullptr;
              if (!slots.is_none()) {
                sl = slots.cast<Arr<uint16_t>>();
+               if (sl.size() != keys.size()) throw Error("slots size != keys size");
                sp = sl.data();
              }
              check(kp_trainer_stage_batch(p.tr->handle(), slot, offs.data(), keys.data(), sp,
@@ -537,5 +538,6 @@ PYBIND11_MODULE(_kpsim_b200, m) {
            })
       .def_property_readonly("dense_dim", [](PyTrainer& p) { return p.tr->dense_dim(); })
       .def_property_readonly("completed_steps", [](PyTrainer& p) { return p.tr->completed_steps(); })
+      .def_property_readonly("merges", [](PyTrainer& p) { return p.tr->metrics().merge_events; })
       .def_property_readonly("table_size", [](PyTrainer& p) { return p.store->cache_size(); });
 }

@@ -38,3 +38,7 @@ def test_reference_arm_json_line():
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert "workload" in d["config"]
+    # the arm is the reference alone: none of this repo's CUDA libraries mapped
+    assert d["repo_so_loaded"] and all(p.startswith("oracle/_ref/") for p in d["repo_so_loaded"])
+    assert d["config"]["mlp"] == "[8->16->8->1]"
+    assert d["cpu_baseline_1core_full_batch"]["cores"] == 1

@@ -242,3 +242,35 @@ def test_f32_envelope_is_small():
     assert np.max(np.abs(w - d["table_w"])) <= 1e-5
     ws = o.worker_state(0)
     assert np.max(np.abs(ws["x"] - d["w0_x"])) <= 1e-5
+
+
+@pytest.mark.parametrize("pool,act,k", [("sum", "relu", 1), ("mean", "tanh", 2)])
+def test_torch64_pinned_to_orc64(pool, act, k):
+    """oracle/torch64.py (the f64 checker the full-size GPU tests use) agrees
+    with the pinned C oracle to f64 rounding on the same batches."""
+    torch = pytest.importorskip("torch")
+    from oracle.torch64 import Torch64Trainer
+    from paper_2201_05500_b200.data import make_batch as mk
+    cfg = O.TrainerCfg(n_workers=1, k=k, minibatch_size=512, embedding_dim=16, n_slots=8,
+                       hidden=(32, 16), pooling=pool, activation=act, alpha=0.02, beta1=0.9,
+                       beta2=0.99, sparse_lr=0.1)
+    o64 = O.Orc(cfg, 64)
+    t64 = Torch64Trainer(cfg, "cpu")
+    assert np.array_equal(t64.worker_state()["x"], o64.worker_state(0)["x"])
+    for b in range(3):
+        bt = mk(512, V=3000, zipf_s=1.1, n_slots=8, seed=70 + b)
+        keys, slots, offs = bt.keys, bt.slots, bt.offs
+        if b == 1:  # multi-hot slots
+            keys, slots = np.repeat(bt.keys, 2), np.repeat(bt.slots, 2)
+            offs = (bt.offs.astype(np.int64) * 2).astype(np.uint32)
+        ro = o64.batch(offs, keys, bt.labels, slots=slots, predict_first=True, want_preds=True)
+        rt = t64.batch(offs, keys, bt.labels, slots=slots, predict_first=True)
+        assert abs(ro["loss"] - rt["loss"]) < 1e-12
+        assert np.max(np.abs(ro["preds"] - rt["preds"])) < 1e-12
+    ko, wo, ao, _ = o64.table()
+    kt, wt, at = t64.table()
+    assert np.array_equal(ko, kt)
+    assert np.max(np.abs(wo - wt)) <= 1e-12 * max(1.0, np.abs(wo).max())
+    assert np.max(np.abs(ao - at) / ao) <= 1e-12
+    xo, xt = o64.worker_state(0)["x"], t64.worker_state()["x"]
+    assert np.max(np.abs(xo - xt)) <= 1e-12
