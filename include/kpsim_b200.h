@@ -259,6 +259,23 @@ int kp_trainer_table(kp_trainer* tr, kp_table** out);
  * [3] owner-side unique keys [4] keys received (G > 1). Returns and resets. */
 int kp_trainer_profile(kp_trainer* tr, int enable, double* stage_ms, uint64_t* counters);
 int kp_trainer_stream(kp_trainer* tr, kp_stream* s);
+/* Trainer::ledger (proj/include/kpsim/trainer.hpp:81, ledger.hpp:13-19) from
+ * MEASURED traffic: bytes this rank sent over NVLink since creation and the
+ * transmissions, indexed by TransferCategory: [0] gpu_pull (keys to remote
+ * owners + their rows back), [1] gpu_push (per-key gradients to remote
+ * owners), [2] dense_merge (the k-step merge's two rounds; one transmission
+ * per worker per merge), [3] sparse_sync and [4] cold_tier_io (0: one node,
+ * the sparse sync IS the push; no cold tier). All zero at G = 1. */
+int kp_trainer_ledger(kp_trainer* tr, uint64_t bytes[5], uint64_t count[5]);
+/* Trainer::dense_trajectory (trainer.hpp:82, recorded at trainer.cpp:215-227):
+ * opt-in (per-step x_bar readback; with G > 1 a collective, so enable it on
+ * every rank alike). */
+int kp_trainer_record_trajectory(kp_trainer* tr, int enable);
+/* StepRecord i (optimizer.hpp:55-63): step (1-based), merged, loss, a3
+ * increment, x_bar[D], frozen v_bar[D] (any output may be NULL);
+ * *n_steps = records so far. */
+int kp_trainer_trajectory(kp_trainer* tr, uint64_t i, uint64_t* step, int* merged, double* loss,
+                          double* a3, float* x_bar, float* v_bar, uint64_t* n_steps);
 
 #ifdef __cplusplus
 }

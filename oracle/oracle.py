@@ -11,6 +11,7 @@ this module. The product path never does.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import os
 import subprocess
 
@@ -33,6 +34,7 @@ def build(quiet: bool = True) -> None:
         raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
 
 
+@functools.lru_cache(maxsize=None)
 def _lib(name: str) -> C.CDLL:
     path = os.path.join(REF_DIR, name)
     if not os.path.exists(path):
@@ -304,7 +306,13 @@ class Ref:
         xb, vb, loss = np.zeros(D), np.zeros(D), C.c_double()
         if self.lib.ref_trainer_trajectory(self.h, step, xb, vb, C.byref(loss)):
             raise IndexError(step)
-        return {"x_bar": xb, "v_bar": vb, "loss": loss.value}
+        f = self.lib.ref_trainer_trajectory_flags
+        f.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int), C.POINTER(C.c_double),
+                      C.POINTER(C.c_uint64)]
+        merged, a3, n = C.c_int(), C.c_double(), C.c_uint64()
+        f(self.h, step, C.byref(merged), C.byref(a3), C.byref(n))
+        return {"x_bar": xb, "v_bar": vb, "loss": loss.value, "merged": bool(merged.value),
+                "a3_increment": a3.value, "n_steps": n.value}
 
     def table(self):
         n = int(self.lib.ref_trainer_table_size(self.h))

@@ -177,6 +177,19 @@ int ref_trainer_trajectory(void* h, uint64_t step, double* xbar, double* vbar,
   });
 }
 
+// the same StepRecord's merged flag and a3 increment (optimizer.hpp:55-63)
+int ref_trainer_trajectory_flags(void* h, uint64_t step, int* merged, double* a3,
+                                 uint64_t* n_steps) {
+  auto* t = static_cast<RefTrainer*>(h);
+  return guard([&] {
+    const auto& steps = t->trainer->dense_trajectory().steps;
+    *n_steps = steps.size();
+    if (step >= steps.size()) return;
+    *merged = steps[step].merged ? 1 : 0;
+    *a3 = steps[step].a3_increment;
+  });
+}
+
 uint64_t ref_trainer_table_size(void* h) {
   return static_cast<RefTrainer*>(h)->store->cache_size();
 }

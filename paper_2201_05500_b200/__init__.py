@@ -31,10 +31,13 @@ try:
         gemm_tn,
         device_count,
         global_merge,
+        kstep_ratio,
         launch_count,
         local_adam_step,
+        read_instances,
         shard,
         version,
+        write_instances,
     )
 except ImportError as e:  # pragma: no cover - exercised only on broken installs
     raise ImportError(
@@ -45,8 +48,8 @@ except ImportError as e:  # pragma: no cover - exercised only on broken installs
 __all__ = [
     "AdamHyper", "Comm", "ConfigError", "DeviceError", "KpsimError", "KStepEngine", "StoreError",
     "TieredStore", "Trainer", "WorkerState", "accumulate_moments", "adagrad_sparse_update", "auc_device",
-    "comm_unique_id", "compute_auc", "dedup", "dedup_runs", "gemm_nt", "gemm_tn", "device_count", "global_merge", "launch_count",
-    "local_adam_step", "shard", "version",
+    "comm_unique_id", "compute_auc", "dedup", "dedup_runs", "gemm_nt", "gemm_tn", "device_count", "global_merge", "kstep_ratio", "launch_count",
+    "local_adam_step", "read_instances", "shard", "version", "write_instances",
 ]
 
 __version__ = "0.1.0"

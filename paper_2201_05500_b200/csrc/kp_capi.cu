@@ -165,6 +165,19 @@ struct kp_trainer {
     uint64_t seq[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     DevBuf scratch;
   } peer;
+  // communication ledger (ledger.hpp TransferCategory order): bytes this
+  // rank SENT over NVLink, and the transmissions (one per peer and step)
+  uint64_t led_bytes[5] = {0, 0, 0, 0, 0}, led_count[5] = {0, 0, 0, 0, 0};
+  // dense trajectory (Trainer::dense_trajectory, trainer.cpp:215-227), opt-in
+  struct TrajStep {
+    uint64_t step = 0;
+    int merged = 0;
+    double loss = 0, a3 = 0;
+    std::vector<float> x_bar, v_bar;
+  };
+  bool traj_on = false;
+  std::vector<TrajStep> traj;
+  std::vector<float> traj_prev_vbar;  // frozen v_bar before the step (a3)
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev;
@@ -652,6 +665,12 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
     }
     for (int p = 1; p < R; ++p) tr->off_send[p] = tr->off_send[p - 1] + tr->cnt_send[p - 1];
     const uint32_t Rn = (uint32_t)tot;
+    // GpuPull: keys to each remote owner and its rows back (ledger.hpp)
+    for (int p = 0; p < R; ++p)
+      if (p != tr->rank && tr->cnt_send[p]) {
+        tr->led_bytes[kLedPull] += tr->cnt_send[p] * (8 + 4ull * tr->e);
+        tr->led_count[kLedPull] += 1;
+      }
     const bool peer = peer_ready(tr);
     uint64_t* rk;
     if (peer) {
@@ -709,6 +728,53 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   tr->mark(2);
   issue_staged(tr, -1);  // this step's host readbacks are done
   return pr;
+}
+
+// Bytes this rank sends over the fabric for one merge (two rounds, v then
+// the term), per path: peer (owner reads every rank's W chunk slices and
+// stores its result into every other rank), NCCL chunked (send W slices of
+// each peer's chunk + ring allgather), NCCL allgather of every worker vector.
+uint64_t merge_bytes_sent(const kp_trainer* tr) {
+  const uint64_t R = tr->world, W = tr->W, D = tr->D, me = tr->rank;
+  const uint64_t C = (D + R - 1) / R;
+  const uint64_t my_len = std::min<uint64_t>(C, D > me * C ? D - me * C : 0);
+  uint64_t per_round;
+  if (tr->peer.mode == 1) {
+    // served: every other owner reads its chunk of my W worker vectors; sent:
+    // my merged chunk to every other rank
+    per_round = (D - my_len) * W * 4 + (R - 1) * my_len * 4;
+  } else if ((R - 1) * W * D * 4 <= (24ull << 20)) {
+    per_round = (R - 1) * W * D * 4;  // ring allgather of W*D per rank
+  } else {
+    per_round = (D - my_len) * W * 4 + (R - 1) * C * 4;
+  }
+  return 2 * per_round;
+}
+
+// StepRecord (optimizer.hpp:55-63) for the step just taken: x_bar (a
+// collective when G > 1 and the replicas differ), the frozen v_bar of worker
+// 0, merged, a3 = sum_j |1/sqrt(v_bar_before) - 1/sqrt(v_bar_after)| at
+// merges (optimizer.cpp:126-131). The loss is filled in at batch end.
+void record_trajectory(kp_trainer* tr, uint64_t t, bool merged) {
+  const uint64_t D = tr->D;
+  kp_trainer::TrajStep r;
+  r.step = t;
+  r.merged = merged ? 1 : 0;
+  r.x_bar.resize(D);
+  r.v_bar.resize(D);
+  float* xb = tr->xbar.get<float>(D);
+  compute_xbar(tr, xb);
+  KP_CUDA(cudaMemcpyAsync(r.x_bar.data(), xb, D * 4, cudaMemcpyDeviceToHost, tr->s));
+  KP_CUDA(cudaMemcpyAsync(r.v_bar.data(), tr->vbar, D * 4, cudaMemcpyDeviceToHost, tr->s));
+  KP_CUDA(cudaStreamSynchronize(tr->s));
+  if (merged) {
+    double a3 = 0.0;
+    for (uint64_t j = 0; j < D; ++j)
+      a3 += std::abs(1.0 / std::sqrt((double)tr->traj_prev_vbar[j]) - 1.0 / std::sqrt((double)r.v_bar[j]));
+    r.a3 = a3;
+  }
+  tr->traj_prev_vbar = r.v_bar;
+  tr->traj.push_back(std::move(r));
 }
 
 void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fused_preds) {
@@ -857,6 +923,12 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
                      tr->sg_owner, s);
     tr->mark(4);
   }
+  if (tr->world > 1)  // GpuPush: per-key gradients to each remote owner
+    for (int p = 0; p < tr->world; ++p)
+      if (p != tr->rank && tr->cnt_send[p]) {
+        tr->led_bytes[kLedPush] += tr->cnt_send[p] * 4ull * tr->e;
+        tr->led_count[kLedPush] += 1;
+      }
   // dense k-step Adam (KStepEngine::step, optimizer.cpp:113-144)
   const uint64_t t = tr->t_global + 1;
   const bool merged = (t % tr->cfg.k) == 0;
@@ -875,12 +947,17 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
                    tr->cfg.reset_local_v != 0, tr->mws);
     tr->merges++;
     tr->x_uniform = true;
+    if (tr->world > 1) {  // DenseMerge: one model transmission per worker (trainer.cpp:99-107)
+      tr->led_bytes[kLedDense] += merge_bytes_sent(tr);
+      tr->led_count[kLedDense] += tr->W;
+    }
   }
   tr->t_global = t;
   uint32_t* chk = static_cast<uint32_t*>(tr->check.p);
   for (uint32_t l = 0; l < tr->W; ++l)
     dense_check(tr->v + l * D, tr->vbar + l * D, tr->x + l * D, D, chk, s, l == 0 ? chk + 1 : nullptr);
   tr->mark(5);
+  if (tr->traj_on) record_trajectory(tr, t, merged);
 }
 
 void predict_pass(kp_trainer* tr, const StepView& sv, float* d_preds_out) {
@@ -1071,6 +1148,14 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
     }
   }
   out->loss = cnt ? total / (double)cnt : std::nan("");
+  if (tr->traj_on && tr->traj.size() >= n_mb) {  // per-step losses (trainer.cpp:217-223)
+    const size_t first = tr->traj.size() - n_mb;
+    for (uint64_t j = 0; j < n_mb; ++j) {
+      uint64_t count = 0;
+      for (uint64_t w = 0; w < N; ++w) count += cstart(w * n_mb + j + 1) - cstart(w * n_mb + j);
+      tr->traj[first + j].loss = count ? lsum[j] / (double)count : std::nan("");
+    }
+  }
   out->auc = out->cumulative_auc = std::nan("");
   out->has_auc = 0;
   if (predict_first) {
@@ -1750,6 +1835,43 @@ int kp_trainer_profile(kp_trainer* tr, int enable, double* stage_ms, uint64_t* c
     for (double& d : tr->stage_ms) d = 0;
     tr->prof_steps = tr->prof_unique = tr->prof_occ = tr->prof_owner_unique = tr->prof_recv = 0;
     tr->prof = enable != 0;
+  });
+}
+
+int kp_trainer_ledger(kp_trainer* tr, uint64_t bytes[5], uint64_t count[5]) {
+  return guard([&] {
+    for (int i = 0; i < 5; ++i) {
+      bytes[i] = tr->led_bytes[i];
+      count[i] = tr->led_count[i];
+    }
+  });
+}
+
+int kp_trainer_record_trajectory(kp_trainer* tr, int enable) {
+  return guard([&] {
+    if (enable && !tr->traj_on) {
+      tr->traj_prev_vbar.resize(tr->D);
+      KP_CUDA(cudaSetDevice(tr->device));
+      KP_CUDA(cudaMemcpyAsync(tr->traj_prev_vbar.data(), tr->vbar, tr->D * 4, cudaMemcpyDeviceToHost, tr->s));
+      KP_CUDA(cudaStreamSynchronize(tr->s));
+    }
+    tr->traj_on = enable != 0;
+  });
+}
+
+int kp_trainer_trajectory(kp_trainer* tr, uint64_t i, uint64_t* step, int* merged, double* loss,
+                          double* a3, float* x_bar, float* v_bar, uint64_t* n_steps) {
+  return guard([&] {
+    if (n_steps) *n_steps = tr->traj.size();
+    if (!step && !x_bar && !v_bar && !merged && !loss && !a3) return;
+    KP_CHECK(i < tr->traj.size(), kErrGeneric, "trajectory step index out of range");
+    const auto& r = tr->traj[i];
+    if (step) *step = r.step;
+    if (merged) *merged = r.merged;
+    if (loss) *loss = r.loss;
+    if (a3) *a3 = r.a3;
+    if (x_bar) std::memcpy(x_bar, r.x_bar.data(), tr->D * 4);
+    if (v_bar) std::memcpy(v_bar, r.v_bar.data(), tr->D * 4);
   });
 }
 

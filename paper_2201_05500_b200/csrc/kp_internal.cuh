@@ -20,6 +20,8 @@ namespace kp {
 // kernel). g_abort is the word for the kernels launched on this host thread
 // (nullptr: no guard, single GPU); set it with AbortScope.
 constexpr uint32_t kAbortTimeout = 16u;
+// ledger categories (proj/include/kpsim/ledger.hpp TransferCategory)
+enum LedgerCat : int { kLedPull = 0, kLedPush = 1, kLedDense = 2, kLedSparse = 3, kLedCold = 4 };
 extern thread_local const uint32_t* g_abort;
 struct AbortScope {
   explicit AbortScope(const uint32_t* p) { g_abort = p; }

@@ -653,4 +653,167 @@ void Trainer::set_worker_state(std::size_t l, const WorkerState& s) {
   check(kp_trainer_set_worker_state(tr_, (uint32_t)l, x.data(), m.data(), v.data(), vb.data()));
 }
 
+// ---------------------------------------------------------------- ledger --
+LedgerReport Trainer::ledger() const {
+  uint64_t bytes[5], count[5];
+  check(kp_trainer_ledger(tr_, bytes, count));
+  LedgerReport rep;
+  for (int i = 0; i < 5; ++i) {
+    if (!count[i] && !bytes[i]) continue;
+    rep.categories[static_cast<TransferCategory>(i)] = {bytes[i], count[i]};
+    rep.total.bytes += bytes[i];
+    rep.total.count += count[i];
+  }
+  return rep;
+}
+
+const char* to_string(TransferCategory c) {
+  switch (c) {
+    case TransferCategory::GpuPull: return "gpu_pull";
+    case TransferCategory::GpuPush: return "gpu_push";
+    case TransferCategory::DenseMerge: return "dense_merge";
+    case TransferCategory::SparseSync: return "sparse_sync";
+    case TransferCategory::ColdTierIo: return "cold_tier_io";
+  }
+  return "?";
+}
+
+std::uint64_t LedgerReport::bytes(TransferCategory c) const {
+  auto it = categories.find(c);
+  return it == categories.end() ? 0 : it->second.bytes;
+}
+
+KStepRatios kstep_ratio(const LedgerReport& kstep, const LedgerReport& baseline) {
+  const auto base_dense = baseline.bytes(TransferCategory::DenseMerge);
+  const auto base_total = baseline.total.bytes;
+  if (base_total == 0) throw Error("kstep_ratio: zero-byte baseline ledger");
+  KStepRatios r;
+  r.dense_bytes = base_dense == 0 ? 0.0
+                                  : static_cast<double>(kstep.bytes(TransferCategory::DenseMerge)) /
+                                        static_cast<double>(base_dense);
+  r.total_bytes = static_cast<double>(kstep.total.bytes) / static_cast<double>(base_total);
+  return r;
+}
+
+// ------------------------------------------------------------ trajectory --
+void Trainer::record_trajectory(bool on) { check(kp_trainer_record_trajectory(tr_, on ? 1 : 0)); }
+
+Trajectory Trainer::dense_trajectory() const {
+  Trajectory tj;
+  tj.dim = D_;
+  tj.workers = config_.n_workers;
+  uint64_t n = 0;
+  check(kp_trainer_trajectory(tr_, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &n));
+  std::vector<float> xb(D_), vb(D_);
+  for (uint64_t i = 0; i < n; ++i) {
+    StepRecord r;
+    int merged = 0;
+    check(kp_trainer_trajectory(tr_, i, &r.step, &merged, &r.loss, &r.a3_increment, xb.data(),
+                                vb.data(), nullptr));
+    r.merged = merged != 0;
+    to_f64(xb, r.x_bar);
+    to_f64(vb, r.v_bar);
+    tj.steps.push_back(std::move(r));
+  }
+  return tj;
+}
+
+// -------------------------------------------------------------- data file --
+namespace {
+// one line of the instance file (proj/src/data.cpp:72-110): "label<TAB>ids"
+// with ids comma separated (empty tokens skipped), parsed by std::stoull
+// (base 10, leading blanks and a sign accepted, trailing junk ignored),
+// collected into a std::set (ascending, deduped)
+void parse_line(const std::string& line, int lineno, std::set<ParameterKey>& seen, int& label) {
+  const auto tab = line.find('\t');
+  if (tab == std::string::npos)
+    throw Error("instance file line " + std::to_string(lineno) + ": missing tab separator");
+  const std::string label_s = line.substr(0, tab);
+  if (label_s != "0" && label_s != "1")
+    throw Error("instance file line " + std::to_string(lineno) + ": label must be 0 or 1");
+  label = label_s == "1" ? 1 : 0;
+  seen.clear();
+  std::size_t pos = tab + 1;
+  while (pos <= line.size()) {
+    std::size_t end = line.find(',', pos);
+    if (end == std::string::npos) end = line.size();
+    if (end > pos) {
+      const std::string tok = line.substr(pos, end - pos);
+      try {
+        seen.insert(std::stoull(tok));
+      } catch (const std::exception&) {
+        throw Error("instance file line " + std::to_string(lineno) + ": bad feature id '" + tok + "'");
+      }
+    }
+    pos = end + 1;
+  }
+  if (seen.empty()) throw Error("instance file line " + std::to_string(lineno) + ": no feature ids");
+}
+}  // namespace
+
+void read_instances_csr(const std::string& path, std::vector<std::uint32_t>& offs,
+                        std::vector<ParameterKey>& keys, std::vector<std::int32_t>& labels) {
+  std::ifstream in(path);
+  if (!in) throw Error("cannot open instance file: " + path);
+  offs.assign(1, 0);
+  keys.clear();
+  labels.clear();
+  std::string line;
+  std::set<ParameterKey> seen;
+  int lineno = 0;
+  while (std::getline(in, line)) {
+    ++lineno;
+    if (line.empty()) continue;
+    int label = 0;
+    parse_line(line, lineno, seen, label);
+    keys.insert(keys.end(), seen.begin(), seen.end());
+    if (keys.size() > 0xFFFFFFFFull) throw Error("instance file: more than 2^32 feature ids");
+    offs.push_back(static_cast<std::uint32_t>(keys.size()));
+    labels.push_back(label);
+  }
+}
+
+std::vector<Instance> read_instances(const std::string& path) {
+  std::vector<std::uint32_t> offs;
+  std::vector<ParameterKey> keys;
+  std::vector<std::int32_t> labels;
+  read_instances_csr(path, offs, keys, labels);
+  std::vector<Instance> out(labels.size());
+  for (std::size_t i = 0; i < labels.size(); ++i) {
+    out[i].feature_ids.assign(keys.begin() + offs[i], keys.begin() + offs[i + 1]);
+    out[i].label = labels[i];
+  }
+  return out;
+}
+
+void write_instances(const std::string& path, const std::vector<Instance>& instances) {
+  std::ofstream out(path);
+  if (!out) throw Error("cannot write instance file: " + path);
+  for (const auto& inst : instances) {
+    out << inst.label << '\t';
+    for (std::size_t i = 0; i < inst.feature_ids.size(); ++i) {
+      if (i > 0) out << ',';
+      out << inst.feature_ids[i];
+    }
+    out << '\n';
+  }
+}
+
+std::vector<Batch> make_batches(std::vector<Instance> instances, std::uint64_t batch_size) {
+  if (batch_size < 1) throw ConfigError("batch_size must be >= 1");
+  std::vector<Batch> batches;
+  Batch current;
+  current.id = 0;
+  for (auto& inst : instances) {
+    current.instances.push_back(std::move(inst));
+    if (current.instances.size() == batch_size) {
+      batches.push_back(std::move(current));
+      current = Batch{};
+      current.id = batches.size();
+    }
+  }
+  if (!current.instances.empty()) batches.push_back(std::move(current));
+  return batches;
+}
+
 }  // namespace kpsim_b200

@@ -181,6 +181,51 @@ struct Batch {
   std::uint64_t id = 0;
 };
 
+// Replayable dataset file, one instance per line "label<TAB>id,id,..."
+// (proj/include/kpsim/data.hpp:45-51, proj/src/data.cpp:59-124): same
+// parsing rules and error messages as the reference.
+std::vector<Instance> read_instances(const std::string& path);
+void write_instances(const std::string& path, const std::vector<Instance>& instances);
+std::vector<Batch> make_batches(std::vector<Instance> instances, std::uint64_t batch_size);
+// read_instances straight into the CSR layout the trainer consumes:
+// offs[n+1], keys[offs[n]] (each instance's ids ascending, deduped), labels[n]
+void read_instances_csr(const std::string& path, std::vector<std::uint32_t>& offs,
+                        std::vector<ParameterKey>& keys, std::vector<std::int32_t>& labels);
+
+// ------------------------------------------------------------- ledger --
+// proj/include/kpsim/ledger.hpp:13-68, filled from MEASURED traffic (bytes
+// this rank sent over NVLink, kp_trainer_ledger) instead of a cost model.
+enum class TransferCategory : std::uint8_t { GpuPull, GpuPush, DenseMerge, SparseSync, ColdTierIo };
+const char* to_string(TransferCategory c);
+struct CategoryTotals {
+  std::uint64_t bytes = 0;
+  std::uint64_t count = 0;
+};
+struct KStepRatios {
+  double dense_bytes = 0.0;  // DenseMerge bytes, k-step over baseline
+  double total_bytes = 0.0;  // all bytes, k-step over baseline
+};
+struct LedgerReport {
+  std::map<TransferCategory, CategoryTotals> categories;
+  CategoryTotals total;
+  std::uint64_t bytes(TransferCategory c) const;
+};
+// kstep_ratio (proj/src/ledger.cpp:132-145); throws Error on a zero-byte baseline
+KStepRatios kstep_ratio(const LedgerReport& kstep, const LedgerReport& baseline);
+
+// ------------------------------------------------------- trajectory ----
+struct StepRecord {  // proj/include/kpsim/optimizer.hpp:55-63
+  std::uint64_t step = 0;
+  bool merged = false;
+  double loss = 0.0;
+  double a3_increment = 0.0;
+  std::vector<double> x_bar, v_bar;
+};
+struct Trajectory {
+  std::size_t dim = 0, workers = 0;
+  std::vector<StepRecord> steps;
+};
+
 struct BatchRecord {
   std::uint64_t batch = 0;
   std::size_t instances = 0;
@@ -247,6 +292,12 @@ class Trainer {
   std::size_t local_workers() const { return W_; }
   std::uint64_t completed_steps() const { return steps_; }
   kp_trainer* handle() const { return tr_; }
+  // Trainer::ledger (trainer.hpp:81): measured bytes per category
+  LedgerReport ledger() const;
+  // Trainer::dense_trajectory (trainer.hpp:82); recording is opt-in
+  // (record_trajectory(true) before training; collective when G > 1)
+  void record_trajectory(bool on);
+  Trajectory dense_trajectory() const;
   int rank() const { return rank_; }
   int world() const { return world_; }
 

@@ -68,6 +68,38 @@ TrainerConfig config_from_kwargs(const py::kwargs& kw) {
   return c;
 }
 
+py::dict ledger_to_dict(const LedgerReport& r) {
+  py::dict d;
+  for (int i = 0; i < 5; ++i) {
+    const auto c = static_cast<TransferCategory>(i);
+    auto it = r.categories.find(c);
+    py::dict e;
+    e["bytes"] = it == r.categories.end() ? 0 : it->second.bytes;
+    e["count"] = it == r.categories.end() ? 0 : it->second.count;
+    d[to_string(c)] = e;
+  }
+  py::dict t;
+  t["bytes"] = r.total.bytes;
+  t["count"] = r.total.count;
+  d["total"] = t;
+  return d;
+}
+
+LedgerReport ledger_from_dict(const py::dict& d) {
+  LedgerReport r;
+  for (int i = 0; i < 5; ++i) {
+    const auto c = static_cast<TransferCategory>(i);
+    if (!d.contains(to_string(c))) continue;
+    py::dict e = d[to_string(c)];
+    CategoryTotals t{e["bytes"].cast<std::uint64_t>(), e["count"].cast<std::uint64_t>()};
+    if (!t.bytes && !t.count) continue;
+    r.categories[c] = t;
+    r.total.bytes += t.bytes;
+    r.total.count += t.count;
+  }
+  return r;
+}
+
 }  // namespace
 
 PYBIND11_MODULE(_kpsim_b200, m) {
@@ -84,6 +116,44 @@ PYBIND11_MODULE(_kpsim_b200, m) {
     return kp_device_count(&n) == KP_OK ? n : 0;
   });
   m.def("launch_count", [] { return kp_launch_count(); });
+  // ---- data file (proj/src/data.cpp:72-124) + ledger arithmetic ----
+  m.def(
+      "read_instances",
+      [](const std::string& path) {
+        std::vector<std::uint32_t> offs;
+        std::vector<ParameterKey> keys;
+        std::vector<std::int32_t> labels;
+        read_instances_csr(path, offs, keys, labels);
+        return py::make_tuple(Arr<std::uint32_t>((py::ssize_t)offs.size(), offs.data()),
+                              Arr<std::uint64_t>((py::ssize_t)keys.size(), keys.data()),
+                              Arr<std::int32_t>((py::ssize_t)labels.size(), labels.data()));
+      },
+      py::arg("path"));
+  m.def(
+      "write_instances",
+      [](const std::string& path, Arr<std::uint32_t> offs, Arr<std::uint64_t> keys,
+         Arr<std::int32_t> labels) {
+        const std::size_t n = labels.size();
+        if ((std::size_t)offs.size() != n + 1) throw Error("offs must have n+1 entries");
+        if ((std::size_t)keys.size() != offs.data()[n]) throw Error("keys size != offs[n]");
+        std::vector<Instance> insts(n);
+        for (std::size_t i = 0; i < n; ++i) {
+          insts[i].feature_ids.assign(keys.data() + offs.data()[i], keys.data() + offs.data()[i + 1]);
+          insts[i].label = labels.data()[i];
+        }
+        write_instances(path, insts);
+      },
+      py::arg("path"), py::arg("offs"), py::arg("keys"), py::arg("labels"));
+  m.def(
+      "kstep_ratio",
+      [](const py::dict& kstep, const py::dict& baseline) {
+        const KStepRatios r = kstep_ratio(ledger_from_dict(kstep), ledger_from_dict(baseline));
+        py::dict d;
+        d["dense_bytes"] = r.dense_bytes;
+        d["total_bytes"] = r.total_bytes;
+        return d;
+      },
+      py::arg("kstep"), py::arg("baseline"));
 
   // ---- optimizer ----
   py::class_<AdamHyper>(m, "AdamHyper")
@@ -530,6 +600,25 @@ PYBIND11_MODULE(_kpsim_b200, m) {
              return d;
            },
            py::arg("enable"))
+      .def("ledger", [](PyTrainer& p) { return ledger_to_dict(p.tr->ledger()); })
+      .def("record_trajectory", [](PyTrainer& p, bool on) { p.tr->record_trajectory(on); },
+           py::arg("on") = true)
+      .def("dense_trajectory",
+           [](PyTrainer& p) {
+             const Trajectory tj = p.tr->dense_trajectory();
+             py::list out;
+             for (const auto& r : tj.steps) {
+               py::dict d;
+               d["step"] = r.step;
+               d["merged"] = r.merged;
+               d["loss"] = r.loss;
+               d["a3_increment"] = r.a3_increment;
+               d["x_bar"] = Arr<double>((py::ssize_t)r.x_bar.size(), r.x_bar.data());
+               d["v_bar"] = Arr<double>((py::ssize_t)r.v_bar.size(), r.v_bar.data());
+               out.append(d);
+             }
+             return out;
+           })
       .def("stream",
            [](PyTrainer& p) {
              kp_stream s = nullptr;

@@ -55,3 +55,47 @@ def test_sharded_training_matches_oracle(tmp_path, k, S, variant, peer):
         for a, b in zip(res["auc"], res["oracle_auc"]):
             if a is not None and b == b:
                 assert abs(a - b) <= 5e-3
+
+
+def _run(tmp_path, args, peer="1", port=29578):
+    world = min(_gpus(), 4)
+    out = tmp_path / "res.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tools", "mgpu_parity.py"),
+           str(out)] + [str(a) for a in args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env=dict(os.environ, KP_PEER=peer))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return json.loads(out.read_text())
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("k", [1, 4, 16, 64])
+def test_sharded_kstep_sweep_matches_oracle(tmp_path, k):
+    """configs[3]'s k sweep across G ranks: 24 predict-then-train batches,
+    per-batch loss/AUC, the final cumulative AUC, the sharded key set and the
+    state against the f64 oracle running the same N=G workers."""
+    res = _run(tmp_path, [k, 4, "base", 24], port=29580 + k % 7)
+    assert res["owners_ok"] and res["keyset_equal"]
+    assert res["steps"] == res["oracle_steps"] and res["merges"] == res["oracle_merges"]
+    assert res["w_max_abs"] <= 2e-4 and res["x_max_abs"] <= 2e-4
+    for a, b in zip(res["loss"], res["oracle_loss"]):
+        assert abs(a - b) <= 1e-4
+    for a, b in zip(res["auc"], res["oracle_auc"]):
+        if a is not None and b == b:
+            assert abs(a - b) <= 5e-3
+    assert abs(res["cum_auc"] - res["oracle_cum_auc"]) <= 5e-3
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+def test_ledger_measured_bytes(tmp_path):
+    """Trainer::ledger from measured traffic: gpu_pull / gpu_push bytes equal
+    the remote unique keys of each rank's slices x (8 + 4e) / x 4e, merges
+    are floor(T/k), and kstep_ratio's dense ratio is merges(k)/merges(1)."""
+    res = _run(tmp_path, [1, 4, "ledger"], port=29590)
+    assert res["merges_ok"]
+    for r in res["per_rank"]:
+        assert r["pull_ok"] and r["push_ok"]
+    for k, ratio in res["kstep_ratio"].items():
+        assert ratio["dense_bytes"] == pytest.approx((16 // int(k)) / 16, rel=1e-12)
+        assert ratio["total_bytes"] < 1.0

@@ -28,6 +28,9 @@ def main():
     k = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     S = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     variant = sys.argv[4] if len(sys.argv) > 4 else "base"
+    n_batches = int(sys.argv[5]) if len(sys.argv) > 5 else 4
+    if variant == "ledger":
+        return ledger_main(out_path, S)
     extra = (dict(pooling="mean", sparse_rule="adam", activation="tanh", sparse_eps=1e-6)
              if variant == "mean_adam" else {})
     dist.init_process_group("gloo")
@@ -41,7 +44,7 @@ def main():
     tr = DistributedTrainer(device=local, table_capacity=1 << 16, **cfg)
     res = {"loss": [], "auc": []}
     batches = []
-    for b in range(4):
+    for b in range(n_batches):
         if S > 1:
             bt = make_batch(600 + 17 * b, V=4000, zipf_s=1.1, n_slots=S, seed=b)
         else:
@@ -50,6 +53,7 @@ def main():
         r = tr.train_batch(bt, predict_first=True)
         res["loss"].append(r["loss"])
         res["auc"].append(r.get("auc"))
+        tr_cum = r.get("cumulative_auc")
     keys, w, s1, _ = tr.tr.table()
     x = tr.tr.worker_state(0)["x"]
     parts = [None] * world
@@ -64,6 +68,7 @@ def main():
             r = orc.batch(bt.offs, bt.keys, bt.labels, slots=bt.slots, predict_first=True)
             oloss.append(r["loss"])
             oauc.append(r["auc"])
+            orc_cum = r["cumulative_auc"]
         ok, ow, oa, _ = orc.table()
         allk = np.concatenate([np.array(p[0], np.uint64) for p in parts])
         allw = np.concatenate([np.array(p[1], np.float64).reshape(-1, 8) for p in parts])
@@ -85,10 +90,71 @@ def main():
             "loss": res["loss"], "oracle_loss": oloss,
             "auc": res["auc"], "oracle_auc": oauc,
             "table_rows_per_rank": [len(p[0]) for p in parts],
+            "batches": n_batches, "steps": tr.tr.completed_steps, "merges": tr.tr.merges,
+            "oracle_steps": orc.steps(), "oracle_merges": orc.merges(),
+            "cum_auc": tr_cum, "oracle_cum_auc": orc_cum,
         }
         with open(out_path, "w") as f:
             json.dump(summary, f)
         print(json.dumps(summary))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def ledger_main(out_path, S):
+    """Measured-traffic ledger (Trainer::ledger, trainer.hpp:81) for the same
+    batches at k = 1/4/16/64: each rank's gpu_pull / gpu_push bytes against the
+    counts implied by the batches (remote unique keys x (8 + 4e) and x 4e),
+    merge events against floor(T/k), and kstep_ratio (ledger.cpp:132-145)
+    of every k over k = 1 next to the paper's Figure-9 ratios."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2201_05500_b200 as kp
+    from paper_2201_05500_b200.data import make_batch
+    from paper_2201_05500_b200.dist import DistributedTrainer, rank_slice
+
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    e, mb = 16, 128
+    batches = [make_batch(world * mb, V=50000, zipf_s=1.1, n_slots=S, seed=900 + b) for b in range(16)]
+    ledgers, merges = {}, {}
+    for k in (1, 4, 16, 64):
+        tr = DistributedTrainer(device=local, table_capacity=1 << 18, n_workers=world, k=k,
+                                minibatch_size=mb, embedding_dim=e, n_slots=S, hidden=[64, 32],
+                                alpha=0.02, beta1=0.9, beta2=0.99, sparse_lr=0.1)
+        for bt in batches:
+            tr.train_batch(bt)
+        ledgers[k] = tr.tr.ledger()
+        merges[k] = tr.tr.merges
+        D = tr.tr.dense_dim
+        del tr
+    # expected sparse bytes from the batches (one minibatch step per batch)
+    remote = 0
+    for bt in batches:
+        first, n = rank_slice(bt.n, world, 1, mb, rank)
+        u = np.unique(bt.keys[bt.offs[first]:bt.offs[first + n]])
+        remote += int(np.count_nonzero(u % np.uint64(world) != np.uint64(rank)))
+    got = {k: ledgers[k] for k in ledgers}
+    parts = [None] * world
+    dist.all_gather_object(parts, (got, remote, merges, D))
+    if rank == 0:
+        res = {"world": world, "e": e, "D": D, "per_rank": []}
+        for g, (led, rem, mg, _) in enumerate(parts):
+            res["per_rank"].append({
+                "pull_ok": all(led[k]["gpu_pull"]["bytes"] == rem * (8 + 4 * e) for k in led),
+                "push_ok": all(led[k]["gpu_push"]["bytes"] == rem * 4 * e for k in led),
+                "merges": mg, "ledger": {str(k): v for k, v in led.items()}})
+        led0 = parts[0][0]
+        res["kstep_ratio"] = {str(k): kp.kstep_ratio(led0[k], led0[1]) for k in (4, 16, 64)}
+        res["paper_fig9_model_transmission_ratio"] = {"10": 0.181, "20": 0.108, "50": 0.064,
+                                                      "100": 0.028, "200": 0.012}
+        res["merges_ok"] = all(p[2][k] == 16 // k for p in parts for k in (1, 4, 16, 64))
+        with open(out_path, "w") as f:
+            json.dump(res, f)
+        print(json.dumps(res))
     dist.barrier()
     dist.destroy_process_group()
 
