@@ -41,7 +41,8 @@ def _nccl_dir():
 
 
 NCCL_DIR = _nccl_dir()
-CUDA_SRCS = ["kp_sort", "kp_table", "kp_embed", "kp_mlp", "kp_gemm_tc", "kp_dense", "kp_auc", "kp_peer", "kp_capi"]
+CUDA_SRCS = ["kp_sort", "kp_table", "kp_embed", "kp_mlp", "kp_gemm_tc", "kp_gemm_h3", "kp_dense", "kp_auc", "kp_peer",
+             "kp_capi"]
 HOST_SRCS = ["kpsim_b200", "module"]
 
 

@@ -145,6 +145,12 @@ struct kp_trainer {
   uint64_t hist_n = 0;
   DevBuf rows, rowocc, bag_offs, bag_of_occ, pooled, inv_count, dpooled, preds, err, loss, check;
   DevBuf inst_max;  // max |pooled row| per instance, from the pool kernel
+  // planes mode: the pooling kernel writes the first layer's input as fp16
+  // hi/lo planes (in the `pooled` buffer, same bytes) + an exponent per instance
+  bool planes = false;
+  DevBuf inst_exp;
+  const __half* plane_hi(size_t nb) const { return static_cast<const __half*>(pooled.p); }
+  const __half* plane_lo(size_t nb) const { return static_cast<const __half*>(pooled.p) + nb * e; }
   DevBuf xbar, pred_keep, lossg;
   // exchange buffers (G > 1)
   DevBuf perm, pos, send_keys, recv_keys, owner_rows, owner_idx, send_rows, recv_rows, send_grads,
@@ -722,9 +728,17 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   compose(pr.idx, tr->dd.d_inverse, sv.n_occ, rowocc, s);
   float* pooled = tr->pooled.get<float>((size_t)std::max<uint32_t>(nb, 1) * tr->e);
   float* invc = tr->inv_count.get<float>(std::max<uint32_t>(nb, 1));
-  // max |row| of the MLP input per instance (fp16-operand first layer)
-  float* imax = tr->inst_max.get<float>(std::max<uint32_t>(sv.n_inst, 1));
-  pool(bag_offs, nb, rowocc, pr.src, tr->e, tr->cfg.pooling == 1, pooled, invc, s, imax, tr->S);
+  if (tr->planes) {
+    // the first layer's input as fp16 planes (hi at pooled, lo behind it)
+    __half* hi = reinterpret_cast<__half*>(pooled);
+    int* iexp = tr->inst_exp.get<int>(std::max<uint32_t>(sv.n_inst, 1));
+    pool_planes(bag_offs, sv.n_inst, tr->S, rowocc, pr.src, tr->e, tr->cfg.pooling == 1, hi,
+                hi + (size_t)nb * tr->e, iexp, invc, s);
+  } else {
+    // max |row| of the MLP input per instance (fp16-operand first layer)
+    float* imax = tr->inst_max.get<float>(std::max<uint32_t>(sv.n_inst, 1));
+    pool(bag_offs, nb, rowocc, pr.src, tr->e, tr->cfg.pooling == 1, pooled, invc, s, imax, tr->S);
+  }
   tr->mark(2);
   issue_staged(tr, -1);  // this step's host readbacks are done
   return pr;
@@ -888,12 +902,20 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
       continue;
     }
     tr->mlp.in_rowmax = static_cast<const float*>(tr->inst_max.p) + lo;
+    if (tr->planes) {
+      const size_t nbags = (size_t)sv.n_inst * tr->S;
+      tr->mlp.in_hi = tr->plane_hi(nbags) + (size_t)lo * in_w;
+      tr->mlp.in_lo = tr->plane_lo(nbags) + (size_t)lo * in_w;
+      tr->mlp.in_exp = static_cast<const int*>(tr->inst_exp.p) + lo;
+    }
     mlp_forward(tr->shape, tr->x + l * D, pooled + (size_t)lo * in_w, Bw, preds + lo, tr->mlp, s);
     tr->mlp.in_rowmax = nullptr;
     mlp_backward(tr->shape, tr->x + l * D, pooled + (size_t)lo * in_w, Bw, preds + lo,
                  sv.labels + lo, tr->g + l * D, dpooled + (size_t)lo * in_w,
                  tr->cfg.pooling == 1 ? invc + (size_t)lo * tr->S : nullptr, tr->S, tr->e,
                  d_loss_slot, tr->mlp, s, (overlap && l + 1 == tr->W) ? &hook : nullptr);
+    tr->mlp.in_hi = tr->mlp.in_lo = nullptr;
+    tr->mlp.in_exp = nullptr;
   }
   tc_reserve_sms(0);
   if (fused_preds)
@@ -965,9 +987,17 @@ void predict_pass(kp_trainer* tr, const StepView& sv, float* d_preds_out) {
   compute_xbar(tr, xb);
   pull_and_pool(tr, sv, false);
   tr->mlp.in_rowmax = static_cast<const float*>(tr->inst_max.p);
+  if (tr->planes) {
+    const size_t nbags = (size_t)sv.n_inst * tr->S;
+    tr->mlp.in_hi = tr->plane_hi(nbags);
+    tr->mlp.in_lo = tr->plane_lo(nbags);
+    tr->mlp.in_exp = static_cast<const int*>(tr->inst_exp.p);
+  }
   mlp_forward(tr->shape, xb, static_cast<const float*>(tr->pooled.p), sv.n_inst, d_preds_out,
               tr->mlp, tr->s);
   tr->mlp.in_rowmax = nullptr;
+  tr->mlp.in_hi = tr->mlp.in_lo = nullptr;
+  tr->mlp.in_exp = nullptr;
   tr->mark(3);
 }
 
@@ -1521,8 +1551,29 @@ int kp_gemm_nt(const float* d_A, int lda, const float* d_B, int ldb, float* d_C,
     KP_CHECK(engine < 2 || tc_ok, kErrConfig, "gemm_nt: shape/alignment not supported by tcgen05 path");
     KP_CHECK(engine != 3 || (ldb % 8 == 0 && K % 8 == 0), kErrConfig,
              "gemm_nt: fp16 path needs K and ldb multiples of 8");
+    KP_CHECK(engine < 4 || (lda == K && ldb == K && K % 8 == 0), kErrConfig,
+             "gemm_nt: pre-split fp16 path needs contiguous rows and K % 8 == 0");
     if (engine == 1 || !tc_ok) {
       simt_gemm_nt(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, st(s));
+    } else if (engine == 4 || engine == 5) {
+      // 3xFP16 on pre-split planes (kp_gemm_h3.cu): split both operands per
+      // row, then the all-TMA GEMM; engine 5 runs it stream-K over K
+      struct PWs {
+        DevBuf ah, al, ae, bh, bl, be, ws;
+      };
+      PWs& w = dev_ws<PWs>();
+      auto* ah = reinterpret_cast<__half*>(w.ah.get<uint16_t>((size_t)M * K));
+      auto* al = reinterpret_cast<__half*>(w.al.get<uint16_t>((size_t)M * K));
+      auto* bh = reinterpret_cast<__half*>(w.bh.get<uint16_t>((size_t)N * K));
+      auto* bl = reinterpret_cast<__half*>(w.bl.get<uint16_t>((size_t)N * K));
+      int* ae = w.ae.get<int>(M);
+      int* be = w.be.get<int>(N);
+      split_rows_h(d_A, M, K, K, ah, al, ae, st(s));
+      split_rows_h(d_B, N, K, K, bh, bl, be, st(s));
+      GemmEpi ep{0, 0, nullptr, nullptr, 0, nullptr, 1, 1};
+      h3_gemm(H3Operand{ah, al, ae, K}, false, H3Operand{bh, bl, be, K}, false, M, N, K, d_C, ldc, ep,
+              engine == 5, engine == 5 ? w.ws.get<float>(h3_splitk_ws_floats(M, N)) : nullptr, st(s));
+      KP_CUDA(cudaStreamSynchronize(st(s)));
     } else if (engine == 3) {
       // fp16-operand path (per-row scaled 3xFP16), as used for the first MLP layer
       struct HWs {
@@ -1553,8 +1604,30 @@ int kp_gemm_tn(const float* d_A, int lda, const float* d_B, int ldb, float* d_C,
   return guard([&] {
     const bool tc_ok = tc_gemm_supported(M, N, K, d_A, lda, d_B, ldb);
     KP_CHECK(engine != 2 || tc_ok, kErrConfig, "gemm_tn: shape/alignment not supported by tcgen05 path");
+    KP_CHECK(engine < 4 || (lda == M && ldb == N && M % 8 == 0 && N % 8 == 0), kErrConfig,
+             "gemm_tn: pre-split fp16 path needs contiguous rows and M, N % 8 == 0");
     if (engine == 1 || !tc_ok) {
       simt_gemm_tn(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, st(s));
+    } else if (engine == 4 || engine == 5) {
+      // both operands MN-major ([K][M], [K][N]): planes with one exponent per
+      // column, the all-TMA 3xFP16 GEMM (engine 5: stream-K over K)
+      struct PWs {
+        DevBuf ah, al, ae, bh, bl, be, cm, ws;
+      };
+      PWs& w = dev_ws<PWs>();
+      auto* ah = reinterpret_cast<__half*>(w.ah.get<uint16_t>((size_t)M * K));
+      auto* al = reinterpret_cast<__half*>(w.al.get<uint16_t>((size_t)M * K));
+      auto* bh = reinterpret_cast<__half*>(w.bh.get<uint16_t>((size_t)N * K));
+      auto* bl = reinterpret_cast<__half*>(w.bl.get<uint16_t>((size_t)N * K));
+      int* ae = w.ae.get<int>(M);
+      int* be = w.be.get<int>(N);
+      unsigned* cm = w.cm.get<unsigned>(std::max(M, N));
+      split_cols_scaled_h(d_A, K, M, nullptr, cm, ah, al, ae, st(s));
+      split_cols_scaled_h(d_B, K, N, nullptr, cm, bh, bl, be, st(s));
+      GemmEpi ep{0, 0, nullptr, nullptr, 0, nullptr, 1, 1};
+      h3_gemm(H3Operand{ah, al, ae, M}, true, H3Operand{bh, bl, be, N}, true, M, N, K, d_C, ldc, ep,
+              engine == 5, engine == 5 ? w.ws.get<float>(h3_splitk_ws_floats(M, N)) : nullptr, st(s));
+      KP_CUDA(cudaStreamSynchronize(st(s)));
     } else {
       const int sp = tc_splits(M, N, K);
       if (sp == 1) {
@@ -1656,6 +1729,9 @@ int kp_trainer_create(const kp_trainer_config* cfg, kp_comm* comm, int device, k
       m.D += m.widths[l + 1];
     }
     tr->D = m.D;
+    // layer 1 on pre-split fp16 planes written by the pooling kernel
+    tr->planes = c.n_hidden >= 1 && tc_enabled() && tc_h_enabled() && h3_enabled() &&
+                 pool_planes_supported(c.n_slots, c.embedding_dim);
     const uint64_t D = m.D, W = tr->W;
     std::vector<double> x0(D);
     init_dense_host(c.seed, D, x0.data());

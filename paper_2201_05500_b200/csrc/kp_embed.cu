@@ -15,6 +15,7 @@
 // sum (chunk partials combined in chunk order) -- deterministic, no float
 // atomics.
 #include "kp_table.cuh"
+#include "kp_tcgen05.cuh"
 
 namespace kp {
 namespace {
@@ -281,6 +282,87 @@ __global__ void __launch_bounds__(256, 5) k_pool_inst(const uint32_t* __restrict
 #pragma unroll
     for (int off = 16; off; off >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, off));
     if (lane == 0) inst_max[inst] = wmax;
+  }
+}
+
+// Pooling straight into the first layer's fp16 operand planes (kp_gemm_h3.cu):
+// one block per instance holds the instance's whole pooled row (S*e floats,
+// NP float4 cells per thread) in registers, reduces its max |x|, and writes
+// hi = rn(x * 2^e), lo = rn(x * 2^e - hi) with e = row_exp(max) -- the same 4
+// bytes per element as the fp32 row, so the GEMMs never split on chip. Cell
+// c = (bag c / (e/4), float4 column c % (e/4)); a bag's rows are summed in
+// occurrence order (model.cpp:93), bit-identical to k_pool before the split.
+template <int NT, int NP>
+__global__ void __launch_bounds__(NT, NP <= 4 ? 4 : 2) k_pool_planes(const uint32_t* __restrict__ bag_offs, uint32_t n_inst,
+                                                    uint32_t S, const uint32_t* __restrict__ rowocc,
+                                                    const float* __restrict__ src, uint32_t e, int mean,
+                                                    __half* __restrict__ hi, __half* __restrict__ lo,
+                                                    int* __restrict__ inst_exp, float* __restrict__ inv_count) {
+  __shared__ float red[NT / 32];
+  const uint32_t lpr = e >> 2, ncell = S * lpr;
+  for (uint64_t inst = blockIdx.x; inst < n_inst; inst += gridDim.x) {
+    uint32_t o0[NP], o1[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const uint32_t c = threadIdx.x + p * NT;
+      const uint64_t b = inst * S + (c < ncell ? c / lpr : 0);
+      o0[p] = c < ncell ? bag_offs[b] : 0;
+      o1[p] = c < ncell ? bag_offs[b + 1] : 0;
+    }
+    float4 v[NP];
+    // first occurrence of every cell's bag: NP independent row loads in flight
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const uint32_t c = threadIdx.x + p * NT;
+      v[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (o0[p] < o1[p]) {
+        const uint32_t rr = rowocc[o0[p]];
+        if (rr != kNoRow) v[p] = __ldg(reinterpret_cast<const float4*>(src + (uint64_t)rr * e) + c % lpr);
+      }
+    }
+    float mx = 0.f;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const uint32_t c = threadIdx.x + p * NT;
+      for (uint32_t o = o0[p] + 1; o < o1[p]; ++o) {  // multi-feature bags, occurrence order
+        const uint32_t rr = rowocc[o];
+        if (rr == kNoRow) continue;
+        const float4 x = __ldg(reinterpret_cast<const float4*>(src + (uint64_t)rr * e) + c % lpr);
+        v[p].x = __fadd_rn(v[p].x, x.x), v[p].y = __fadd_rn(v[p].y, x.y);
+        v[p].z = __fadd_rn(v[p].z, x.z), v[p].w = __fadd_rn(v[p].w, x.w);
+      }
+      if (mean && c < ncell) {
+        const uint32_t len = o1[p] - o0[p];
+        const float inv = len ? __fdiv_rn(1.f, (float)len) : 1.f;  // model.cpp:95-97
+        if (len) v[p].x = __fmul_rn(v[p].x, inv), v[p].y = __fmul_rn(v[p].y, inv),
+                 v[p].z = __fmul_rn(v[p].z, inv), v[p].w = __fmul_rn(v[p].w, inv);
+        if (c % lpr == 0) inv_count[inst * S + c / lpr] = inv;
+      }
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[p].x), fabsf(v[p].y)), fmaxf(fabsf(v[p].z), fabsf(v[p].w))));
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = 0.f;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) mx = fmaxf(mx, red[w]);
+    __syncthreads();  // red is reused by the next instance
+    const int ex = tc::row_exp(mx);
+    if (threadIdx.x == 0) inst_exp[inst] = ex;
+    const float sc = tc::pow2f(ex);
+    uint2* h2 = reinterpret_cast<uint2*>(hi + inst * ncell * 4);
+    uint2* l2 = reinterpret_cast<uint2*>(lo + inst * ncell * 4);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const uint32_t c = threadIdx.x + p * NT;
+      if (c >= ncell) break;
+      uint2 hh, ll;
+      tc::split_h2(__fmul_rn(v[p].x, sc), __fmul_rn(v[p].y, sc), hh.x, ll.x);
+      tc::split_h2(__fmul_rn(v[p].z, sc), __fmul_rn(v[p].w, sc), hh.y, ll.y);
+      h2[c] = hh;
+      l2[c] = ll;
+    }
   }
 }
 
@@ -601,6 +683,38 @@ void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_row_of_
   if (n_bags == 0) return;
   dispatch_e<PoolF>(e, d_bag_offs, n_bags, d_row_of_occ, d_src, e, mean, d_pooled, d_inv_count,
                     d_inst_max, S, s);
+}
+
+bool pool_planes_supported(uint32_t S, uint32_t e) {
+  return e % 4 == 0 && e <= 128 && (S * e) % 8 == 0 && S * e / 4 <= 256 * 16;
+}
+
+void pool_planes(const uint32_t* d_bag_offs, uint32_t n_inst, uint32_t S, const uint32_t* d_row_of_occ,
+                 const float* d_src, uint32_t e, bool mean, __half* d_hi, __half* d_lo, int* d_inst_exp,
+                 float* d_inv_count, cudaStream_t s) {
+  KP_CHECK(pool_planes_supported(S, e), kErrConfig, "pool_planes: unsupported S*e");
+  if (n_inst == 0) return;
+  const uint32_t cells = S * e / 4;
+  const unsigned grid = (unsigned)std::min<uint64_t>(n_inst, 148ull * 64);
+  // threads per instance: the cells rounded up to warps (<= 256), then the
+  // fewest float4 cells per thread that cover the row
+  if (cells <= 64) {
+    k_pool_planes<64, 1><<<grid, 64, 0, s>>>(d_bag_offs, n_inst, S, d_row_of_occ, d_src, e, mean, d_hi, d_lo,
+                                              d_inst_exp, d_inv_count);
+  } else if (cells <= 256) {
+    k_pool_planes<256, 1><<<grid, 256, 0, s>>>(d_bag_offs, n_inst, S, d_row_of_occ, d_src, e, mean, d_hi, d_lo,
+                                                d_inst_exp, d_inv_count);
+  } else if (cells <= 256 * 4) {
+    k_pool_planes<256, 4><<<grid, 256, 0, s>>>(d_bag_offs, n_inst, S, d_row_of_occ, d_src, e, mean, d_hi, d_lo,
+                                                d_inst_exp, d_inv_count);
+  } else if (cells <= 256 * 8) {
+    k_pool_planes<256, 8><<<grid, 256, 0, s>>>(d_bag_offs, n_inst, S, d_row_of_occ, d_src, e, mean, d_hi, d_lo,
+                                                d_inst_exp, d_inv_count);
+  } else {
+    k_pool_planes<256, 16><<<grid, 256, 0, s>>>(d_bag_offs, n_inst, S, d_row_of_occ, d_src, e, mean, d_hi, d_lo,
+                                                 d_inst_exp, d_inv_count);
+  }
+  ::kp::count_launch();
 }
 
 void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* d_sorted_vals,

@@ -1,0 +1,614 @@
+// fp32-accurate GEMM on pre-split fp16 operands ("3xFP16", tcgen05 kind::f16).
+//
+//   C = epi( 2^-(ea[m] + eb[n]) * sum_k (Ah*Bh + Ah*Bl + Al*Bh)(m, n, k) )
+//
+// Every operand arrives in HBM as two fp16 planes, hi = rn(x * 2^e) and
+// lo = rn(x * 2^e - hi), with a power-of-two scale per row of A (ea) and per
+// row of B (eb) that puts the row's max |x| in [2^14, 2^15): hi + lo carries 22
+// significant bits like tf32 hi + lo, at the fp16 tensor rate (2x tf32), and
+// the dropped lo*lo term is ~2^-22 relative. The planes are produced by the
+// kernels that write the operands anyway (the pooling kernel writes the MLP
+// input as planes, the weight and upstream-gradient splits below), so the
+// GEMM itself only streams them: no on-chip split, TMA straight into the
+// UMMA layouts, both MMA operands from shared memory.
+//
+// Layer 1 of the CTR MLP (proj/src/model.cpp:100-191) at configs[1]
+// (B = 65536, S*e = 6400, hidden 256) runs three of these:
+//   forward   Z = X W1^T       A = X planes [B][6400] (K-major), B = W1 [256][6400]
+//   dX        dX = dZ W1       A = dZ1 [B][256] (K-major), B = W1^T [6400][256]
+//   dW        dW = dZ^T X      A = dZ' [B][256] (MN-major), B = X [B][6400] (MN-major),
+//             split over the batch (stream-K, deterministic fix-up)
+//
+// CTA pair (cluster of 2, tcgen05.mma.cta_group::2): tile M = 256 (128 rows
+// per CTA) x N = 256 (each CTA holds 128 of the B rows), k-block 32. TMEM:
+// two 256-column fp32 accumulators; the tensor core's accumulation is not
+// IEEE round-to-nearest and its error grows with K, so the MMA switches
+// accumulator every H3_CH k-blocks (512 k) and the epilogue warps fold the
+// finished one into fp32 registers with RN adds -- fp32-level accuracy
+// independent of K (the same scheme as kp_gemm_tc.cu).
+// Warps (per CTA): 0 TMA producer; 1 TMEM allocator, the leader's lane 0
+// issues the MMAs, the peer's lane 0 relays its TMA completions; 2-3 idle;
+// 4-19 drain + epilogue (warp w: TMEM lane quarter w%4, 64-column quarter
+// (w-4)/4, TMA store of 32x16 fp32 boxes). setmaxnreg moves registers from
+// warpgroup 0 to the epilogue warpgroups (64 fp32 running sums per thread).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <mutex>
+
+#include "kp_internal.cuh"
+#include "kp_tcgen05.cuh"
+
+namespace kp {
+namespace {
+
+using namespace tc;
+
+constexpr int H3_BM = 128;   // rows per CTA (pair: 256)
+constexpr int H3_BN = 256;   // tile columns (each CTA holds 128 B rows)
+constexpr int H3_BK = 32;    // k per stage
+constexpr int H3_NS = 4;     // smem stages
+constexpr int H3_CH = 16;    // k-blocks per accumulator chunk (512 k)
+constexpr int H3_WARPS = 20;  // warpgroup 0: producer, MMA, 2 idle; warpgroups 1-4: epilogue
+constexpr int H3_EPI_T = 512;
+constexpr uint32_t H3_PLANE = H3_BM * H3_BK * 2;  // 8 KB: one plane tile per CTA
+constexpr uint32_t H3_STAGE = 4 * H3_PLANE;       // A hi, A lo, B hi, B lo
+constexpr uint32_t H3_EPI = 16 * 2 * 2048;        // per epilogue warp two 32x16 fp32 store tiles
+// register split (setmaxnreg, per warpgroup): the epilogue holds 64 fp32
+// running sums per thread; the TMA / MMA warps need few
+constexpr int H3_REG_LO = 56, H3_REG_HI = 112;
+constexpr uint32_t H3_SMEM = H3_NS * H3_STAGE + H3_EPI + 1024 + 256;
+constexpr int H3_VUNITS = 148;  // stream-K virtual units (partition independent of the grid)
+
+struct H3Args {
+  int M, N, K;
+  int nblocks_m, nblocks_n, nk;  // tiles and k-blocks
+  int splitk;                    // stream-K over H3_VUNITS virtual units
+  const int* ea;                 // per-row exponents of A (nullable = 0)
+  const int* eb;                 // per-row exponents of B (nullable = 0)
+  int mode;                      // 0 store, 1 act(x + bias[n]), 3 x * coeff[m*S + n/e]
+  int act;
+  const float* bias;
+  const float* coeff;
+  uint32_t S, e;
+};
+
+// the k-block range of virtual unit v over T = tiles * nk iterations
+__device__ __forceinline__ int64_t vstart(int64_t v, int64_t T) { return v * T / H3_VUNITS; }
+
+// Iterates the (tile, kb0, kb1) segments of one physical unit: data-parallel
+// (whole tiles w = unit, unit+units, ...) or stream-K (the virtual units
+// v = unit, unit+units, ... each own [vstart(v), vstart(v+1)) of the
+// flattened tile x k-block space; segment id = tile + v is unique).
+struct SegIter {
+  int tiles, nk, splitk, units;
+  int64_t T;
+  int v;  // current virtual unit (stream-K) / tile (DP)
+  int64_t t, tend;
+  __device__ SegIter(const H3Args& a, int unit, int units_)
+      : tiles(a.nblocks_m * a.nblocks_n), nk(a.nk), splitk(a.splitk), units(units_) {
+    T = (int64_t)tiles * nk;
+    v = unit;
+    t = tend = 0;
+    if (splitk && v < H3_VUNITS) {
+      t = vstart(v, T);
+      tend = vstart(v + 1, T);
+    }
+  }
+  // next segment: tile index, [kb0, kb1), segment id; false when done
+  __device__ bool next(int& tile, int& kb0, int& kb1, int& sid) {
+    if (!splitk) {
+      if (v >= tiles) return false;
+      tile = v;
+      kb0 = 0;
+      kb1 = nk;
+      sid = v;
+      v += units;
+      return true;
+    }
+    while (t >= tend) {
+      v += units;
+      if (v >= H3_VUNITS) return false;
+      t = vstart(v, T);
+      tend = vstart(v + 1, T);
+    }
+    tile = (int)(t / nk);
+    kb0 = (int)(t % nk);
+    const int64_t e = kb0 + (tend - t);
+    kb1 = (int)(e < nk ? e : nk);
+    sid = tile + v;
+    t += kb1 - kb0;
+    return true;
+  }
+};
+
+// tile -> (m-block, n-block), n fastest: concurrently running units share A rows
+__device__ __forceinline__ void tile_mn(const H3Args& a, int tile, int& mb, int& nb) {
+  nb = tile % a.nblocks_n;
+  mb = tile / a.nblocks_n;
+}
+
+__device__ __forceinline__ float act_fwd(int act, float z) { return act == 0 ? (z > 0.f ? z : 0.f) : tanhf(z); }
+
+// one plane tile (this CTA's 128 rows x 32 k) of a K-major or MN-major operand
+template <bool MN>
+__device__ __forceinline__ void load_plane(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int k0, int r0) {
+  if (MN) {  // two 64(mn) x 32(k) SW128 boxes, LBO = 4 KB apart
+    tma_load_2d(dst, map, bar, r0, k0);
+    tma_load_2d(dst + 4096, map, bar, r0 + 64, k0);
+  } else {   // one 32(k) x 128(rows) SW64 box
+    tma_load_2d(dst, map, bar, k0, r0);
+  }
+}
+template <bool MN>
+__device__ __forceinline__ uint64_t plane_desc(uint32_t base, int kk) {
+  return MN ? sdesc_mn128(base + (uint32_t)kk * 2048u, 4096u) : sdesc_k64(base + (uint32_t)kk * 32u);
+}
+
+template <bool AMN, bool BMN>
+__global__ void __launch_bounds__(H3_WARPS * 32, 1)
+    k_h3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
+         const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
+         const __grid_constant__ CUtensorMap tmC, H3Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* epi = smem + H3_NS * H3_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + H3_EPI);
+  uint64_t* full = bars;              // TMA -> MMA (local)
+  uint64_t* conv = bars + H3_NS;      // peer's TMA landed -> leader's MMA (1 arrival)
+  uint64_t* empty = bars + 2 * H3_NS; // MMA done with stage -> producers (both CTAs)
+  uint64_t* tfull = bars + 3 * H3_NS; // chunk accumulated -> drains (both CTAs)
+  uint64_t* tempty = tfull + 2;       // drained -> MMA (leader; 2 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int unit = blockIdx.x >> 1, units = gridDim.x >> 1;
+  auto sAh = [&](int s) { return smem + s * H3_STAGE; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < H3_NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 2);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  fence_before();
+  __syncthreads();
+  cluster_sync();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(H3_REG_LO));
+  if (warp == 0) {
+    // ---- TMA producer: this CTA's 128 A rows and 128 B rows per k-block
+    if (lane == 0) {
+      prefetch_map(&tmAh);
+      prefetch_map(&tmAl);
+      prefetch_map(&tmBh);
+      prefetch_map(&tmBl);
+      SegIter it(a, unit, units);
+      int tile, kb0, kb1, sid, g = 0;
+      while (it.next(tile, kb0, kb1, sid)) {
+        int mb, nb;
+        tile_mn(a, tile, mb, nb);
+        const int m0 = mb * 2 * H3_BM + (int)rank * H3_BM;
+        const int n0 = nb * H3_BN + (int)rank * (H3_BN / 2);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          const int s = g % H3_NS;
+          if (g >= H3_NS) mbar_wait(&empty[s], ((g / H3_NS) & 1) ^ 1);
+          mbar_expect_tx(&full[s], H3_STAGE);
+          uint8_t* st = sAh(s);
+          load_plane<AMN>(st, &tmAh, &full[s], kb * H3_BK, m0);
+          load_plane<AMN>(st + H3_PLANE, &tmAl, &full[s], kb * H3_BK, m0);
+          load_plane<BMN>(st + 2 * H3_PLANE, &tmBh, &full[s], kb * H3_BK, n0);
+          load_plane<BMN>(st + 3 * H3_PLANE, &tmBl, &full[s], kb * H3_BK, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---- MMA issuer (leader CTA): both CTAs' tiles, M = 256
+      constexpr uint32_t idesc = idesc_f16(AMN, BMN, 2 * H3_BM, H3_BN);
+      SegIter it(a, unit, units);
+      int tile, kb0, kb1, sid, g = 0, c = 0;
+      while (it.next(tile, kb0, kb1, sid)) {
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          const int s = g % H3_NS;
+          const int kin = (kb - kb0) % H3_CH, buf = c & 1;
+          if (kin == 0 && c >= 2) mbar_wait(&tempty[buf], ((c >> 1) - 1) & 1);
+          mbar_wait(&full[s], (g / H3_NS) & 1);
+          mbar_wait(&conv[s], (g / H3_NS) & 1);
+          fence_after();
+          const uint32_t d = tmem + (uint32_t)(buf * H3_BN);
+          const uint32_t ah = smem_u32(sAh(s)), al = ah + H3_PLANE, bh = ah + 2 * H3_PLANE,
+                         bl = ah + 3 * H3_PLANE;
+#pragma unroll
+          for (int kk = 0; kk < H3_BK / 16; ++kk) {
+            const uint64_t dah = plane_desc<AMN>(ah, kk), dal = plane_desc<AMN>(al, kk);
+            const uint64_t dbh = plane_desc<BMN>(bh, kk), dbl = plane_desc<BMN>(bl, kk);
+            mma_f16_pair(d, dah, dbh, idesc, (kin | kk) != 0);
+            mma_f16_pair(d, dah, dbl, idesc, 1);
+            mma_f16_pair(d, dal, dbh, idesc, 1);
+          }
+          commit_pair(&empty[s]);
+          if (kin == H3_CH - 1 || kb == kb1 - 1) {
+            commit_pair(&tfull[buf]);
+            ++c;
+          }
+        }
+      }
+    } else if (lane == 0) {
+      // ---- peer CTA: relay "my TMA landed" to the leader's MMA issuer
+      SegIter it(a, unit, units);
+      int tile, kb0, kb1, sid, g = 0;
+      while (it.next(tile, kb0, kb1, sid))
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          const int s = g % H3_NS;
+          mbar_wait(&full[s], (g / H3_NS) & 1);
+          mbar_arrive_leader(&conv[s]);
+        }
+    }
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(H3_REG_HI));
+    // ---- drain + epilogue (16 warps): TMEM lane quarter q, columns [cq*64, +64)
+    const int q = warp & 3, cq = (warp - 4) >> 2;
+    const int et = threadIdx.x - 128;
+    uint8_t* dense_base = epi + (warp - 4) * 4096;
+    uint32_t tma_seq = 0;
+    SegIter it(a, unit, units);
+    int tile, kb0, kb1, sid, c = 0;
+    while (it.next(tile, kb0, kb1, sid)) {
+      int mb, nb;
+      tile_mn(a, tile, mb, nb);
+      const int mrow0 = mb * 2 * H3_BM + (int)rank * H3_BM + q * 32;  // this warp's 32 rows
+      const int ncol0 = nb * H3_BN + cq * 64;                          // this warp's 64 columns
+      float acc[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+      const int nch = (kb1 - kb0 + H3_CH - 1) / H3_CH;
+      for (int ci = 0; ci < nch; ++ci, ++c) {
+        const int buf = c & 1;
+        mbar_wait(&tfull[buf], (c >> 1) & 1);
+        fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * H3_BN + cq * 64 + c0), r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[c0 + j] = __fadd_rn(acc[c0 + j], __uint_as_float(r[j]));
+        }
+        fence_before();
+        named_sync(1, H3_EPI_T);
+        if (et == 0) mbar_arrive_leader(&tempty[buf]);
+      }
+      // epilogue: row per lane; exact power-of-two unscaling, then the op
+      const int m = mrow0 + lane;
+      const float sa = (a.ea && m < a.M) ? pow2f(-__ldg(a.ea + m)) : 1.f;
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        uint8_t* dense = dense_base + (tma_seq & 1) * 2048;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        const int n = ncol0 + c0;
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int nn = min(n + j, a.N - 1);
+          const float sb = a.eb ? pow2f(-__ldg(a.eb + nn)) : 1.f;
+          v[j] = __fmul_rn(__fmul_rn(acc[c0 + j], sa), sb);
+          if (a.mode == 1) v[j] = act_fwd(a.act, __fadd_rn(v[j], __ldg(a.bias + nn)));
+        }
+        if (a.mode == 3) {
+          const float* cp = a.coeff + (size_t)min(m, a.M - 1) * a.S;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], __ldg(cp + min(n + j, a.N - 1) / a.e));
+        }
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+          *reinterpret_cast<float4*>(dense + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4)) =
+              make_float4(v[4 * cc], v[4 * cc + 1], v[4 * cc + 2], v[4 * cc + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          if (a.splitk)  // partial tile of segment sid: rows sid*256 + local row
+            tma_store_2d(&tmC, dense, cq * 64 + c0, sid * 2 * H3_BM + (int)rank * H3_BM + q * 32);
+          else
+            tma_store_2d(&tmC, dense, n, mrow0);
+        }
+        ++tma_seq;
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc_pair(tmem, 512);
+}
+
+// stream-K fix-up: C tile = sum of its segments' partials in k order
+__global__ void k_h3_fixup(const float* __restrict__ part, int nblocks_n, int nk, int64_t T, int M,
+                           int N, float* __restrict__ C, int ldc) {
+  const int tile = blockIdx.y;
+  const int mb = tile / nblocks_n, nb = tile % nblocks_n;
+  const int64_t t0 = (int64_t)tile * nk, t1 = t0 + nk - 1;
+  // unit(t) = max v with vstart(v) <= t = floor(((t+1)*V - 1) / T)
+  const int v0 = (int)(((t0 + 1) * H3_VUNITS - 1) / T), v1 = (int)(((t1 + 1) * H3_VUNITS - 1) / T);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * H3_BM * H3_BN; i += gridDim.x * blockDim.x) {
+    const int r = i / H3_BN, cc = i % H3_BN;
+    const int m = mb * 2 * H3_BM + r, n = nb * H3_BN + cc;
+    if (m >= M || n >= N) continue;
+    float s = 0.f;
+    for (int v = v0; v <= v1; ++v) s = __fadd_rn(s, part[((size_t)(tile + v) * 2 * H3_BM + r) * H3_BN + cc]);
+    C[(size_t)m * ldc + n] = s;
+  }
+}
+
+// ---- host ------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// fp16 plane [rows][cols] (ld halves): K-major boxes 32(k) x 128(rows) SW64,
+// MN-major boxes 64(mn) x 32(k) SW128 (rows = K, cols = MN)
+bool map_plane(CUtensorMap* m, const __half* p, uint64_t rows, uint64_t cols, uint64_t ld, bool mn) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {mn ? 64u : 32u, mn ? 32u : 128u};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(p), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// fp32 [rows][cols] output, 16 x 32 boxes, SW64 (the epilogue's dense tiles)
+bool map_out(CUtensorMap* m, float* p, uint64_t rows, uint64_t cols, uint64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {16, 32};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+thread_local int g_h3_reserve = 0;
+
+template <bool AMN, bool BMN>
+int h3_units() {
+  static int units = 0;
+  if (units) return units;
+  int dev = 0, sms = 0;
+  KP_CUDA(cudaGetDevice(&dev));
+  KP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  units = sms / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(4, 1, 1);
+  cfg.blockDim = dim3(H3_WARPS * 32, 1, 1);
+  cfg.dynamicSmemBytes = H3_SMEM;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_h3<AMN, BMN>, &cfg) == cudaSuccess && n > 0) units = std::min(units, n);
+  cudaGetLastError();
+  return units;
+}
+
+template <bool AMN, bool BMN>
+void launch_h3(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, bool splitk,
+               float* ws, const H3Args& a0, cudaStream_t s) {
+  CUtensorMap tah, tal, tbh, tbl, tcm;
+  // K-major operand [rows][K]; MN-major [K][rows]
+  auto mk = [&](CUtensorMap* m, const __half* p, const H3Operand& op, int rows, bool mn) {
+    return mn ? map_plane(m, p, K, rows, op.ld, true) : map_plane(m, p, rows, K, op.ld, false);
+  };
+  bool ok = mk(&tah, A.hi, A, M, AMN) && mk(&tal, A.lo, A, M, AMN) && mk(&tbh, B.hi, B, N, BMN) &&
+            mk(&tbl, B.lo, B, N, BMN);
+  H3Args a = a0;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.nblocks_m = (int)ceil_div(M, 2 * H3_BM);
+  a.nblocks_n = (int)ceil_div(N, H3_BN);
+  a.nk = (int)ceil_div(K, H3_BK);
+  a.splitk = splitk ? 1 : 0;
+  a.ea = A.exp;
+  a.eb = B.exp;
+  const int tiles = a.nblocks_m * a.nblocks_n;
+  if (splitk) {
+    a.mode = 0;  // partials are plain sums (scales are exact and applied per partial)
+    ok = ok && map_out(&tcm, ws, (uint64_t)(tiles + H3_VUNITS) * 2 * H3_BM, H3_BN, H3_BN);
+  } else {
+    ok = ok && map_out(&tcm, C, M, N, ldc);
+  }
+  KP_CHECK(ok, kErrCuda, "cuTensorMapEncodeTiled failed (3xFP16 GEMM operands)");
+  static std::atomic<uint64_t> attr{0};
+  int dev = 0;
+  KP_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr.load(std::memory_order_acquire) & bit)) {
+    KP_CUDA(cudaFuncSetAttribute(k_h3<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, H3_SMEM));
+    attr.fetch_or(bit, std::memory_order_release);
+  }
+  const int units_all = std::max(1, h3_units<AMN, BMN>() - (g_h3_reserve + 1) / 2);
+  const int work = splitk ? H3_VUNITS : tiles;
+  const unsigned grid = (unsigned)std::min(work, units_all) * 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(H3_WARPS * 32, 1, 1);
+  cfg.dynamicSmemBytes = H3_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  KP_CUDA(cudaLaunchKernelEx(&cfg, k_h3<AMN, BMN>, tah, tal, tbh, tbl, tcm, a));
+  ::kp::count_launch();
+  if (splitk) {
+    const int64_t T = (int64_t)tiles * a.nk;
+    k_h3_fixup<<<dim3(64, tiles), 256, 0, s>>>(ws, a.nblocks_n, a.nk, T, M, N, C, ldc);
+    ::kp::count_launch();
+  }
+}
+
+// ---- plane producers ----------------------------------------------------------
+// one warp per row of X [rows][K] (K <= 1024): max |x| -> e = row_exp, planes of x * 2^e
+__global__ void k_split_rows(const float* __restrict__ x, int rows, int K, int ld, __half* __restrict__ hi,
+                             __half* __restrict__ lo, int* __restrict__ exps) {
+  const int lane = threadIdx.x & 31;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+    const float* row = x + (size_t)r * ld;
+    float mx = 0.f;
+    for (int k = lane; k < K; k += 32) mx = fmaxf(mx, fabsf(row[k]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int e = row_exp(mx);
+    if (lane == 0) exps[r] = e;
+    const float sc = pow2f(e);
+    for (int k = 2 * lane; k < K; k += 64) {
+      const float x0 = __fmul_rn(row[k], sc), x1 = k + 1 < K ? __fmul_rn(row[k + 1], sc) : 0.f;
+      uint32_t h, l;
+      split_h2(x0, x1, h, l);
+      if (k + 1 < K) {
+        *reinterpret_cast<uint32_t*>(hi + (size_t)r * K + k) = h;
+        *reinterpret_cast<uint32_t*>(lo + (size_t)r * K + k) = l;
+      } else {
+        hi[(size_t)r * K + k] = __ushort_as_half((unsigned short)(h & 0xFFFF));
+        lo[(size_t)r * K + k] = __ushort_as_half((unsigned short)(l & 0xFFFF));
+      }
+    }
+  }
+}
+
+// dW's A operand: D[b][o] = dZ[b][o] * 2^-xe[b] (X's row scale moved onto the
+// other factor, so the sum over b needs no per-k scale), split with a scale
+// per COLUMN o (the GEMM row of dW): pass 1 column maxima, pass 2 planes.
+__global__ void k_colmax_scaled(const float* __restrict__ dz, int B, int N, const int* __restrict__ xe,
+                                unsigned* __restrict__ cmax) {
+  // block = 256 columns (thread per column), rows strided by gridDim.y
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float mx = 0.f;
+  for (int b = blockIdx.y; b < B; b += gridDim.y)
+    mx = fmaxf(mx, fabsf(__fmul_rn(dz[(size_t)b * N + n], xe ? pow2f(-__ldg(xe + b)) : 1.f)));
+  if (mx > 0.f) atomicMax(cmax + n, __float_as_uint(mx));
+}
+__global__ void k_split_cols_scaled(const float* __restrict__ dz, int B, int N, const int* __restrict__ xe,
+                                    const unsigned* __restrict__ cmax, __half* __restrict__ hi,
+                                    __half* __restrict__ lo, int* __restrict__ exps) {
+  const int n2 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;  // column pair
+  if (n2 >= N) return;
+  const int e0 = row_exp(__uint_as_float(cmax[n2])), e1 = n2 + 1 < N ? row_exp(__uint_as_float(cmax[n2 + 1])) : 0;
+  if (blockIdx.y == 0) {
+    exps[n2] = e0;
+    if (n2 + 1 < N) exps[n2 + 1] = e1;
+  }
+  const float s0 = pow2f(e0), s1 = pow2f(e1);
+  for (int b = blockIdx.y; b < B; b += gridDim.y) {
+    const float xs = xe ? pow2f(-__ldg(xe + b)) : 1.f;
+    const float x0 = __fmul_rn(__fmul_rn(dz[(size_t)b * N + n2], xs), s0);
+    const float x1 = n2 + 1 < N ? __fmul_rn(__fmul_rn(dz[(size_t)b * N + n2 + 1], xs), s1) : 0.f;
+    uint32_t h, l;
+    split_h2(x0, x1, h, l);
+    if (n2 + 1 < N) {
+      *reinterpret_cast<uint32_t*>(hi + (size_t)b * N + n2) = h;
+      *reinterpret_cast<uint32_t*>(lo + (size_t)b * N + n2) = l;
+    } else {
+      hi[(size_t)b * N + n2] = __ushort_as_half((unsigned short)(h & 0xFFFF));
+      lo[(size_t)b * N + n2] = __ushort_as_half((unsigned short)(l & 0xFFFF));
+    }
+  }
+}
+
+}  // namespace
+
+void h3_reserve_sms(int n) { g_h3_reserve = n < 0 ? 0 : n; }
+
+bool h3_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("KP_GEMM_H3");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+bool h3_supported(int M, int N, int K, const H3Operand& A, const H3Operand& B) {
+  if (M <= 0 || N <= 0 || K <= 0 || !encode_fn()) return false;
+  for (const H3Operand* o : {&A, &B}) {
+    if ((o->ld * 2) % 16) return false;
+    if (reinterpret_cast<uintptr_t>(o->hi) % 16 || reinterpret_cast<uintptr_t>(o->lo) % 16) return false;
+  }
+  return true;
+}
+
+// C[m][n] = epi(sum_k A(m,k) B(n,k)); A/B K-major ([rows][K]) unless *_mn
+void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M, int N, int K, float* C,
+             int ldc, const GemmEpi& ep, bool splitk, float* ws, cudaStream_t s) {
+  H3Args a{};
+  a.mode = ep.mode;
+  a.act = ep.act;
+  a.bias = ep.bias;
+  a.coeff = ep.coeff;
+  a.S = ep.S;
+  a.e = ep.e;
+  KP_CHECK(ep.mode == 0 || ep.mode == 1 || ep.mode == 3, kErrGeneric, "h3_gemm: unsupported epilogue");
+  if (!a_mn && !b_mn) launch_h3<false, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
+  else if (a_mn && b_mn) launch_h3<true, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
+  else if (a_mn) launch_h3<true, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
+  else launch_h3<false, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
+}
+
+size_t h3_splitk_ws_floats(int M, int N) {
+  const size_t tiles = ceil_div(M, 2 * H3_BM) * ceil_div(N, H3_BN);
+  return (tiles + H3_VUNITS) * 2 * H3_BM * H3_BN;
+}
+
+void split_rows_h(const float* X, int rows, int K, int ld, __half* hi, __half* lo, int* exps, cudaStream_t s) {
+  k_split_rows<<<std::min<unsigned>(ceil_div((uint64_t)rows * 32, 256), 148 * 16), 256, 0, s>>>(X, rows, K, ld, hi,
+                                                                                                lo, exps);
+  ::kp::count_launch();
+}
+
+void split_cols_scaled_h(const float* dz, int B, int N, const int* xe, unsigned* cmax_ws, __half* hi, __half* lo,
+                         int* exps, cudaStream_t s) {
+  KP_CUDA(cudaMemsetAsync(cmax_ws, 0, (size_t)N * 4, s));
+  const unsigned gy = (unsigned)std::min<uint64_t>(std::max<uint64_t>(1, B / 64), 512);
+  k_colmax_scaled<<<dim3(ceil_div(N, 256), gy), 256, 0, s>>>(dz, B, N, xe, cmax_ws);
+  ::kp::count_launch();
+  k_split_cols_scaled<<<dim3(ceil_div(N, 512), gy), 256, 0, s>>>(dz, B, N, xe, cmax_ws, hi, lo, exps);
+  ::kp::count_launch();
+}
+
+}  // namespace kp

@@ -239,6 +239,35 @@ void simt_gemm_tn(int M, int N, int K, const float* A, int lda, const float* B, 
 // out[i] = sum_z part[z][i] in z order
 void reduce_splits(const float* part, int splits, size_t n, float* out, cudaStream_t s);
 
+// 3xFP16 GEMM on pre-split fp16 operand planes (kp_gemm_h3.cu). An operand
+// is hi/lo planes of x * 2^exp[row] (exp nullable = 0), ld in halves.
+struct H3Operand {
+  const __half* hi;
+  const __half* lo;
+  const int* exp;
+  int ld;
+};
+bool h3_enabled();  // KP_GEMM_H3=0 keeps layer 1 on the on-chip-split kernels
+bool h3_supported(int M, int N, int K, const H3Operand& A, const H3Operand& B);
+// C[m][n] = epi(2^-(ea[m]+eb[n]) sum_k A(m,k) B(n,k)); a_mn / b_mn: operand
+// stored [K][rows] (MN-major) instead of [rows][K]. splitk: deterministic
+// stream-K over the K range into `ws` (h3_splitk_ws_floats) + fix-up; only
+// the plain store epilogue (mode 0).
+void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M, int N, int K, float* C,
+             int ldc, const GemmEpi& ep, bool splitk, float* ws, cudaStream_t s);
+size_t h3_splitk_ws_floats(int M, int N);
+void h3_reserve_sms(int n);
+// planes of each row of X [rows][K] with its own exponent (one warp per row)
+void split_rows_h(const float* X, int rows, int K, int ld, __half* hi, __half* lo, int* exps, cudaStream_t s);
+// planes of D[b][n] = dz[b][n] * 2^-xe[b] with one exponent per column n
+void split_cols_scaled_h(const float* dz, int B, int N, const int* xe, unsigned* cmax_ws, __half* hi,
+                         __half* lo, int* exps, cudaStream_t s);
+// pooling written as the first layer's planes (see kp_embed.cu k_pool_planes)
+bool pool_planes_supported(uint32_t S, uint32_t e);
+void pool_planes(const uint32_t* d_bag_offs, uint32_t n_inst, uint32_t S, const uint32_t* d_row_of_occ,
+                 const float* d_src, uint32_t e, bool mean, __half* d_hi, __half* d_lo, int* d_inst_exp,
+                 float* d_inv_count, cudaStream_t s);
+
 // ---------------------------------------------------------------- MLP ----
 struct MlpShape {
   uint32_t n_layers = 0;          // hidden + 1
@@ -254,6 +283,12 @@ struct MlpWs {
   // fp16-operand first layer: split weights (+ exponents) and row maxima
   DevBuf hhi, hlo, hexp, thi, tlo, texp, amax;
   const float* in_rowmax = nullptr;  // max |input row| from the producer (pool), else computed
+  // first-layer input as fp16 planes from the pooling kernel (3xFP16 GEMMs on
+  // pre-split operands); null: fp32 input
+  const __half* in_hi = nullptr;
+  const __half* in_lo = nullptr;
+  const int* in_exp = nullptr;
+  DevBuf dzh, dzl, dze, dwh, dwl, dwe, cmax, skws;  // layer-1 backward planes, stream-K partials
 };
 // Forward over B instances (input [B][in]); writes preds (sigmoid) and
 // logits; keeps activations in ws for backward.

@@ -5,13 +5,16 @@
 // activation relu/tanh, linear logit head, sigmoid, mean BCE (:34-38,126-135);
 // upstream (p - y)/n with n the worker's minibatch size (:153-155).
 //
-// Round-1 implementation: a tiled fp32 SIMT GEMM (128x128x8 tiles, 8x8 per
-// thread, register double buffering) with fused epilogues (bias+activation,
-// activation derivative, mean-pooling coefficient) and deterministic split-K
-// for the weight gradients; the out=1 head is a warp-per-instance GEMV fused
-// with sigmoid, loss and the upstream gradient. fp32 keeps the stated
-// tolerance against the reference; the tcgen05 (3xTF32) replacement is the
-// next step.
+// GEMMs: the first layer (the wide S*e contraction) runs on the 3xFP16
+// tcgen05 kernel over pre-split fp16 planes (kp_gemm_h3.cu) when the pooling
+// kernel wrote its output as planes, else on the on-chip-split tcgen05
+// kernels (kp_gemm_tc.cu: 3xFP16 forward/dX, 3xTF32 dW); the other layers on
+// 3xTF32 tcgen05. The fp32 SIMT GEMM below (128x128x8 tiles) is the fallback
+// for shapes TMA cannot describe and the accuracy reference of the tests.
+// Epilogues are fused (bias+activation, activation derivative, mean-pooling
+// coefficient); weight gradients use deterministic split-K; the out=1 head
+// is a warp-per-instance GEMV fused with sigmoid, loss and the upstream
+// gradient.
 #include <cstdlib>
 
 #include <cuda_fp16.h>
@@ -396,7 +399,16 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
     float* out = ws.act[l].get<float>((size_t)B * N);
     EpiArgs ep{kBiasAct, m.activation, d_x + m.b_off[l], nullptr, 0, nullptr, 1, 1};
     const float* W = d_x + m.w_off[l];
-    if (l == 0 && use_h(B, N, K, in, W)) {
+    if (l == 0 && ws.in_hi) {
+      // first layer on the pooling kernel's fp16 planes: 3xFP16 on pre-split
+      // operands (kp_gemm_h3.cu), W1 split per row
+      __half* hh = reinterpret_cast<__half*>(ws.hhi.get<uint16_t>((size_t)N * K));
+      __half* hl = reinterpret_cast<__half*>(ws.hlo.get<uint16_t>((size_t)N * K));
+      int* he = ws.hexp.get<int>(N);
+      split_h(W, N, K, K, hh, hl, he, s);
+      h3_gemm(H3Operand{ws.in_hi, ws.in_lo, ws.in_exp, K}, false, H3Operand{hh, hl, he, K}, false, B, N, K,
+              out, N, ep, false, nullptr, s);
+    } else if (l == 0 && use_h(B, N, K, in, W)) {
       // first layer (the wide S*e contraction): fp16 operands, per-row scales
       const float* am = ws.in_rowmax;
       if (!am) {
@@ -540,6 +552,37 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
     const int N = m.widths[l + 1], K = m.widths[l];
     float* dZ = static_cast<float*>(ws.dz[cur].p);
     const float* in = layer_in(l);
+    if (l == 0 && ws.in_hi) {
+      // first layer on fp16 planes (kp_gemm_h3.cu): dX = dZ1 W1 (dZ1 split per
+      // row, W1^T per row), then dW = dZ'^T X over the batch with X's row
+      // scales moved onto dZ' (split per column) and X's planes read MN-major
+      if (d_dinput) {
+        __half* dzh = reinterpret_cast<__half*>(ws.dzh.get<uint16_t>((size_t)B * N));
+        __half* dzl = reinterpret_cast<__half*>(ws.dzl.get<uint16_t>((size_t)B * N));
+        int* dze = ws.dze.get<int>(B);
+        split_rows_h(dZ, B, N, N, dzh, dzl, dze, s);
+        float* wt = ws.wt.get<float>((size_t)N * K);
+        dim3 g(ceil_div(K, 32), ceil_div(N, 32));
+        k_transpose<<<g, dim3(32, 8), 0, s>>>(d_x + m.w_off[l], N, K, wt); ::kp::count_launch();
+        __half* th = reinterpret_cast<__half*>(ws.thi.get<uint16_t>((size_t)N * K));
+        __half* tl = reinterpret_cast<__half*>(ws.tlo.get<uint16_t>((size_t)N * K));
+        int* te = ws.texp.get<int>(K);
+        split_h(wt, K, N, N, th, tl, te, s);
+        EpiArgs ep{d_coeff ? kCoeff : kStore, 0, nullptr, nullptr, 0, d_coeff, S, e};
+        h3_gemm(H3Operand{dzh, dzl, dze, N}, false, H3Operand{th, tl, te, N}, false, B, K, N, d_dinput, K, ep,
+                false, nullptr, s);
+        if (after_dinput) (*after_dinput)();
+      }
+      __half* dwh = reinterpret_cast<__half*>(ws.dwh.get<uint16_t>((size_t)B * N));
+      __half* dwl = reinterpret_cast<__half*>(ws.dwl.get<uint16_t>((size_t)B * N));
+      int* dwe = ws.dwe.get<int>(N);
+      split_cols_scaled_h(dZ, B, N, ws.in_exp, ws.cmax.get<unsigned>(N), dwh, dwl, dwe, s);
+      EpiArgs plain{kStore, 0, nullptr, nullptr, 0, nullptr, 1, 1};
+      h3_gemm(H3Operand{dwh, dwl, dwe, N}, true, H3Operand{ws.in_hi, ws.in_lo, nullptr, K}, true, N, K, B,
+              d_grad + m.w_off[l], K, plain, true, ws.skws.get<float>(h3_splitk_ws_floats(N, K)), s);
+      colsum(dZ, nullptr, B, N, d_grad + m.b_off[l], ws, s);
+      continue;
+    }
     // first layer: the input gradient goes first so its consumer can overlap
     // the weight-gradient GEMM
     if (l == 0 && d_dinput) {

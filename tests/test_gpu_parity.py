@@ -457,6 +457,54 @@ def test_tcgen05_gemm_f16_scaled_accuracy(kp, M, N, K, spread):
     assert err_h < 3 * err_simt + 2e-6, (err_h, err_simt)
 
 
+@pytest.mark.parametrize("M,N,K,spread,engine", [(128, 128, 32, 0, 4), (300, 256, 6400, 0, 4),
+                                                 (1000, 256, 6400, 8, 4), (512, 6400, 256, 4, 4),
+                                                 (65, 40, 96, 0, 4), (4096, 256, 6400, 3, 5),
+                                                 (256, 384, 4096, 2, 5), (777, 208, 64, 1, 4)])
+def test_h3_gemm_nt_accuracy(kp, M, N, K, spread, engine):
+    """3xFP16 on pre-split fp16 planes (kp_gemm_h3.cu, the planes-mode first
+    layer), both operands K-major; engine 5 = deterministic stream-K over K:
+    fp32-level error like the SIMT fp32 GEMM, with rows spanning 2^+-spread,
+    a zero row and tiny elements inside a row."""
+    rng = np.random.default_rng(M * 3 + N + K + spread)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    if spread:
+        A *= (2.0 ** rng.integers(-spread, spread + 1, (M, 1))).astype(np.float32)
+        B *= (2.0 ** rng.integers(-spread, spread + 1, (N, 1))).astype(np.float32)
+        A[0] = 0.0
+        A[1, :K // 2] *= np.float32(1e-6)
+    want = A.astype(np.float64) @ B.astype(np.float64).T
+    scale = np.sqrt(K) * np.maximum(np.abs(A).max(1, keepdims=True), 1e-30) * np.abs(B).max(1)
+    h = kp.gemm_nt(A, B, engine=engine)
+    simt = kp.gemm_nt(A, B, engine=1)
+    err_h = np.max(np.abs(h - want) / scale)
+    err_simt = np.max(np.abs(simt - want) / scale)
+    print(f"h3 nt M={M} N={N} K={K} spread={spread} e{engine}: err={err_h:.3e} simt={err_simt:.3e}")
+    assert err_h < 3 * err_simt + 2e-6, (err_h, err_simt)
+    if engine == 5:  # deterministic: bitwise identical on a rerun
+        assert np.array_equal(kp.gemm_nt(A, B, engine=5), h)
+
+
+@pytest.mark.parametrize("M,N,K,engine", [(256, 6400, 4096, 4), (256, 6400, 4096, 5), (128, 256, 65536, 5),
+                                          (40, 104, 300, 4), (256, 512, 20000, 5), (64, 6400, 2048, 5)])
+def test_h3_gemm_tn_accuracy(kp, M, N, K, engine):
+    """3xFP16 planes with both operands MN-major (the weight gradient dZ'^T X
+    over the batch), one exponent per column, stream-K over the batch."""
+    rng = np.random.default_rng(M * N + K + engine)
+    A = rng.standard_normal((K, M)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    A *= (2.0 ** rng.integers(-3, 4, (1, M))).astype(np.float32)
+    want = A.astype(np.float64).T @ B.astype(np.float64)
+    scale = np.sqrt(K) * np.abs(A).max(0)[:, None] * np.abs(B).max(0)[None, :]
+    tc = kp.gemm_tn(A, B, engine=engine)
+    simt = kp.gemm_tn(A, B, engine=1)
+    err_tc = np.max(np.abs(tc - want) / scale)
+    err_simt = np.max(np.abs(simt - want) / scale)
+    print(f"h3 tn M={M} N={N} K={K} e{engine}: err={err_tc:.3e} simt={err_simt:.3e}")
+    assert err_tc < 3 * err_simt + 2e-6, (err_tc, err_simt)
+
+
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 6400, 4096), (128, 256, 65536), (40, 100, 300)])
 def test_tcgen05_gemm_tn_fp32_accuracy(kp, M, N, K):
     """MN-major operands (the weight gradient dZ^T X over the batch), split-K."""
