@@ -488,13 +488,15 @@ def main():
         # MMA at half the bf16 rate); that pipe work is reported beside it.
         h_on = os.environ.get("KP_GEMM_F16", "1") != "0" and D_in % 8 == 0
         f_l1 = 2.0 * B * D_in * hidden[0]                       # one first-layer GEMM
-        f16_flops = 2 * f_l1 if h_on else 0.0  # layer-1 forward + input gradient
+        # layer 1's forward, input gradient and weight gradient all run 3xFP16
+        # (pre-split planes) unless the fp16 path is off
+        f16_flops = (3 if os.environ.get("KP_GEMM_H3", "1") != "0" else 2) * f_l1 if h_on else 0.0
         tf32_flops = flops - f16_flops
         work = 3.0 * f16_flops + 2 * 3.0 * tf32_flops            # bf16-equivalent MMA flops
         sec = stages["mlp"]["ms_per_step"] / 1e3
         alg = flops / sec / 1e12
-        roof = {"kernel": "mlp stage: tcgen05 GEMMs (3xFP16 per-row scaled on the 6400-wide first "
-                          "layer, 3xTF32 on the rest) + head/bias kernels",
+        roof = {"kernel": "mlp stage: tcgen05 GEMMs (3xFP16 on pre-split fp16 planes for the 6400-wide "
+                          "first layer's forward, dX and dW; 3xTF32 on layer 2) + head/bias kernels",
                 "bound": "tensor", "achieved": alg, "peak": bf16s, "unit": "TFLOP/s",
                 "frac": alg / bf16s, "traffic": traffic.get("mlp"),
                 "peak_kind": f"{pk} bf16 dense sustained",

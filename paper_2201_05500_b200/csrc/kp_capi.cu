@@ -628,10 +628,14 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   uint32_t* bag_of_occ = tr->bag_of_occ.get<uint32_t>(std::max<uint32_t>(sv.n_occ, 1));
   uint32_t* err = tr->err.get<uint32_t>(4);
   prepare_bags(sv.offs, sv.occ_base, sv.slots, sv.n_inst, tr->S, bag_offs, bag_of_occ, err, s);
-  uint32_t h_err = 0xFFFFFFFFu;
-  KP_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, s));
+  // [0] first bad slot id, [1] all-ones iff every bag holds exactly its own
+  // occurrence (one feature per slot), read with dedup's one host sync
+  uint32_t h_errw[2] = {0xFFFFFFFFu, 0};
+  KP_CUDA(cudaMemcpyAsync(h_errw, err, 8, cudaMemcpyDeviceToHost, s));
   dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ, err + 1);  // synchronises the stream
   if (sv.n_occ == 0) KP_CUDA(cudaStreamSynchronize(s));
+  const uint32_t h_err = h_errw[0];
+  const bool ident_bags = h_errw[1] == 0xFFFFFFFFu && sv.n_occ == nb;
   // reject bad slot ids before any state (table, weights) changes
   KP_CHECK(h_err == 0xFFFFFFFFu, kErrConfig,
            "slot ids must be < n_slots and non-decreasing within an instance (occurrence " +
@@ -733,7 +737,7 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
     __half* hi = reinterpret_cast<__half*>(pooled);
     int* iexp = tr->inst_exp.get<int>(std::max<uint32_t>(sv.n_inst, 1));
     pool_planes(bag_offs, sv.n_inst, tr->S, rowocc, pr.src, tr->e, tr->cfg.pooling == 1, hi,
-                hi + (size_t)nb * tr->e, iexp, invc, s);
+                hi + (size_t)nb * tr->e, iexp, invc, s, ident_bags);
   } else {
     // max |row| of the MLP input per instance (fp16-operand first layer)
     float* imax = tr->inst_max.get<float>(std::max<uint32_t>(sv.n_inst, 1));

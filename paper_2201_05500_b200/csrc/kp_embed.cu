@@ -366,6 +366,68 @@ __global__ void __launch_bounds__(NT, NP <= 4 ? 4 : 2) k_pool_planes(const uint3
   }
 }
 
+// The same for the common layout of one feature per slot (bag b = occurrence
+// b, flagged by prepare_bags): no bag offsets, cell c's row is rowocc[inst*S
+// + c / (e/4)], and the next instance's row indices are loaded while this
+// instance's rows are in flight (the index -> row chain is the latency).
+template <int NT, int NP>
+__global__ void __launch_bounds__(NT, 4) k_pool_planes_ident(uint32_t n_inst, uint32_t S,
+                                                             const uint32_t* __restrict__ rowocc,
+                                                             const float* __restrict__ src, uint32_t e,
+                                                             __half* __restrict__ hi, __half* __restrict__ lo,
+                                                             int* __restrict__ inst_exp,
+                                                             float* __restrict__ inv_count, int mean) {
+  __shared__ float red[2][NT / 32];
+  const uint32_t lpr = e >> 2, ncell = S * lpr;
+  uint32_t rr[NP];
+  uint64_t inst = blockIdx.x;
+  auto load_idx = [&](uint64_t i, uint32_t (&r)[NP]) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const uint32_t c = threadIdx.x + p * NT;
+      r[p] = (i < n_inst && c < ncell) ? __ldg(rowocc + i * S + c / lpr) : kNoRow;
+    }
+  };
+  load_idx(inst, rr);
+  for (int it = 0; inst < n_inst; inst += gridDim.x, ++it) {
+    float4 v[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const uint32_t c = threadIdx.x + p * NT;
+      v[p] = rr[p] != kNoRow ? __ldg(reinterpret_cast<const float4*>(src + (uint64_t)rr[p] * e) + c % lpr)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    load_idx(inst + gridDim.x, rr);  // next instance's indices, overlapping the row loads
+    float mx = 0.f;
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[p].x), fabsf(v[p].y)), fmaxf(fabsf(v[p].z), fabsf(v[p].w))));
+#pragma unroll
+    for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if ((threadIdx.x & 31) == 0) red[it & 1][threadIdx.x >> 5] = mx;  // double-buffered: one sync
+    __syncthreads();
+    mx = 0.f;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) mx = fmaxf(mx, red[it & 1][w]);
+    const int ex = tc::row_exp(mx);
+    if (threadIdx.x == 0) inst_exp[inst] = ex;
+    if (mean && threadIdx.x < S) inv_count[inst * S + threadIdx.x] = 1.f;  // one feature per bag
+    const float sc = tc::pow2f(ex);
+    uint2* h2 = reinterpret_cast<uint2*>(hi + inst * ncell * 4);
+    uint2* l2 = reinterpret_cast<uint2*>(lo + inst * ncell * 4);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const uint32_t c = threadIdx.x + p * NT;
+      if (c >= ncell) break;
+      uint2 hh, ll;
+      tc::split_h2(__fmul_rn(v[p].x, sc), __fmul_rn(v[p].y, sc), hh.x, ll.x);
+      tc::split_h2(__fmul_rn(v[p].z, sc), __fmul_rn(v[p].w, sc), hh.y, ll.y);
+      h2[c] = hh;
+      l2[c] = ll;
+    }
+  }
+}
+
 __global__ void k_compose(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ inverse,
                           uint32_t n, uint32_t* __restrict__ out) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -691,10 +753,21 @@ bool pool_planes_supported(uint32_t S, uint32_t e) {
 
 void pool_planes(const uint32_t* d_bag_offs, uint32_t n_inst, uint32_t S, const uint32_t* d_row_of_occ,
                  const float* d_src, uint32_t e, bool mean, __half* d_hi, __half* d_lo, int* d_inst_exp,
-                 float* d_inv_count, cudaStream_t s) {
+                 float* d_inv_count, cudaStream_t s, bool ident) {
   KP_CHECK(pool_planes_supported(S, e), kErrConfig, "pool_planes: unsupported S*e");
   if (n_inst == 0) return;
   const uint32_t cells = S * e / 4;
+  if (ident && cells > 256 && cells <= 256 * 8 && S <= 256) {
+    const unsigned grid = (unsigned)std::min<uint64_t>(n_inst, 148ull * 4);
+    if (cells <= 256 * 4)
+      k_pool_planes_ident<256, 4><<<grid, 256, 0, s>>>(n_inst, S, d_row_of_occ, d_src, e, d_hi, d_lo, d_inst_exp,
+                                                        d_inv_count, mean ? 1 : 0);
+    else
+      k_pool_planes_ident<256, 8><<<grid, 256, 0, s>>>(n_inst, S, d_row_of_occ, d_src, e, d_hi, d_lo, d_inst_exp,
+                                                        d_inv_count, mean ? 1 : 0);
+    ::kp::count_launch();
+    return;
+  }
   const unsigned grid = (unsigned)std::min<uint64_t>(n_inst, 148ull * 64);
   // threads per instance: the cells rounded up to warps (<= 256), then the
   // fewest float4 cells per thread that cover the row

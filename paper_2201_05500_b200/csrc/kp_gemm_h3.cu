@@ -55,11 +55,23 @@ constexpr int H3_WARPS = 20;  // warpgroup 0: producer, MMA, 2 idle; warpgroups 
 constexpr int H3_EPI_T = 512;
 constexpr uint32_t H3_PLANE = H3_BM * H3_BK * 2;  // 8 KB: one plane tile per CTA
 constexpr uint32_t H3_STAGE = 4 * H3_PLANE;       // A hi, A lo, B hi, B lo
-constexpr uint32_t H3_EPI = 16 * 2 * 2048;        // per epilogue warp two 32x16 fp32 store tiles
+constexpr uint32_t H3_EPI = 16 * 4096;            // per epilogue warp one 32x32 fp32 store tile
 // register split (setmaxnreg, per warpgroup): the epilogue holds 64 fp32
 // running sums per thread; the TMA / MMA warps need few
-constexpr int H3_REG_LO = 56, H3_REG_HI = 112;
-constexpr uint32_t H3_SMEM = H3_NS * H3_STAGE + H3_EPI + 1024 + 256;
+constexpr int H3_REG_LO = 40, H3_REG_HI = 104;  // 128*40 + 512*104 <= 640*96 (the CTA pool)
+constexpr uint32_t H3_COLP = 16 * 2 * 64 * 4;  // per epilogue warp: 64 column scales + 64 biases
+constexpr uint32_t H3_SMEM = H3_NS * H3_STAGE + H3_EPI + H3_COLP + 1024 + 256;
+// A-resident mode (K <= 256, e.g. dX = dZ1 W1 with K = 256, N = 6400): the
+// unit's whole A (128 rows x 256 k, both planes: 128 KB) stays in shared
+// memory while the unit walks consecutive n-blocks, so only B streams (half
+// the L2->SM bytes per tile); B stages are 16 KB, the epilogue store tiles
+// single-buffered to fit.
+constexpr int H3_AR_MAXKB = 8;
+constexpr uint32_t H3_AR_A = H3_AR_MAXKB * 2 * H3_PLANE;  // 128 KB
+constexpr int H3_AR_NS = 1;
+constexpr uint32_t H3_AR_STAGE = 2 * H3_PLANE;
+constexpr uint32_t H3_AR_SMEM = H3_AR_A + H3_AR_NS * H3_AR_STAGE + H3_EPI + H3_COLP + 1024 + 256;
+static_assert(H3_AR_SMEM <= 232448, "A-resident smem");
 constexpr int H3_VUNITS = 148;  // stream-K virtual units (partition independent of the grid)
 
 struct H3Args {
@@ -68,6 +80,8 @@ struct H3Args {
   int splitk;                    // stream-K over H3_VUNITS virtual units
   const int* ea;                 // per-row exponents of A (nullable = 0)
   const int* eb;                 // per-row exponents of B (nullable = 0)
+  int keep_a, keep_b;            // L2 policy per operand: 1 evict_last (re-read), 0 evict_first
+  int dbg;                       // timing experiments only (KP_H3_DBG): 1 no stores, 2 no drain
   int mode;                      // 0 store, 1 act(x + bias[n]), 3 x * coeff[m*S + n/e]
   int act;
   const float* bias;
@@ -82,24 +96,25 @@ __device__ __forceinline__ int64_t vstart(int64_t v, int64_t T) { return v * T /
 // (whole tiles w = unit, unit+units, ...) or stream-K (the virtual units
 // v = unit, unit+units, ... each own [vstart(v), vstart(v+1)) of the
 // flattened tile x k-block space; segment id = tile + v is unique).
+template <bool SK>
 struct SegIter {
-  int tiles, nk, splitk, units;
-  int64_t T;
+  int tiles, nk, units;
   int v;  // current virtual unit (stream-K) / tile (DP)
-  int64_t t, tend;
-  __device__ SegIter(const H3Args& a, int unit, int units_)
-      : tiles(a.nblocks_m * a.nblocks_n), nk(a.nk), splitk(a.splitk), units(units_) {
-    T = (int64_t)tiles * nk;
+  int64_t T, t, tend;
+  __device__ SegIter(const H3Args& a, int unit, int units_) : tiles(a.nblocks_m * a.nblocks_n), nk(a.nk), units(units_) {
     v = unit;
-    t = tend = 0;
-    if (splitk && v < H3_VUNITS) {
-      t = vstart(v, T);
-      tend = vstart(v + 1, T);
+    if constexpr (SK) {
+      T = (int64_t)tiles * nk;
+      t = tend = 0;
+      if (v < H3_VUNITS) {
+        t = vstart(v, T);
+        tend = vstart(v + 1, T);
+      }
     }
   }
   // next segment: tile index, [kb0, kb1), segment id; false when done
   __device__ bool next(int& tile, int& kb0, int& kb1, int& sid) {
-    if (!splitk) {
+    if constexpr (!SK) {
       if (v >= tiles) return false;
       tile = v;
       kb0 = 0;
@@ -107,20 +122,21 @@ struct SegIter {
       sid = v;
       v += units;
       return true;
+    } else {
+      while (t >= tend) {
+        v += units;
+        if (v >= H3_VUNITS) return false;
+        t = vstart(v, T);
+        tend = vstart(v + 1, T);
+      }
+      tile = (int)(t / nk);
+      kb0 = (int)(t % nk);
+      const int64_t e = kb0 + (tend - t);
+      kb1 = (int)(e < nk ? e : nk);
+      sid = tile + v;
+      t += kb1 - kb0;
+      return true;
     }
-    while (t >= tend) {
-      v += units;
-      if (v >= H3_VUNITS) return false;
-      t = vstart(v, T);
-      tend = vstart(v + 1, T);
-    }
-    tile = (int)(t / nk);
-    kb0 = (int)(t % nk);
-    const int64_t e = kb0 + (tend - t);
-    kb1 = (int)(e < nk ? e : nk);
-    sid = tile + v;
-    t += kb1 - kb0;
-    return true;
   }
 };
 
@@ -134,12 +150,13 @@ __device__ __forceinline__ float act_fwd(int act, float z) { return act == 0 ? (
 
 // one plane tile (this CTA's 128 rows x 32 k) of a K-major or MN-major operand
 template <bool MN>
-__device__ __forceinline__ void load_plane(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int k0, int r0) {
+__device__ __forceinline__ void load_plane(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int k0, int r0,
+                                           uint64_t pol) {
   if (MN) {  // two 64(mn) x 32(k) SW128 boxes, LBO = 4 KB apart
-    tma_load_2d(dst, map, bar, r0, k0);
-    tma_load_2d(dst + 4096, map, bar, r0 + 64, k0);
+    tma_load_2d_hint(dst, map, bar, r0, k0, pol);
+    tma_load_2d_hint(dst + 4096, map, bar, r0 + 64, k0, pol);
   } else {   // one 32(k) x 128(rows) SW64 box
-    tma_load_2d(dst, map, bar, k0, r0);
+    tma_load_2d_hint(dst, map, bar, k0, r0, pol);
   }
 }
 template <bool MN>
@@ -147,29 +164,46 @@ __device__ __forceinline__ uint64_t plane_desc(uint32_t base, int kk) {
   return MN ? sdesc_mn128(base + (uint32_t)kk * 2048u, 4096u) : sdesc_k64(base + (uint32_t)kk * 32u);
 }
 
-template <bool AMN, bool BMN>
+// A-resident units: a contiguous range of tiles (n-block fastest), A reloaded
+// whenever the m-block changes
+__device__ __forceinline__ void ar_range(const H3Args& a, int unit, int units, int& t0, int& t1) {
+  const int64_t T = (int64_t)a.nblocks_m * a.nblocks_n;
+  t0 = (int)(T * unit / units);
+  t1 = (int)(T * (unit + 1) / units);
+}
+
+template <bool AMN, bool BMN, bool AR, bool SK>
 __global__ void __launch_bounds__(H3_WARPS * 32, 1)
     k_h3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
          const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
          const __grid_constant__ CUtensorMap tmC, H3Args a) {
+  static_assert(!AR || !AMN, "A-resident mode: K-major A");
+  constexpr int NS = AR ? H3_AR_NS : H3_NS;
+  constexpr uint32_t STAGE = AR ? H3_AR_STAGE : H3_STAGE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* epi = smem + H3_NS * H3_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + H3_EPI);
+  uint8_t* ares = smem;                       // (AR) resident A: [kb][hi|lo] plane tiles
+  uint8_t* stages = smem + (AR ? H3_AR_A : 0);
+  uint8_t* epi = stages + NS * STAGE;
+  float* colp = reinterpret_cast<float*>(epi + H3_EPI);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(colp) + H3_COLP);
   uint64_t* full = bars;              // TMA -> MMA (local)
-  uint64_t* conv = bars + H3_NS;      // peer's TMA landed -> leader's MMA (1 arrival)
-  uint64_t* empty = bars + 2 * H3_NS; // MMA done with stage -> producers (both CTAs)
-  uint64_t* tfull = bars + 3 * H3_NS; // chunk accumulated -> drains (both CTAs)
+  uint64_t* conv = bars + NS;         // peer's TMA landed -> leader's MMA (1 arrival)
+  uint64_t* empty = bars + 2 * NS;    // MMA done with stage -> producers (both CTAs)
+  uint64_t* tfull = bars + 3 * NS;    // chunk accumulated -> drains (both CTAs)
   uint64_t* tempty = tfull + 2;       // drained -> MMA (leader; 2 arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* afull = tempty + 2;       // (AR) resident A landed (local)
+  uint64_t* aconv = afull + 1;        // (AR) peer's A landed -> leader
+  uint64_t* afree = aconv + 1;        // (AR) MMAs done with the resident A (both CTAs)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afree + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int unit = blockIdx.x >> 1, units = gridDim.x >> 1;
-  auto sAh = [&](int s) { return smem + s * H3_STAGE; };
+  auto sAh = [&](int s) { return stages + s * STAGE; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < H3_NS; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&conv[s], 1);
       mbar_init(&empty[s], 1);
@@ -178,6 +212,9 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 2);
     }
+    mbar_init(afull, 1);
+    mbar_init(aconv, 1);
+    mbar_init(afree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
@@ -196,7 +233,37 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       prefetch_map(&tmAl);
       prefetch_map(&tmBh);
       prefetch_map(&tmBl);
-      SegIter it(a, unit, units);
+      // the operand re-read across tiles stays in L2, the streamed one goes first
+      const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
+      const uint64_t pa = a.keep_a ? pol_keep : pol_stream, pb = a.keep_b ? pol_keep : pol_stream;
+      if constexpr (AR) {
+        int t0, t1, g = 0, prev_mb = -1, na = 0;
+        ar_range(a, unit, units, t0, t1);
+        for (int tile = t0; tile < t1; ++tile) {
+          int mb, nb;
+          tile_mn(a, tile, mb, nb);
+          const int n0 = nb * H3_BN + (int)rank * (H3_BN / 2);
+          if (mb != prev_mb) {  // (re)load the resident A once its previous MMAs are done
+            const int m0 = mb * 2 * H3_BM + (int)rank * H3_BM;
+            if (na > 0) mbar_wait(afree, (na - 1) & 1);
+            mbar_expect_tx(afull, 2u * a.nk * H3_PLANE);
+            for (int kb = 0; kb < a.nk; ++kb) {
+              load_plane<false>(ares + (2 * kb) * H3_PLANE, &tmAh, afull, kb * H3_BK, m0, pa);
+              load_plane<false>(ares + (2 * kb + 1) * H3_PLANE, &tmAl, afull, kb * H3_BK, m0, pa);
+            }
+            prev_mb = mb;
+            ++na;
+          }
+          for (int kb = 0; kb < a.nk; ++kb, ++g) {
+            const int s = g % NS;
+            if (g >= NS) mbar_wait(&empty[s], ((g / NS) & 1) ^ 1);
+            mbar_expect_tx(&full[s], STAGE);
+            load_plane<BMN>(sAh(s), &tmBh, &full[s], kb * H3_BK, n0, pb);
+            load_plane<BMN>(sAh(s) + H3_PLANE, &tmBl, &full[s], kb * H3_BK, n0, pb);
+          }
+        }
+      } else {
+      SegIter<SK> it(a, unit, units);
       int tile, kb0, kb1, sid, g = 0;
       while (it.next(tile, kb0, kb1, sid)) {
         int mb, nb;
@@ -204,30 +271,69 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
         const int m0 = mb * 2 * H3_BM + (int)rank * H3_BM;
         const int n0 = nb * H3_BN + (int)rank * (H3_BN / 2);
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
-          const int s = g % H3_NS;
-          if (g >= H3_NS) mbar_wait(&empty[s], ((g / H3_NS) & 1) ^ 1);
-          mbar_expect_tx(&full[s], H3_STAGE);
+          const int s = g % NS;
+          if (g >= NS) mbar_wait(&empty[s], ((g / NS) & 1) ^ 1);
+          mbar_expect_tx(&full[s], STAGE);
           uint8_t* st = sAh(s);
-          load_plane<AMN>(st, &tmAh, &full[s], kb * H3_BK, m0);
-          load_plane<AMN>(st + H3_PLANE, &tmAl, &full[s], kb * H3_BK, m0);
-          load_plane<BMN>(st + 2 * H3_PLANE, &tmBh, &full[s], kb * H3_BK, n0);
-          load_plane<BMN>(st + 3 * H3_PLANE, &tmBl, &full[s], kb * H3_BK, n0);
+          load_plane<AMN>(st, &tmAh, &full[s], kb * H3_BK, m0, pa);
+          load_plane<AMN>(st + H3_PLANE, &tmAl, &full[s], kb * H3_BK, m0, pa);
+          load_plane<BMN>(st + 2 * H3_PLANE, &tmBh, &full[s], kb * H3_BK, n0, pb);
+          load_plane<BMN>(st + 3 * H3_PLANE, &tmBl, &full[s], kb * H3_BK, n0, pb);
         }
+      }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ---- MMA issuer (leader CTA): both CTAs' tiles, M = 256
       constexpr uint32_t idesc = idesc_f16(AMN, BMN, 2 * H3_BM, H3_BN);
-      SegIter it(a, unit, units);
+      if constexpr (AR) {
+        int t0, t1, g = 0, c = 0, prev_mb = -1, na = 0;
+        ar_range(a, unit, units, t0, t1);
+        for (int tile = t0; tile < t1; ++tile, ++c) {
+          int mb, nb;
+          tile_mn(a, tile, mb, nb);
+          if (mb != prev_mb) {
+            mbar_wait(afull, na & 1);
+            mbar_wait(aconv, na & 1);
+            prev_mb = mb;
+            ++na;
+          }
+          const int buf = c & 1;
+          if (c >= 2) mbar_wait(&tempty[buf], ((c >> 1) - 1) & 1);
+          const uint32_t d = tmem + (uint32_t)(buf * H3_BN);
+          for (int kb = 0; kb < a.nk; ++kb, ++g) {
+            const int s = g % NS;
+            mbar_wait(&full[s], (g / NS) & 1);
+            mbar_wait(&conv[s], (g / NS) & 1);
+            fence_after();
+            const uint32_t ah = smem_u32(ares) + 2u * kb * H3_PLANE, al = ah + H3_PLANE;
+            const uint32_t bh = smem_u32(sAh(s)), bl = bh + H3_PLANE;
+#pragma unroll
+            for (int kk = 0; kk < H3_BK / 16; ++kk) {
+              const uint64_t dah = plane_desc<false>(ah, kk), dal = plane_desc<false>(al, kk);
+              const uint64_t dbh = plane_desc<BMN>(bh, kk), dbl = plane_desc<BMN>(bl, kk);
+              mma_f16_pair(d, dah, dbh, idesc, (kb | kk) != 0);
+              mma_f16_pair(d, dah, dbl, idesc, 1);
+              mma_f16_pair(d, dal, dbh, idesc, 1);
+            }
+            commit_pair(&empty[s]);
+          }
+          commit_pair(&tfull[buf]);
+          int nmb = -1, nnb;
+          if (tile + 1 < t1) tile_mn(a, tile + 1, nmb, nnb);
+          if (nmb != mb) commit_pair(afree);  // the resident A may be replaced
+        }
+      } else {
+      SegIter<SK> it(a, unit, units);
       int tile, kb0, kb1, sid, g = 0, c = 0;
       while (it.next(tile, kb0, kb1, sid)) {
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
-          const int s = g % H3_NS;
+          const int s = g % NS;
           const int kin = (kb - kb0) % H3_CH, buf = c & 1;
           if (kin == 0 && c >= 2) mbar_wait(&tempty[buf], ((c >> 1) - 1) & 1);
-          mbar_wait(&full[s], (g / H3_NS) & 1);
-          mbar_wait(&conv[s], (g / H3_NS) & 1);
+          mbar_wait(&full[s], (g / NS) & 1);
+          mbar_wait(&conv[s], (g / NS) & 1);
           fence_after();
           const uint32_t d = tmem + (uint32_t)(buf * H3_BN);
           const uint32_t ah = smem_u32(sAh(s)), al = ah + H3_PLANE, bh = ah + 2 * H3_PLANE,
@@ -247,16 +353,37 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
           }
         }
       }
+      }
     } else if (lane == 0) {
       // ---- peer CTA: relay "my TMA landed" to the leader's MMA issuer
-      SegIter it(a, unit, units);
+      if constexpr (AR) {
+        int t0, t1, g = 0, prev_mb = -1, na = 0;
+        ar_range(a, unit, units, t0, t1);
+        for (int tile = t0; tile < t1; ++tile) {
+          int mb, nb;
+          tile_mn(a, tile, mb, nb);
+          if (mb != prev_mb) {
+            mbar_wait(afull, na & 1);
+            mbar_arrive_leader(aconv);
+            prev_mb = mb;
+            ++na;
+          }
+          for (int kb = 0; kb < a.nk; ++kb, ++g) {
+            const int s = g % NS;
+            mbar_wait(&full[s], (g / NS) & 1);
+            mbar_arrive_leader(&conv[s]);
+          }
+        }
+      } else {
+      SegIter<SK> it(a, unit, units);
       int tile, kb0, kb1, sid, g = 0;
       while (it.next(tile, kb0, kb1, sid))
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
-          const int s = g % H3_NS;
-          mbar_wait(&full[s], (g / H3_NS) & 1);
+          const int s = g % NS;
+          mbar_wait(&full[s], (g / NS) & 1);
           mbar_arrive_leader(&conv[s]);
         }
+      }
     }
   }
   } else {
@@ -265,14 +392,34 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
     const int q = warp & 3, cq = (warp - 4) >> 2;
     const int et = threadIdx.x - 128;
     uint8_t* dense_base = epi + (warp - 4) * 4096;
-    uint32_t tma_seq = 0;
-    SegIter it(a, unit, units);
+    SegIter<SK> it(a, unit, units);
+    int ar_t = 0, ar_t1 = 0;
+    if constexpr (AR) ar_range(a, unit, units, ar_t, ar_t1);
     int tile, kb0, kb1, sid, c = 0;
-    while (it.next(tile, kb0, kb1, sid)) {
+    for (;;) {
+      if constexpr (AR) {
+        if (ar_t >= ar_t1) break;
+        tile = sid = ar_t++;
+        kb0 = 0;
+        kb1 = a.nk;
+      } else {
+        if (!it.next(tile, kb0, kb1, sid)) break;
+      }
       int mb, nb;
       tile_mn(a, tile, mb, nb);
       const int mrow0 = mb * 2 * H3_BM + (int)rank * H3_BM + q * 32;  // this warp's 32 rows
       const int ncol0 = nb * H3_BN + cq * 64;                          // this warp's 64 columns
+      // column scales / biases and the row scale, loaded while the MMAs run
+      float* csb = colp + (warp - 4) * 128;
+      __syncwarp();  // the previous tile's epilogue is done reading csb
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int nn = min(ncol0 + lane + 32 * h, a.N - 1);
+        csb[lane + 32 * h] = a.eb ? pow2f(-__ldg(a.eb + nn)) : 1.f;
+        csb[64 + lane + 32 * h] = a.mode == 1 ? __ldg(a.bias + nn) : 0.f;
+      }
+      const int m = mrow0 + lane;
+      const float sa = (a.ea && m < a.M) ? pow2f(-__ldg(a.ea + m)) : 1.f;
       float acc[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) acc[j] = 0.f;
@@ -284,8 +431,13 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
 #pragma unroll
         for (int c0 = 0; c0 < 64; c0 += 16) {
           uint32_t r[16];
-          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * H3_BN + cq * 64 + c0), r);
-          tmem_ld_wait();
+          if (a.dbg == 2) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = 0;
+          } else {
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * H3_BN + cq * 64 + c0), r);
+            tmem_ld_wait();
+          }
 #pragma unroll
           for (int j = 0; j < 16; ++j) acc[c0 + j] = __fadd_rn(acc[c0 + j], __uint_as_float(r[j]));
         }
@@ -293,41 +445,47 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
         named_sync(1, H3_EPI_T);
         if (et == 0) mbar_arrive_leader(&tempty[buf]);
       }
-      // epilogue: row per lane; exact power-of-two unscaling, then the op
-      const int m = mrow0 + lane;
-      const float sa = (a.ea && m < a.M) ? pow2f(-__ldg(a.ea + m)) : 1.f;
+      // epilogue: row per lane; exact power-of-two unscaling, then the op;
+      // two 32x32 fp32 boxes per warp (SWIZZLE_128B: lane = row, its eight
+      // 16-byte chunks at chunk ^ (row & 7), conflict-free), one TMA store each
+      __syncwarp();  // csb visible to the warp
+      const uint32_t dense = smem_u32(dense_base);
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 16) {
-        uint8_t* dense = dense_base + (tma_seq & 1) * 2048;
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        __syncwarp();
+      for (int h = 0; h < 2; ++h) {
+        const int c0 = 32 * h;
         const int n = ncol0 + c0;
-        float v[16];
+        float* v = acc + c0;  // transformed in place (registers)
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int nn = min(n + j, a.N - 1);
-          const float sb = a.eb ? pow2f(-__ldg(a.eb + nn)) : 1.f;
-          v[j] = __fmul_rn(__fmul_rn(acc[c0 + j], sa), sb);
-          if (a.mode == 1) v[j] = act_fwd(a.act, __fadd_rn(v[j], __ldg(a.bias + nn)));
+        for (int j = 0; j < 32; ++j) {
+          v[j] = __fmul_rn(__fmul_rn(v[j], sa), csb[c0 + j]);
+          if (a.mode == 1) v[j] = act_fwd(a.act, __fadd_rn(v[j], csb[64 + c0 + j]));
         }
-        if (a.mode == 3) {
+        if (a.mode == 3) {  // mean-pooling coefficient of the column's slot (few distinct per box)
           const float* cp = a.coeff + (size_t)min(m, a.M - 1) * a.S;
+          int slot = -1;
+          float cf = 1.f;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], __ldg(cp + min(n + j, a.N - 1) / a.e));
+          for (int j = 0; j < 32; ++j) {
+            const int sj = min(n + j, a.N - 1) / (int)a.e;
+            if (sj != slot) slot = sj, cf = __ldg(cp + sj);
+            v[j] = __fmul_rn(v[j], cf);
+          }
         }
+        // the previous box has been read out of shared memory
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          *reinterpret_cast<float4*>(dense + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4)) =
-              make_float4(v[4 * cc], v[4 * cc + 1], v[4 * cc + 2], v[4 * cc + 3]);
+        for (int cc = 0; cc < 8; ++cc)
+          st_shared_v4(dense + lane * 128 + ((cc ^ (lane & 7)) << 4), v[4 * cc], v[4 * cc + 1], v[4 * cc + 2],
+                       v[4 * cc + 3]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) {
-          if (a.splitk)  // partial tile of segment sid: rows sid*256 + local row
-            tma_store_2d(&tmC, dense, cq * 64 + c0, sid * 2 * H3_BM + (int)rank * H3_BM + q * 32);
+        if (lane == 0 && a.dbg != 1) {
+          if (SK)  // partial tile of segment sid: rows sid*256 + local row
+            tma_store_2d(&tmC, dense_base, cq * 64 + c0, sid * 2 * H3_BM + (int)rank * H3_BM + q * 32);
           else
-            tma_store_2d(&tmC, dense, n, mrow0);
+            tma_store_2d(&tmC, dense_base, n, mrow0);
         }
-        ++tma_seq;
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -383,22 +541,34 @@ bool map_plane(CUtensorMap* m, const __half* p, uint64_t rows, uint64_t cols, ui
             CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-// fp32 [rows][cols] output, 16 x 32 boxes, SW64 (the epilogue's dense tiles)
+// fp32 [rows][cols] output, 32 x 32 boxes, SW128 (the epilogue's store tiles)
 bool map_out(CUtensorMap* m, float* p, uint64_t rows, uint64_t cols, uint64_t ld) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {ld * 4};
-  cuuint32_t box[2] = {16, 32};
+  cuuint32_t box[2] = {32, 32};
   cuuint32_t es[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 thread_local int g_h3_reserve = 0;
 
+template <bool AMN, bool BMN, bool AR, bool SK>
+void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, float* ws,
+                 const H3Args& a0, cudaStream_t s);
+// stream-K and data-parallel variants are separate kernels (no 64-bit
+// stream-K state in the data-parallel ones)
 template <bool AMN, bool BMN>
+void launch_h3(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, bool splitk,
+               float* ws, const H3Args& a, cudaStream_t s) {
+  if (splitk) launch_h3_t<AMN, BMN, false, true>(A, B, M, N, K, C, ldc, ws, a, s);
+  else launch_h3_t<AMN, BMN, false, false>(A, B, M, N, K, C, ldc, ws, a, s);
+}
+
+template <bool AMN, bool BMN, bool AR, bool SK>
 int h3_units() {
   static int units = 0;
   if (units) return units;
@@ -409,7 +579,7 @@ int h3_units() {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(4, 1, 1);
   cfg.blockDim = dim3(H3_WARPS * 32, 1, 1);
-  cfg.dynamicSmemBytes = H3_SMEM;
+  cfg.dynamicSmemBytes = AR ? H3_AR_SMEM : H3_SMEM;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
@@ -418,14 +588,15 @@ int h3_units() {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_h3<AMN, BMN>, &cfg) == cudaSuccess && n > 0) units = std::min(units, n);
+  if (cudaOccupancyMaxActiveClusters(&n, k_h3<AMN, BMN, AR, SK>, &cfg) == cudaSuccess && n > 0) units = std::min(units, n);
   cudaGetLastError();
   return units;
 }
 
-template <bool AMN, bool BMN>
-void launch_h3(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, bool splitk,
-               float* ws, const H3Args& a0, cudaStream_t s) {
+template <bool AMN, bool BMN, bool AR, bool SK>
+void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, float* ws,
+                 const H3Args& a0, cudaStream_t s) {
+  constexpr bool splitk = SK;
   CUtensorMap tah, tal, tbh, tbl, tcm;
   // K-major operand [rows][K]; MN-major [K][rows]
   auto mk = [&](CUtensorMap* m, const __half* p, const H3Operand& op, int rows, bool mn) {
@@ -451,21 +622,22 @@ void launch_h3(const H3Operand& A, const H3Operand& B, int M, int N, int K, floa
     ok = ok && map_out(&tcm, C, M, N, ldc);
   }
   KP_CHECK(ok, kErrCuda, "cuTensorMapEncodeTiled failed (3xFP16 GEMM operands)");
+  constexpr uint32_t SMEM = AR ? H3_AR_SMEM : H3_SMEM;
   static std::atomic<uint64_t> attr{0};
   int dev = 0;
   KP_CUDA(cudaGetDevice(&dev));
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr.load(std::memory_order_acquire) & bit)) {
-    KP_CUDA(cudaFuncSetAttribute(k_h3<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, H3_SMEM));
+    KP_CUDA(cudaFuncSetAttribute(k_h3<AMN, BMN, AR, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     attr.fetch_or(bit, std::memory_order_release);
   }
-  const int units_all = std::max(1, h3_units<AMN, BMN>() - (g_h3_reserve + 1) / 2);
+  const int units_all = std::max(1, h3_units<AMN, BMN, AR, SK>() - (g_h3_reserve + 1) / 2);
   const int work = splitk ? H3_VUNITS : tiles;
   const unsigned grid = (unsigned)std::min(work, units_all) * 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(H3_WARPS * 32, 1, 1);
-  cfg.dynamicSmemBytes = H3_SMEM;
+  cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -474,7 +646,7 @@ void launch_h3(const H3Operand& A, const H3Operand& B, int M, int N, int K, floa
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  KP_CUDA(cudaLaunchKernelEx(&cfg, k_h3<AMN, BMN>, tah, tal, tbh, tbl, tcm, a));
+  KP_CUDA(cudaLaunchKernelEx(&cfg, k_h3<AMN, BMN, AR, SK>, tah, tal, tbh, tbl, tcm, a));
   ::kp::count_launch();
   if (splitk) {
     const int64_t T = (int64_t)tiles * a.nk;
@@ -515,40 +687,56 @@ __global__ void k_split_rows(const float* __restrict__ x, int rows, int K, int l
 // dW's A operand: D[b][o] = dZ[b][o] * 2^-xe[b] (X's row scale moved onto the
 // other factor, so the sum over b needs no per-k scale), split with a scale
 // per COLUMN o (the GEMM row of dW): pass 1 column maxima, pass 2 planes.
+// Layout for both: a thread owns 4 consecutive columns (float4) of a row,
+// blockDim.x = N/4 threads span a row, blockDim.y rows per block step.
 __global__ void k_colmax_scaled(const float* __restrict__ dz, int B, int N, const int* __restrict__ xe,
                                 unsigned* __restrict__ cmax) {
-  // block = 256 columns (thread per column), rows strided by gridDim.y
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  float mx = 0.f;
-  for (int b = blockIdx.y; b < B; b += gridDim.y)
-    mx = fmaxf(mx, fabsf(__fmul_rn(dz[(size_t)b * N + n], xe ? pow2f(-__ldg(xe + b)) : 1.f)));
-  if (mx > 0.f) atomicMax(cmax + n, __float_as_uint(mx));
+  __shared__ float red[1024];  // [blockDim.y][4 * blockDim.x] <= 1024
+  const int n4 = blockIdx.y * blockDim.x + threadIdx.x;  // column quad (slab blockIdx.y)
+  const bool in = n4 < N / 4;
+  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int b = blockIdx.x * blockDim.y + threadIdx.y; in && b < B; b += gridDim.x * blockDim.y) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(dz + (size_t)b * N) + n4);
+    const float xs = xe ? pow2f(-__ldg(xe + b)) : 1.f;
+    mx.x = fmaxf(mx.x, fabsf(__fmul_rn(v.x, xs)));
+    mx.y = fmaxf(mx.y, fabsf(__fmul_rn(v.y, xs)));
+    mx.z = fmaxf(mx.z, fabsf(__fmul_rn(v.z, xs)));
+    mx.w = fmaxf(mx.w, fabsf(__fmul_rn(v.w, xs)));
+  }
+  const int W = 4 * blockDim.x;  // slab width (columns)
+  float* rr = red + threadIdx.y * W + 4 * threadIdx.x;
+  rr[0] = mx.x, rr[1] = mx.y, rr[2] = mx.z, rr[3] = mx.w;
+  __syncthreads();
+  for (int c = threadIdx.y * blockDim.x + threadIdx.x; c < W; c += blockDim.x * blockDim.y) {
+    float m = 0.f;
+    for (int r = 0; r < (int)blockDim.y; ++r) m = fmaxf(m, red[r * W + c]);
+    const int col = blockIdx.y * W + c;
+    if (m > 0.f && col < N) atomicMax(cmax + col, __float_as_uint(m));
+  }
 }
 __global__ void k_split_cols_scaled(const float* __restrict__ dz, int B, int N, const int* __restrict__ xe,
                                     const unsigned* __restrict__ cmax, __half* __restrict__ hi,
                                     __half* __restrict__ lo, int* __restrict__ exps) {
-  const int n2 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;  // column pair
-  if (n2 >= N) return;
-  const int e0 = row_exp(__uint_as_float(cmax[n2])), e1 = n2 + 1 < N ? row_exp(__uint_as_float(cmax[n2 + 1])) : 0;
-  if (blockIdx.y == 0) {
-    exps[n2] = e0;
-    if (n2 + 1 < N) exps[n2 + 1] = e1;
+  const int n4 = blockIdx.y * blockDim.x + threadIdx.x;
+  if (n4 >= N / 4) return;
+  int ex[4];
+  float sc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    ex[j] = row_exp(__uint_as_float(cmax[4 * n4 + j]));
+    sc[j] = pow2f(ex[j]);
   }
-  const float s0 = pow2f(e0), s1 = pow2f(e1);
-  for (int b = blockIdx.y; b < B; b += gridDim.y) {
+  if (blockIdx.x == 0 && threadIdx.y == 0)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) exps[4 * n4 + j] = ex[j];
+  for (int b = blockIdx.x * blockDim.y + threadIdx.y; b < B; b += gridDim.x * blockDim.y) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(dz + (size_t)b * N) + n4);
     const float xs = xe ? pow2f(-__ldg(xe + b)) : 1.f;
-    const float x0 = __fmul_rn(__fmul_rn(dz[(size_t)b * N + n2], xs), s0);
-    const float x1 = n2 + 1 < N ? __fmul_rn(__fmul_rn(dz[(size_t)b * N + n2 + 1], xs), s1) : 0.f;
-    uint32_t h, l;
-    split_h2(x0, x1, h, l);
-    if (n2 + 1 < N) {
-      *reinterpret_cast<uint32_t*>(hi + (size_t)b * N + n2) = h;
-      *reinterpret_cast<uint32_t*>(lo + (size_t)b * N + n2) = l;
-    } else {
-      hi[(size_t)b * N + n2] = __ushort_as_half((unsigned short)(h & 0xFFFF));
-      lo[(size_t)b * N + n2] = __ushort_as_half((unsigned short)(l & 0xFFFF));
-    }
+    uint2 h, l;
+    split_h2(__fmul_rn(__fmul_rn(v.x, xs), sc[0]), __fmul_rn(__fmul_rn(v.y, xs), sc[1]), h.x, l.x);
+    split_h2(__fmul_rn(__fmul_rn(v.z, xs), sc[2]), __fmul_rn(__fmul_rn(v.w, xs), sc[3]), h.y, l.y);
+    reinterpret_cast<uint2*>(hi + (size_t)b * N)[n4] = h;
+    reinterpret_cast<uint2*>(lo + (size_t)b * N)[n4] = l;
   }
 }
 
@@ -575,8 +763,15 @@ bool h3_supported(int M, int N, int K, const H3Operand& A, const H3Operand& B) {
 
 // C[m][n] = epi(sum_k A(m,k) B(n,k)); A/B K-major ([rows][K]) unless *_mn
 void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M, int N, int K, float* C,
-             int ldc, const GemmEpi& ep, bool splitk, float* ws, cudaStream_t s) {
+             int ldc, const GemmEpi& ep, bool splitk, float* ws, cudaStream_t s, int keep) {
   H3Args a{};
+  static const int dbg = [] {
+    const char* e = getenv("KP_H3_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  a.dbg = dbg;
+  a.keep_a = keep & 1;
+  a.keep_b = (keep >> 1) & 1;
   a.mode = ep.mode;
   a.act = ep.act;
   a.bias = ep.bias;
@@ -584,7 +779,14 @@ void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M
   a.S = ep.S;
   a.e = ep.e;
   KP_CHECK(ep.mode == 0 || ep.mode == 1 || ep.mode == 3, kErrGeneric, "h3_gemm: unsupported epilogue");
-  if (!a_mn && !b_mn) launch_h3<false, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
+  static const bool ar_on = [] {
+    const char* e = getenv("KP_H3_AR");
+    return e && e[0] == '1';
+  }();
+  const bool ar = ar_on && !a_mn && !splitk && ceil_div(K, H3_BK) <= H3_AR_MAXKB && N > H3_BN;
+  if (ar && !b_mn) launch_h3_t<false, false, true, false>(A, B, M, N, K, C, ldc, ws, a, s);
+  else if (ar) launch_h3_t<false, true, true, false>(A, B, M, N, K, C, ldc, ws, a, s);
+  else if (!a_mn && !b_mn) launch_h3<false, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
   else if (a_mn && b_mn) launch_h3<true, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
   else if (a_mn) launch_h3<true, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
   else launch_h3<false, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
@@ -603,11 +805,16 @@ void split_rows_h(const float* X, int rows, int K, int ld, __half* hi, __half* l
 
 void split_cols_scaled_h(const float* dz, int B, int N, const int* xe, unsigned* cmax_ws, __half* hi, __half* lo,
                          int* exps, cudaStream_t s) {
+  KP_CHECK(N % 4 == 0, kErrConfig, "split_cols_scaled_h: N must be a multiple of 4");
   KP_CUDA(cudaMemsetAsync(cmax_ws, 0, (size_t)N * 4, s));
-  const unsigned gy = (unsigned)std::min<uint64_t>(std::max<uint64_t>(1, B / 64), 512);
-  k_colmax_scaled<<<dim3(ceil_div(N, 256), gy), 256, 0, s>>>(dz, B, N, xe, cmax_ws);
+  // slabs of up to 1024 columns (blockIdx.y), rows strided over blockIdx.x
+  const int W = std::min(N, 1024);
+  const dim3 blk(W / 4, std::max(1, std::min(8, 256 / (W / 4))));
+  const unsigned slabs = ceil_div(N, W);
+  const dim3 g((unsigned)std::min<uint64_t>(ceil_div(B, blk.y), std::max<uint64_t>(1, 148 * 8 / slabs)), slabs);
+  k_colmax_scaled<<<g, blk, 0, s>>>(dz, B, N, xe, cmax_ws);
   ::kp::count_launch();
-  k_split_cols_scaled<<<dim3(ceil_div(N, 512), gy), 256, 0, s>>>(dz, B, N, xe, cmax_ws, hi, lo, exps);
+  k_split_cols_scaled<<<g, blk, 0, s>>>(dz, B, N, xe, cmax_ws, hi, lo, exps);
   ::kp::count_launch();
 }
 

@@ -253,8 +253,10 @@ bool h3_supported(int M, int N, int K, const H3Operand& A, const H3Operand& B);
 // stored [K][rows] (MN-major) instead of [rows][K]. splitk: deterministic
 // stream-K over the K range into `ws` (h3_splitk_ws_floats) + fix-up; only
 // the plain store epilogue (mode 0).
+// keep: operands re-read across tiles (bit 0 A, bit 1 B) load with an L2
+// evict_last policy, the others evict_first
 void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M, int N, int K, float* C,
-             int ldc, const GemmEpi& ep, bool splitk, float* ws, cudaStream_t s);
+             int ldc, const GemmEpi& ep, bool splitk, float* ws, cudaStream_t s, int keep = 3);
 size_t h3_splitk_ws_floats(int M, int N);
 void h3_reserve_sms(int n);
 // planes of each row of X [rows][K] with its own exponent (one warp per row)
@@ -266,7 +268,7 @@ void split_cols_scaled_h(const float* dz, int B, int N, const int* xe, unsigned*
 bool pool_planes_supported(uint32_t S, uint32_t e);
 void pool_planes(const uint32_t* d_bag_offs, uint32_t n_inst, uint32_t S, const uint32_t* d_row_of_occ,
                  const float* d_src, uint32_t e, bool mean, __half* d_hi, __half* d_lo, int* d_inst_exp,
-                 float* d_inv_count, cudaStream_t s);
+                 float* d_inv_count, cudaStream_t s, bool ident = false);
 
 // ---------------------------------------------------------------- MLP ----
 struct MlpShape {

@@ -407,7 +407,7 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
       int* he = ws.hexp.get<int>(N);
       split_h(W, N, K, K, hh, hl, he, s);
       h3_gemm(H3Operand{ws.in_hi, ws.in_lo, ws.in_exp, K}, false, H3Operand{hh, hl, he, K}, false, B, N, K,
-              out, N, ep, false, nullptr, s);
+              out, N, ep, false, nullptr, s, /*keep W1*/ 2);
     } else if (l == 0 && use_h(B, N, K, in, W)) {
       // first layer (the wide S*e contraction): fp16 operands, per-row scales
       const float* am = ws.in_rowmax;
@@ -579,7 +579,8 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
       split_cols_scaled_h(dZ, B, N, ws.in_exp, ws.cmax.get<unsigned>(N), dwh, dwl, dwe, s);
       EpiArgs plain{kStore, 0, nullptr, nullptr, 0, nullptr, 1, 1};
       h3_gemm(H3Operand{dwh, dwl, dwe, N}, true, H3Operand{ws.in_hi, ws.in_lo, nullptr, K}, true, N, K, B,
-              d_grad + m.w_off[l], K, plain, true, ws.skws.get<float>(h3_splitk_ws_floats(N, K)), s);
+              d_grad + m.w_off[l], K, plain, true, ws.skws.get<float>(h3_splitk_ws_floats(N, K)), s,
+              /*keep dZ', stream X*/ 1);
       colsum(dZ, nullptr, B, N, d_grad + m.b_off[l], ws, s);
       continue;
     }

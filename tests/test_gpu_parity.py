@@ -460,7 +460,8 @@ def test_tcgen05_gemm_f16_scaled_accuracy(kp, M, N, K, spread):
 @pytest.mark.parametrize("M,N,K,spread,engine", [(128, 128, 32, 0, 4), (300, 256, 6400, 0, 4),
                                                  (1000, 256, 6400, 8, 4), (512, 6400, 256, 4, 4),
                                                  (65, 40, 96, 0, 4), (4096, 256, 6400, 3, 5),
-                                                 (256, 384, 4096, 2, 5), (777, 208, 64, 1, 4)])
+                                                 (256, 384, 4096, 2, 5), (777, 208, 64, 1, 4),
+                                                 (3000, 1000, 200, 2, 4), (65536, 6400, 256, 1, 4)])
 def test_h3_gemm_nt_accuracy(kp, M, N, K, spread, engine):
     """3xFP16 on pre-split fp16 planes (kp_gemm_h3.cu, the planes-mode first
     layer), both operands K-major; engine 5 = deterministic stream-K over K:
