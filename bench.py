@@ -200,6 +200,46 @@ class Clocks:
                 "samples": len(sm)}
 
 
+class NvLink:
+    """NVLink data bytes this GPU transmitted / received (NVML field counters
+    NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX, KiB, summed over the links),
+    read around the timed region: the measured NVLink traffic of the step."""
+
+    TX, RX = 138, 139
+
+    def __init__(self, device):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.links = [l for l in range(18) if self._state(l)]
+        except Exception:
+            self.h = None
+
+    def _state(self, l):
+        try:
+            return self.nv.nvmlDeviceGetNvLinkState(self.h, l) == 1
+        except Exception:
+            return False
+
+    def read(self):
+        if self.h is None or not self.links:
+            return None
+        try:
+            q = [(self.TX, l) for l in self.links] + [(self.RX, l) for l in self.links]
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, q)
+            out = [0, 0]
+            for i, v in enumerate(vals):
+                if v.nvmlReturn != 0:
+                    return None
+                out[0 if i < len(self.links) else 1] += int(v.value.ullVal) * 1024
+            return out
+        except Exception:
+            return None
+
+
 # ------------------------------------------------------------- reference arm --
 def run_reference(args, rank):
     """The reference's own CPU implementation (oracle/_ref/libkpsim_ref.so, the
@@ -417,6 +457,8 @@ def main():
     l0 = kp.launch_count()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nvl = NvLink(local) if world > 1 else None
+    nv0 = nvl.read() if nvl else None
     with Clocks(local) as clk:
         ev0.record(stream)
         w0 = time.perf_counter()
@@ -425,6 +467,7 @@ def main():
         ev1.record(stream)
         barrier()
         wall = time.perf_counter() - w0
+    nv1 = nvl.read() if nvl else None
     launches = kp.launch_count() - l0
     prof = tr.profile(False)
     dev_ms = ev0.elapsed_time(ev1)
@@ -529,6 +572,16 @@ def main():
                   "exchange_stage_ms": stages["exchange"]["ms_per_step"],
                   "note": "rows and gradients move inside the pull/push kernels and the "
                           "copy engines, overlapped; the stages above include them"}
+        if nv0 and nv1:
+            # measured by the NVLink hardware counters over the timed region
+            # (this rank; max over ranks of the step time as the denominator)
+            sec = dev_ms / 1e3
+            tx, rx = (nv1[0] - nv0[0]) / args.steps, (nv1[1] - nv0[1]) / args.steps
+            nvlink["measured"] = {
+                "tx_bytes_per_step": tx, "rx_bytes_per_step": rx,
+                "tx_gbs": tx * args.steps / sec / 1e9, "rx_gbs": rx * args.steps / sec / 1e9,
+                "frac_of_900_gbs_per_direction": max(tx, rx) * args.steps / sec / 900e9,
+                "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX counters, rank 0"}
 
     if rank == 0:
         cpu = None

@@ -14,6 +14,8 @@
 // the fp32 oracle; the backward reduce is a fixed-order two-level segmented
 // sum (chunk partials combined in chunk order) -- deterministic, no float
 // atomics.
+#include <cstdlib>
+
 #include "kp_table.cuh"
 #include "kp_tcgen05.cuh"
 
@@ -513,6 +515,126 @@ __device__ __forceinline__ void sum_range(const SegArgs& a, uint32_t p, uint32_t
   }
 }
 
+// Pipelined chunk walk (float4 rows, LPG >= 8 lanes per row, CH <= 64):
+//  * the chunk's source-row indices are loaded up front, KP per lane
+//    (position p0 + gl + LPG*k), and broadcast by shuffles -- no
+//    index -> row dependency inside the row loop;
+//  * a segment that ends inside the chunk has its table row index and its
+//    current state (w, s1[, s2]) loaded BEFORE its gradient rows are summed,
+//    so the read-modify-write overlaps the sum: a one-feature key costs two
+//    dependent latencies instead of four.
+// Arithmetic (sum order, x 1/N, the rule) is the scalar path's, bit for bit.
+template <int LPG, int KP>
+__device__ __forceinline__ uint32_t pos_row(const uint32_t (&srow)[KP], uint32_t rel) {
+  // the two groups of a warp walk different chunks: shuffle within the group
+  const uint32_t gmask = LPG == 32 ? 0xffffffffu : (((1u << LPG) - 1u) << ((threadIdx.x & 31) & ~(LPG - 1)));
+  const uint32_t k = rel / LPG;
+  uint32_t v = srow[0];
+#pragma unroll
+  for (int i = 1; i < KP; ++i) v = k == (uint32_t)i ? srow[i] : v;
+  return __shfl_sync(gmask, v, (int)(rel % LPG), LPG);
+}
+
+template <int LPG, int NV, bool V4>
+__device__ __forceinline__ void sum_range_pre(const SegArgs& a, const uint32_t (&srow)[64 / LPG], uint32_t p0,
+                                              uint32_t p, uint32_t q, Row<LPG, NV, V4>& acc, int gl) {
+  constexpr int UR = 8;
+  Row<LPG, NV, V4> r[UR];
+  // group-uniform loop bounds: every lane takes part in the shuffles
+  for (; p + UR <= q; p += UR) {
+    uint32_t sr[UR];
+#pragma unroll
+    for (int u = 0; u < UR; ++u) sr[u] = pos_row<LPG, 64 / LPG>(srow, p + u - p0);
+#pragma unroll
+    for (int u = 0; u < UR; ++u) r[u].load(a.rows_src + (uint64_t)sr[u] * a.e, gl, a.e);
+#pragma unroll
+    for (int u = 0; u < UR; ++u) acc.add(r[u]);
+  }
+  if (p < q) {
+    uint32_t sr[UR];
+#pragma unroll
+    for (int u = 0; u < UR; ++u) sr[u] = pos_row<LPG, 64 / LPG>(srow, min(p + u, q - 1) - p0);
+#pragma unroll
+    for (int u = 0; u < UR; ++u)
+      if (p + u < q) r[u].load(a.rows_src + (uint64_t)sr[u] * a.e, gl, a.e);
+#pragma unroll
+    for (int u = 0; u < UR; ++u)
+      if (p + u < q) acc.add(r[u]);
+  }
+}
+
+template <int LPG, int NV, bool V4>
+__global__ void __launch_bounds__(256, 3) k_seg_chunks_pre(SegArgs a, TView t) {
+  static_assert(V4 && LPG >= 8, "pipelined walk: float4 rows, >= 8 lanes");
+  constexpr int KP = 64 / LPG;
+  if (aborted(t.abort)) return;  // no row updates after a peer timeout
+  const int gl = threadIdx.x % LPG;
+  const uint32_t nchunks = (a.n_pos + a.CH - 1) / a.CH;
+  const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPG;
+  const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / LPG;
+  for (uint64_t c = g0; c < nchunks; c += ng) {
+    const uint32_t p0 = (uint32_t)c * a.CH, p1 = min(a.n_pos, p0 + a.CH);
+    uint32_t srow[KP];
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const uint32_t p = p0 + gl + LPG * k;
+      srow[k] = p < p1 ? src_row(a, p) : 0u;
+    }
+    uint32_t u = a.first[c];  // largest u with seg[u] <= p0
+    uint32_t s0 = a.seg[u], s1 = a.seg[u + 1];
+    for (;;) {
+      const uint32_t s2 = s1 < p1 ? a.seg[u + 2] : 0u;  // next segment's end, in flight
+      const bool before = s0 < p0, after = s1 > p1;
+      const bool fin = !before && !after;
+      // the finalized segment's row state, loaded while its gradients are summed
+      uint32_t trow = kNoRow;
+      float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f), m4 = w4, v4 = w4;
+      if (fin && a.apply) {
+        trow = a.table_rows[u];
+        if (trow != kNoRow) {
+          const uint64_t o = (uint64_t)trow * a.e;
+          w4 = reinterpret_cast<const float4*>(t.w + o)[gl];
+          m4 = reinterpret_cast<const float4*>(t.s1 + o)[gl];
+          if (a.rule != 0) v4 = reinterpret_cast<const float4*>(t.s2 + o)[gl];
+        }
+      }
+      Row<LPG, NV, V4> acc;
+      acc.zero();
+      sum_range_pre(a, srow, p0, max(s0, p0), min(s1, p1), acc, gl);
+      if (fin) {
+        if (!a.apply) {
+          finalize(a, t, u, acc, gl);
+        } else if (trow != kNoRow) {
+          acc.scale(a.inv_n);  // trainer.cpp:204-206 (x 1/N)
+          float* wv = &w4.x;
+          float* mv = &m4.x;
+          float* vv = &v4.x;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (a.rule == 0) adagrad1(wv[q], mv[q], acc.v[q], a.lr);
+            else adam1(wv[q], mv[q], vv[q], acc.v[q], a.lr, a.b1, a.b2);
+          }
+          const uint64_t o = (uint64_t)trow * a.e;
+          reinterpret_cast<float4*>(t.w + o)[gl] = w4;
+          reinterpret_cast<float4*>(t.s1 + o)[gl] = m4;
+          if (a.rule != 0) reinterpret_cast<float4*>(t.s2 + o)[gl] = v4;
+        }
+      } else {
+        acc.store(a.partials + ((uint64_t)c * 2 + (before ? 0 : 1)) * a.e, gl, a.e);
+        if (before && after) {  // spans the chunk: its (unused) tail slot reads as 0
+          acc.zero();
+          acc.store(a.partials + ((uint64_t)c * 2 + 1) * a.e, gl, a.e);
+        }
+      }
+      if (s1 >= p1) break;
+      ++u;
+      s0 = s1;
+      s1 = s2;
+    }
+  }
+  if (a.peer) __threadfence_system();  // remote stores complete before the signal
+}
+
 // Phase 1: one group per chunk of CH sorted positions.
 template <int LPG, int NV, bool V4>
 __global__ void __launch_bounds__(256, 6) k_seg_chunks(SegArgs a, TView t) {
@@ -651,7 +773,22 @@ template <int LPG, int NV, bool V4>
 void launch_seg(const SegArgs& a, const TView& t, float* Q, cudaStream_t s) {
   const uint32_t nchunks = (a.n_pos + a.CH - 1) / a.CH;
   const uint32_t nP = 2 * nchunks;
-  k_seg_chunks<LPG, NV, V4><<<grid_cap(((uint64_t)nchunks * LPG + 255) / 256), 256, 0, s>>>(a, t); ::kp::count_launch();
+  static const bool pre_on = [] {
+    const char* e = getenv("KP_SEG_PRE");
+    return !(e && e[0] == '0');
+  }();
+  if constexpr (V4 && LPG >= 8) {
+    if (pre_on && a.CH <= 64) {
+      k_seg_chunks_pre<LPG, NV, V4><<<grid_cap(((uint64_t)nchunks * LPG + 255) / 256), 256, 0, s>>>(a, t);
+      ::kp::count_launch();
+    } else {
+      k_seg_chunks<LPG, NV, V4><<<grid_cap(((uint64_t)nchunks * LPG + 255) / 256), 256, 0, s>>>(a, t);
+      ::kp::count_launch();
+    }
+  } else {
+    k_seg_chunks<LPG, NV, V4><<<grid_cap(((uint64_t)nchunks * LPG + 255) / 256), 256, 0, s>>>(a, t);
+    ::kp::count_launch();
+  }
   const uint32_t nQ = nP / QB;
   float* Q2 = Q + (uint64_t)(nQ + 1) * a.e;
   if (nQ) {
