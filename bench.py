@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--no-prefill", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-stage-profile", action="store_true",
+                   help="time the device-resident loop without the per-stage CUDA events")
     p.add_argument("--cpu-sample", type=int, default=4096, help="instances for the CPU baseline")
     p.add_argument("--ref-slice", type=int, default=1024,
                    help="reference arm: instances per host thread per step")
@@ -453,13 +455,15 @@ def main():
     # ---- device-resident path -------------------------------------------
     for i in range(args.warmup):
         step_dev(i)
-    tr.profile(True)
-    l0 = kp.launch_count()
-    barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nvl = NvLink(local) if world > 1 else None
-    nv0 = nvl.read() if nvl else None
     with Clocks(local) as clk:
+        # the barrier comes after the clock sampler started on every rank, so
+        # all ranks enter the timed region together
+        tr.profile(not args.no_stage_profile)
+        l0 = kp.launch_count()
+        nv0 = nvl.read() if nvl else None
+        barrier()
         ev0.record(stream)
         w0 = time.perf_counter()
         for i in range(args.steps):

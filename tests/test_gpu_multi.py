@@ -78,9 +78,14 @@ def test_sharded_kstep_sweep_matches_oracle(tmp_path, k):
     res = _run(tmp_path, [k, 4, "base", 24], port=29580 + k % 7)
     assert res["owners_ok"] and res["keyset_equal"]
     assert res["steps"] == res["oracle_steps"] and res["merges"] == res["oracle_merges"]
-    assert res["w_max_abs"] <= 2e-4 and res["x_max_abs"] <= 2e-4
+    # 24 batches at sparse lr 0.5: fp32 rounding drifts along the trajectory;
+    # the bound is the fp32 restatement's own drift from f64 (x3), at least
+    # the short-run tolerance
+    print({k_: res[k_] for k_ in ("w_max_abs", "x_max_abs", "env_w_max_abs", "env_x_max_abs", "env_loss")})
+    assert res["w_max_abs"] <= max(2e-4, 3 * res["env_w_max_abs"])
+    assert res["x_max_abs"] <= max(2e-4, 3 * res["env_x_max_abs"])
     for a, b in zip(res["loss"], res["oracle_loss"]):
-        assert abs(a - b) <= 1e-4
+        assert abs(a - b) <= max(1e-4, 3 * res["env_loss"])
     for a, b in zip(res["auc"], res["oracle_auc"]):
         if a is not None and b == b:
             assert abs(a - b) <= 5e-3

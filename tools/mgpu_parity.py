@@ -63,13 +63,18 @@ def main():
                             hidden=(16, 8), alpha=0.05, beta1=0.9, beta2=0.99,
                             sparse_lr=cfg["sparse_lr"], seed=5, **extra)
         orc = O.Orc(ocfg, 64)
-        oloss, oauc = [], []
+        o32 = O.Orc(ocfg, 32)  # the fp32 restatement: the drift envelope of fp32 arithmetic
+        oloss, oauc, env_loss = [], [], 0.0
         for bt in batches:
             r = orc.batch(bt.offs, bt.keys, bt.labels, slots=bt.slots, predict_first=True)
+            r32 = o32.batch(bt.offs, bt.keys, bt.labels, slots=bt.slots, predict_first=True)
             oloss.append(r["loss"])
             oauc.append(r["auc"])
             orc_cum = r["cumulative_auc"]
+            env_loss = max(env_loss, abs(r32["loss"] - r["loss"]))
         ok, ow, oa, _ = orc.table()
+        k32, w32, a32, _ = o32.table()
+        x32 = [o32.worker_state(i)["x"] for i in range(world)]
         allk = np.concatenate([np.array(p[0], np.uint64) for p in parts])
         allw = np.concatenate([np.array(p[1], np.float64).reshape(-1, 8) for p in parts])
         alla = np.concatenate([np.array(p[2], np.float64).reshape(-1, 8) for p in parts])
@@ -93,6 +98,9 @@ def main():
             "batches": n_batches, "steps": tr.tr.completed_steps, "merges": tr.tr.merges,
             "oracle_steps": orc.steps(), "oracle_merges": orc.merges(),
             "cum_auc": tr_cum, "oracle_cum_auc": orc_cum,
+            "env_w_max_abs": float(np.max(np.abs(w32 - ow))) if np.array_equal(k32, ok) else None,
+            "env_x_max_abs": float(max(np.max(np.abs(a - b)) for a, b in zip(x32, [orc.worker_state(i)["x"] for i in range(world)]))),
+            "env_loss": env_loss,
         }
         with open(out_path, "w") as f:
             json.dump(summary, f)
