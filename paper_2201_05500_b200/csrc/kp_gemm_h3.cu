@@ -509,7 +509,8 @@ __global__ void k_h3_fixup(const float* __restrict__ part, int nblocks_n, int nk
     const int m = mb * 2 * H3_BM + r, n = nb * H3_BN + cc;
     if (m >= M || n >= N) continue;
     float s = 0.f;
-    for (int v = v0; v <= v1; ++v) s = __fadd_rn(s, part[((size_t)(tile + v) * 2 * H3_BM + r) * H3_BN + cc]);
+    for (int v = v0; v <= v1; ++v)  // (with fewer k-blocks than virtual units some own none)
+      if (vstart(v + 1, T) > vstart(v, T)) s = __fadd_rn(s, part[((size_t)(tile + v) * 2 * H3_BM + r) * H3_BN + cc]);
     C[(size_t)m * ldc + n] = s;
   }
 }

@@ -488,7 +488,8 @@ def test_h3_gemm_nt_accuracy(kp, M, N, K, spread, engine):
 
 
 @pytest.mark.parametrize("M,N,K,engine", [(256, 6400, 4096, 4), (256, 6400, 4096, 5), (128, 256, 65536, 5),
-                                          (40, 104, 300, 4), (256, 512, 20000, 5), (64, 6400, 2048, 5)])
+                                          (40, 104, 300, 4), (256, 512, 20000, 5), (64, 6400, 2048, 5),
+                                          (16, 32, 70, 5), (40, 104, 300, 5), (256, 256, 4096, 5)])
 def test_h3_gemm_tn_accuracy(kp, M, N, K, engine):
     """3xFP16 planes with both operands MN-major (the weight gradient dZ'^T X
     over the batch), one exponent per column, stream-K over the batch."""
@@ -504,6 +505,12 @@ def test_h3_gemm_tn_accuracy(kp, M, N, K, engine):
     err_simt = np.max(np.abs(simt - want) / scale)
     print(f"h3 tn M={M} N={N} K={K} e{engine}: err={err_tc:.3e} simt={err_simt:.3e}")
     assert err_tc < 3 * err_simt + 2e-6, (err_tc, err_simt)
+    if engine == 5:
+        # stream-K with fewer k-blocks than virtual units (K <= 4096): some
+        # units own no range; a different shape in between must not leave
+        # stale partials behind
+        kp.gemm_tn(A[: K // 2 + 1], B[: K // 2 + 1], engine=5)
+        assert np.array_equal(kp.gemm_tn(A, B, engine=5), tc)
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 6400, 4096), (128, 256, 65536), (40, 100, 300)])

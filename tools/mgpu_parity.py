@@ -44,11 +44,12 @@ def main():
     tr = DistributedTrainer(device=local, table_capacity=1 << 16, **cfg)
     res = {"loss": [], "auc": []}
     batches = []
+    grow = 0 if os.environ.get("MGPU_CONST_BATCH") == "1" else 17
     for b in range(n_batches):
         if S > 1:
-            bt = make_batch(600 + 17 * b, V=4000, zipf_s=1.1, n_slots=S, seed=b)
+            bt = make_batch(600 + grow * b, V=4000, zipf_s=1.1, n_slots=S, seed=b)
         else:
-            bt = make_batch(600 + 17 * b, V=4000, zipf_s=1.1, nnz=7, poisson=True, seed=b)
+            bt = make_batch(600 + grow * b, V=4000, zipf_s=1.1, nnz=7, poisson=True, seed=b)
         batches.append(bt)
         r = tr.train_batch(bt, predict_first=True)
         res["loss"].append(r["loss"])
