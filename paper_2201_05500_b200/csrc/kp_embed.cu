@@ -773,9 +773,9 @@ template <int LPG, int NV, bool V4>
 void launch_seg(const SegArgs& a, const TView& t, float* Q, cudaStream_t s) {
   const uint32_t nchunks = (a.n_pos + a.CH - 1) / a.CH;
   const uint32_t nP = 2 * nchunks;
-  static const bool pre_on = [] {
+  static const bool pre_on = [] {  // measured slower at configs[1] (DESIGN 4.1): opt-in
     const char* e = getenv("KP_SEG_PRE");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   if constexpr (V4 && LPG >= 8) {
     if (pre_on && a.CH <= 64) {

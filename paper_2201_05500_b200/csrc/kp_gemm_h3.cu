@@ -49,29 +49,23 @@ using namespace tc;
 constexpr int H3_BM = 128;   // rows per CTA (pair: 256)
 constexpr int H3_BN = 256;   // tile columns (each CTA holds 128 B rows)
 constexpr int H3_BK = 32;    // k per stage
+// epilogue store box: H3_EB fp32 columns x 32 rows per TMA store (16: SW64,
+// 2 KB; 32: SW128, 4 KB), one per epilogue warp; the smaller box leaves
+// room for a fifth operand stage
+constexpr int H3_EB = 16;
+constexpr int H3_EPIB = 2;   // store boxes per epilogue warp (double-buffered)
 constexpr int H3_NS = 4;     // smem stages
 constexpr int H3_CH = 16;    // k-blocks per accumulator chunk (512 k)
 constexpr int H3_WARPS = 20;  // warpgroup 0: producer, MMA, 2 idle; warpgroups 1-4: epilogue
 constexpr int H3_EPI_T = 512;
 constexpr uint32_t H3_PLANE = H3_BM * H3_BK * 2;  // 8 KB: one plane tile per CTA
 constexpr uint32_t H3_STAGE = 4 * H3_PLANE;       // A hi, A lo, B hi, B lo
-constexpr uint32_t H3_EPI = 16 * 4096;            // per epilogue warp one 32x32 fp32 store tile
+constexpr uint32_t H3_EPI = 16 * H3_EPIB * 32 * H3_EB * 4;  // per epilogue warp H3_EPIB 32 x H3_EB fp32 store tiles
 // register split (setmaxnreg, per warpgroup): the epilogue holds 64 fp32
 // running sums per thread; the TMA / MMA warps need few
 constexpr int H3_REG_LO = 40, H3_REG_HI = 104;  // 128*40 + 512*104 <= 640*96 (the CTA pool)
 constexpr uint32_t H3_COLP = 16 * 2 * 64 * 4;  // per epilogue warp: 64 column scales + 64 biases
 constexpr uint32_t H3_SMEM = H3_NS * H3_STAGE + H3_EPI + H3_COLP + 1024 + 256;
-// A-resident mode (K <= 256, e.g. dX = dZ1 W1 with K = 256, N = 6400): the
-// unit's whole A (128 rows x 256 k, both planes: 128 KB) stays in shared
-// memory while the unit walks consecutive n-blocks, so only B streams (half
-// the L2->SM bytes per tile); B stages are 16 KB, the epilogue store tiles
-// single-buffered to fit.
-constexpr int H3_AR_MAXKB = 8;
-constexpr uint32_t H3_AR_A = H3_AR_MAXKB * 2 * H3_PLANE;  // 128 KB
-constexpr int H3_AR_NS = 1;
-constexpr uint32_t H3_AR_STAGE = 2 * H3_PLANE;
-constexpr uint32_t H3_AR_SMEM = H3_AR_A + H3_AR_NS * H3_AR_STAGE + H3_EPI + H3_COLP + 1024 + 256;
-static_assert(H3_AR_SMEM <= 232448, "A-resident smem");
 constexpr int H3_VUNITS = 148;  // stream-K virtual units (partition independent of the grid)
 
 struct H3Args {
@@ -164,26 +158,16 @@ __device__ __forceinline__ uint64_t plane_desc(uint32_t base, int kk) {
   return MN ? sdesc_mn128(base + (uint32_t)kk * 2048u, 4096u) : sdesc_k64(base + (uint32_t)kk * 32u);
 }
 
-// A-resident units: a contiguous range of tiles (n-block fastest), A reloaded
-// whenever the m-block changes
-__device__ __forceinline__ void ar_range(const H3Args& a, int unit, int units, int& t0, int& t1) {
-  const int64_t T = (int64_t)a.nblocks_m * a.nblocks_n;
-  t0 = (int)(T * unit / units);
-  t1 = (int)(T * (unit + 1) / units);
-}
-
-template <bool AMN, bool BMN, bool AR, bool SK>
+template <bool AMN, bool BMN, bool SK>
 __global__ void __launch_bounds__(H3_WARPS * 32, 1)
     k_h3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
          const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
          const __grid_constant__ CUtensorMap tmC, H3Args a) {
-  static_assert(!AR || !AMN, "A-resident mode: K-major A");
-  constexpr int NS = AR ? H3_AR_NS : H3_NS;
-  constexpr uint32_t STAGE = AR ? H3_AR_STAGE : H3_STAGE;
+  constexpr int NS = H3_NS;
+  constexpr uint32_t STAGE = H3_STAGE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* ares = smem;                       // (AR) resident A: [kb][hi|lo] plane tiles
-  uint8_t* stages = smem + (AR ? H3_AR_A : 0);
+  uint8_t* stages = smem;
   uint8_t* epi = stages + NS * STAGE;
   float* colp = reinterpret_cast<float*>(epi + H3_EPI);
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(colp) + H3_COLP);
@@ -192,10 +176,7 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
   uint64_t* empty = bars + 2 * NS;    // MMA done with stage -> producers (both CTAs)
   uint64_t* tfull = bars + 3 * NS;    // chunk accumulated -> drains (both CTAs)
   uint64_t* tempty = tfull + 2;       // drained -> MMA (leader; 2 arrivals)
-  uint64_t* afull = tempty + 2;       // (AR) resident A landed (local)
-  uint64_t* aconv = afull + 1;        // (AR) peer's A landed -> leader
-  uint64_t* afree = aconv + 1;        // (AR) MMAs done with the resident A (both CTAs)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afree + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -212,9 +193,6 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 2);
     }
-    mbar_init(afull, 1);
-    mbar_init(aconv, 1);
-    mbar_init(afree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
@@ -236,33 +214,6 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       // the operand re-read across tiles stays in L2, the streamed one goes first
       const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
       const uint64_t pa = a.keep_a ? pol_keep : pol_stream, pb = a.keep_b ? pol_keep : pol_stream;
-      if constexpr (AR) {
-        int t0, t1, g = 0, prev_mb = -1, na = 0;
-        ar_range(a, unit, units, t0, t1);
-        for (int tile = t0; tile < t1; ++tile) {
-          int mb, nb;
-          tile_mn(a, tile, mb, nb);
-          const int n0 = nb * H3_BN + (int)rank * (H3_BN / 2);
-          if (mb != prev_mb) {  // (re)load the resident A once its previous MMAs are done
-            const int m0 = mb * 2 * H3_BM + (int)rank * H3_BM;
-            if (na > 0) mbar_wait(afree, (na - 1) & 1);
-            mbar_expect_tx(afull, 2u * a.nk * H3_PLANE);
-            for (int kb = 0; kb < a.nk; ++kb) {
-              load_plane<false>(ares + (2 * kb) * H3_PLANE, &tmAh, afull, kb * H3_BK, m0, pa);
-              load_plane<false>(ares + (2 * kb + 1) * H3_PLANE, &tmAl, afull, kb * H3_BK, m0, pa);
-            }
-            prev_mb = mb;
-            ++na;
-          }
-          for (int kb = 0; kb < a.nk; ++kb, ++g) {
-            const int s = g % NS;
-            if (g >= NS) mbar_wait(&empty[s], ((g / NS) & 1) ^ 1);
-            mbar_expect_tx(&full[s], STAGE);
-            load_plane<BMN>(sAh(s), &tmBh, &full[s], kb * H3_BK, n0, pb);
-            load_plane<BMN>(sAh(s) + H3_PLANE, &tmBl, &full[s], kb * H3_BK, n0, pb);
-          }
-        }
-      } else {
       SegIter<SK> it(a, unit, units);
       int tile, kb0, kb1, sid, g = 0;
       while (it.next(tile, kb0, kb1, sid)) {
@@ -281,50 +232,11 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
           load_plane<BMN>(st + 3 * H3_PLANE, &tmBl, &full[s], kb * H3_BK, n0, pb);
         }
       }
-      }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ---- MMA issuer (leader CTA): both CTAs' tiles, M = 256
       constexpr uint32_t idesc = idesc_f16(AMN, BMN, 2 * H3_BM, H3_BN);
-      if constexpr (AR) {
-        int t0, t1, g = 0, c = 0, prev_mb = -1, na = 0;
-        ar_range(a, unit, units, t0, t1);
-        for (int tile = t0; tile < t1; ++tile, ++c) {
-          int mb, nb;
-          tile_mn(a, tile, mb, nb);
-          if (mb != prev_mb) {
-            mbar_wait(afull, na & 1);
-            mbar_wait(aconv, na & 1);
-            prev_mb = mb;
-            ++na;
-          }
-          const int buf = c & 1;
-          if (c >= 2) mbar_wait(&tempty[buf], ((c >> 1) - 1) & 1);
-          const uint32_t d = tmem + (uint32_t)(buf * H3_BN);
-          for (int kb = 0; kb < a.nk; ++kb, ++g) {
-            const int s = g % NS;
-            mbar_wait(&full[s], (g / NS) & 1);
-            mbar_wait(&conv[s], (g / NS) & 1);
-            fence_after();
-            const uint32_t ah = smem_u32(ares) + 2u * kb * H3_PLANE, al = ah + H3_PLANE;
-            const uint32_t bh = smem_u32(sAh(s)), bl = bh + H3_PLANE;
-#pragma unroll
-            for (int kk = 0; kk < H3_BK / 16; ++kk) {
-              const uint64_t dah = plane_desc<false>(ah, kk), dal = plane_desc<false>(al, kk);
-              const uint64_t dbh = plane_desc<BMN>(bh, kk), dbl = plane_desc<BMN>(bl, kk);
-              mma_f16_pair(d, dah, dbh, idesc, (kb | kk) != 0);
-              mma_f16_pair(d, dah, dbl, idesc, 1);
-              mma_f16_pair(d, dal, dbh, idesc, 1);
-            }
-            commit_pair(&empty[s]);
-          }
-          commit_pair(&tfull[buf]);
-          int nmb = -1, nnb;
-          if (tile + 1 < t1) tile_mn(a, tile + 1, nmb, nnb);
-          if (nmb != mb) commit_pair(afree);  // the resident A may be replaced
-        }
-      } else {
       SegIter<SK> it(a, unit, units);
       int tile, kb0, kb1, sid, g = 0, c = 0;
       while (it.next(tile, kb0, kb1, sid)) {
@@ -353,28 +265,8 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
           }
         }
       }
-      }
     } else if (lane == 0) {
       // ---- peer CTA: relay "my TMA landed" to the leader's MMA issuer
-      if constexpr (AR) {
-        int t0, t1, g = 0, prev_mb = -1, na = 0;
-        ar_range(a, unit, units, t0, t1);
-        for (int tile = t0; tile < t1; ++tile) {
-          int mb, nb;
-          tile_mn(a, tile, mb, nb);
-          if (mb != prev_mb) {
-            mbar_wait(afull, na & 1);
-            mbar_arrive_leader(aconv);
-            prev_mb = mb;
-            ++na;
-          }
-          for (int kb = 0; kb < a.nk; ++kb, ++g) {
-            const int s = g % NS;
-            mbar_wait(&full[s], (g / NS) & 1);
-            mbar_arrive_leader(&conv[s]);
-          }
-        }
-      } else {
       SegIter<SK> it(a, unit, units);
       int tile, kb0, kb1, sid, g = 0;
       while (it.next(tile, kb0, kb1, sid))
@@ -383,7 +275,6 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
           mbar_wait(&full[s], (g / NS) & 1);
           mbar_arrive_leader(&conv[s]);
         }
-      }
     }
   }
   } else {
@@ -391,20 +282,11 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
     // ---- drain + epilogue (16 warps): TMEM lane quarter q, columns [cq*64, +64)
     const int q = warp & 3, cq = (warp - 4) >> 2;
     const int et = threadIdx.x - 128;
-    uint8_t* dense_base = epi + (warp - 4) * 4096;
+    uint8_t* dense_base = epi + (warp - 4) * (H3_EPIB * 32 * H3_EB * 4);
+    uint32_t tma_seq = 0;
     SegIter<SK> it(a, unit, units);
-    int ar_t = 0, ar_t1 = 0;
-    if constexpr (AR) ar_range(a, unit, units, ar_t, ar_t1);
     int tile, kb0, kb1, sid, c = 0;
-    for (;;) {
-      if constexpr (AR) {
-        if (ar_t >= ar_t1) break;
-        tile = sid = ar_t++;
-        kb0 = 0;
-        kb1 = a.nk;
-      } else {
-        if (!it.next(tile, kb0, kb1, sid)) break;
-      }
+    while (it.next(tile, kb0, kb1, sid)) {
       int mb, nb;
       tile_mn(a, tile, mb, nb);
       const int mrow0 = mb * 2 * H3_BM + (int)rank * H3_BM + q * 32;  // this warp's 32 rows
@@ -446,17 +328,18 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
         if (et == 0) mbar_arrive_leader(&tempty[buf]);
       }
       // epilogue: row per lane; exact power-of-two unscaling, then the op;
-      // two 32x32 fp32 boxes per warp (SWIZZLE_128B: lane = row, its eight
-      // 16-byte chunks at chunk ^ (row & 7), conflict-free), one TMA store each
+      // 32 x H3_EB fp32 boxes, one TMA store each (lane = row; its 16-byte
+      // chunks XOR-swizzled by the row, conflict-free)
       __syncwarp();  // csb visible to the warp
-      const uint32_t dense = smem_u32(dense_base);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c0 = 32 * h;
+      for (int h = 0; h < 64 / H3_EB; ++h, ++tma_seq) {
+        uint8_t* box = dense_base + (tma_seq % H3_EPIB) * (32 * H3_EB * 4);
+        const uint32_t dense = smem_u32(box);
+        const int c0 = H3_EB * h;
         const int n = ncol0 + c0;
         float* v = acc + c0;  // transformed in place (registers)
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < H3_EB; ++j) {
           v[j] = __fmul_rn(__fmul_rn(v[j], sa), csb[c0 + j]);
           if (a.mode == 1) v[j] = act_fwd(a.act, __fadd_rn(v[j], csb[64 + c0 + j]));
         }
@@ -465,26 +348,31 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
           int slot = -1;
           float cf = 1.f;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
+          for (int j = 0; j < H3_EB; ++j) {
             const int sj = min(n + j, a.N - 1) / (int)a.e;
             if (sj != slot) slot = sj, cf = __ldg(cp + sj);
             v[j] = __fmul_rn(v[j], cf);
           }
         }
-        // the previous box has been read out of shared memory
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        // the store that last used this buffer has read it out of shared memory
+        if (lane == 0) {
+          if (H3_EPIB == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
         __syncwarp();
 #pragma unroll
-        for (int cc = 0; cc < 8; ++cc)
-          st_shared_v4(dense + lane * 128 + ((cc ^ (lane & 7)) << 4), v[4 * cc], v[4 * cc + 1], v[4 * cc + 2],
+        for (int cc = 0; cc < H3_EB / 4; ++cc) {
+          const uint32_t sw = H3_EB == 32 ? (uint32_t)(cc ^ (lane & 7)) : (uint32_t)(cc ^ ((lane >> 1) & 3));
+          st_shared_v4(dense + lane * (H3_EB * 4) + (sw << 4), v[4 * cc], v[4 * cc + 1], v[4 * cc + 2],
                        v[4 * cc + 3]);
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0 && a.dbg != 1) {
           if (SK)  // partial tile of segment sid: rows sid*256 + local row
-            tma_store_2d(&tmC, dense_base, cq * 64 + c0, sid * 2 * H3_BM + (int)rank * H3_BM + q * 32);
+            tma_store_2d(&tmC, box, cq * 64 + c0, sid * 2 * H3_BM + (int)rank * H3_BM + q * 32);
           else
-            tma_store_2d(&tmC, dense_base, n, mrow0);
+            tma_store_2d(&tmC, box, n, mrow0);
         }
       }
     }
@@ -542,22 +430,22 @@ bool map_plane(CUtensorMap* m, const __half* p, uint64_t rows, uint64_t cols, ui
             CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-// fp32 [rows][cols] output, 32 x 32 boxes, SW128 (the epilogue's store tiles)
+// fp32 [rows][cols] output, H3_EB x 32 boxes (the epilogue's store tiles)
 bool map_out(CUtensorMap* m, float* p, uint64_t rows, uint64_t cols, uint64_t ld) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {ld * 4};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {(cuuint32_t)H3_EB, 32};
   cuuint32_t es[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            H3_EB == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 thread_local int g_h3_reserve = 0;
 
-template <bool AMN, bool BMN, bool AR, bool SK>
+template <bool AMN, bool BMN, bool SK>
 void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, float* ws,
                  const H3Args& a0, cudaStream_t s);
 // stream-K and data-parallel variants are separate kernels (no 64-bit
@@ -565,11 +453,11 @@ void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, fl
 template <bool AMN, bool BMN>
 void launch_h3(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, bool splitk,
                float* ws, const H3Args& a, cudaStream_t s) {
-  if (splitk) launch_h3_t<AMN, BMN, false, true>(A, B, M, N, K, C, ldc, ws, a, s);
-  else launch_h3_t<AMN, BMN, false, false>(A, B, M, N, K, C, ldc, ws, a, s);
+  if (splitk) launch_h3_t<AMN, BMN, true>(A, B, M, N, K, C, ldc, ws, a, s);
+  else launch_h3_t<AMN, BMN, false>(A, B, M, N, K, C, ldc, ws, a, s);
 }
 
-template <bool AMN, bool BMN, bool AR, bool SK>
+template <bool AMN, bool BMN, bool SK>
 int h3_units() {
   static int units = 0;
   if (units) return units;
@@ -580,7 +468,7 @@ int h3_units() {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(4, 1, 1);
   cfg.blockDim = dim3(H3_WARPS * 32, 1, 1);
-  cfg.dynamicSmemBytes = AR ? H3_AR_SMEM : H3_SMEM;
+  cfg.dynamicSmemBytes = H3_SMEM;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
@@ -589,12 +477,12 @@ int h3_units() {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_h3<AMN, BMN, AR, SK>, &cfg) == cudaSuccess && n > 0) units = std::min(units, n);
+  if (cudaOccupancyMaxActiveClusters(&n, k_h3<AMN, BMN, SK>, &cfg) == cudaSuccess && n > 0) units = std::min(units, n);
   cudaGetLastError();
   return units;
 }
 
-template <bool AMN, bool BMN, bool AR, bool SK>
+template <bool AMN, bool BMN, bool SK>
 void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, float* ws,
                  const H3Args& a0, cudaStream_t s) {
   constexpr bool splitk = SK;
@@ -623,16 +511,16 @@ void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, fl
     ok = ok && map_out(&tcm, C, M, N, ldc);
   }
   KP_CHECK(ok, kErrCuda, "cuTensorMapEncodeTiled failed (3xFP16 GEMM operands)");
-  constexpr uint32_t SMEM = AR ? H3_AR_SMEM : H3_SMEM;
+  constexpr uint32_t SMEM = H3_SMEM;
   static std::atomic<uint64_t> attr{0};
   int dev = 0;
   KP_CUDA(cudaGetDevice(&dev));
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr.load(std::memory_order_acquire) & bit)) {
-    KP_CUDA(cudaFuncSetAttribute(k_h3<AMN, BMN, AR, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    KP_CUDA(cudaFuncSetAttribute(k_h3<AMN, BMN, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     attr.fetch_or(bit, std::memory_order_release);
   }
-  const int units_all = std::max(1, h3_units<AMN, BMN, AR, SK>() - (g_h3_reserve + 1) / 2);
+  const int units_all = std::max(1, h3_units<AMN, BMN, SK>() - (g_h3_reserve + 1) / 2);
   const int work = splitk ? H3_VUNITS : tiles;
   const unsigned grid = (unsigned)std::min(work, units_all) * 2;
   cudaLaunchConfig_t cfg = {};
@@ -647,7 +535,7 @@ void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, fl
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  KP_CUDA(cudaLaunchKernelEx(&cfg, k_h3<AMN, BMN, AR, SK>, tah, tal, tbh, tbl, tcm, a));
+  KP_CUDA(cudaLaunchKernelEx(&cfg, k_h3<AMN, BMN, SK>, tah, tal, tbh, tbl, tcm, a));
   ::kp::count_launch();
   if (splitk) {
     const int64_t T = (int64_t)tiles * a.nk;
@@ -780,14 +668,7 @@ void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M
   a.S = ep.S;
   a.e = ep.e;
   KP_CHECK(ep.mode == 0 || ep.mode == 1 || ep.mode == 3, kErrGeneric, "h3_gemm: unsupported epilogue");
-  static const bool ar_on = [] {
-    const char* e = getenv("KP_H3_AR");
-    return e && e[0] == '1';
-  }();
-  const bool ar = ar_on && !a_mn && !splitk && ceil_div(K, H3_BK) <= H3_AR_MAXKB && N > H3_BN;
-  if (ar && !b_mn) launch_h3_t<false, false, true, false>(A, B, M, N, K, C, ldc, ws, a, s);
-  else if (ar) launch_h3_t<false, true, true, false>(A, B, M, N, K, C, ldc, ws, a, s);
-  else if (!a_mn && !b_mn) launch_h3<false, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
+  if (!a_mn && !b_mn) launch_h3<false, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
   else if (a_mn && b_mn) launch_h3<true, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
   else if (a_mn) launch_h3<true, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
   else launch_h3<false, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
