@@ -66,12 +66,34 @@ constexpr uint32_t H3_EPI = 16 * H3_EPIB * 32 * H3_EB * 4;  // per epilogue warp
 constexpr int H3_REG_LO = 40, H3_REG_HI = 104;  // 128*40 + 512*104 <= 640*96 (the CTA pool)
 constexpr uint32_t H3_COLP = 16 * 2 * 64 * 4;  // per epilogue warp: 64 column scales + 64 biases
 constexpr uint32_t H3_SMEM = H3_NS * H3_STAGE + H3_EPI + H3_COLP + 1024 + 256;
-constexpr int H3_VUNITS = 148;  // stream-K virtual units (partition independent of the grid)
+// Tile width BN: 256 (2 TMEM accumulators) or 128 (4 accumulators: the MMA
+// may run 3 tiles ahead of the epilogue -- for short-K, wide-N products like
+// dX, K = 256, whose per-tile epilogue is as long as its MMAs). Each CTA holds
+// BN/2 rows of B.
+template <int BN>
+struct H3Cfg {
+  static constexpr int NBUF = 512 / BN;
+  static constexpr int BROWS = BN / 2;
+  static constexpr uint32_t B_PLANE = BROWS * H3_BK * 2;
+  static constexpr uint32_t STAGE = 2 * H3_PLANE + 2 * B_PLANE;
+  static constexpr int NS = BN == 256 ? 4 : 6;
+  static constexpr int CW = BN / 4;  // columns per epilogue warp
+  static constexpr uint32_t SMEM = NS * STAGE + H3_EPI + H3_COLP + 1024 + 256;
+};
+static_assert(H3Cfg<128>::SMEM <= 232448 && H3Cfg<256>::SMEM <= 232448, "h3 smem");
+// stream-K virtual units (the partition depends only on the problem shape,
+// not on the grid): 148, or fewer so that each owns >= 8 k-blocks
+constexpr int H3_VUNITS = 148;
+__host__ __device__ __forceinline__ int h3_vunits(int64_t T) {
+  const int64_t v = T / 8;
+  return v < 1 ? 1 : (v > H3_VUNITS ? H3_VUNITS : (int)v);
+}
 
 struct H3Args {
   int M, N, K;
   int nblocks_m, nblocks_n, nk;  // tiles and k-blocks
-  int splitk;                    // stream-K over H3_VUNITS virtual units
+  int splitk;                    // stream-K over vunits virtual units
+  int vunits;
   const int* ea;                 // per-row exponents of A (nullable = 0)
   const int* eb;                 // per-row exponents of B (nullable = 0)
   int keep_a, keep_b;            // L2 policy per operand: 1 evict_last (re-read), 0 evict_first
@@ -84,7 +106,7 @@ struct H3Args {
 };
 
 // the k-block range of virtual unit v over T = tiles * nk iterations
-__device__ __forceinline__ int64_t vstart(int64_t v, int64_t T) { return v * T / H3_VUNITS; }
+__device__ __forceinline__ int64_t vstart(int64_t v, int64_t T, int V) { return v * T / V; }
 
 // Iterates the (tile, kb0, kb1) segments of one physical unit: data-parallel
 // (whole tiles w = unit, unit+units, ...) or stream-K (the virtual units
@@ -92,17 +114,18 @@ __device__ __forceinline__ int64_t vstart(int64_t v, int64_t T) { return v * T /
 // flattened tile x k-block space; segment id = tile + v is unique).
 template <bool SK>
 struct SegIter {
-  int tiles, nk, units;
+  int tiles, nk, units, V;
   int v;  // current virtual unit (stream-K) / tile (DP)
   int64_t T, t, tend;
-  __device__ SegIter(const H3Args& a, int unit, int units_) : tiles(a.nblocks_m * a.nblocks_n), nk(a.nk), units(units_) {
+  __device__ SegIter(const H3Args& a, int unit, int units_)
+      : tiles(a.nblocks_m * a.nblocks_n), nk(a.nk), units(units_), V(a.vunits) {
     v = unit;
     if constexpr (SK) {
       T = (int64_t)tiles * nk;
       t = tend = 0;
-      if (v < H3_VUNITS) {
-        t = vstart(v, T);
-        tend = vstart(v + 1, T);
+      if (v < V) {
+        t = vstart(v, T, V);
+        tend = vstart(v + 1, T, V);
       }
     }
   }
@@ -119,9 +142,9 @@ struct SegIter {
     } else {
       while (t >= tend) {
         v += units;
-        if (v >= H3_VUNITS) return false;
-        t = vstart(v, T);
-        tend = vstart(v + 1, T);
+        if (v >= V) return false;
+        t = vstart(v, T, V);
+        tend = vstart(v + 1, T, V);
       }
       tile = (int)(t / nk);
       kb0 = (int)(t % nk);
@@ -142,14 +165,14 @@ __device__ __forceinline__ void tile_mn(const H3Args& a, int tile, int& mb, int&
 
 __device__ __forceinline__ float act_fwd(int act, float z) { return act == 0 ? (z > 0.f ? z : 0.f) : tanhf(z); }
 
-// one plane tile (this CTA's 128 rows x 32 k) of a K-major or MN-major operand
-template <bool MN>
+// one plane tile (ROWS of this CTA's rows x 32 k) of a K-major or MN-major operand
+template <bool MN, int ROWS = 128>
 __device__ __forceinline__ void load_plane(uint8_t* dst, const CUtensorMap* map, uint64_t* bar, int k0, int r0,
                                            uint64_t pol) {
-  if (MN) {  // two 64(mn) x 32(k) SW128 boxes, LBO = 4 KB apart
-    tma_load_2d_hint(dst, map, bar, r0, k0, pol);
-    tma_load_2d_hint(dst + 4096, map, bar, r0 + 64, k0, pol);
-  } else {   // one 32(k) x 128(rows) SW64 box
+  if (MN) {  // 64(mn) x 32(k) SW128 boxes, LBO = 4 KB apart
+#pragma unroll
+    for (int i = 0; i < ROWS / 64; ++i) tma_load_2d_hint(dst + 4096 * i, map, bar, r0 + 64 * i, k0, pol);
+  } else {   // one 32(k) x ROWS SW64 box
     tma_load_2d_hint(dst, map, bar, k0, r0, pol);
   }
 }
@@ -158,13 +181,14 @@ __device__ __forceinline__ uint64_t plane_desc(uint32_t base, int kk) {
   return MN ? sdesc_mn128(base + (uint32_t)kk * 2048u, 4096u) : sdesc_k64(base + (uint32_t)kk * 32u);
 }
 
-template <bool AMN, bool BMN, bool SK>
+template <bool AMN, bool BMN, bool SK, int BN>
 __global__ void __launch_bounds__(H3_WARPS * 32, 1)
     k_h3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
          const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
          const __grid_constant__ CUtensorMap tmC, H3Args a) {
-  constexpr int NS = H3_NS;
-  constexpr uint32_t STAGE = H3_STAGE;
+  using Cfg = H3Cfg<BN>;
+  constexpr int NS = Cfg::NS, NBUF = Cfg::NBUF, CW = Cfg::CW;
+  constexpr uint32_t STAGE = Cfg::STAGE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stages = smem;
@@ -175,8 +199,8 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
   uint64_t* conv = bars + NS;         // peer's TMA landed -> leader's MMA (1 arrival)
   uint64_t* empty = bars + 2 * NS;    // MMA done with stage -> producers (both CTAs)
   uint64_t* tfull = bars + 3 * NS;    // chunk accumulated -> drains (both CTAs)
-  uint64_t* tempty = tfull + 2;       // drained -> MMA (leader; 2 arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + NBUF;    // drained -> MMA (leader; 2 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -189,7 +213,7 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       mbar_init(&conv[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NBUF; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 2);
     }
@@ -220,7 +244,7 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
         int mb, nb;
         tile_mn(a, tile, mb, nb);
         const int m0 = mb * 2 * H3_BM + (int)rank * H3_BM;
-        const int n0 = nb * H3_BN + (int)rank * (H3_BN / 2);
+        const int n0 = nb * BN + (int)rank * Cfg::BROWS;
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % NS;
           if (g >= NS) mbar_wait(&empty[s], ((g / NS) & 1) ^ 1);
@@ -228,28 +252,28 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
           uint8_t* st = sAh(s);
           load_plane<AMN>(st, &tmAh, &full[s], kb * H3_BK, m0, pa);
           load_plane<AMN>(st + H3_PLANE, &tmAl, &full[s], kb * H3_BK, m0, pa);
-          load_plane<BMN>(st + 2 * H3_PLANE, &tmBh, &full[s], kb * H3_BK, n0, pb);
-          load_plane<BMN>(st + 3 * H3_PLANE, &tmBl, &full[s], kb * H3_BK, n0, pb);
+          load_plane<BMN, Cfg::BROWS>(st + 2 * H3_PLANE, &tmBh, &full[s], kb * H3_BK, n0, pb);
+          load_plane<BMN, Cfg::BROWS>(st + 2 * H3_PLANE + Cfg::B_PLANE, &tmBl, &full[s], kb * H3_BK, n0, pb);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ---- MMA issuer (leader CTA): both CTAs' tiles, M = 256
-      constexpr uint32_t idesc = idesc_f16(AMN, BMN, 2 * H3_BM, H3_BN);
+      constexpr uint32_t idesc = idesc_f16(AMN, BMN, 2 * H3_BM, BN);
       SegIter<SK> it(a, unit, units);
       int tile, kb0, kb1, sid, g = 0, c = 0;
       while (it.next(tile, kb0, kb1, sid)) {
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % NS;
-          const int kin = (kb - kb0) % H3_CH, buf = c & 1;
-          if (kin == 0 && c >= 2) mbar_wait(&tempty[buf], ((c >> 1) - 1) & 1);
+          const int kin = (kb - kb0) % H3_CH, buf = c % NBUF;
+          if (kin == 0 && c >= NBUF) mbar_wait(&tempty[buf], ((c / NBUF) - 1) & 1);
           mbar_wait(&full[s], (g / NS) & 1);
           mbar_wait(&conv[s], (g / NS) & 1);
           fence_after();
-          const uint32_t d = tmem + (uint32_t)(buf * H3_BN);
+          const uint32_t d = tmem + (uint32_t)(buf * BN);
           const uint32_t ah = smem_u32(sAh(s)), al = ah + H3_PLANE, bh = ah + 2 * H3_PLANE,
-                         bl = ah + 3 * H3_PLANE;
+                         bl = bh + Cfg::B_PLANE;
 #pragma unroll
           for (int kk = 0; kk < H3_BK / 16; ++kk) {
             const uint64_t dah = plane_desc<AMN>(ah, kk), dal = plane_desc<AMN>(al, kk);
@@ -290,34 +314,34 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       int mb, nb;
       tile_mn(a, tile, mb, nb);
       const int mrow0 = mb * 2 * H3_BM + (int)rank * H3_BM + q * 32;  // this warp's 32 rows
-      const int ncol0 = nb * H3_BN + cq * 64;                          // this warp's 64 columns
+      const int ncol0 = nb * BN + cq * CW;                             // this warp's CW columns
       // column scales / biases and the row scale, loaded while the MMAs run
       float* csb = colp + (warp - 4) * 128;
       __syncwarp();  // the previous tile's epilogue is done reading csb
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < CW / 32; ++h) {
         const int nn = min(ncol0 + lane + 32 * h, a.N - 1);
         csb[lane + 32 * h] = a.eb ? pow2f(-__ldg(a.eb + nn)) : 1.f;
         csb[64 + lane + 32 * h] = a.mode == 1 ? __ldg(a.bias + nn) : 0.f;
       }
       const int m = mrow0 + lane;
       const float sa = (a.ea && m < a.M) ? pow2f(-__ldg(a.ea + m)) : 1.f;
-      float acc[64];
+      float acc[CW];
 #pragma unroll
-      for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+      for (int j = 0; j < CW; ++j) acc[j] = 0.f;
       const int nch = (kb1 - kb0 + H3_CH - 1) / H3_CH;
       for (int ci = 0; ci < nch; ++ci, ++c) {
-        const int buf = c & 1;
-        mbar_wait(&tfull[buf], (c >> 1) & 1);
+        const int buf = c % NBUF;
+        mbar_wait(&tfull[buf], (c / NBUF) & 1);
         fence_after();
 #pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
+        for (int c0 = 0; c0 < CW; c0 += 16) {
           uint32_t r[16];
           if (a.dbg == 2) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) r[j] = 0;
           } else {
-            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * H3_BN + cq * 64 + c0), r);
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + cq * CW + c0), r);
             tmem_ld_wait();
           }
 #pragma unroll
@@ -332,7 +356,7 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       // chunks XOR-swizzled by the row, conflict-free)
       __syncwarp();  // csb visible to the warp
 #pragma unroll
-      for (int h = 0; h < 64 / H3_EB; ++h, ++tma_seq) {
+      for (int h = 0; h < CW / H3_EB; ++h, ++tma_seq) {
         uint8_t* box = dense_base + (tma_seq % H3_EPIB) * (32 * H3_EB * 4);
         const uint32_t dense = smem_u32(box);
         const int c0 = H3_EB * h;
@@ -370,7 +394,7 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
         __syncwarp();
         if (lane == 0 && a.dbg != 1) {
           if (SK)  // partial tile of segment sid: rows sid*256 + local row
-            tma_store_2d(&tmC, box, cq * 64 + c0, sid * 2 * H3_BM + (int)rank * H3_BM + q * 32);
+            tma_store_2d(&tmC, box, cq * CW + c0, sid * 2 * H3_BM + (int)rank * H3_BM + q * 32);
           else
             tma_store_2d(&tmC, box, n, mrow0);
         }
@@ -385,20 +409,30 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
 }
 
 // stream-K fix-up: C tile = sum of its segments' partials in k order
-__global__ void k_h3_fixup(const float* __restrict__ part, int nblocks_n, int nk, int64_t T, int M,
+__global__ void k_h3_fixup(const float* __restrict__ part, int nblocks_n, int nk, int64_t T, int V, int M,
                            int N, float* __restrict__ C, int ldc) {
   const int tile = blockIdx.y;
   const int mb = tile / nblocks_n, nb = tile % nblocks_n;
   const int64_t t0 = (int64_t)tile * nk, t1 = t0 + nk - 1;
   // unit(t) = max v with vstart(v) <= t = floor(((t+1)*V - 1) / T)
-  const int v0 = (int)(((t0 + 1) * H3_VUNITS - 1) / T), v1 = (int)(((t1 + 1) * H3_VUNITS - 1) / T);
+  const int v0 = (int)(((t0 + 1) * V - 1) / T), v1 = (int)(((t1 + 1) * V - 1) / T);
+  // the tile's contributing virtual units, once per block (some own no k-block
+  // when the k-blocks are fewer than the units)
+  __shared__ int vlist[H3_VUNITS];
+  __shared__ int nv;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int v = v0; v <= v1; ++v)
+      if (vstart(v + 1, T, V) > vstart(v, T, V)) vlist[c++] = v;
+    nv = c;
+  }
+  __syncthreads();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * H3_BM * H3_BN; i += gridDim.x * blockDim.x) {
     const int r = i / H3_BN, cc = i % H3_BN;
     const int m = mb * 2 * H3_BM + r, n = nb * H3_BN + cc;
     if (m >= M || n >= N) continue;
     float s = 0.f;
-    for (int v = v0; v <= v1; ++v)  // (with fewer k-blocks than virtual units some own none)
-      if (vstart(v + 1, T) > vstart(v, T)) s = __fadd_rn(s, part[((size_t)(tile + v) * 2 * H3_BM + r) * H3_BN + cc]);
+    for (int j = 0; j < nv; ++j) s = __fadd_rn(s, part[((size_t)(tile + vlist[j]) * 2 * H3_BM + r) * H3_BN + cc]);
     C[(size_t)m * ldc + n] = s;
   }
 }
@@ -417,14 +451,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// fp16 plane [rows][cols] (ld halves): K-major boxes 32(k) x 128(rows) SW64,
+// fp16 plane [rows][cols] (ld halves): K-major boxes 32(k) x box_rows SW64,
 // MN-major boxes 64(mn) x 32(k) SW128 (rows = K, cols = MN)
-bool map_plane(CUtensorMap* m, const __half* p, uint64_t rows, uint64_t cols, uint64_t ld, bool mn) {
+bool map_plane(CUtensorMap* m, const __half* p, uint64_t rows, uint64_t cols, uint64_t ld, bool mn,
+               uint32_t box_rows = 128) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {mn ? 64u : 32u, mn ? 32u : 128u};
+  cuuint32_t box[2] = {mn ? 64u : 32u, mn ? 32u : box_rows};
   cuuint32_t es[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(p), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
@@ -445,19 +480,27 @@ bool map_out(CUtensorMap* m, float* p, uint64_t rows, uint64_t cols, uint64_t ld
 
 thread_local int g_h3_reserve = 0;
 
-template <bool AMN, bool BMN, bool SK>
+template <bool AMN, bool BMN, bool SK, int BN>
 void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, float* ws,
                  const H3Args& a0, cudaStream_t s);
 // stream-K and data-parallel variants are separate kernels (no 64-bit
-// stream-K state in the data-parallel ones)
+// stream-K state in the data-parallel ones); KP_H3_BN=128 selects 128-wide
+// tiles (4 accumulators in flight) for the data-parallel ones
 template <bool AMN, bool BMN>
 void launch_h3(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, bool splitk,
                float* ws, const H3Args& a, cudaStream_t s) {
-  if (splitk) launch_h3_t<AMN, BMN, true>(A, B, M, N, K, C, ldc, ws, a, s);
-  else launch_h3_t<AMN, BMN, false>(A, B, M, N, K, C, ldc, ws, a, s);
+  static const int bn_env = [] {
+    const char* e = getenv("KP_H3_BN");
+    return e ? atoi(e) : 0;
+  }();
+  // (128-wide tiles for dX measured slower: 702 vs 556 us -- opt-in only)
+  const bool narrow = bn_env == 128;
+  if (splitk) launch_h3_t<AMN, BMN, true, 256>(A, B, M, N, K, C, ldc, ws, a, s);
+  else if (narrow) launch_h3_t<AMN, BMN, false, 128>(A, B, M, N, K, C, ldc, ws, a, s);
+  else launch_h3_t<AMN, BMN, false, 256>(A, B, M, N, K, C, ldc, ws, a, s);
 }
 
-template <bool AMN, bool BMN, bool SK>
+template <bool AMN, bool BMN, bool SK, int BN>
 int h3_units() {
   static int units = 0;
   if (units) return units;
@@ -468,7 +511,7 @@ int h3_units() {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(4, 1, 1);
   cfg.blockDim = dim3(H3_WARPS * 32, 1, 1);
-  cfg.dynamicSmemBytes = H3_SMEM;
+  cfg.dynamicSmemBytes = H3Cfg<BN>::SMEM;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
@@ -477,33 +520,35 @@ int h3_units() {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_h3<AMN, BMN, SK>, &cfg) == cudaSuccess && n > 0) units = std::min(units, n);
+  if (cudaOccupancyMaxActiveClusters(&n, k_h3<AMN, BMN, SK, BN>, &cfg) == cudaSuccess && n > 0) units = std::min(units, n);
   cudaGetLastError();
   return units;
 }
 
-template <bool AMN, bool BMN, bool SK>
+template <bool AMN, bool BMN, bool SK, int BN>
 void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, float* ws,
                  const H3Args& a0, cudaStream_t s) {
+  static_assert(!SK || BN == 256, "stream-K partial tiles are 256 wide");
   constexpr bool splitk = SK;
   CUtensorMap tah, tal, tbh, tbl, tcm;
   // K-major operand [rows][K]; MN-major [K][rows]
-  auto mk = [&](CUtensorMap* m, const __half* p, const H3Operand& op, int rows, bool mn) {
-    return mn ? map_plane(m, p, K, rows, op.ld, true) : map_plane(m, p, rows, K, op.ld, false);
+  auto mk = [&](CUtensorMap* m, const __half* p, const H3Operand& op, int rows, bool mn, uint32_t box_rows) {
+    return mn ? map_plane(m, p, K, rows, op.ld, true) : map_plane(m, p, rows, K, op.ld, false, box_rows);
   };
-  bool ok = mk(&tah, A.hi, A, M, AMN) && mk(&tal, A.lo, A, M, AMN) && mk(&tbh, B.hi, B, N, BMN) &&
-            mk(&tbl, B.lo, B, N, BMN);
+  bool ok = mk(&tah, A.hi, A, M, AMN, 128) && mk(&tal, A.lo, A, M, AMN, 128) &&
+            mk(&tbh, B.hi, B, N, BMN, BN / 2) && mk(&tbl, B.lo, B, N, BMN, BN / 2);
   H3Args a = a0;
   a.M = M;
   a.N = N;
   a.K = K;
   a.nblocks_m = (int)ceil_div(M, 2 * H3_BM);
-  a.nblocks_n = (int)ceil_div(N, H3_BN);
+  a.nblocks_n = (int)ceil_div(N, BN);
   a.nk = (int)ceil_div(K, H3_BK);
   a.splitk = splitk ? 1 : 0;
   a.ea = A.exp;
   a.eb = B.exp;
   const int tiles = a.nblocks_m * a.nblocks_n;
+  a.vunits = h3_vunits((int64_t)tiles * a.nk);
   if (splitk) {
     a.mode = 0;  // partials are plain sums (scales are exact and applied per partial)
     ok = ok && map_out(&tcm, ws, (uint64_t)(tiles + H3_VUNITS) * 2 * H3_BM, H3_BN, H3_BN);
@@ -511,17 +556,17 @@ void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, fl
     ok = ok && map_out(&tcm, C, M, N, ldc);
   }
   KP_CHECK(ok, kErrCuda, "cuTensorMapEncodeTiled failed (3xFP16 GEMM operands)");
-  constexpr uint32_t SMEM = H3_SMEM;
+  constexpr uint32_t SMEM = H3Cfg<BN>::SMEM;
   static std::atomic<uint64_t> attr{0};
   int dev = 0;
   KP_CUDA(cudaGetDevice(&dev));
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr.load(std::memory_order_acquire) & bit)) {
-    KP_CUDA(cudaFuncSetAttribute(k_h3<AMN, BMN, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    KP_CUDA(cudaFuncSetAttribute(k_h3<AMN, BMN, SK, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     attr.fetch_or(bit, std::memory_order_release);
   }
-  const int units_all = std::max(1, h3_units<AMN, BMN, SK>() - (g_h3_reserve + 1) / 2);
-  const int work = splitk ? H3_VUNITS : tiles;
+  const int units_all = std::max(1, h3_units<AMN, BMN, SK, BN>() - (g_h3_reserve + 1) / 2);
+  const int work = splitk ? a.vunits : tiles;
   const unsigned grid = (unsigned)std::min(work, units_all) * 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
@@ -535,11 +580,11 @@ void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, fl
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  KP_CUDA(cudaLaunchKernelEx(&cfg, k_h3<AMN, BMN, SK>, tah, tal, tbh, tbl, tcm, a));
+  KP_CUDA(cudaLaunchKernelEx(&cfg, k_h3<AMN, BMN, SK, BN>, tah, tal, tbh, tbl, tcm, a));
   ::kp::count_launch();
   if (splitk) {
     const int64_t T = (int64_t)tiles * a.nk;
-    k_h3_fixup<<<dim3(64, tiles), 256, 0, s>>>(ws, a.nblocks_n, a.nk, T, M, N, C, ldc);
+    k_h3_fixup<<<dim3(64, tiles), 256, 0, s>>>(ws, a.nblocks_n, a.nk, T, a.vunits, M, N, C, ldc);
     ::kp::count_launch();
   }
 }
