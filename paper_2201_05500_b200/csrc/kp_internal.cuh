@@ -76,12 +76,11 @@ void shard(const uint64_t* d_unique, uint32_t n, uint32_t G, uint32_t* d_perm,
 struct Table {
   int device = 0;
   uint64_t capacity = 0;  // max rows
-  uint64_t nslots = 0;    // power of two, 16 slots per 128 B bucket
+  uint64_t nslots = 0;    // power of two, 8 slots per 128 B bucket line (keys + rows)
   uint32_t dim = 0;
   int rule = 0;  // 0 adagrad {w, acc}; 1 adam {w, m, v}
   float init_w = 0.f, init_s1 = 0.f, init_s2 = 0.f;
-  uint64_t* d_keys = nullptr;
-  uint32_t* d_rows = nullptr;
+  uint8_t* d_lines = nullptr;  // [nslots / 8] x 128 B: 8 keys u64 + 8 rows u32 + pad
   uint64_t* d_row_key = nullptr;
   float* d_w = nullptr;
   float* d_s1 = nullptr;

@@ -59,25 +59,29 @@ __device__ uint32_t probe(const TView& t, uint64_t key, int gl, uint32_t gmask, 
   }
   uint64_t b = mix64(key) & t.bmask;
   uint64_t probes = 0;
+  const bool klane = gl < kSlotsPerLine;  // lanes 0-7 read the line's keys, 8-15 its rows
   for (;;) {
-    const uint64_t slot = b * GS + gl;
-    const uint64_t k = *(volatile uint64_t*)(t.keys + slot);
-    const uint32_t match = __ballot_sync(gmask, k == key) >> gbase;
+    uint64_t k = 0;
+    uint32_t rv = 0;
+    if (klane) k = *(volatile uint64_t*)line_key(t.lines, b, gl);
+    else rv = *(volatile uint32_t*)line_row(t.lines, b, gl - kSlotsPerLine);
+    const uint32_t match = (__ballot_sync(gmask, klane && k == key) >> gbase) & 0xFFu;
     if (match) {
-      const uint64_t s = b * GS + (__ffs(match) - 1);
-      volatile uint32_t* rp = t.rows + s;
-      uint32_t r = *rp;
-      while (r == kNoRow && INSERT) r = *rp;  // inserter in flight (same key, same launch)
+      const int i = __ffs(match) - 1;
+      uint32_t r = __shfl_sync(gmask, rv, gbase + kSlotsPerLine + i);
+      if (r == kNoRow && INSERT) {  // inserter in flight (same key, same launch)
+        volatile uint32_t* rp = line_row(t.lines, b, i);
+        while (r == kNoRow) r = *rp;
+      }
       return r >= kFullRow ? kNoRow : r;
     }
-    const uint32_t empty = __ballot_sync(gmask, k == kEmptyKey) >> gbase;
+    const uint32_t empty = (__ballot_sync(gmask, klane && k == kEmptyKey) >> gbase) & 0xFFu;
     if (empty) {
       if (!INSERT) return kNoRow;
       const int el = __ffs(empty) - 1;
-      const uint64_t s = b * GS + el;
       unsigned long long old = 0;
       if (gl == el)
-        old = atomicCAS((unsigned long long*)(t.keys + s), (unsigned long long)kEmptyKey,
+        old = atomicCAS((unsigned long long*)line_key(t.lines, b, el), (unsigned long long)kEmptyKey,
                         (unsigned long long)key);
       old = __shfl_sync(gmask, old, gbase + el);
       if (old == kEmptyKey) {
@@ -94,11 +98,11 @@ __device__ uint32_t probe(const TView& t, uint64_t key, int gl, uint32_t gmask, 
         row = __shfl_sync(gmask, row, gbase + el);
         if (row != kNoRow) init_row(t, row, gl);
         __threadfence();
-        if (gl == el) *(volatile uint32_t*)(t.rows + s) = row == kNoRow ? kFullRow : row;
+        if (gl == el) *(volatile uint32_t*)line_row(t.lines, b, el) = row == kNoRow ? kFullRow : row;
         return row;
       }
       if (old == key) {
-        volatile uint32_t* rp = t.rows + s;
+        volatile uint32_t* rp = line_row(t.lines, b, el);
         uint32_t r = *rp;
         while (r == kNoRow) r = *rp;
         return r >= kFullRow ? kNoRow : r;
@@ -122,6 +126,7 @@ __global__ void k_probe(TView t, const uint64_t* __restrict__ keys, uint32_t n,
   const uint32_t gmask = 0xFFFFu << gbase;
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / GS;
   const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / GS;
+  // (two keys' lines in flight per group measured slower: 108 vs 95 us)
   for (uint64_t i = g0; i < n; i += ng) {
     const uint32_t r = probe<INSERT>(t, keys[i], gl, gmask, gbase);
     if (gl == 0) {
@@ -135,10 +140,12 @@ __global__ void k_export(TView t, uint64_t nslots, uint64_t* __restrict__ out_ke
                          uint32_t* __restrict__ out_rows, unsigned long long* __restrict__ cnt) {
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < nslots;
        s += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = t.rows[s];
+    const uint64_t b = s / kSlotsPerLine;
+    const int i = (int)(s % kSlotsPerLine);
+    const uint32_t r = *line_row(t.lines, b, i);
     if (r < t.capacity) {
       const unsigned long long p = atomicAdd(cnt, 1ull);
-      out_keys[p] = t.keys[s];
+      out_keys[p] = *line_key(t.lines, b, i);
       out_rows[p] = r;
     }
   }
@@ -240,19 +247,17 @@ Table* table_create(int device, uint64_t capacity, uint32_t dim, int rule, float
   t->init_s1 = init_s1;
   t->init_s2 = init_s2;
   uint64_t ns = 16;
-  while (ns < 2 * capacity) ns <<= 1;  // load factor <= 0.5
+  while (ns < 2 * capacity) ns <<= 1;  // load factor <= 0.5 (>= 2 bucket lines)
   t->nslots = ns;
   try {
-    KP_CUDA(cudaMalloc(&t->d_keys, ns * 8));
-    KP_CUDA(cudaMalloc(&t->d_rows, ns * 4));
+    KP_CUDA(cudaMalloc(&t->d_lines, ns / kSlotsPerLine * kLineBytes));
     KP_CUDA(cudaMalloc(&t->d_row_key, capacity * 8));
     KP_CUDA(cudaMalloc(&t->d_w, capacity * dim * 4));
     KP_CUDA(cudaMalloc(&t->d_s1, capacity * dim * 4));
     if (rule == 1) KP_CUDA(cudaMalloc(&t->d_s2, capacity * dim * 4));
     KP_CUDA(cudaMalloc(&t->d_epoch, capacity * 4));
     KP_CUDA(cudaMalloc(&t->d_scalars, 64));
-    KP_CUDA(cudaMemset(t->d_keys, 0xFF, ns * 8));
-    KP_CUDA(cudaMemset(t->d_rows, 0xFF, ns * 4));
+    KP_CUDA(cudaMemset(t->d_lines, 0xFF, ns / kSlotsPerLine * kLineBytes));  // empty keys, kNoRow rows
     KP_CUDA(cudaMemset(t->d_epoch, 0, capacity * 4));
     uint32_t sc[16] = {0, kNoRow, 0, 0};
     KP_CUDA(cudaMemcpy(t->d_scalars, sc, 64, cudaMemcpyHostToDevice));
@@ -266,8 +271,7 @@ Table* table_create(int device, uint64_t capacity, uint32_t dim, int rule, float
 void table_destroy(Table* t) {
   if (!t) return;
   cudaSetDevice(t->device);
-  cudaFree(t->d_keys);
-  cudaFree(t->d_rows);
+  cudaFree(t->d_lines);
   cudaFree(t->d_row_key);
   cudaFree(t->d_w);
   cudaFree(t->d_s1);

@@ -4,13 +4,15 @@
 
 namespace kp {
 
-// Open addressing: slot keys u64 [nslots] + slot rows u32 [nslots]; a bucket is
-// 16 consecutive slots = one 128 B line of keys, probed by a 16-lane group with
-// one coalesced load and two ballots. Rows are dense SoA fp32 arrays
-// w[rows][dim], s1[rows][dim] (AdaGrad acc | Adam m), s2 (Adam v).
+// Open addressing in 128-byte bucket lines: 8 slot keys u64 (bytes 0-63)
+// and their 8 row indices u32 (bytes 64-95) in the same line, so one
+// coalesced load of a 16-lane group (8 key lanes + 8 row lanes) resolves a
+// hit; two ballots find a match / an empty slot. Rows are dense SoA fp32
+// arrays w[rows][dim], s1[rows][dim] (AdaGrad acc | Adam m), s2 (Adam v).
+constexpr int kSlotsPerLine = 8;
+constexpr int kLineBytes = 128;
 struct TView {
-  uint64_t* keys;
-  uint32_t* rows;
+  uint8_t* lines;
   uint64_t* row_key;
   float* w;
   float* s1;
@@ -25,17 +27,23 @@ struct TView {
   const uint32_t* abort;  // g_abort at view time (null: unguarded)
 };
 
+__host__ __device__ __forceinline__ uint64_t* line_key(uint8_t* lines, uint64_t b, int i) {
+  return reinterpret_cast<uint64_t*>(lines + b * kLineBytes) + i;
+}
+__host__ __device__ __forceinline__ uint32_t* line_row(uint8_t* lines, uint64_t b, int i) {
+  return reinterpret_cast<uint32_t*>(lines + b * kLineBytes + 64) + i;
+}
+
 inline TView view(const Table* t) {
   TView v;
-  v.keys = t->d_keys;
-  v.rows = t->d_rows;
+  v.lines = t->d_lines;
   v.row_key = t->d_row_key;
   v.w = t->d_w;
   v.s1 = t->d_s1;
   v.s2 = t->d_s2;
   v.epoch = t->d_epoch;
   v.sc = t->d_scalars;
-  v.bmask = t->nslots / 16 - 1;
+  v.bmask = t->nslots / kSlotsPerLine - 1;
   v.capacity = t->capacity;
   v.dim = t->dim;
   v.rule = t->rule;
