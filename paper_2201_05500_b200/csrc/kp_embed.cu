@@ -509,6 +509,8 @@ __device__ __forceinline__ void sum_range(const SegArgs& a, uint32_t p, uint32_t
 #pragma unroll
     for (int u = 0; u < UR; ++u) acc.add(r[u]);
   }
+  // (the tail one row at a time: batching its loads with predicates
+  // measured slower, 0.76 vs 0.70 ms -- registers/occupancy)
   for (; p < q; ++p) {
     r[0].load(a.rows_src + (uint64_t)src_row(a, p) * a.e, gl, a.e);
     acc.add(r[0]);
