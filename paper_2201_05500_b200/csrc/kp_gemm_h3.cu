@@ -623,12 +623,14 @@ __global__ void k_split_rows(const float* __restrict__ x, int rows, int K, int l
 // per COLUMN o (the GEMM row of dW): pass 1 column maxima, pass 2 planes.
 // Layout for both: a thread owns 4 consecutive columns (float4) of a row,
 // blockDim.x = N/4 threads span a row, blockDim.y rows per block step.
+// (csum, optional: the plain column sums of dz -- the layer's bias gradient --
+// as per-block partials [gridDim.x][N] in a fixed order, reduced after)
 __global__ void k_colmax_scaled(const float* __restrict__ dz, int B, int N, const int* __restrict__ xe,
-                                unsigned* __restrict__ cmax) {
+                                unsigned* __restrict__ cmax, float* __restrict__ csum) {
   __shared__ float red[1024];  // [blockDim.y][4 * blockDim.x] <= 1024
   const int n4 = blockIdx.y * blockDim.x + threadIdx.x;  // column quad (slab blockIdx.y)
   const bool in = n4 < N / 4;
-  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f), sm = mx;
   for (int b = blockIdx.x * blockDim.y + threadIdx.y; in && b < B; b += gridDim.x * blockDim.y) {
     const float4 v = __ldg(reinterpret_cast<const float4*>(dz + (size_t)b * N) + n4);
     const float xs = xe ? pow2f(-__ldg(xe + b)) : 1.f;
@@ -636,6 +638,8 @@ __global__ void k_colmax_scaled(const float* __restrict__ dz, int B, int N, cons
     mx.y = fmaxf(mx.y, fabsf(__fmul_rn(v.y, xs)));
     mx.z = fmaxf(mx.z, fabsf(__fmul_rn(v.z, xs)));
     mx.w = fmaxf(mx.w, fabsf(__fmul_rn(v.w, xs)));
+    sm.x = __fadd_rn(sm.x, v.x), sm.y = __fadd_rn(sm.y, v.y);
+    sm.z = __fadd_rn(sm.z, v.z), sm.w = __fadd_rn(sm.w, v.w);
   }
   const int W = 4 * blockDim.x;  // slab width (columns)
   float* rr = red + threadIdx.y * W + 4 * threadIdx.x;
@@ -646,6 +650,28 @@ __global__ void k_colmax_scaled(const float* __restrict__ dz, int B, int N, cons
     for (int r = 0; r < (int)blockDim.y; ++r) m = fmaxf(m, red[r * W + c]);
     const int col = blockIdx.y * W + c;
     if (m > 0.f && col < N) atomicMax(cmax + col, __float_as_uint(m));
+  }
+  if (!csum) return;
+  __syncthreads();
+  rr[0] = sm.x, rr[1] = sm.y, rr[2] = sm.z, rr[3] = sm.w;
+  __syncthreads();
+  for (int c = threadIdx.y * blockDim.x + threadIdx.x; c < W; c += blockDim.x * blockDim.y) {
+    float t = 0.f;
+    for (int r = 0; r < (int)blockDim.y; ++r) t = __fadd_rn(t, red[r * W + c]);  // rows in y order
+    const int col = blockIdx.y * W + c;
+    if (col < N) csum[(size_t)blockIdx.x * N + col] = t;
+  }
+}
+
+// out[n] = sum over the per-block partials in block order (deterministic)
+__global__ void k_sum_parts(const float* __restrict__ part, int nparts, int N, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < N; n += (gridDim.x * blockDim.x) >> 5) {
+    float v = 0.f;
+    for (int c = lane; c < nparts; c += 32) v = __fadd_rn(v, part[(size_t)c * N + n]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) out[n] = v;
   }
 }
 __global__ void k_split_cols_scaled(const float* __restrict__ dz, int B, int N, const int* __restrict__ xe,
@@ -719,6 +745,12 @@ void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M
   else launch_h3<false, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
 }
 
+size_t split_cols_colsum_ws_floats(int B, int N) {
+  const int W = std::min(N, 1024);
+  const int by = std::max(1, std::min(8, 256 / (W / 4)));
+  return (size_t)std::min<uint64_t>(ceil_div(B, by), std::max<uint64_t>(1, 148 * 8 / ceil_div(N, W))) * N;
+}
+
 size_t h3_splitk_ws_floats(int M, int N) {
   const size_t tiles = ceil_div(M, 2 * H3_BM) * ceil_div(N, H3_BN);
   return (tiles + H3_VUNITS) * 2 * H3_BM * H3_BN;
@@ -731,7 +763,7 @@ void split_rows_h(const float* X, int rows, int K, int ld, __half* hi, __half* l
 }
 
 void split_cols_scaled_h(const float* dz, int B, int N, const int* xe, unsigned* cmax_ws, __half* hi, __half* lo,
-                         int* exps, cudaStream_t s) {
+                         int* exps, cudaStream_t s, float* colsum_out, float* colsum_ws) {
   KP_CHECK(N % 4 == 0, kErrConfig, "split_cols_scaled_h: N must be a multiple of 4");
   KP_CUDA(cudaMemsetAsync(cmax_ws, 0, (size_t)N * 4, s));
   // slabs of up to 1024 columns (blockIdx.y), rows strided over blockIdx.x
@@ -739,8 +771,13 @@ void split_cols_scaled_h(const float* dz, int B, int N, const int* xe, unsigned*
   const dim3 blk(W / 4, std::max(1, std::min(8, 256 / (W / 4))));
   const unsigned slabs = ceil_div(N, W);
   const dim3 g((unsigned)std::min<uint64_t>(ceil_div(B, blk.y), std::max<uint64_t>(1, 148 * 8 / slabs)), slabs);
-  k_colmax_scaled<<<g, blk, 0, s>>>(dz, B, N, xe, cmax_ws);
+  k_colmax_scaled<<<g, blk, 0, s>>>(dz, B, N, xe, cmax_ws, colsum_out ? colsum_ws : nullptr);
   ::kp::count_launch();
+  if (colsum_out) {
+    k_sum_parts<<<std::min<unsigned>(ceil_div((uint64_t)N * 32, 256), 148 * 16), 256, 0, s>>>(colsum_ws, (int)g.x, N,
+                                                                                          colsum_out);
+    ::kp::count_launch();
+  }
   k_split_cols_scaled<<<g, blk, 0, s>>>(dz, B, N, xe, cmax_ws, hi, lo, exps);
   ::kp::count_launch();
 }

@@ -261,8 +261,12 @@ void h3_reserve_sms(int n);
 // planes of each row of X [rows][K] with its own exponent (one warp per row)
 void split_rows_h(const float* X, int rows, int K, int ld, __half* hi, __half* lo, int* exps, cudaStream_t s);
 // planes of D[b][n] = dz[b][n] * 2^-xe[b] with one exponent per column n
+// colsum_out (optional): the plain column sums of dz (a bias gradient) from the
+// same read, via colsum_ws (split_cols_colsum_ws_floats)
 void split_cols_scaled_h(const float* dz, int B, int N, const int* xe, unsigned* cmax_ws, __half* hi,
-                         __half* lo, int* exps, cudaStream_t s);
+                         __half* lo, int* exps, cudaStream_t s, float* colsum_out = nullptr,
+                         float* colsum_ws = nullptr);
+size_t split_cols_colsum_ws_floats(int B, int N);
 // pooling written as the first layer's planes (see kp_embed.cu k_pool_planes)
 bool pool_planes_supported(uint32_t S, uint32_t e);
 void pool_planes(const uint32_t* d_bag_offs, uint32_t n_inst, uint32_t S, const uint32_t* d_row_of_occ,

@@ -491,6 +491,55 @@ void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, c
   }
 }
 
+// The head's three reductions in one pass (model.cpp:163-177 for the last
+// two layers): virtual column n < W: sum_b delta[b] * a[b][n] (head weight
+// gradient), W <= n < W + W2: sum_b dz[b][n - W] (the hidden layer's bias
+// gradient), n == W + W2: sum_b delta[b] (head bias). Per 512-row chunk
+// partials like k_colsum_part (fixed order), reduced by k_reduce_chunks_to.
+__global__ void k_colsum_head(const float* __restrict__ a, const float* __restrict__ delta,
+                              const float* __restrict__ dz, int B, int W, int W2, float* __restrict__ part) {
+  __shared__ float red[8][33];
+  const int NT = W + W2 + 1;
+  const int n = blockIdx.x * 32 + threadIdx.x;
+  const int c = blockIdx.y;
+  const int b0 = c * COLSUM_ROWS, b1 = min(B, b0 + COLSUM_ROWS);
+  float acc = 0.f;
+  if (n < NT) {
+    for (int b = b0 + threadIdx.y; b < b1; b += 8) {
+      float x;
+      if (n < W) x = __fmul_rn(delta[b], a[(size_t)b * W + n]);
+      else if (n < W + W2) x = dz[(size_t)b * W2 + (n - W)];
+      else x = delta[b];
+      acc = __fadd_rn(acc, x);
+    }
+  }
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && n < NT) {
+    float t = red[0][threadIdx.x];
+    for (int i = 1; i < 8; ++i) t = __fadd_rn(t, red[i][threadIdx.x]);
+    part[(size_t)c * NT + n] = t;
+  }
+}
+
+// k_reduce_chunks writing column n to out0[n] (n < n0), out1[n - n0]
+// (n < n0 + n1), out2[n - n0 - n1]
+__global__ void k_reduce_chunks_to(const float* __restrict__ part, int chunks, int N, int n0, int n1,
+                                   float* __restrict__ out0, float* __restrict__ out1, float* __restrict__ out2) {
+  const int lane = threadIdx.x & 31;
+  for (int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < N; n += (gridDim.x * blockDim.x) >> 5) {
+    float v = 0.f;
+    for (int c = lane; c < chunks; c += 32) v = __fadd_rn(v, part[(size_t)c * N + n]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) {
+      if (n < n0) out0[n] = v;
+      else if (n < n0 + n1) out1[n - n0] = v;
+      else out2[n - n0 - n1] = v;
+    }
+  }
+}
+
 // column sums of the chunk partials [chunks][N]: one warp per column, lane j
 // adds chunks j, j+32, ... in order, then a fixed xor tree (deterministic)
 __global__ void k_reduce_chunks(const float* __restrict__ part, int chunks, int N,
@@ -548,8 +597,20 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
                                  static_cast<const float*>(ws.logits.p), d_preds, d_labels,
                                  (float)B, delta, dprev, mode, m.activation, d_coeff, S, e, lossp); ::kp::count_launch();
   k_loss_finalize<<<1, 32, 0, s>>>(lossp, hb, B, d_loss_sum); ::kp::count_launch();
-  colsum(layer_in(L - 1), delta, B, W, d_grad + m.w_off[L - 1], ws, s);
-  colsum(delta, nullptr, B, 1, d_grad + m.b_off[L - 1], ws, s);
+  // head weight + bias gradients, and (with hidden layers) the last hidden
+  // layer's bias gradient (the column sums of dprev = its dZ): one pass
+  const bool fused_bias = L >= 2;
+  {
+    const int W2 = fused_bias ? W : 0;
+    const int NT = W + W2 + 1;
+    const int chunks = std::max(1, (int)((B + COLSUM_ROWS - 1) / COLSUM_ROWS));
+    float* part = ws.partials.get<float>((size_t)chunks * NT);
+    k_colsum_head<<<dim3(ceil_div(NT, 32), chunks), dim3(32, 8), 0, s>>>(layer_in(L - 1), delta, dprev, B, W, W2,
+                                                                          part); ::kp::count_launch();
+    k_reduce_chunks_to<<<grid_cap(ceil_div((uint64_t)NT * 32, 256)), 256, 0, s>>>(
+        part, chunks, NT, W, W2, d_grad + m.w_off[L - 1], fused_bias ? d_grad + m.b_off[L - 2] : nullptr,
+        d_grad + m.b_off[L - 1]); ::kp::count_launch();
+  }
   // ---- hidden layers, top down ----
   int cur = 0;
   for (int l = (int)L - 2; l >= 0; --l) {
@@ -580,12 +641,15 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
       __half* dwh = reinterpret_cast<__half*>(ws.dwh.get<uint16_t>((size_t)B * N));
       __half* dwl = reinterpret_cast<__half*>(ws.dwl.get<uint16_t>((size_t)B * N));
       int* dwe = ws.dwe.get<int>(N);
-      split_cols_scaled_h(dZ, B, N, ws.in_exp, ws.cmax.get<unsigned>(N), dwh, dwl, dwe, s);
+      // (the layer's bias gradient = column sums of dZ, from the same read)
+      const bool bias_here = l != (int)L - 2;
+      split_cols_scaled_h(dZ, B, N, ws.in_exp, ws.cmax.get<unsigned>(N), dwh, dwl, dwe, s,
+                          bias_here ? d_grad + m.b_off[l] : nullptr,
+                          bias_here ? ws.partials.get<float>(split_cols_colsum_ws_floats(B, N)) : nullptr);
       EpiArgs plain{kStore, 0, nullptr, nullptr, 0, nullptr, 1, 1};
       h3_gemm(H3Operand{dwh, dwl, dwe, N}, true, H3Operand{ws.in_hi, ws.in_lo, nullptr, K}, true, N, K, B,
               d_grad + m.w_off[l], K, plain, true, ws.skws.get<float>(h3_splitk_ws_floats(N, K)), s,
               /*keep dZ', stream X*/ 1);
-      colsum(dZ, nullptr, B, N, d_grad + m.b_off[l], ws, s);
       continue;
     }
     // first layer: the input gradient goes first so its consumer can overlap
@@ -615,7 +679,7 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
       k_reduce_splits<<<grid_cap(ceil_div((uint64_t)N * K, 256)), 256, 0, s>>>(
           part, got, (size_t)N * K, d_grad + m.w_off[l]); ::kp::count_launch();
     }
-    colsum(dZ, nullptr, B, N, d_grad + m.b_off[l], ws, s);
+    if (l != (int)L - 2) colsum(dZ, nullptr, B, N, d_grad + m.b_off[l], ws, s);  // (L-2: with the head's)
     // upstream for the layer below: dX = dZ . W_l, then act' or pooling coeff
     if (l > 0) {
       float* next = ws.dz[cur ^ 1].get<float>((size_t)B * K);
