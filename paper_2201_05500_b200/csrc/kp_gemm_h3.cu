@@ -427,13 +427,23 @@ __global__ void k_h3_fixup(const float* __restrict__ part, int nblocks_n, int nk
     nv = c;
   }
   __syncthreads();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * H3_BM * H3_BN; i += gridDim.x * blockDim.x) {
-    const int r = i / H3_BN, cc = i % H3_BN;
+  // 4 consecutive columns per thread (float4 partial loads)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * H3_BM * H3_BN / 4; i += gridDim.x * blockDim.x) {
+    const int r = (4 * i) / H3_BN, cc = (4 * i) % H3_BN;
     const int m = mb * 2 * H3_BM + r, n = nb * H3_BN + cc;
     if (m >= M || n >= N) continue;
-    float s = 0.f;
-    for (int j = 0; j < nv; ++j) s = __fadd_rn(s, part[((size_t)(tile + vlist[j]) * 2 * H3_BM + r) * H3_BN + cc]);
-    C[(size_t)m * ldc + n] = s;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < nv; ++j) {
+      const float4 p = *reinterpret_cast<const float4*>(part + ((size_t)(tile + vlist[j]) * 2 * H3_BM + r) * H3_BN + cc);
+      s.x = __fadd_rn(s.x, p.x), s.y = __fadd_rn(s.y, p.y), s.z = __fadd_rn(s.z, p.z), s.w = __fadd_rn(s.w, p.w);
+    }
+    float* c = C + (size_t)m * ldc + n;
+    if (n + 3 < N && (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) {
+      *reinterpret_cast<float4*>(c) = s;
+    } else {
+      const float v[4] = {s.x, s.y, s.z, s.w};
+      for (int t = 0; t < 4 && n + t < N; ++t) c[t] = v[t];
+    }
   }
 }
 
@@ -618,6 +628,52 @@ __global__ void k_split_rows(const float* __restrict__ x, int rows, int K, int l
   }
 }
 
+// W [N][K] -> planes of W^T ([K][N]) with one exponent per row of W^T (per
+// column k of W): a block owns 32 columns of W, stages the 32 x N tile in
+// shared memory (N <= 256), reduces each column's max and writes the
+// transposed planes -- the transpose and the per-row split of round 1 in one
+// read of W.
+__global__ void k_split_t(const float* __restrict__ w, int N, int K, __half* __restrict__ hi,
+                          __half* __restrict__ lo, int* __restrict__ exps) {
+  __shared__ float tile[256][33];
+  __shared__ float cmax[8][32];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  const int k0 = blockIdx.x * 32, k = k0 + tx;
+  float mx = 0.f;
+  for (int n = ty; n < N; n += 8) {
+    const float v = k < K ? w[(size_t)n * K + k] : 0.f;
+    tile[n][tx] = v;
+    mx = fmaxf(mx, fabsf(v));
+  }
+  cmax[ty][tx] = mx;
+  __syncthreads();
+  if (ty == 0) {
+    float m = cmax[0][tx];
+    for (int i = 1; i < 8; ++i) m = fmaxf(m, cmax[i][tx]);
+    cmax[0][tx] = pow2f(row_exp(m));
+    if (k < K) exps[k] = row_exp(m);
+  }
+  __syncthreads();
+  // row kk of W^T = column k0 + kk of W: consecutive threads take consecutive n
+  for (int kk = ty; kk < 32; kk += 8) {
+    const int kr = k0 + kk;
+    if (kr >= K) break;
+    const float sc = cmax[0][kk];
+    for (int n2 = 2 * tx; n2 < N; n2 += 64) {
+      const float x0 = __fmul_rn(tile[n2][kk], sc), x1 = n2 + 1 < N ? __fmul_rn(tile[n2 + 1][kk], sc) : 0.f;
+      uint32_t h, l;
+      split_h2(x0, x1, h, l);
+      if (n2 + 1 < N) {
+        *reinterpret_cast<uint32_t*>(hi + (size_t)kr * N + n2) = h;
+        *reinterpret_cast<uint32_t*>(lo + (size_t)kr * N + n2) = l;
+      } else {
+        hi[(size_t)kr * N + n2] = __ushort_as_half((unsigned short)(h & 0xFFFF));
+        lo[(size_t)kr * N + n2] = __ushort_as_half((unsigned short)(l & 0xFFFF));
+      }
+    }
+  }
+}
+
 // dW's A operand: D[b][o] = dZ[b][o] * 2^-xe[b] (X's row scale moved onto the
 // other factor, so the sum over b needs no per-k scale), split with a scale
 // per COLUMN o (the GEMM row of dW): pass 1 column maxima, pass 2 planes.
@@ -754,6 +810,12 @@ size_t split_cols_colsum_ws_floats(int B, int N) {
 size_t h3_splitk_ws_floats(int M, int N) {
   const size_t tiles = ceil_div(M, 2 * H3_BM) * ceil_div(N, H3_BN);
   return (tiles + H3_VUNITS) * 2 * H3_BM * H3_BN;
+}
+
+void split_t_h(const float* W, int N, int K, __half* hi, __half* lo, int* exps, cudaStream_t s) {
+  KP_CHECK(N <= 256 && N % 2 == 0, kErrConfig, "split_t_h: N must be even and <= 256");
+  k_split_t<<<ceil_div(K, 32), 256, 0, s>>>(W, N, K, hi, lo, exps);
+  ::kp::count_launch();
 }
 
 void split_rows_h(const float* X, int rows, int K, int ld, __half* hi, __half* lo, int* exps, cudaStream_t s) {

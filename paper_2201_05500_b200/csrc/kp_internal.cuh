@@ -258,6 +258,8 @@ void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M
              int ldc, const GemmEpi& ep, bool splitk, float* ws, cudaStream_t s, int keep = 3);
 size_t h3_splitk_ws_floats(int M, int N);
 void h3_reserve_sms(int n);
+// planes of W^T ([K][N], one exponent per row of W^T) from W [N][K], N <= 256
+void split_t_h(const float* W, int N, int K, __half* hi, __half* lo, int* exps, cudaStream_t s);
 // planes of each row of X [rows][K] with its own exponent (one warp per row)
 void split_rows_h(const float* X, int rows, int K, int ld, __half* hi, __half* lo, int* exps, cudaStream_t s);
 // planes of D[b][n] = dz[b][n] * 2^-xe[b] with one exponent per column n
@@ -294,6 +296,7 @@ struct MlpWs {
   const __half* in_lo = nullptr;
   const int* in_exp = nullptr;
   DevBuf dzh, dzl, dze, dwh, dwl, dwe, cmax, skws;  // layer-1 backward planes, stream-K partials
+  DevBuf hdone;  // head backward's last-block counter (the loss finalize)
 };
 // Forward over B instances (input [B][in]); writes preds (sigmoid) and
 // logits; keeps activations in ws for backward.

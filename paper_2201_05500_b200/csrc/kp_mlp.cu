@@ -294,8 +294,10 @@ __global__ void k_head_bwd(const float* __restrict__ in, int B, int W, const flo
                            const int32_t* __restrict__ labels, float nb,
                            float* __restrict__ delta, float* __restrict__ dprev, int mode, int act,
                            const float* __restrict__ coeff, uint32_t S, uint32_t e,
-                           double* __restrict__ loss_part) {
+                           double* __restrict__ loss_part, unsigned* __restrict__ done,
+                           double* __restrict__ loss_sum, int n_loss) {
   __shared__ double s_loss[8];
+  __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -324,22 +326,24 @@ __global__ void k_head_bwd(const float* __restrict__ in, int B, int W, const flo
     double t = 0.0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += s_loss[q];
     loss_part[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;  // the last block finalizes
   }
-}
-
-// loss_sum += (sum / n) * n  -- the reference's loss_sum += bwd.loss * mb.size
-__global__ void k_loss_finalize(const double* __restrict__ part, int nparts, int n,
-                                double* __restrict__ loss_sum) {
-  // 32 lanes sum strided partials, then lane 0 combines them in lane order
+  __syncthreads();
+  if (!last || warp != 0) return;
+  __threadfence();
+  // loss_sum += (sum / n) * n, the reference's loss_sum += bwd.loss * mb.size
+  // (trainer.cpp:177): 32 lanes sum strided partials, lane 0 combines in order
+  __shared__ double s_fin[32];
   double t = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += 32) t += part[i];
-  __shared__ double s[32];
-  s[threadIdx.x] = t;
+  for (int i = lane; i < (int)gridDim.x; i += 32) t += *reinterpret_cast<volatile double*>(loss_part + i);
+  s_fin[lane] = t;
   __syncwarp();
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
     double u = 0.0;
-    for (int i = 0; i < 32; ++i) u += s[i];
-    *loss_sum += (u / (double)n) * (double)n;
+    for (int i = 0; i < 32; ++i) u += s_fin[i];
+    *loss_sum += (u / (double)n_loss) * (double)n_loss;
+    *done = 0u;  // ready for the next launch (stream order)
   }
 }
 
@@ -505,12 +509,23 @@ __global__ void k_colsum_head(const float* __restrict__ a, const float* __restri
   const int b0 = c * COLSUM_ROWS, b1 = min(B, b0 + COLSUM_ROWS);
   float acc = 0.f;
   if (n < NT) {
-    for (int b = b0 + threadIdx.y; b < b1; b += 8) {
-      float x;
-      if (n < W) x = __fmul_rn(delta[b], a[(size_t)b * W + n]);
-      else if (n < W + W2) x = dz[(size_t)b * W2 + (n - W)];
-      else x = delta[b];
-      acc = __fadd_rn(acc, x);
+    // the column's source, then 4 independent loads in flight per step
+    const float* src = n < W ? a + n : (n < W + W2 ? dz + (n - W) : delta);
+    const int ld = n < W ? W : (n < W + W2 ? W2 : 1);
+    const bool wt = n < W;
+    int b = b0 + threadIdx.y;
+    for (; b + 24 < b1; b += 32) {
+      float x0 = src[(size_t)b * ld], x1 = src[(size_t)(b + 8) * ld];
+      float x2 = src[(size_t)(b + 16) * ld], x3 = src[(size_t)(b + 24) * ld];
+      if (wt) {
+        x0 = __fmul_rn(delta[b], x0), x1 = __fmul_rn(delta[b + 8], x1);
+        x2 = __fmul_rn(delta[b + 16], x2), x3 = __fmul_rn(delta[b + 24], x3);
+      }
+      acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, x0), x1), x2), x3);
+    }
+    for (; b < b1; b += 8) {
+      const float x = src[(size_t)b * ld];
+      acc = __fadd_rn(acc, wt ? __fmul_rn(delta[b], x) : x);
     }
   }
   red[threadIdx.y][threadIdx.x] = acc;
@@ -593,10 +608,14 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
   }
   const unsigned hb = grid_cap(((uint64_t)B * 32 + 255) / 256);
   double* lossp = ws.lossp.get<double>(hb);
+  if (!ws.hdone.p) {
+    ws.hdone.get<unsigned>(1);
+    KP_CUDA(cudaMemsetAsync(ws.hdone.p, 0, 4, s));
+  }
   k_head_bwd<<<hb, 256, 0, s>>>(layer_in(L - 1), B, W, d_x + m.w_off[L - 1],
                                  static_cast<const float*>(ws.logits.p), d_preds, d_labels,
-                                 (float)B, delta, dprev, mode, m.activation, d_coeff, S, e, lossp); ::kp::count_launch();
-  k_loss_finalize<<<1, 32, 0, s>>>(lossp, hb, B, d_loss_sum); ::kp::count_launch();
+                                 (float)B, delta, dprev, mode, m.activation, d_coeff, S, e, lossp,
+                                 static_cast<unsigned*>(ws.hdone.p), d_loss_sum, (int)B); ::kp::count_launch();
   // head weight + bias gradients, and (with hidden layers) the last hidden
   // layer's bias gradient (the column sums of dprev = its dZ): one pass
   const bool fused_bias = L >= 2;
@@ -626,13 +645,17 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
         __half* dzl = reinterpret_cast<__half*>(ws.dzl.get<uint16_t>((size_t)B * N));
         int* dze = ws.dze.get<int>(B);
         split_rows_h(dZ, B, N, N, dzh, dzl, dze, s);
-        float* wt = ws.wt.get<float>((size_t)N * K);
-        dim3 g(ceil_div(K, 32), ceil_div(N, 32));
-        k_transpose<<<g, dim3(32, 8), 0, s>>>(d_x + m.w_off[l], N, K, wt); ::kp::count_launch();
         __half* th = reinterpret_cast<__half*>(ws.thi.get<uint16_t>((size_t)N * K));
         __half* tl = reinterpret_cast<__half*>(ws.tlo.get<uint16_t>((size_t)N * K));
         int* te = ws.texp.get<int>(K);
-        split_h(wt, K, N, N, th, tl, te, s);
+        if (N <= 256 && N % 2 == 0) {
+          split_t_h(d_x + m.w_off[l], N, K, th, tl, te, s);  // transpose + split in one pass
+        } else {
+          float* wt = ws.wt.get<float>((size_t)N * K);
+          dim3 g(ceil_div(K, 32), ceil_div(N, 32));
+          k_transpose<<<g, dim3(32, 8), 0, s>>>(d_x + m.w_off[l], N, K, wt); ::kp::count_launch();
+          split_h(wt, K, N, N, th, tl, te, s);
+        }
         EpiArgs ep{d_coeff ? kCoeff : kStore, 0, nullptr, nullptr, 0, d_coeff, S, e};
         h3_gemm(H3Operand{dzh, dzl, dze, N}, false, H3Operand{th, tl, te, N}, false, B, K, N, d_dinput, K, ep,
                 false, nullptr, s);
