@@ -161,7 +161,8 @@ int kp_compute_auc(const float* d_scores, const int32_t* d_labels, uint32_t n, d
  * 2 = tcgen05 3xTF32 only (KP_ERR_CONFIG if unsupported), 3 = tcgen05 fp16
  * operands with per-row power-of-two scales (3xFP16, the first-layer path),
  * 4 = 3xFP16 on operands pre-split into fp16 planes (the planes-mode first
- * layer, kp_gemm_h3.cu), 5 = the same with the deterministic stream-K split. */
+ * layer, kp_gemm_h3.cu), 5 = the same with the deterministic stream-K split,
+ * 6 = whole tiles for the full waves and stream-K for the last partial wave. */
 int kp_gemm_nt(const float* d_A, int lda, const float* d_B, int ldb, float* d_C, int ldc, int M,
                int N, int K, int engine, kp_stream s);
 /* C[M][N] = A[K][M]^T . B[K][N] (the weight gradient dW = dZ^T X of

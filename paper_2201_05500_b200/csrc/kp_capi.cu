@@ -148,6 +148,14 @@ struct kp_trainer {
   // planes mode: the pooling kernel writes the first layer's input as fp16
   // hi/lo planes (in the `pooled` buffer, same bytes) + an exponent per instance
   bool planes = false;
+  // this step's first layer gathers its rows (one feature per slot, planes;
+  // KP_FUSED_POOL=1 at trainer creation; else the pooling pass writes the planes)
+  bool fused_pool = false;
+  bool ga_on = false;
+  const float* ga_src = nullptr;
+  uint64_t ga_nrows = 0;
+  const uint32_t* ga_rowocc = nullptr;
+  DevBuf umax;
   DevBuf inst_exp;
   const __half* plane_hi(size_t nb) const { return static_cast<const __half*>(pooled.p); }
   const __half* plane_lo(size_t nb) const { return static_cast<const __half*>(pooled.p) + nb * e; }
@@ -732,7 +740,19 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   compose(pr.idx, tr->dd.d_inverse, sv.n_occ, rowocc, s);
   float* pooled = tr->pooled.get<float>((size_t)std::max<uint32_t>(nb, 1) * tr->e);
   float* invc = tr->inv_count.get<float>(std::max<uint32_t>(nb, 1));
-  if (tr->planes) {
+  // one feature per slot, KP_FUSED_POOL=1: the first layer's forward gathers
+  // the rows itself (kp_gemm_h3.cu, TMA gather4) and writes the planes; only
+  // the instance exponents here
+  tr->ga_on = tr->fused_pool && tr->planes && ident_bags && tr->e % 32 == 0 && sv.n_occ > 0;
+  if (tr->ga_on) {
+    int* iexp = tr->inst_exp.get<int>(std::max<uint32_t>(sv.n_inst, 1));
+    float* umax = tr->umax.get<float>(std::max<uint32_t>(U, 1));
+    inst_exps_ident(pr.src, pr.idx, U, tr->e, tr->dd.d_inverse, sv.n_inst, tr->S, umax, iexp, invc,
+                    tr->cfg.pooling == 1, s);
+    tr->ga_src = pr.src;
+    tr->ga_nrows = tr->world == 1 ? tr->tab.t->capacity : std::max<uint32_t>(U, 1);
+    tr->ga_rowocc = rowocc;
+  } else if (tr->planes) {
     // the first layer's input as fp16 planes (hi at pooled, lo behind it)
     __half* hi = reinterpret_cast<__half*>(pooled);
     int* iexp = tr->inst_exp.get<int>(std::max<uint32_t>(sv.n_inst, 1));
@@ -911,6 +931,13 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
       tr->mlp.in_hi = tr->plane_hi(nbags) + (size_t)lo * in_w;
       tr->mlp.in_lo = tr->plane_lo(nbags) + (size_t)lo * in_w;
       tr->mlp.in_exp = static_cast<const int*>(tr->inst_exp.p) + lo;
+      if (tr->ga_on) {
+        tr->mlp.ga_src = tr->ga_src;
+        tr->mlp.ga_nrows = tr->ga_nrows;
+        tr->mlp.ga_rowocc = tr->ga_rowocc + (size_t)lo * tr->S;
+        tr->mlp.ga_S = tr->S;
+        tr->mlp.ga_e = tr->e;
+      }
     }
     mlp_forward(tr->shape, tr->x + l * D, pooled + (size_t)lo * in_w, Bw, preds + lo, tr->mlp, s);
     tr->mlp.in_rowmax = nullptr;
@@ -920,6 +947,8 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
                  d_loss_slot, tr->mlp, s, (overlap && l + 1 == tr->W) ? &hook : nullptr);
     tr->mlp.in_hi = tr->mlp.in_lo = nullptr;
     tr->mlp.in_exp = nullptr;
+    tr->mlp.ga_src = nullptr;
+    tr->mlp.ga_rowocc = nullptr;
   }
   tc_reserve_sms(0);
   if (fused_preds)
@@ -996,12 +1025,21 @@ void predict_pass(kp_trainer* tr, const StepView& sv, float* d_preds_out) {
     tr->mlp.in_hi = tr->plane_hi(nbags);
     tr->mlp.in_lo = tr->plane_lo(nbags);
     tr->mlp.in_exp = static_cast<const int*>(tr->inst_exp.p);
+    if (tr->ga_on) {
+      tr->mlp.ga_src = tr->ga_src;
+      tr->mlp.ga_nrows = tr->ga_nrows;
+      tr->mlp.ga_rowocc = tr->ga_rowocc;
+      tr->mlp.ga_S = tr->S;
+      tr->mlp.ga_e = tr->e;
+    }
   }
   mlp_forward(tr->shape, xb, static_cast<const float*>(tr->pooled.p), sv.n_inst, d_preds_out,
               tr->mlp, tr->s);
   tr->mlp.in_rowmax = nullptr;
   tr->mlp.in_hi = tr->mlp.in_lo = nullptr;
   tr->mlp.in_exp = nullptr;
+  tr->mlp.ga_src = nullptr;
+  tr->mlp.ga_rowocc = nullptr;
   tr->mark(3);
 }
 
@@ -1559,7 +1597,7 @@ int kp_gemm_nt(const float* d_A, int lda, const float* d_B, int ldb, float* d_C,
              "gemm_nt: pre-split fp16 path needs contiguous rows and K % 8 == 0");
     if (engine == 1 || !tc_ok) {
       simt_gemm_nt(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, st(s));
-    } else if (engine == 4 || engine == 5) {
+    } else if (engine >= 4 && engine <= 6) {
       // 3xFP16 on pre-split planes (kp_gemm_h3.cu): split both operands per
       // row, then the all-TMA GEMM; engine 5 runs it stream-K over K
       struct PWs {
@@ -1576,7 +1614,7 @@ int kp_gemm_nt(const float* d_A, int lda, const float* d_B, int ldb, float* d_C,
       split_rows_h(d_B, N, K, K, bh, bl, be, st(s));
       GemmEpi ep{0, 0, nullptr, nullptr, 0, nullptr, 1, 1};
       h3_gemm(H3Operand{ah, al, ae, K}, false, H3Operand{bh, bl, be, K}, false, M, N, K, d_C, ldc, ep,
-              engine == 5, engine == 5 ? w.ws.get<float>(h3_splitk_ws_floats(M, N)) : nullptr, st(s));
+              engine - 4, engine > 4 ? w.ws.get<float>(h3_splitk_ws_floats(M, N)) : nullptr, st(s));
       KP_CUDA(cudaStreamSynchronize(st(s)));
     } else if (engine == 3) {
       // fp16-operand path (per-row scaled 3xFP16), as used for the first MLP layer
@@ -1612,7 +1650,7 @@ int kp_gemm_tn(const float* d_A, int lda, const float* d_B, int ldb, float* d_C,
              "gemm_tn: pre-split fp16 path needs contiguous rows and M, N % 8 == 0");
     if (engine == 1 || !tc_ok) {
       simt_gemm_tn(M, N, K, d_A, lda, d_B, ldb, d_C, ldc, st(s));
-    } else if (engine == 4 || engine == 5) {
+    } else if (engine >= 4 && engine <= 6) {
       // both operands MN-major ([K][M], [K][N]): planes with one exponent per
       // column, the all-TMA 3xFP16 GEMM (engine 5: stream-K over K)
       struct PWs {
@@ -1630,7 +1668,7 @@ int kp_gemm_tn(const float* d_A, int lda, const float* d_B, int ldb, float* d_C,
       split_cols_scaled_h(d_B, K, N, nullptr, cm, bh, bl, be, st(s));
       GemmEpi ep{0, 0, nullptr, nullptr, 0, nullptr, 1, 1};
       h3_gemm(H3Operand{ah, al, ae, M}, true, H3Operand{bh, bl, be, N}, true, M, N, K, d_C, ldc, ep,
-              engine == 5, engine == 5 ? w.ws.get<float>(h3_splitk_ws_floats(M, N)) : nullptr, st(s));
+              engine - 4, engine > 4 ? w.ws.get<float>(h3_splitk_ws_floats(M, N)) : nullptr, st(s));
       KP_CUDA(cudaStreamSynchronize(st(s)));
     } else {
       const int sp = tc_splits(M, N, K);
@@ -1734,8 +1772,15 @@ int kp_trainer_create(const kp_trainer_config* cfg, kp_comm* comm, int device, k
     }
     tr->D = m.D;
     // layer 1 on pre-split fp16 planes written by the pooling kernel
+    {
+      // opt-in (KP_FUSED_POOL=1): measured slower, see DESIGN.md §4.3
+      const char* e = getenv("KP_FUSED_POOL");
+      tr->fused_pool = e && e[0] == '1';
+    }
+    // (the backward's plane operands [B][hidden1] and W1^T [S*e][hidden1]
+    // need 16-byte rows: hidden1 % 8 == 0)
     tr->planes = c.n_hidden >= 1 && tc_enabled() && tc_h_enabled() && h3_enabled() &&
-                 pool_planes_supported(c.n_slots, c.embedding_dim);
+                 pool_planes_supported(c.n_slots, c.embedding_dim) && m.widths[1] % 8 == 0;
     const uint64_t D = m.D, W = tr->W;
     std::vector<double> x0(D);
     init_dense_host(c.seed, D, x0.data());

@@ -430,6 +430,48 @@ __global__ void __launch_bounds__(NT, 4) k_pool_planes_ident(uint32_t n_inst, ui
   }
 }
 
+// max |x| of each unique key's source row (half a warp per row of e <= 64
+// floats as float4s; kNoRow -> 0)
+__global__ void k_unique_maxabs(const float* __restrict__ src, const uint32_t* __restrict__ idx, uint32_t U,
+                                uint32_t e, float* __restrict__ umax) {
+  const uint32_t lpr = e >> 2;  // float4 lanes per row (<= 16)
+  const uint32_t lane = threadIdx.x & 31, sub = lane / lpr, per = 32 / lpr;
+  const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const unsigned gmask = lpr == 32 ? 0xffffffffu : (((1u << lpr) - 1u) << (sub * lpr));
+  for (uint64_t u0 = (uint64_t)w0 * per; u0 < U; u0 += (uint64_t)nw * per) {
+    const uint64_t u = u0 + sub;
+    float mx = 0.f;
+    if (u < U && sub < per) {
+      const uint32_t r = __ldg(idx + u);
+      if (r != kNoRow) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(src + (uint64_t)r * e) + lane % lpr);
+        mx = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+      }
+    }
+    for (uint32_t o = lpr / 2; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, o, lpr));
+    if (u < U && sub < per && lane % lpr == 0) umax[u] = mx;
+  }
+}
+
+// per instance: row_exp(max over its S slots of umax[inverse[i*S + s]]) --
+// the exponent k_pool_planes_ident computes from the pooled row itself
+__global__ void k_inst_exp(const uint32_t* __restrict__ inverse, const float* __restrict__ umax,
+                           uint32_t n_inst, uint32_t S, int* __restrict__ inst_exp, float* __restrict__ inv_count,
+                           int mean) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = w0; i < n_inst; i += nw) {
+    float mx = 0.f;
+    for (uint32_t s = lane; s < S; s += 32) {
+      mx = fmaxf(mx, __ldg(umax + __ldg(inverse + i * S + s)));
+      if (mean) inv_count[i * S + s] = 1.f;  // one feature per bag
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) inst_exp[i] = tc::row_exp(mx);
+  }
+}
+
 __global__ void k_compose(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ inverse,
                           uint32_t n, uint32_t* __restrict__ out) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -926,6 +968,21 @@ void pool_planes(const uint32_t* d_bag_offs, uint32_t n_inst, uint32_t S, const 
     k_pool_planes<256, 16><<<grid, 256, 0, s>>>(d_bag_offs, n_inst, S, d_row_of_occ, d_src, e, mean, d_hi, d_lo,
                                                  d_inst_exp, d_inv_count);
   }
+  ::kp::count_launch();
+}
+
+void inst_exps_ident(const float* d_src, const uint32_t* d_idx, uint32_t U, uint32_t e,
+                     const uint32_t* d_inverse, uint32_t n_inst, uint32_t S, float* d_umax_ws,
+                     int* d_inst_exp, float* d_inv_count, bool mean, cudaStream_t s) {
+  KP_CHECK(e % 4 == 0 && e <= 128, kErrConfig, "inst_exps_ident: e must be a multiple of 4, <= 128");
+  if (n_inst == 0) return;
+  if (U) {
+    const uint64_t per = 32 / (e / 4);
+    k_unique_maxabs<<<grid_cap(((U + per - 1) / per * 32 + 255) / 256), 256, 0, s>>>(d_src, d_idx, U, e, d_umax_ws);
+    ::kp::count_launch();
+  }
+  k_inst_exp<<<grid_cap(((uint64_t)n_inst * 32 + 255) / 256), 256, 0, s>>>(d_inverse, d_umax_ws, n_inst, S,
+                                                                           d_inst_exp, d_inv_count, mean ? 1 : 0);
   ::kp::count_launch();
 }
 

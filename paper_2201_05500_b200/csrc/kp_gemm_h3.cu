@@ -35,6 +35,7 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -63,14 +64,17 @@ constexpr uint32_t H3_STAGE = 4 * H3_PLANE;       // A hi, A lo, B hi, B lo
 constexpr uint32_t H3_EPI = 16 * H3_EPIB * 32 * H3_EB * 4;  // per epilogue warp H3_EPIB 32 x H3_EB fp32 store tiles
 // register split (setmaxnreg, per warpgroup): the epilogue holds 64 fp32
 // running sums per thread; the TMA / MMA warps need few
-constexpr int H3_REG_LO = 40, H3_REG_HI = 104;  // 128*40 + 512*104 <= 640*96 (the CTA pool)
+constexpr int H3_REG_LO = 64, H3_REG_HI = 104;  // 128*64 + 512*104 <= 640*96 (the CTA pool)
 constexpr uint32_t H3_COLP = 16 * 2 * 64 * 4;  // per epilogue warp: 64 column scales + 64 biases
 constexpr uint32_t H3_SMEM = H3_NS * H3_STAGE + H3_EPI + H3_COLP + 1024 + 256;
 // Tile width BN: 256 (2 TMEM accumulators) or 128 (4 accumulators: the MMA
 // may run 3 tiles ahead of the epilogue -- for short-K, wide-N products like
 // dX, K = 256, whose per-tile epilogue is as long as its MMAs). Each CTA holds
 // BN/2 rows of B.
-template <int BN>
+// GA (gathered A): A's rows are fetched as fp32 by TMA gather4 from a row
+// table (one feature per slot: A[m][slot*e + j] = src[rowocc[m*S + slot]][j]),
+// into NG staging slots, and split into the A planes on chip by warps 2-3.
+template <int BN, bool GA = false>
 struct H3Cfg {
   static constexpr int NBUF = 512 / BN;
   static constexpr int BROWS = BN / 2;
@@ -78,9 +82,15 @@ struct H3Cfg {
   static constexpr uint32_t STAGE = 2 * H3_PLANE + 2 * B_PLANE;
   static constexpr int NS = BN == 256 ? 4 : 6;
   static constexpr int CW = BN / 4;  // columns per epilogue warp
-  static constexpr uint32_t SMEM = NS * STAGE + H3_EPI + H3_COLP + 1024 + 256;
+  static constexpr int EPIB = GA ? 1 : H3_EPIB;  // (GA: one store box per warp, room for the staging)
+  static constexpr uint32_t EPI = 16 * EPIB * 32 * H3_EB * 4;
+  static constexpr int NG = GA ? 2 : 0;
+  static constexpr uint32_t GSLOT = H3_BM * H3_BK * 4;  // 128 rows x 32 fp32
+  static constexpr uint32_t GEXP = GA ? H3_BM * 4 : 0;  // the tile rows' exponents
+  static constexpr uint32_t SMEM = NS * STAGE + EPI + H3_COLP + NG * GSLOT + GEXP + 1024 + 256;
 };
-static_assert(H3Cfg<128>::SMEM <= 232448 && H3Cfg<256>::SMEM <= 232448, "h3 smem");
+static_assert(H3Cfg<128>::SMEM <= 232448 && H3Cfg<256>::SMEM <= 232448 && H3Cfg<256, true>::SMEM <= 232448,
+              "h3 smem");
 // stream-K virtual units (the partition depends only on the problem shape,
 // not on the grid): 148, or fewer so that each owns >= 8 k-blocks
 constexpr int H3_VUNITS = 148;
@@ -94,63 +104,98 @@ struct H3Args {
   int nblocks_m, nblocks_n, nk;  // tiles and k-blocks
   int splitk;                    // stream-K over vunits virtual units
   int vunits;
+  int tiles_dp;                  // stream-K kernels: whole tiles [0, tiles_dp) first, the rest stream-K
   const int* ea;                 // per-row exponents of A (nullable = 0)
   const int* eb;                 // per-row exponents of B (nullable = 0)
   int keep_a, keep_b;            // L2 policy per operand: 1 evict_last (re-read), 0 evict_first
-  int dbg;                       // timing experiments only (KP_H3_DBG): 1 no stores, 2 no drain
+  int dbg;                       // timing experiments only (KP_H3_DBG): 1 no stores, 2 no drain,
+                                 // 3 no A conversion, 4 no A gathers (GA)
   int mode;                      // 0 store, 1 act(x + bias[n]), 3 x * coeff[m*S + n/e]
   int act;
   const float* bias;
   const float* coeff;
   uint32_t S, e;
+  // GA: row of (m, slot) in the gather source, S slots of gkps k-blocks;
+  // gstore: also store the A planes (for a later GEMM over the same input)
+  const uint32_t* grow;
+  uint32_t gS, gkps;
+  int gstore;
 };
 
 // the k-block range of virtual unit v over T = tiles * nk iterations
 __device__ __forceinline__ int64_t vstart(int64_t v, int64_t T, int V) { return v * T / V; }
 
 // Iterates the (tile, kb0, kb1) segments of one physical unit: data-parallel
-// (whole tiles w = unit, unit+units, ...) or stream-K (the virtual units
-// v = unit, unit+units, ... each own [vstart(v), vstart(v+1)) of the
-// flattened tile x k-block space; segment id = tile + v is unique).
+// (whole tiles w = unit, unit+units, ...) or stream-K: first the whole tiles
+// [0, tiles_dp) as in data-parallel, then the virtual units v = unit,
+// unit+units, ... each owning [vstart(v), vstart(v+1)) of the flattened
+// (tail tile x k-block) space; a stream-K segment's partial-tile id is
+// (tile - tiles_dp) + v (unique). The split depends only on the shape.
 template <bool SK>
 struct SegIter {
-  int tiles, nk, units, V;
-  int v;  // current virtual unit (stream-K) / tile (DP)
+  int tiles, nk, units, V, tdp, u0;
+  int v;  // current whole tile, then (stream-K) virtual unit
+  bool whole;
   int64_t T, t, tend;
   __device__ SegIter(const H3Args& a, int unit, int units_)
       : tiles(a.nblocks_m * a.nblocks_n), nk(a.nk), units(units_), V(a.vunits) {
     v = unit;
+    u0 = unit;
     if constexpr (SK) {
-      T = (int64_t)tiles * nk;
+      tdp = a.tiles_dp;
+      whole = v < tdp;
+      T = (int64_t)(tiles - tdp) * nk;
       t = tend = 0;
-      if (v < V) {
-        t = vstart(v, T, V);
-        tend = vstart(v + 1, T, V);
-      }
+      if (!whole) start_sk(unit);
     }
   }
-  // next segment: tile index, [kb0, kb1), segment id; false when done
-  __device__ bool next(int& tile, int& kb0, int& kb1, int& sid) {
+  __device__ void start_sk(int u) {
+    v = u;
+    t = tend = 0;
+    if (v < V) {
+      t = vstart(v, T, V);
+      tend = vstart(v + 1, T, V);
+    }
+  }
+  // next segment: tile index, [kb0, kb1), partial-tile id (stream-K part),
+  // partial; false when done
+  __device__ bool next(int& tile, int& kb0, int& kb1, int& sid, bool& partial) {
     if constexpr (!SK) {
       if (v >= tiles) return false;
       tile = v;
       kb0 = 0;
       kb1 = nk;
       sid = v;
+      partial = false;
       v += units;
       return true;
     } else {
+      if (whole) {
+        tile = v;
+        kb0 = 0;
+        kb1 = nk;
+        sid = v;
+        partial = false;
+        v += units;
+        if (v >= tdp) {
+          whole = false;
+          start_sk(u0);
+        }
+        return true;
+      }
       while (t >= tend) {
         v += units;
         if (v >= V) return false;
         t = vstart(v, T, V);
         tend = vstart(v + 1, T, V);
       }
-      tile = (int)(t / nk);
+      const int lt = (int)(t / nk);
+      tile = tdp + lt;
       kb0 = (int)(t % nk);
       const int64_t e = kb0 + (tend - t);
       kb1 = (int)(e < nk ? e : nk);
-      sid = tile + v;
+      sid = lt + v;
+      partial = true;
       t += kb1 - kb0;
       return true;
     }
@@ -181,26 +226,34 @@ __device__ __forceinline__ uint64_t plane_desc(uint32_t base, int kk) {
   return MN ? sdesc_mn128(base + (uint32_t)kk * 2048u, 4096u) : sdesc_k64(base + (uint32_t)kk * 32u);
 }
 
-template <bool AMN, bool BMN, bool SK, int BN>
+template <bool AMN, bool BMN, bool SK, int BN, bool GA>
 __global__ void __launch_bounds__(H3_WARPS * 32, 1)
     k_h3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
          const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
-         const __grid_constant__ CUtensorMap tmC, H3Args a) {
-  using Cfg = H3Cfg<BN>;
-  constexpr int NS = Cfg::NS, NBUF = Cfg::NBUF, CW = Cfg::CW;
+         const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmP,
+         const __grid_constant__ CUtensorMap tmG, H3Args a) {
+  static_assert(!GA || (!AMN && BN == 256), "gathered A: K-major, 256-wide tiles");
+  using Cfg = H3Cfg<BN, GA>;
+  // (NG: the staging ring's modulus, 1 without staging)
+  constexpr int NS = Cfg::NS, NBUF = Cfg::NBUF, CW = Cfg::CW, EPIB = Cfg::EPIB, NG = Cfg::NG > 0 ? Cfg::NG : 1;
   constexpr uint32_t STAGE = Cfg::STAGE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stages = smem;
   uint8_t* epi = stages + NS * STAGE;
-  float* colp = reinterpret_cast<float*>(epi + H3_EPI);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(colp) + H3_COLP);
+  float* colp = reinterpret_cast<float*>(epi + Cfg::EPI);
+  uint8_t* gstage = reinterpret_cast<uint8_t*>(colp) + H3_COLP;  // GA: fp32 staging slots
+  int* gexp = reinterpret_cast<int*>(gstage + Cfg::NG * Cfg::GSLOT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(gexp) + Cfg::GEXP);
   uint64_t* full = bars;              // TMA -> MMA (local)
   uint64_t* conv = bars + NS;         // peer's TMA landed -> leader's MMA (1 arrival)
   uint64_t* empty = bars + 2 * NS;    // MMA done with stage -> producers (both CTAs)
   uint64_t* tfull = bars + 3 * NS;    // chunk accumulated -> drains (both CTAs)
   uint64_t* tempty = tfull + NBUF;    // drained -> MMA (leader; 2 arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NBUF);
+  uint64_t* cvt = tempty + NBUF;      // GA: A planes written -> MMA / relay (local)
+  uint64_t* gfull = cvt + NS;         // GA: gathered rows landed -> converters
+  uint64_t* gempty = gfull + Cfg::NG; // GA: staging slot read -> producer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gempty + Cfg::NG);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -217,6 +270,13 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 2);
     }
+    if constexpr (GA) {
+      for (int s = 0; s < NS; ++s) mbar_init(&cvt[s], 1);
+      for (int j = 0; j < NG; ++j) {
+        mbar_init(&gfull[j], 1);
+        mbar_init(&gempty[j], 1);
+      }
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
@@ -228,7 +288,113 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
 
   if (warp < 4) {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(H3_REG_LO));
-  if (warp == 0) {
+  if (GA && warp == 0) {
+    // ---- gathered-A producer: lane l fetches A rows 4l..4l+3 (fp32, 32 k of
+    // their slot's source row) with one gather4 per k-block; lane 0 also the
+    // B planes. The next slot's row indices are loaded one slot ahead.
+    if (lane == 0) {
+      prefetch_map(&tmBh);
+      prefetch_map(&tmBl);
+      prefetch_map(&tmG);
+    }
+    const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
+    const uint64_t pb = a.keep_b ? pol_keep : pol_stream;
+    SegIter<SK> it(a, unit, units);
+    int tile, kb0, kb1, sid, g = 0;
+    bool partial;
+    while (it.next(tile, kb0, kb1, sid, partial)) {
+      int mb, nb;
+      tile_mn(a, tile, mb, nb);
+      const int m0 = mb * 2 * H3_BM + (int)rank * H3_BM;
+      const int n0 = nb * BN + (int)rank * Cfg::BROWS;
+      auto rows_of = [&](int slot, uint32_t (&r)[4]) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int m = m0 + 4 * lane + t;
+          r[t] = (m < a.M && slot < (int)a.gS) ? __ldg(a.grow + (size_t)m * a.gS + slot) : 0u;
+        }
+      };
+      int slot = kb0 / (int)a.gkps;
+      uint32_t ri[4], nx[4];
+      rows_of(slot, ri);
+      rows_of(slot + 1, nx);
+      for (int kb = kb0; kb < kb1; ++kb, ++g) {
+        const int s = g % NS, j = g % NG;
+        const int sl = kb / (int)a.gkps;
+        if (sl != slot) {  // (slots advance one at a time inside a segment)
+          slot = sl;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) ri[t] = nx[t];
+          rows_of(slot + 1, nx);
+        }
+        if (lane == 0) {
+          if (g >= NS) mbar_wait(&empty[s], ((g / NS) & 1) ^ 1);
+          mbar_expect_tx(&full[s], 2 * Cfg::B_PLANE);
+          uint8_t* st = sAh(s);
+          load_plane<BMN, Cfg::BROWS>(st + 2 * H3_PLANE, &tmBh, &full[s], kb * H3_BK, n0, pb);
+          load_plane<BMN, Cfg::BROWS>(st + 2 * H3_PLANE + Cfg::B_PLANE, &tmBl, &full[s], kb * H3_BK, n0, pb);
+          if (g >= NG) mbar_wait(&gempty[j], ((g / NG) & 1) ^ 1);
+          if (a.dbg == 4) mbar_arrive(&gfull[j]);  // timing experiment: no gathers
+          else mbar_expect_tx(&gfull[j], Cfg::GSLOT);
+        }
+        __syncwarp();
+        if (a.dbg != 4)
+          tma_gather4(gstage + j * Cfg::GSLOT + lane * (4 * H3_BK * 4), &tmG, &gfull[j],
+                      (kb % (int)a.gkps) * H3_BK, ri);
+      }
+    }
+  } else if (GA && (warp == 2 || warp == 3)) {
+    // ---- converters: staging fp32 rows -> x * 2^e(row) -> hi/lo fp16 in the
+    // SW64 K-major layout the A planes' TMA would have produced; optionally
+    // stored to the planes in HBM (TMA) for a later GEMM
+    const int ct = threadIdx.x - 64, w2 = warp - 2;
+    SegIter<SK> it(a, unit, units);
+    int tile, kb0, kb1, sid, g = 0;
+    bool partial;
+    while (it.next(tile, kb0, kb1, sid, partial)) {
+      int mb, nb;
+      tile_mn(a, tile, mb, nb);
+      const int m0 = mb * 2 * H3_BM + (int)rank * H3_BM;
+      named_sync(2, 64);  // the previous segment's conversions are done with gexp
+      for (int r = ct; r < H3_BM; r += 64) gexp[r] = (a.ea && m0 + r < a.M) ? __ldg(a.ea + m0 + r) : 0;
+      named_sync(2, 64);
+      for (int kb = kb0; kb < kb1; ++kb, ++g) {
+        const int s = g % NS, j = g % NG;
+        mbar_wait(&gfull[j], (g / NG) & 1);
+        if (g >= NS) mbar_wait(&empty[s], ((g / NS) & 1) ^ 1);  // the MMAs are done with the A slots
+        if (ct == 0 && g >= NS && a.gstore)  // ... and so is this slot's previous plane store
+          asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(2 * NS - 2) : "memory");
+        named_sync(2, 64);
+        const uint8_t* gs = gstage + j * Cfg::GSLOT;
+        uint8_t* ah = sAh(s);
+#pragma unroll 4
+        for (int i = 0; i < (a.dbg == 3 ? 0 : 16); ++i) {  // (dbg 3: timing experiment, no conversion)
+          // 8 lanes per row (one 128-byte row per quarter warp: conflict-free)
+          const int r = w2 * 64 + i * 4 + (lane >> 3), c = lane & 7;
+          const float4 v = *reinterpret_cast<const float4*>(gs + r * (H3_BK * 4) + c * 16);
+          const float sc = pow2f(gexp[r]);
+          uint32_t h0, l0, h1, l1;
+          split_h2(__fmul_rn(v.x, sc), __fmul_rn(v.y, sc), h0, l0);
+          split_h2(__fmul_rn(v.z, sc), __fmul_rn(v.w, sc), h1, l1);
+          // SW64: row r's 16-byte chunk q at q ^ ((r >> 1) & 3); halves 4c..4c+3 = 8 bytes
+          const uint32_t off = (uint32_t)(r * 64) + ((uint32_t)((c >> 1) ^ ((r >> 1) & 3)) << 4) + ((c & 1) << 3);
+          st_shared_v2(smem_u32(ah) + off, h0, h1);
+          st_shared_v2(smem_u32(ah + H3_PLANE) + off, l0, l1);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        named_sync(2, 64);
+        if (ct == 0) {
+          mbar_arrive(&gempty[j]);
+          if (a.gstore) {
+            tma_store_2d(&tmAh, ah, kb * H3_BK, m0);
+            tma_store_2d(&tmAl, ah + H3_PLANE, kb * H3_BK, m0);
+          }
+          mbar_arrive(&cvt[s]);
+        }
+      }
+    }
+    if (ct == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else if (warp == 0) {
     // ---- TMA producer: this CTA's 128 A rows and 128 B rows per k-block
     if (lane == 0) {
       prefetch_map(&tmAh);
@@ -240,7 +406,8 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       const uint64_t pa = a.keep_a ? pol_keep : pol_stream, pb = a.keep_b ? pol_keep : pol_stream;
       SegIter<SK> it(a, unit, units);
       int tile, kb0, kb1, sid, g = 0;
-      while (it.next(tile, kb0, kb1, sid)) {
+      bool partial;
+      while (it.next(tile, kb0, kb1, sid, partial)) {
         int mb, nb;
         tile_mn(a, tile, mb, nb);
         const int m0 = mb * 2 * H3_BM + (int)rank * H3_BM;
@@ -263,12 +430,14 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       constexpr uint32_t idesc = idesc_f16(AMN, BMN, 2 * H3_BM, BN);
       SegIter<SK> it(a, unit, units);
       int tile, kb0, kb1, sid, g = 0, c = 0;
-      while (it.next(tile, kb0, kb1, sid)) {
+      bool partial;
+      while (it.next(tile, kb0, kb1, sid, partial)) {
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % NS;
           const int kin = (kb - kb0) % H3_CH, buf = c % NBUF;
           if (kin == 0 && c >= NBUF) mbar_wait(&tempty[buf], ((c / NBUF) - 1) & 1);
           mbar_wait(&full[s], (g / NS) & 1);
+          if constexpr (GA) mbar_wait(&cvt[s], (g / NS) & 1);
           mbar_wait(&conv[s], (g / NS) & 1);
           fence_after();
           const uint32_t d = tmem + (uint32_t)(buf * BN);
@@ -293,10 +462,12 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       // ---- peer CTA: relay "my TMA landed" to the leader's MMA issuer
       SegIter<SK> it(a, unit, units);
       int tile, kb0, kb1, sid, g = 0;
-      while (it.next(tile, kb0, kb1, sid))
+      bool partial;
+      while (it.next(tile, kb0, kb1, sid, partial))
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = g % NS;
           mbar_wait(&full[s], (g / NS) & 1);
+          if constexpr (GA) mbar_wait(&cvt[s], (g / NS) & 1);
           mbar_arrive_leader(&conv[s]);
         }
     }
@@ -306,11 +477,12 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
     // ---- drain + epilogue (16 warps): TMEM lane quarter q, columns [cq*64, +64)
     const int q = warp & 3, cq = (warp - 4) >> 2;
     const int et = threadIdx.x - 128;
-    uint8_t* dense_base = epi + (warp - 4) * (H3_EPIB * 32 * H3_EB * 4);
+    uint8_t* dense_base = epi + (warp - 4) * (EPIB * 32 * H3_EB * 4);
     uint32_t tma_seq = 0;
     SegIter<SK> it(a, unit, units);
     int tile, kb0, kb1, sid, c = 0;
-    while (it.next(tile, kb0, kb1, sid)) {
+    bool partial;
+    while (it.next(tile, kb0, kb1, sid, partial)) {
       int mb, nb;
       tile_mn(a, tile, mb, nb);
       const int mrow0 = mb * 2 * H3_BM + (int)rank * H3_BM + q * 32;  // this warp's 32 rows
@@ -326,6 +498,7 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       }
       const int m = mrow0 + lane;
       const float sa = (a.ea && m < a.M) ? pow2f(-__ldg(a.ea + m)) : 1.f;
+      const int mode = partial ? 0 : a.mode;  // partial tiles: plain scaled sums (the fix-up applies the op)
       float acc[CW];
 #pragma unroll
       for (int j = 0; j < CW; ++j) acc[j] = 0.f;
@@ -357,7 +530,7 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       __syncwarp();  // csb visible to the warp
 #pragma unroll
       for (int h = 0; h < CW / H3_EB; ++h, ++tma_seq) {
-        uint8_t* box = dense_base + (tma_seq % H3_EPIB) * (32 * H3_EB * 4);
+        uint8_t* box = dense_base + (tma_seq % EPIB) * (32 * H3_EB * 4);
         const uint32_t dense = smem_u32(box);
         const int c0 = H3_EB * h;
         const int n = ncol0 + c0;
@@ -365,9 +538,9 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
 #pragma unroll
         for (int j = 0; j < H3_EB; ++j) {
           v[j] = __fmul_rn(__fmul_rn(v[j], sa), csb[c0 + j]);
-          if (a.mode == 1) v[j] = act_fwd(a.act, __fadd_rn(v[j], csb[64 + c0 + j]));
+          if (mode == 1) v[j] = act_fwd(a.act, __fadd_rn(v[j], csb[64 + c0 + j]));
         }
-        if (a.mode == 3) {  // mean-pooling coefficient of the column's slot (few distinct per box)
+        if (mode == 3) {  // mean-pooling coefficient of the column's slot (few distinct per box)
           const float* cp = a.coeff + (size_t)min(m, a.M - 1) * a.S;
           int slot = -1;
           float cf = 1.f;
@@ -380,7 +553,7 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
         }
         // the store that last used this buffer has read it out of shared memory
         if (lane == 0) {
-          if (H3_EPIB == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          if (EPIB == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         }
         __syncwarp();
@@ -393,8 +566,8 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0 && a.dbg != 1) {
-          if (SK)  // partial tile of segment sid: rows sid*256 + local row
-            tma_store_2d(&tmC, box, cq * CW + c0, sid * 2 * H3_BM + (int)rank * H3_BM + q * 32);
+          if (SK && partial)  // partial tile of segment sid: rows sid*256 + local row
+            tma_store_2d(&tmP, box, cq * CW + c0, sid * 2 * H3_BM + (int)rank * H3_BM + q * 32);
           else
             tma_store_2d(&tmC, box, n, mrow0);
         }
@@ -408,12 +581,14 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
   if (warp == 1) tmem_dealloc_pair(tmem, 512);
 }
 
-// stream-K fix-up: C tile = sum of its segments' partials in k order
-__global__ void k_h3_fixup(const float* __restrict__ part, int nblocks_n, int nk, int64_t T, int V, int M,
-                           int N, float* __restrict__ C, int ldc) {
-  const int tile = blockIdx.y;
+// stream-K fix-up: C tile = op(sum of its segments' partials in k order),
+// for the stream-K tiles tdp + blockIdx.y (op: mode 0 store, 1 act(x + bias))
+__global__ void k_h3_fixup(const float* __restrict__ part, int nblocks_n, int nk, int tdp, int64_t T, int V,
+                           int M, int N, float* __restrict__ C, int ldc, int mode, int act,
+                           const float* __restrict__ bias) {
+  const int lt = blockIdx.y, tile = tdp + lt;
   const int mb = tile / nblocks_n, nb = tile % nblocks_n;
-  const int64_t t0 = (int64_t)tile * nk, t1 = t0 + nk - 1;
+  const int64_t t0 = (int64_t)lt * nk, t1 = t0 + nk - 1;
   // unit(t) = max v with vstart(v) <= t = floor(((t+1)*V - 1) / T)
   const int v0 = (int)(((t0 + 1) * V - 1) / T), v1 = (int)(((t1 + 1) * V - 1) / T);
   // the tile's contributing virtual units, once per block (some own no k-block
@@ -434,14 +609,17 @@ __global__ void k_h3_fixup(const float* __restrict__ part, int nblocks_n, int nk
     if (m >= M || n >= N) continue;
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int j = 0; j < nv; ++j) {
-      const float4 p = *reinterpret_cast<const float4*>(part + ((size_t)(tile + vlist[j]) * 2 * H3_BM + r) * H3_BN + cc);
+      const float4 p = *reinterpret_cast<const float4*>(part + ((size_t)(lt + vlist[j]) * 2 * H3_BM + r) * H3_BN + cc);
       s.x = __fadd_rn(s.x, p.x), s.y = __fadd_rn(s.y, p.y), s.z = __fadd_rn(s.z, p.z), s.w = __fadd_rn(s.w, p.w);
     }
+    float v[4] = {s.x, s.y, s.z, s.w};
+    if (mode == 1)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) v[t] = act_fwd(act, __fadd_rn(v[t], __ldg(bias + min(n + t, N - 1))));
     float* c = C + (size_t)m * ldc + n;
     if (n + 3 < N && (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) {
-      *reinterpret_cast<float4*>(c) = s;
+      *reinterpret_cast<float4*>(c) = make_float4(v[0], v[1], v[2], v[3]);
     } else {
-      const float v[4] = {s.x, s.y, s.z, s.w};
       for (int t = 0; t < 4 && n + t < N; ++t) c[t] = v[t];
     }
   }
@@ -488,29 +666,66 @@ bool map_out(CUtensorMap* m, float* p, uint64_t rows, uint64_t cols, uint64_t ld
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// gather source rows [nrows][e] fp32: boxes of 32 columns x 1 row (gather4
+// fetches four of them)
+bool map_rows(CUtensorMap* m, const float* p, uint64_t nrows, uint32_t e) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {e, nrows};
+  cuuint64_t strides[1] = {(cuuint64_t)e * 4};
+  cuuint32_t box[2] = {(cuuint32_t)H3_BK, 1};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fprintf(stderr, "map_rows: cuTensorMapEncodeTiled %d (rows %llu, e %u, p %p)\n", (int)r,
+                                 (unsigned long long)nrows, e, (const void*)p);
+  return r == CUDA_SUCCESS;
+}
+
 thread_local int g_h3_reserve = 0;
 
-template <bool AMN, bool BMN, bool SK, int BN>
+template <bool AMN, bool BMN, bool SK, int BN, bool GA = false>
 void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, float* ws,
-                 const H3Args& a0, cudaStream_t s);
+                 const H3Args& a0, cudaStream_t s, int split, const H3Gather* ga = nullptr);
 // stream-K and data-parallel variants are separate kernels (no 64-bit
 // stream-K state in the data-parallel ones); KP_H3_BN=128 selects 128-wide
 // tiles (4 accumulators in flight) for the data-parallel ones
 template <bool AMN, bool BMN>
-void launch_h3(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, bool splitk,
-               float* ws, const H3Args& a, cudaStream_t s) {
+void launch_h3(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, int splitk,
+               float* ws, const H3Args& a, cudaStream_t s, const H3Gather* ga = nullptr) {
   static const int bn_env = [] {
     const char* e = getenv("KP_H3_BN");
     return e ? atoi(e) : 0;
   }();
   // (128-wide tiles for dX measured slower: 702 vs 556 us -- opt-in only)
   const bool narrow = bn_env == 128;
-  if (splitk) launch_h3_t<AMN, BMN, true, 256>(A, B, M, N, K, C, ldc, ws, a, s);
-  else if (narrow) launch_h3_t<AMN, BMN, false, 128>(A, B, M, N, K, C, ldc, ws, a, s);
-  else launch_h3_t<AMN, BMN, false, 256>(A, B, M, N, K, C, ldc, ws, a, s);
+  static const bool hybrid = [] {
+    const char* e = getenv("KP_H3_HYBRID");
+    return !(e && e[0] == '0');
+  }();
+  if (splitk == 2) {
+    // whole tiles in full waves of the 74 pairs, the last partial wave
+    // stream-K (shape-only split); all whole: the data-parallel kernel
+    const int tiles = (int)(ceil_div(M, 2 * H3_BM) * ceil_div(N, H3_BN));
+    // (below one full wave -- short-K small batches -- the fix-up costs more
+    // than the balance gains; at configs[1] the split measured -5 us in situ)
+    if (tiles % (H3_VUNITS / 2) == 0 || tiles < H3_VUNITS / 2 || !hybrid) splitk = 0;
+  }
+  if constexpr (!AMN) {
+    if (ga) {
+      if (splitk) launch_h3_t<false, BMN, true, 256, true>(A, B, M, N, K, C, ldc, ws, a, s, splitk, ga);
+      else launch_h3_t<false, BMN, false, 256, true>(A, B, M, N, K, C, ldc, ws, a, s, 0, ga);
+      return;
+    }
+  }
+  KP_CHECK(!ga, kErrGeneric, "h3_gemm: gathered A must be K-major");
+  if (splitk) launch_h3_t<AMN, BMN, true, 256>(A, B, M, N, K, C, ldc, ws, a, s, splitk);
+  else if (narrow) launch_h3_t<AMN, BMN, false, 128>(A, B, M, N, K, C, ldc, ws, a, s, 0);
+  else launch_h3_t<AMN, BMN, false, 256>(A, B, M, N, K, C, ldc, ws, a, s, 0);
 }
 
-template <bool AMN, bool BMN, bool SK, int BN>
+template <bool AMN, bool BMN, bool SK, int BN, bool GA>
 int h3_units() {
   static int units = 0;
   if (units) return units;
@@ -521,7 +736,7 @@ int h3_units() {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(4, 1, 1);
   cfg.blockDim = dim3(H3_WARPS * 32, 1, 1);
-  cfg.dynamicSmemBytes = H3Cfg<BN>::SMEM;
+  cfg.dynamicSmemBytes = H3Cfg<BN, GA>::SMEM;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
@@ -530,17 +745,18 @@ int h3_units() {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_h3<AMN, BMN, SK, BN>, &cfg) == cudaSuccess && n > 0) units = std::min(units, n);
+  if (cudaOccupancyMaxActiveClusters(&n, k_h3<AMN, BMN, SK, BN, GA>, &cfg) == cudaSuccess && n > 0)
+    units = std::min(units, n);
   cudaGetLastError();
   return units;
 }
 
-template <bool AMN, bool BMN, bool SK, int BN>
+template <bool AMN, bool BMN, bool SK, int BN, bool GA>
 void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, float* ws,
-                 const H3Args& a0, cudaStream_t s) {
+                 const H3Args& a0, cudaStream_t s, int split, const H3Gather* ga) {
   static_assert(!SK || BN == 256, "stream-K partial tiles are 256 wide");
   constexpr bool splitk = SK;
-  CUtensorMap tah, tal, tbh, tbl, tcm;
+  CUtensorMap tah, tal, tbh, tbl, tcm, tpm, tgm;
   // K-major operand [rows][K]; MN-major [K][rows]
   auto mk = [&](CUtensorMap* m, const __half* p, const H3Operand& op, int rows, bool mn, uint32_t box_rows) {
     return mn ? map_plane(m, p, K, rows, op.ld, true) : map_plane(m, p, rows, K, op.ld, false, box_rows);
@@ -558,25 +774,49 @@ void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, fl
   a.ea = A.exp;
   a.eb = B.exp;
   const int tiles = a.nblocks_m * a.nblocks_n;
-  a.vunits = h3_vunits((int64_t)tiles * a.nk);
+  // stream-K: all tiles (split 1), or the tiles past the last full wave of
+  // H3_VUNITS/2 pairs (split 2), over up to H3_VUNITS virtual units
+  a.tiles_dp = split == 2 ? tiles / (H3_VUNITS / 2) * (H3_VUNITS / 2) : 0;
+  a.vunits = split == 2 ? std::min(h3_vunits((int64_t)(tiles - a.tiles_dp) * a.nk), H3_VUNITS / 2)
+                        : h3_vunits((int64_t)tiles * a.nk);
+  // the output map is used by whole tiles only (stream-K writes partials)
+  KP_CHECK(a.tiles_dp == 0 || (reinterpret_cast<uintptr_t>(C) % 16 == 0 && ((size_t)ldc * 4) % 16 == 0),
+           kErrGeneric, "h3_gemm: whole tiles need a 16-byte aligned output");
+  const int tail = tiles - a.tiles_dp;
+  const int64_t T = (int64_t)tail * a.nk;
+  if (!splitk || a.tiles_dp > 0) ok = ok && map_out(&tcm, C, M, N, ldc);
   if (splitk) {
-    a.mode = 0;  // partials are plain sums (scales are exact and applied per partial)
-    ok = ok && map_out(&tcm, ws, (uint64_t)(tiles + H3_VUNITS) * 2 * H3_BM, H3_BN, H3_BN);
+    KP_CHECK(ws != nullptr, kErrGeneric, "h3_gemm: stream-K needs a workspace");
+    ok = ok && map_out(&tpm, ws, (uint64_t)(tail + H3_VUNITS) * 2 * H3_BM, H3_BN, H3_BN);
+    if (a.tiles_dp == 0) tcm = tpm;
   } else {
-    ok = ok && map_out(&tcm, C, M, N, ldc);
+    tpm = tcm;
+  }
+  if constexpr (GA) {
+    // A = rows of ga->src, (m, slot) -> ga->rowocc[m*S + slot]; its planes
+    // (A.hi / A.lo) are outputs when ga->store
+    KP_CHECK(ga && ga->e % H3_BK == 0 && (uint64_t)ga->S * ga->e == (uint64_t)K && A.exp, kErrGeneric,
+             "h3_gemm: gathered A needs K = S*e, e % 32 == 0 and row exponents");
+    a.grow = ga->rowocc;
+    a.gS = ga->S;
+    a.gkps = ga->e / H3_BK;
+    a.gstore = ga->store ? 1 : 0;
+    ok = ok && map_rows(&tgm, ga->src, ga->nrows, ga->e);
+  } else {
+    tgm = tah;
   }
   KP_CHECK(ok, kErrCuda, "cuTensorMapEncodeTiled failed (3xFP16 GEMM operands)");
-  constexpr uint32_t SMEM = H3Cfg<BN>::SMEM;
+  constexpr uint32_t SMEM = H3Cfg<BN, GA>::SMEM;
   static std::atomic<uint64_t> attr{0};
   int dev = 0;
   KP_CUDA(cudaGetDevice(&dev));
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr.load(std::memory_order_acquire) & bit)) {
-    KP_CUDA(cudaFuncSetAttribute(k_h3<AMN, BMN, SK, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    KP_CUDA(cudaFuncSetAttribute(k_h3<AMN, BMN, SK, BN, GA>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     attr.fetch_or(bit, std::memory_order_release);
   }
-  const int units_all = std::max(1, h3_units<AMN, BMN, SK, BN>() - (g_h3_reserve + 1) / 2);
-  const int work = splitk ? a.vunits : tiles;
+  const int units_all = std::max(1, h3_units<AMN, BMN, SK, BN, GA>() - (g_h3_reserve + 1) / 2);
+  const int work = splitk ? std::max(a.vunits, a.tiles_dp > 0 ? H3_VUNITS / 2 : 0) : tiles;
   const unsigned grid = (unsigned)std::min(work, units_all) * 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
@@ -590,11 +830,11 @@ void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, fl
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  KP_CUDA(cudaLaunchKernelEx(&cfg, k_h3<AMN, BMN, SK, BN>, tah, tal, tbh, tbl, tcm, a));
+  KP_CUDA(cudaLaunchKernelEx(&cfg, k_h3<AMN, BMN, SK, BN, GA>, tah, tal, tbh, tbl, tcm, tpm, tgm, a));
   ::kp::count_launch();
-  if (splitk) {
-    const int64_t T = (int64_t)tiles * a.nk;
-    k_h3_fixup<<<dim3(64, tiles), 256, 0, s>>>(ws, a.nblocks_n, a.nk, T, a.vunits, M, N, C, ldc);
+  if (splitk && tail > 0) {
+    k_h3_fixup<<<dim3(64, tail), 256, 0, s>>>(ws, a.nblocks_n, a.nk, a.tiles_dp, T, a.vunits, M, N, C, ldc,
+                                              a.mode, a.act, a.bias);
     ::kp::count_launch();
   }
 }
@@ -779,7 +1019,7 @@ bool h3_supported(int M, int N, int K, const H3Operand& A, const H3Operand& B) {
 
 // C[m][n] = epi(sum_k A(m,k) B(n,k)); A/B K-major ([rows][K]) unless *_mn
 void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M, int N, int K, float* C,
-             int ldc, const GemmEpi& ep, bool splitk, float* ws, cudaStream_t s, int keep) {
+             int ldc, const GemmEpi& ep, int splitk, float* ws, cudaStream_t s, int keep, const H3Gather* ga) {
   H3Args a{};
   static const int dbg = [] {
     const char* e = getenv("KP_H3_DBG");
@@ -795,10 +1035,12 @@ void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M
   a.S = ep.S;
   a.e = ep.e;
   KP_CHECK(ep.mode == 0 || ep.mode == 1 || ep.mode == 3, kErrGeneric, "h3_gemm: unsupported epilogue");
-  if (!a_mn && !b_mn) launch_h3<false, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
+  KP_CHECK(splitk == 0 || ep.mode != 3, kErrGeneric, "h3_gemm: stream-K fix-up has no coefficient epilogue");
+  KP_CHECK(!ga || !a_mn, kErrGeneric, "h3_gemm: gathered A is K-major");
+  if (!a_mn && !b_mn) launch_h3<false, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s, ga);
   else if (a_mn && b_mn) launch_h3<true, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
   else if (a_mn) launch_h3<true, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
-  else launch_h3<false, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
+  else launch_h3<false, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s, ga);
 }
 
 size_t split_cols_colsum_ws_floats(int B, int N) {
@@ -807,8 +1049,9 @@ size_t split_cols_colsum_ws_floats(int B, int N) {
   return (size_t)std::min<uint64_t>(ceil_div(B, by), std::max<uint64_t>(1, 148 * 8 / ceil_div(N, W))) * N;
 }
 
-size_t h3_splitk_ws_floats(int M, int N) {
-  const size_t tiles = ceil_div(M, 2 * H3_BM) * ceil_div(N, H3_BN);
+size_t h3_splitk_ws_floats(int M, int N, bool tail_only) {
+  size_t tiles = ceil_div(M, 2 * H3_BM) * ceil_div(N, H3_BN);
+  if (tail_only) tiles = std::min<size_t>(tiles, H3_VUNITS / 2);
   return (tiles + H3_VUNITS) * 2 * H3_BM * H3_BN;
 }
 

@@ -178,7 +178,8 @@ struct SparseRule {
 };
 // Segments are [seg[u], seg[u+1]) of sorted positions p; the upstream row of
 // position p is rows_src[map(p)] with map(p) = bag_of_occ[sorted_vals[p]]
-// (bag_of_occ may be null: identity). Output: apply the rule to table row
+// (bag_of_occ may be null: identity; sorted_vals null: map(p) = p, rows
+// already in sorted order). Output: apply the rule to table row
 // table_rows[u] (fused push) when `t` is set, else store to grad_out[out_idx[u]]
 // -- or, with `pm`, to peer_dst(pm, out_idx[u]) in the owners' windows.
 void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* d_sorted_vals,
@@ -249,14 +250,27 @@ struct H3Operand {
 bool h3_enabled();  // KP_GEMM_H3=0 keeps layer 1 on the on-chip-split kernels
 bool h3_supported(int M, int N, int K, const H3Operand& A, const H3Operand& B);
 // C[m][n] = epi(2^-(ea[m]+eb[n]) sum_k A(m,k) B(n,k)); a_mn / b_mn: operand
-// stored [K][rows] (MN-major) instead of [rows][K]. splitk: deterministic
-// stream-K over the K range into `ws` (h3_splitk_ws_floats) + fix-up; only
-// the plain store epilogue (mode 0).
+// stored [K][rows] (MN-major) instead of [rows][K]. splitk: 0 data-parallel
+// tiles; 1 deterministic stream-K over all tiles' K ranges into `ws`
+// (h3_splitk_ws_floats) + fix-up; 2 whole tiles for the full waves of the
+// GPU's pairs and stream-K for the last partial wave. Stream-K: epilogue
+// modes 0 and 1 (applied by the fix-up), the split depends only on the shape.
 // keep: operands re-read across tiles (bit 0 A, bit 1 B) load with an L2
 // evict_last policy, the others evict_first
+// Gathered A (one feature per slot): A[m][slot*e + j] = src[rowocc[m*S + slot]][j],
+// fetched by TMA gather4 and split into planes on chip with the row exponents
+// A.exp; with `store` the planes also go to A.hi / A.lo (for a later GEMM).
+struct H3Gather {
+  const float* src;
+  uint64_t nrows;
+  const uint32_t* rowocc;
+  uint32_t S, e;
+  bool store;
+};
 void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M, int N, int K, float* C,
-             int ldc, const GemmEpi& ep, bool splitk, float* ws, cudaStream_t s, int keep = 3);
-size_t h3_splitk_ws_floats(int M, int N);
+             int ldc, const GemmEpi& ep, int splitk, float* ws, cudaStream_t s, int keep = 3,
+             const H3Gather* ga = nullptr);
+size_t h3_splitk_ws_floats(int M, int N, bool tail_only = false);
 void h3_reserve_sms(int n);
 // planes of W^T ([K][N], one exponent per row of W^T) from W [N][K], N <= 256
 void split_t_h(const float* W, int N, int K, __half* hi, __half* lo, int* exps, cudaStream_t s);
@@ -274,6 +288,13 @@ bool pool_planes_supported(uint32_t S, uint32_t e);
 void pool_planes(const uint32_t* d_bag_offs, uint32_t n_inst, uint32_t S, const uint32_t* d_row_of_occ,
                  const float* d_src, uint32_t e, bool mean, __half* d_hi, __half* d_lo, int* d_inst_exp,
                  float* d_inv_count, cudaStream_t s, bool ident = false);
+// One feature per slot, pooling fused into the first layer (the forward GEMM
+// gathers the rows itself): only the per-instance exponents of the planes the
+// pooling kernel would write -- row_exp(max over the instance's S rows of
+// max |x|), from one max per unique key -- and the mean coefficients (1).
+void inst_exps_ident(const float* d_src, const uint32_t* d_idx, uint32_t U, uint32_t e,
+                     const uint32_t* d_inverse, uint32_t n_inst, uint32_t S, float* d_umax_ws,
+                     int* d_inst_exp, float* d_inv_count, bool mean, cudaStream_t s);
 
 // ---------------------------------------------------------------- MLP ----
 struct MlpShape {
@@ -297,6 +318,13 @@ struct MlpWs {
   const int* in_exp = nullptr;
   DevBuf dzh, dzl, dze, dwh, dwl, dwe, cmax, skws;  // layer-1 backward planes, stream-K partials
   DevBuf hdone;  // head backward's last-block counter (the loss finalize)
+  // planes mode, one feature per slot: the forward gathers its input rows
+  // (row of (b, slot) = ga_rowocc[b*S + slot] of ga_src [ga_nrows][e]) and
+  // writes the planes at in_hi / in_lo for the weight gradient
+  const float* ga_src = nullptr;
+  uint64_t ga_nrows = 0;
+  const uint32_t* ga_rowocc = nullptr;
+  uint32_t ga_S = 0, ga_e = 0;
 };
 // Forward over B instances (input [B][in]); writes preds (sigmoid) and
 // logits; keeps activations in ws for backward.

@@ -414,8 +414,13 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
       __half* hl = reinterpret_cast<__half*>(ws.hlo.get<uint16_t>((size_t)N * K));
       int* he = ws.hexp.get<int>(N);
       split_h(W, N, K, K, hh, hl, he, s);
+      // (the last partial wave of tiles stream-K: 256 tiles = 3.46 waves at B = 65536)
+      // one feature per slot: the GEMM gathers the table rows itself (TMA
+      // gather4) and writes the planes on the way -- no pooling pass
+      const H3Gather ga{ws.ga_src, ws.ga_nrows, ws.ga_rowocc, ws.ga_S, ws.ga_e, true};
       h3_gemm(H3Operand{ws.in_hi, ws.in_lo, ws.in_exp, K}, false, H3Operand{hh, hl, he, K}, false, B, N, K,
-              out, N, ep, false, nullptr, s, /*keep W1*/ 2);
+              out, N, ep, 2, ws.skws.get<float>(h3_splitk_ws_floats(B, N, true)), s, /*keep W1*/ 2,
+              ws.ga_src ? &ga : nullptr);
     } else if (l == 0 && use_h(B, N, K, in, W)) {
       // first layer (the wide S*e contraction): fp16 operands, per-row scales
       const float* am = ws.in_rowmax;

@@ -255,11 +255,14 @@ __global__ void __launch_bounds__(ST, 4) k_downsweep(
   // Warp-striped items (warp w owns tile elements [w*IPT*32, (w+1)*IPT*32),
   // round r lane l -> w*IPT*32 + r*32 + l): element order = (warp, round,
   // lane), so a warp-local running count per digit gives a stable rank with
-  // no block barrier per round; one scan over [digit][warp] counts (digit
-  // major) then turns (digit, warp, rank-in-warp) into the tile position.
+  // no block barrier per round; one scan over the [warp][digit] counts in
+  // (digit, warp) order then turns (digit, warp, rank-in-warp) into the tile
+  // position. (Warp-major rows: a warp's lanes hit banks by digit, and the
+  // scan reads each digit's column with consecutive threads -- the digit-major
+  // layout had 8- and 16-way bank conflicts in those two places.)
   __shared__ KOUT s_keys[TILE];
   __shared__ uint32_t s_vals[TILE];
-  __shared__ uint32_t s_wh[R * NW];  // [digit][warp] counts -> exclusive tile positions
+  __shared__ __align__(16) uint32_t s_wh[NW * R];  // [warp][digit] counts -> exclusive tile positions
   __shared__ uint32_t s_start[R], s_off[R];
   __shared__ uint32_t s_warp[NW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -285,42 +288,57 @@ __global__ void __launch_bounds__(ST, 4) k_downsweep(
       d[r] = R;
     }
   }
+  uint32_t* wrow = s_wh + warp * R;
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     const uint32_t peers = match_digit<R>(d[r], full);
     const bool leader = lane == __ffs(peers) - 1;
     uint32_t before = 0;
-    if (d[r] < R) before = s_wh[d[r] * NW + warp];
+    if (d[r] < R) before = wrow[d[r]];
     __syncwarp();
     if (d[r] < R) {
       rw[r] = before + __popc(peers & lt);
-      if (leader) s_wh[d[r] * NW + warp] = before + __popc(peers);
+      if (leader) wrow[d[r]] = before + __popc(peers);
     }
     __syncwarp();
   }
   __syncthreads();
-  // exclusive scan of s_wh in (digit, warp) order: thread t owns R*NW/ST entries
+  // exclusive scan in (digit, warp) order: thread t owns digits [t*DPT, +DPT);
+  // the column is read twice (sums, then positions) instead of held
   {
-    constexpr int PER = R * NW / ST;
-    uint32_t loc[PER], sum = 0;
+    constexpr int DPT = R / ST;
+    static_assert(DPT == 1 || DPT == 2, "256 or 512 digits");
+    uint32_t t0 = 0, t1 = 0;  // the owned digits' totals
 #pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      loc[j] = s_wh[tid * PER + j];
-      sum += loc[j];
+    for (int w = 0; w < NW; ++w) {
+      if constexpr (DPT == 2) {
+        const uint2 x = *reinterpret_cast<const uint2*>(s_wh + w * R + 2 * tid);
+        t0 += x.x;
+        t1 += x.y;
+      } else {
+        t0 += s_wh[w * R + tid];
+      }
     }
     uint32_t tot;
-    uint32_t pre = block_excl_scan(sum, s_warp, tot);
+    uint32_t p0 = block_excl_scan(t0 + t1, s_warp, tot), p1 = p0 + t0;
+    s_start[tid * DPT] = p0;  // first tile position of the digit
+    if constexpr (DPT == 2) s_start[tid * DPT + 1] = p1;
 #pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      s_wh[tid * PER + j] = pre;
-      pre += loc[j];
+    for (int w = 0; w < NW; ++w) {
+      if constexpr (DPT == 2) {
+        uint2* q = reinterpret_cast<uint2*>(s_wh + w * R + 2 * tid);
+        const uint2 x = *q;
+        *q = make_uint2(p0, p1);
+        p0 += x.x;
+        p1 += x.y;
+      } else {
+        const uint32_t x = s_wh[w * R + tid];
+        s_wh[w * R + tid] = p0;
+        p0 += x;
+      }
     }
   }
-  __syncthreads();
-  for (int i = tid; i < R; i += ST) {
-    s_start[i] = s_wh[i * NW];  // first tile position of digit i
-    s_off[i] = totals[i];
-  }
+  for (int i = tid; i < R; i += ST) s_off[i] = totals[i];
   __syncthreads();
   scan_digits<R>(s_off, s_off, s_warp);  // global digit starts (in place: values read first)
   __syncthreads();
@@ -328,7 +346,7 @@ __global__ void __launch_bounds__(ST, 4) k_downsweep(
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     if (d[r] < R) {
-      const uint32_t p = s_wh[d[r] * NW + warp] + rw[r];
+      const uint32_t p = wrow[d[r]] + rw[r];
       s_keys[p] = k[r];
       s_vals[p] = v[r];
     }

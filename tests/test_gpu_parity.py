@@ -284,16 +284,17 @@ def test_trainer_slots_and_sparse_adam_vs_oracle(kp, S, pool, rule):
         assert close(tr.worker_state(i)["x"], o64.worker_state(i)["x"])
 
 
-@pytest.mark.parametrize("S,e,pool,rule,multi", [(12, 16, "sum", "adagrad", False),
-                                                 (10, 128, "mean", "adam", True),
-                                                 (16, 64, "sum", "adagrad", False),
-                                                 (9, 4, "mean", "adagrad", True)])
-def test_trainer_pooling_paths_vs_oracle(kp, S, e, pool, rule, multi):
+@pytest.mark.parametrize("S,e,pool,rule,multi,act", [(12, 16, "sum", "adagrad", False, "relu"),
+                                                     (10, 128, "mean", "adam", True, "relu"),
+                                                     (16, 64, "sum", "adagrad", False, "relu"),
+                                                     (9, 4, "mean", "adagrad", True, "relu"),
+                                                     (16, 64, "mean", "adam", False, "tanh")])
+def test_trainer_pooling_paths_vs_oracle(kp, S, e, pool, rule, multi, act):
     """Instance-major pooling (S >= 8, e <= 64: one warp per instance, row
     maxima without atomics) and the atomic row-max path (e = 128 / multi-hot),
     feeding the fp16 first layer: state vs the f64 oracle."""
     cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=256, embedding_dim=e, n_slots=S,
-                       hidden=(32, 16), pooling=pool, activation="relu", alpha=0.02, sparse_lr=0.1,
+                       hidden=(32, 16), pooling=pool, activation=act, alpha=0.02, sparse_lr=0.1,
                        sparse_rule=rule, sparse_beta1=0.9, sparse_beta2=0.99, sparse_eps=1e-6)
     o64 = O.Orc(cfg, 64)
     tr = kp.Trainer(table_capacity=1 << 16, **trainer_kwargs(vars(cfg)))
@@ -461,12 +462,17 @@ def test_tcgen05_gemm_f16_scaled_accuracy(kp, M, N, K, spread):
                                                  (1000, 256, 6400, 8, 4), (512, 6400, 256, 4, 4),
                                                  (65, 40, 96, 0, 4), (4096, 256, 6400, 3, 5),
                                                  (256, 384, 4096, 2, 5), (777, 208, 64, 1, 4),
-                                                 (3000, 1000, 200, 2, 4), (65536, 6400, 256, 1, 4)])
+                                                 (3000, 1000, 200, 2, 4), (65536, 6400, 256, 1, 4),
+                                                 (65536, 256, 6400, 1, 6), (4096, 256, 6400, 3, 5),
+                                                 (19456, 256, 512, 0, 6), (18944, 256, 64, 0, 6),
+                                                 (20000, 300, 96, 2, 6)])
 def test_h3_gemm_nt_accuracy(kp, M, N, K, spread, engine):
     """3xFP16 on pre-split fp16 planes (kp_gemm_h3.cu, the planes-mode first
-    layer), both operands K-major; engine 5 = deterministic stream-K over K:
-    fp32-level error like the SIMT fp32 GEMM, with rows spanning 2^+-spread,
-    a zero row and tiny elements inside a row."""
+    layer), both operands K-major; engine 5 = deterministic stream-K over K,
+    6 = whole tiles for the full waves of 74 pairs + stream-K for the last
+    partial wave (the forward's split): fp32-level error like the SIMT fp32
+    GEMM, with rows spanning 2^+-spread, a zero row and tiny elements inside
+    a row."""
     rng = np.random.default_rng(M * 3 + N + K + spread)
     A = rng.standard_normal((M, K)).astype(np.float32)
     B = rng.standard_normal((N, K)).astype(np.float32)
@@ -483,8 +489,15 @@ def test_h3_gemm_nt_accuracy(kp, M, N, K, spread, engine):
     err_simt = np.max(np.abs(simt - want) / scale)
     print(f"h3 nt M={M} N={N} K={K} spread={spread} e{engine}: err={err_h:.3e} simt={err_simt:.3e}")
     assert err_h < 3 * err_simt + 2e-6, (err_h, err_simt)
-    if engine == 5:  # deterministic: bitwise identical on a rerun
-        assert np.array_equal(kp.gemm_nt(A, B, engine=5), h)
+    if engine in (5, 6):  # deterministic: bitwise identical on a rerun
+        assert np.array_equal(kp.gemm_nt(A, B, engine=engine), h)
+    if engine == 6 and N <= 256:
+        # the whole tiles (full waves of 74 pairs of 256 rows) are the
+        # data-parallel kernel's, bit for bit
+        whole = (M + 255) // 256 // 74 * 74 * 256
+        h4 = kp.gemm_nt(A, B, engine=4)
+        bad = np.nonzero(np.any(h[:whole] != h4[:whole], axis=1))[0]
+        assert len(bad) == 0, (len(bad), bad[:8], np.unique(bad // 256)[:8])
 
 
 @pytest.mark.parametrize("M,N,K,engine", [(256, 6400, 4096, 4), (256, 6400, 4096, 5), (128, 256, 65536, 5),
@@ -617,3 +630,42 @@ def test_trainer_online_auc_matches_host(kp):
         labels.append(bt.labels)
         assert r["auc"] == O.orc_auc(scores[-1], bt.labels)
         assert r["cumulative_auc"] == O.orc_auc(np.concatenate(scores), np.concatenate(labels))
+
+
+@pytest.mark.parametrize("B,S,e,pool,workers,hidden", [(4096, 100, 64, "sum", 1, (256, 128)),
+                                                       (3000, 26, 32, "mean", 2, (64, 32)),
+                                                       (20000, 100, 64, "sum", 1, (256, 128)),
+                                                       (1000, 12, 96, "sum", 1, (264, 16)),
+                                                       (1000, 12, 96, "sum", 1, (300, 16))])
+def test_fused_pool_gather_bitwise(kp, monkeypatch, B, S, e, pool, workers, hidden):
+    """One feature per slot: the first layer's forward fetches the table rows
+    itself (TMA gather4 into its pipeline, split into fp16 planes on chip, the
+    planes stored for the weight gradient) instead of a pooling pass. Same
+    exponents, same planes, same GEMM: every trained bit (table rows and
+    accumulators, dense x, losses, predictions) equals the pooling-pass path
+    (the default). Covers the hybrid stream-K split (20000 rows: 79 tiles),
+    W=2 worker slices, mean pooling and N > 256 (two column tiles); hidden
+    300 (rows of 600 bytes) takes neither planes path (it used to fail the
+    backward's tensor-map encode)."""
+    out = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("KP_FUSED_POOL", fused)  # read at trainer creation
+        cfg = O.TrainerCfg(n_workers=workers, k=2, minibatch_size=B, embedding_dim=e, n_slots=S,
+                           hidden=hidden, pooling=pool, activation="relu", alpha=0.02, sparse_lr=0.1)
+        tr = kp.Trainer(table_capacity=1 << 20, **trainer_kwargs(vars(cfg)))
+        losses, preds = [], []
+        for b in range(3):
+            bt = make_batch(B, V=10**6, zipf_s=1.1, n_slots=S, seed=300 + b)
+            r = tr.train_batch(bt.offs, bt.keys, bt.labels, slots=bt.slots, predict_first=True)
+            losses.append(r["loss"])
+            preds.append(np.asarray(r["preds"]).copy() if "preds" in r else None)
+        k, w, s1, _ = tr.table()
+        out.append((losses, preds, k, w, s1, tr.worker_state(0)["x"]))
+    (l1, p1, k1, w1, a1, x1), (l0, p0, k0, w0, a0, x0) = out
+    assert l1 == l0
+    for a, b in zip(p1, p0):
+        assert (a is None and b is None) or np.array_equal(a, b)
+    assert np.array_equal(k1, k0)
+    assert np.array_equal(w1, w0)
+    assert np.array_equal(a1, a0)
+    assert np.array_equal(x1, x0)

@@ -1,0 +1,10 @@
+mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider --timeout=200 -x -k "h3_gemm" > gpurun_out/pytest_h3.log 2>&1; echo h3 rc=$?; tail -3 gpurun_out/pytest_h3.log
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout=400 -x > gpurun_out/pytest_gpu.log 2>&1; echo gpu rc=$?; tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), d['roofline']['frac'], {k:round(v['ms_per_step'],3) for k,v in d['stages'].items()})"
+timeout 600 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum -k regex:"^k_h3" --clock-control none -c 8 --csv --log-file gpurun_out/h3.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo ncu rc=$?
+python - <<PY
+import csv
+rows=[r for r in csv.reader(open('gpurun_out/h3.csv')) if len(r)>10 and r[0].isdigit()]
+for r in rows[-8:]: print('   ', r[4][:60], r[-1])
+PY
