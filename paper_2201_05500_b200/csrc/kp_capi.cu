@@ -1779,8 +1779,11 @@ int kp_trainer_create(const kp_trainer_config* cfg, kp_comm* comm, int device, k
     }
     // (the backward's plane operands [B][hidden1] and W1^T [S*e][hidden1]
     // need 16-byte rows: hidden1 % 8 == 0)
+    if (const char* e = getenv("KP_TC_MIN_MFLOP")) tr->mlp.tc_min_flop = atof(e) * 1e6;
     tr->planes = c.n_hidden >= 1 && tc_enabled() && tc_h_enabled() && h3_enabled() &&
-                 pool_planes_supported(c.n_slots, c.embedding_dim) && m.widths[1] % 8 == 0;
+                 pool_planes_supported(c.n_slots, c.embedding_dim) && m.widths[1] % 8 == 0 &&
+                 tc_worth((int)std::min<uint64_t>(c.minibatch_size, 1u << 30), (int)m.widths[1],
+                          (int)m.widths[0], tr->mlp.tc_min_flop);
     const uint64_t D = m.D, W = tr->W;
     std::vector<double> x0(D);
     init_dense_host(c.seed, D, x0.data());

@@ -296,6 +296,9 @@ void inst_exps_ident(const float* d_src, const uint32_t* d_idx, uint32_t U, uint
                      const uint32_t* d_inverse, uint32_t n_inst, uint32_t S, float* d_umax_ws,
                      int* d_inst_exp, float* d_inv_count, bool mean, cudaStream_t s);
 
+// is an M x N x K product big enough for the tcgen05 kernels (else the SIMT one)
+bool tc_worth(int M, int N, int K, double min_flop);
+
 // ---------------------------------------------------------------- MLP ----
 struct MlpShape {
   uint32_t n_layers = 0;          // hidden + 1
@@ -321,6 +324,9 @@ struct MlpWs {
   // planes mode, one feature per slot: the forward gathers its input rows
   // (row of (b, slot) = ga_rowocc[b*S + slot] of ga_src [ga_nrows][e]) and
   // writes the planes at in_hi / in_lo for the weight gradient
+  // products below this many flops run on the small-tile SIMT kernel
+  // (KP_TC_MIN_MFLOP at trainer creation; 512 MFLOP: configs[0] is all SIMT)
+  double tc_min_flop = 512e6;
   const float* ga_src = nullptr;
   uint64_t ga_nrows = 0;
   const uint32_t* ga_rowocc = nullptr;

@@ -186,11 +186,109 @@ __global__ void __launch_bounds__(GT) k_gemm(int M, int N, int K, const float* _
   }
 }
 
+// Small tiles (32 x 64, 8 outputs per thread) for the skinny products of small
+// batches (configs[0]'s [208->64->32->1] at 4096 instances): the 128 x 128 tile
+// leaves most of the GPU idle there -- 32 CTAs for a 4096 x 32 layer.
+constexpr int SBM = 32, SBN = 64, SBK = 32;
+template <bool A_K, bool B_K>
+__global__ void __launch_bounds__(256) k_gemm_s(int M, int N, int K, const float* __restrict__ A, int lda,
+                                                const float* __restrict__ B, int ldb, float* __restrict__ C,
+                                                int ldc, int kps, EpiArgs ep) {
+  __shared__ __align__(16) float As[SBK][SBM + 4];  // [k][m]
+  __shared__ __align__(16) float Bs[SBK][SBN + 4];  // [k][n]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // columns tx*4.., rows ty*2..
+  const int m0 = blockIdx.y * SBM, n0 = blockIdx.x * SBN;
+  const int kb = blockIdx.z * kps, ke = min(K, kb + kps);
+  if (blockIdx.z > 0) C += (size_t)blockIdx.z * M * ldc;
+  float acc[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  // the next k-chunk's operands are loaded into registers while this one is
+  // multiplied (loads run along each operand's contiguous dimension)
+  constexpr int NA = SBM * SBK / 256, NB = SBN * SBK / 256;
+  float ra[NA], rb[NB];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < NA; ++q) {
+      const int i = threadIdx.x + q * 256;
+      const int m = A_K ? i / SBK : i % SBM, k = A_K ? i % SBK : i / SBM;
+      const int gm = m0 + m, gk = k0 + k;
+      ra[q] = (gm < M && gk < ke) ? (A_K ? A[(size_t)gm * lda + gk] : A[(size_t)gk * lda + gm]) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      const int i = threadIdx.x + q * 256;
+      const int n = B_K ? i / SBK : i % SBN, k = B_K ? i % SBK : i / SBN;
+      const int gn = n0 + n, gk = k0 + k;
+      rb[q] = (gn < N && gk < ke) ? (B_K ? B[(size_t)gn * ldb + gk] : B[(size_t)gk * ldb + gn]) : 0.f;
+    }
+  };
+  if (kb < ke) load(kb);
+  for (int k0 = kb; k0 < ke; k0 += SBK) {
+#pragma unroll
+    for (int q = 0; q < NA; ++q) {
+      const int i = threadIdx.x + q * 256;
+      As[A_K ? i % SBK : i / SBM][A_K ? i / SBK : i % SBM] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      const int i = threadIdx.x + q * 256;
+      Bs[B_K ? i % SBK : i / SBN][B_K ? i / SBK : i % SBN] = rb[q];
+    }
+    __syncthreads();
+    if (k0 + SBK < ke) load(k0 + SBK);
+#pragma unroll 8
+    for (int k = 0; k < SBK; ++k) {
+      const float2 a = *reinterpret_cast<const float2*>(&As[k][ty * 2]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
+      const float av[2] = {a.x, a.y}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int m = m0 + ty * 2 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float v = acc[i][j];
+      if (ep.mode == kBiasAct) {
+        v = act_fwd(ep.act, __fadd_rn(v, ep.bias[n]));
+      } else if (ep.mode == kDAct) {
+        v = __fmul_rn(v, act_bwd(ep.act, ep.aux[(size_t)m * ep.ld_aux + n]));
+      } else if (ep.mode == kCoeff) {
+        v = __fmul_rn(v, ep.coeff[(size_t)m * ep.S + n / ep.e]);
+      }
+      C[(size_t)m * ldc + n] = v;
+    }
+  }
+}
+
+// the small tiles when the 128 x 128 ones would not cover the SMs
+bool small_tiles(int M, int N) { return ceil_div(M, BM) * ceil_div(N, BN) < 148; }
+
 template <bool A_K, bool B_K>
 int gemm(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
           int splits, const EpiArgs& ep, cudaStream_t s) {
   if (M <= 0 || N <= 0) return 0;
   splits = splits < 1 ? 1 : splits;
+  if (small_tiles(M, N)) {
+    int kps = (K + splits - 1) / splits;
+    kps = std::max(SBK, (kps + SBK - 1) / SBK * SBK);
+    splits = K > 0 ? (K + kps - 1) / kps : 1;
+    dim3 grid(ceil_div(N, SBN), ceil_div(M, SBM), splits);
+    k_gemm_s<A_K, B_K><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, kps, ep);
+    ::kp::count_launch();
+    return splits;
+  }
   int kps = (K + splits - 1) / splits;
   kps = (kps + BK - 1) / BK * BK;
   splits = K > 0 ? (K + kps - 1) / kps : 1;
@@ -207,6 +305,34 @@ int gemm(int M, int N, int K, const float* A, int lda, const float* B, int ldb, 
 }
 
 // out[i] = sum_z part[z][i], z ascending (deterministic split-K reduce)
+// small outputs with many splits (the SIMT weight gradients of configs[0]):
+// 32 outputs per block, 8 thread rows each summing a fixed z-range, then the
+// 8 range sums in order -- a fixed tree, deterministic like the flat one
+__global__ void k_reduce_splits_wide(const float* __restrict__ part, int splits, size_t n,
+                                     float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const size_t i = blockIdx.x * (size_t)32 + threadIdx.x;
+  const int z0 = threadIdx.y * splits / 8, z1 = (threadIdx.y + 1) * splits / 8;
+  float v = 0.f;
+  if (i < n) {
+    int z = z0;
+    for (; z + 4 <= z1; z += 4) {
+      const float a = part[(size_t)z * n + i], b = part[(size_t)(z + 1) * n + i];
+      const float c = part[(size_t)(z + 2) * n + i], d = part[(size_t)(z + 3) * n + i];
+      v = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(v, a), b), c), d);
+    }
+    for (; z < z1; ++z) v = __fadd_rn(v, part[(size_t)z * n + i]);
+  }
+  red[threadIdx.y][threadIdx.x] = v;
+  __syncthreads();
+  if (threadIdx.y == 0 && i < n) {
+    float t = red[0][threadIdx.x];
+#pragma unroll
+    for (int r = 1; r < 8; ++r) t = __fadd_rn(t, red[r][threadIdx.x]);
+    out[i] = t;
+  }
+}
+
 __global__ void k_reduce_splits(const float* __restrict__ part, int splits, size_t n,
                                 float* __restrict__ out) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
@@ -353,11 +479,22 @@ unsigned grid_cap(uint64_t blocks) {
   return (unsigned)blocks;
 }
 
+// split-K reduce: the wide form when few outputs would leave the GPU idle
+void reduce_splits_any(const float* part, int splits, size_t n, float* out, cudaStream_t s) {
+  if (n < 148 * 256 && splits >= 16) {
+    k_reduce_splits_wide<<<(unsigned)ceil_div(n, 32), dim3(32, 8), 0, s>>>(part, splits, n, out);
+  } else {
+    k_reduce_splits<<<grid_cap(ceil_div(n, 256)), 256, 0, s>>>(part, splits, n, out);
+  }
+  ::kp::count_launch();
+}
+
 // split-K count: enough CTAs to cover ~2 waves of 148 SMs
 int pick_splits(int M, int N, int K) {
-  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, BN));
+  const bool sm = small_tiles(M, N);
+  const int tiles = sm ? (int)(ceil_div(M, SBM) * ceil_div(N, SBN)) : (int)(ceil_div(M, BM) * ceil_div(N, BN));
   int sp = (2 * 148 + tiles - 1) / tiles;
-  const int max_sp = (K + 255) / 256;  // >= 256 rows per split
+  const int max_sp = sm ? (K + 63) / 64 : (K + 255) / 256;  // >= 64 / 256 rows per split
   if (sp > max_sp) sp = max_sp;
   return sp < 1 ? 1 : sp;
 }
@@ -377,7 +514,7 @@ void simt_gemm_tn(int M, int N, int K, const float* A, int lda, const float* B, 
 }
 
 void reduce_splits(const float* part, int splits, size_t n, float* out, cudaStream_t s) {
-  k_reduce_splits<<<grid_cap(ceil_div(n, 256)), 256, 0, s>>>(part, splits, n, out); ::kp::count_launch();
+  reduce_splits_any(part, splits, n, out, s);
 }
 
 static bool gemm_pre() {
@@ -388,13 +525,15 @@ static bool gemm_pre() {
   return on;
 }
 
-// tiny GEMMs (configs[0]'s hidden layers: 4096 x 32 x 64) finish sooner on the
-// SIMT kernel than a persistent tcgen05 launch with its TMEM/barrier set-up
-static bool tc_worth(int M, int N, int K) { return 2.0 * M * N * K >= 64e6; }
+// small GEMMs (all of configs[0]'s layers: <= 109 MFLOP at 4096 instances)
+// finish sooner on the small-tile SIMT kernel than a persistent tcgen05 launch
+// with its TMEM/barrier set-up and operand splits
+bool tc_worth(int M, int N, int K, double min_flop) { return 2.0 * M * N * K >= min_flop; }
 
 // fp16-operand GEMM for the first layer: K-major, 16-byte aligned, K % 8 == 0
-static bool use_h(int M, int N, int K, const float* A, const float* W) {
-  return tc_enabled() && tc_h_enabled() && K % 8 == 0 && tc_gemm_supported(M, N, K, A, K, W, K);
+static bool use_h(int M, int N, int K, const float* A, const float* W, double min_flop) {
+  return tc_enabled() && tc_h_enabled() && tc_worth(M, N, K, min_flop) && K % 8 == 0 &&
+         tc_gemm_supported(M, N, K, A, K, W, K);
 }
 
 void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_t B,
@@ -421,7 +560,7 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
       h3_gemm(H3Operand{ws.in_hi, ws.in_lo, ws.in_exp, K}, false, H3Operand{hh, hl, he, K}, false, B, N, K,
               out, N, ep, 2, ws.skws.get<float>(h3_splitk_ws_floats(B, N, true)), s, /*keep W1*/ 2,
               ws.ga_src ? &ga : nullptr);
-    } else if (l == 0 && use_h(B, N, K, in, W)) {
+    } else if (l == 0 && use_h(B, N, K, in, W, ws.tc_min_flop)) {
       // first layer (the wide S*e contraction): fp16 operands, per-row scales
       const float* am = ws.in_rowmax;
       if (!am) {
@@ -434,7 +573,7 @@ void mlp_forward(const MlpShape& m, const float* d_x, const float* d_in, uint32_
       int* he = ws.hexp.get<int>(N);
       split_h(W, N, K, K, hh, hl, he, s);
       tc_gemm_nt_h(B, N, K, in, K, am, hh, hl, he, K, out, N, ep, s);
-    } else if (tc_enabled() && tc_worth(B, N, K) && tc_gemm_supported(B, N, K, in, K, W, K)) {
+    } else if (tc_enabled() && tc_worth(B, N, K, ws.tc_min_flop) && tc_gemm_supported(B, N, K, in, K, W, K)) {
       float* whi = ws.whi.get<float>((size_t)N * K);
       float* wlo = ws.wlo.get<float>((size_t)N * K);
       if (gemm_pre()) {
@@ -469,7 +608,7 @@ __global__ void k_transpose(const float* __restrict__ in, int R, int Cc, float* 
 // dX[B][K] = dZ[B][N] . W[N][K]  (W^T kept K-major for the tensor-core path)
 void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, const EpiArgs& ep,
              MlpWs& ws, cudaStream_t s, bool first = false) {
-  if (first && N % 8 == 0 && use_h(B, K, N, dZ, W)) {
+  if (first && N % 8 == 0 && use_h(B, K, N, dZ, W, ws.tc_min_flop)) {
     // first layer's input gradient (the wide output): fp16 operands
     float* wt = ws.wt.get<float>((size_t)N * K);
     dim3 g(ceil_div(K, 32), ceil_div(N, 32));
@@ -483,7 +622,7 @@ void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, c
     tc_gemm_nt_h(B, K, N, dZ, N, am, th, tl, te, N, out, K, ep, s);
     return;
   }
-  if (tc_enabled() && tc_worth(B, K, N) && tc_gemm_supported(B, K, N, dZ, N, W, N)) {
+  if (tc_enabled() && tc_worth(B, K, N, ws.tc_min_flop) && tc_gemm_supported(B, K, N, dZ, N, W, N)) {
     float* wt = ws.wt.get<float>((size_t)N * K);
     dim3 g(ceil_div(K, 32), ceil_div(N, 32));
     k_transpose<<<g, dim3(32, 8), 0, s>>>(W, N, K, wt); ::kp::count_launch();
@@ -689,23 +828,21 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
     }
     // dW_l[o][i] = sum_b dZ[b][o] in[b][i]   (deterministic split-K)
     EpiArgs plain{kStore, 0, nullptr, nullptr, 0, nullptr, 1, 1};
-    if (tc_enabled() && tc_worth(N, K, B) && tc_gemm_supported(N, K, B, dZ, N, in, K)) {
+    if (tc_enabled() && tc_worth(N, K, B, ws.tc_min_flop) && tc_gemm_supported(N, K, B, dZ, N, in, K)) {
       const int tsp = tc_splits(N, K, B);
       if (tsp == 1) {
         tc_gemm_tn(N, K, B, dZ, N, in, K, d_grad + m.w_off[l], K, 1, s);
       } else {
         float* part = ws.partials.get<float>((size_t)tsp * N * K);
         const int got = tc_gemm_tn(N, K, B, dZ, N, in, K, part, K, tsp, s);
-        k_reduce_splits<<<grid_cap(ceil_div((uint64_t)N * K, 256)), 256, 0, s>>>(
-            part, got, (size_t)N * K, d_grad + m.w_off[l]); ::kp::count_launch();
+        reduce_splits_any(part, got, (size_t)N * K, d_grad + m.w_off[l], s);
       }
     } else if (const int sp = pick_splits(N, K, B); sp == 1) {
       gemm<false, false>(N, K, B, dZ, N, in, K, d_grad + m.w_off[l], K, 1, plain, s);
     } else {
       float* part = ws.partials.get<float>((size_t)sp * N * K);
       const int got = gemm<false, false>(N, K, B, dZ, N, in, K, part, K, sp, plain, s);
-      k_reduce_splits<<<grid_cap(ceil_div((uint64_t)N * K, 256)), 256, 0, s>>>(
-          part, got, (size_t)N * K, d_grad + m.w_off[l]); ::kp::count_launch();
+      reduce_splits_any(part, got, (size_t)N * K, d_grad + m.w_off[l], s);
     }
     if (l != (int)L - 2) colsum(dZ, nullptr, B, N, d_grad + m.b_off[l], ws, s);  // (L-2: with the head's)
     // upstream for the layer below: dX = dZ . W_l, then act' or pooling coeff

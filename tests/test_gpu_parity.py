@@ -289,10 +289,16 @@ def test_trainer_slots_and_sparse_adam_vs_oracle(kp, S, pool, rule):
                                                      (16, 64, "sum", "adagrad", False, "relu"),
                                                      (9, 4, "mean", "adagrad", True, "relu"),
                                                      (16, 64, "mean", "adam", False, "tanh")])
-def test_trainer_pooling_paths_vs_oracle(kp, S, e, pool, rule, multi, act):
+@pytest.mark.parametrize("tc_min", ["0", None])
+def test_trainer_pooling_paths_vs_oracle(kp, monkeypatch, S, e, pool, rule, multi, act, tc_min):
     """Instance-major pooling (S >= 8, e <= 64: one warp per instance, row
     maxima without atomics) and the atomic row-max path (e = 128 / multi-hot),
-    feeding the fp16 first layer: state vs the f64 oracle."""
+    feeding the first layer -- on the tensor-core paths (fp16 planes / fp16
+    operands; KP_TC_MIN_MFLOP=0 forces them at this small batch) and on the
+    small-tile SIMT kernel the default routes these small products to:
+    state vs the f64 oracle."""
+    if tc_min is not None:
+        monkeypatch.setenv("KP_TC_MIN_MFLOP", tc_min)
     cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=256, embedding_dim=e, n_slots=S,
                        hidden=(32, 16), pooling=pool, activation=act, alpha=0.02, sparse_lr=0.1,
                        sparse_rule=rule, sparse_beta1=0.9, sparse_beta2=0.99, sparse_eps=1e-6)
@@ -648,6 +654,7 @@ def test_fused_pool_gather_bitwise(kp, monkeypatch, B, S, e, pool, workers, hidd
     300 (rows of 600 bytes) takes neither planes path (it used to fail the
     backward's tensor-map encode)."""
     out = []
+    monkeypatch.setenv("KP_TC_MIN_MFLOP", "0")  # the planes path at every size here
     for fused in ("1", "0"):
         monkeypatch.setenv("KP_FUSED_POOL", fused)  # read at trainer creation
         cfg = O.TrainerCfg(n_workers=workers, k=2, minibatch_size=B, embedding_dim=e, n_slots=S,
