@@ -644,6 +644,10 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   if (sv.n_occ == 0) KP_CUDA(cudaStreamSynchronize(s));
   const uint32_t h_err = h_errw[0];
   const bool ident_bags = h_errw[1] == 0xFFFFFFFFu && sv.n_occ == nb;
+  // the identity occurrence -> bag map: the bag of sorted position p is the
+  // sorted occurrence itself (dedup skipped writing the copy)
+  if (h_errw[1] == 0xFFFFFFFFu && sv.n_occ > 0)
+    tr->dd.d_sorted_mapped = const_cast<uint32_t*>(tr->dd.sorted_vals);
   // reject bad slot ids before any state (table, weights) changes
   KP_CHECK(h_err == 0xFFFFFFFFu, kErrConfig,
            "slot ids must be < n_slots and non-decreasing within an instance (occurrence " +
@@ -735,15 +739,24 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
     pr.src = rrows;
     pr.idx = pos;
   }
-  // pooling over the composed per-occurrence source rows
+  // pooling over the composed per-occurrence source rows (the one-feature
+  // planes kernel composes on the fly: its index prefetch reads inverse, then
+  // the unique's row)
+  tr->ga_on = tr->fused_pool && tr->planes && ident_bags && tr->e % 32 == 0 && sv.n_occ > 0;
+  // (measured: pool 0.52 vs 0.48 ms against compose's 0.02 -- off; KP_POOL_COMPOSE=1)
+  static const bool pool_compose = [] {
+    const char* e = getenv("KP_POOL_COMPOSE");
+    return e && e[0] == '1';
+  }();
+  const bool compose_in_pool =
+      pool_compose && tr->planes && ident_bags && !tr->ga_on && planes_ident_kernel(tr->S, tr->e);
   uint32_t* rowocc = tr->rowocc.get<uint32_t>(std::max<uint32_t>(sv.n_occ, 1));
-  compose(pr.idx, tr->dd.d_inverse, sv.n_occ, rowocc, s);
+  if (!compose_in_pool) compose(pr.idx, tr->dd.d_inverse, sv.n_occ, rowocc, s);
   float* pooled = tr->pooled.get<float>((size_t)std::max<uint32_t>(nb, 1) * tr->e);
   float* invc = tr->inv_count.get<float>(std::max<uint32_t>(nb, 1));
   // one feature per slot, KP_FUSED_POOL=1: the first layer's forward gathers
   // the rows itself (kp_gemm_h3.cu, TMA gather4) and writes the planes; only
   // the instance exponents here
-  tr->ga_on = tr->fused_pool && tr->planes && ident_bags && tr->e % 32 == 0 && sv.n_occ > 0;
   if (tr->ga_on) {
     int* iexp = tr->inst_exp.get<int>(std::max<uint32_t>(sv.n_inst, 1));
     float* umax = tr->umax.get<float>(std::max<uint32_t>(U, 1));
@@ -756,8 +769,9 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
     // the first layer's input as fp16 planes (hi at pooled, lo behind it)
     __half* hi = reinterpret_cast<__half*>(pooled);
     int* iexp = tr->inst_exp.get<int>(std::max<uint32_t>(sv.n_inst, 1));
-    pool_planes(bag_offs, sv.n_inst, tr->S, rowocc, pr.src, tr->e, tr->cfg.pooling == 1, hi,
-                hi + (size_t)nb * tr->e, iexp, invc, s, ident_bags);
+    pool_planes(bag_offs, sv.n_inst, tr->S, compose_in_pool ? pr.idx : rowocc, pr.src, tr->e,
+                tr->cfg.pooling == 1, hi, hi + (size_t)nb * tr->e, iexp, invc, s, ident_bags,
+                compose_in_pool ? tr->dd.d_inverse : nullptr);
   } else {
     // max |row| of the MLP input per instance (fp16-operand first layer)
     float* imax = tr->inst_max.get<float>(std::max<uint32_t>(sv.n_inst, 1));

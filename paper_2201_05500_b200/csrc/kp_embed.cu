@@ -372,9 +372,12 @@ __global__ void __launch_bounds__(NT, NP <= 4 ? 4 : 2) k_pool_planes(const uint3
 // b, flagged by prepare_bags): no bag offsets, cell c's row is rowocc[inst*S
 // + c / (e/4)], and the next instance's row indices are loaded while this
 // instance's rows are in flight (the index -> row chain is the latency).
+// (inverse set: rowocc is the unique -> row map and the row of occurrence o is
+// rowocc[inverse[o]] -- the compose pass folded into the index prefetch)
 template <int NT, int NP>
 __global__ void __launch_bounds__(NT, 4) k_pool_planes_ident(uint32_t n_inst, uint32_t S,
                                                              const uint32_t* __restrict__ rowocc,
+                                                             const uint32_t* __restrict__ inverse,
                                                              const float* __restrict__ src, uint32_t e,
                                                              __half* __restrict__ hi, __half* __restrict__ lo,
                                                              int* __restrict__ inst_exp,
@@ -387,7 +390,12 @@ __global__ void __launch_bounds__(NT, 4) k_pool_planes_ident(uint32_t n_inst, ui
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       const uint32_t c = threadIdx.x + p * NT;
-      r[p] = (i < n_inst && c < ncell) ? __ldg(rowocc + i * S + c / lpr) : kNoRow;
+      r[p] = (i < n_inst && c < ncell) ? __ldg((inverse ? inverse : rowocc) + i * S + c / lpr) : kNoRow;
+    }
+    if (inverse) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+        if (r[p] != kNoRow) r[p] = __ldg(rowocc + r[p]);
     }
   };
   load_idx(inst, rr);
@@ -928,24 +936,32 @@ void pool(const uint32_t* d_bag_offs, uint32_t n_bags, const uint32_t* d_row_of_
                     d_inst_max, S, s);
 }
 
+// one feature per slot, 256 < S*e/4 <= 2048 cells: k_pool_planes_ident
+bool planes_ident_kernel(uint32_t S, uint32_t e) {
+  const uint32_t cells = S * e / 4;
+  return cells > 256 && cells <= 256 * 8 && S <= 256;
+}
+
 bool pool_planes_supported(uint32_t S, uint32_t e) {
   return e % 4 == 0 && e <= 128 && (S * e) % 8 == 0 && S * e / 4 <= 256 * 16;
 }
 
 void pool_planes(const uint32_t* d_bag_offs, uint32_t n_inst, uint32_t S, const uint32_t* d_row_of_occ,
                  const float* d_src, uint32_t e, bool mean, __half* d_hi, __half* d_lo, int* d_inst_exp,
-                 float* d_inv_count, cudaStream_t s, bool ident) {
+                 float* d_inv_count, cudaStream_t s, bool ident, const uint32_t* d_inverse) {
   KP_CHECK(pool_planes_supported(S, e), kErrConfig, "pool_planes: unsupported S*e");
+  KP_CHECK(!d_inverse || (ident && planes_ident_kernel(S, e)), kErrGeneric,
+           "pool_planes: the unique -> row map form is for one feature per slot");
   if (n_inst == 0) return;
   const uint32_t cells = S * e / 4;
-  if (ident && cells > 256 && cells <= 256 * 8 && S <= 256) {
+  if (ident && planes_ident_kernel(S, e)) {
     const unsigned grid = (unsigned)std::min<uint64_t>(n_inst, 148ull * 4);
     if (cells <= 256 * 4)
-      k_pool_planes_ident<256, 4><<<grid, 256, 0, s>>>(n_inst, S, d_row_of_occ, d_src, e, d_hi, d_lo, d_inst_exp,
-                                                        d_inv_count, mean ? 1 : 0);
+      k_pool_planes_ident<256, 4><<<grid, 256, 0, s>>>(n_inst, S, d_row_of_occ, d_inverse, d_src, e, d_hi, d_lo,
+                                                        d_inst_exp, d_inv_count, mean ? 1 : 0);
     else
-      k_pool_planes_ident<256, 8><<<grid, 256, 0, s>>>(n_inst, S, d_row_of_occ, d_src, e, d_hi, d_lo, d_inst_exp,
-                                                        d_inv_count, mean ? 1 : 0);
+      k_pool_planes_ident<256, 8><<<grid, 256, 0, s>>>(n_inst, S, d_row_of_occ, d_inverse, d_src, e, d_hi, d_lo,
+                                                        d_inst_exp, d_inv_count, mean ? 1 : 0);
     ::kp::count_launch();
     return;
   }

@@ -55,7 +55,8 @@ struct DedupWs {
 // d_occ_map (optional): per-occurrence map materialised in sorted order
 // (ws.d_sorted_mapped[p] = occ_map[sorted_vals[p]]), e.g. the bag of each occurrence.
 // d_occ_ident (optional, device word): 0xFFFFFFFF when occ_map is the identity
-// (one feature in every slot), which skips its random gather.
+// (one feature in every slot), which skips its random gather -- and the
+// d_sorted_mapped write: the caller then uses sorted_vals (equal).
 void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
            const uint32_t* d_occ_map = nullptr, const uint32_t* d_occ_ident = nullptr);
 // dedup() of keys made of runs [run_off[i], run_off[i+1]), each strictly
@@ -287,7 +288,11 @@ size_t split_cols_colsum_ws_floats(int B, int N);
 bool pool_planes_supported(uint32_t S, uint32_t e);
 void pool_planes(const uint32_t* d_bag_offs, uint32_t n_inst, uint32_t S, const uint32_t* d_row_of_occ,
                  const float* d_src, uint32_t e, bool mean, __half* d_hi, __half* d_lo, int* d_inst_exp,
-                 float* d_inv_count, cudaStream_t s, bool ident = false);
+                 float* d_inv_count, cudaStream_t s, bool ident = false,
+                 const uint32_t* d_inverse = nullptr);
+// (d_inverse set: d_row_of_occ is the unique -> row map, row of occurrence o
+// = d_row_of_occ[d_inverse[o]]; one feature per slot with planes_ident_kernel)
+bool planes_ident_kernel(uint32_t S, uint32_t e);
 // One feature per slot, pooling fused into the first layer (the forward GEMM
 // gathers the rows itself): only the per-instance exponents of the planes the
 // pooling kernel would write -- row_exp(max over the instance's S rows of

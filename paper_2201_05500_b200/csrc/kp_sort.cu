@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(ST) k_dedup_emit(const KT* __restrict__ sk,
       ++uid;
     }
     inverse[occ[r]] = uid - 1;
-    if (occ_map) sorted_mapped[i] = mp[r];  // e.g. bag of each sorted position
+    if (occ_map && !ident) sorted_mapped[i] = mp[r];  // e.g. bag of each sorted position (identity: = sv)
   }
   if (blockIdx.x == nb - 1 && threadIdx.x == 0) {
     const uint32_t U = bbase[blockIdx.x] + tot;
