@@ -190,6 +190,12 @@ struct kp_trainer {
     std::vector<float> x_bar, v_bar;
   };
   bool traj_on = false;
+  // sync-free single-GPU step: no dedup readback -- the pass
+  // plan and the one-feature-per-slot layout are predicted from the previous
+  // batch and checked on the device (kAbortPlan: the batch wrote nothing and
+  // is rerun with the readbacks)
+  bool async_step = false, force_sync = false, pred_ident = false;
+  bool sync_free = true;  // KP_SYNC_FREE=0 at trainer creation: every step reads back
   std::vector<TrajStep> traj;
   std::vector<float> traj_prev_vbar;  // frozen v_bar before the step (a3)
   // profiling
@@ -407,7 +413,8 @@ struct StepView {
 struct PullResult {
   const float* src;
   const uint32_t* idx;
-  uint32_t U;
+  uint32_t U;          // unique keys (an upper bound when dU is set)
+  const uint32_t* dU;  // U on the device (sync-free step), else null
 };
 
 // ---- NVLink peer windows ------------------------------------------------
@@ -635,30 +642,40 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   uint32_t* bag_offs = tr->bag_offs.get<uint32_t>(nb + 1);
   uint32_t* bag_of_occ = tr->bag_of_occ.get<uint32_t>(std::max<uint32_t>(sv.n_occ, 1));
   uint32_t* err = tr->err.get<uint32_t>(4);
-  prepare_bags(sv.offs, sv.occ_base, sv.slots, sv.n_inst, tr->S, bag_offs, bag_of_occ, err, s);
+  uint32_t* chk = static_cast<uint32_t*>(tr->check.p);
+  prepare_bags(sv.offs, sv.occ_base, sv.slots, sv.n_inst, tr->S, bag_offs, bag_of_occ, err, s,
+               tr->async_step ? chk : nullptr);
   // [0] first bad slot id, [1] all-ones iff every bag holds exactly its own
-  // occurrence (one feature per slot), read with dedup's one host sync
+  // occurrence (one feature per slot), read with dedup's one host sync --
+  // or, on the sync-free step, predicted and checked on the device
   uint32_t h_errw[2] = {0xFFFFFFFFu, 0};
-  KP_CUDA(cudaMemcpyAsync(h_errw, err, 8, cudaMemcpyDeviceToHost, s));
-  dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ, err + 1);  // synchronises the stream
-  if (sv.n_occ == 0) KP_CUDA(cudaStreamSynchronize(s));
+  const bool ran_async = tr->async_step &&
+                         dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ, err + 1, chk, tr->pred_ident ? 1 : 0);
+  if (!ran_async) {
+    KP_CUDA(cudaMemcpyAsync(h_errw, err, 8, cudaMemcpyDeviceToHost, s));
+    dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ, err + 1);  // synchronises the stream
+    if (sv.n_occ == 0) KP_CUDA(cudaStreamSynchronize(s));
+    tr->pred_ident = h_errw[1] == 0xFFFFFFFFu;
+  }
   const uint32_t h_err = h_errw[0];
-  const bool ident_bags = h_errw[1] == 0xFFFFFFFFu && sv.n_occ == nb;
+  const bool ident_word = ran_async ? tr->pred_ident : h_errw[1] == 0xFFFFFFFFu;
+  const bool ident_bags = ident_word && sv.n_occ == nb;
   // the identity occurrence -> bag map: the bag of sorted position p is the
   // sorted occurrence itself (dedup skipped writing the copy)
-  if (h_errw[1] == 0xFFFFFFFFu && sv.n_occ > 0)
-    tr->dd.d_sorted_mapped = const_cast<uint32_t*>(tr->dd.sorted_vals);
-  // reject bad slot ids before any state (table, weights) changes
+  if (ident_word && sv.n_occ > 0) tr->dd.d_sorted_mapped = const_cast<uint32_t*>(tr->dd.sorted_vals);
+  // reject bad slot ids before any state (table, weights) changes (the
+  // sync-free step: its state writes are guarded, the batch end raises)
   KP_CHECK(h_err == 0xFFFFFFFFu, kErrConfig,
            "slot ids must be < n_slots and non-decreasing within an instance (occurrence " +
                std::to_string(h_err) + ")");
   tr->mark(0);
-  const uint32_t U = tr->dd.n_unique;
+  const uint32_t U = ran_async ? sv.n_occ : tr->dd.n_unique;
   PullResult pr{};
   pr.U = U;
+  pr.dU = ran_async ? tr->dd.d_nunique : nullptr;
   if (tr->world == 1) {
     uint32_t* rows = tr->rows.get<uint32_t>(std::max<uint32_t>(U, 1));
-    table_pull(tr->tab.t, tr->dd.d_unique, U, rows, stamp, s);
+    table_pull(tr->tab.t, tr->dd.d_unique, U, rows, stamp, s, pr.dU);
     pr.src = tr->tab.t->d_w;
     pr.idx = rows;
     tr->mark(1);
@@ -742,7 +759,7 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   // pooling over the composed per-occurrence source rows (the one-feature
   // planes kernel composes on the fly: its index prefetch reads inverse, then
   // the unique's row)
-  tr->ga_on = tr->fused_pool && tr->planes && ident_bags && tr->e % 32 == 0 && sv.n_occ > 0;
+  tr->ga_on = tr->fused_pool && tr->planes && ident_bags && tr->e % 32 == 0 && sv.n_occ > 0 && !pr.dU;
   // (measured: pool 0.52 vs 0.48 ms against compose's 0.02 -- off; KP_POOL_COMPOSE=1)
   static const bool pool_compose = [] {
     const char* e = getenv("KP_POOL_COMPOSE");
@@ -836,7 +853,7 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
   tr->mark(-1);
   PullResult pr = pull_and_pool(tr, sv, false);
   if (tr->prof) {
-    tr->prof_unique += pr.U;
+    if (!pr.dU) tr->prof_unique += pr.U;  // (sync-free step: added at the batch-end readback)
     tr->prof_occ += sv.n_occ;
     if (tr->world > 1) {
       tr->prof_owner_unique += tr->dd_owner.n_unique;
@@ -971,7 +988,7 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
   // sparse push (x 1/N, trainer.cpp:202-207)
   if (tr->world == 1) {
     seg_reduce_apply(tr->dd.d_seg, pr.U, tr->dd.d_sorted_mapped, nullptr, sv.n_occ, dpooled, tr->e,
-                     inv_n, tr->tab.t, pr.idx, rule, nullptr, nullptr, tr->sg, s);
+                     inv_n, tr->tab.t, pr.idx, rule, nullptr, nullptr, tr->sg, s, nullptr, pr.dU);
     tr->mark(4);
   } else {
     if (!exchanged) {
@@ -1079,9 +1096,16 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
   uint32_t* err = tr->err.get<uint32_t>(4);
   KP_CUDA(cudaMemsetAsync(err, 0xFF, 4, s));
   KP_CUDA(cudaMemsetAsync(tr->check.get<uint32_t>(2), 0, 8, s));  // [0] flags [1] steps applied
-  // G > 1: every state-writing kernel of this batch (predict pass included)
-  // checks the peer-timeout bit (kAbortTimeout) of the check word first
-  AbortScope abort_guard(tr->world > 1 ? static_cast<const uint32_t*>(tr->check.p) : nullptr);
+  // the sync-free single-GPU step: one minibatch step per batch, no
+  // per-step host work that needs U (trajectory, gathered-A forward)
+  struct AsyncReset {
+    kp_trainer* t;
+    ~AsyncReset() { t->async_step = false; }
+  } async_reset{tr};
+  tr->async_step = tr->sync_free && !tr->force_sync && tr->world == 1 && n_mb == 1 && !tr->traj_on && !tr->fused_pool;
+  // G > 1 (and the sync-free step): every state-writing kernel of this batch
+  // (predict pass included) checks the abort bits of the check word first
+  AbortScope abort_guard(tr->world > 1 || tr->async_step ? static_cast<const uint32_t*>(tr->check.p) : nullptr);
   double* d_loss = tr->loss.get<double>(n_mb);
   KP_CUDA(cudaMemsetAsync(d_loss, 0, n_mb * 8, s));
 
@@ -1172,9 +1196,12 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
     run_step(tr, sv, d_loss + j, fused && j == 0 ? d_pred_keep : nullptr);
   }
   // error flags, loss, predictions
-  uint32_t h_err = 0, h_chkw[2] = {0, 0};
-  KP_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, s));
+  uint32_t h_errw2[2] = {0, 0}, h_chkw[2] = {0, 0}, h_nu = 0;
+  KP_CUDA(cudaMemcpyAsync(h_errw2, err, 8, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaMemcpyAsync(h_chkw, tr->check.p, 8, cudaMemcpyDeviceToHost, s));
+  if (tr->async_step && tr->dd.d_nunique)
+    KP_CUDA(cudaMemcpyAsync(&h_nu, tr->dd.d_nunique, 4, cudaMemcpyDeviceToHost, s));
+  const uint32_t& h_err = h_errw2[0];
   const uint32_t h_chk = h_chkw[0];
   std::vector<double> lsum(n_mb);
   KP_CUDA(cudaMemcpyAsync(lsum.data(), d_loss, n_mb * 8, cudaMemcpyDeviceToHost, s));
@@ -1183,6 +1210,32 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
   uint32_t h_sc[4] = {0, 0, 0, 0};  // table scalars ([2] = full flag), same readback
   KP_CUDA(cudaMemcpyAsync(h_sc, tr->tab.t->d_scalars, 16, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaStreamSynchronize(s));
+  if (tr->async_step) {
+    if (h_chkw[0] & kAbortPlan) {
+      // the device found the pass plan or the predicted layout wrong (or a
+      // bad slot id): nothing was written -- roll the host counters back and
+      // rerun the batch with the readbacks (or raise the slot error)
+      tr->marks.clear();
+      tr->ev_used = 0;
+      tr->t_global = steps_before;
+      tr->merges = merges_before;
+      tr->x_uniform = uniform_before;
+      tr->pred_ident = h_errw2[1] == 0xFFFFFFFFu;
+      KP_CHECK(h_err == 0xFFFFFFFFu, kErrConfig,
+               "slot ids must be < n_slots and non-decreasing within an instance (occurrence " +
+                   std::to_string(h_err) + ")");
+      tr->force_sync = true;
+      struct Unforce {
+        kp_trainer* t;
+        ~Unforce() { t->force_sync = false; }
+      } unforce{tr};
+      train_batch_impl(tr, h_offs, d_offs, d_keys, d_slots, d_labels, n, global_n, global_first, predict_first,
+                       h_preds, out);
+      return;
+    }
+    tr->pred_ident = h_errw2[1] == 0xFFFFFFFFu;
+    if (tr->prof) tr->prof_unique += h_nu;
+  }
   tr->harvest();
   if (tr->prof) tr->prof_steps += n_mb;
   KP_CHECK(h_err == 0xFFFFFFFFu, kErrConfig,
@@ -1790,6 +1843,8 @@ int kp_trainer_create(const kp_trainer_config* cfg, kp_comm* comm, int device, k
       // opt-in (KP_FUSED_POOL=1): measured slower, see DESIGN.md §4.3
       const char* e = getenv("KP_FUSED_POOL");
       tr->fused_pool = e && e[0] == '1';
+      const char* f = getenv("KP_SYNC_FREE");
+      tr->sync_free = !(f && f[0] == '0');
     }
     // (the backward's plane operands [B][hidden1] and W1^T [S*e][hidden1]
     // need 16-byte rows: hidden1 % 8 == 0)

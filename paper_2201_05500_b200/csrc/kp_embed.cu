@@ -31,7 +31,8 @@ unsigned grid_cap(uint64_t blocks) {
 __global__ void k_prepare_bags(const uint32_t* __restrict__ offs, uint32_t occ_base,
                                const uint16_t* __restrict__ slots, uint32_t n_inst, uint32_t S,
                                uint32_t* __restrict__ bag_offs, uint32_t* __restrict__ bag_of_occ,
-                               uint32_t* __restrict__ err) {
+                               uint32_t* __restrict__ err,
+                               uint32_t* __restrict__ abort_word) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -67,6 +68,7 @@ __global__ void k_prepare_bags(const uint32_t* __restrict__ offs, uint32_t occ_b
           const int prev = pv[k];
           if (s >= S || (int)s < prev) {
             atomicMin(err, o);
+            if (abort_word) atomicOr(abort_word, kAbortPlan);
             nonid = true;
             bag_of_occ[o] = i * S;  // keep downstream indexing in bounds; the batch is rejected
             continue;
@@ -770,7 +772,8 @@ __device__ __forceinline__ void sum_p(const float* P, uint64_t lo, uint64_t hi, 
 // chunk, binary search over the segment starts (a per-segment fill would put
 // a Zipf-hot key's thousands of chunks on one thread)
 __global__ void k_chunk_first(const uint32_t* __restrict__ seg, uint32_t U, uint32_t CH,
-                              uint32_t nchunks, uint32_t* __restrict__ first) {
+                              uint32_t nchunks, uint32_t* __restrict__ first, const uint32_t* __restrict__ dU) {
+  if (dU) U = *dU;  // (U on the device only: the sync-free step)
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += gridDim.x * blockDim.x) {
     const uint32_t p0 = c * CH;
     uint32_t lo = 0, hi = U;  // largest u with seg[u] <= p0
@@ -916,10 +919,10 @@ __global__ void k_gather_rows(const float* __restrict__ src, const uint32_t* __r
 
 void prepare_bags(const uint32_t* d_offs, uint32_t occ_base, const uint16_t* d_slots,
                   uint32_t n_inst, uint32_t S, uint32_t* d_bag_offs, uint32_t* d_bag_of_occ,
-                  uint32_t* d_err, cudaStream_t s) {
+                  uint32_t* d_err, cudaStream_t s, uint32_t* d_abort) {
   KP_CUDA(cudaMemsetAsync(d_err + 1, 0xFF, 4, s));
   k_prepare_bags<<<grid_cap(((uint64_t)n_inst * 32 + 255) / 256), 256, 0, s>>>(
-      d_offs, occ_base, d_slots, n_inst, S, d_bag_offs, d_bag_of_occ, d_err); ::kp::count_launch();
+      d_offs, occ_base, d_slots, n_inst, S, d_bag_offs, d_bag_of_occ, d_err, d_abort); ::kp::count_launch();
 }
 
 void compose(const uint32_t* d_idx, const uint32_t* d_inverse, uint32_t n, uint32_t* d_out,
@@ -1006,7 +1009,8 @@ void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* 
                       const uint32_t* d_bag_of_occ, uint32_t n_pos, const float* d_rows_src,
                       uint32_t e, float inv_n, Table* t, const uint32_t* d_table_rows,
                       const SparseRule& r, float* d_grad_out, const uint32_t* d_out_idx,
-                      SegWs& ws, cudaStream_t s, const PeerMap* pm) {
+                      SegWs& ws, cudaStream_t s, const PeerMap* pm,
+                      const uint32_t* d_nunique) {
   if (n_unique == 0 || n_pos == 0) return;
   SegArgs a;
   a.seg = d_seg;
@@ -1027,7 +1031,8 @@ void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* 
   const uint32_t nchunks = (n_pos + a.CH - 1) / a.CH;
   a.partials = ws.partials.get<float>((size_t)nchunks * 2 * e);
   uint32_t* first = ws.first.get<uint32_t>(nchunks);
-  k_chunk_first<<<grid_cap(((uint64_t)nchunks + 255) / 256), 256, 0, s>>>(d_seg, n_unique, a.CH, nchunks, first); ::kp::count_launch();
+  k_chunk_first<<<grid_cap(((uint64_t)nchunks + 255) / 256), 256, 0, s>>>(d_seg, n_unique, a.CH, nchunks, first,
+                                                                           d_nunique); ::kp::count_launch();
   a.first = first;
   a.apply = t != nullptr;
   a.peer = pm != nullptr;

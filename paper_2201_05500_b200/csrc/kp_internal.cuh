@@ -19,7 +19,12 @@ namespace kp {
 // before the wait (stream order makes k_wait's store visible to every later
 // kernel). g_abort is the word for the kernels launched on this host thread
 // (nullptr: no guard, single GPU); set it with AbortScope.
+// kAbortPlan: the single-GPU step ran without the dedup readback (pass plan
+// from the previous batch's key span, U on the device only) and the batch's
+// span outgrew the plan -- the same guard keeps every state write out and the
+// host reruns the batch with the exact plan.
 constexpr uint32_t kAbortTimeout = 16u;
+constexpr uint32_t kAbortPlan = 32u;
 // ledger categories (proj/include/kpsim/ledger.hpp TransferCategory)
 enum LedgerCat : int { kLedPull = 0, kLedPush = 1, kLedDense = 2, kLedSparse = 3, kLedCold = 4 };
 extern thread_local const uint32_t* g_abort;
@@ -28,7 +33,7 @@ struct AbortScope {
   ~AbortScope() { g_abort = nullptr; }
 };
 __device__ __forceinline__ bool aborted(const uint32_t* a) {
-  return a != nullptr && (*reinterpret_cast<const volatile uint32_t*>(a) & kAbortTimeout);
+  return a != nullptr && (*reinterpret_cast<const volatile uint32_t*>(a) & (kAbortTimeout | kAbortPlan));
 }
 
 // ------------------------------------------------------------- dedup ----
@@ -57,8 +62,17 @@ struct DedupWs {
 // d_occ_ident (optional, device word): 0xFFFFFFFF when occ_map is the identity
 // (one feature in every slot), which skips its random gather -- and the
 // d_sorted_mapped write: the caller then uses sorted_vals (equal).
-void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
-           const uint32_t* d_occ_map = nullptr, const uint32_t* d_occ_ident = nullptr);
+// d_abort (optional): no host sync when a pass plan exists (the previous
+// call's key span): U stays on the device (ws.n_unique = kUnknownU) and a
+// span that outgrows the plan sets kAbortPlan in *d_abort (the caller's
+// state writes are guarded by it and it reruns the batch); returns whether
+// it ran that way.
+constexpr uint32_t kUnknownU = 0xFFFFFFFFu;
+// expect_ident (0/1; -1 none): the caller's prediction of *d_occ_ident ==
+// all-ones, checked on the device the same way.
+bool dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
+           const uint32_t* d_occ_map = nullptr, const uint32_t* d_occ_ident = nullptr,
+           uint32_t* d_abort = nullptr, int expect_ident = -1);
 // dedup() of keys made of runs [run_off[i], run_off[i+1]), each strictly
 // ascending: merge tree instead of the radix sort, identical outputs
 void dedup_runs(const uint64_t* d_keys, uint32_t n, const std::vector<uint64_t>& run_off,
@@ -94,8 +108,9 @@ Table* table_create(int device, uint64_t capacity, uint32_t dim, int rule, float
                     float init_s1, float init_s2);
 void table_destroy(Table* t);
 // insert-if-absent; rows_out[i] = row of keys[i] (kNoRow if the table is full)
+// (d_n: the key count on the device, n its upper bound)
 void table_pull(Table* t, const uint64_t* d_keys, uint32_t n, uint32_t* d_rows_out,
-                bool stamp_epoch, cudaStream_t s);
+                bool stamp_epoch, cudaStream_t s, const uint32_t* d_n = nullptr);
 // lookup only; kNoRow when absent
 void table_lookup(const Table* t, const uint64_t* d_keys, uint32_t n, uint32_t* d_rows_out,
                   cudaStream_t s);
@@ -116,9 +131,11 @@ void table_gather(const Table* t, const uint32_t* d_rows, uint32_t n, float* d_w
 // bags: CSR over occurrences; bag b = instance*S + slot. d_err[0]: first bad
 // occurrence (caller presets 0xFFFFFFFF); d_err[1]: 0xFFFFFFFF iff
 // bag_of_occ[o] == o for every occurrence (set here).
+// (d_abort: a bad slot id also sets kAbortPlan there -- the sync-free step
+// keeps its state writes out and raises at the batch-end readback)
 void prepare_bags(const uint32_t* d_offs, uint32_t occ_base, const uint16_t* d_slots,
                   uint32_t n_inst, uint32_t S, uint32_t* d_bag_offs, uint32_t* d_bag_of_occ,
-                  uint32_t* d_err, cudaStream_t s);
+                  uint32_t* d_err, cudaStream_t s, uint32_t* d_abort = nullptr);
 // row_of_occ[o] = idx[inverse[o]]  (source row of every occurrence)
 void compose(const uint32_t* d_idx, const uint32_t* d_inverse, uint32_t n, uint32_t* d_out,
              cudaStream_t s);
@@ -183,11 +200,13 @@ struct SparseRule {
 // already in sorted order). Output: apply the rule to table row
 // table_rows[u] (fused push) when `t` is set, else store to grad_out[out_idx[u]]
 // -- or, with `pm`, to peer_dst(pm, out_idx[u]) in the owners' windows.
+// d_nunique: U on the device (n_unique is then only an upper bound).
 void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* d_sorted_vals,
                       const uint32_t* d_bag_of_occ, uint32_t n_pos, const float* d_rows_src,
                       uint32_t e, float inv_n, Table* t, const uint32_t* d_table_rows,
                       const SparseRule& r, float* d_grad_out, const uint32_t* d_out_idx,
-                      SegWs& ws, cudaStream_t s, const PeerMap* pm = nullptr);
+                      SegWs& ws, cudaStream_t s, const PeerMap* pm = nullptr,
+                      const uint32_t* d_nunique = nullptr);
 void gather_rows(const float* d_src, const uint32_t* d_idx, uint32_t n, uint32_t e, float* d_out,
                  cudaStream_t s);
 

@@ -689,8 +689,25 @@ static bool spec_enabled() {
   return on;
 }
 
-void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
-           const uint32_t* d_occ_map, const uint32_t* d_occ_ident) {
+// the batch's key span against the planned passes' (a miss aborts the step)
+__global__ void k_plan_check(const unsigned long long* __restrict__ mm, int planned, uint32_t* abort_word,
+                             const uint32_t* __restrict__ ident_word, int expect_ident) {
+  if (expect_ident >= 0 && (*ident_word == 0xFFFFFFFFu) != (expect_ident != 0)) atomicOr(abort_word, kAbortPlan);
+  const uint64_t span = mm[1] - mm[0];
+  const int bits = span == 0 ? 0 : 64 - __clzll((long long)span);
+  bool ok;
+  if (planned > 32) ok = ((planned + 7) / 8) * 8 >= bits;
+  else if (bits > 32) ok = false;
+  else {
+    const int np = planned == 0 ? 1 : (planned + 8) / 9;
+    const int db = planned == 0 ? 1 : (planned + np - 1) / np;
+    ok = np * db >= bits;
+  }
+  if (!ok) atomicOr(abort_word, kAbortPlan);
+}
+
+bool dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
+           const uint32_t* d_occ_map, const uint32_t* d_occ_ident, uint32_t* d_abort, int expect_ident) {
   ws.n = n;
   ws.d_nunique = ws.scalars.get<uint32_t>(4);
   if (n == 0) {
@@ -700,12 +717,21 @@ void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
     ws.d_seg = ws.seg.get<uint32_t>(1);
     KP_CUDA(cudaMemsetAsync(ws.d_seg, 0, 4, s));
     KP_CUDA(cudaMemsetAsync(ws.d_nunique, 0, 4, s));
-    return;
+    return false;
   }
   const uint32_t nb = ceil_div(n, TILE);
   auto* mm = ws.minmax.get<unsigned long long>(2);
   k_minmax_init<<<1, 1, 0, s>>>(mm); ::kp::count_launch();
   k_minmax<<<min(nb * 2, 1184u), 256, 0, s>>>(d_keys, n, mm); ::kp::count_launch();
+  if (spec_enabled() && ws.spec_bits >= 0 && d_abort) {
+    // no readback at all: the plan is checked on the device
+    const int planned = ws.spec_bits;
+    dedup_sort(d_keys, n, ws, s, d_occ_map, d_occ_ident, planned, mm, nb);
+    k_plan_check<<<1, 1, 0, s>>>(mm, planned, d_abort, d_occ_ident, d_occ_ident ? expect_ident : -1);
+    ::kp::count_launch();
+    ws.n_unique = kUnknownU;
+    return true;
+  }
   if (spec_enabled() && ws.spec_bits >= 0) {
     // Plan the passes from the previous call's key span and check it with
     // the final readback (one host sync per dedup instead of two); a batch
@@ -718,11 +744,11 @@ void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
     KP_CUDA(cudaStreamSynchronize(s));
     const int bits = span_bits(h_mm);
     ws.spec_bits = bits;
-    if (plan_covers(planned, bits)) return;
+    if (plan_covers(planned, bits)) return false;
     dedup_sort(d_keys, n, ws, s, d_occ_map, d_occ_ident, bits, mm, nb);
     KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
     KP_CUDA(cudaStreamSynchronize(s));
-    return;
+    return false;
   }
   unsigned long long h_mm[2];
   KP_CUDA(cudaMemcpyAsync(h_mm, mm, 16, cudaMemcpyDeviceToHost, s));
@@ -732,6 +758,7 @@ void dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
   dedup_sort(d_keys, n, ws, s, d_occ_map, d_occ_ident, bits, mm, nb);
   KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaStreamSynchronize(s));
+  return false;
 }
 
 // Same outputs as dedup() when the keys are R runs that are each strictly

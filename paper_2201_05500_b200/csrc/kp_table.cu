@@ -119,8 +119,15 @@ __device__ uint32_t probe(const TView& t, uint64_t key, int gl, uint32_t gmask, 
 
 template <bool INSERT>
 __global__ void k_probe(TView t, const uint64_t* __restrict__ keys, uint32_t n,
-                        uint32_t* __restrict__ rows_out, uint32_t epoch) {
-  if (INSERT && aborted(t.abort)) return;  // no inserts after a peer timeout
+                        uint32_t* __restrict__ rows_out, uint32_t epoch, const uint32_t* __restrict__ d_n) {
+  if (d_n) n = min(n, *d_n);
+  if (INSERT && aborted(t.abort)) {
+    // no inserts after a peer timeout / plan miss -- but defined outputs: the
+    // rest of the (discarded) step still indexes rows with them
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+      rows_out[i] = kNoRow;
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int gl = lane & (GS - 1), gbase = lane & GS;
   const uint32_t gmask = 0xFFFFu << gbase;
@@ -282,16 +289,19 @@ void table_destroy(Table* t) {
 }
 
 void table_pull(Table* t, const uint64_t* d_keys, uint32_t n, uint32_t* d_rows_out,
-                bool stamp_epoch, cudaStream_t s) {
+                bool stamp_epoch, cudaStream_t s, const uint32_t* d_n) {
   if (n == 0) return;
-  k_probe<true><<<grid_for((uint64_t)n * GS, 256), 256, 0, s>>>(view(t), d_keys, n, d_rows_out,
-                                                                 stamp_epoch ? t->epoch : 0); ::kp::count_launch();
+  // (a device count: n is an upper bound -- the occurrences; U is ~1/6 of it
+  // at configs[1], the grid is sized for that and strides)
+  const uint64_t work = d_n ? std::max<uint64_t>(n / 4, 1) : n;
+  k_probe<true><<<grid_for(work * GS, 256), 256, 0, s>>>(view(t), d_keys, n, d_rows_out,
+                                                          stamp_epoch ? t->epoch : 0, d_n); ::kp::count_launch();
 }
 
 void table_lookup(const Table* t, const uint64_t* d_keys, uint32_t n, uint32_t* d_rows_out,
                   cudaStream_t s) {
   if (n == 0) return;
-  k_probe<false><<<grid_for((uint64_t)n * GS, 256), 256, 0, s>>>(view(t), d_keys, n, d_rows_out, 0); ::kp::count_launch();
+  k_probe<false><<<grid_for((uint64_t)n * GS, 256), 256, 0, s>>>(view(t), d_keys, n, d_rows_out, 0, nullptr); ::kp::count_launch();
 }
 
 uint64_t table_size(const Table* t, cudaStream_t s) {

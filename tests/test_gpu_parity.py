@@ -676,3 +676,69 @@ def test_fused_pool_gather_bitwise(kp, monkeypatch, B, S, e, pool, workers, hidd
     assert np.array_equal(w1, w0)
     assert np.array_equal(a1, a0)
     assert np.array_equal(x1, x0)
+
+
+def _train_n(kp, monkeypatch, sync_free, batches, S=8, e=16, hidden=(32, 16), B=None):
+    monkeypatch.setenv("KP_SYNC_FREE", sync_free)  # read at trainer creation
+    cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=B or len(batches[0].labels), embedding_dim=e,
+                       n_slots=S, hidden=hidden, pooling="sum", activation="relu", alpha=0.02, sparse_lr=0.1)
+    tr = kp.Trainer(table_capacity=1 << 18, **trainer_kwargs(vars(cfg)))
+    losses = []
+    for bt in batches:
+        r = tr.train_batch(bt.offs, bt.keys, bt.labels, slots=bt.slots, predict_first=True)
+        losses.append((r["loss"], np.asarray(r["preds"]).copy()))
+    return tr, losses
+
+
+def test_sync_free_step_replans_bitwise(kp, monkeypatch):
+    """The single-GPU step without the dedup readback (pass plan and the
+    one-feature-per-slot layout predicted from the previous batch, checked on
+    the device): a batch whose key span outgrows the plan (1e3 -> 1e12 keys),
+    one that switches to multi-hot bags (the layout prediction fails) and
+    back are rerun with the readbacks -- every result and every trained bit
+    equals the always-readback trainer (KP_SYNC_FREE=0)."""
+    def mk(V, seed, multi=False):
+        bt = make_batch(512, V=V, zipf_s=1.1, n_slots=8, seed=seed)
+        if multi:  # two features in every slot
+            bt.keys = np.repeat(bt.keys, 2)
+            bt.slots = np.repeat(bt.slots, 2)
+            bt.offs = (bt.offs.astype(np.int64) * 2).astype(bt.offs.dtype)
+        return bt
+    batches = [mk(10**3, 1), mk(10**3, 2), mk(10**12, 3), mk(10**12, 4, multi=True), mk(10**4, 5),
+               mk(10**4, 6)]
+    t1, r1 = _train_n(kp, monkeypatch, "1", batches)
+    t0, r0 = _train_n(kp, monkeypatch, "0", batches)
+    for (l1, p1), (l0, p0) in zip(r1, r0):
+        assert l1 == l0
+        assert np.array_equal(p1, p0)
+    k1, w1, a1, _ = t1.table()
+    k0, w0, a0, _ = t0.table()
+    assert np.array_equal(k1, k0) and np.array_equal(w1, w0) and np.array_equal(a1, a0)
+    assert np.array_equal(t1.worker_state(0)["x"], t0.worker_state(0)["x"])
+
+
+def test_sync_free_step_bad_slot_writes_nothing(kp, monkeypatch):
+    """A bad slot id on a sync-free step is found after the fact (no readback
+    before the state writes): the guarded kernels wrote nothing, the call
+    raises ConfigError, and training continues exactly like the trainer that
+    never saw the bad batch."""
+    good = [make_batch(512, V=10**5, zipf_s=1.1, n_slots=8, seed=20 + i) for i in range(3)]
+    bad = make_batch(512, V=10**5, zipf_s=1.1, n_slots=8, seed=30)
+    bad.slots = bad.slots.copy()
+    bad.slots[100] = 9  # >= n_slots
+    monkeypatch.setenv("KP_SYNC_FREE", "1")
+    cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=512, embedding_dim=16, n_slots=8, hidden=(32, 16),
+                       pooling="sum", activation="relu", alpha=0.02, sparse_lr=0.1)
+    ta = kp.Trainer(table_capacity=1 << 18, **trainer_kwargs(vars(cfg)))
+    tb = kp.Trainer(table_capacity=1 << 18, **trainer_kwargs(vars(cfg)))
+    ra = [ta.train_batch(good[0].offs, good[0].keys, good[0].labels, slots=good[0].slots)["loss"]]
+    ra.append(ta.train_batch(good[1].offs, good[1].keys, good[1].labels, slots=good[1].slots)["loss"])
+    with pytest.raises(ValueError):
+        ta.train_batch(bad.offs, bad.keys, bad.labels, slots=bad.slots)
+    ra.append(ta.train_batch(good[2].offs, good[2].keys, good[2].labels, slots=good[2].slots)["loss"])
+    rb = [tb.train_batch(g.offs, g.keys, g.labels, slots=g.slots)["loss"] for g in good]
+    assert ra == rb
+    ka, wa, aa, _ = ta.table()
+    kb, wb, ab, _ = tb.table()
+    assert np.array_equal(ka, kb) and np.array_equal(wa, wb) and np.array_equal(aa, ab)
+    assert np.array_equal(ta.worker_state(0)["x"], tb.worker_state(0)["x"])
