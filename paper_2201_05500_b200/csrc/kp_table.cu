@@ -13,7 +13,10 @@ namespace {
 
 constexpr uint32_t kPending = 0xFFFFFFFEu;
 constexpr uint32_t kFullRow = 0xFFFFFFFDu;  // slot claimed but the table had no free row
-constexpr int GS = 16;  // lanes per probing group = slots per bucket
+// lanes per probing group = slots per bucket line: lane i reads slot i's key
+// and row (two independent loads of the same 128-byte line), four keys per
+// warp in flight
+constexpr int GS = kSlotsPerLine;
 
 __device__ __forceinline__ void init_row(const TView& t, uint32_t row, int gl) {
   const uint64_t o = (uint64_t)row * t.dim;
@@ -59,23 +62,20 @@ __device__ uint32_t probe(const TView& t, uint64_t key, int gl, uint32_t gmask, 
   }
   uint64_t b = mix64(key) & t.bmask;
   uint64_t probes = 0;
-  const bool klane = gl < kSlotsPerLine;  // lanes 0-7 read the line's keys, 8-15 its rows
   for (;;) {
-    uint64_t k = 0;
-    uint32_t rv = 0;
-    if (klane) k = *(volatile uint64_t*)line_key(t.lines, b, gl);
-    else rv = *(volatile uint32_t*)line_row(t.lines, b, gl - kSlotsPerLine);
-    const uint32_t match = (__ballot_sync(gmask, klane && k == key) >> gbase) & 0xFFu;
+    const uint64_t k = *(volatile uint64_t*)line_key(t.lines, b, gl);
+    const uint32_t rv = *(volatile uint32_t*)line_row(t.lines, b, gl);
+    const uint32_t match = (__ballot_sync(gmask, k == key) >> gbase) & 0xFFu;
     if (match) {
       const int i = __ffs(match) - 1;
-      uint32_t r = __shfl_sync(gmask, rv, gbase + kSlotsPerLine + i);
+      uint32_t r = __shfl_sync(gmask, rv, gbase + i);
       if (r == kNoRow && INSERT) {  // inserter in flight (same key, same launch)
         volatile uint32_t* rp = line_row(t.lines, b, i);
         while (r == kNoRow) r = *rp;
       }
       return r >= kFullRow ? kNoRow : r;
     }
-    const uint32_t empty = (__ballot_sync(gmask, klane && k == kEmptyKey) >> gbase) & 0xFFu;
+    const uint32_t empty = (__ballot_sync(gmask, k == kEmptyKey) >> gbase) & 0xFFu;
     if (empty) {
       if (!INSERT) return kNoRow;
       const int el = __ffs(empty) - 1;
@@ -129,8 +129,8 @@ __global__ void k_probe(TView t, const uint64_t* __restrict__ keys, uint32_t n,
     return;
   }
   const int lane = threadIdx.x & 31;
-  const int gl = lane & (GS - 1), gbase = lane & GS;
-  const uint32_t gmask = 0xFFFFu << gbase;
+  const int gl = lane & (GS - 1), gbase = lane & ~(GS - 1);
+  const uint32_t gmask = ((1u << GS) - 1u) << gbase;
   const uint64_t g0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / GS;
   const uint64_t ng = (uint64_t)gridDim.x * blockDim.x / GS;
   // (two keys' lines in flight per group measured slower: 108 vs 95 us)
