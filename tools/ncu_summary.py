@@ -20,11 +20,11 @@ import sys
 # kernel -> bench.py stage (kp_capi.cu profile marks)
 STAGE = [
     (r"k_prepare_bags|k_minmax|k_upsweep|k_scan_rows|k_downsweep|k_head_count|k_dedup_emit"
-     r"|k_key_range|k_owner", "dedup"),
+     r"|k_key_range|k_owner|k_plan_check", "dedup"),
     (r"k_probe|k_insert|k_gather_rows", "pull"),
-    (r"k_compose|k_pool", "pool"),
+    (r"k_compose|k_pool|k_unique_maxabs|k_inst_exp", "pool"),
     (r"k_split|k_tc_gemm|k_gemm|k_h3|k_colmax|k_head_|k_loss|k_colsum|k_reduce_splits|k_reduce_chunks"
-     r"|k_transpose|k_rowmax", "mlp"),
+     r"|k_transpose|k_rowmax|k_sum_parts", "mlp"),
     (r"k_seg_|k_chunk_first", "push"),
     (r"k_moments|k_cmean|k_terms|k_check|k_local_step|k_merge", "dense"),
 ]
