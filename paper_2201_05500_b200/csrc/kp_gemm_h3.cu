@@ -67,10 +67,9 @@ constexpr uint32_t H3_EPI = 16 * H3_EPIB * 32 * H3_EB * 4;  // per epilogue warp
 constexpr int H3_REG_LO = 64, H3_REG_HI = 104;  // 128*64 + 512*104 <= 640*96 (the CTA pool)
 constexpr uint32_t H3_COLP = 16 * 2 * 64 * 4;  // per epilogue warp: 64 column scales + 64 biases
 constexpr uint32_t H3_SMEM = H3_NS * H3_STAGE + H3_EPI + H3_COLP + 1024 + 256;
-// Tile width BN: 256 (2 TMEM accumulators) or 128 (4 accumulators: the MMA
-// may run 3 tiles ahead of the epilogue -- for short-K, wide-N products like
-// dX, K = 256, whose per-tile epilogue is as long as its MMAs). Each CTA holds
-// BN/2 rows of B.
+// Tile width BN = 256 (2 TMEM accumulators; each CTA holds BN/2 rows of B).
+// (A 128-wide variant with 4 accumulators in flight measured slower for dX,
+// 702 vs 556 us, and was dropped.)
 // GA (gathered A): A's rows are fetched as fp32 by TMA gather4 from a row
 // table (one feature per slot: A[m][slot*e + j] = src[rowocc[m*S + slot]][j]),
 // into NG staging slots, and split into the A planes on chip by warps 2-3.
@@ -89,8 +88,7 @@ struct H3Cfg {
   static constexpr uint32_t GEXP = GA ? H3_BM * 4 : 0;  // the tile rows' exponents
   static constexpr uint32_t SMEM = NS * STAGE + EPI + H3_COLP + NG * GSLOT + GEXP + 1024 + 256;
 };
-static_assert(H3Cfg<128>::SMEM <= 232448 && H3Cfg<256>::SMEM <= 232448 && H3Cfg<256, true>::SMEM <= 232448,
-              "h3 smem");
+static_assert(H3Cfg<256>::SMEM <= 232448 && H3Cfg<256, true>::SMEM <= 232448, "h3 smem");
 // stream-K virtual units (the partition depends only on the problem shape,
 // not on the grid): 148, or fewer so that each owns >= 8 k-blocks
 constexpr int H3_VUNITS = 148;
@@ -226,7 +224,7 @@ __device__ __forceinline__ uint64_t plane_desc(uint32_t base, int kk) {
   return MN ? sdesc_mn128(base + (uint32_t)kk * 2048u, 4096u) : sdesc_k64(base + (uint32_t)kk * 32u);
 }
 
-template <bool AMN, bool BMN, bool SK, int BN, bool GA>
+template <bool AMN, bool BMN, bool SK, int BN, bool GA, int EM>
 __global__ void __launch_bounds__(H3_WARPS * 32, 1)
     k_h3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
          const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
@@ -494,11 +492,15 @@ __global__ void __launch_bounds__(H3_WARPS * 32, 1)
       for (int h = 0; h < CW / 32; ++h) {
         const int nn = min(ncol0 + lane + 32 * h, a.N - 1);
         csb[lane + 32 * h] = a.eb ? pow2f(-__ldg(a.eb + nn)) : 1.f;
-        csb[64 + lane + 32 * h] = a.mode == 1 ? __ldg(a.bias + nn) : 0.f;
+        csb[64 + lane + 32 * h] = EM == 1 ? __ldg(a.bias + nn) : 0.f;
       }
       const int m = mrow0 + lane;
       const float sa = (a.ea && m < a.M) ? pow2f(-__ldg(a.ea + m)) : 1.f;
-      const int mode = partial ? 0 : a.mode;  // partial tiles: plain scaled sums (the fix-up applies the op)
+      // the epilogue op is a template parameter (EM): one op's code per kernel
+      // keeps the unrolled epilogue small (the runtime-selected version with
+      // every op inlined 64-wide measured instruction-fetch stalls on top);
+      // partial tiles: plain scaled sums (the fix-up applies the op)
+      const int mode = partial ? 0 : EM;
       float acc[CW];
 #pragma unroll
       for (int j = 0; j < CW; ++j) acc[j] = 0.f;
@@ -685,21 +687,39 @@ bool map_rows(CUtensorMap* m, const float* p, uint64_t nrows, uint32_t e) {
 
 thread_local int g_h3_reserve = 0;
 
-template <bool AMN, bool BMN, bool SK, int BN, bool GA = false>
+template <bool AMN, bool BMN, bool SK, int BN, bool GA, int EM>
 void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, float* ws,
-                 const H3Args& a0, cudaStream_t s, int split, const H3Gather* ga = nullptr);
+                 const H3Args& a0, cudaStream_t s, int split, const H3Gather* ga);
+// one kernel per epilogue op (EM): the ops each operand layout uses -- the
+// forward's bias + activation and the input gradient's mean-pool coefficient
+// on K-major operands, plain stores everywhere
+template <bool AMN, bool BMN, bool SK, bool GA>
+void launch_em(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, float* ws,
+               const H3Args& a, cudaStream_t s, int split, const H3Gather* ga) {
+  if (a.mode == 1) {
+    if constexpr (!AMN && !BMN) {
+      launch_h3_t<AMN, BMN, SK, 256, GA, 1>(A, B, M, N, K, C, ldc, ws, a, s, split, ga);
+      return;
+    }
+  } else if (a.mode == 3) {
+    if constexpr (!AMN && !BMN && !SK && !GA) {
+      launch_h3_t<AMN, BMN, SK, 256, GA, 3>(A, B, M, N, K, C, ldc, ws, a, s, split, ga);
+      return;
+    }
+  } else if (a.mode == 0) {
+    if constexpr (!GA) {
+      launch_h3_t<AMN, BMN, SK, 256, GA, 0>(A, B, M, N, K, C, ldc, ws, a, s, split, ga);
+      return;
+    }
+  }
+  KP_CHECK(false, kErrGeneric, "h3_gemm: epilogue op not built for this operand layout");
+}
+
 // stream-K and data-parallel variants are separate kernels (no 64-bit
-// stream-K state in the data-parallel ones); KP_H3_BN=128 selects 128-wide
-// tiles (4 accumulators in flight) for the data-parallel ones
+// stream-K state in the data-parallel ones)
 template <bool AMN, bool BMN>
 void launch_h3(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, int splitk,
                float* ws, const H3Args& a, cudaStream_t s, const H3Gather* ga = nullptr) {
-  static const int bn_env = [] {
-    const char* e = getenv("KP_H3_BN");
-    return e ? atoi(e) : 0;
-  }();
-  // (128-wide tiles for dX measured slower: 702 vs 556 us -- opt-in only)
-  const bool narrow = bn_env == 128;
   static const bool hybrid = [] {
     const char* e = getenv("KP_H3_HYBRID");
     return !(e && e[0] == '0');
@@ -712,20 +732,19 @@ void launch_h3(const H3Operand& A, const H3Operand& B, int M, int N, int K, floa
     // than the balance gains; at configs[1] the split measured -5 us in situ)
     if (tiles % (H3_VUNITS / 2) == 0 || tiles < H3_VUNITS / 2 || !hybrid) splitk = 0;
   }
-  if constexpr (!AMN) {
+  if constexpr (!AMN && !BMN) {
     if (ga) {
-      if (splitk) launch_h3_t<false, BMN, true, 256, true>(A, B, M, N, K, C, ldc, ws, a, s, splitk, ga);
-      else launch_h3_t<false, BMN, false, 256, true>(A, B, M, N, K, C, ldc, ws, a, s, 0, ga);
+      if (splitk) launch_em<false, false, true, true>(A, B, M, N, K, C, ldc, ws, a, s, splitk, ga);
+      else launch_em<false, false, false, true>(A, B, M, N, K, C, ldc, ws, a, s, 0, ga);
       return;
     }
   }
   KP_CHECK(!ga, kErrGeneric, "h3_gemm: gathered A must be K-major");
-  if (splitk) launch_h3_t<AMN, BMN, true, 256>(A, B, M, N, K, C, ldc, ws, a, s, splitk);
-  else if (narrow) launch_h3_t<AMN, BMN, false, 128>(A, B, M, N, K, C, ldc, ws, a, s, 0);
-  else launch_h3_t<AMN, BMN, false, 256>(A, B, M, N, K, C, ldc, ws, a, s, 0);
+  if (splitk) launch_em<AMN, BMN, true, false>(A, B, M, N, K, C, ldc, ws, a, s, splitk, nullptr);
+  else launch_em<AMN, BMN, false, false>(A, B, M, N, K, C, ldc, ws, a, s, 0, nullptr);
 }
 
-template <bool AMN, bool BMN, bool SK, int BN, bool GA>
+template <bool AMN, bool BMN, bool SK, int BN, bool GA, int EM>
 int h3_units() {
   static int units = 0;
   if (units) return units;
@@ -745,13 +764,13 @@ int h3_units() {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_h3<AMN, BMN, SK, BN, GA>, &cfg) == cudaSuccess && n > 0)
+  if (cudaOccupancyMaxActiveClusters(&n, k_h3<AMN, BMN, SK, BN, GA, EM>, &cfg) == cudaSuccess && n > 0)
     units = std::min(units, n);
   cudaGetLastError();
   return units;
 }
 
-template <bool AMN, bool BMN, bool SK, int BN, bool GA>
+template <bool AMN, bool BMN, bool SK, int BN, bool GA, int EM>
 void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, float* C, int ldc, float* ws,
                  const H3Args& a0, cudaStream_t s, int split, const H3Gather* ga) {
   static_assert(!SK || BN == 256, "stream-K partial tiles are 256 wide");
@@ -812,10 +831,10 @@ void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, fl
   KP_CUDA(cudaGetDevice(&dev));
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr.load(std::memory_order_acquire) & bit)) {
-    KP_CUDA(cudaFuncSetAttribute(k_h3<AMN, BMN, SK, BN, GA>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    KP_CUDA(cudaFuncSetAttribute(k_h3<AMN, BMN, SK, BN, GA, EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     attr.fetch_or(bit, std::memory_order_release);
   }
-  const int units_all = std::max(1, h3_units<AMN, BMN, SK, BN, GA>() - (g_h3_reserve + 1) / 2);
+  const int units_all = std::max(1, h3_units<AMN, BMN, SK, BN, GA, EM>() - (g_h3_reserve + 1) / 2);
   const int work = splitk ? std::max(a.vunits, a.tiles_dp > 0 ? H3_VUNITS / 2 : 0) : tiles;
   const unsigned grid = (unsigned)std::min(work, units_all) * 2;
   cudaLaunchConfig_t cfg = {};
@@ -830,7 +849,7 @@ void launch_h3_t(const H3Operand& A, const H3Operand& B, int M, int N, int K, fl
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  KP_CUDA(cudaLaunchKernelEx(&cfg, k_h3<AMN, BMN, SK, BN, GA>, tah, tal, tbh, tbl, tcm, tpm, tgm, a));
+  KP_CUDA(cudaLaunchKernelEx(&cfg, k_h3<AMN, BMN, SK, BN, GA, EM>, tah, tal, tbh, tbl, tcm, tpm, tgm, a));
   ::kp::count_launch();
   if (splitk && tail > 0) {
     k_h3_fixup<<<dim3(64, tail), 256, 0, s>>>(ws, a.nblocks_n, a.nk, a.tiles_dp, T, a.vunits, M, N, C, ldc,
@@ -1037,10 +1056,9 @@ void h3_gemm(const H3Operand& A, bool a_mn, const H3Operand& B, bool b_mn, int M
   KP_CHECK(ep.mode == 0 || ep.mode == 1 || ep.mode == 3, kErrGeneric, "h3_gemm: unsupported epilogue");
   KP_CHECK(splitk == 0 || ep.mode != 3, kErrGeneric, "h3_gemm: stream-K fix-up has no coefficient epilogue");
   KP_CHECK(!ga || !a_mn, kErrGeneric, "h3_gemm: gathered A is K-major");
-  if (!a_mn && !b_mn) launch_h3<false, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s, ga);
-  else if (a_mn && b_mn) launch_h3<true, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
-  else if (a_mn) launch_h3<true, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
-  else launch_h3<false, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s, ga);
+  KP_CHECK(a_mn == b_mn, kErrGeneric, "h3_gemm: both operands K-major or both MN-major");
+  if (!a_mn) launch_h3<false, false>(A, B, M, N, K, C, ldc, splitk, ws, a, s, ga);
+  else launch_h3<true, true>(A, B, M, N, K, C, ldc, splitk, ws, a, s);
 }
 
 size_t split_cols_colsum_ws_floats(int B, int N) {
