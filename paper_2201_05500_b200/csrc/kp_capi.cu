@@ -643,8 +643,14 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   uint32_t* bag_of_occ = tr->bag_of_occ.get<uint32_t>(std::max<uint32_t>(sv.n_occ, 1));
   uint32_t* err = tr->err.get<uint32_t>(4);
   uint32_t* chk = static_cast<uint32_t*>(tr->check.p);
+  // (sync-free, predicted one feature per slot on the planes path: the bag
+  // maps are the identity and unread -- only the checks run; the device
+  // check of the prediction aborts the step otherwise)
+  const bool skip_maps = tr->async_step && tr->pred_ident && tr->planes && sv.n_occ == nb &&
+                         planes_ident_kernel(tr->S, tr->e) && !tr->fused_pool &&
+                         dedup_async_ready(tr->dd, sv.n_occ);
   prepare_bags(sv.offs, sv.occ_base, sv.slots, sv.n_inst, tr->S, bag_offs, bag_of_occ, err, s,
-               tr->async_step ? chk : nullptr);
+               tr->async_step ? chk : nullptr, !skip_maps);
   // [0] first bad slot id, [1] all-ones iff every bag holds exactly its own
   // occurrence (one feature per slot), read with dedup's one host sync --
   // or, on the sync-free step, predicted and checked on the device

@@ -32,7 +32,9 @@ __global__ void k_prepare_bags(const uint32_t* __restrict__ offs, uint32_t occ_b
                                const uint16_t* __restrict__ slots, uint32_t n_inst, uint32_t S,
                                uint32_t* __restrict__ bag_offs, uint32_t* __restrict__ bag_of_occ,
                                uint32_t* __restrict__ err,
-                               uint32_t* __restrict__ abort_word) {
+                               uint32_t* __restrict__ abort_word, int maps) {
+  // (maps == 0: only the checks -- the caller predicted one feature per slot,
+  // whose maps are the identity and go unread; a miss aborts the step)
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -47,7 +49,9 @@ __global__ void k_prepare_bags(const uint32_t* __restrict__ offs, uint32_t occ_b
       }
     } else {
       if (o0 == o1) {
-        for (uint32_t s = lane; s < S; s += 32) bag_offs[(uint64_t)i * S + s] = o0;
+        if (maps)
+          for (uint32_t s = lane; s < S; s += 32) bag_offs[(uint64_t)i * S + s] = o0;
+        nonid = true;  // an empty instance: not one feature in every slot
         continue;
       }
       for (uint32_t ob = o0; ob < o1; ob += 128) {
@@ -70,19 +74,21 @@ __global__ void k_prepare_bags(const uint32_t* __restrict__ offs, uint32_t occ_b
             atomicMin(err, o);
             if (abort_word) atomicOr(abort_word, kAbortPlan);
             nonid = true;
-            bag_of_occ[o] = i * S;  // keep downstream indexing in bounds; the batch is rejected
+            if (maps) bag_of_occ[o] = i * S;  // keep downstream indexing in bounds; the batch is rejected
             continue;
           }
-          for (int t = prev + 1; t <= (int)s; ++t) bag_offs[(uint64_t)i * S + t] = o;
-          if (o == o1 - 1)
-            for (uint32_t t = s + 1; t < S; ++t) bag_offs[(uint64_t)i * S + t] = o1;
-          bag_of_occ[o] = i * S + s;
+          if (maps) {
+            for (int t = prev + 1; t <= (int)s; ++t) bag_offs[(uint64_t)i * S + t] = o;
+            if (o == o1 - 1)
+              for (uint32_t t = s + 1; t < S; ++t) bag_offs[(uint64_t)i * S + t] = o1;
+            bag_of_occ[o] = i * S + s;
+          }
           nonid |= o != i * S + s;
         }
       }
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) bag_offs[(uint64_t)n_inst * S] = offs[n_inst] - occ_base;
+  if (maps && blockIdx.x == 0 && threadIdx.x == 0) bag_offs[(uint64_t)n_inst * S] = offs[n_inst] - occ_base;
   // one store per warp that saw a mismatch, skipped once another landed
   if (__any_sync(0xffffffffu, nonid) && lane == 0 && *(volatile uint32_t*)(err + 1) != 0u) err[1] = 0u;
 }
@@ -919,10 +925,10 @@ __global__ void k_gather_rows(const float* __restrict__ src, const uint32_t* __r
 
 void prepare_bags(const uint32_t* d_offs, uint32_t occ_base, const uint16_t* d_slots,
                   uint32_t n_inst, uint32_t S, uint32_t* d_bag_offs, uint32_t* d_bag_of_occ,
-                  uint32_t* d_err, cudaStream_t s, uint32_t* d_abort) {
+                  uint32_t* d_err, cudaStream_t s, uint32_t* d_abort, bool maps) {
   KP_CUDA(cudaMemsetAsync(d_err + 1, 0xFF, 4, s));
   k_prepare_bags<<<grid_cap(((uint64_t)n_inst * 32 + 255) / 256), 256, 0, s>>>(
-      d_offs, occ_base, d_slots, n_inst, S, d_bag_offs, d_bag_of_occ, d_err, d_abort); ::kp::count_launch();
+      d_offs, occ_base, d_slots, n_inst, S, d_bag_offs, d_bag_of_occ, d_err, d_abort, maps ? 1 : 0); ::kp::count_launch();
 }
 
 void compose(const uint32_t* d_idx, const uint32_t* d_inverse, uint32_t n, uint32_t* d_out,

@@ -68,6 +68,9 @@ struct DedupWs {
 // state writes are guarded by it and it reruns the batch); returns whether
 // it ran that way.
 constexpr uint32_t kUnknownU = 0xFFFFFFFFu;
+struct DedupWs;
+// would dedup() of n keys with d_abort run without the readback?
+bool dedup_async_ready(const DedupWs& ws, uint32_t n);
 // expect_ident (0/1; -1 none): the caller's prediction of *d_occ_ident ==
 // all-ones, checked on the device the same way.
 bool dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
@@ -132,10 +135,12 @@ void table_gather(const Table* t, const uint32_t* d_rows, uint32_t n, float* d_w
 // occurrence (caller presets 0xFFFFFFFF); d_err[1]: 0xFFFFFFFF iff
 // bag_of_occ[o] == o for every occurrence (set here).
 // (d_abort: a bad slot id also sets kAbortPlan there -- the sync-free step
-// keeps its state writes out and raises at the batch-end readback)
+// keeps its state writes out and raises at the batch-end readback; maps =
+// false: only the checks, for a batch predicted to hold one feature per slot
+// -- its maps are the identity and nothing reads them)
 void prepare_bags(const uint32_t* d_offs, uint32_t occ_base, const uint16_t* d_slots,
                   uint32_t n_inst, uint32_t S, uint32_t* d_bag_offs, uint32_t* d_bag_of_occ,
-                  uint32_t* d_err, cudaStream_t s, uint32_t* d_abort = nullptr);
+                  uint32_t* d_err, cudaStream_t s, uint32_t* d_abort = nullptr, bool maps = true);
 // row_of_occ[o] = idx[inverse[o]]  (source row of every occurrence)
 void compose(const uint32_t* d_idx, const uint32_t* d_inverse, uint32_t n, uint32_t* d_out,
              cudaStream_t s);

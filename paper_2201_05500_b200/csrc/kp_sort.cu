@@ -706,6 +706,8 @@ __global__ void k_plan_check(const unsigned long long* __restrict__ mm, int plan
   if (!ok) atomicOr(abort_word, kAbortPlan);
 }
 
+bool dedup_async_ready(const DedupWs& ws, uint32_t n) { return n > 0 && spec_enabled() && ws.spec_bits >= 0; }
+
 bool dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
            const uint32_t* d_occ_map, const uint32_t* d_occ_ident, uint32_t* d_abort, int expect_ident) {
   ws.n = n;

@@ -690,15 +690,21 @@ def _train_n(kp, monkeypatch, sync_free, batches, S=8, e=16, hidden=(32, 16), B=
     return tr, losses
 
 
-def test_sync_free_step_replans_bitwise(kp, monkeypatch):
+@pytest.mark.parametrize("S,e,tc_min", [(8, 16, None), (20, 64, "0")])
+def test_sync_free_step_replans_bitwise(kp, monkeypatch, S, e, tc_min):
     """The single-GPU step without the dedup readback (pass plan and the
     one-feature-per-slot layout predicted from the previous batch, checked on
     the device): a batch whose key span outgrows the plan (1e3 -> 1e12 keys),
     one that switches to multi-hot bags (the layout prediction fails) and
     back are rerun with the readbacks -- every result and every trained bit
-    equals the always-readback trainer (KP_SYNC_FREE=0)."""
+    equals the always-readback trainer (KP_SYNC_FREE=0). The second case runs
+    the planes path, where a predicted one-feature batch skips writing the
+    (identity) bag maps."""
+    if tc_min is not None:
+        monkeypatch.setenv("KP_TC_MIN_MFLOP", tc_min)
+
     def mk(V, seed, multi=False):
-        bt = make_batch(512, V=V, zipf_s=1.1, n_slots=8, seed=seed)
+        bt = make_batch(512, V=V, zipf_s=1.1, n_slots=S, seed=seed)
         if multi:  # two features in every slot
             bt.keys = np.repeat(bt.keys, 2)
             bt.slots = np.repeat(bt.slots, 2)
@@ -706,8 +712,8 @@ def test_sync_free_step_replans_bitwise(kp, monkeypatch):
         return bt
     batches = [mk(10**3, 1), mk(10**3, 2), mk(10**12, 3), mk(10**12, 4, multi=True), mk(10**4, 5),
                mk(10**4, 6)]
-    t1, r1 = _train_n(kp, monkeypatch, "1", batches)
-    t0, r0 = _train_n(kp, monkeypatch, "0", batches)
+    t1, r1 = _train_n(kp, monkeypatch, "1", batches, S=S, e=e)
+    t0, r0 = _train_n(kp, monkeypatch, "0", batches, S=S, e=e)
     for (l1, p1), (l0, p0) in zip(r1, r0):
         assert l1 == l0
         assert np.array_equal(p1, p0)
