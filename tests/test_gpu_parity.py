@@ -748,3 +748,29 @@ def test_sync_free_step_bad_slot_writes_nothing(kp, monkeypatch):
     kb, wb, ab, _ = tb.table()
     assert np.array_equal(ka, kb) and np.array_equal(wa, wb) and np.array_equal(aa, ab)
     assert np.array_equal(ta.worker_state(0)["x"], tb.worker_state(0)["x"])
+
+
+def test_sync_free_predict_pass_bitwise(kp, monkeypatch):
+    """Predict-then-train between merges (k = 3, two local workers: the
+    replicas differ, so the predictions take their own pull + x-bar forward
+    before the training step) on the sync-free step, with a plan miss in the
+    middle: predictions, losses and state equal the always-readback
+    trainer's bit for bit."""
+    out = []
+    for sf in ("1", "0"):
+        monkeypatch.setenv("KP_SYNC_FREE", sf)
+        cfg = O.TrainerCfg(n_workers=2, k=3, minibatch_size=256, embedding_dim=16, n_slots=8,
+                           hidden=(32, 16), pooling="sum", activation="relu", alpha=0.02, sparse_lr=0.1)
+        tr = kp.Trainer(table_capacity=1 << 18, **trainer_kwargs(vars(cfg)))
+        res = []
+        for b, V in enumerate([10**3, 10**3, 10**3, 10**12, 10**12, 10**4, 10**4]):
+            bt = make_batch(512, V=V, zipf_s=1.1, n_slots=8, seed=60 + b)
+            r = tr.train_batch(bt.offs, bt.keys, bt.labels, slots=bt.slots, predict_first=True)
+            res.append((r["loss"], np.asarray(r["preds"]).copy()))
+        k, w, a, _ = tr.table()
+        out.append((res, k, w, a, tr.worker_state(0)["x"], tr.worker_state(1)["x"]))
+    (r1, k1, w1, a1, x1, y1), (r0, k0, w0, a0, x0, y0) = out
+    for (l1, p1), (l0, p0) in zip(r1, r0):
+        assert l1 == l0 and np.array_equal(p1, p0)
+    assert np.array_equal(k1, k0) and np.array_equal(w1, w0) and np.array_equal(a1, a0)
+    assert np.array_equal(x1, x0) and np.array_equal(y1, y0)
