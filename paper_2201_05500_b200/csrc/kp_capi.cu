@@ -1025,6 +1025,22 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
   const uint64_t t = tr->t_global + 1;
   const bool merged = (t % tr->cfg.k) == 0;
   AdamParams h{(float)tr->cfg.alpha, (float)tr->cfg.beta1, (float)tr->cfg.beta2};
+  uint32_t* chk = static_cast<uint32_t*>(tr->check.p);
+  if (tr->W == 1 && tr->world == 1) {
+    // one pass: moments, the local step or the single-worker merge, checks
+    dense_step_single(tr->x, tr->m, tr->v, tr->vbar, tr->g, D, h, merged, tr->cfg.reset_local_v != 0, chk,
+                      chk + 1, s);
+    if (merged) {
+      tr->merges++;
+      tr->x_uniform = true;
+    } else {
+      tr->x_uniform = false;
+    }
+    tr->t_global = t;
+    tr->mark(5);
+    if (tr->traj_on) record_trajectory(tr, t, merged);
+    return;
+  }
   if (!merged) {
     for (uint32_t l = 0; l < tr->W; ++l)
       dense_local_step(tr->x + l * D, tr->m + l * D, tr->v + l * D, tr->vbar + l * D, tr->g + l * D,
@@ -1045,7 +1061,6 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
     }
   }
   tr->t_global = t;
-  uint32_t* chk = static_cast<uint32_t*>(tr->check.p);
   for (uint32_t l = 0; l < tr->W; ++l)
     dense_check(tr->v + l * D, tr->vbar + l * D, tr->x + l * D, D, chk, s, l == 0 ? chk + 1 : nullptr);
   tr->mark(5);

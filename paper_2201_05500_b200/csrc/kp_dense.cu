@@ -118,7 +118,47 @@ __global__ void k_check(const float* __restrict__ v, const float* __restrict__ v
   if (f) atomicOr(flag, f);
 }
 
+// One worker on one GPU, the whole dense step in one pass: moments, then the
+// local step or the single-worker merge, then the state checks -- the same
+// expression trees as k_moments / k_local_step / k_merge_single / k_check in
+// sequence (bitwise their results), one read and write of each vector.
+__global__ void k_dense_step_single(float* __restrict__ x, float* __restrict__ m, float* __restrict__ v,
+                                    float* __restrict__ vbar, const float* __restrict__ g, uint64_t D,
+                                    float alpha, float b1, float b2, int merge, int reset, uint32_t* flag,
+                                    uint32_t* done, const uint32_t* abort) {
+  if (aborted(abort)) return;
+  if (done && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(done, 1u);
+  uint32_t f = 0;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < D;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    float mj = m[j], vj = v[j], xj = x[j], vb;
+    moments(mj, vj, g[j], b1, b2);
+    if (!merge) {
+      vb = vbar[j];
+      xj = __fsub_rn(xj, __fdiv_rn(__fmul_rn(alpha, mj), __fsqrt_rn(vb)));
+    } else {
+      vb = __fadd_rn(vj, __fdiv_rn(__fadd_rn(0.f, __fsub_rn(vj, vj)), 1.f));
+      const float t = __fsub_rn(xj, __fdiv_rn(__fmul_rn(alpha, mj), __fsqrt_rn(vb)));
+      xj = __fadd_rn(t, __fdiv_rn(__fadd_rn(0.f, __fsub_rn(t, t)), 1.f));
+      vbar[j] = vb;
+      if (reset) vj = vb;
+    }
+    m[j] = mj;
+    v[j] = vj;
+    x[j] = xj;
+    if (!isfinite(xj) || !isfinite(vj)) f |= 1;
+    if (!(vj > 0.f) || !(vb > 0.f)) f |= 2;
+  }
+  if (f) atomicOr(flag, f);
+}
+
 }  // namespace
+
+void dense_step_single(float* x, float* m, float* v, float* vbar, const float* g, uint64_t D, const AdamParams& h,
+                       bool merge, bool reset, uint32_t* d_flag, uint32_t* d_done, cudaStream_t s) {
+  k_dense_step_single<<<grid_for(D), 256, 0, s>>>(x, m, v, vbar, g, D, h.alpha, h.beta1, h.beta2, merge ? 1 : 0,
+                                                  reset ? 1 : 0, d_flag, d_done, g_abort); ::kp::count_launch();
+}
 
 void dense_local_step(float* x, float* m, float* v, const float* vbar, const float* g, uint64_t D,
                       const AdamParams& h, cudaStream_t s) {

@@ -393,6 +393,10 @@ void merge_terms(const float* x, const float* m, const float* vbar, uint64_t D, 
                  float* out, cudaStream_t s);
 void dense_check(const float* v, const float* vbar, const float* x, uint64_t D, uint32_t* d_flag,
                  cudaStream_t s, uint32_t* d_done = nullptr);
+// one worker on one GPU: moments + local step or merge + checks in one pass
+// (bitwise the separate kernels' results)
+void dense_step_single(float* x, float* m, float* v, float* vbar, const float* g, uint64_t D, const AdamParams& h,
+                       bool merge, bool reset, uint32_t* d_flag, uint32_t* d_done, cudaStream_t s);
 // dst = src (D floats), skipped when the step was aborted (g_abort)
 void dense_copy(float* dst, const float* src, uint64_t D, cudaStream_t s);
 

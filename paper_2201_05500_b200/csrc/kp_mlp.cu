@@ -456,18 +456,34 @@ __global__ void k_head_bwd(const float* __restrict__ in, int B, int W, const flo
     last = atomicAdd(done, 1u) == gridDim.x - 1;  // the last block finalizes
   }
   __syncthreads();
-  if (!last || warp != 0) return;
+  if (!last) return;
   __threadfence();
   // loss_sum += (sum / n) * n, the reference's loss_sum += bwd.loss * mb.size
-  // (trainer.cpp:177): 32 lanes sum strided partials, lane 0 combines in order
+  // (trainer.cpp:177): every thread of the last block sums a strided set of
+  // partials (four loads in flight -- one lane walking them was a chain of
+  // L2 round trips), then the block's sums combine in thread order
   __shared__ double s_fin[32];
+  const int nt = (int)blockDim.x, ng = (int)gridDim.x;
   double t = 0.0;
-  for (int i = lane; i < (int)gridDim.x; i += 32) t += *reinterpret_cast<volatile double*>(loss_part + i);
-  s_fin[lane] = t;
-  __syncwarp();
-  if (lane == 0) {
+  int i = (int)threadIdx.x;
+  for (; i + 3 * nt < ng; i += 4 * nt) {
+    const double a = *reinterpret_cast<volatile double*>(loss_part + i);
+    const double b = *reinterpret_cast<volatile double*>(loss_part + i + nt);
+    const double c = *reinterpret_cast<volatile double*>(loss_part + i + 2 * nt);
+    const double d = *reinterpret_cast<volatile double*>(loss_part + i + 3 * nt);
+    t += a;
+    t += b;
+    t += c;
+    t += d;
+  }
+  for (; i < ng; i += nt) t += *reinterpret_cast<volatile double*>(loss_part + i);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);  // fixed butterfly
+  if (lane == 0) s_fin[warp] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
     double u = 0.0;
-    for (int i = 0; i < 32; ++i) u += s_fin[i];
+    for (int q = 0; q < (nt >> 5); ++q) u += s_fin[q];
     *loss_sum += (u / (double)n_loss) * (double)n_loss;
     *done = 0u;  // ready for the next launch (stream order)
   }
