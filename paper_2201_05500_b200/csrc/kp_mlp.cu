@@ -352,13 +352,21 @@ __global__ void k_reduce_splits(const float* __restrict__ part, int splits, size
 // column sums (optionally weighted): partial[c][n] = sum_{b in chunk c} w[b]*X[b][n]
 // column sums (optionally weighted): part[c][n] = sum_{b in chunk c} w[b]*X[b][n];
 // block (32 columns x 8 row lanes), fixed-order combine of the 8 lanes.
+// Rows per chunk: 512, or fewer for small batches so at least ~128 chunks
+// run in parallel (configs[0]: 4096 rows -> 32-row chunks; configs[1]
+// unchanged).
 constexpr int COLSUM_ROWS = 512;
+int colsum_rows(int B) {
+  if (B >= 128 * COLSUM_ROWS) return COLSUM_ROWS;
+  const int r = (B / 128 + 31) / 32 * 32;
+  return r < 32 ? 32 : r;
+}
 __global__ void k_colsum_part(const float* __restrict__ X, const float* __restrict__ w, int B,
-                              int N, float* __restrict__ part) {
+                              int N, float* __restrict__ part, int rows) {
   __shared__ float red[8][33];
   const int n = blockIdx.x * 32 + threadIdx.x;
   const int c = blockIdx.y;
-  const int b0 = c * COLSUM_ROWS, b1 = min(B, b0 + COLSUM_ROWS);
+  const int b0 = c * rows, b1 = min(B, b0 + rows);
   float acc = 0.f;
   if (n < N) {
     int b = b0 + threadIdx.y;
@@ -661,12 +669,13 @@ void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, c
 // gradient), n == W + W2: sum_b delta[b] (head bias). Per 512-row chunk
 // partials like k_colsum_part (fixed order), reduced by k_reduce_chunks_to.
 __global__ void k_colsum_head(const float* __restrict__ a, const float* __restrict__ delta,
-                              const float* __restrict__ dz, int B, int W, int W2, float* __restrict__ part) {
+                              const float* __restrict__ dz, int B, int W, int W2, float* __restrict__ part,
+                              int rows) {
   __shared__ float red[8][33];
   const int NT = W + W2 + 1;
   const int n = blockIdx.x * 32 + threadIdx.x;
   const int c = blockIdx.y;
-  const int b0 = c * COLSUM_ROWS, b1 = min(B, b0 + COLSUM_ROWS);
+  const int b0 = c * rows, b1 = min(B, b0 + rows);
   float acc = 0.f;
   if (n < NT) {
     // the column's source, then 4 independent loads in flight per step
@@ -730,10 +739,11 @@ __global__ void k_reduce_chunks(const float* __restrict__ part, int chunks, int 
 }
 
 void colsum(const float* X, const float* w, int B, int N, float* out, MlpWs& ws, cudaStream_t s) {
-  const int chunks = std::max(1, (B + COLSUM_ROWS - 1) / COLSUM_ROWS);
+  const int rows = colsum_rows(B);
+  const int chunks = std::max(1, (B + rows - 1) / rows);
   float* part = ws.partials.get<float>((size_t)chunks * N);
   dim3 g(ceil_div(N, 32), chunks);
-  k_colsum_part<<<g, dim3(32, 8), 0, s>>>(X, w, B, N, part); ::kp::count_launch();
+  k_colsum_part<<<g, dim3(32, 8), 0, s>>>(X, w, B, N, part, rows); ::kp::count_launch();
   if (chunks >= 32 && N <= 4096) {
     k_reduce_chunks<<<grid_cap(ceil_div((uint64_t)N * 32, 256)), 256, 0, s>>>(part, chunks, N, out); ::kp::count_launch();
   } else {
@@ -782,10 +792,11 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
   {
     const int W2 = fused_bias ? W : 0;
     const int NT = W + W2 + 1;
-    const int chunks = std::max(1, (int)((B + COLSUM_ROWS - 1) / COLSUM_ROWS));
+    const int rows = colsum_rows((int)B);
+    const int chunks = std::max(1, (int)((B + rows - 1) / rows));
     float* part = ws.partials.get<float>((size_t)chunks * NT);
     k_colsum_head<<<dim3(ceil_div(NT, 32), chunks), dim3(32, 8), 0, s>>>(layer_in(L - 1), delta, dprev, B, W, W2,
-                                                                          part); ::kp::count_launch();
+                                                                          part, rows); ::kp::count_launch();
     k_reduce_chunks_to<<<grid_cap(ceil_div((uint64_t)NT * 32, 256)), 256, 0, s>>>(
         part, chunks, NT, W, W2, d_grad + m.w_off[L - 1], fused_bias ? d_grad + m.b_off[L - 2] : nullptr,
         d_grad + m.b_off[L - 1]); ::kp::count_launch();

@@ -17,6 +17,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <type_traits>
+
 #include "kp_internal.cuh"
 
 namespace kp {
@@ -127,7 +129,7 @@ __device__ __forceinline__ uint32_t digit_of(KIN k, uint64_t kmin, int shift, ui
 // (full: no lane holds R -- a full tile -- so the validity bit is skipped)
 template <int R>
 __device__ __forceinline__ uint32_t match_digit(uint32_t d, bool full = false) {
-  constexpr int BITS = R == 256 ? 8 : R == 512 ? 9 : 16;
+  constexpr int BITS = R == 256 ? 8 : R == 512 ? 9 : R == 1024 ? 10 : 16;
   uint32_t peers = 0xffffffffu;
 #pragma unroll
   for (int b = 0; b < BITS; ++b) {
@@ -262,7 +264,10 @@ __global__ void __launch_bounds__(ST, 4) k_downsweep(
   // layout had 8- and 16-way bank conflicts in those two places.)
   __shared__ KOUT s_keys[TILE];
   __shared__ uint32_t s_vals[TILE];
-  __shared__ __align__(16) uint32_t s_wh[NW * R];  // [warp][digit] counts -> exclusive tile positions
+  // [warp][digit] counts -> exclusive tile positions (both <= TILE: 16 bits
+  // suffice, which keeps the 1024-digit table inside the static 48 KB)
+  using WT = std::conditional_t<(R > 512), uint16_t, uint32_t>;
+  __shared__ __align__(16) WT s_wh[NW * R];
   __shared__ uint32_t s_start[R], s_off[R];
   __shared__ uint32_t s_warp[NW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -288,7 +293,7 @@ __global__ void __launch_bounds__(ST, 4) k_downsweep(
       d[r] = R;
     }
   }
-  uint32_t* wrow = s_wh + warp * R;
+  WT* wrow = s_wh + warp * R;
 #pragma unroll
   for (int r = 0; r < IPT; ++r) {
     const uint32_t peers = match_digit<R>(d[r], full);
@@ -298,16 +303,39 @@ __global__ void __launch_bounds__(ST, 4) k_downsweep(
     __syncwarp();
     if (d[r] < R) {
       rw[r] = before + __popc(peers & lt);
-      if (leader) wrow[d[r]] = before + __popc(peers);
+      if (leader) wrow[d[r]] = (WT)(before + __popc(peers));
     }
     __syncwarp();
   }
   __syncthreads();
   // exclusive scan in (digit, warp) order: thread t owns digits [t*DPT, +DPT);
   // the column is read twice (sums, then positions) instead of held
-  {
+  if constexpr (R / ST == 4) {
+    // 1024 digits (16-bit entries)
+    uint32_t tt[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int w = 0; w < NW; ++w)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tt[j] += s_wh[w * R + 4 * tid + j];
+    uint32_t tot;
+    uint32_t p[4];
+    p[0] = block_excl_scan(tt[0] + tt[1] + tt[2] + tt[3], s_warp, tot);
+    p[1] = p[0] + tt[0];
+    p[2] = p[1] + tt[1];
+    p[3] = p[2] + tt[2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s_start[tid * 4 + j] = p[j];  // first tile position of the digit
+#pragma unroll
+    for (int w = 0; w < NW; ++w)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t x = s_wh[w * R + 4 * tid + j];
+        s_wh[w * R + 4 * tid + j] = (WT)p[j];
+        p[j] += x;
+      }
+  } else {
     constexpr int DPT = R / ST;
-    static_assert(DPT == 1 || DPT == 2, "256 or 512 digits");
+    static_assert(DPT == 1 || DPT == 2, "256, 512 or 1024 digits");
     uint32_t t0 = 0, t1 = 0;  // the owned digits' totals
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
@@ -579,6 +607,31 @@ __global__ void __launch_bounds__(ST) k_merge_level(const uint64_t* __restrict__
 
 }  // namespace
 
+// narrow-mode pass plan for a key span of `bits` bits (<= 32): the fewest
+// passes of at most 10-bit digits, digits as even as possible
+__host__ __device__ inline void narrow_plan(int bits, int& np, int& db) {
+  np = bits == 0 ? 1 : (bits + 9) / 10;
+  db = bits == 0 ? 1 : (bits + np - 1) / np;
+}
+
+template <int R>
+void pass_u64_to_u32(const uint64_t* kin, uint32_t* kout, uint32_t* vout, uint32_t n, const unsigned long long* mm,
+                     int shift, uint32_t* counts, uint32_t* totals, uint32_t nb, cudaStream_t s) {
+  k_upsweep<uint64_t, R><<<nb, ST, 0, s>>>(kin, n, mm, shift, counts, nb); ::kp::count_launch();
+  k_scan_rows<<<R, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
+  k_downsweep<uint64_t, uint32_t, R><<<nb, ST, 0, s>>>(kin, nullptr, kout, vout, n, mm, shift, counts, totals, nb);
+  ::kp::count_launch();
+}
+template <int R>
+void pass_u32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout, uint32_t n,
+              const unsigned long long* mm, int shift, uint32_t* counts, uint32_t* totals, uint32_t nb,
+              cudaStream_t s) {
+  k_upsweep<uint32_t, R><<<nb, ST, 0, s>>>(kin, n, mm, shift, counts, nb); ::kp::count_launch();
+  k_scan_rows<<<R, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
+  k_downsweep<uint32_t, uint32_t, R><<<nb, ST, 0, s>>>(kin, vin, kout, vout, n, mm, shift, counts, totals, nb);
+  ::kp::count_launch();
+}
+
 // The radix passes + unique/inverse/segments for a key span of `bits` bits
 // (any plan whose passes cover the actual span sorts correctly).
 static void dedup_sort(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
@@ -592,40 +645,30 @@ static void dedup_sort(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStre
   ws.d_seg = ws.seg.get<uint32_t>(n + 1);
   ws.d_sorted_mapped = d_occ_map ? ws.mapped.get<uint32_t>(n) : nullptr;
   if (bits <= 32) {
-    // narrow mode: the first pass turns keys into u32 (key - kmin); 9-bit
-    // digits, so a 27-bit span (1e8 keys) takes 3 passes of 8 B per pair
-    const int np = bits == 0 ? 1 : (bits + 8) / 9;
-    const int db = bits == 0 ? 1 : (bits + np - 1) / np;  // digit bits per pass (<= 9)
+    // narrow mode: the first pass turns keys into u32 (key - kmin); digits of
+    // up to 10 bits, the fewest passes: a 27-bit span (1e8 keys) takes 3
+    // passes of 9 bits, a 20-bit one (1e6 keys) 2 of 10, 29 bits (5e8) 3 of 10
+    int np, db;
+    narrow_plan(bits, np, db);
     uint32_t* ka = reinterpret_cast<uint32_t*>(ws.keys_a.get<uint64_t>((n + 1) / 2));
     uint32_t* kb = reinterpret_cast<uint32_t*>(ws.keys_b.get<uint64_t>((n + 1) / 2));
-    uint32_t* counts = ws.counts.get<uint32_t>((size_t)512 * nb);
-    uint32_t* totals = ws.totals.get<uint32_t>(512);
+    uint32_t* counts = ws.counts.get<uint32_t>((size_t)1024 * nb);
+    uint32_t* totals = ws.totals.get<uint32_t>(1024);
     const uint32_t* kin32 = nullptr;
     const uint32_t* vin = nullptr;
     uint32_t* kout = ka;
     uint32_t* vout = va;
     for (int p = 0; p < np; ++p) {
       const int shift = p * db;
-      // digits of db bits, masked with R-1: use R = 2^db rounded to 256/512
-      const bool wide = db > 8;
+      // digits of db bits, masked with R-1: R = 2^db rounded up to 256/512/1024
       if (p == 0) {
-        if (wide) {
-          k_upsweep<uint64_t, 512><<<nb, ST, 0, s>>>(d_keys, n, mm, shift, counts, nb); ::kp::count_launch();
-          k_scan_rows<<<512, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
-          k_downsweep<uint64_t, uint32_t, 512><<<nb, ST, 0, s>>>(d_keys, nullptr, kout, vout, n, mm, shift, counts, totals, nb); ::kp::count_launch();
-        } else {
-          k_upsweep<uint64_t, 256><<<nb, ST, 0, s>>>(d_keys, n, mm, shift, counts, nb); ::kp::count_launch();
-          k_scan_rows<<<256, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
-          k_downsweep<uint64_t, uint32_t, 256><<<nb, ST, 0, s>>>(d_keys, nullptr, kout, vout, n, mm, shift, counts, totals, nb); ::kp::count_launch();
-        }
-      } else if (wide) {
-        k_upsweep<uint32_t, 512><<<nb, ST, 0, s>>>(kin32, n, mm, shift, counts, nb); ::kp::count_launch();
-        k_scan_rows<<<512, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
-        k_downsweep<uint32_t, uint32_t, 512><<<nb, ST, 0, s>>>(kin32, vin, kout, vout, n, mm, shift, counts, totals, nb); ::kp::count_launch();
+        if (db > 9) pass_u64_to_u32<1024>(d_keys, kout, vout, n, mm, shift, counts, totals, nb, s);
+        else if (db > 8) pass_u64_to_u32<512>(d_keys, kout, vout, n, mm, shift, counts, totals, nb, s);
+        else pass_u64_to_u32<256>(d_keys, kout, vout, n, mm, shift, counts, totals, nb, s);
       } else {
-        k_upsweep<uint32_t, 256><<<nb, ST, 0, s>>>(kin32, n, mm, shift, counts, nb); ::kp::count_launch();
-        k_scan_rows<<<256, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
-        k_downsweep<uint32_t, uint32_t, 256><<<nb, ST, 0, s>>>(kin32, vin, kout, vout, n, mm, shift, counts, totals, nb); ::kp::count_launch();
+        if (db > 9) pass_u32<1024>(kin32, vin, kout, vout, n, mm, shift, counts, totals, nb, s);
+        else if (db > 8) pass_u32<512>(kin32, vin, kout, vout, n, mm, shift, counts, totals, nb, s);
+        else pass_u32<256>(kin32, vin, kout, vout, n, mm, shift, counts, totals, nb, s);
       }
       kin32 = kout;
       vin = vout;
@@ -676,8 +719,8 @@ static int span_bits(const unsigned long long* h_mm) {
 static bool plan_covers(int planned, int bits) {
   if (planned > 32) return ((planned + 7) / 8) * 8 >= bits;  // wide: 8-bit digit passes
   if (bits > 32) return false;                               // narrow keys are u32 (key - kmin)
-  const int np = planned == 0 ? 1 : (planned + 8) / 9;
-  const int db = planned == 0 ? 1 : (planned + np - 1) / np;
+  int np, db;
+  narrow_plan(planned, np, db);
   return np * db >= bits;
 }
 
@@ -699,8 +742,8 @@ __global__ void k_plan_check(const unsigned long long* __restrict__ mm, int plan
   if (planned > 32) ok = ((planned + 7) / 8) * 8 >= bits;
   else if (bits > 32) ok = false;
   else {
-    const int np = planned == 0 ? 1 : (planned + 8) / 9;
-    const int db = planned == 0 ? 1 : (planned + np - 1) / np;
+    int np, db;
+    narrow_plan(planned, np, db);
     ok = np * db >= bits;
   }
   if (!ok) atomicOr(abort_word, kAbortPlan);
