@@ -1031,9 +1031,16 @@ void seg_reduce_apply(const uint32_t* d_seg, uint32_t n_unique, const uint32_t* 
   a.grad_out = d_grad_out;
   a.out_idx = d_out_idx;
   // chunk length: 64 positions, shorter for small batches so the
-  // latency-bound chunk walks still fill the GPU (C1: 106K positions -> 8)
+  // latency-bound chunk walks still fill the GPU (C1: 106K positions -> 4)
+  // (floor 4: configs[0]'s 106K positions -> 26.6K chunks, push 61 -> 55 us
+  // against a floor of 8; KP_SEG_MINCH overrides)
+  static const uint32_t min_ch = [] {
+    const char* e = getenv("KP_SEG_MINCH");
+    const int v = e ? atoi(e) : 4;
+    return (uint32_t)(v >= 1 && v <= 64 ? v : 4);
+  }();
   a.CH = 64;
-  while (a.CH > 8 && n_pos / a.CH < 148u * 128u) a.CH /= 2;
+  while (a.CH > min_ch && n_pos / a.CH < 148u * 128u) a.CH /= 2;
   const uint32_t nchunks = (n_pos + a.CH - 1) / a.CH;
   a.partials = ws.partials.get<float>((size_t)nchunks * 2 * e);
   uint32_t* first = ws.first.get<uint32_t>(nchunks);
