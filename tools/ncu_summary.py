@@ -26,7 +26,7 @@ STAGE = [
     (r"k_split|k_tc_gemm|k_gemm|k_h3|k_colmax|k_head_|k_loss|k_colsum|k_reduce_splits|k_reduce_chunks"
      r"|k_transpose|k_rowmax|k_sum_parts", "mlp"),
     (r"k_seg_|k_chunk_first", "push"),
-    (r"k_moments|k_cmean|k_terms|k_check|k_local_step|k_merge", "dense"),
+    (r"k_moments|k_cmean|k_terms|k_check|k_local_step|k_merge|k_dense_step", "dense"),
 ]
 
 
