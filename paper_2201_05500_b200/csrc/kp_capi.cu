@@ -175,7 +175,7 @@ struct kp_trainer {
   struct {
     int mode = -1;
     PeerWin keys, rows, grads, flags;
-    PeerWin dv, dx, terms, vb;  // k-step merge over NVLink
+    PeerWin dv, dx, dm, vb;  // k-step merge over NVLink (the trainer's v, x, m; v_bar)
     uint64_t seq[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     DevBuf scratch;
   } peer;
@@ -248,7 +248,7 @@ struct kp_trainer {
     if (copy_s) cudaStreamDestroy(copy_s);
     if (xs) cudaStreamDestroy(xs);
     for (PeerWin* w : {&peer.keys, &peer.rows, &peer.grads, &peer.flags, &peer.dv, &peer.dx,
-                       &peer.terms, &peer.vb}) {
+                       &peer.dm, &peer.vb}) {
       for (size_t p = 0; p < w->remote.size(); ++p)
         if (w->remote[p] && w->remote[p] != w->local) cudaIpcCloseMemHandle(w->remote[p]);
       if (w->local && w->owned) cudaFree(w->local);
@@ -523,13 +523,13 @@ bool peer_ready(kp_trainer* tr) {
     const uint32_t W = tr->W;
     ok = win_alloc(tr, P.dv, (size_t)W * D * 4, tr->v) && ok;
     ok = win_alloc(tr, P.dx, (size_t)W * D * 4, tr->x) && ok;
-    ok = win_alloc(tr, P.terms, (size_t)W * D * 4) && ok;
+    ok = win_alloc(tr, P.dm, (size_t)W * D * 4, tr->m) && ok;
     ok = win_alloc(tr, P.vb, (size_t)D * 4) && ok;
   }
   if (first || grew) {
     P.mode = all_ok(tr, ok) ? 1 : 0;
     if (P.mode == 0)
-      for (auto* w : {&P.keys, &P.rows, &P.grads, &P.flags, &P.dv, &P.dx, &P.terms, &P.vb})
+      for (auto* w : {&P.keys, &P.rows, &P.grads, &P.flags, &P.dv, &P.dx, &P.dm, &P.vb})
         win_release(tr, *w);
   }
   return P.mode == 1;
@@ -586,27 +586,19 @@ void merge_states_peer(kp_trainer* tr, float alpha, bool reset) {
   KP_CHECK(P.dv.local != nullptr, kErrCuda, "peer merge: dense-state windows not mapped");
   const uint64_t C = (D + R - 1) / R;
   const uint64_t c0 = std::min<uint64_t>(D, (uint64_t)me * C), c1 = std::min<uint64_t>(D, c0 + C);
-  PeerVecs pv{};
-  // round 1: v_bar
-  peer_exchange_sync(tr, 3, true, true);  // every rank's v is final
+  // one round: every rank's v, x and m are final -> each owner merges its
+  // chunk straight from the peers' buffers into every rank -> all stored
+  peer_exchange_sync(tr, 3, true, true);
+  PeerMerge pm{};
   for (int p = 0; p < R; ++p) {
-    pv.src[p] = reinterpret_cast<uintptr_t>(P.dv.remote[p]);
-    pv.dst[p] = reinterpret_cast<uintptr_t>(P.vb.remote[p]);
+    pm.v[p] = reinterpret_cast<uintptr_t>(P.dv.remote[p]);
+    pm.x[p] = reinterpret_cast<uintptr_t>(P.dx.remote[p]);
+    pm.m[p] = reinterpret_cast<uintptr_t>(P.dm.remote[p]);
+    pm.vb[p] = reinterpret_cast<uintptr_t>(P.vb.remote[p]);
   }
-  peer_cmean(pv, R, W, D, c0, c1, s);
-  peer_exchange_sync(tr, 4, true, true);  // v_bar complete everywhere
+  peer_merge(pm, R, W, D, c0, c1, alpha, s);
+  peer_exchange_sync(tr, 4, true, true);  // v_bar and x complete everywhere
   const float* vb = static_cast<const float*>(P.vb.local);
-  float* terms = static_cast<float*>(P.terms.local);
-  for (uint32_t l = 0; l < W; ++l)
-    merge_terms(tr->x + l * D, tr->m + l * D, vb, D, alpha, terms + l * D, s);
-  // round 2: x = cmean(terms), into worker 0 of every rank
-  peer_exchange_sync(tr, 5, true, true);
-  for (int p = 0; p < R; ++p) {
-    pv.src[p] = reinterpret_cast<uintptr_t>(P.terms.remote[p]);
-    pv.dst[p] = reinterpret_cast<uintptr_t>(P.dx.remote[p]);
-  }
-  peer_cmean(pv, R, W, D, c0, c1, s);
-  peer_exchange_sync(tr, 6, true, true);
   float* x = tr->x;
   // guarded copies (not cudaMemcpy): a timed-out merge must not publish v_bar
   for (uint32_t l = 0; l < W; ++l) {
@@ -815,9 +807,10 @@ uint64_t merge_bytes_sent(const kp_trainer* tr) {
   const uint64_t my_len = std::min<uint64_t>(C, D > me * C ? D - me * C : 0);
   uint64_t per_round;
   if (tr->peer.mode == 1) {
-    // served: every other owner reads its chunk of my W worker vectors; sent:
-    // my merged chunk to every other rank
-    per_round = (D - my_len) * W * 4 + (R - 1) * my_len * 4;
+    // one round (k_merge_peer): every other owner reads its chunk of my W
+    // workers' v, x and m; I store my merged chunk's v_bar and x into every
+    // other rank
+    return 3 * (D - my_len) * W * 4 + 2 * (R - 1) * my_len * 4;
   } else if ((R - 1) * W * D * 4 <= (24ull << 20)) {
     per_round = (R - 1) * W * D * 4;  // ring allgather of W*D per rank
   } else {

@@ -183,6 +183,15 @@ struct PeerVecs {
 // centered mean of elements [c0, c1) over all ranks' workers, into every rank
 void peer_cmean(const PeerVecs& pv, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1,
                 cudaStream_t s);
+// The whole k-step merge of elements [c0, c1) in one pass over NVLink: v_bar =
+// cmean(v), terms x - alpha*m/sqrt(v_bar) of every rank's workers, x = cmean(
+// terms) -- stored into every rank's v_bar window and worker-0 x.
+struct PeerMerge {
+  uintptr_t v[kMaxPeers], x[kMaxPeers], m[kMaxPeers];  // rank p's [W][D] worker vectors
+  uintptr_t vb[kMaxPeers];                             // rank p's [D] v_bar window
+};
+void peer_merge(const PeerMerge& pm, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1, float alpha,
+                cudaStream_t s);
 // keys[t] = unique[perm[t]] -> peer windows (the owner's received keys)
 void peer_send_keys(const uint64_t* d_unique, const uint32_t* d_perm, uint32_t n, const PeerMap& pm,
                     cudaStream_t s);

@@ -108,7 +108,53 @@ __global__ void k_cmean_peer(PeerVecs pv, int R, uint32_t W, uint64_t D, uint64_
   __threadfence_system();
 }
 
+// k_cmean_peer (v) -> merge_terms on every rank -> k_cmean_peer (terms) in
+// one kernel: the owner of chunk [c0, c1) reads every rank's v, x and m
+// there, so the merge needs one exchange round instead of two; the same
+// expression trees and worker order, so the result is bitwise the two-round
+// one's. It writes only its own chunk of every rank's x (worker 0), which no
+// other owner reads.
+__global__ void k_merge_peer(PeerMerge pm, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1, float alpha,
+                             const uint32_t* abort) {
+  if (aborted(abort)) return;
+  const float n = (float)(R * W);
+  for (uint64_t j = c0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < c1;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const float vbase = reinterpret_cast<const float*>(pm.v[0])[j];
+    float acc = 0.f;
+    for (int p = 0; p < R; ++p) {
+      const float* vp = reinterpret_cast<const float*>(pm.v[p]);
+      for (uint32_t l = 0; l < W; ++l) acc = __fadd_rn(acc, __fsub_rn(vp[(uint64_t)l * D + j], vbase));
+    }
+    const float vb = __fadd_rn(vbase, __fdiv_rn(acc, n));
+    const float sq = __fsqrt_rn(vb);
+    auto term = [&](int p, uint32_t l) {
+      const float xv = reinterpret_cast<const float*>(pm.x[p])[(uint64_t)l * D + j];
+      const float mv = reinterpret_cast<const float*>(pm.m[p])[(uint64_t)l * D + j];
+      return __fsub_rn(xv, __fdiv_rn(__fmul_rn(alpha, mv), sq));
+    };
+    const float tbase = term(0, 0);
+    float tacc = 0.f;
+    for (int p = 0; p < R; ++p)
+      for (uint32_t l = 0; l < W; ++l) tacc = __fadd_rn(tacc, __fsub_rn(term(p, l), tbase));
+    const float xb = __fadd_rn(tbase, __fdiv_rn(tacc, n));
+    for (int p = 0; p < R; ++p) {
+      reinterpret_cast<float*>(pm.vb[p])[j] = vb;
+      reinterpret_cast<float*>(pm.x[p])[j] = xb;
+    }
+  }
+  __threadfence_system();
+}
+
 }  // namespace
+
+void peer_merge(const PeerMerge& pm, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1, float alpha,
+                cudaStream_t s) {
+  if (c1 <= c0) return;
+  k_merge_peer<<<(unsigned)std::min<uint64_t>((c1 - c0 + 255) / 256, 148 * 8), 256, 0, s>>>(pm, R, W, D, c0, c1,
+                                                                                             alpha, g_abort);
+  ::kp::count_launch();
+}
 
 void peer_cmean(const PeerVecs& pv, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1,
                 cudaStream_t s) {
