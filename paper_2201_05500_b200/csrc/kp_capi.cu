@@ -681,16 +681,16 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
     const int R = tr->world;
     uint32_t* perm = tr->perm.get<uint32_t>(std::max<uint32_t>(U, 1));
     uint32_t* pos = tr->pos.get<uint32_t>(std::max<uint32_t>(U, 1));
-    tr->cnt_send.assign(R, 0);
-    shard(tr->dd.d_unique, U, R, perm, pos, tr->cnt_send.data(), tr->sh, s);
-    // counts matrix via allgather
+    // counts matrix via allgather, straight from the shard's device counts
+    // (one host readback for both: this rank's row is its send counts)
     uint64_t* cd = tr->counts_dev.get<uint64_t>((size_t)R * R + R);
-    KP_CUDA(cudaMemcpyAsync(cd, tr->cnt_send.data(), R * 8, cudaMemcpyHostToDevice, s));
+    shard(tr->dd.d_unique, U, R, perm, pos, nullptr, tr->sh, s, cd);
     KP_NCCL(ncclAllGather(cd, cd + R, R, ncclUint64, tr->comm->nc, s));
     tr->mat.assign((size_t)R * R, 0);
     KP_CUDA(cudaMemcpyAsync(tr->mat.data(), cd + R, (size_t)R * R * 8, cudaMemcpyDeviceToHost, s));
     KP_CUDA(cudaStreamSynchronize(s));
     const std::vector<uint64_t>& mat = tr->mat;
+    tr->cnt_send.assign(mat.begin() + (size_t)tr->rank * R, mat.begin() + (size_t)(tr->rank + 1) * R);
     tr->cnt_recv.assign(R, 0);
     tr->off_send.assign(R, 0);
     tr->off_recv.assign(R, 0);
@@ -727,12 +727,15 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
       // each source's keys arrive ascending: merge the R runs
       std::vector<uint64_t> run_off(R + 1, 0);
       for (int p = 0; p < R; ++p) run_off[p + 1] = run_off[p] + tr->cnt_recv[p];
-      dedup_runs(rk, Rn, run_off, tr->dd_owner, s);
+      dedup_runs(rk, Rn, run_off, tr->dd_owner, s, /*readback*/ false);
     }
     tr->mark(0);
-    const uint32_t Uo = tr->dd_owner.n_unique;
+    // (the owner's U stays on the device: Rn bounds it)
+    const bool uo_dev = tr->dd_owner.n_unique == kUnknownU;
+    const uint32_t Uo = uo_dev ? Rn : tr->dd_owner.n_unique;
+    const uint32_t* dUo = uo_dev ? tr->dd_owner.d_nunique : nullptr;
     uint32_t* orows = tr->owner_rows.get<uint32_t>(std::max<uint32_t>(Uo, 1));
-    table_pull(tr->tab.t, tr->dd_owner.d_unique, Uo, orows, stamp, s);
+    table_pull(tr->tab.t, tr->dd_owner.d_unique, Uo, orows, stamp, s, dUo);
     uint32_t* oidx = tr->owner_idx.get<uint32_t>(std::max<uint32_t>(Rn, 1));
     if (Rn) k_compose<<<grid1(Rn), 256, 0, s>>>(orows, tr->dd_owner.d_inverse, Rn, oidx); ::kp::count_launch();
     float* rrows;
@@ -855,7 +858,7 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
     if (!pr.dU) tr->prof_unique += pr.U;  // (sync-free step: added at the batch-end readback)
     tr->prof_occ += sv.n_occ;
     if (tr->world > 1) {
-      tr->prof_owner_unique += tr->dd_owner.n_unique;
+      if (tr->dd_owner.n_unique != kUnknownU) tr->prof_owner_unique += tr->dd_owner.n_unique;
       for (auto c : tr->cnt_recv) tr->prof_recv += c;
     }
   }
@@ -1002,10 +1005,11 @@ void run_step(kp_trainer* tr, const StepView& sv, double* d_loss_slot, float* fu
     if (peer && peer_ce) KP_CUDA(cudaStreamWaitEvent(s, tr->ev_xdone, 0));
     if (peer) peer_exchange_sync(tr, 2, false, true);
     tr->mark(6);
-    seg_reduce_apply(tr->dd_owner.d_seg, tr->dd_owner.n_unique, tr->dd_owner.sorted_vals, nullptr,
-                     (uint32_t)Rn, rgr, tr->e, inv_n, tr->tab.t,
+    const bool uo_dev = tr->dd_owner.n_unique == kUnknownU;  // (U on the device: Rn bounds it)
+    seg_reduce_apply(tr->dd_owner.d_seg, uo_dev ? (uint32_t)Rn : tr->dd_owner.n_unique, tr->dd_owner.sorted_vals,
+                     nullptr, (uint32_t)Rn, rgr, tr->e, inv_n, tr->tab.t,
                      static_cast<const uint32_t*>(tr->owner_rows.p), rule, nullptr, nullptr,
-                     tr->sg_owner, s);
+                     tr->sg_owner, s, nullptr, uo_dev ? tr->dd_owner.d_nunique : nullptr);
     tr->mark(4);
   }
   if (tr->world > 1)  // GpuPush: per-key gradients to each remote owner

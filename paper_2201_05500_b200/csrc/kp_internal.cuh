@@ -78,17 +78,20 @@ bool dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
            uint32_t* d_abort = nullptr, int expect_ident = -1);
 // dedup() of keys made of runs [run_off[i], run_off[i+1]), each strictly
 // ascending: merge tree instead of the radix sort, identical outputs
+// (readback false: no host sync, ws.n_unique = kUnknownU, U on the device)
 void dedup_runs(const uint64_t* d_keys, uint32_t n, const std::vector<uint64_t>& run_off,
-                DedupWs& ws, cudaStream_t s);
+                DedupWs& ws, cudaStream_t s, bool readback = true);
 
 // Stable bucket of ascending unique keys by owner = key % G.
 // perm[i] = unique index placed at bucket slot i; pos[u] = slot of unique u;
-// counts[G] on host.
+// counts[G] on host -- or, with d_counts (h_counts null), as u64 on the
+// device only, with no host sync (the trainer allgathers them first).
 struct ShardWs {
   DevBuf bcount, scalars;
 };
 void shard(const uint64_t* d_unique, uint32_t n, uint32_t G, uint32_t* d_perm,
-           uint32_t* d_pos, uint64_t* h_counts, ShardWs& ws, cudaStream_t s);
+           uint32_t* d_pos, uint64_t* h_counts, ShardWs& ws, cudaStream_t s,
+           uint64_t* d_counts = nullptr);
 
 // ------------------------------------------------------------- table ----
 struct Table {

@@ -811,7 +811,7 @@ bool dedup(const uint64_t* d_keys, uint32_t n, DedupWs& ws, cudaStream_t s,
 // order): a pairwise merge tree (log2 R levels of merge path) replaces the
 // radix passes.
 void dedup_runs(const uint64_t* d_keys, uint32_t n, const std::vector<uint64_t>& run_off,
-                DedupWs& ws, cudaStream_t s) {
+                DedupWs& ws, cudaStream_t s, bool readback) {
   const int R = (int)run_off.size() - 1;
   if (n == 0 || R < 1 || R > kMaxRuns) {
     dedup(d_keys, n, ws, s);
@@ -872,21 +872,38 @@ void dedup_runs(const uint64_t* d_keys, uint32_t n, const std::vector<uint64_t>&
   k_scan_rows<<<1, ST, 0, s>>>(bcount, nb, ws.d_nunique + 1); ::kp::count_launch();
   k_dedup_emit<uint64_t><<<nb, ST, 0, s>>>(kin, mm, vin, n, bcount, ws.d_unique, ws.d_inverse, ws.d_seg,
                                            ws.d_nunique, nb, nullptr, nullptr, nullptr); ::kp::count_launch();
+  if (!readback) {  // U stays on the device (ws.d_nunique)
+    ws.n_unique = kUnknownU;
+    return;
+  }
   KP_CUDA(cudaMemcpyAsync(&ws.n_unique, ws.d_nunique, 4, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaStreamSynchronize(s));
 }
 
+__global__ void k_counts_u64(const uint32_t* __restrict__ in, uint32_t G, uint64_t* __restrict__ out) {
+  if (threadIdx.x < G) out[threadIdx.x] = in[threadIdx.x];
+}
+
 void shard(const uint64_t* d_unique, uint32_t n, uint32_t G, uint32_t* d_perm, uint32_t* d_pos,
-           uint64_t* h_counts, ShardWs& ws, cudaStream_t s) {
+           uint64_t* h_counts, ShardWs& ws, cudaStream_t s, uint64_t* d_counts) {
   KP_CHECK(G >= 1 && G <= MAXG, kErrConfig, "shard: G must be in [1, 64]");
-  for (uint32_t g = 0; g < G; ++g) h_counts[g] = 0;
-  if (n == 0) return;
+  KP_CHECK(h_counts || d_counts, kErrGeneric, "shard: no output for the counts");
+  if (h_counts)
+    for (uint32_t g = 0; g < G; ++g) h_counts[g] = 0;
+  if (n == 0) {
+    if (d_counts) KP_CUDA(cudaMemsetAsync(d_counts, 0, G * 8, s));
+    return;
+  }
   const uint32_t nb = ceil_div(n, TILE);
   uint32_t* counts = ws.bcount.get<uint32_t>((size_t)G * nb);
   uint32_t* totals = ws.scalars.get<uint32_t>(MAXG);
   k_shard_count<<<nb, ST, 0, s>>>(d_unique, n, G, counts, nb); ::kp::count_launch();
   k_scan_rows<<<G, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
   k_shard_emit<<<nb, ST, 0, s>>>(d_unique, n, G, counts, totals, nb, d_perm, d_pos); ::kp::count_launch();
+  if (d_counts) {
+    k_counts_u64<<<1, MAXG, 0, s>>>(totals, G, d_counts); ::kp::count_launch();
+  }
+  if (!h_counts) return;
   uint32_t h[MAXG];
   KP_CUDA(cudaMemcpyAsync(h, totals, G * 4, cudaMemcpyDeviceToHost, s));
   KP_CUDA(cudaStreamSynchronize(s));
