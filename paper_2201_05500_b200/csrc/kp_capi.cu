@@ -196,6 +196,7 @@ struct kp_trainer {
   // is rerun with the readbacks)
   bool async_step = false, force_sync = false, pred_ident = false;
   bool sync_free = true;  // KP_SYNC_FREE=0 at trainer creation: every step reads back
+  DevBuf pflag;           // G > 1: the local dedup's plan-miss flag (travels with the counts)
   std::vector<TrajStep> traj;
   std::vector<float> traj_prev_vbar;  // frozen v_bar before the step (a3)
   // profiling
@@ -647,16 +648,61 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
   // occurrence (one feature per slot), read with dedup's one host sync --
   // or, on the sync-free step, predicted and checked on the device
   uint32_t h_errw[2] = {0xFFFFFFFFu, 0};
-  const bool ran_async = tr->async_step &&
-                         dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ, err + 1, chk, tr->pred_ident ? 1 : 0);
+  // G > 1: no readback after the local dedup either -- its plan check goes to
+  // a flag word that travels with the send counts in the counts allgather
+  // (one readback for all three; a miss anywhere redoes the sort and the
+  // counts on every rank, before anything was sent or written)
+  const bool g_async = tr->world > 1 && tr->sync_free && !tr->fused_pool && dedup_async_ready(tr->dd, sv.n_occ);
+  uint32_t* pflag = g_async ? tr->pflag.get<uint32_t>(1) : nullptr;
+  if (g_async) {
+    KP_CUDA(cudaMemsetAsync(pflag, 0, 4, s));
+    dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ, err + 1, pflag, -1);
+  }
+  const bool ran_async = g_async || (tr->async_step && dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ, err + 1, chk,
+                                                             tr->pred_ident ? 1 : 0));
   if (!ran_async) {
     KP_CUDA(cudaMemcpyAsync(h_errw, err, 8, cudaMemcpyDeviceToHost, s));
     dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ, err + 1);  // synchronises the stream
     if (sv.n_occ == 0) KP_CUDA(cudaStreamSynchronize(s));
     tr->pred_ident = h_errw[1] == 0xFFFFFFFFu;
   }
+  // G > 1: the send counts (+ this rank's plan flag and error words) of every
+  // rank in one allgather and one readback; a plan miss anywhere redoes the
+  // sort with the exact plan (and the readback) and the counts on every rank
+  std::vector<uint64_t> gath;
+  auto gather_counts = [&](uint32_t n_bound, const uint32_t* dn) {
+    const int R = tr->world;
+    const size_t RS = (size_t)R + 2;
+    uint32_t* perm = tr->perm.get<uint32_t>(std::max<uint32_t>(n_bound, 1));
+    uint32_t* pos = tr->pos.get<uint32_t>(std::max<uint32_t>(n_bound, 1));
+    uint64_t* cd = tr->counts_dev.get<uint64_t>(RS * (R + 1));
+    shard(tr->dd.d_unique, n_bound, R, perm, pos, nullptr, tr->sh, s, cd, dn);
+    pack_step_flags(pflag, err, cd + R, s);
+    KP_NCCL(ncclAllGather(cd, cd + RS, RS, ncclUint64, tr->comm->nc, s));
+    gath.assign(RS * R, 0);
+    KP_CUDA(cudaMemcpyAsync(gath.data(), cd + RS, RS * R * 8, cudaMemcpyDeviceToHost, s));
+    KP_CUDA(cudaStreamSynchronize(s));
+  };
+  if (g_async) {
+    const int R = tr->world;
+    gather_counts(sv.n_occ, tr->dd.d_nunique);
+    bool miss = false;
+    for (int p = 0; p < R; ++p) miss |= gath[(size_t)p * (R + 2) + R] != 0;
+    if (miss) {  // (collective: every rank saw the same flags)
+      dedup(sv.keys, sv.n_occ, tr->dd, s, bag_of_occ, err + 1);  // exact plan, readback
+      pflag = nullptr;
+      gather_counts(tr->dd.n_unique, nullptr);
+    }
+    const uint64_t ew = gath[(size_t)tr->rank * (R + 2) + R + 1];
+    h_errw[0] = (uint32_t)ew;
+    h_errw[1] = (uint32_t)(ew >> 32);
+    tr->pred_ident = h_errw[1] == 0xFFFFFFFFu;
+    uint64_t u = 0;
+    for (int q = 0; q < R; ++q) u += gath[(size_t)tr->rank * (R + 2) + q];
+    tr->dd.n_unique = (uint32_t)u;  // this rank's unique keys = what it sends
+  }
   const uint32_t h_err = h_errw[0];
-  const bool ident_word = ran_async ? tr->pred_ident : h_errw[1] == 0xFFFFFFFFu;
+  const bool ident_word = (ran_async && !g_async) ? tr->pred_ident : h_errw[1] == 0xFFFFFFFFu;
   const bool ident_bags = ident_word && sv.n_occ == nb;
   // the identity occurrence -> bag map: the bag of sorted position p is the
   // sorted occurrence itself (dedup skipped writing the copy)
@@ -667,10 +713,11 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
            "slot ids must be < n_slots and non-decreasing within an instance (occurrence " +
                std::to_string(h_err) + ")");
   tr->mark(0);
-  const uint32_t U = ran_async ? sv.n_occ : tr->dd.n_unique;
+  const bool u_dev = ran_async && !g_async;
+  const uint32_t U = u_dev ? sv.n_occ : tr->dd.n_unique;
   PullResult pr{};
   pr.U = U;
-  pr.dU = ran_async ? tr->dd.d_nunique : nullptr;
+  pr.dU = u_dev ? tr->dd.d_nunique : nullptr;
   if (tr->world == 1) {
     uint32_t* rows = tr->rows.get<uint32_t>(std::max<uint32_t>(U, 1));
     table_pull(tr->tab.t, tr->dd.d_unique, U, rows, stamp, s, pr.dU);
@@ -679,16 +726,14 @@ PullResult pull_and_pool(kp_trainer* tr, const StepView& sv, bool stamp) {
     tr->mark(1);
   } else {
     const int R = tr->world;
-    uint32_t* perm = tr->perm.get<uint32_t>(std::max<uint32_t>(U, 1));
-    uint32_t* pos = tr->pos.get<uint32_t>(std::max<uint32_t>(U, 1));
     // counts matrix via allgather, straight from the shard's device counts
-    // (one host readback for both: this rank's row is its send counts)
-    uint64_t* cd = tr->counts_dev.get<uint64_t>((size_t)R * R + R);
-    shard(tr->dd.d_unique, U, R, perm, pos, nullptr, tr->sh, s, cd);
-    KP_NCCL(ncclAllGather(cd, cd + R, R, ncclUint64, tr->comm->nc, s));
+    // (one host readback: this rank's row is its send counts)
+    if (!g_async) gather_counts(U, nullptr);
+    uint32_t* perm = static_cast<uint32_t*>(tr->perm.p);
+    uint32_t* pos = static_cast<uint32_t*>(tr->pos.p);
     tr->mat.assign((size_t)R * R, 0);
-    KP_CUDA(cudaMemcpyAsync(tr->mat.data(), cd + R, (size_t)R * R * 8, cudaMemcpyDeviceToHost, s));
-    KP_CUDA(cudaStreamSynchronize(s));
+    for (int p = 0; p < R; ++p)
+      for (int q = 0; q < R; ++q) tr->mat[(size_t)p * R + q] = gath[(size_t)p * (R + 2) + q];
     const std::vector<uint64_t>& mat = tr->mat;
     tr->cnt_send.assign(mat.begin() + (size_t)tr->rank * R, mat.begin() + (size_t)(tr->rank + 1) * R);
     tr->cnt_recv.assign(R, 0);

@@ -91,7 +91,10 @@ struct ShardWs {
 };
 void shard(const uint64_t* d_unique, uint32_t n, uint32_t G, uint32_t* d_perm,
            uint32_t* d_pos, uint64_t* h_counts, ShardWs& ws, cudaStream_t s,
-           uint64_t* d_counts = nullptr);
+           uint64_t* d_counts = nullptr, const uint32_t* d_n = nullptr);
+// out[0] = *d_pflag (0 when null), out[1] = err[0] | err[1] << 32 (the step's
+// plan flag and error words, allgathered with the counts)
+void pack_step_flags(const uint32_t* d_pflag, const uint32_t* d_err, uint64_t* d_out, cudaStream_t s);
 
 // ------------------------------------------------------------- table ----
 struct Table {

@@ -474,7 +474,8 @@ constexpr int MAXG = 64;
 
 __global__ void __launch_bounds__(ST) k_shard_count(const uint64_t* __restrict__ keys, uint32_t n,
                                                     uint32_t G, uint32_t* __restrict__ counts,
-                                                    uint32_t nb) {
+                                                    uint32_t nb, const uint32_t* __restrict__ dn) {
+  if (dn) n = min(n, *dn);  // (the key count on the device, n its bound)
   __shared__ uint32_t hist[MAXG];
   if (threadIdx.x < MAXG) hist[threadIdx.x] = 0;
   __syncthreads();
@@ -492,7 +493,8 @@ __global__ void __launch_bounds__(ST) k_shard_emit(const uint64_t* __restrict__ 
                                                    uint32_t G, const uint32_t* __restrict__ counts,
                                                    const uint32_t* __restrict__ totals,
                                                    uint32_t nb, uint32_t* __restrict__ perm,
-                                                   uint32_t* __restrict__ pos) {
+                                                   uint32_t* __restrict__ pos, const uint32_t* __restrict__ dn) {
+  if (dn) n = min(n, *dn);
   __shared__ uint32_t s_off[MAXG], s_run[MAXG];
   __shared__ uint16_t s_wcnt[2][NW][MAXG];
   const int tid = threadIdx.x;
@@ -884,8 +886,18 @@ __global__ void k_counts_u64(const uint32_t* __restrict__ in, uint32_t G, uint64
   if (threadIdx.x < G) out[threadIdx.x] = in[threadIdx.x];
 }
 
+__global__ void k_pack_step_flags(const uint32_t* __restrict__ pflag, const uint32_t* __restrict__ err,
+                                  uint64_t* __restrict__ out) {
+  out[0] = pflag ? *pflag : 0u;
+  out[1] = (uint64_t)err[0] | ((uint64_t)err[1] << 32);
+}
+
+void pack_step_flags(const uint32_t* d_pflag, const uint32_t* d_err, uint64_t* d_out, cudaStream_t s) {
+  k_pack_step_flags<<<1, 1, 0, s>>>(d_pflag, d_err, d_out); ::kp::count_launch();
+}
+
 void shard(const uint64_t* d_unique, uint32_t n, uint32_t G, uint32_t* d_perm, uint32_t* d_pos,
-           uint64_t* h_counts, ShardWs& ws, cudaStream_t s, uint64_t* d_counts) {
+           uint64_t* h_counts, ShardWs& ws, cudaStream_t s, uint64_t* d_counts, const uint32_t* d_n) {
   KP_CHECK(G >= 1 && G <= MAXG, kErrConfig, "shard: G must be in [1, 64]");
   KP_CHECK(h_counts || d_counts, kErrGeneric, "shard: no output for the counts");
   if (h_counts)
@@ -897,9 +909,9 @@ void shard(const uint64_t* d_unique, uint32_t n, uint32_t G, uint32_t* d_perm, u
   const uint32_t nb = ceil_div(n, TILE);
   uint32_t* counts = ws.bcount.get<uint32_t>((size_t)G * nb);
   uint32_t* totals = ws.scalars.get<uint32_t>(MAXG);
-  k_shard_count<<<nb, ST, 0, s>>>(d_unique, n, G, counts, nb); ::kp::count_launch();
+  k_shard_count<<<nb, ST, 0, s>>>(d_unique, n, G, counts, nb, d_n); ::kp::count_launch();
   k_scan_rows<<<G, ST, 0, s>>>(counts, nb, totals); ::kp::count_launch();
-  k_shard_emit<<<nb, ST, 0, s>>>(d_unique, n, G, counts, totals, nb, d_perm, d_pos); ::kp::count_launch();
+  k_shard_emit<<<nb, ST, 0, s>>>(d_unique, n, G, counts, totals, nb, d_perm, d_pos, d_n); ::kp::count_launch();
   if (d_counts) {
     k_counts_u64<<<1, MAXG, 0, s>>>(totals, G, d_counts); ::kp::count_launch();
   }

@@ -93,6 +93,19 @@ def test_sharded_kstep_sweep_matches_oracle(tmp_path, k):
 
 
 @pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+def test_sharded_plan_miss_matches_oracle(tmp_path):
+    """The sharded step's local dedup runs without a readback (its pass plan
+    from the previous batch, the check flag allgathered with the send
+    counts): batches whose key space jumps from 4e3 to 1e12 and back make the
+    plan miss, every rank redoes its sort and the counts, and the state still
+    matches the f64 oracle."""
+    res = _run(tmp_path, [1, 4, "span", 6], port=29586)
+    assert res["owners_ok"] and res["keyset_equal"]
+    assert res["w_max_abs"] <= 2e-4 and res["x_max_abs"] <= 2e-4
+    assert all(abs(a - b) <= 1e-4 for a, b in zip(res["loss"], res["oracle_loss"]))
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
 def test_ledger_measured_bytes(tmp_path):
     """Trainer::ledger from measured traffic: gpu_pull / gpu_push bytes equal
     the remote unique keys of each rank's slices x (8 + 4e) / x 4e, merges

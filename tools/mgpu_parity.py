@@ -45,11 +45,16 @@ def main():
     res = {"loss": [], "auc": []}
     batches = []
     grow = 0 if os.environ.get("MGPU_CONST_BATCH") == "1" else 17
+    # variant "span": the key space jumps 4e3 -> 1e12 -> 1e5 between batches,
+    # so the sync-free dedup's pass plan (from the previous batch) misses on
+    # some rank and every rank redoes its sort and the counts exchange
+    spans = [4000, 4000, 10**12, 10**12, 10**5, 4000]
     for b in range(n_batches):
+        V = spans[b % len(spans)] if variant == "span" else 4000
         if S > 1:
-            bt = make_batch(600 + grow * b, V=4000, zipf_s=1.1, n_slots=S, seed=b)
+            bt = make_batch(600 + grow * b, V=V, zipf_s=1.1, n_slots=S, seed=b)
         else:
-            bt = make_batch(600 + grow * b, V=4000, zipf_s=1.1, nnz=7, poisson=True, seed=b)
+            bt = make_batch(600 + grow * b, V=V, zipf_s=1.1, nnz=7, poisson=True, seed=b)
         batches.append(bt)
         r = tr.train_batch(bt, predict_first=True)
         res["loss"].append(r["loss"])
