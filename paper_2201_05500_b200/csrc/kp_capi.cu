@@ -17,6 +17,9 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <map>
+#include <set>
+#include <tuple>
 #include <vector>
 
 #include "kp_table.cuh"
@@ -77,6 +80,10 @@ unsigned grid1(uint64_t n) {
 thread_local const uint32_t* kp::g_abort = nullptr;
 std::atomic<uint64_t> g_launches{0};
 void kp::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+std::atomic<uint64_t>& kp::devbuf_generation() {
+  static std::atomic<uint64_t> g{0};
+  return g;
+}
 
 struct MergeWs {
   DevBuf allg, cm, terms, chunk, full;
@@ -196,6 +203,47 @@ struct kp_trainer {
   // is rerun with the readbacks)
   bool async_step = false, force_sync = false, pred_ident = false;
   bool sync_free = true;  // KP_SYNC_FREE=0 at trainer creation: every step reads back
+  // The sync-free single-GPU batch as a CUDA graph (KP_GRAPH=0 at trainer
+  // creation: off): captured the second time a batch with the same inputs
+  // (pointers, sizes) and the same step-dependent choices arrives, then
+  // replayed; the readbacks land in pinned host memory.
+  bool graphs = true;
+  struct GraphKey {
+    const void* p[4];
+    uint64_t n, n_occ, gn, gfirst;
+    int flags;  // predict_first | preds | fused | merged | pred_ident
+    int spec;
+    bool operator<(const GraphKey& o) const {
+      return std::tie(p[0], p[1], p[2], p[3], n, n_occ, gn, gfirst, flags, spec) <
+             std::tie(o.p[0], o.p[1], o.p[2], o.p[3], o.n, o.n_occ, o.gn, o.gfirst, o.flags, o.spec);
+    }
+  };
+  struct GraphEnt {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0;
+  };
+  std::map<GraphKey, GraphEnt> gcache;
+  std::set<GraphKey> gseen;
+  uint64_t ggen = 0;  // devbuf generation the cache was built at
+  void graphs_clear() {
+    for (auto& kv : gcache)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    gcache.clear();
+    gseen.clear();
+  }
+  // pinned readback block: [0..1] err words, [2..3] check words, [4] U,
+  // [5..8] table scalars; then the losses (double) and the predictions
+  uint32_t* rb = nullptr;
+  size_t rb_bytes = 0;
+  void* rb_ensure(size_t bytes) {
+    if (bytes > rb_bytes) {
+      if (rb) cudaFreeHost(rb);
+      graphs_clear();  // captured graphs point at the old block
+      KP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&rb), bytes));
+      rb_bytes = bytes;
+    }
+    return rb;
+  }
   DevBuf pflag;           // G > 1: the local dedup's plan-miss flag (travels with the counts)
   std::vector<TrajStep> traj;
   std::vector<float> traj_prev_vbar;  // frozen v_bar before the step (a3)
@@ -254,6 +302,8 @@ struct kp_trainer {
         if (w->remote[p] && w->remote[p] != w->local) cudaIpcCloseMemHandle(w->remote[p]);
       if (w->local && w->owned) cudaFree(w->local);
     }
+    graphs_clear();
+    if (rb) cudaFreeHost(rb);
     if (ev_dinput) cudaEventDestroy(ev_dinput);
     if (ev_xdone) cudaEventDestroy(ev_xdone);
     if (tab.t) table_destroy(tab.t);
@@ -1157,8 +1207,7 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
                std::to_string(my_lo) + ", " + std::to_string(my_hi) + ")");
   KP_CHECK(h_offs[0] == 0, kErrGeneric, "offs[0] must be 0");
   uint32_t* err = tr->err.get<uint32_t>(4);
-  KP_CUDA(cudaMemsetAsync(err, 0xFF, 4, s));
-  KP_CUDA(cudaMemsetAsync(tr->check.get<uint32_t>(2), 0, 8, s));  // [0] flags [1] steps applied
+  uint32_t* chk_w = tr->check.get<uint32_t>(2);  // [0] flags [1] steps applied
   // the sync-free single-GPU step: one minibatch step per batch, no
   // per-step host work that needs U (trajectory, gathered-A forward)
   struct AsyncReset {
@@ -1170,16 +1219,51 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
   // (predict pass included) checks the abort bits of the check word first
   AbortScope abort_guard(tr->world > 1 || tr->async_step ? static_cast<const uint32_t*>(tr->check.p) : nullptr);
   double* d_loss = tr->loss.get<double>(n_mb);
-  KP_CUDA(cudaMemsetAsync(d_loss, 0, n_mb * 8, s));
-
   // predictions use x_bar (trainer.cpp:141-151); when every replica holds
   // the same x (initial state, right after a merge, no set_worker_state
   // since) x_bar IS each worker's x, and the training forward doubles as the
   // prediction
   const bool fused = predict_first && n_mb == 1 && tr->x_uniform;
-  float* d_pred_keep = nullptr;
+  float* d_pred_keep = predict_first ? tr->pred_keep.get<float>(std::max<uint32_t>(n, 1)) : nullptr;
+  const uint64_t steps_before = tr->t_global, merges_before = tr->merges;
+  const bool uniform_before = tr->x_uniform;
+  // pinned readback block (see kp_trainer::rb)
+  uint32_t* rb = static_cast<uint32_t*>(tr->rb_ensure(64 + n_mb * 8 + (size_t)(predict_first ? n : 0) * 4));
+  double* rb_loss = reinterpret_cast<double*>(reinterpret_cast<char*>(rb) + 64);
+  float* rb_preds = reinterpret_cast<float*>(reinterpret_cast<char*>(rb) + 64 + n_mb * 8);
+  // CUDA graph of the whole sync-free batch: replayed when this exact batch
+  // shape (inputs, sizes, step-dependent choices) was captured before
+  const bool merged_next = ((tr->t_global + 1) % tr->cfg.k) == 0;
+  static const bool sync_debug = getenv("KP_SYNC_DEBUG") != nullptr;
+  const bool gmode = tr->graphs && tr->async_step && W == 1 && !tr->prof && n_mb == 1 && !sync_debug &&
+                     dedup_async_ready(tr->dd, h_offs[n]);
+  kp_trainer::GraphKey gk{};
+  if (gmode) {
+    const uint64_t gen = devbuf_generation().load();
+    if (gen != tr->ggen) {
+      tr->graphs_clear();
+      tr->ggen = gen;
+    }
+    gk.p[0] = d_offs;
+    gk.p[1] = d_keys;
+    gk.p[2] = d_slots;
+    gk.p[3] = d_labels;
+    gk.n = n;
+    gk.n_occ = h_offs[n];
+    gk.gn = global_n;
+    gk.gfirst = global_first;
+    gk.flags = (predict_first ? 1 : 0) | (fused ? 4 : 0) | (merged_next ? 8 : 0) | (tr->pred_ident ? 16 : 0);
+    gk.spec = tr->dd.spec_bits;
+  }
+  auto it = gmode ? tr->gcache.find(gk) : tr->gcache.end();
+  const bool replay = gmode && it != tr->gcache.end();
+  const bool capture = gmode && !replay && tr->gseen.count(gk) > 0;
+  if (gmode && !replay && !capture) tr->gseen.insert(gk);
+  auto body = [&]() {
+  KP_CUDA(cudaMemsetAsync(err, 0xFF, 4, s));
+  KP_CUDA(cudaMemsetAsync(chk_w, 0, 8, s));
+  KP_CUDA(cudaMemsetAsync(d_loss, 0, n_mb * 8, s));
   if (predict_first) {
-    d_pred_keep = tr->pred_keep.get<float>(std::max<uint32_t>(n, 1));
     if (!fused) {
       StepView pv;
       pv.offs = d_offs;
@@ -1193,8 +1277,6 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
       predict_pass(tr, pv, d_pred_keep);
     }
   }
-  const uint64_t steps_before = tr->t_global, merges_before = tr->merges;
-  const bool uniform_before = tr->x_uniform;
   for (uint64_t j = 0; j < n_mb; ++j) {
     StepView sv;
     sv.wlo.resize(W);
@@ -1258,21 +1340,72 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
     }
     run_step(tr, sv, d_loss + j, fused && j == 0 ? d_pred_keep : nullptr);
   }
-  // error flags, loss, predictions
-  uint32_t h_errw2[2] = {0, 0}, h_chkw[2] = {0, 0}, h_nu = 0;
-  KP_CUDA(cudaMemcpyAsync(h_errw2, err, 8, cudaMemcpyDeviceToHost, s));
-  KP_CUDA(cudaMemcpyAsync(h_chkw, tr->check.p, 8, cudaMemcpyDeviceToHost, s));
+  // error flags, loss, predictions -> the pinned readback block
+  KP_CUDA(cudaMemcpyAsync(rb, err, 8, cudaMemcpyDeviceToHost, s));
+  KP_CUDA(cudaMemcpyAsync(rb + 2, tr->check.p, 8, cudaMemcpyDeviceToHost, s));
   if (tr->async_step && tr->dd.d_nunique)
-    KP_CUDA(cudaMemcpyAsync(&h_nu, tr->dd.d_nunique, 4, cudaMemcpyDeviceToHost, s));
+    KP_CUDA(cudaMemcpyAsync(rb + 4, tr->dd.d_nunique, 4, cudaMemcpyDeviceToHost, s));
+  KP_CUDA(cudaMemcpyAsync(rb_loss, d_loss, n_mb * 8, cudaMemcpyDeviceToHost, s));
+  if (predict_first)
+    KP_CUDA(cudaMemcpyAsync(rb_preds, d_pred_keep, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+  // table scalars ([2] = full flag), same readback
+  KP_CUDA(cudaMemcpyAsync(rb + 5, tr->tab.t->d_scalars, 16, cudaMemcpyDeviceToHost, s));
+  };  // body
+  if (replay) {
+    issue_staged(tr, -1);  // a pending next-batch copy goes outside the graph
+    KP_CUDA(cudaGraphLaunch(it->second.exec, s));
+    g_launches.fetch_add(it->second.launches, std::memory_order_relaxed);
+    // the host-side effects of the captured step (run_step, W = 1, one GPU)
+    tr->t_global += 1;
+    if (merged_next) tr->merges++;
+    tr->x_uniform = merged_next;
+  } else if (capture) {
+    issue_staged(tr, -1);
+    const uint64_t l0 = g_launches.load(), gen0 = devbuf_generation().load();
+    KP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    bool ok = true;
+    try {
+      body();
+    } catch (...) {
+      ok = false;
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(s, &g);
+    cudaGraphExec_t ex = nullptr;
+    ok = ok && ec == cudaSuccess && g && devbuf_generation().load() == gen0 &&
+         cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
+      // (no graph for this trainer after all: undo the capture pass's host
+      // effects and run the batch directly)
+      cudaGetLastError();
+      if (ex) cudaGraphExecDestroy(ex);
+      tr->graphs = false;
+      tr->graphs_clear();
+      tr->t_global = steps_before;
+      tr->merges = merges_before;
+      tr->x_uniform = uniform_before;
+      tr->marks.clear();
+      tr->ev_used = 0;
+      train_batch_impl(tr, h_offs, d_offs, d_keys, d_slots, d_labels, n, global_n, global_first, predict_first,
+                       h_preds, out);
+      return;
+    }
+    tr->gcache[gk] = kp_trainer::GraphEnt{ex, g_launches.load() - l0};
+    g_launches.store(l0);  // counted when it runs, below
+    KP_CUDA(cudaGraphLaunch(ex, s));
+    g_launches.fetch_add(tr->gcache[gk].launches, std::memory_order_relaxed);
+  } else {
+    body();
+  }
+  KP_CUDA(cudaStreamSynchronize(s));
+  uint32_t h_errw2[2] = {rb[0], rb[1]}, h_chkw[2] = {rb[2], rb[3]};
+  const uint32_t h_nu = rb[4];
+  uint32_t h_sc[4] = {rb[5], rb[6], rb[7], rb[8]};
   const uint32_t& h_err = h_errw2[0];
   const uint32_t h_chk = h_chkw[0];
-  std::vector<double> lsum(n_mb);
-  KP_CUDA(cudaMemcpyAsync(lsum.data(), d_loss, n_mb * 8, cudaMemcpyDeviceToHost, s));
-  if (predict_first && h_preds)
-    KP_CUDA(cudaMemcpyAsync(h_preds, d_pred_keep, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
-  uint32_t h_sc[4] = {0, 0, 0, 0};  // table scalars ([2] = full flag), same readback
-  KP_CUDA(cudaMemcpyAsync(h_sc, tr->tab.t->d_scalars, 16, cudaMemcpyDeviceToHost, s));
-  KP_CUDA(cudaStreamSynchronize(s));
+  std::vector<double> lsum(rb_loss, rb_loss + n_mb);
+  if (predict_first && h_preds) std::memcpy(h_preds, rb_preds, (size_t)n * 4);
   if (tr->async_step) {
     if (h_chkw[0] & kAbortPlan) {
       // the device found the pass plan or the predicted layout wrong (or a
@@ -1908,6 +2041,8 @@ int kp_trainer_create(const kp_trainer_config* cfg, kp_comm* comm, int device, k
       tr->fused_pool = e && e[0] == '1';
       const char* f = getenv("KP_SYNC_FREE");
       tr->sync_free = !(f && f[0] == '0');
+      const char* g = getenv("KP_GRAPH");
+      tr->graphs = !(g && g[0] == '0');
     }
     // (the backward's plane operands [B][hidden1] and W1^T [S*e][hidden1]
     // need 16-byte rows: hidden1 % 8 == 0)

@@ -1,5 +1,7 @@
 // Shared helpers for the sm_100a hot-path kernels.
 #pragma once
+
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -45,6 +47,9 @@ constexpr uint32_t kNoRow = 0xFFFFFFFFu;
 
 // process-wide count of kernels launched by this library (kp_launch_count)
 void count_launch();
+// bumped whenever a DevBuf (re)allocates: CUDA graphs captured over the old
+// buffers are stale
+std::atomic<uint64_t>& devbuf_generation();
 
 inline unsigned ceil_div(uint64_t a, uint64_t b) { return (unsigned)((a + b - 1) / b); }
 
@@ -64,6 +69,7 @@ struct DevBuf {
     size_t n = bytes + bytes / 4 + 256;
     KP_CUDA(cudaMalloc(&p, n));
     cap = n;
+    devbuf_generation().fetch_add(1, std::memory_order_relaxed);
     return p;
   }
   template <class T>
@@ -82,6 +88,7 @@ struct DevBuf {
     if (p) KP_CUDA(cudaFree(p));
     p = q;
     cap = nc;
+    devbuf_generation().fetch_add(1, std::memory_order_relaxed);
     return static_cast<T*>(p);
   }
 };

@@ -774,3 +774,30 @@ def test_sync_free_predict_pass_bitwise(kp, monkeypatch):
         assert l1 == l0 and np.array_equal(p1, p0)
     assert np.array_equal(k1, k0) and np.array_equal(w1, w0) and np.array_equal(a1, a0)
     assert np.array_equal(x1, x0) and np.array_equal(y1, y0)
+
+
+def test_graph_replay_bitwise(kp, monkeypatch):
+    """The sync-free batch captured as a CUDA graph on the second sight of a
+    batch shape and replayed after (different batch contents through the
+    same input buffers, merge and non-merge steps at k = 2, predictions):
+    every result and trained bit equals the directly launched batch
+    (KP_GRAPH=0)."""
+    out = []
+    for g in ("1", "0"):
+        monkeypatch.setenv("KP_GRAPH", g)
+        cfg = O.TrainerCfg(n_workers=1, k=2, minibatch_size=2048, embedding_dim=64, n_slots=20,
+                           hidden=(64, 32), pooling="sum", activation="relu", alpha=0.02, sparse_lr=0.1)
+        tr = kp.Trainer(table_capacity=1 << 20, **trainer_kwargs(vars(cfg)))
+        res = []
+        for b in range(8):
+            bt = make_batch(2048, V=10**6, zipf_s=1.1, n_slots=20, seed=80 + b)
+            r = tr.train_batch(bt.offs, bt.keys, bt.labels, slots=bt.slots, predict_first=True)
+            res.append((r["loss"], np.asarray(r["preds"]).copy(), r["minibatch_steps"], r["merges"]))
+        k, w, a, _ = tr.table()
+        out.append((res, k, w, a, tr.worker_state(0)))
+    (r1, k1, w1, a1, s1), (r0, k0, w0, a0, s0) = out
+    for x, y in zip(r1, r0):
+        assert x[0] == y[0] and np.array_equal(x[1], y[1]) and x[2:] == y[2:]
+    assert np.array_equal(k1, k0) and np.array_equal(w1, w0) and np.array_equal(a1, a0)
+    for f in ("x", "m", "v", "v_bar"):
+        assert np.array_equal(s1[f], s0[f]), f
