@@ -204,9 +204,9 @@ struct kp_trainer {
   bool async_step = false, force_sync = false, pred_ident = false;
   bool sync_free = true;  // KP_SYNC_FREE=0 at trainer creation: every step reads back
   // The sync-free single-GPU batch as a CUDA graph (KP_GRAPH=0 at trainer
-  // creation: off): captured the second time a batch with the same inputs
-  // (pointers, sizes) and the same step-dependent choices arrives, then
-  // replayed; the readbacks land in pinned host memory.
+  // creation: off): captured the first time a batch with these inputs
+  // (pointers, sizes) and step-dependent choices runs sync-free, replayed
+  // after; the readbacks land in pinned host memory.
   bool graphs = true;
   struct GraphKey {
     const void* p[4];
@@ -229,7 +229,6 @@ struct kp_trainer {
     for (auto& kv : gcache)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     gcache.clear();
-    gseen.clear();
   }
   // pinned readback block: [0..1] err words, [2..3] check words, [4] U,
   // [5..8] table scalars; then the losses (double) and the predictions
@@ -1257,8 +1256,7 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
   }
   auto it = gmode ? tr->gcache.find(gk) : tr->gcache.end();
   const bool replay = gmode && it != tr->gcache.end();
-  const bool capture = gmode && !replay && tr->gseen.count(gk) > 0;
-  if (gmode && !replay && !capture) tr->gseen.insert(gk);
+  const bool capture = gmode && !replay;
   auto body = [&]() {
   KP_CUDA(cudaMemsetAsync(err, 0xFF, 4, s));
   KP_CUDA(cudaMemsetAsync(chk_w, 0, 8, s));
@@ -1376,12 +1374,16 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
          cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
     if (g) cudaGraphDestroy(g);
     if (!ok) {
-      // (no graph for this trainer after all: undo the capture pass's host
-      // effects and run the batch directly)
+      // undo the capture pass's host effects and run the batch directly; the
+      // first failure for a shape (a buffer that had to grow: allocations are
+      // refused inside a capture) defers the capture to the next batch of the
+      // shape, a second one turns graphs off for this trainer
       cudaGetLastError();
       if (ex) cudaGraphExecDestroy(ex);
-      tr->graphs = false;
+      const bool again = tr->gseen.count(gk) > 0;
       tr->graphs_clear();
+      if (again) tr->graphs = false;
+      else tr->gseen.insert(gk);
       tr->t_global = steps_before;
       tr->merges = merges_before;
       tr->x_uniform = uniform_before;
@@ -1391,6 +1393,7 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
                        h_preds, out);
       return;
     }
+    if (tr->gcache.size() >= 16) tr->graphs_clear();  // (bounded: many shapes -> recapture)
     tr->gcache[gk] = kp_trainer::GraphEnt{ex, g_launches.load() - l0};
     g_launches.store(l0);  // counted when it runs, below
     KP_CUDA(cudaGraphLaunch(ex, s));

@@ -65,9 +65,13 @@ struct DevBuf {
   }
   void* ensure(size_t bytes) {
     if (bytes <= cap) return p;
-    if (p) KP_CUDA(cudaFree(p));
+    // (the new block first: a failed allocation -- e.g. refused inside a
+    // CUDA-graph capture -- leaves the old one intact)
     size_t n = bytes + bytes / 4 + 256;
-    KP_CUDA(cudaMalloc(&p, n));
+    void* q = nullptr;
+    KP_CUDA(cudaMalloc(&q, n));
+    if (p) KP_CUDA(cudaFree(p));
+    p = q;
     cap = n;
     devbuf_generation().fetch_add(1, std::memory_order_relaxed);
     return p;
