@@ -124,7 +124,6 @@ struct kp_trainer {
   // double-buffered staged batches (H2D on a copy stream overlapping compute)
   struct Staged {
     DevBuf offs, keys, slots, labels;
-    std::vector<uint32_t> h_offs;
     uint32_t n = 0;
     bool has_slots = false, ready = false, used_set = false;
     cudaEvent_t ev = nullptr;    // H2D of this slot done (copy stream)
@@ -666,7 +665,7 @@ void issue_staged(kp_trainer* tr, int slot) {
     auto& st = tr->stage[i];
     if (!st.pending) continue;
     if (st.used_set) KP_CUDA(cudaStreamWaitEvent(tr->copy_s, st.used, 0));
-    const uint32_t n = st.n, O = st.h_offs[n];
+    const uint32_t n = st.n, O = st.h_src_offs[n];
     KP_CUDA(cudaMemcpyAsync(st.offs.p, st.h_src_offs, (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, tr->copy_s));
     KP_CUDA(cudaMemcpyAsync(st.keys.p, st.h_src_keys, (size_t)O * 8, cudaMemcpyHostToDevice, tr->copy_s));
     if (st.has_slots)
@@ -1350,8 +1349,8 @@ void train_batch_impl(kp_trainer* tr, const uint32_t* h_offs, const uint32_t* d_
   KP_CUDA(cudaMemcpyAsync(rb + 5, tr->tab.t->d_scalars, 16, cudaMemcpyDeviceToHost, s));
   };  // body
   if (replay) {
-    issue_staged(tr, -1);  // a pending next-batch copy goes outside the graph
     KP_CUDA(cudaGraphLaunch(it->second.exec, s));
+    issue_staged(tr, -1);  // a pending next-batch copy: outside the graph, after its launch
     g_launches.fetch_add(it->second.launches, std::memory_order_relaxed);
     // the host-side effects of the captured step (run_step, W = 1, one GPU)
     tr->t_global += 1;
@@ -2128,8 +2127,7 @@ int kp_trainer_stage_batch(kp_trainer* tr, int slot, const uint32_t* offs, const
     st.h_src_slots = slots;
     st.h_src_labels = labels;
     st.pending = true;
-    st.h_offs.assign(offs, offs + n + 1);
-    st.n = n;
+    st.n = n;  // (offs stays the caller's: valid until train_staged returns)
     st.has_slots = slots != nullptr;
     st.ready = true;
   });
@@ -2145,7 +2143,7 @@ int kp_trainer_train_staged(kp_trainer* tr, int slot, uint64_t global_n, uint64_
     if (st.pending) issue_staged(tr, slot);
     KP_CUDA(cudaStreamWaitEvent(tr->s, st.ev, 0));
     st.ready = false;
-    train_batch_impl(tr, st.h_offs.data(), static_cast<const uint32_t*>(st.offs.p),
+    train_batch_impl(tr, st.h_src_offs, static_cast<const uint32_t*>(st.offs.p),
                      static_cast<const uint64_t*>(st.keys.p),
                      st.has_slots ? static_cast<const uint16_t*>(st.slots.p) : nullptr,
                      static_cast<const int32_t*>(st.labels.p), st.n, global_n, global_first,

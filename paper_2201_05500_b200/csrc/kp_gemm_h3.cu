@@ -978,20 +978,106 @@ __global__ void k_colmax_scaled(const float* __restrict__ dz, int B, int N, cons
   }
 }
 
+__device__ __forceinline__ void sum_parts_warp(const float* __restrict__ part, int nparts, int N, int n, int lane,
+                                               float* __restrict__ out) {
+  float v = 0.f;
+  for (int c = lane; c < nparts; c += 32) v = __fadd_rn(v, part[(size_t)c * N + n]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) out[n] = v;
+}
+
+// k_split_rows (dX's A operand) and k_colmax_scaled (dW's column scales and
+// the bias-gradient partials) from ONE read of dz, for N % 128 == 0, N <= 1024
+// (one slab; a row spans N/128 whole warps): the colmax layout and row order,
+// the row max through shared memory. Bit for bit the two kernels' outputs.
+__global__ void k_rows_colmax(const float* __restrict__ dz, int B, int N, const int* __restrict__ xe,
+                              unsigned* __restrict__ cmax, float* __restrict__ csum, __half* __restrict__ rhi,
+                              __half* __restrict__ rlo, int* __restrict__ rexps) {
+  constexpr int RU = 4;  // rows in flight per thread (one barrier per RU rows)
+  __shared__ float red[1024];
+  __shared__ float rm[2][RU][8][8];  // [iteration parity][row u][row ty][warp of the row]
+  const int n4 = threadIdx.x, lane = threadIdx.x & 31, wr = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int step = gridDim.x * blockDim.y;
+  float4 mx = make_float4(0.f, 0.f, 0.f, 0.f), sm = mx;
+  int it = 0;
+  for (int b0 = blockIdx.x * blockDim.y; b0 < B; b0 += RU * step, ++it) {  // block-uniform
+    float4 v[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      const int b = b0 + u * step + threadIdx.y;
+      v[u] = b < B ? __ldg(reinterpret_cast<const float4*>(dz + (size_t)b * N) + n4)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      float m = fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w)));
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) rm[it & 1][u][threadIdx.y][wr] = m;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {  // rows in the colmax kernel's order (b ascending)
+      const int b = b0 + u * step + threadIdx.y;
+      if (b >= B) break;
+      float r = rm[it & 1][u][threadIdx.y][0];
+      for (int i = 1; i < nw; ++i) r = fmaxf(r, rm[it & 1][u][threadIdx.y][i]);
+      const int e = row_exp(r);
+      if (n4 == 0) rexps[b] = e;
+      const float sc = pow2f(e);
+      uint2 h, l;
+      split_h2(__fmul_rn(v[u].x, sc), __fmul_rn(v[u].y, sc), h.x, l.x);
+      split_h2(__fmul_rn(v[u].z, sc), __fmul_rn(v[u].w, sc), h.y, l.y);
+      reinterpret_cast<uint2*>(rhi + (size_t)b * N)[n4] = h;
+      reinterpret_cast<uint2*>(rlo + (size_t)b * N)[n4] = l;
+      const float xs = xe ? pow2f(-__ldg(xe + b)) : 1.f;
+      mx.x = fmaxf(mx.x, fabsf(__fmul_rn(v[u].x, xs)));
+      mx.y = fmaxf(mx.y, fabsf(__fmul_rn(v[u].y, xs)));
+      mx.z = fmaxf(mx.z, fabsf(__fmul_rn(v[u].z, xs)));
+      mx.w = fmaxf(mx.w, fabsf(__fmul_rn(v[u].w, xs)));
+      sm.x = __fadd_rn(sm.x, v[u].x), sm.y = __fadd_rn(sm.y, v[u].y);
+      sm.z = __fadd_rn(sm.z, v[u].z), sm.w = __fadd_rn(sm.w, v[u].w);
+    }
+  }
+  const int W = 4 * blockDim.x;
+  float* rr = red + threadIdx.y * W + 4 * threadIdx.x;
+  rr[0] = mx.x, rr[1] = mx.y, rr[2] = mx.z, rr[3] = mx.w;
+  __syncthreads();
+  for (int c = threadIdx.y * blockDim.x + threadIdx.x; c < W; c += blockDim.x * blockDim.y) {
+    float mm = 0.f;
+    for (int q = 0; q < (int)blockDim.y; ++q) mm = fmaxf(mm, red[q * W + c]);
+    if (mm > 0.f) atomicMax(cmax + c, __float_as_uint(mm));
+  }
+  if (!csum) return;
+  __syncthreads();
+  rr[0] = sm.x, rr[1] = sm.y, rr[2] = sm.z, rr[3] = sm.w;
+  __syncthreads();
+  for (int c = threadIdx.y * blockDim.x + threadIdx.x; c < W; c += blockDim.x * blockDim.y) {
+    float t = 0.f;
+    for (int q = 0; q < (int)blockDim.y; ++q) t = __fadd_rn(t, red[q * W + c]);  // rows in y order
+    csum[(size_t)blockIdx.x * N + c] = t;
+  }
+}
+
 // out[n] = sum over the per-block partials in block order (deterministic)
 __global__ void k_sum_parts(const float* __restrict__ part, int nparts, int N, float* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  for (int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < N; n += (gridDim.x * blockDim.x) >> 5) {
-    float v = 0.f;
-    for (int c = lane; c < nparts; c += 32) v = __fadd_rn(v, part[(size_t)c * N + n]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) out[n] = v;
-  }
+  for (int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < N; n += (gridDim.x * blockDim.x) >> 5)
+    sum_parts_warp(part, nparts, N, n, lane, out);
 }
+// (part/sum_out, optional: k_sum_parts folded in -- the warps of the first
+// slab's blocks reduce the colsum partials, same order, bit for bit)
 __global__ void k_split_cols_scaled(const float* __restrict__ dz, int B, int N, const int* __restrict__ xe,
                                     const unsigned* __restrict__ cmax, __half* __restrict__ hi,
-                                    __half* __restrict__ lo, int* __restrict__ exps) {
+                                    __half* __restrict__ lo, int* __restrict__ exps,
+                                    const float* __restrict__ part = nullptr, int nparts = 0,
+                                    float* __restrict__ sum_out = nullptr) {
+  if (sum_out && blockIdx.y == 0) {
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x, wpb = (blockDim.x * blockDim.y) >> 5;
+    for (int n = blockIdx.x * wpb + (tid >> 5); n < N; n += gridDim.x * wpb)
+      sum_parts_warp(part, nparts, N, n, tid & 31, sum_out);
+  }
   const int n4 = blockIdx.y * blockDim.x + threadIdx.x;
   if (n4 >= N / 4) return;
   int ex[4];
@@ -1082,6 +1168,38 @@ void split_t_h(const float* W, int N, int K, __half* hi, __half* lo, int* exps, 
 void split_rows_h(const float* X, int rows, int K, int ld, __half* hi, __half* lo, int* exps, cudaStream_t s) {
   k_split_rows<<<std::min<unsigned>(ceil_div((uint64_t)rows * 32, 256), 148 * 16), 256, 0, s>>>(X, rows, K, ld, hi,
                                                                                                 lo, exps);
+  ::kp::count_launch();
+}
+
+static dim3 cols_block(int N) {
+  const int W = std::min(N, 1024);
+  return dim3(W / 4, std::max(1, std::min(8, 256 / (W / 4))));
+}
+static dim3 cols_grid(int B, int N, dim3 blk) {
+  const int W = std::min(N, 1024);
+  const unsigned slabs = ceil_div(N, W);
+  return dim3((unsigned)std::min<uint64_t>(ceil_div(B, blk.y), std::max<uint64_t>(1, 148 * 8 / slabs)), slabs);
+}
+
+bool rows_colmax_fusable(int N) {
+  const char* e = getenv("KP_SPLIT_FUSE");  // (per call: tests toggle it)
+  return !(e && e[0] == '0') && N % 128 == 0 && N <= 1024;
+}
+
+void split_rows_colmax_h(const float* dz, int B, int N, const int* xe, unsigned* cmax_ws, __half* rhi,
+                         __half* rlo, int* rexps, float* colsum_ws, cudaStream_t s) {
+  KP_CHECK(rows_colmax_fusable(N), kErrConfig, "split_rows_colmax_h: N must be a multiple of 128, <= 1024");
+  KP_CUDA(cudaMemsetAsync(cmax_ws, 0, (size_t)N * 4, s));
+  const dim3 blk = cols_block(N), g = cols_grid(B, N, blk);
+  k_rows_colmax<<<g, blk, 0, s>>>(dz, B, N, xe, cmax_ws, colsum_ws, rhi, rlo, rexps);
+  ::kp::count_launch();
+}
+
+void split_cols_after_h(const float* dz, int B, int N, const int* xe, const unsigned* cmax_ws, __half* hi, __half* lo,
+                        int* exps, float* colsum_out, const float* colsum_ws, cudaStream_t s) {
+  const dim3 blk = cols_block(N), g = cols_grid(B, N, blk);
+  k_split_cols_scaled<<<g, blk, 0, s>>>(dz, B, N, xe, cmax_ws, hi, lo, exps, colsum_ws, (int)g.x,
+                                        colsum_out);
   ::kp::count_launch();
 }
 

@@ -323,6 +323,14 @@ void split_cols_scaled_h(const float* dz, int B, int N, const int* xe, unsigned*
                          __half* lo, int* exps, cudaStream_t s, float* colsum_out = nullptr,
                          float* colsum_ws = nullptr);
 size_t split_cols_colsum_ws_floats(int B, int N);
+// split_rows_h(dz) + the column pass of split_cols_scaled_h from one read of
+// dz (N % 128 == 0, N <= 1024; KP_SPLIT_FUSE=0: off), then the planes (and the
+// colsum reduction) after: bit for bit the unfused pair
+bool rows_colmax_fusable(int N);
+void split_rows_colmax_h(const float* dz, int B, int N, const int* xe, unsigned* cmax_ws, __half* rhi,
+                         __half* rlo, int* rexps, float* colsum_ws, cudaStream_t s);
+void split_cols_after_h(const float* dz, int B, int N, const int* xe, const unsigned* cmax_ws, __half* hi, __half* lo,
+                        int* exps, float* colsum_out, const float* colsum_ws, cudaStream_t s);
 // pooling written as the first layer's planes (see kp_embed.cu k_pool_planes)
 bool pool_planes_supported(uint32_t S, uint32_t e);
 void pool_planes(const uint32_t* d_bag_offs, uint32_t n_inst, uint32_t S, const uint32_t* d_row_of_occ,

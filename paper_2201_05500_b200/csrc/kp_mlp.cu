@@ -811,11 +811,18 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
       // first layer on fp16 planes (kp_gemm_h3.cu): dX = dZ1 W1 (dZ1 split per
       // row, W1^T per row), then dW = dZ'^T X over the batch with X's row
       // scales moved onto dZ' (split per column) and X's planes read MN-major
+      // (the layer's bias gradient = column sums of dZ, from the same read)
+      const bool bias_here = l != (int)L - 2;
+      float* colsum_ws = bias_here ? ws.partials.get<float>(split_cols_colsum_ws_floats(B, N)) : nullptr;
+      unsigned* cmax = ws.cmax.get<unsigned>(N);
+      const bool fuse = d_dinput && rows_colmax_fusable(N);
       if (d_dinput) {
         __half* dzh = reinterpret_cast<__half*>(ws.dzh.get<uint16_t>((size_t)B * N));
         __half* dzl = reinterpret_cast<__half*>(ws.dzl.get<uint16_t>((size_t)B * N));
         int* dze = ws.dze.get<int>(B);
-        split_rows_h(dZ, B, N, N, dzh, dzl, dze, s);
+        // dX's row-split operand and dW's column scales (+ bias partials) in one read
+        if (fuse) split_rows_colmax_h(dZ, B, N, ws.in_exp, cmax, dzh, dzl, dze, colsum_ws, s);
+        else split_rows_h(dZ, B, N, N, dzh, dzl, dze, s);
         __half* th = reinterpret_cast<__half*>(ws.thi.get<uint16_t>((size_t)N * K));
         __half* tl = reinterpret_cast<__half*>(ws.tlo.get<uint16_t>((size_t)N * K));
         int* te = ws.texp.get<int>(K);
@@ -835,11 +842,12 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
       __half* dwh = reinterpret_cast<__half*>(ws.dwh.get<uint16_t>((size_t)B * N));
       __half* dwl = reinterpret_cast<__half*>(ws.dwl.get<uint16_t>((size_t)B * N));
       int* dwe = ws.dwe.get<int>(N);
-      // (the layer's bias gradient = column sums of dZ, from the same read)
-      const bool bias_here = l != (int)L - 2;
-      split_cols_scaled_h(dZ, B, N, ws.in_exp, ws.cmax.get<unsigned>(N), dwh, dwl, dwe, s,
-                          bias_here ? d_grad + m.b_off[l] : nullptr,
-                          bias_here ? ws.partials.get<float>(split_cols_colsum_ws_floats(B, N)) : nullptr);
+      if (fuse)
+        split_cols_after_h(dZ, B, N, ws.in_exp, cmax, dwh, dwl, dwe, bias_here ? d_grad + m.b_off[l] : nullptr,
+                           colsum_ws, s);
+      else
+        split_cols_scaled_h(dZ, B, N, ws.in_exp, cmax, dwh, dwl, dwe, s, bias_here ? d_grad + m.b_off[l] : nullptr,
+                            colsum_ws);
       EpiArgs plain{kStore, 0, nullptr, nullptr, 0, nullptr, 1, 1};
       h3_gemm(H3Operand{dwh, dwl, dwe, N}, true, H3Operand{ws.in_hi, ws.in_lo, nullptr, K}, true, N, K, B,
               d_grad + m.w_off[l], K, plain, true, ws.skws.get<float>(h3_splitk_ws_floats(N, K)), s,

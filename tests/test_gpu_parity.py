@@ -678,6 +678,34 @@ def test_fused_pool_gather_bitwise(kp, monkeypatch, B, S, e, pool, workers, hidd
     assert np.array_equal(x1, x0)
 
 
+@pytest.mark.parametrize("B,hidden,workers", [(1000, (128, 32), 1), (4096, (256,), 2), (777, (384, 64, 16), 1)])
+def test_split_rows_colmax_fused_bitwise(kp, monkeypatch, B, hidden, workers):
+    """The first layer's backward splits dZ1 for the input gradient (per row)
+    and takes dW's column scales and the bias-gradient partials from the SAME
+    read of dZ1 (k_rows_colmax) instead of two passes (KP_SPLIT_FUSE=0): every
+    trained bit equals the two-pass path. Ragged row counts, one and several
+    hidden layers (bias partials off / on), W=2 worker slices."""
+    out = []
+    monkeypatch.setenv("KP_TC_MIN_MFLOP", "0")  # the planes path at every size here
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("KP_SPLIT_FUSE", fuse)
+        cfg = O.TrainerCfg(n_workers=workers, k=2, minibatch_size=B, embedding_dim=16, n_slots=8,
+                           hidden=hidden, pooling="sum", activation="relu", alpha=0.02, sparse_lr=0.1)
+        tr = kp.Trainer(table_capacity=1 << 20, **trainer_kwargs(vars(cfg)))
+        losses = []
+        for b in range(3):
+            bt = make_batch(B, V=10**5, zipf_s=1.1, n_slots=8, seed=700 + b)
+            losses.append(tr.train_batch(bt.offs, bt.keys, bt.labels, slots=bt.slots)["loss"])
+        k, w, s1, _ = tr.table()
+        out.append((losses, k, w, s1, tr.worker_state(0)["x"]))
+    (l1, k1, w1, a1, x1), (l0, k0, w0, a0, x0) = out
+    assert l1 == l0
+    assert np.array_equal(k1, k0)
+    assert np.array_equal(w1, w0)
+    assert np.array_equal(a1, a0)
+    assert np.array_equal(x1, x0)
+
+
 def _train_n(kp, monkeypatch, sync_free, batches, S=8, e=16, hidden=(32, 16), B=None):
     monkeypatch.setenv("KP_SYNC_FREE", sync_free)  # read at trainer creation
     cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=B or len(batches[0].labels), embedding_dim=e,
