@@ -757,6 +757,53 @@ __global__ void __launch_bounds__(256) k_seg_blocksum(const float* __restrict__ 
   }
 }
 
+// Both block-sum levels in one launch (LPG <= 4, small rows: the step is
+// latency-bound there, configs[0]): block j's 64 groups form
+// Q[64j .. 64j+63] as k_seg_blocksum does, then (a full block) its first
+// group sums those 64 in order into Q2[j] -- the second level's sum, bit for
+// bit, without the second launch.
+template <int LPG, int NV, bool V4>
+__global__ void __launch_bounds__(256) k_seg_blocksum12(const float* __restrict__ src, uint32_t nP, uint32_t e,
+                                                         float* Q, float* __restrict__ Q2) {
+  const int gl = threadIdx.x % LPG, g = threadIdx.x / LPG;  // 64 groups
+  const uint64_t nQ = nP / QB, j = (uint64_t)blockIdx.x * QB + g;
+  constexpr int UB = V4 ? 16 : 4;
+  Row<LPG, NV, V4> acc, r[UB];
+  if (j < nQ) {
+    acc.zero();
+    for (uint32_t i = 0; i < QB; i += UB) {
+#pragma unroll
+      for (int u = 0; u < UB; ++u) r[u].load(src + (j * QB + i + u) * e, gl, e);
+#pragma unroll
+      for (int u = 0; u < UB; ++u) acc.add(r[u]);
+    }
+    acc.store(Q + j * e, gl, e);
+  }
+  if ((uint64_t)(blockIdx.x + 1) * QB > nQ) return;  // (block-uniform) partial block: no Q2 entry
+  __syncthreads();
+  if (g != 0) return;
+  acc.zero();
+  const float* q0 = Q + (uint64_t)blockIdx.x * QB * e;
+  for (uint32_t i = 0; i < QB; i += UB) {
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {  // (written by this block: L2 loads, not the read-only path)
+      if (V4) {
+        const float4 x = __ldcg(reinterpret_cast<const float4*>(q0 + (i + u) * e) + gl);
+        r[u].v[0] = x.x, r[u].v[1] = x.y, r[u].v[2] = x.z, r[u].v[3] = x.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          const uint32_t jj = gl + 32 * q;
+          r[u].v[q] = jj < e ? __ldcg(q0 + (i + u) * e + jj) : 0.f;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) acc.add(r[u]);
+  }
+  acc.store(Q2 + (uint64_t)blockIdx.x * e, gl, e);
+}
+
 template <int LPG, int NV, bool V4>
 __device__ __forceinline__ void sum_p(const float* P, uint64_t lo, uint64_t hi, uint32_t e,
                                       Row<LPG, NV, V4>& acc, int gl) {
@@ -852,10 +899,15 @@ void launch_seg(const SegArgs& a, const TView& t, float* Q, cudaStream_t s) {
   }
   const uint32_t nQ = nP / QB;
   float* Q2 = Q + (uint64_t)(nQ + 1) * a.e;
-  if (nQ) {
+  const char* bs_env = getenv("KP_SEG_BS12");  // =0: the two block-sum levels as two launches
+  const bool one = LPG <= 4 && !(bs_env && bs_env[0] == '0');
+  if (nQ && one) {
+    k_seg_blocksum12<LPG, NV, V4><<<(nQ + QB - 1) / QB, QB * LPG, 0, s>>>(a.partials, nP, a.e, Q, Q2);
+    ::kp::count_launch();
+  } else if (nQ) {
     k_seg_blocksum<LPG, NV, V4><<<grid_cap(((uint64_t)nQ * LPG + 255) / 256), 256, 0, s>>>(a.partials, nP, a.e, Q); ::kp::count_launch();
   }
-  if (nQ >= QB) {
+  if (nQ >= QB && !one) {
     k_seg_blocksum<LPG, NV, V4><<<grid_cap(((uint64_t)(nQ / QB) * LPG + 255) / 256), 256, 0, s>>>(Q, nQ, a.e, Q2); ::kp::count_launch();
   }
   if (nchunks > 1) {

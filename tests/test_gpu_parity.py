@@ -706,6 +706,32 @@ def test_split_rows_colmax_fused_bitwise(kp, monkeypatch, B, hidden, workers):
     assert np.array_equal(x1, x0)
 
 
+@pytest.mark.parametrize("B,S,e,zipf,V", [(4096, 26, 8, 1.1, 10**6), (8192, 26, 8, 1.3, 100), (6000, 16, 16, 1.2, 500)])
+def test_seg_blocksum_one_launch_bitwise(kp, monkeypatch, B, S, e, zipf, V):
+    """Small rows (e <= 16): the push's two block-sum levels (64-partial sums
+    Q, then 64-Q sums Q2 for the hottest keys) run as one launch; every
+    trained bit equals the two-launch path (KP_SEG_BS12=0). V=100 at Zipf 1.3
+    puts one key on ~60K sorted positions, so the Q2 level is exercised."""
+    out = []
+    for one in ("1", "0"):
+        monkeypatch.setenv("KP_SEG_BS12", one)
+        cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=B, embedding_dim=e, n_slots=S,
+                           hidden=(32,), pooling="sum", activation="relu", alpha=0.02, sparse_lr=0.1)
+        tr = kp.Trainer(table_capacity=1 << 20, **trainer_kwargs(vars(cfg)))
+        losses = []
+        for b in range(3):
+            bt = make_batch(B, V=V, zipf_s=zipf, n_slots=S, seed=950 + b)
+            losses.append(tr.train_batch(bt.offs, bt.keys, bt.labels, slots=bt.slots)["loss"])
+        k, w, s1, _ = tr.table()
+        out.append((losses, k, w, s1, tr.worker_state(0)["x"]))
+    (l1, k1, w1, a1, x1), (l0, k0, w0, a0, x0) = out
+    assert l1 == l0
+    assert np.array_equal(k1, k0)
+    assert np.array_equal(w1, w0)
+    assert np.array_equal(a1, a0)
+    assert np.array_equal(x1, x0)
+
+
 def _train_n(kp, monkeypatch, sync_free, batches, S=8, e=16, hidden=(32, 16), B=None):
     monkeypatch.setenv("KP_SYNC_FREE", sync_free)  # read at trainer creation
     cfg = O.TrainerCfg(n_workers=1, k=1, minibatch_size=B or len(batches[0].labels), embedding_dim=e,
