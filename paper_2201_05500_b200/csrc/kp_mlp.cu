@@ -429,28 +429,82 @@ __global__ void k_head_bwd(const float* __restrict__ in, int B, int W, const flo
                            float* __restrict__ delta, float* __restrict__ dprev, int mode, int act,
                            const float* __restrict__ coeff, uint32_t S, uint32_t e,
                            double* __restrict__ loss_part, unsigned* __restrict__ done,
-                           double* __restrict__ loss_sum, int n_loss) {
+                           double* __restrict__ loss_sum, int n_loss, float* __restrict__ cpart, int W2) {
   __shared__ double s_loss[8];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   double lsum = 0.0;
-  for (int b = wid; b < B; b += nw) {
-    const float y = (float)labels[b];
-    const float d = __fdiv_rn(__fsub_rn(preds[b], y), nb);
-    if (lane == 0) {
-      delta[b] = d;
-      const float z = logits[b];
-      const float sp = __fadd_rn(fmaxf(z, 0.f), log1pf(expf(-fabsf(z))));
-      lsum += (double)__fsub_rn(sp, __fmul_rn(y, z));
+  if (cpart) {
+    // (W <= 256) the head's three column sums from the rows in registers:
+    // sum_b delta*a[b][i] (head weights), sum_b dprev[b][i] (the hidden
+    // layer's bias, W2 = W), sum_b delta (head bias) -- per lane over its
+    // rows in order, then the block's warps in order into cpart[block][NT]
+    constexpr int MAXC = 8;
+    float wacc[MAXC], bacc[MAXC], dacc = 0.f;
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) wacc[q] = 0.f, bacc[q] = 0.f;
+    for (int b = wid; b < B; b += nw) {
+      const float y = (float)labels[b];
+      const float d = __fdiv_rn(__fsub_rn(preds[b], y), nb);
+      if (lane == 0) {
+        delta[b] = d;
+        const float z = logits[b];
+        const float sp = __fadd_rn(fmaxf(z, 0.f), log1pf(expf(-fabsf(z))));
+        lsum += (double)__fsub_rn(sp, __fmul_rn(y, z));
+        dacc = __fadd_rn(dacc, d);
+      }
+#pragma unroll
+      for (int q = 0; q < MAXC; ++q) {
+        const int i = lane + 32 * q;
+        if (i < W) {
+          const float av = in[(size_t)b * W + i];
+          wacc[q] = __fadd_rn(wacc[q], __fmul_rn(d, av));
+          if (dprev) {
+            float g = __fmul_rn(d, w[i]);
+            if (mode == kDAct) g = __fmul_rn(g, act_bwd(act, av));
+            else if (mode == kCoeff) g = __fmul_rn(g, coeff[(size_t)b * S + i / e]);
+            dprev[(size_t)b * W + i] = g;
+            if (W2) bacc[q] = __fadd_rn(bacc[q], g);
+          }
+        }
+      }
     }
-    if (dprev) {
-      for (int i = lane; i < W; i += 32) {
-        float g = __fmul_rn(d, w[i]);
-        if (mode == kDAct) g = __fmul_rn(g, act_bwd(act, in[(size_t)b * W + i]));
-        else if (mode == kCoeff) g = __fmul_rn(g, coeff[(size_t)b * S + i / e]);
-        dprev[(size_t)b * W + i] = g;
+    __shared__ float s_col[8][2 * 256 + 1];
+    const int NT = W + W2 + 1;
+#pragma unroll
+    for (int q = 0; q < MAXC; ++q) {
+      const int i = lane + 32 * q;
+      if (i < W) {
+        s_col[warp][i] = wacc[q];
+        if (W2) s_col[warp][W + i] = bacc[q];
+      }
+    }
+    if (lane == 0) s_col[warp][W + W2] = dacc;
+    __syncthreads();
+    for (int n = threadIdx.x; n < NT; n += blockDim.x) {
+      float t = s_col[0][n];
+      for (int q = 1; q < (int)(blockDim.x >> 5); ++q) t = __fadd_rn(t, s_col[q][n]);
+      cpart[(size_t)blockIdx.x * NT + n] = t;
+    }
+  } else {
+    for (int b = wid; b < B; b += nw) {
+      const float y = (float)labels[b];
+      const float d = __fdiv_rn(__fsub_rn(preds[b], y), nb);
+      if (lane == 0) {
+        delta[b] = d;
+        const float z = logits[b];
+        const float sp = __fadd_rn(fmaxf(z, 0.f), log1pf(expf(-fabsf(z))));
+        lsum += (double)__fsub_rn(sp, __fmul_rn(y, z));
+      }
+      if (dprev) {
+        for (int i = lane; i < W; i += 32) {
+          float g = __fmul_rn(d, w[i]);
+          if (mode == kDAct) g = __fmul_rn(g, act_bwd(act, in[(size_t)b * W + i]));
+          else if (mode == kCoeff) g = __fmul_rn(g, coeff[(size_t)b * S + i / e]);
+          dprev[(size_t)b * W + i] = g;
+        }
       }
     }
   }
@@ -776,22 +830,34 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
     dprev = d_dinput;
     mode = d_coeff ? kCoeff : kStore;
   }
-  const unsigned hb = grid_cap(((uint64_t)B * 32 + 255) / 256);
+  // head weight + bias gradients, and (with hidden layers) the last hidden
+  // layer's bias gradient (the column sums of dprev = its dZ): in the head's
+  // backward pass itself (W <= 256: per-block partials, ~8 rows per warp), or
+  // one extra pass over a and dprev
+  const bool fused_bias = L >= 2;
+  const int W2 = fused_bias ? W : 0;
+  const int NT = W + W2 + 1;
+  const char* hf_env = getenv("KP_HEAD_FUSE");  // =0: the separate column-sum pass
+  const bool head_cols = W <= 256 && !(hf_env && hf_env[0] == '0');
+  // (fused: ~8 rows per warp, but at least two blocks per SM for small batches)
+  const unsigned hb = head_cols ? grid_cap(std::max<uint64_t>((B + 63) / 64, std::min<uint64_t>(296, (B + 7) / 8)))
+                                : grid_cap(((uint64_t)B * 32 + 255) / 256);
   double* lossp = ws.lossp.get<double>(hb);
   if (!ws.hdone.p) {
     ws.hdone.get<unsigned>(1);
     KP_CUDA(cudaMemsetAsync(ws.hdone.p, 0, 4, s));
   }
+  float* cpart = head_cols ? ws.partials.get<float>((size_t)hb * NT) : nullptr;
   k_head_bwd<<<hb, 256, 0, s>>>(layer_in(L - 1), B, W, d_x + m.w_off[L - 1],
                                  static_cast<const float*>(ws.logits.p), d_preds, d_labels,
                                  (float)B, delta, dprev, mode, m.activation, d_coeff, S, e, lossp,
-                                 static_cast<unsigned*>(ws.hdone.p), d_loss_sum, (int)B); ::kp::count_launch();
-  // head weight + bias gradients, and (with hidden layers) the last hidden
-  // layer's bias gradient (the column sums of dprev = its dZ): one pass
-  const bool fused_bias = L >= 2;
-  {
-    const int W2 = fused_bias ? W : 0;
-    const int NT = W + W2 + 1;
+                                 static_cast<unsigned*>(ws.hdone.p), d_loss_sum, (int)B, cpart, W2);
+  ::kp::count_launch();
+  if (head_cols) {
+    k_reduce_chunks_to<<<grid_cap(ceil_div((uint64_t)NT * 32, 256)), 256, 0, s>>>(
+        cpart, (int)hb, NT, W, W2, d_grad + m.w_off[L - 1], fused_bias ? d_grad + m.b_off[L - 2] : nullptr,
+        d_grad + m.b_off[L - 1]); ::kp::count_launch();
+  } else {
     const int rows = colsum_rows((int)B);
     const int chunks = std::max(1, (int)((B + rows - 1) / rows));
     float* part = ws.partials.get<float>((size_t)chunks * NT);
