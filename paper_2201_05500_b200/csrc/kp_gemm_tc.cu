@@ -15,14 +15,9 @@
 // epilogue warps fold the finished one into fp32 registers with RN adds:
 // fp32-level accuracy, independent of K, at tensor-core rate.
 //
-// CTA = one 128 x 128 output tile of one K split, 192 threads:
-//   warp 0    TMA producer (128B-swizzled tiles, canonical UMMA SW128 layouts)
-//   warp 1    TMEM allocator + single-thread MMA issuer (tcgen05.mma/commit)
-//   warps 2-5 hi/lo splitters (smem -> smem, fence.proxy.async), chunk
-//             drains (tcgen05.ld 32x32b) and the epilogue (bias/activation/
-//             derivative/pooling coefficient -> HBM)
-// Pipelines: full[s] (TMA tx) -> conv[s] (128 arrivals) -> MMA -> empty[s]
-// (tcgen05.commit); tfull[b] (commit) -> drain -> tempty[b] (128 arrivals).
+// Layout: a persistent, warp-specialised kernel of 18 warps per CTA (TMA
+// producer, TMEM allocator + MMA issuer, 8 splitter warps, 8 drain/epilogue
+// warps; CTA pairs with cta_group::2) -- see the block above k_tc_gemm.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>

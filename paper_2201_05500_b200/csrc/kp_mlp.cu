@@ -9,8 +9,10 @@
 // tcgen05 kernel over pre-split fp16 planes (kp_gemm_h3.cu) when the pooling
 // kernel wrote its output as planes, else on the on-chip-split tcgen05
 // kernels (kp_gemm_tc.cu: 3xFP16 forward/dX, 3xTF32 dW); the other layers on
-// 3xTF32 tcgen05. The fp32 SIMT GEMM below (128x128x8 tiles) is the fallback
-// for shapes TMA cannot describe and the accuracy reference of the tests.
+// 3xTF32 tcgen05. Products below KP_TC_MIN_MFLOP (512 MFLOP: every layer of
+// configs[0]) run on the small-tile fp32 SIMT GEMM (k_gemm_s, 32x64 tiles),
+// where a tcgen05 launch costs more than the arithmetic; the 128x128x8 SIMT
+// GEMM is the fallback for shapes TMA cannot describe.
 // Epilogues are fused (bias+activation, activation derivative, mean-pooling
 // coefficient); weight gradients use deterministic split-K; the out=1 head
 // is a warp-per-instance GEMV fused with sigmoid, loss and the upstream
