@@ -53,6 +53,9 @@ def parse():
     p.add_argument("--no-prefill", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--diag-h2d", action="store_true",
+                   help="diagnostic only: a 66 MB pinned->device copy on a side stream inside every "
+                        "device-resident step (how much the e2e path's staged copy costs the step)")
     p.add_argument("--no-stage-profile", action="store_true",
                    help="(no effect: the timed loop never records the per-stage CUDA events; a "
                         "separate profiled pass of the same length measures the stages)")
@@ -426,7 +429,16 @@ def main():
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(tr.stream())
 
+    diag = None
+    if args.diag_h2d:
+        nb = sum(v.nbytes for k, v in pin[0].items() if k != "_t")
+        diag = (torch.empty(nb, dtype=torch.uint8).pin_memory(), torch.empty(nb, dtype=torch.uint8, device=f"cuda:{local}"),
+                torch.cuda.Stream(device=f"cuda:{local}"))
+
     def step_dev(i):
+        if diag is not None:
+            with torch.cuda.stream(diag[2]):
+                diag[1].copy_(diag[0], non_blocking=True)
         bt, d = batches[i % len(batches)], dev[i % len(dev)]
         return tr.train_batch_device(bt.offs, d["offs"].data_ptr(), d["keys"].data_ptr(),
                                      d["slots"].data_ptr(), d["labels"].data_ptr(), bt.n,
