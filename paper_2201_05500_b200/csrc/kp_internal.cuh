@@ -244,6 +244,9 @@ struct GemmEpi {
   // fp16-operand GEMM (tc_gemm_nt_h): per-row max |A| and per-row exponent of B
   const float* a_rowmax = nullptr;
   const int* b_exp = nullptr;
+  // (small-tile SIMT GEMM, one K split) column sums of each 32-row tile's
+  // outputs -> csum_part[m-tile][N]: the next layer's bias gradient partials
+  float* csum_part = nullptr;
 };
 // tcgen05 3xTF32 GEMMs (operands split hi/lo on the fly in shared memory)
 bool tc_gemm_supported(int M, int N, int K, const float* A, int lda, const float* B, int ldb);
@@ -373,6 +376,7 @@ struct MlpWs {
   const int* in_exp = nullptr;
   DevBuf dzh, dzl, dze, dwh, dwl, dwe, cmax, skws;  // layer-1 backward planes, stream-K partials
   DevBuf hdone;  // head backward's last-block counter (the loss finalize)
+  DevBuf cpart;  // bias-gradient partials from a small-tile dX epilogue
   // planes mode, one feature per slot: the forward gathers its input rows
   // (row of (b, slot) = ga_rowocc[b*S + slot] of ga_src [ga_nrows][e]) and
   // writes the planes at in_hi / in_lo for the weight gradient

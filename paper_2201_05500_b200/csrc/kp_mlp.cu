@@ -253,14 +253,15 @@ __global__ void __launch_bounds__(256) k_gemm_s(int M, int N, int K, const float
     }
     __syncthreads();
   }
+  float out[2][4];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int m = m0 + ty * 2 + i;
-    if (m >= M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int n = n0 + tx * 4 + j;
-      if (n >= N) continue;
+      out[i][j] = 0.f;
+      if (m >= M || n >= N) continue;
       float v = acc[i][j];
       if (ep.mode == kBiasAct) {
         v = act_fwd(ep.act, __fadd_rn(v, ep.bias[n]));
@@ -270,6 +271,18 @@ __global__ void __launch_bounds__(256) k_gemm_s(int M, int N, int K, const float
         v = __fmul_rn(v, ep.coeff[(size_t)m * ep.S + n / ep.e]);
       }
       C[(size_t)m * ldc + n] = v;
+      out[i][j] = v;
+    }
+  }
+  if (ep.csum_part) {  // (one K split) this tile's column sums: row pairs in order
+    float* red = &As[0][0];  // 16 x 64 <= 32 x 36 floats; free after the k loop's last barrier
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[ty * SBN + tx * 4 + j] = __fadd_rn(out[0][j], out[1][j]);
+    __syncthreads();
+    if (tid < SBN && n0 + tid < N) {
+      float t = red[tid];
+      for (int q = 1; q < 16; ++q) t = __fadd_rn(t, red[q * SBN + tid]);
+      ep.csum_part[(size_t)blockIdx.y * N + n0 + tid] = t;
     }
   }
 }
@@ -686,8 +699,12 @@ __global__ void k_transpose(const float* __restrict__ in, int R, int Cc, float* 
 }
 
 // dX[B][K] = dZ[B][N] . W[N][K]  (W^T kept K-major for the tensor-core path)
-void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, const EpiArgs& ep,
+// (returns true when the small-tile path also wrote ep.csum_part; the other
+// paths ignore it)
+bool dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, EpiArgs ep,
              MlpWs& ws, cudaStream_t s, bool first = false) {
+  float* const csum = ep.csum_part;
+  ep.csum_part = nullptr;
   if (first && N % 8 == 0 && use_h(B, K, N, dZ, W, ws.tc_min_flop)) {
     // first layer's input gradient (the wide output): fp16 operands
     float* wt = ws.wt.get<float>((size_t)N * K);
@@ -700,7 +717,7 @@ void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, c
     float* am = ws.amax.get<float>(B);
     rowmax(dZ, B, N, N, am, s);
     tc_gemm_nt_h(B, K, N, dZ, N, am, th, tl, te, N, out, K, ep, s);
-    return;
+    return false;
   }
   if (tc_enabled() && tc_worth(B, K, N, ws.tc_min_flop) && tc_gemm_supported(B, K, N, dZ, N, W, N)) {
     float* wt = ws.wt.get<float>((size_t)N * K);
@@ -714,9 +731,12 @@ void dx_gemm(int B, int K, int N, const float* dZ, const float* W, float* out, c
     } else {
       tc_gemm_nt(B, K, N, dZ, N, wt, N, out, K, ep, s);
     }
-  } else {
-    gemm<true, false>(B, K, N, dZ, N, W, K, out, K, 1, ep, s);
+    return false;
   }
+  const bool cs = csum && small_tiles(B, K);  // (one K split on the small tiles)
+  if (cs) ep.csum_part = csum;
+  gemm<true, false>(B, K, N, dZ, N, W, K, out, K, 1, ep, s);
+  return cs;
 }
 
 // The head's three reductions in one pass (model.cpp:163-177 for the last
@@ -871,6 +891,7 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
   }
   // ---- hidden layers, top down ----
   int cur = 0;
+  bool csum_ready = false;  // ws.cpart holds this layer's bias-gradient partials
   for (int l = (int)L - 2; l >= 0; --l) {
     const int N = m.widths[l + 1], K = m.widths[l];
     float* dZ = static_cast<float*>(ws.dz[cur].p);
@@ -947,14 +968,34 @@ void mlp_backward(const MlpShape& m, const float* d_x, const float* d_in, uint32
       const int got = gemm<false, false>(N, K, B, dZ, N, in, K, part, K, sp, plain, s);
       reduce_splits_any(part, got, (size_t)N * K, d_grad + m.w_off[l], s);
     }
-    if (l != (int)L - 2) colsum(dZ, nullptr, B, N, d_grad + m.b_off[l], ws, s);  // (L-2: with the head's)
+    if (l != (int)L - 2) {  // (L-2: with the head's)
+      if (csum_ready) {  // partials from the GEMM that produced dZ (one per 32-row tile)
+        const int chunks = (int)ceil_div(B, 32);
+        if (chunks >= 32 && N <= 4096) {
+          k_reduce_chunks<<<grid_cap(ceil_div((uint64_t)N * 32, 256)), 256, 0, s>>>(
+              static_cast<const float*>(ws.cpart.p), chunks, N, d_grad + m.b_off[l]);
+        } else {
+          k_reduce_splits<<<grid_cap(ceil_div(N, 256)), 256, 0, s>>>(static_cast<const float*>(ws.cpart.p), chunks,
+                                                                      (size_t)N, d_grad + m.b_off[l]);
+        }
+        ::kp::count_launch();
+      } else {
+        colsum(dZ, nullptr, B, N, d_grad + m.b_off[l], ws, s);
+      }
+    }
+    csum_ready = false;
     // upstream for the layer below: dX = dZ . W_l, then act' or pooling coeff
     if (l > 0) {
       float* next = ws.dz[cur ^ 1].get<float>((size_t)B * K);
       EpiArgs ep{kDAct, m.activation, nullptr, static_cast<const float*>(ws.act[l - 1].p), K, nullptr, 1, 1};
+      // (the layer below's bias gradient partials from the same epilogue when
+      // that layer takes the plain column-sum path: small tiles, not layer L-2)
+      const char* cf_env = getenv("KP_COLSUM_FUSE");
+      if (l - 1 != (int)L - 2 && !(l - 1 == 0 && ws.in_hi) && !(cf_env && cf_env[0] == '0'))
+        ep.csum_part = ws.cpart.get<float>((size_t)ceil_div(B, 32) * K);
       // hidden layers: the 3xTF32 path (measured faster than fp16 at K = 128,
       // where the row-max/split passes and the A split per unit dominate)
-      dx_gemm(B, K, N, dZ, d_x + m.w_off[l], next, ep, ws, s, false);
+      csum_ready = dx_gemm(B, K, N, dZ, d_x + m.w_off[l], next, ep, ws, s, false);
       cur ^= 1;
     }
   }
