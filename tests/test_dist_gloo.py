@@ -1,4 +1,4 @@
-"""CPU, world_size 2 over gloo: the host-side multi-rank logic.
+"""CPU, world_size 2 and 8 over gloo: the host-side multi-rank logic.
 
 - rank slices partition the global batch exactly like shard_batch's cells
   (proj/src/trainer.cpp:32-53; test_trainer.cpp:58-99 balance/multiset);
@@ -61,8 +61,10 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_gloo_world2_bootstrap_and_routing():
-    world, port = 2, _free_port()
+@pytest.mark.parametrize("world", [2, 8])
+def test_gloo_world_bootstrap_and_routing(world):
+    """world 8: the host-side path of an 8-GPU box (one rank per GPU)."""
+    port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
@@ -73,12 +75,14 @@ def test_gloo_world2_bootstrap_and_routing():
         p.join(timeout=60)
         assert p.exitcode == 0
     parts = res[0]
-    assert res[1] == parts
+    assert all(res[r] == parts for r in range(world))
     assert all(p[2] == bytes(range(128)) for p in parts)
-    assert parts[0][0] == 0 and parts[0][0] + parts[0][1] == parts[1][0]
+    assert parts[0][0] == 0
+    for r in range(1, world):
+        assert parts[r - 1][0] + parts[r - 1][1] == parts[r][0]
     from paper_2201_05500_b200.data import make_batch
     bt = make_batch(1000, V=5000, zipf_s=1.1, nnz=5, seed=3)
-    assert parts[1][0] + parts[1][1] == bt.n
+    assert parts[world - 1][0] + parts[world - 1][1] == bt.n
     # owner g receives from every rank exactly the keys with key % G == g
     for g in range(world):
         recv = set()
