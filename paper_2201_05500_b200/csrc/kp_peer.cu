@@ -146,13 +146,80 @@ __global__ void k_merge_peer(PeerMerge pm, int R, uint32_t W, uint64_t D, uint64
   __threadfence_system();
 }
 
+// The same with RW = R * W <= 8 known at compile time: each element's R*W
+// remote v loads are issued together, then its R*W x and m loads, so one
+// element costs two NVLink round trips instead of 3*R*W dependent ones. The
+// adds run in the same (rank, worker) order: bitwise k_merge_peer's result.
+template <int RW>
+__global__ void k_merge_peer_rw(PeerMerge pm, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1, float alpha,
+                                const uint32_t* abort) {
+  if (aborted(abort)) return;
+  const float n = (float)RW;
+  const float* vp[RW];
+  const float* xp[RW];
+  const float* mp[RW];
+#pragma unroll
+  for (int i = 0; i < RW; ++i) {
+    const uint32_t p = i / W, l = i % W;
+    vp[i] = reinterpret_cast<const float*>(pm.v[p]) + (uint64_t)l * D;
+    xp[i] = reinterpret_cast<const float*>(pm.x[p]) + (uint64_t)l * D;
+    mp[i] = reinterpret_cast<const float*>(pm.m[p]) + (uint64_t)l * D;
+  }
+  for (uint64_t j = c0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < c1;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    float vv[RW], xv[RW], mv[RW];
+#pragma unroll
+    for (int i = 0; i < RW; ++i) vv[i] = vp[i][j];
+#pragma unroll
+    for (int i = 0; i < RW; ++i) {
+      xv[i] = xp[i][j];
+      mv[i] = mp[i][j];
+    }
+    const float vbase = vv[0];
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < RW; ++i) acc = __fadd_rn(acc, __fsub_rn(vv[i], vbase));
+    const float vb = __fadd_rn(vbase, __fdiv_rn(acc, n));
+    const float sq = __fsqrt_rn(vb);
+    float t[RW];
+#pragma unroll
+    for (int i = 0; i < RW; ++i) t[i] = __fsub_rn(xv[i], __fdiv_rn(__fmul_rn(alpha, mv[i]), sq));
+    float tacc = 0.f;
+#pragma unroll
+    for (int i = 0; i < RW; ++i) tacc = __fadd_rn(tacc, __fsub_rn(t[i], t[0]));
+    const float xb = __fadd_rn(t[0], __fdiv_rn(tacc, n));
+#pragma unroll
+    for (int i = 0; i < RW; i += (int)W) {
+      const uint32_t p = i / W;
+      reinterpret_cast<float*>(pm.vb[p])[j] = vb;
+      reinterpret_cast<float*>(pm.x[p])[j] = xb;
+    }
+  }
+  __threadfence_system();
+}
+
 }  // namespace
 
 void peer_merge(const PeerMerge& pm, int R, uint32_t W, uint64_t D, uint64_t c0, uint64_t c1, float alpha,
                 cudaStream_t s) {
   if (c1 <= c0) return;
-  k_merge_peer<<<(unsigned)std::min<uint64_t>((c1 - c0 + 255) / 256, 148 * 8), 256, 0, s>>>(pm, R, W, D, c0, c1,
-                                                                                             alpha, g_abort);
+  const unsigned grid = (unsigned)std::min<uint64_t>((c1 - c0 + 255) / 256, 148 * 8);
+  static const bool rw_on = [] {
+    const char* e = getenv("KP_MERGE_RW");
+    return !(e && e[0] == '0');
+  }();
+  const uint64_t rw = (uint64_t)R * W;
+#define KP_MERGE_RW_CASE(N) \
+  case N: k_merge_peer_rw<N><<<grid, 256, 0, s>>>(pm, W, D, c0, c1, alpha, g_abort); break;
+  if (rw_on && rw <= 8) {
+    switch (rw) {
+      KP_MERGE_RW_CASE(1) KP_MERGE_RW_CASE(2) KP_MERGE_RW_CASE(3) KP_MERGE_RW_CASE(4)
+      KP_MERGE_RW_CASE(5) KP_MERGE_RW_CASE(6) KP_MERGE_RW_CASE(7) KP_MERGE_RW_CASE(8)
+    }
+  } else {
+    k_merge_peer<<<grid, 256, 0, s>>>(pm, R, W, D, c0, c1, alpha, g_abort);
+  }
+#undef KP_MERGE_RW_CASE
   ::kp::count_launch();
 }
 
