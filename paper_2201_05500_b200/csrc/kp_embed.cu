@@ -733,9 +733,12 @@ __global__ void __launch_bounds__(256, 6) k_seg_chunks(SegArgs a, TView t) {
 // Phase 2: a segment spanning chunks c0 < c1 owns the contiguous flattened
 // partial range P[2c0+1 .. 2c1] (tail of c0, then head of each later chunk;
 // the unused tail slots in between hold 0). Short ranges are summed in order;
-// long ones (Zipf-hot keys) as loose head + 64-entry block sums Q + loose tail,
-// the hottest (more than 128 Q blocks) with a second level Q2 of 64-Q sums.
-constexpr uint32_t QB = 64;
+// long ones (Zipf-hot keys) as loose head + QB-entry block sums Q + loose tail,
+// the hottest (more than 2*QB Q blocks) with a second level Q2 of QB-Q sums.
+// QB = 16: the fix-up's loose head/tail walks are what a hot key waits on
+// (configs[1] push 0.712 -> 0.705 ms, configs[0] 0.051 -> 0.039 ms vs 64).
+constexpr uint32_t QB = 16;
+static_assert(QB % 16 == 0, "block sums load 16 (float4) or 4 rows per round");
 
 template <int LPG, int NV, bool V4>
 __global__ void __launch_bounds__(256) k_seg_blocksum(const float* __restrict__ src, uint32_t nP, uint32_t e,
@@ -758,14 +761,14 @@ __global__ void __launch_bounds__(256) k_seg_blocksum(const float* __restrict__ 
 }
 
 // Both block-sum levels in one launch (LPG <= 4, small rows: the step is
-// latency-bound there, configs[0]): block j's 64 groups form
-// Q[64j .. 64j+63] as k_seg_blocksum does, then (a full block) its first
+// latency-bound there, configs[0]): block j's QB groups form
+// Q[QB*j .. QB*j+QB-1] as k_seg_blocksum does, then (a full block) its first
 // group sums those 64 in order into Q2[j] -- the second level's sum, bit for
 // bit, without the second launch.
 template <int LPG, int NV, bool V4>
 __global__ void __launch_bounds__(256) k_seg_blocksum12(const float* __restrict__ src, uint32_t nP, uint32_t e,
                                                          float* Q, float* __restrict__ Q2) {
-  const int gl = threadIdx.x % LPG, g = threadIdx.x / LPG;  // 64 groups
+  const int gl = threadIdx.x % LPG, g = threadIdx.x / LPG;  // QB groups
   const uint64_t nQ = nP / QB, j = (uint64_t)blockIdx.x * QB + g;
   constexpr int UB = V4 ? 16 : 4;
   Row<LPG, NV, V4> acc, r[UB];
@@ -864,7 +867,7 @@ __global__ void __launch_bounds__(256) k_seg_fix(SegArgs a, TView t, const float
       sum_p(a.partials, lo, qa * QB, a.e, acc, gl);
       if (qb - qa <= 2 * QB) {
         sum_p(Q, qa, qb, a.e, acc, gl);
-      } else {  // the hottest keys: a second level of 64-block sums
+      } else {  // the hottest keys: a second level of QB-block sums
         const uint64_t q2a = (qa + QB - 1) / QB, q2b = qb / QB;
         sum_p(Q, qa, q2a * QB, a.e, acc, gl);
         sum_p(Q2, q2a, q2b, a.e, acc, gl);
